@@ -1,0 +1,144 @@
+/*
+ * msfm_b200 — C-ABI of the B200-native fine-stage hot path of Multistage SfM.
+ *
+ * The reference (pkg/src/msfm) is pure Python and has no FFI; its "plugin
+ * surface" is the Python function set the stages call.  Each
+ * entry point below is the native body of one of those functions, batched over
+ * pairs / images / tracks.  The Python drop-in (paper_1512_06235_b200/) binds
+ * them with ctypes exactly as a maintainer would from msfm.
+ *
+ * Conventions
+ *   - every function returns 0 on success, a negative MSFM_E* code on error;
+ *     msfm_last_error() returns the thread's last message.  No exceptions and
+ *     no hidden state cross the ABI.
+ *   - pointers named d_* are device pointers (caller-owned, e.g. torch
+ *     tensors); h_* are host pointers.  `stream` is a cudaStream_t (void*).
+ *   - all work is enqueued on `stream`; nothing synchronises the host unless
+ *     stated.
+ */
+#ifndef MSFM_B200_H
+#define MSFM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MSFM_OK 0
+#define MSFM_EINVAL (-1)      /* bad argument (ValueError in the Python layer) */
+#define MSFM_ECUDA (-2)       /* CUDA runtime / launch failure */
+#define MSFM_EWORKSPACE (-3)  /* workspace too small */
+#define MSFM_ECAPACITY (-4)   /* an output capacity would be exceeded */
+
+const char* msfm_last_error(void);
+int msfm_version(void);
+
+/* ------------------------------------------------------------------------
+ * Feature bank: all images' features concatenated (SoA, HBM-resident).
+ *   xy    f32 [n_total][2]          FeatureSet.xy            features.py:55
+ *   desc  u8  [n_total][128]        FeatureSet.descriptors   features.py:58
+ *   norm2 i32 [n_total]             |desc|^2 (msfm_feature_norms)
+ *   img_off i64 [n_images]          first feature of image i
+ *   img_n   i32 [n_images]          feature count of image i
+ *   img_wh  i32 [n_images][2]       width, height
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    const float* d_xy;
+    const uint8_t* d_desc;
+    const int32_t* d_norm2;
+    const int64_t* d_img_off;
+    const int32_t* d_img_n;
+    const int32_t* d_img_wh;
+    int32_t n_images;
+} msfm_bank;
+
+/* |desc|^2 per feature (exact int32). */
+int msfm_feature_norms(const uint8_t* d_desc, int64_t n, int32_t* d_norm2, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Spatial index of every target image (replaces msfm.guided.build_grid /
+ * OverlapGrid, guided.py:46-137).
+ *
+ * The reference's union of the 4 containing cells (offset grids of cell size
+ * 2D) of a line sample equals the 3x3 block of D-sized "subcells" around the
+ * sample's subcell: cell_g(f) == cell_g(s) for some g  <=>  |u_f-u_s| <= 1 and
+ * |v_f-v_s| <= 1, with u = 2*floor(x/2D) + [floor((x-D)/2D) == floor(x/2D)]
+ * evaluated in the reference's float64 rounding.  The index therefore stores,
+ * per feature, its subcell (u, v) (int16 each), and two CSR bucket tables of
+ * D x D buckets (bucket = floor(x/D), floor(y/D)): row-major (rows of y) and
+ * column-major (rows of x), used to enumerate the features near a line.
+ *   d_sub    [n_total]       short2 (u, v)
+ *   d_dims   [n_images][2]   nbx, nby buckets
+ *   d_roff/d_coff [n_images] first bucket of image i in the row/col tables
+ *   d_rstart/d_cstart [n_buckets_total+1] CSR starts (global feature index)
+ *   d_rmem/d_cmem [n_total]  image-local feature ids in bucket order
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    const int32_t* d_sub;        /* short2 packed: (u & 0xffff) | (v << 16)      */
+    const int32_t* d_dims;
+    const int64_t* d_roff;
+    const int64_t* d_coff;
+    const int32_t* d_rstart;
+    const int32_t* d_cstart;
+    const int32_t* d_rmem;
+    const int32_t* d_cmem;
+    double D;                    /* cell half-size = d * inflation (grid.d)      */
+} msfm_grids;
+
+/* Host-only: bucket dims (nbx, nby) of one image for cell half-size D. */
+int msfm_grid_dims(int32_t width, int32_t height, double D, int32_t dims_out[2]);
+
+/* Build the index of all images.  Bucket totals: sum over images of
+ * nbx*nby (row table and col table each).  Outputs are caller-allocated:
+ * d_sub[n_total], d_rstart/d_cstart[n_buckets_total+1], d_rmem/d_cmem[n_total]. */
+size_t msfm_grid_workspace_bytes(int64_t n_buckets_total);
+int msfm_grid_build(const msfm_bank* bank, const int32_t* d_dims, const int64_t* d_roff,
+                    const int64_t* d_coff, int64_t n_buckets_total, int64_t n_total, double D,
+                    int32_t* d_sub, int32_t* d_rstart, int32_t* d_cstart, int32_t* d_rmem,
+                    int32_t* d_cmem, void* d_workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Geometry-aware (epipolar-guided) matching of a batch of image pairs.
+ * Replaces msfm.guided.guided_match_pair(strategy="grid") (guided.py:393-480)
+ * + ratio_filter/_dedupe_targets (matching.py:82-113), batched over the pair
+ * loop of densify_stage (densify.py:220-240).
+ *
+ * Pair k: query image d_pair_q[k], target image d_pair_t[k], fundamental
+ * matrix d_pair_F[9k..9k+8] (row-major, p_t^T F p_q = 0, from
+ * fundamental_from_poses geometry.py:69-83), query feature ids
+ * d_qlist[d_qlist_off[k] .. d_qlist_off[k+1]) in ascending order.
+ * A pair whose F row starts with NaN is skipped (degenerate geometry,
+ * densify.py:161-165).
+ *
+ * Output (device): the matches of pair k are written to positions
+ * [qlist_off[k], qlist_off[k] + d_out_count[k]) of the four SoA arrays, sorted
+ * by query id (one match per query at most, so capacity = total queries):
+ *   out_q (query fid), out_t (target fid), out_dist (f32 L2 distance),
+ *   out_ratio (f32 best/second ratio, 0 for single-candidate accepts).
+ * d_stats (optional, [2*n_pairs] int64): SearchStats (queries, comparisons)
+ * exactly as guided.py:459-460 counts them.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    double d;            /* band half-width (BAND_D_PX = 8)                      */
+    float ratio;         /* Lowe ratio, compared in f32 (RATIO_GUIDED = 0.8)     */
+    float single_cap;    /* single-candidate cap (SINGLE_CANDIDATE_CAP = 45)     */
+    int32_t max_nt;      /* max target feature count over the batch (<= 65536)   */
+    int32_t chunk_pairs; /* pairs per internal chunk (workspace bound), 0 = auto  */
+} msfm_match_params;
+
+size_t msfm_guided_workspace_bytes(int32_t n_pairs, const int64_t* h_qlist_off,
+                                   const msfm_match_params* prm);
+int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids, int32_t n_pairs,
+                      const int32_t* d_pair_q, const int32_t* d_pair_t, const double* d_pair_F,
+                      const int64_t* d_qlist_off, const int32_t* d_qlist,
+                      const int64_t* h_qlist_off, const msfm_match_params* prm,
+                      int32_t* d_out_q, int32_t* d_out_t, float* d_out_dist, float* d_out_ratio,
+                      int32_t* d_out_count, int64_t* d_stats,
+                      void* d_workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSFM_B200_H */

@@ -1,0 +1,100 @@
+"""ctypes binding of libmsfm_b200.so (the C-ABI in include/msfm_b200.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+visible, every entry point raises DeviceUnavailableError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .types import DeviceUnavailableError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmsfm_b200.so")
+
+c_int32_p = ctypes.POINTER(ctypes.c_int32)
+VP = ctypes.c_void_p
+
+
+class Bank(ctypes.Structure):
+    _fields_ = [("d_xy", VP), ("d_desc", VP), ("d_norm2", VP), ("d_img_off", VP),
+                ("d_img_n", VP), ("d_img_wh", VP), ("n_images", ctypes.c_int32)]
+
+
+class Grids(ctypes.Structure):
+    _fields_ = [("d_sub", VP), ("d_dims", VP), ("d_roff", VP), ("d_coff", VP),
+                ("d_rstart", VP), ("d_cstart", VP), ("d_rmem", VP), ("d_cmem", VP),
+                ("D", ctypes.c_double)]
+
+
+class MatchParams(ctypes.Structure):
+    _fields_ = [("d", ctypes.c_double), ("ratio", ctypes.c_float),
+                ("single_cap", ctypes.c_float), ("max_nt", ctypes.c_int32),
+                ("chunk_pairs", ctypes.c_int32)]
+
+
+_SIGS = {
+    "msfm_last_error": (ctypes.c_char_p, []),
+    "msfm_version": (ctypes.c_int, []),
+    "msfm_feature_norms": (ctypes.c_int, [VP, ctypes.c_int64, VP, VP]),
+    "msfm_grid_dims": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_double, c_int32_p]),
+    "msfm_grid_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int64]),
+    "msfm_grid_build": (ctypes.c_int, [ctypes.POINTER(Bank), VP, VP, VP, ctypes.c_int64,
+                                       ctypes.c_int64, ctypes.c_double, VP, VP, VP, VP, VP,
+                                       VP, ctypes.c_size_t, VP]),
+    "msfm_guided_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int32, VP,
+                                                      ctypes.POINTER(MatchParams)]),
+    "msfm_guided_match": (ctypes.c_int, [ctypes.POINTER(Bank), ctypes.POINTER(Grids),
+                                         ctypes.c_int32, VP, VP, VP, VP, VP, VP,
+                                         ctypes.POINTER(MatchParams), VP, VP, VP, VP, VP, VP,
+                                         VP, ctypes.c_size_t, VP]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def load(require_device: bool = True):
+    """Load the library (and check a CUDA device exists unless told not to)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise DeviceUnavailableError(
+                f"{LIB_PATH} is missing; run `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    if require_device:
+        import torch
+        if not torch.cuda.is_available():
+            raise DeviceUnavailableError("no CUDA device visible: the B200 path has no CPU fallback")
+    return _lib
+
+
+class MsfmCallError(RuntimeError):
+    pass
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = _lib.msfm_last_error().decode(errors="replace") if _lib else ""
+        if rc == -1:
+            raise ValueError(f"{what}: {msg}")
+        raise MsfmCallError(f"{what} failed ({rc}): {msg}")
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None for None)."""
+    return None if t is None else t.data_ptr()
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream

@@ -1,0 +1,129 @@
+"""Device-resident feature bank and spatial index.
+
+All images of a stage live in HBM as one SoA: xy f32 (n,2), descriptors u8
+(n,128) in 16-byte-aligned rows (so a 128-B row is eight coalesced 16-B
+vector loads), |desc|^2 i32 (n), plus per-image offsets.  The target-image
+index (build_grid, guided.py:110-137) is built once per stage on the device.
+Host arrays are staged through pinned memory and copied with one
+``cudaMemcpyAsync`` per array.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+
+
+class FeatureBank:
+    """Feature sets of many images, resident on one CUDA device."""
+
+    def __init__(self, feature_sets, device=None, image_ids=None, stream=None):
+        import torch
+
+        lib = _lib.load()
+        self.device = torch.device(device or "cuda")
+        ids = sorted(feature_sets) if image_ids is None else list(image_ids)
+        self.image_ids = ids
+        self.index_of = {i: k for k, i in enumerate(ids)}
+        sets = [feature_sets[i] for i in ids]
+        n = np.array([len(fs) for fs in sets], dtype=np.int64)
+        off = np.zeros(len(sets), dtype=np.int64)
+        if len(sets) > 1:
+            np.cumsum(n[:-1], out=off[1:])
+        self.n_total = int(n.sum())
+        self.counts = n
+        self.offsets = off
+        self.wh = np.array([[int(fs.width), int(fs.height)] for fs in sets], dtype=np.int32).reshape(-1, 2)
+        xy = np.concatenate([np.asarray(fs.xy, np.float32).reshape(-1, 2) for fs in sets]) \
+            if sets else np.zeros((0, 2), np.float32)
+        desc = np.concatenate([np.asarray(fs.descriptors, np.uint8).reshape(-1, 128) for fs in sets]) \
+            if sets else np.zeros((0, 128), np.uint8)
+        dev = self.device
+        self.xy = _to_device(xy, dev)
+        self.desc = _to_device(desc, dev)
+        self.img_off = _to_device(off, dev)
+        self.img_n = _to_device(n.astype(np.int32), dev)
+        self.img_wh = _to_device(self.wh, dev)
+        self.norm2 = torch.empty(self.n_total, dtype=torch.int32, device=dev)
+        st = _lib.stream_handle(stream)
+        _lib.check(lib.msfm_feature_norms(_lib.ptr(self.desc), self.n_total,
+                                          _lib.ptr(self.norm2), st), "msfm_feature_norms")
+        self.max_n = int(n.max()) if len(n) else 0
+        self._grids = {}
+
+    @property
+    def h2d_bytes(self) -> int:
+        return int(self.xy.numel() * 4 + self.desc.numel() + self.img_off.numel() * 8
+                   + self.img_n.numel() * 4 + self.img_wh.numel() * 4)
+
+    def cstruct(self) -> _lib.Bank:
+        return _lib.Bank(_lib.ptr(self.xy), _lib.ptr(self.desc), _lib.ptr(self.norm2),
+                         _lib.ptr(self.img_off), _lib.ptr(self.img_n), _lib.ptr(self.img_wh),
+                         len(self.image_ids))
+
+    def grid(self, D: float, stream=None) -> "SpatialIndex":
+        key = float(D)
+        if key not in self._grids:
+            self._grids[key] = SpatialIndex(self, key, stream)
+        return self._grids[key]
+
+
+class SpatialIndex:
+    """Subcell ids + row/column bucket CSR tables of every image (msfm_grid_build)."""
+
+    def __init__(self, bank: FeatureBank, D: float, stream=None):
+        import torch
+
+        lib = _lib.load()
+        if not D > 0:
+            raise ValueError(f"cell half-size d must be positive, got {D}")
+        self.D = float(D)
+        nimg = len(bank.image_ids)
+        dims = np.zeros((nimg, 2), dtype=np.int32)
+        buf = (ctypes.c_int32 * 2)()
+        for k in range(nimg):
+            _lib.check(lib.msfm_grid_dims(int(bank.wh[k, 0]), int(bank.wh[k, 1]), self.D, buf),
+                       "msfm_grid_dims")
+            dims[k] = (buf[0], buf[1])
+        cells = dims[:, 0].astype(np.int64) * dims[:, 1]
+        roff = np.zeros(nimg, np.int64)
+        if nimg > 1:
+            np.cumsum(cells[:-1], out=roff[1:])
+        nb = int(cells.sum())
+        dev = bank.device
+        self.dims = _to_device(dims, dev)
+        self.roff = _to_device(roff, dev)
+        self.coff = self.roff  # the column table has the same per-image sizes
+        self.sub = torch.empty(bank.n_total, dtype=torch.int32, device=dev)
+        self.rstart = torch.empty(nb + 1, dtype=torch.int32, device=dev)
+        self.cstart = torch.empty(nb + 1, dtype=torch.int32, device=dev)
+        self.rmem = torch.empty(max(bank.n_total, 1), dtype=torch.int32, device=dev)
+        self.cmem = torch.empty(max(bank.n_total, 1), dtype=torch.int32, device=dev)
+        ws_bytes = lib.msfm_grid_workspace_bytes(nb)
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        st = _lib.stream_handle(stream)
+        b = bank.cstruct()
+        _lib.check(lib.msfm_grid_build(ctypes.byref(b), _lib.ptr(self.dims), _lib.ptr(self.roff),
+                                       _lib.ptr(self.coff), nb, bank.n_total, self.D,
+                                       _lib.ptr(self.sub), _lib.ptr(self.rstart),
+                                       _lib.ptr(self.cstart), _lib.ptr(self.rmem),
+                                       _lib.ptr(self.cmem), _lib.ptr(ws), ws_bytes, st),
+                   "msfm_grid_build")
+        self._ws = ws  # keep alive until the stream has consumed it
+
+    def cstruct(self) -> _lib.Grids:
+        return _lib.Grids(_lib.ptr(self.sub), _lib.ptr(self.dims), _lib.ptr(self.roff),
+                          _lib.ptr(self.coff), _lib.ptr(self.rstart), _lib.ptr(self.cstart),
+                          _lib.ptr(self.rmem), _lib.ptr(self.cmem), self.D)
+
+
+def _to_device(a: np.ndarray, device):
+    import torch
+
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if device.type == "cuda":
+        t = t.pin_memory().to(device, non_blocking=True)
+    return t

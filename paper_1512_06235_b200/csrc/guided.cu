@@ -1,0 +1,1251 @@
+// Geometry-aware (epipolar-guided) pair matching on sm_100a.
+//
+// Native body of msfm.guided.guided_match_pair (pkg/src/msfm/guided.py:393-480)
+// batched over densify_stage's pair loop (densify.py:220-240), bit-exact with the
+// reference.  Compiled with -fmad=false: every fp64
+// product/sum that the reference rounds separately is rounded separately here,
+// and the fused ones are written as explicit fma().
+//
+// Pipeline per chunk of pairs (all device-side, no host round trips):
+//   plan     1 CTA      per-pair table / dedupe offsets (scan)
+//   lines    CTA/pair   epipolar line, clip, bucket key, hash-group insert
+//   groups   CTA/pair   compact occupied hash slots into group records
+//   gscan    1 CTA      group prefix over pairs
+//   scatter  CTA/pair   member lists
+//   prep     thr/group  padded clip + sample count, member-band deviation -> strip R
+//   match    warp/group strip gather, exact C' test, mma.sync u8 distance tiles,
+//                      fp32 band prefilter (+exact fp64 fallback), top-2, ratio, dedupe
+//   compact  CTA/pair   ordered compaction of dedupe winners
+#include <math.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace msfm {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr unsigned long long EMPTY = 0xffffffffffffffffull;
+constexpr int CAP = 512;       // candidates per round (9-bit local index in keys)
+constexpr int WARPS = 8;       // match kernel warps per CTA
+constexpr unsigned NONE = 0xffffffffu;
+
+// ------------------------------------------------------------------ geometry
+// `hom @ F.T` as numpy/OpenBLAS rounds it: dgemm for >= 2 rows, dgemv for 1.
+__device__ __forceinline__ void epiline(const double* F, double x, double y, bool single_row,
+                                        double l[3]) {
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        if (single_row) l[i] = fma(x, F[3 * i], y * F[3 * i + 1]) + F[3 * i + 2];
+        else            l[i] = fma(y, F[3 * i + 1], x * F[3 * i]) + F[3 * i + 2];
+    }
+}
+
+// clip_lines_batch (guided.py:297-338) with pad 0.
+__device__ bool clip_batch(const double l[3], double W, double H, double pa[2], double pb[2]) {
+    const double a = l[0], b = l[1], c = l[2];
+    const double x0 = -0.0, x1 = W, y0 = -0.0, y1 = H;
+    double cx[4], cy[4];
+    bool valid[4];
+    const double xs[2] = {x0, x1}, ys[2] = {y0, y1};
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+        double y = -(a * xs[k] + c) / b;
+        valid[k] = fabs(b) > 1e-15 && y >= y0 - 1e-9 && y <= y1 + 1e-9;
+        cx[k] = xs[k];
+        cy[k] = y < y0 ? y0 : (y > y1 ? y1 : y);
+    }
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+        double x = -(b * ys[k] + c) / a;
+        valid[k + 2] = fabs(a) > 1e-15 && x >= x0 - 1e-9 && x <= x1 + 1e-9;
+        cx[k + 2] = x < x0 ? x0 : (x > x1 ? x1 : x);
+        cy[k + 2] = ys[k];
+    }
+    double span = x1 - x0;
+    if (y1 - y0 > span) span = y1 - y0;
+    if (span < 1.0) span = 1.0;
+    int imin = -1, imax = -1;
+    double kmin = 0, kmax = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        if (!valid[k]) continue;
+        double key = cx[k] * (4.0 * span) + cy[k];
+        if (imin < 0 || key < kmin) { kmin = key; imin = k; }
+        if (imax < 0 || key > kmax) { kmax = key; imax = k; }
+    }
+    if (imin < 0) return false;
+    pa[0] = cx[imin]; pa[1] = cy[imin];
+    pb[0] = cx[imax]; pb[1] = cy[imax];
+    return np_hypot(pb[0] - pa[0], pb[1] - pa[1]) > 1e-12;
+}
+
+// clip_line_to_bounds (guided.py:140-170), scalar path, used with pad = d.
+__device__ bool clip_scalar(double a, double b, double c, double W, double H, double pad,
+                            double pa[2], double pb[2]) {
+    const double x0 = -pad, x1 = W + pad, y0 = -pad, y1 = H + pad;
+    double px[4], py[4];
+    int n = 0;
+    if (fabs(b) > 1e-15) {
+        const double xs[2] = {x0, x1};
+        for (int k = 0; k < 2; k++) {
+            double y = -(a * xs[k] + c) / b;
+            if (y0 - 1e-9 <= y && y <= y1 + 1e-9) {
+                double yy = y < y0 ? y0 : y;
+                yy = yy > y1 ? y1 : yy;
+                px[n] = xs[k]; py[n] = yy; n++;
+            }
+        }
+    }
+    if (fabs(a) > 1e-15) {
+        const double ys[2] = {y0, y1};
+        for (int k = 0; k < 2; k++) {
+            double x = -(b * ys[k] + c) / a;
+            if (x0 - 1e-9 <= x && x <= x1 + 1e-9) {
+                double xx = x < x0 ? x0 : x;
+                xx = xx > x1 ? x1 : xx;
+                px[n] = xx; py[n] = ys[k]; n++;
+            }
+        }
+    }
+    if (n < 2) return false;
+    int imin = 0, imax = 0;
+    for (int k = 1; k < n; k++) {
+        if (px[k] < px[imin] || (px[k] == px[imin] && py[k] < py[imin])) imin = k;
+        if (px[k] > px[imax] || (px[k] == px[imax] && py[k] > py[imax])) imax = k;
+    }
+    pa[0] = px[imin]; pa[1] = py[imin];
+    pb[0] = px[imax]; pb[1] = py[imax];
+    return !(np_hypot(pb[0] - pa[0], pb[1] - pa[1]) < 1e-12);
+}
+
+// group_queries composite key (guided.py:363-373), int64 wrap semantics.
+__device__ __forceinline__ unsigned long long composite_key(const double pa[2], const double pb[2]) {
+    long long c[4] = {(long long)floor(pa[0] / 2.0), (long long)floor(pa[1] / 2.0),
+                      (long long)floor(pb[0] / 2.0), (long long)floor(pb[1] / 2.0)};
+    unsigned long long k = (unsigned long long)(c[0] + 4096);
+#pragma unroll
+    for (int i = 1; i < 4; i++) k = k * 8192ull + (unsigned long long)(c[i] + 4096);
+    return k;
+}
+
+// Reference subcell index of a coordinate (see msfm_grids in the header):
+// u = 2*floor(fl(x/2D)) + [floor(fl((x-D)/2D)) == floor(fl(x/2D))]   (guided.py:64-68)
+__device__ __forceinline__ int exact_subcell(double x, double D) {
+    double c0 = floor(x / (2.0 * D));
+    double c1 = floor((x - D) / (2.0 * D));
+    return 2 * (int)c0 + (c1 == c0 ? 1 : 0);
+}
+
+// ------------------------------------------------------------------ block scan
+template <int NT>
+__device__ __forceinline__ int block_exclusive_scan(int v, int* total, int* smem /*NT/32+1*/) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) smem[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int s = lane < NT / 32 ? smem[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(FULL, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < NT / 32) smem[lane] = s;
+        if (lane == NT / 32 - 1) smem[NT / 32] = s;
+    }
+    __syncthreads();
+    int base = wid > 0 ? smem[wid - 1] : 0;
+    *total = smem[NT / 32];
+    __syncthreads();
+    return base + x - v;
+}
+
+// ------------------------------------------------------------------ features
+__global__ void norms_kernel(const uint8_t* __restrict__ desc, int64_t n, int32_t* __restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint4* row = reinterpret_cast<const uint4*>(desc + i * 128);
+    unsigned s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        uint4 v = row[k];
+        s = __dp4a(v.x, v.x, s); s = __dp4a(v.y, v.y, s);
+        s = __dp4a(v.z, v.z, s); s = __dp4a(v.w, v.w, s);
+    }
+    out[i] = (int32_t)s;
+}
+
+// ------------------------------------------------------------------ grid build
+struct GridBuildArgs {
+    const float2* xy; const int64_t* img_off; const int32_t* img_n; const int32_t* img_wh;
+    const int32_t* dims; const int64_t* roff; const int64_t* coff;
+    int32_t* sub; int32_t* rcount; int32_t* ccount; int32_t* rcur; int32_t* ccur;
+    int32_t* rmem; int32_t* cmem; double D;
+};
+
+__device__ __forceinline__ int bucket_of(float v, double D, int nb) {
+    int b = (int)floor((double)v / D);
+    return b < 0 ? 0 : (b >= nb ? nb - 1 : b);
+}
+
+__global__ void grid_count_kernel(GridBuildArgs a) {
+    const int img = blockIdx.x;
+    const int64_t off = a.img_off[img];
+    const int n = a.img_n[img];
+    const int nbx = a.dims[2 * img], nby = a.dims[2 * img + 1];
+    for (int f = threadIdx.x; f < n; f += blockDim.x) {
+        float2 p = a.xy[off + f];
+        int u = exact_subcell((double)p.x, a.D), v = exact_subcell((double)p.y, a.D);
+        a.sub[off + f] = (u & 0xffff) | (v << 16);
+        int bx = bucket_of(p.x, a.D, nbx), by = bucket_of(p.y, a.D, nby);
+        atomicAdd(&a.rcount[a.roff[img] + (int64_t)by * nbx + bx], 1);
+        atomicAdd(&a.ccount[a.coff[img] + (int64_t)bx * nby + by], 1);
+    }
+}
+
+__global__ void grid_scatter_kernel(GridBuildArgs a) {
+    const int img = blockIdx.x;
+    const int64_t off = a.img_off[img];
+    const int n = a.img_n[img];
+    const int nbx = a.dims[2 * img], nby = a.dims[2 * img + 1];
+    for (int f = threadIdx.x; f < n; f += blockDim.x) {
+        float2 p = a.xy[off + f];
+        int bx = bucket_of(p.x, a.D, nbx), by = bucket_of(p.y, a.D, nby);
+        int r = atomicAdd(&a.rcur[a.roff[img] + (int64_t)by * nbx + bx], 1);
+        int c = atomicAdd(&a.ccur[a.coff[img] + (int64_t)bx * nby + by], 1);
+        a.rmem[r] = f;
+        a.cmem[c] = f;
+    }
+}
+
+// exclusive scan of int32 (in place) over n elements: tiles of 4096
+constexpr int SCAN_T = 1024, SCAN_PER = 4;
+__global__ void scan_tiles_kernel(const int32_t* __restrict__ in, int64_t n, int32_t* bsum) {
+    __shared__ int sm[SCAN_T / 32 + 1];
+    int64_t base = (int64_t)blockIdx.x * SCAN_T * SCAN_PER;
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_PER; k++) {
+        int64_t i = base + (int64_t)threadIdx.x * SCAN_PER + k;
+        if (i < n) s += in[i];
+    }
+    int total;
+    block_exclusive_scan<SCAN_T>(s, &total, sm);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = total;
+}
+
+__global__ void scan_bsum_kernel(int32_t* bsum, int64_t nb) {
+    __shared__ int sm[SCAN_T / 32 + 1];
+    int carry = 0;
+    for (int64_t b0 = 0; b0 < nb; b0 += SCAN_T) {
+        int64_t i = b0 + threadIdx.x;
+        int v = i < nb ? bsum[i] : 0;
+        int total;
+        int ex = block_exclusive_scan<SCAN_T>(v, &total, sm);
+        if (i < nb) bsum[i] = carry + ex;
+        carry += total;
+    }
+}
+
+__global__ void scan_apply_kernel(int32_t* data, int64_t n, const int32_t* bsum, int32_t* copy) {
+    __shared__ int sm[SCAN_T / 32 + 1];
+    int64_t base = (int64_t)blockIdx.x * SCAN_T * SCAN_PER;
+    int v[SCAN_PER];
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_PER; k++) {
+        int64_t i = base + (int64_t)threadIdx.x * SCAN_PER + k;
+        v[k] = i < n ? data[i] : 0;
+        s += v[k];
+    }
+    int total;
+    int ex = block_exclusive_scan<SCAN_T>(s, &total, sm) + bsum[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < SCAN_PER; k++) {
+        int64_t i = base + (int64_t)threadIdx.x * SCAN_PER + k;
+        if (i < n) {
+            data[i] = ex;
+            if (copy) copy[i] = ex;
+        }
+        ex += v[k];
+    }
+}
+
+int exclusive_scan(int32_t* data, int64_t n, int32_t* copy, int32_t* bsum, cudaStream_t st) {
+    int64_t nb = (n + SCAN_T * SCAN_PER - 1) / (SCAN_T * SCAN_PER);
+    if (nb == 0) return MSFM_OK;
+    scan_tiles_kernel<<<(unsigned)nb, SCAN_T, 0, st>>>(data, n, bsum);
+    scan_bsum_kernel<<<1, SCAN_T, 0, st>>>(bsum, nb);
+    scan_apply_kernel<<<(unsigned)nb, SCAN_T, 0, st>>>(data, n, bsum, copy);
+    MSFM_LAUNCH_CHECK();
+    return MSFM_OK;
+}
+
+// ------------------------------------------------------------------ matching
+struct GroupPrep {      // one per group (dense gid order), written by prep_kernel
+    double pax, pay, pbx, pby;   // padded clip of the representative line (pad = d)
+    double len;                  // |pb - pa|
+    int K;                       // sample count - 1, -1: line misses the padded image
+    float R;                     // strip half-width around the rep line
+    double sl0, sl1, sl2;        // singleton member's own (dgemv) line
+};
+
+struct ChunkArgs {
+    // bank
+    const float2* xy; const uint8_t* desc; const int32_t* norm2;
+    const int64_t* img_off; const int32_t* img_n; const int32_t* img_wh;
+    // index
+    const int32_t* sub; const int32_t* dims; const int64_t* roff; const int64_t* coff;
+    const int32_t* rstart; const int32_t* cstart; const int32_t* rmem; const int32_t* cmem;
+    double D, d;
+    float ratio, single_cap;
+    // pairs
+    const int32_t* pair_q; const int32_t* pair_t; const double* pair_F;
+    const int64_t* qlist_off; const int32_t* qlist;
+    int32_t p0, npairs; int64_t qbase;
+    // chunk workspace
+    int64_t* tab_off; int64_t* tbase; int32_t* ngroups; int32_t* gstart;
+    unsigned long long* tab_key; unsigned* tab_rep; unsigned* tab_cnt;
+    int32_t* q_tab; double* q_line;
+    int4* grec; int32_t* gfill; int32_t* members; GroupPrep* prep;
+    unsigned long long* mstate;  // per member slot: best (d2<<32 | tid)
+    unsigned* mstate2;           // per member slot: second d2
+    int32_t* res_tid; float* res_dist; float* res_ratio;
+    unsigned long long* dedupe;
+    unsigned long long* stats;   // [2*n_pairs] (global pair index) or null
+    // outputs
+    int32_t* out_q; int32_t* out_t; float* out_dist; float* out_ratio; int32_t* out_count;
+};
+
+__device__ __forceinline__ int nextpow2(int v) {
+    int p = 2;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+__global__ void plan_kernel(ChunkArgs a) {
+    __shared__ int sm[SCAN_T / 32 + 1];
+    long long carry_t = 0, carry_d = 0;
+    for (int b0 = 0; b0 < a.npairs; b0 += SCAN_T) {
+        int p = b0 + threadIdx.x;
+        int ts = 0, nt = 0;
+        if (p < a.npairs) {
+            int pg = a.p0 + p;
+            int nq = (int)(a.qlist_off[pg + 1] - a.qlist_off[pg]);
+            ts = nextpow2(nq + 1);
+            nt = a.img_n[a.pair_t[pg]];
+        }
+        int tot_t, tot_d;
+        int ex_t = block_exclusive_scan<SCAN_T>(ts, &tot_t, sm);
+        int ex_d = block_exclusive_scan<SCAN_T>(nt, &tot_d, sm);
+        if (p < a.npairs) {
+            a.tab_off[p] = carry_t + ex_t;
+            a.tbase[p] = carry_d + ex_d;
+        }
+        carry_t += tot_t;
+        carry_d += tot_d;
+    }
+    if (threadIdx.x == 0) {
+        a.tab_off[a.npairs] = carry_t;
+        a.tbase[a.npairs] = carry_d;
+    }
+}
+
+__global__ void __launch_bounds__(256) lines_kernel(ChunkArgs a) {
+    const int p = blockIdx.x, pg = a.p0 + p;
+    const int64_t q0 = a.qlist_off[pg];
+    const int nq = (int)(a.qlist_off[pg + 1] - q0);
+    const int64_t s0 = q0 - a.qbase;
+    const int64_t t0 = a.tab_off[p];
+    const int tsize = (int)(a.tab_off[p + 1] - t0);
+    const int ti = a.pair_t[pg], qi = a.pair_q[pg];
+    const int nt = a.img_n[ti];
+    const int64_t db = a.tbase[p];
+    for (int e = threadIdx.x; e < tsize; e += blockDim.x) {
+        a.tab_key[t0 + e] = EMPTY;
+        a.tab_rep[t0 + e] = NONE;
+        a.tab_cnt[t0 + e] = 0;
+    }
+    for (int e = threadIdx.x; e < nt; e += blockDim.x) a.dedupe[db + e] = EMPTY;
+    for (int i = threadIdx.x; i < nq; i += blockDim.x) {
+        a.res_tid[s0 + i] = -1;
+        a.gfill[s0 + i] = 0;
+    }
+    if (threadIdx.x == 0) a.ngroups[p] = 0;
+    __syncthreads();
+    double F[9];
+#pragma unroll
+    for (int j = 0; j < 9; j++) F[j] = a.pair_F[9 * (int64_t)pg + j];
+    if (isnan(F[0])) {
+        for (int i = threadIdx.x; i < nq; i += blockDim.x) a.q_tab[s0 + i] = -1;
+        return;
+    }
+    const double W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1];
+    const int64_t qoff = a.img_off[qi];
+    const unsigned mask = (unsigned)tsize - 1;
+    for (int i = threadIdx.x; i < nq; i += blockDim.x) {
+        const int fid = a.qlist[q0 + i];
+        const float2 p2 = a.xy[qoff + fid];
+        double l[3];
+        epiline(F, (double)p2.x, (double)p2.y, nq == 1, l);
+        const double nrm = np_hypot(l[0], l[1]);
+        int slot = -1;
+        if (nrm > 1e-12) {
+            l[0] /= nrm; l[1] /= nrm; l[2] /= nrm;
+            double pa[2], pb[2];
+            if (clip_batch(l, W, H, pa, pb)) {
+                const unsigned long long key = composite_key(pa, pb);
+                unsigned h = (unsigned)mix64(key) & mask;
+                while (true) {
+                    unsigned long long prev = atomicCAS(&a.tab_key[t0 + h], EMPTY, key);
+                    if (prev == EMPTY || prev == key) break;
+                    h = (h + 1) & mask;
+                }
+                atomicMin(&a.tab_rep[t0 + h], (unsigned)i);
+                atomicAdd(&a.tab_cnt[t0 + h], 1u);
+                slot = (int)h;
+                double* L = a.q_line + 3 * (s0 + i);
+                L[0] = l[0]; L[1] = l[1]; L[2] = l[2];
+            }
+        }
+        a.q_tab[s0 + i] = slot;
+    }
+}
+
+__global__ void __launch_bounds__(256) groups_kernel(ChunkArgs a) {
+    __shared__ int sm[256 / 32 + 1];
+    const int p = blockIdx.x, pg = a.p0 + p;
+    const int64_t s0 = a.qlist_off[pg] - a.qbase;
+    const int64_t t0 = a.tab_off[p];
+    const int tsize = (int)(a.tab_off[p + 1] - t0);
+    int gcarry = 0, mcarry = 0;
+    for (int e0 = 0; e0 < tsize; e0 += 256) {
+        const int e = e0 + threadIdx.x;
+        bool occ = false;
+        unsigned cnt = 0, rep = 0;
+        if (e < tsize) {
+            occ = a.tab_key[t0 + e] != EMPTY;
+            if (occ) { cnt = a.tab_cnt[t0 + e]; rep = a.tab_rep[t0 + e]; }
+        }
+        int gtot, mtot;
+        int lg = block_exclusive_scan<256>(occ ? 1 : 0, &gtot, sm);
+        int mo = block_exclusive_scan<256>((int)cnt, &mtot, sm);
+        if (occ) {
+            const int g = gcarry + lg;
+            a.grec[s0 + g] = make_int4((int)rep, (int)cnt, (int)(s0 + mcarry + mo), 0);
+            a.tab_rep[t0 + e] = (unsigned)g;
+        }
+        gcarry += gtot;
+        mcarry += mtot;
+    }
+    if (threadIdx.x == 0) a.ngroups[p] = gcarry;
+}
+
+__global__ void gscan_kernel(ChunkArgs a) {
+    __shared__ int sm[SCAN_T / 32 + 1];
+    int carry = 0;
+    for (int b0 = 0; b0 < a.npairs; b0 += SCAN_T) {
+        int p = b0 + threadIdx.x;
+        int v = p < a.npairs ? a.ngroups[p] : 0;
+        int total;
+        int ex = block_exclusive_scan<SCAN_T>(v, &total, sm);
+        if (p < a.npairs) a.gstart[p] = carry + ex;
+        carry += total;
+    }
+    if (threadIdx.x == 0) a.gstart[a.npairs] = carry;
+}
+
+__global__ void __launch_bounds__(256) scatter_kernel(ChunkArgs a) {
+    const int p = blockIdx.x, pg = a.p0 + p;
+    const int64_t q0 = a.qlist_off[pg];
+    const int nq = (int)(a.qlist_off[pg + 1] - q0);
+    const int64_t s0 = q0 - a.qbase;
+    const int64_t t0 = a.tab_off[p];
+    for (int i = threadIdx.x; i < nq; i += blockDim.x) {
+        const int h = a.q_tab[s0 + i];
+        if (h < 0) continue;
+        const int lg = (int)a.tab_rep[t0 + h];
+        const int4 g = a.grec[s0 + lg];
+        const int pos = g.z + atomicAdd(&a.gfill[s0 + lg], 1);
+        a.members[pos] = (int)(s0 + i);
+    }
+}
+
+__device__ __forceinline__ int find_pair(const int32_t* gstart, int npairs, int gid) {
+    int lo = 0, hi = npairs - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (gstart[mid] <= gid) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// Upper bound of |dist_m(f) - dist_rep(f)| over the image rectangle restricted
+// to the member's band (|dist_m| <= d + 0.5): the difference is affine, so its
+// maximum over that convex polygon sits at one of its vertices.
+__device__ double band_deviation(const double m[3], const double r[3], double W, double H,
+                                 double d) {
+    const double da = m[0] - r[0], db = m[1] - r[1], dc = m[2] - r[2];
+    const double B = d + 0.5;
+    double dev = 0.0;
+    const double cx[4] = {0.0, W, 0.0, W}, cy[4] = {0.0, 0.0, H, H};
+    for (int k = 0; k < 4; k++) {
+        double dm = m[0] * cx[k] + m[1] * cy[k] + m[2];
+        if (fabs(dm) <= B) dev = fmax(dev, fabs(da * cx[k] + db * cy[k] + dc));
+    }
+    for (int s = -1; s <= 1; s += 2) {
+        // m0 x + m1 y + m2 = s*B  intersected with the four edges
+        if (fabs(m[1]) > 1e-12) {
+            for (int e = 0; e < 2; e++) {
+                double x = e ? W : 0.0;
+                double y = (s * B - m[2] - m[0] * x) / m[1];
+                if (y >= -1e-6 && y <= H + 1e-6) dev = fmax(dev, fabs(da * x + db * y + dc));
+            }
+        }
+        if (fabs(m[0]) > 1e-12) {
+            for (int e = 0; e < 2; e++) {
+                double y = e ? H : 0.0;
+                double x = (s * B - m[2] - m[1] * y) / m[0];
+                if (x >= -1e-6 && x <= W + 1e-6) dev = fmax(dev, fabs(da * x + db * y + dc));
+            }
+        }
+    }
+    return dev;
+}
+
+__global__ void __launch_bounds__(128) prep_kernel(ChunkArgs a, int max_groups) {
+    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int total = a.gstart[a.npairs];
+    if (gid >= total || gid >= max_groups) return;
+    const int p = find_pair(a.gstart, a.npairs, gid);
+    const int pg = a.p0 + p;
+    const int64_t q0 = a.qlist_off[pg];
+    const int64_t s0 = q0 - a.qbase;
+    const int4 g = a.grec[s0 + (gid - a.gstart[p])];
+    const int ti = a.pair_t[pg], qi = a.pair_q[pg];
+    const double W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1];
+    const double* rl = a.q_line + 3 * (s0 + g.x);
+    const double r[3] = {rl[0], rl[1], rl[2]};
+    GroupPrep out;
+    double pa[2], pb[2];
+    out.sl0 = r[0]; out.sl1 = r[1]; out.sl2 = r[2];
+    if (clip_scalar(r[0], r[1], r[2], W, H, a.d, pa, pb)) {
+        out.pax = pa[0]; out.pay = pa[1]; out.pbx = pb[0]; out.pby = pb[1];
+        out.len = np_hypot(pb[0] - pa[0], pb[1] - pa[1]);
+        long long K = (long long)ceil(out.len / a.d);
+        out.K = (int)(K < 1 ? 1 : K);
+    } else {
+        out.pax = out.pay = out.pbx = out.pby = 0.0;
+        out.len = 0.0;
+        out.K = -1;
+    }
+    double dev = 0.0;
+    if (g.y == 1) {
+        // a singleton's own band uses the dgemv-rounded line (guided.py:443-446, m == 1)
+        double F[9];
+        for (int j = 0; j < 9; j++) F[j] = a.pair_F[9 * (int64_t)pg + j];
+        const int fid = a.qlist[q0 + g.x];
+        const float2 p2 = a.xy[a.img_off[qi] + fid];
+        double l[3];
+        epiline(F, (double)p2.x, (double)p2.y, true, l);
+        double nrm = fmax(np_hypot(l[0], l[1]), 1e-15);
+        l[0] /= nrm; l[1] /= nrm; l[2] /= nrm;
+        out.sl0 = l[0]; out.sl1 = l[1]; out.sl2 = l[2];
+        dev = band_deviation(l, r, W, H, a.d);
+    } else {
+        for (int j = 0; j < g.y; j++) {
+            const double* ml = a.q_line + 3 * (int64_t)a.members[g.z + j];
+            const double m[3] = {ml[0], ml[1], ml[2]};
+            dev = fmax(dev, band_deviation(m, r, W, H, a.d));
+        }
+    }
+    double R = a.d + dev + 0.05;
+    const double reach = 2.0 * sqrt(2.0) * a.D + 0.05;   // C' never reaches further
+    out.R = (float)(R < reach ? R : reach);
+    a.prep[gid] = out;
+}
+
+// mma.sync m16n8k32 u8 x u8 -> s32 (legacy IMMA path; rows = candidates, cols = members)
+__device__ __forceinline__ void mma_u8(int (&c)[4], unsigned a0, unsigned a1, unsigned a2,
+                                       unsigned a3, unsigned b0, unsigned b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};\n"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void top2_push(unsigned key, unsigned& b1, unsigned& b2) {
+    unsigned lo = min(key, b1), hi = max(key, b1);
+    b1 = lo;
+    b2 = min(b2, hi);
+}
+
+__device__ __forceinline__ void top2_merge(unsigned& b1, unsigned& b2, unsigned o1, unsigned o2) {
+    unsigned lo = min(b1, o1), hi = max(b1, o1);
+    b1 = lo;
+    b2 = min(hi, min(b2, o2));
+}
+
+struct GroupCtx {
+    // representative line and its padded sample segment
+    float ar, br, cr;       // rep line (fp32)
+    float R, hsure;         // strip half-width, sure-in-C' distance
+    float pbx, pby, dirx, diry, len, spacing;  // fp32 segment geometry
+    double pax, pay, pbx64, pby64;
+    int K;
+    float invK, dxf, dyf;   // fp32 sample interpolation
+    float slack;            // subcell boundary slack for the fp32 fast path
+    double Wd, Hd;          // target image size
+};
+
+// Exact subcell of sample k of the rep line (guided.py:173-187 + cell_indices)
+__device__ __forceinline__ void sample_subcell(const GroupCtx& G, double D, float invD, int k,
+                                               int& u, int& v) {
+    const float t = (float)k * G.invK;
+    const float sx = fmaf(t, G.dxf, G.pbx), sy = fmaf(t, G.dyf, G.pby);
+    const float qx = sx * invD, qy = sy * invD;
+    const float fx = floorf(qx), fy = floorf(qy);
+    const float rx = qx - fx, ry = qy - fy;
+    if (rx > G.slack && rx < 1.0f - G.slack && ry > G.slack && ry < 1.0f - G.slack) {
+        u = (int)fx; v = (int)fy;
+        return;
+    }
+    const double kd = (double)k, rk = (double)(G.K - k), Kd = (double)G.K;
+    const double ex = (kd * G.pax + rk * G.pbx64) / Kd;
+    const double ey = (kd * G.pay + rk * G.pby64) / Kd;
+    u = exact_subcell(ex, D);
+    v = exact_subcell(ey, D);
+}
+
+// f in C'(rep) <=> some sample subcell is within Chebyshev distance 1 of f's.
+__device__ bool in_cprime_exact(const GroupCtx& G, double D, float invD, float fx, float fy,
+                                int fu, int fv) {
+    if (G.K < 0) return false;
+    const float tau = (fx - G.pbx) * G.dirx + (fy - G.pby) * G.diry;
+    const float reach = 2.0f * 1.41421356f * (float)D + 1.0f;
+    int klo = (int)floorf((tau - reach) / G.spacing) - 1;
+    int khi = (int)ceilf((tau + reach) / G.spacing) + 1;
+    if (klo < 0) klo = 0;
+    if (khi > G.K) khi = G.K;
+    for (int k = klo; k <= khi; k++) {
+        int u, v;
+        sample_subcell(G, D, invD, k, u, v);
+        if (abs(u - fu) <= 1 && abs(v - fv) <= 1) return true;
+    }
+    return false;
+}
+
+struct WarpSmem {
+    unsigned short list[CAP];
+    unsigned valid[CAP / 32];
+    unsigned anyb[CAP / 8];
+};
+
+__device__ __forceinline__ bool band_exact(const double* ml, bool gemv, double x, double y,
+                                           double d) {
+    double v = gemv ? fma(ml[0], x, ml[1] * y) : fma(ml[1], y, ml[0] * x);
+    v = v + ml[2];
+    return fabs(v) <= d;
+}
+
+template <bool STATS>
+__device__ void process_round(const ChunkArgs& a, const GroupCtx& G, WarpSmem& S, int n,
+                              const int4& grp, int64_t toff, int64_t qoff, int64_t qlbase,
+                              const double* singleton_line, bool first_round,
+                              int& cols_total) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const double D = a.D;
+    const float invD = (float)(1.0 / D);
+    // ---- exact C' membership for candidates outside the sure zone
+    for (int j = lane; j < ((n + 31) & ~31); j += 32) {
+        bool need = false;
+        int f = 0;
+        if (j < n) {
+            need = !((S.valid[j >> 5] >> (j & 31)) & 1u);
+            f = S.list[j];
+        }
+        bool ok = false;
+        if (need) {
+            const float2 p2 = a.xy[toff + f];
+            const int su = a.sub[toff + f];
+            const int fu = (short)(su & 0xffff), fv = su >> 16;
+            ok = in_cprime_exact(G, D, invD, p2.x, p2.y, fu, fv);
+        }
+        unsigned bal = __ballot_sync(FULL, ok);
+        if (lane == 0) S.valid[j >> 5] |= bal;
+    }
+    if (STATS) {
+        for (int w = lane; w < CAP / 8; w += 32) S.anyb[w] = 0;
+    }
+    __syncwarp();
+    const int m = grp.y;
+    const bool gemv_band = (m == 1);
+    const int ntiles = (n + 15) >> 4;
+    for (int mt0 = 0; mt0 < m; mt0 += 8) {
+        // B fragment: member mt0+g, bytes [32t, 32t+32)
+        unsigned bw[8];
+        {
+            const int j = mt0 + g;
+            if (j < m) {
+                const int slot = a.members[grp.z + j];
+                const int fid = a.qlist[qlbase + slot];
+                const uint4* row = reinterpret_cast<const uint4*>(a.desc + (qoff + fid) * 128) + 2 * t;
+                uint4 v0 = __ldg(row), v1 = __ldg(row + 1);
+                bw[0] = v0.x; bw[1] = v0.y; bw[2] = v0.z; bw[3] = v0.w;
+                bw[4] = v1.x; bw[5] = v1.y; bw[6] = v1.z; bw[7] = v1.w;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; k++) bw[k] = 0;
+            }
+        }
+        // epilogue columns 2t, 2t+1
+        float la[2], lb[2], lc[2], lo[2], hi[2];
+        unsigned qn9[2];
+        const double* mline[2];
+        int mslot[2];
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+            const int j = mt0 + 2 * t + c;
+            if (j < m) {
+                const int slot = a.members[grp.z + j];
+                mslot[c] = slot;
+                const double* L = (m == 1) ? singleton_line : a.q_line + 3 * (int64_t)slot;
+                mline[c] = L;
+                const double A = L[0], B = L[1], C = L[2];
+                la[c] = (float)A; lb[c] = (float)B; lc[c] = (float)C;
+                const int fid = a.qlist[qlbase + slot];
+                qn9[c] = (unsigned)a.norm2[qoff + fid] << 9;
+                const float eps = (float)((fabs(A) * G.Wd + fabs(B) * G.Hd + fabs(C)) * 0x1p-20) + 1e-6f;
+                lo[c] = (float)a.d - eps;
+                hi[c] = (float)a.d + eps;
+            } else {
+                mslot[c] = -1;
+                mline[c] = nullptr;
+                la[c] = 0.f; lb[c] = 0.f; lc[c] = 1e30f;
+                lo[c] = -1.f; hi[c] = -1.f;
+                qn9[c] = 0;
+            }
+        }
+        unsigned b1[2] = {NONE, NONE}, b2[2] = {NONE, NONE};
+        for (int mt = 0; mt < ntiles; mt++) {
+            const int r0 = mt * 16 + g, r1 = r0 + 8;
+            const bool v0 = r0 < n && ((S.valid[r0 >> 5] >> (r0 & 31)) & 1u);
+            const bool v1 = r1 < n && ((S.valid[r1 >> 5] >> (r1 & 31)) & 1u);
+            const int f0 = r0 < n ? S.list[r0] : 0, f1 = r1 < n ? S.list[r1] : 0;
+            const uint4* row0 = reinterpret_cast<const uint4*>(a.desc + (toff + f0) * 128) + 2 * t;
+            const uint4* row1 = reinterpret_cast<const uint4*>(a.desc + (toff + f1) * 128) + 2 * t;
+            const uint4 x00 = __ldg(row0), x01 = __ldg(row0 + 1);
+            const uint4 x10 = __ldg(row1), x11 = __ldg(row1 + 1);
+            float2 p0 = a.xy[toff + f0], p1 = a.xy[toff + f1];
+            if (!v0) { p0.x = 1e30f; p0.y = 1e30f; }
+            if (!v1) { p1.x = 1e30f; p1.y = 1e30f; }
+            const unsigned tb0 = ((unsigned)a.norm2[toff + f0] << 9) | (unsigned)r0;
+            const unsigned tb1 = ((unsigned)a.norm2[toff + f1] << 9) | (unsigned)r1;
+            int acc[4] = {0, 0, 0, 0};
+            mma_u8(acc, x00.x, x10.x, x00.y, x10.y, bw[0], bw[1]);
+            mma_u8(acc, x00.z, x10.z, x00.w, x10.w, bw[2], bw[3]);
+            mma_u8(acc, x01.x, x11.x, x01.y, x11.y, bw[4], bw[5]);
+            mma_u8(acc, x01.z, x11.z, x01.w, x11.w, bw[6], bw[7]);
+            bool inb[4];
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const int c = e & 1;
+                const float2 P = (e < 2) ? p0 : p1;
+                const float v = fmaf(la[c], P.x, fmaf(lb[c], P.y, lc[c]));
+                const float av = fabsf(v);
+                bool in = av <= lo[c];
+                if (!in && av <= hi[c]) {
+                    in = band_exact(mline[c], gemv_band, (double)P.x, (double)P.y, a.d);
+                }
+                inb[e] = in;
+                const unsigned base = ((e < 2) ? tb0 : tb1) + qn9[c];
+                const unsigned key = in ? base - ((unsigned)acc[e] << 10) : NONE;
+                top2_push(key, b1[c], b2[c]);
+            }
+            if (STATS) {
+                unsigned m0 = __ballot_sync(FULL, inb[0] || inb[1]);
+                unsigned m1 = __ballot_sync(FULL, inb[2] || inb[3]);
+                if (lane == 0) {
+                    m0 |= m0 >> 1; m0 |= m0 >> 2;
+                    m1 |= m1 >> 1; m1 |= m1 >> 2;
+                    S.anyb[2 * mt] |= m0 & 0x11111111u;
+                    S.anyb[2 * mt + 1] |= m1 & 0x11111111u;
+                }
+            }
+        }
+        // reduce across the 8 lanes sharing t
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+                unsigned o1 = __shfl_xor_sync(FULL, b1[c], o);
+                unsigned o2 = __shfl_xor_sync(FULL, b2[c], o);
+                top2_merge(b1[c], b2[c], o1, o2);
+            }
+        }
+        if (g == 0) {
+#pragma unroll
+            for (int c = 0; c < 2; c++) {
+                if (mslot[c] < 0) continue;
+                unsigned long long best = ~0ull;
+                unsigned sec = NONE;
+                if (b1[c] != NONE) {
+                    const unsigned d2 = b1[c] >> 9;
+                    const int tid = S.list[b1[c] & 511u];
+                    best = ((unsigned long long)d2 << 32) | (unsigned)tid;
+                }
+                if (b2[c] != NONE) sec = b2[c] >> 9;
+                if (!first_round) {
+                    const unsigned long long ob = a.mstate[mslot[c]];
+                    const unsigned os = a.mstate2[mslot[c]];
+                    const unsigned bd = (unsigned)(best >> 32), od = (unsigned)(ob >> 32);
+                    const unsigned nb = min(bd, od), nh = max(bd, od);
+                    const unsigned long long nbest = (bd < od) ? best : ob;
+                    sec = min(nh, min(sec, os));
+                    best = (nb == NONE) ? ~0ull : nbest;
+                }
+                a.mstate[mslot[c]] = best;
+                a.mstate2[mslot[c]] = sec;
+            }
+        }
+    }
+    if (STATS) {
+        __syncwarp();
+        int cnt = 0;
+        for (int w = lane; w < ((ntiles * 2 + 31) & ~31); w += 32) cnt += w < ntiles * 2 ? __popc(S.anyb[w]) : 0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+        cols_total += cnt;
+    }
+    __syncwarp();
+}
+
+template <bool STATS>
+__global__ void __launch_bounds__(WARPS * 32) match_kernel(ChunkArgs a) {
+    __shared__ WarpSmem smem[WARPS];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WarpSmem& S = smem[warp];
+    const int total = a.gstart[a.npairs];
+    const double D = a.D;
+    for (int gid = blockIdx.x * WARPS + warp; gid < total; gid += gridDim.x * WARPS) {
+        const int p = find_pair(a.gstart, a.npairs, gid);
+        const int pg = a.p0 + p;
+        const int64_t q0 = a.qlist_off[pg];
+        const int64_t s0 = q0 - a.qbase;
+        const int4 grp = a.grec[s0 + (gid - a.gstart[p])];
+        const GroupPrep P = a.prep[gid];
+        if (P.K < 0) continue;   // line misses the padded image: empty C'
+        const int ti = a.pair_t[pg], qi = a.pair_q[pg];
+        const int64_t toff = a.img_off[ti], qoff = a.img_off[qi];
+        const int W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1];
+        const double* rl = a.q_line + 3 * (s0 + grp.x);
+        GroupCtx G;
+        G.ar = (float)rl[0]; G.br = (float)rl[1]; G.cr = (float)rl[2];
+        G.R = P.R;
+        {
+            const double hs2 = D * D - 0.25 * a.d * a.d;
+            G.hsure = hs2 > 0 ? (float)(sqrt(hs2) - 0.075) : -1.0f;
+        }
+        G.pax = P.pax; G.pay = P.pay; G.pbx64 = P.pbx; G.pby64 = P.pby;
+        G.pbx = (float)P.pbx; G.pby = (float)P.pby;
+        G.dxf = (float)(P.pax - P.pbx); G.dyf = (float)(P.pay - P.pby);
+        G.len = (float)P.len;
+        G.dirx = P.len > 0 ? (float)((P.pax - P.pbx) / P.len) : 0.f;
+        G.diry = P.len > 0 ? (float)((P.pay - P.pby) / P.len) : 0.f;
+        G.K = P.K;
+        G.invK = 1.0f / (float)P.K;
+        G.spacing = fmaxf((float)(P.len / P.K), 1e-6f);
+        G.slack = (float)(4e-6 * ((double)W + (double)H + 4.0 * a.d) / D) + 1e-4f;
+        G.Wd = (double)W; G.Hd = (double)H;
+        const double singleton[3] = {P.sl0, P.sl1, P.sl2};
+
+        // ---- strip enumeration: rows of buckets along the minor direction
+        const bool horiz = fabsf(G.br) >= fabsf(G.ar);
+        const float alpha = horiz ? G.ar : G.br, beta = horiz ? G.br : G.ar;
+        const float Pmax = horiz ? (float)W : (float)H, Qmax = horiz ? (float)H : (float)W;
+        const int nbx = a.dims[2 * ti], nby = a.dims[2 * ti + 1];
+        const int nalong = horiz ? nbx : nby, nrows = horiz ? nby : nbx;
+        const int64_t toffb = horiz ? a.roff[ti] : a.coff[ti];
+        const int32_t* start = horiz ? a.rstart : a.cstart;
+        const int32_t* mem = horiz ? a.rmem : a.cmem;
+        const float Df = (float)D;
+        float qlo, qhi;
+        {
+            const float q00 = (-G.R - G.cr) / beta, q01 = (G.R - G.cr) / beta;
+            const float q10 = (-G.R - G.cr - alpha * Pmax) / beta, q11 = (G.R - G.cr - alpha * Pmax) / beta;
+            qlo = fminf(fminf(q00, q01), fminf(q10, q11));
+            qhi = fmaxf(fmaxf(q00, q01), fmaxf(q10, q11));
+        }
+        int rlo = (int)floorf((fmaxf(qlo, 0.f) - 0.01f) / Df), rhi = (int)floorf((fminf(qhi, Qmax) + 0.01f) / Df);
+        rlo = max(rlo, 0);
+        rhi = min(rhi, nrows - 1);
+        int n = 0;
+        bool first_round = true;
+        int cols_total = 0;
+        if (lane < CAP / 32) S.valid[lane] = 0;
+        __syncwarp();
+        for (int r0 = rlo; r0 <= rhi; r0 += 32) {
+            const int r = r0 + lane;
+            int bs = 0, len = 0;
+            if (r <= rhi) {
+                int blo = 0, bhi = nalong - 1;
+                if (fabsf(alpha) > 1e-6f) {
+                    const float y0 = r * Df - 0.01f, y1 = (r + 1) * Df + 0.01f;
+                    const float e00 = (-G.R - beta * y0 - G.cr) / alpha, e01 = (G.R - beta * y0 - G.cr) / alpha;
+                    const float e10 = (-G.R - beta * y1 - G.cr) / alpha, e11 = (G.R - beta * y1 - G.cr) / alpha;
+                    const float plo = fminf(fminf(e00, e01), fminf(e10, e11));
+                    const float phi = fmaxf(fmaxf(e00, e01), fmaxf(e10, e11));
+                    blo = max(blo, (int)floorf(fmaxf(plo - 0.01f, -1.f) / Df));
+                    bhi = min(bhi, (int)floorf(fminf(phi + 0.01f, Pmax + 1.f) / Df));
+                }
+                if (blo <= bhi) {
+                    const int64_t cb = toffb + (int64_t)r * nalong;
+                    bs = start[cb + blo];
+                    len = start[cb + bhi + 1] - bs;
+                }
+            }
+            int incl = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int y = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int tot = __shfl_sync(FULL, incl, 31);
+            for (int j0 = 0; j0 < tot; j0 += 32) {
+                const int j = j0 + lane;
+                int o = 0;
+#pragma unroll
+                for (int s = 16; s > 0; s >>= 1) {
+                    int v = __shfl_sync(FULL, incl, o + s - 1);
+                    if (v <= j) o += s;
+                }
+                const int ob = __shfl_sync(FULL, bs, o & 31);
+                const int oex = __shfl_sync(FULL, incl - len, o & 31);
+                bool pass = false, sure = false;
+                int f = 0;
+                if (j < tot) {
+                    f = mem[ob + (j - oex)];
+                    const float2 p2 = a.xy[toff + f];
+                    const float dr = fmaf(G.ar, p2.x, fmaf(G.br, p2.y, G.cr));
+                    const float adr = fabsf(dr);
+                    pass = adr <= G.R;
+                    const float tau = (p2.x - G.pbx) * G.dirx + (p2.y - G.pby) * G.diry;
+                    sure = adr <= G.hsure && tau >= 0.05f && tau <= G.len - 0.05f;
+                }
+                const unsigned bal = __ballot_sync(FULL, pass);
+                const int cnt = __popc(bal);
+                if (n + cnt > CAP) {
+                    __syncwarp();
+                    process_round<STATS>(a, G, S, n, grp, toff, qoff, q0 - s0, singleton, first_round, cols_total);
+                    first_round = false;
+                    n = 0;
+                    if (lane < CAP / 32) S.valid[lane] = 0;
+                    __syncwarp();
+                }
+                const int k = __popc(bal & ((1u << lane) - 1u));
+                if (pass) S.list[n + k] = (unsigned short)f;
+                // sure bits, compacted to list order (positions n .. n+cnt-1)
+                const unsigned bits = __reduce_or_sync(FULL, (pass && sure) ? (1u << k) : 0u);
+                if (lane == 0 && cnt) {
+                    const int w = n >> 5, sh = n & 31;
+                    S.valid[w] |= bits << sh;
+                    if (sh && sh + cnt > 32) S.valid[w + 1] |= bits >> (32 - sh);
+                }
+                n += cnt;
+                __syncwarp();
+            }
+        }
+        if (n > 0) {
+            __syncwarp();
+            process_round<STATS>(a, G, S, n, grp, toff, qoff, q0 - s0, singleton, first_round, cols_total);
+            first_round = false;
+        }
+        __syncwarp();
+        // ---- ratio test + dedupe per member (ratio_filter / _dedupe_targets)
+        if (!first_round) {
+            for (int j = lane; j < grp.y; j += 32) {
+                const int slot = a.members[grp.z + j];
+                const unsigned long long best = a.mstate[slot];
+                const unsigned sec = a.mstate2[slot];
+                if (best == ~0ull) continue;
+                const unsigned bd2 = (unsigned)(best >> 32);
+                const int tid = (int)(best & 0xffffffffu);
+                const float db = sqrtf((float)bd2);
+                float r;
+                bool acc;
+                if (sec == NONE) {
+                    acc = db < a.single_cap;
+                    r = 0.0f;
+                } else {
+                    const float ds = sqrtf((float)sec);
+                    r = ds > 0.0f ? db / ds : 1.0f;
+                    acc = r < a.ratio;
+                }
+                if (!acc) continue;
+                const int qid = a.qlist[q0 - s0 + slot];
+                a.res_tid[slot] = tid;
+                a.res_dist[slot] = db;
+                a.res_ratio[slot] = r;
+                const unsigned long long key =
+                    ((unsigned long long)__float_as_uint(db) << 32) | (unsigned)qid;
+                atomicMin(&a.dedupe[a.tbase[p] + tid], key);
+            }
+        }
+        if (STATS && lane == 0 && cols_total > 0) {
+            atomicAdd(&a.stats[2 * pg], (unsigned long long)grp.y);
+            atomicAdd(&a.stats[2 * pg + 1], (unsigned long long)grp.y * (unsigned long long)cols_total);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) compact_kernel(ChunkArgs a) {
+    __shared__ int sm[256 / 32 + 1];
+    const int p = blockIdx.x, pg = a.p0 + p;
+    const int64_t q0 = a.qlist_off[pg];
+    const int nq = (int)(a.qlist_off[pg + 1] - q0);
+    const int64_t s0 = q0 - a.qbase;
+    const int64_t db = a.tbase[p];
+    int carry = 0;
+    for (int i0 = 0; i0 < nq; i0 += 256) {
+        const int i = i0 + threadIdx.x;
+        bool keep = false;
+        int tid = -1, qid = 0;
+        float dist = 0.f;
+        if (i < nq) {
+            tid = a.res_tid[s0 + i];
+            if (tid >= 0) {
+                qid = a.qlist[q0 + i];
+                dist = a.res_dist[s0 + i];
+                const unsigned long long key =
+                    ((unsigned long long)__float_as_uint(dist) << 32) | (unsigned)qid;
+                keep = a.dedupe[db + tid] == key;
+            }
+        }
+        int tot;
+        const int ex = block_exclusive_scan<256>(keep ? 1 : 0, &tot, sm);
+        if (keep) {
+            const int64_t o = q0 + carry + ex;
+            a.out_q[o] = qid;
+            a.out_t[o] = tid;
+            a.out_dist[o] = dist;
+            a.out_ratio[o] = a.res_ratio[s0 + i];
+        }
+        carry += tot;
+    }
+    if (threadIdx.x == 0) a.out_count[pg] = carry;
+}
+
+// workspace plan for one chunk
+struct ChunkSizes {
+    int64_t P, Q, T, NT;
+};
+
+size_t chunk_bytes(const ChunkSizes& c) {
+    size_t b = 0;
+    b += aligned_bytes<int64_t>(c.P + 1) * 2;          // tab_off, tbase
+    b += aligned_bytes<int32_t>(c.P + 1) * 2;          // ngroups, gstart
+    b += aligned_bytes<unsigned long long>(c.T);       // tab_key
+    b += aligned_bytes<unsigned>(c.T) * 2;             // tab_rep, tab_cnt
+    b += aligned_bytes<int32_t>(c.Q);                  // q_tab
+    b += aligned_bytes<double>(3 * c.Q);               // q_line
+    b += aligned_bytes<int4>(c.Q);                     // grec
+    b += aligned_bytes<int32_t>(c.Q) * 2;              // gfill, members
+    b += aligned_bytes<GroupPrep>(c.Q);                // prep
+    b += aligned_bytes<unsigned long long>(c.Q);       // mstate
+    b += aligned_bytes<unsigned>(c.Q);                 // mstate2
+    b += aligned_bytes<int32_t>(c.Q) * 3;              // res_tid/dist/ratio
+    b += aligned_bytes<unsigned long long>(c.NT);      // dedupe
+    return b + 4096;
+}
+
+}  // namespace
+}  // namespace msfm
+
+using namespace msfm;
+
+extern "C" int msfm_feature_norms(const uint8_t* d_desc, int64_t n, int32_t* d_norm2, void* stream) {
+    if (n < 0 || (n > 0 && (!d_desc || !d_norm2))) {
+        set_error("msfm_feature_norms: bad arguments");
+        return MSFM_EINVAL;
+    }
+    if (n == 0) return MSFM_OK;
+    norms_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(d_desc, n, d_norm2);
+    MSFM_LAUNCH_CHECK();
+    return MSFM_OK;
+}
+
+extern "C" int msfm_grid_dims(int32_t width, int32_t height, double D, int32_t dims_out[2]) {
+    if (!(D > 0) || width < 0 || height < 0 || !dims_out) {
+        set_error("msfm_grid_dims: cell half-size D must be positive, got %g", D);
+        return MSFM_EINVAL;
+    }
+    dims_out[0] = (int32_t)floor((double)width / D) + 1;
+    dims_out[1] = (int32_t)floor((double)height / D) + 1;
+    return MSFM_OK;
+}
+
+extern "C" size_t msfm_grid_workspace_bytes(int64_t n_buckets_total) {
+    int64_t nb = (n_buckets_total + 1 + SCAN_T * SCAN_PER - 1) / (SCAN_T * SCAN_PER) + 1;
+    return aligned_bytes<int32_t>(n_buckets_total + 1) * 2 + aligned_bytes<int32_t>(nb) + 1024;
+}
+
+extern "C" int msfm_grid_build(const msfm_bank* bank, const int32_t* d_dims, const int64_t* d_roff,
+                               const int64_t* d_coff, int64_t n_buckets_total, int64_t n_total,
+                               double D, int32_t* d_sub, int32_t* d_rstart, int32_t* d_cstart,
+                               int32_t* d_rmem, int32_t* d_cmem, void* d_workspace,
+                               size_t workspace_bytes, void* stream) {
+    if (!bank || !(D > 0) || n_buckets_total < 0 || n_total < 0) {
+        set_error("msfm_grid_build: bad arguments (D=%g)", D);
+        return MSFM_EINVAL;
+    }
+    if (workspace_bytes < msfm_grid_workspace_bytes(n_buckets_total)) {
+        set_error("msfm_grid_build: workspace too small");
+        return MSFM_EWORKSPACE;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    Arena ar(d_workspace, workspace_bytes);
+    int32_t* rcur = ar.take<int32_t>(n_buckets_total + 1);
+    int32_t* ccur = ar.take<int32_t>(n_buckets_total + 1);
+    int64_t nb = (n_buckets_total + 1 + SCAN_T * SCAN_PER - 1) / (SCAN_T * SCAN_PER) + 1;
+    int32_t* bsum = ar.take<int32_t>(nb);
+    MSFM_CUDA_TRY(cudaMemsetAsync(d_rstart, 0, sizeof(int32_t) * (n_buckets_total + 1), st));
+    MSFM_CUDA_TRY(cudaMemsetAsync(d_cstart, 0, sizeof(int32_t) * (n_buckets_total + 1), st));
+    if (bank->n_images == 0) return MSFM_OK;
+    GridBuildArgs a{reinterpret_cast<const float2*>(bank->d_xy), bank->d_img_off, bank->d_img_n,
+                    bank->d_img_wh, d_dims, d_roff, d_coff, d_sub, d_rstart, d_cstart, rcur, ccur,
+                    d_rmem, d_cmem, D};
+    grid_count_kernel<<<bank->n_images, 256, 0, st>>>(a);
+    MSFM_LAUNCH_CHECK();
+    int rc = exclusive_scan(d_rstart, n_buckets_total + 1, rcur, bsum, st);
+    if (rc) return rc;
+    rc = exclusive_scan(d_cstart, n_buckets_total + 1, ccur, bsum, st);
+    if (rc) return rc;
+    grid_scatter_kernel<<<bank->n_images, 256, 0, st>>>(a);
+    MSFM_LAUNCH_CHECK();
+    return MSFM_OK;
+}
+
+static void plan_chunks(int32_t n_pairs, const int64_t* h_qlist_off, const msfm_match_params* prm,
+                        std::vector<int>& bounds, ChunkSizes& worst) {
+    const int cp = prm->chunk_pairs > 0 ? prm->chunk_pairs : 256;
+    bounds.clear();
+    worst = {0, 0, 0, 0};
+    int p = 0;
+    bounds.push_back(0);
+    while (p < n_pairs) {
+        int e = p + cp < n_pairs ? p + cp : n_pairs;
+        ChunkSizes c;
+        c.P = e - p;
+        c.Q = h_qlist_off[e] - h_qlist_off[p];
+        c.T = 2 * (c.Q + c.P) + 2 * c.P;
+        c.NT = c.P * (int64_t)prm->max_nt;
+        if (c.P > worst.P) worst.P = c.P;
+        if (c.Q > worst.Q) worst.Q = c.Q;
+        if (c.T > worst.T) worst.T = c.T;
+        if (c.NT > worst.NT) worst.NT = c.NT;
+        bounds.push_back(e);
+        p = e;
+    }
+}
+
+extern "C" size_t msfm_guided_workspace_bytes(int32_t n_pairs, const int64_t* h_qlist_off,
+                                              const msfm_match_params* prm) {
+    if (!prm || !h_qlist_off || n_pairs < 0) return 0;
+    std::vector<int> bounds;
+    ChunkSizes w;
+    plan_chunks(n_pairs, h_qlist_off, prm, bounds, w);
+    return chunk_bytes(w);
+}
+
+extern "C" int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids, int32_t n_pairs,
+                                 const int32_t* d_pair_q, const int32_t* d_pair_t,
+                                 const double* d_pair_F, const int64_t* d_qlist_off,
+                                 const int32_t* d_qlist, const int64_t* h_qlist_off,
+                                 const msfm_match_params* prm, int32_t* d_out_q, int32_t* d_out_t,
+                                 float* d_out_dist, float* d_out_ratio, int32_t* d_out_count,
+                                 int64_t* d_stats, void* d_workspace, size_t workspace_bytes,
+                                 void* stream) {
+    if (!bank || !grids || !prm || n_pairs < 0 || !h_qlist_off) {
+        set_error("msfm_guided_match: null argument");
+        return MSFM_EINVAL;
+    }
+    if (!(prm->d > 0)) {
+        set_error("msfm_guided_match: band d must be positive, got %g", prm->d);
+        return MSFM_EINVAL;
+    }
+    if (!(grids->D > 0)) {
+        set_error("msfm_guided_match: grid cell half-size must be positive, got %g", grids->D);
+        return MSFM_EINVAL;
+    }
+    if (prm->max_nt > 65536) {
+        set_error("msfm_guided_match: images with more than 65536 features are not supported");
+        return MSFM_EINVAL;
+    }
+    if (!(prm->ratio <= 1.0f)) {
+        set_error("msfm_guided_match: ratio > 1 is not supported (got %g)", (double)prm->ratio);
+        return MSFM_EINVAL;
+    }
+    if (n_pairs == 0) return MSFM_OK;
+    std::vector<int> bounds;
+    ChunkSizes w;
+    plan_chunks(n_pairs, h_qlist_off, prm, bounds, w);
+    if (workspace_bytes < chunk_bytes(w)) {
+        set_error("msfm_guided_match: workspace too small (%zu < %zu)", workspace_bytes, chunk_bytes(w));
+        return MSFM_EWORKSPACE;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (d_stats) MSFM_CUDA_TRY(cudaMemsetAsync(d_stats, 0, sizeof(int64_t) * 2 * n_pairs, st));
+    Arena ar(d_workspace, workspace_bytes);
+    ChunkArgs a;
+    a.xy = reinterpret_cast<const float2*>(bank->d_xy);
+    a.desc = bank->d_desc; a.norm2 = bank->d_norm2;
+    a.img_off = bank->d_img_off; a.img_n = bank->d_img_n; a.img_wh = bank->d_img_wh;
+    a.sub = grids->d_sub; a.dims = grids->d_dims; a.roff = grids->d_roff; a.coff = grids->d_coff;
+    a.rstart = grids->d_rstart; a.cstart = grids->d_cstart; a.rmem = grids->d_rmem; a.cmem = grids->d_cmem;
+    a.D = grids->D; a.d = prm->d; a.ratio = prm->ratio; a.single_cap = prm->single_cap;
+    a.pair_q = d_pair_q; a.pair_t = d_pair_t; a.pair_F = d_pair_F;
+    a.qlist_off = d_qlist_off; a.qlist = d_qlist;
+    a.tab_off = ar.take<int64_t>(w.P + 1); a.tbase = ar.take<int64_t>(w.P + 1);
+    a.ngroups = ar.take<int32_t>(w.P + 1); a.gstart = ar.take<int32_t>(w.P + 1);
+    a.tab_key = ar.take<unsigned long long>(w.T);
+    a.tab_rep = ar.take<unsigned>(w.T); a.tab_cnt = ar.take<unsigned>(w.T);
+    a.q_tab = ar.take<int32_t>(w.Q); a.q_line = ar.take<double>(3 * w.Q);
+    a.grec = ar.take<int4>(w.Q);
+    a.gfill = ar.take<int32_t>(w.Q); a.members = ar.take<int32_t>(w.Q);
+    a.prep = ar.take<GroupPrep>(w.Q);
+    a.mstate = ar.take<unsigned long long>(w.Q); a.mstate2 = ar.take<unsigned>(w.Q);
+    a.res_tid = ar.take<int32_t>(w.Q); a.res_dist = ar.take<float>(w.Q); a.res_ratio = ar.take<float>(w.Q);
+    a.dedupe = ar.take<unsigned long long>(w.NT);
+    a.stats = reinterpret_cast<unsigned long long*>(d_stats);
+    a.out_q = d_out_q; a.out_t = d_out_t; a.out_dist = d_out_dist; a.out_ratio = d_out_ratio;
+    a.out_count = d_out_count;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    for (size_t c = 0; c + 1 < bounds.size(); c++) {
+        const int p0 = bounds[c], p1 = bounds[c + 1];
+        a.p0 = p0;
+        a.npairs = p1 - p0;
+        a.qbase = h_qlist_off[p0];
+        const int64_t Q = h_qlist_off[p1] - h_qlist_off[p0];
+        plan_kernel<<<1, SCAN_T, 0, st>>>(a);
+        lines_kernel<<<a.npairs, 256, 0, st>>>(a);
+        groups_kernel<<<a.npairs, 256, 0, st>>>(a);
+        gscan_kernel<<<1, SCAN_T, 0, st>>>(a);
+        scatter_kernel<<<a.npairs, 256, 0, st>>>(a);
+        if (Q > 0) prep_kernel<<<(unsigned)((Q + 127) / 128), 128, 0, st>>>(a, (int)Q);
+        if (d_stats) match_kernel<true><<<nsm * 4, WARPS * 32, 0, st>>>(a);
+        else         match_kernel<false><<<nsm * 4, WARPS * 32, 0, st>>>(a);
+        compact_kernel<<<a.npairs, 256, 0, st>>>(a);
+        MSFM_LAUNCH_CHECK();
+    }
+    return MSFM_OK;
+}

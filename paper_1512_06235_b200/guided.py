@@ -1,0 +1,190 @@
+"""Geometry-aware pair matching: batched device API + reference-shaped drop-in.
+
+``match_pairs`` is the throughput API (one C-ABI call for a whole stage's
+pairs, results stay on the device).  ``guided_match_pair`` keeps the exact
+signature, defaults, errors and return type of the reference
+``msfm.guided.guided_match_pair`` (pkg/src/msfm/guided.py:393-480) and runs the
+same kernels on a two-image bank.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .bank import FeatureBank
+from .types import FeatureRef, Match, SearchStats
+
+BAND_D_PX = 8.0          # guided.py:39
+GRID_INFLATION = 1.25    # guided.py:40
+RATIO_GUIDED = 0.8       # matching.py:22
+SINGLE_CANDIDATE_CAP = 45.0  # matching.py:27
+
+
+@dataclass
+class PairMatches:
+    """Device-resident output of ``match_pairs`` (per-pair segments)."""
+
+    q: "object"       # int32 (total_queries,) — segment k at [qoff[k], qoff[k]+count[k])
+    t: "object"
+    dist: "object"    # float32
+    ratio: "object"   # float32
+    count: "object"   # int32 (n_pairs,)
+    qoff: np.ndarray  # host int64 (n_pairs+1,)
+    stats: "object"   # int64 (n_pairs, 2) or None
+
+    def to_host(self):
+        """Concatenated (pair_index, q, t, dist, ratio) numpy arrays in pair order."""
+        import torch
+
+        cnt = self.count.cpu().numpy().astype(np.int64)
+        idx = np.concatenate([np.arange(self.qoff[k], self.qoff[k] + cnt[k])
+                              for k in range(len(cnt))]) if len(cnt) else np.zeros(0, np.int64)
+        sel = torch.from_numpy(idx).to(self.q.device)
+        pair = np.repeat(np.arange(len(cnt)), cnt)
+        return (pair, self.q[sel].cpu().numpy(), self.t[sel].cpu().numpy(),
+                self.dist[sel].cpu().numpy(), self.ratio[sel].cpu().numpy())
+
+
+def match_pairs(bank: FeatureBank, q_img, t_img, F, query_lists, *, d: float = BAND_D_PX,
+                ratio: float = RATIO_GUIDED, inflation: float = GRID_INFLATION,
+                grid_d: float | None = None, single_cap: float = SINGLE_CANDIDATE_CAP,
+                with_stats: bool = False, chunk_pairs: int = 0, stream=None,
+                device_inputs=None) -> PairMatches:
+    """Match every pair k: query image q_img[k] against target t_img[k].
+
+    ``F`` is (P,3,3) float64 (NaN rows mark degenerate pairs, skipped as
+    densify.py:161-165 does); ``query_lists[k]`` are the query feature ids
+    (ascending, unique).  Image ids are the bank's.
+    """
+    import torch
+
+    lib = _lib.load()
+    if d <= 0:
+        raise ValueError(f"cell half-size d must be positive, got {d}")
+    D = float(grid_d) if grid_d is not None else float(d) * float(inflation)
+    P = len(q_img)
+    dev = bank.device
+    if device_inputs is None:
+        device_inputs = prepare_pairs(bank, q_img, t_img, F, query_lists)
+    pq, pt, pF, qoff_d, qlist_d, qoff = device_inputs
+    nq_total = int(qoff[-1]) if P else 0
+    grid = bank.grid(D, stream)
+    prm = _lib.MatchParams(float(d), float(np.float32(ratio)), float(np.float32(single_cap)),
+                           max(bank.max_n, 1), int(chunk_pairs))
+    qoff_c = np.ascontiguousarray(qoff, dtype=np.int64)
+    ws_bytes = lib.msfm_guided_workspace_bytes(P, qoff_c.ctypes.data, ctypes.byref(prm))
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    cap = max(nq_total, 1)
+    out_q = torch.empty(cap, dtype=torch.int32, device=dev)
+    out_t = torch.empty(cap, dtype=torch.int32, device=dev)
+    out_d = torch.empty(cap, dtype=torch.float32, device=dev)
+    out_r = torch.empty(cap, dtype=torch.float32, device=dev)
+    out_c = torch.zeros(max(P, 1), dtype=torch.int32, device=dev)
+    stats = torch.zeros((max(P, 1), 2), dtype=torch.int64, device=dev) if with_stats else None
+    b, g = bank.cstruct(), grid.cstruct()
+    _lib.check(lib.msfm_guided_match(ctypes.byref(b), ctypes.byref(g), P, _lib.ptr(pq), _lib.ptr(pt),
+                                     _lib.ptr(pF), _lib.ptr(qoff_d), _lib.ptr(qlist_d),
+                                     qoff_c.ctypes.data, ctypes.byref(prm), _lib.ptr(out_q),
+                                     _lib.ptr(out_t), _lib.ptr(out_d), _lib.ptr(out_r),
+                                     _lib.ptr(out_c), _lib.ptr(stats), _lib.ptr(ws), ws_bytes,
+                                     _lib.stream_handle(stream)),
+               "msfm_guided_match")
+    res = PairMatches(out_q, out_t, out_d, out_r, out_c[:P], qoff, stats)
+    res._keep = (ws, device_inputs)
+    return res
+
+
+def prepare_pairs(bank: FeatureBank, q_img, t_img, F, query_lists):
+    """Stage the pair table on the device (index translation + one copy per array)."""
+    import torch
+
+    P = len(q_img)
+    qi = np.array([bank.index_of[int(i)] for i in q_img], dtype=np.int32)
+    ti = np.array([bank.index_of[int(i)] for i in t_img], dtype=np.int32)
+    Fh = np.ascontiguousarray(np.asarray(F, dtype=np.float64).reshape(P, 9))
+    lens = np.array([len(x) for x in query_lists], dtype=np.int64)
+    qoff = np.zeros(P + 1, dtype=np.int64)
+    np.cumsum(lens, out=qoff[1:])
+    qlist = np.concatenate([np.asarray(x, dtype=np.int32) for x in query_lists]) \
+        if P else np.zeros(0, np.int32)
+    dev = bank.device
+
+    def up(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().to(dev, non_blocking=True)
+
+    return (up(qi), up(ti), up(Fh), up(qoff), up(qlist if len(qlist) else np.zeros(1, np.int32)),
+            qoff)
+
+
+# ---------------------------------------------------------------------------
+# drop-in for msfm.guided.guided_match_pair
+# ---------------------------------------------------------------------------
+
+_BANK_CACHE: dict = {}
+
+
+def _pair_bank(query_fs, target_fs):
+    """Two-image bank, cached by object identity (FeatureSets are immutable
+    after load)."""
+    key = (id(query_fs), id(target_fs))
+    hit = _BANK_CACHE.get(key)
+    if hit is not None and hit[0] is query_fs and hit[1] is target_fs:
+        return hit[2]
+    if len(_BANK_CACHE) > 64:
+        _BANK_CACHE.clear()
+    bank = FeatureBank({0: query_fs, 1: target_fs})
+    _BANK_CACHE[key] = (query_fs, target_fs, bank)
+    return bank
+
+
+class _Sub:
+    """Target subset view (target_indices) with the attributes the bank reads."""
+
+    def __init__(self, fs, idx):
+        self.xy = np.asarray(fs.xy)[idx]
+        self.descriptors = np.asarray(fs.descriptors)[idx]
+        self.width, self.height = fs.width, fs.height
+
+    def __len__(self):
+        return len(self.xy)
+
+
+def guided_match_pair(query_fs, target_fs, geom, *, d: float = BAND_D_PX,
+                      ratio: float = RATIO_GUIDED, inflation: float = GRID_INFLATION,
+                      strategy: str = "grid", query_indices=None, target_indices=None,
+                      grid=None, single_cap: float = SINGLE_CANDIDATE_CAP,
+                      stats: SearchStats | None = None) -> list:
+    """Drop-in for msfm.guided.guided_match_pair (guided.py:393-480)."""
+    ti = np.arange(len(target_fs)) if target_indices is None else np.asarray(target_indices)
+    if len(ti) == 0:
+        return []
+    if strategy != "grid":
+        if strategy in ("linear", "radial"):
+            raise NotImplementedError(f"strategy {strategy!r} has no B200 kernel yet")
+        raise ValueError(f"unknown strategy {strategy!r}")
+    D = float(grid.d) if grid is not None and hasattr(grid, "d") else d * inflation
+    if D <= 0:
+        raise ValueError(f"cell half-size d must be positive, got {D}")
+    qi = np.arange(len(query_fs)) if query_indices is None else np.asarray(query_indices)
+    qi = np.unique(qi.astype(np.int64))  # duplicates cannot change the match set
+    if target_indices is None:
+        tfs = target_fs
+        bank = _pair_bank(query_fs, target_fs)
+    else:
+        tfs = _Sub(target_fs, ti)
+        bank = FeatureBank({0: query_fs, 1: tfs})
+    F = np.asarray(geom.F if hasattr(geom, "F") else geom, dtype=np.float64).reshape(1, 3, 3)
+    res = match_pairs(bank, [0], [1], F, [qi.astype(np.int32)], d=d, ratio=ratio,
+                      grid_d=D, single_cap=single_cap, with_stats=stats is not None)
+    _, q, t, dist, rat = res.to_host()
+    if stats is not None:
+        s = res.stats.cpu().numpy()
+        stats.add(int(s[0, 0]), int(s[0, 1]))
+    qimg, timg = query_fs.image_id, target_fs.image_id
+    return [Match(query=FeatureRef(qimg, int(a)), target=FeatureRef(timg, int(ti[b])),
+                  distance=float(c), ratio=float(r))
+            for a, b, c, r in zip(q, t, dist, rat)]
