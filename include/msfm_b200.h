@@ -35,6 +35,14 @@ extern "C" {
 const char* msfm_last_error(void);
 int msfm_version(void);
 
+/* Number of kernels this library has launched so far (process-wide). */
+int64_t msfm_launch_count(void);
+/* Optional CUDA-event timing of the library's hot kernels, recorded on the
+ * stream each kernel is launched on.  enable(1) clears previous records;
+ * read() synchronises on the recorded events and sums their durations. */
+int msfm_profile_enable(int on);
+int msfm_profile_read(const char* kernel_name, double* total_ms, int64_t* launches);
+
 /* ------------------------------------------------------------------------
  * Feature bank: all images' features concatenated (SoA, HBM-resident).
  *   xy    f32 [n_total][2]          FeatureSet.xy            features.py:55

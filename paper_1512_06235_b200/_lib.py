@@ -38,6 +38,10 @@ class MatchParams(ctypes.Structure):
 _SIGS = {
     "msfm_last_error": (ctypes.c_char_p, []),
     "msfm_version": (ctypes.c_int, []),
+    "msfm_launch_count": (ctypes.c_int64, []),
+    "msfm_profile_enable": (ctypes.c_int, [ctypes.c_int]),
+    "msfm_profile_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double),
+                                         ctypes.POINTER(ctypes.c_int64)]),
     "msfm_feature_norms": (ctypes.c_int, [VP, ctypes.c_int64, VP, VP]),
     "msfm_grid_dims": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_double, c_int32_p]),
     "msfm_grid_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int64]),
@@ -98,3 +102,20 @@ def stream_handle(stream=None) -> int:
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
+
+
+def launch_count() -> int:
+    return int(load(require_device=False).msfm_launch_count())
+
+
+def profile_enable(on: bool) -> None:
+    check(load(require_device=False).msfm_profile_enable(1 if on else 0), "msfm_profile_enable")
+
+
+def profile_read(name: str):
+    """(total_ms, launches) of a library kernel recorded since profile_enable(True)."""
+    ms = ctypes.c_double(0.0)
+    n = ctypes.c_int64(0)
+    check(load(require_device=False).msfm_profile_read(name.encode(), ctypes.byref(ms),
+                                                         ctypes.byref(n)), "msfm_profile_read")
+    return ms.value, n.value

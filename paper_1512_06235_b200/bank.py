@@ -17,41 +17,64 @@ import numpy as np
 from . import _lib
 
 
+class HostBank:
+    """Concatenated feature arrays in pinned host memory (the H2D staging area)."""
+
+    def __init__(self, feature_sets, image_ids=None):
+        import torch
+
+        ids = sorted(feature_sets) if image_ids is None else list(image_ids)
+        sets = [feature_sets[i] for i in ids]
+        self.image_ids = ids
+        self.counts = np.array([len(fs) for fs in sets], dtype=np.int64)
+        self.offsets = np.zeros(len(sets), dtype=np.int64)
+        if len(sets) > 1:
+            np.cumsum(self.counts[:-1], out=self.offsets[1:])
+        self.wh = np.array([[int(fs.width), int(fs.height)] for fs in sets],
+                           dtype=np.int32).reshape(-1, 2)
+        n = int(self.counts.sum())
+        self.xy = torch.empty((n, 2), dtype=torch.float32).pin_memory()
+        self.desc = torch.empty((n, 128), dtype=torch.uint8).pin_memory()
+        xy_np, desc_np = self.xy.numpy(), self.desc.numpy()
+        for k, fs in enumerate(sets):
+            lo, hi = self.offsets[k], self.offsets[k] + self.counts[k]
+            xy_np[lo:hi] = np.asarray(fs.xy, np.float32).reshape(-1, 2)
+            desc_np[lo:hi] = np.asarray(fs.descriptors, np.uint8).reshape(-1, 128)
+        self.img_off = torch.from_numpy(self.offsets.copy()).pin_memory()
+        self.img_n = torch.from_numpy(self.counts.astype(np.int32)).pin_memory()
+        self.img_wh = torch.from_numpy(self.wh.copy()).pin_memory()
+
+    @property
+    def nbytes(self) -> int:
+        return sum(int(t.numel() * t.element_size())
+                   for t in (self.xy, self.desc, self.img_off, self.img_n, self.img_wh))
+
+
 class FeatureBank:
     """Feature sets of many images, resident on one CUDA device."""
 
-    def __init__(self, feature_sets, device=None, image_ids=None, stream=None):
+    def __init__(self, feature_sets=None, device=None, image_ids=None, stream=None, host=None):
         import torch
 
         lib = _lib.load()
         self.device = torch.device(device or "cuda")
-        ids = sorted(feature_sets) if image_ids is None else list(image_ids)
-        self.image_ids = ids
-        self.index_of = {i: k for k, i in enumerate(ids)}
-        sets = [feature_sets[i] for i in ids]
-        n = np.array([len(fs) for fs in sets], dtype=np.int64)
-        off = np.zeros(len(sets), dtype=np.int64)
-        if len(sets) > 1:
-            np.cumsum(n[:-1], out=off[1:])
-        self.n_total = int(n.sum())
-        self.counts = n
-        self.offsets = off
-        self.wh = np.array([[int(fs.width), int(fs.height)] for fs in sets], dtype=np.int32).reshape(-1, 2)
-        xy = np.concatenate([np.asarray(fs.xy, np.float32).reshape(-1, 2) for fs in sets]) \
-            if sets else np.zeros((0, 2), np.float32)
-        desc = np.concatenate([np.asarray(fs.descriptors, np.uint8).reshape(-1, 128) for fs in sets]) \
-            if sets else np.zeros((0, 128), np.uint8)
+        if host is None:
+            host = HostBank(feature_sets, image_ids)
+        self.image_ids = host.image_ids
+        self.index_of = {i: k for k, i in enumerate(self.image_ids)}
+        self.counts, self.offsets, self.wh = host.counts, host.offsets, host.wh
+        self.n_total = int(self.counts.sum())
         dev = self.device
-        self.xy = _to_device(xy, dev)
-        self.desc = _to_device(desc, dev)
-        self.img_off = _to_device(off, dev)
-        self.img_n = _to_device(n.astype(np.int32), dev)
-        self.img_wh = _to_device(self.wh, dev)
+        self.xy = host.xy.to(dev, non_blocking=True)
+        self.desc = host.desc.to(dev, non_blocking=True)
+        self.img_off = host.img_off.to(dev, non_blocking=True)
+        self.img_n = host.img_n.to(dev, non_blocking=True)
+        self.img_wh = host.img_wh.to(dev, non_blocking=True)
         self.norm2 = torch.empty(self.n_total, dtype=torch.int32, device=dev)
         st = _lib.stream_handle(stream)
         _lib.check(lib.msfm_feature_norms(_lib.ptr(self.desc), self.n_total,
                                           _lib.ptr(self.norm2), st), "msfm_feature_norms")
-        self.max_n = int(n.max()) if len(n) else 0
+        self.max_n = int(self.counts.max()) if len(self.counts) else 0
         self._grids = {}
 
     @property

@@ -9,6 +9,18 @@
 namespace msfm {
 
 void set_error(const char* fmt, ...);
+void count_launches(int n);
+bool profiling();
+void prof_begin(const char* name, cudaStream_t st, void** token);
+void prof_end(void* token, cudaStream_t st);
+
+// RAII: CUDA events around the kernels launched in scope (when profiling is on)
+struct ProfScope {
+    void* tok;
+    cudaStream_t st;
+    ProfScope(const char* name, cudaStream_t s) : tok(nullptr), st(s) { prof_begin(name, s, &tok); }
+    ~ProfScope() { prof_end(tok, st); }
+};
 
 #define MSFM_CUDA_TRY(expr)                                                          \
     do {                                                                             \

@@ -285,16 +285,31 @@ int exclusive_scan(int32_t* data, int64_t n, int32_t* copy, int32_t* bsum, cudaS
     scan_bsum_kernel<<<1, SCAN_T, 0, st>>>(bsum, nb);
     scan_apply_kernel<<<(unsigned)nb, SCAN_T, 0, st>>>(data, n, bsum, copy);
     MSFM_LAUNCH_CHECK();
+    count_launches(3);
     return MSFM_OK;
 }
 
 // ------------------------------------------------------------------ matching
-struct GroupPrep {      // one per group (dense gid order), written by prep_kernel
-    double pax, pay, pbx, pby;   // padded clip of the representative line (pad = d)
-    double len;                  // |pb - pa|
-    int K;                       // sample count - 1, -1: line misses the padded image
-    float R;                     // strip half-width around the rep line
-    double sl0, sl1, sl2;        // singleton member's own (dgemv) line
+// Per-group context, computed once by prep_kernel (one thread per group) so the
+// warp-per-group match kernel starts from fp32 values and never divides in fp64.
+struct GroupRec {
+    int p, rep, cnt, moff;                 // chunk-local pair, rep slot, members, member offset
+    float ar, br, cr, R;                   // rep line (fp32) and strip half-width
+    float hsure, pbx, pby, dirx;           // sure-in-C' radius, padded segment origin (pb) + dir
+    float diry, len, spacing, invK;
+    float dxf, dyf, slack, invD;
+    int K, horiz, rlo, rhi;                // K<0: C' empty; strip orientation and bucket-row range
+    float alpha, beta, inv_alpha, Pmax;    // strip row math in the chosen orientation
+    double pax, pay, pbx64, pby64;         // exact sample interpolation (guided.py:187)
+    double sl0, sl1, sl2, spare;           // singleton member's own (dgemv) line
+};
+
+// Per-member epilogue constants (written by prep_kernel, indexed like members[]).
+struct MemberRec {
+    float a, b, c, lo;    // member line (fp32) and sure-in-band threshold d - eps
+    float hi;             // d + eps: above it the fp32 value is surely out of band
+    unsigned qn9;         // |q|^2 << 9
+    int fid, slot;        // query feature id, chunk-local slot
 };
 
 struct ChunkArgs {
@@ -314,7 +329,7 @@ struct ChunkArgs {
     int64_t* tab_off; int64_t* tbase; int32_t* ngroups; int32_t* gstart;
     unsigned long long* tab_key; unsigned* tab_rep; unsigned* tab_cnt;
     int32_t* q_tab; double* q_line;
-    int4* grec; int32_t* gfill; int32_t* members; GroupPrep* prep;
+    int4* grec; int32_t* gfill; int32_t* members; GroupRec* grp; MemberRec* mrec;
     unsigned long long* mstate;  // per member slot: best (d2<<32 | tid)
     unsigned* mstate2;           // per member slot: second d2
     int32_t* res_tid; float* res_dist; float* res_ratio;
@@ -530,46 +545,84 @@ __global__ void __launch_bounds__(128) prep_kernel(ChunkArgs a, int max_groups) 
     const int64_t s0 = q0 - a.qbase;
     const int4 g = a.grec[s0 + (gid - a.gstart[p])];
     const int ti = a.pair_t[pg], qi = a.pair_q[pg];
-    const double W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1];
+    const int Wi = a.img_wh[2 * ti], Hi = a.img_wh[2 * ti + 1];
+    const double W = Wi, H = Hi, D = a.D, d = a.d;
+    const int64_t qoff = a.img_off[qi];
     const double* rl = a.q_line + 3 * (s0 + g.x);
     const double r[3] = {rl[0], rl[1], rl[2]};
-    GroupPrep out;
-    double pa[2], pb[2];
-    out.sl0 = r[0]; out.sl1 = r[1]; out.sl2 = r[2];
-    if (clip_scalar(r[0], r[1], r[2], W, H, a.d, pa, pb)) {
-        out.pax = pa[0]; out.pay = pa[1]; out.pbx = pb[0]; out.pby = pb[1];
-        out.len = np_hypot(pb[0] - pa[0], pb[1] - pa[1]);
-        long long K = (long long)ceil(out.len / a.d);
-        out.K = (int)(K < 1 ? 1 : K);
-    } else {
-        out.pax = out.pay = out.pbx = out.pby = 0.0;
-        out.len = 0.0;
-        out.K = -1;
+    GroupRec o;
+    o.p = p; o.rep = (int)(s0 + g.x); o.cnt = g.y; o.moff = g.z;
+    o.sl0 = r[0]; o.sl1 = r[1]; o.sl2 = r[2]; o.spare = 0.0;
+    double pa[2] = {0, 0}, pb[2] = {0, 0}, len = 0.0;
+    o.K = -1;
+    if (clip_scalar(r[0], r[1], r[2], W, H, d, pa, pb)) {
+        len = np_hypot(pb[0] - pa[0], pb[1] - pa[1]);
+        long long K = (long long)ceil(len / d);
+        o.K = (int)(K < 1 ? 1 : K);
     }
+    o.pax = pa[0]; o.pay = pa[1]; o.pbx64 = pb[0]; o.pby64 = pb[1];
+    // members: own line (dgemv rounding for a singleton, guided.py:443-446), band
+    // deviation from the rep line, fp32 epilogue constants
     double dev = 0.0;
-    if (g.y == 1) {
-        // a singleton's own band uses the dgemv-rounded line (guided.py:443-446, m == 1)
-        double F[9];
+    double F[9];
+    if (g.y == 1)
         for (int j = 0; j < 9; j++) F[j] = a.pair_F[9 * (int64_t)pg + j];
-        const int fid = a.qlist[q0 + g.x];
-        const float2 p2 = a.xy[a.img_off[qi] + fid];
-        double l[3];
-        epiline(F, (double)p2.x, (double)p2.y, true, l);
-        double nrm = fmax(np_hypot(l[0], l[1]), 1e-15);
-        l[0] /= nrm; l[1] /= nrm; l[2] /= nrm;
-        out.sl0 = l[0]; out.sl1 = l[1]; out.sl2 = l[2];
-        dev = band_deviation(l, r, W, H, a.d);
-    } else {
-        for (int j = 0; j < g.y; j++) {
-            const double* ml = a.q_line + 3 * (int64_t)a.members[g.z + j];
-            const double m[3] = {ml[0], ml[1], ml[2]};
-            dev = fmax(dev, band_deviation(m, r, W, H, a.d));
+    for (int j = 0; j < g.y; j++) {
+        const int slot = a.members[g.z + j];
+        const int fid = a.qlist[a.qbase + slot];
+        double m[3];
+        if (g.y == 1) {
+            const float2 p2 = a.xy[qoff + fid];
+            epiline(F, (double)p2.x, (double)p2.y, true, m);
+            double nrm = fmax(np_hypot(m[0], m[1]), 1e-15);
+            m[0] /= nrm; m[1] /= nrm; m[2] /= nrm;
+            o.sl0 = m[0]; o.sl1 = m[1]; o.sl2 = m[2];
+        } else {
+            const double* ml = a.q_line + 3 * (int64_t)slot;
+            m[0] = ml[0]; m[1] = ml[1]; m[2] = ml[2];
         }
+        dev = fmax(dev, band_deviation(m, r, W, H, d));
+        MemberRec mr;
+        mr.a = (float)m[0]; mr.b = (float)m[1]; mr.c = (float)m[2];
+        const float eps = (float)((fabs(m[0]) * W + fabs(m[1]) * H + fabs(m[2])) * 0x1p-20) + 1e-6f;
+        mr.lo = (float)d - eps;
+        mr.hi = (float)d + eps;
+        mr.qn9 = (unsigned)a.norm2[qoff + fid] << 9;
+        mr.fid = fid;
+        mr.slot = slot;
+        a.mrec[g.z + j] = mr;
     }
-    double R = a.d + dev + 0.05;
-    const double reach = 2.0 * sqrt(2.0) * a.D + 0.05;   // C' never reaches further
-    out.R = (float)(R < reach ? R : reach);
-    a.prep[gid] = out;
+    const double reach = 2.0 * sqrt(2.0) * D + 0.05;   // C' never reaches further
+    double R = d + dev + 0.05;
+    R = R < reach ? R : reach;
+    o.ar = (float)r[0]; o.br = (float)r[1]; o.cr = (float)r[2]; o.R = (float)R;
+    const double hs2 = D * D - 0.25 * d * d;
+    o.hsure = hs2 > 0 ? (float)(sqrt(hs2) - 0.075) : -1.0f;
+    o.pbx = (float)pb[0]; o.pby = (float)pb[1];
+    o.dirx = len > 0 ? (float)((pa[0] - pb[0]) / len) : 0.f;
+    o.diry = len > 0 ? (float)((pa[1] - pb[1]) / len) : 0.f;
+    o.len = (float)len;
+    o.spacing = o.K > 0 ? fmaxf((float)(len / o.K), 1e-6f) : 1.0f;
+    o.invK = o.K > 0 ? (float)(1.0 / o.K) : 0.f;
+    o.dxf = (float)(pa[0] - pb[0]); o.dyf = (float)(pa[1] - pb[1]);
+    o.slack = (float)(4e-6 * (W + H + 4.0 * d) / D) + 1e-4f;
+    o.invD = (float)(1.0 / D);
+    // strip rows: buckets along the minor direction of the line
+    const bool horiz = fabs(r[1]) >= fabs(r[0]);
+    const double al = horiz ? r[0] : r[1], be = horiz ? r[1] : r[0];
+    const double Pm = horiz ? W : H, Qm = horiz ? H : W;
+    const int nrows = horiz ? a.dims[2 * ti + 1] : a.dims[2 * ti];
+    double qv[4] = {(-R - r[2]) / be, (R - r[2]) / be, (-R - r[2] - al * Pm) / be, (R - r[2] - al * Pm) / be};
+    double qlo = fmin(fmin(qv[0], qv[1]), fmin(qv[2], qv[3]));
+    double qhi = fmax(fmax(qv[0], qv[1]), fmax(qv[2], qv[3]));
+    int rlo = (int)floor((fmax(qlo, 0.0) - 0.01) / D), rhi = (int)floor((fmin(qhi, Qm) + 0.01) / D);
+    o.horiz = horiz;
+    o.rlo = rlo < 0 ? 0 : rlo;
+    o.rhi = rhi > nrows - 1 ? nrows - 1 : rhi;
+    o.alpha = (float)al; o.beta = (float)be;
+    o.inv_alpha = fabs(al) > 1e-6 ? (float)(1.0 / al) : 0.f;
+    o.Pmax = (float)Pm;
+    a.grp[gid] = o;
 }
 
 // mma.sync m16n8k32 u8 x u8 -> s32 (legacy IMMA path; rows = candidates, cols = members)
@@ -594,24 +647,12 @@ __device__ __forceinline__ void top2_merge(unsigned& b1, unsigned& b2, unsigned 
     b2 = min(hi, min(b2, o2));
 }
 
-struct GroupCtx {
-    // representative line and its padded sample segment
-    float ar, br, cr;       // rep line (fp32)
-    float R, hsure;         // strip half-width, sure-in-C' distance
-    float pbx, pby, dirx, diry, len, spacing;  // fp32 segment geometry
-    double pax, pay, pbx64, pby64;
-    int K;
-    float invK, dxf, dyf;   // fp32 sample interpolation
-    float slack;            // subcell boundary slack for the fp32 fast path
-    double Wd, Hd;          // target image size
-};
-
-// Exact subcell of sample k of the rep line (guided.py:173-187 + cell_indices)
-__device__ __forceinline__ void sample_subcell(const GroupCtx& G, double D, float invD, int k,
-                                               int& u, int& v) {
+// Exact subcell of sample k of the rep line (guided.py:173-187 + cell_indices):
+// fp32 interpolation, exact fp64 evaluation only near a subcell boundary.
+__device__ __forceinline__ void sample_subcell(const GroupRec& G, double D, int k, int& u, int& v) {
     const float t = (float)k * G.invK;
     const float sx = fmaf(t, G.dxf, G.pbx), sy = fmaf(t, G.dyf, G.pby);
-    const float qx = sx * invD, qy = sy * invD;
+    const float qx = sx * G.invD, qy = sy * G.invD;
     const float fx = floorf(qx), fy = floorf(qy);
     const float rx = qx - fx, ry = qy - fy;
     if (rx > G.slack && rx < 1.0f - G.slack && ry > G.slack && ry < 1.0f - G.slack) {
@@ -626,79 +667,97 @@ __device__ __forceinline__ void sample_subcell(const GroupCtx& G, double D, floa
 }
 
 // f in C'(rep) <=> some sample subcell is within Chebyshev distance 1 of f's.
-__device__ bool in_cprime_exact(const GroupCtx& G, double D, float invD, float fx, float fy,
-                                int fu, int fv) {
+__device__ bool in_cprime_exact(const GroupRec& G, double D, float fx, float fy, int fu, int fv) {
     if (G.K < 0) return false;
     const float tau = (fx - G.pbx) * G.dirx + (fy - G.pby) * G.diry;
     const float reach = 2.0f * 1.41421356f * (float)D + 1.0f;
-    int klo = (int)floorf((tau - reach) / G.spacing) - 1;
-    int khi = (int)ceilf((tau + reach) / G.spacing) + 1;
+    const float inv_sp = 1.0f / G.spacing;
+    int klo = (int)floorf((tau - reach) * inv_sp) - 1;
+    int khi = (int)ceilf((tau + reach) * inv_sp) + 1;
     if (klo < 0) klo = 0;
     if (khi > G.K) khi = G.K;
     for (int k = klo; k <= khi; k++) {
         int u, v;
-        sample_subcell(G, D, invD, k, u, v);
+        sample_subcell(G, D, k, u, v);
         if (abs(u - fu) <= 1 && abs(v - fv) <= 1) return true;
     }
     return false;
 }
 
 struct WarpSmem {
-    unsigned short list[CAP];
-    unsigned valid[CAP / 32];
-    unsigned anyb[CAP / 8];
+    unsigned short list[CAP];    // candidate feature ids (target-local)
+    unsigned short ulist[CAP];   // positions whose C' membership is not yet decided
+    unsigned valid[CAP / 32];    // candidate in C'
+    unsigned anyb[CAP / 8];      // stats: candidate inside some member band
+    GroupRec grec;               // this warp's group context (broadcast reads)
 };
 
-__device__ __forceinline__ bool band_exact(const double* ml, bool gemv, double x, double y,
-                                           double d) {
-    double v = gemv ? fma(ml[0], x, ml[1] * y) : fma(ml[1], y, ml[0] * x);
-    v = v + ml[2];
+// the reference's float64 band value for one (member, target) element, guided.py:447
+__device__ __forceinline__ bool band_exact(double A, double B, double C, bool gemv, double x,
+                                           double y, double d) {
+    double v = gemv ? fma(A, x, B * y) : fma(B, y, A * x);
+    v = v + C;
     return fabs(v) <= d;
 }
 
+__device__ __forceinline__ bool member_band(const ChunkArgs& a, const GroupRec& G,
+                                            const MemberRec& M, float x, float y) {
+    const float v = fabsf(fmaf(M.a, x, fmaf(M.b, y, M.c)));
+    if (v <= M.lo) return true;
+    if (v > M.hi) return false;
+    if (G.cnt == 1) return band_exact(G.sl0, G.sl1, G.sl2, true, x, y, a.d);
+    const double* L = a.q_line + 3 * (int64_t)M.slot;
+    return band_exact(L[0], L[1], L[2], false, x, y, a.d);
+}
+
 template <bool STATS>
-__device__ void process_round(const ChunkArgs& a, const GroupCtx& G, WarpSmem& S, int n,
-                              const int4& grp, int64_t toff, int64_t qoff, int64_t qlbase,
-                              const double* singleton_line, bool first_round,
-                              int& cols_total) {
+__device__ void process_round(const ChunkArgs& a, const GroupRec& G, WarpSmem& S, int n,
+                              int64_t toff, int64_t qoff, bool first_round, int& cols_total) {
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const double D = a.D;
-    const float invD = (float)(1.0 / D);
-    // ---- exact C' membership for candidates outside the sure zone
-    for (int j = lane; j < ((n + 31) & ~31); j += 32) {
-        bool need = false;
-        int f = 0;
-        if (j < n) {
-            need = !((S.valid[j >> 5] >> (j & 31)) & 1u);
-            f = S.list[j];
-        }
-        bool ok = false;
-        if (need) {
+    const int m = G.cnt;
+    const MemberRec* MR = a.mrec + G.moff;
+    // ---- C' membership of the candidates outside the sure zone that some member
+    //      band actually contains (compacted so every lane does useful work)
+    int nu = 0;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+        const int j = j0 + lane;
+        const bool need = j < n && !((S.valid[j >> 5] >> (j & 31)) & 1u);
+        const unsigned bal = __ballot_sync(FULL, need);
+        if (need) S.ulist[nu + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)j;
+        nu += __popc(bal);
+    }
+    __syncwarp();
+    for (int u0 = 0; u0 < nu; u0 += 32) {
+        const int uj = u0 + lane;
+        if (uj < nu) {
+            const int j = S.ulist[uj];
+            const int f = S.list[j];
             const float2 p2 = a.xy[toff + f];
-            const int su = a.sub[toff + f];
-            const int fu = (short)(su & 0xffff), fv = su >> 16;
-            ok = in_cprime_exact(G, D, invD, p2.x, p2.y, fu, fv);
+            bool any = false;
+            for (int k = 0; k < m && !any; k++) any = member_band(a, G, MR[k], p2.x, p2.y);
+            if (any) {
+                const int su = a.sub[toff + f];
+                if (in_cprime_exact(G, D, p2.x, p2.y, (short)(su & 0xffff), su >> 16))
+                    atomicOr(&S.valid[j >> 5], 1u << (j & 31));
+            }
         }
-        unsigned bal = __ballot_sync(FULL, ok);
-        if (lane == 0) S.valid[j >> 5] |= bal;
     }
     if (STATS) {
         for (int w = lane; w < CAP / 8; w += 32) S.anyb[w] = 0;
     }
     __syncwarp();
-    const int m = grp.y;
     const bool gemv_band = (m == 1);
     const int ntiles = (n + 15) >> 4;
     for (int mt0 = 0; mt0 < m; mt0 += 8) {
-        // B fragment: member mt0+g, bytes [32t, 32t+32)
+        // B fragment: member mt0+g, bytes [32t, 32t+32) (K permuted consistently with A)
         unsigned bw[8];
         {
             const int j = mt0 + g;
             if (j < m) {
-                const int slot = a.members[grp.z + j];
-                const int fid = a.qlist[qlbase + slot];
+                const int fid = MR[j].fid;
                 const uint4* row = reinterpret_cast<const uint4*>(a.desc + (qoff + fid) * 128) + 2 * t;
-                uint4 v0 = __ldg(row), v1 = __ldg(row + 1);
+                const uint4 v0 = __ldg(row), v1 = __ldg(row + 1);
                 bw[0] = v0.x; bw[1] = v0.y; bw[2] = v0.z; bw[3] = v0.w;
                 bw[4] = v1.x; bw[5] = v1.y; bw[6] = v1.z; bw[7] = v1.w;
             } else {
@@ -709,29 +768,19 @@ __device__ void process_round(const ChunkArgs& a, const GroupCtx& G, WarpSmem& S
         // epilogue columns 2t, 2t+1
         float la[2], lb[2], lc[2], lo[2], hi[2];
         unsigned qn9[2];
-        const double* mline[2];
         int mslot[2];
 #pragma unroll
         for (int c = 0; c < 2; c++) {
             const int j = mt0 + 2 * t + c;
             if (j < m) {
-                const int slot = a.members[grp.z + j];
-                mslot[c] = slot;
-                const double* L = (m == 1) ? singleton_line : a.q_line + 3 * (int64_t)slot;
-                mline[c] = L;
-                const double A = L[0], B = L[1], C = L[2];
-                la[c] = (float)A; lb[c] = (float)B; lc[c] = (float)C;
-                const int fid = a.qlist[qlbase + slot];
-                qn9[c] = (unsigned)a.norm2[qoff + fid] << 9;
-                const float eps = (float)((fabs(A) * G.Wd + fabs(B) * G.Hd + fabs(C)) * 0x1p-20) + 1e-6f;
-                lo[c] = (float)a.d - eps;
-                hi[c] = (float)a.d + eps;
+                const MemberRec M = MR[j];
+                la[c] = M.a; lb[c] = M.b; lc[c] = M.c; lo[c] = M.lo; hi[c] = M.hi;
+                qn9[c] = M.qn9;
+                mslot[c] = M.slot;
             } else {
-                mslot[c] = -1;
-                mline[c] = nullptr;
-                la[c] = 0.f; lb[c] = 0.f; lc[c] = 1e30f;
-                lo[c] = -1.f; hi[c] = -1.f;
+                la[c] = 0.f; lb[c] = 0.f; lc[c] = 1e30f; lo[c] = -1.f; hi[c] = -1.f;
                 qn9[c] = 0;
+                mslot[c] = -1;
             }
         }
         unsigned b1[2] = {NONE, NONE}, b2[2] = {NONE, NONE};
@@ -759,11 +808,11 @@ __device__ void process_round(const ChunkArgs& a, const GroupCtx& G, WarpSmem& S
             for (int e = 0; e < 4; e++) {
                 const int c = e & 1;
                 const float2 P = (e < 2) ? p0 : p1;
-                const float v = fmaf(la[c], P.x, fmaf(lb[c], P.y, lc[c]));
-                const float av = fabsf(v);
+                const float av = fabsf(fmaf(la[c], P.x, fmaf(lb[c], P.y, lc[c])));
                 bool in = av <= lo[c];
                 if (!in && av <= hi[c]) {
-                    in = band_exact(mline[c], gemv_band, (double)P.x, (double)P.y, a.d);
+                    const double* L = gemv_band ? &G.sl0 : a.q_line + 3 * (int64_t)mslot[c];
+                    in = band_exact(L[0], L[1], L[2], gemv_band, (double)P.x, (double)P.y, a.d);
                 }
                 inb[e] = in;
                 const unsigned base = ((e < 2) ? tb0 : tb1) + qn9[c];
@@ -807,10 +856,10 @@ __device__ void process_round(const ChunkArgs& a, const GroupCtx& G, WarpSmem& S
                     const unsigned long long ob = a.mstate[mslot[c]];
                     const unsigned os = a.mstate2[mslot[c]];
                     const unsigned bd = (unsigned)(best >> 32), od = (unsigned)(ob >> 32);
-                    const unsigned nb = min(bd, od), nh = max(bd, od);
+                    const unsigned nh = max(bd, od);
                     const unsigned long long nbest = (bd < od) ? best : ob;
                     sec = min(nh, min(sec, os));
-                    best = (nb == NONE) ? ~0ull : nbest;
+                    best = nbest;
                 }
                 a.mstate[mslot[c]] = best;
                 a.mstate2[mslot[c]] = sec;
@@ -820,7 +869,7 @@ __device__ void process_round(const ChunkArgs& a, const GroupCtx& G, WarpSmem& S
     if (STATS) {
         __syncwarp();
         int cnt = 0;
-        for (int w = lane; w < ((ntiles * 2 + 31) & ~31); w += 32) cnt += w < ntiles * 2 ? __popc(S.anyb[w]) : 0;
+        for (int w = lane; w < ntiles * 2; w += 32) cnt += __popc(S.anyb[w]);
 #pragma unroll
         for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
         cols_total += cnt;
@@ -829,82 +878,50 @@ __device__ void process_round(const ChunkArgs& a, const GroupCtx& G, WarpSmem& S
 }
 
 template <bool STATS>
-__global__ void __launch_bounds__(WARPS * 32) match_kernel(ChunkArgs a) {
+__global__ void __launch_bounds__(WARPS * 32, 3) match_kernel(ChunkArgs a) {
     __shared__ WarpSmem smem[WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpSmem& S = smem[warp];
     const int total = a.gstart[a.npairs];
-    const double D = a.D;
+    const float Df = (float)a.D;
     for (int gid = blockIdx.x * WARPS + warp; gid < total; gid += gridDim.x * WARPS) {
-        const int p = find_pair(a.gstart, a.npairs, gid);
-        const int pg = a.p0 + p;
-        const int64_t q0 = a.qlist_off[pg];
-        const int64_t s0 = q0 - a.qbase;
-        const int4 grp = a.grec[s0 + (gid - a.gstart[p])];
-        const GroupPrep P = a.prep[gid];
-        if (P.K < 0) continue;   // line misses the padded image: empty C'
+        {
+            static_assert(sizeof(GroupRec) % 16 == 0, "GroupRec must be 16-byte granular");
+            const uint4* src = reinterpret_cast<const uint4*>(a.grp + gid);
+            uint4* dst = reinterpret_cast<uint4*>(&S.grec);
+            if (lane < (int)(sizeof(GroupRec) / 16)) dst[lane] = __ldg(src + lane);
+            __syncwarp();
+        }
+        const GroupRec& G = S.grec;
+        if (G.K < 0) { __syncwarp(); continue; }   // rep line misses the padded image: C' is empty
+        const int pg = a.p0 + G.p;
         const int ti = a.pair_t[pg], qi = a.pair_q[pg];
         const int64_t toff = a.img_off[ti], qoff = a.img_off[qi];
-        const int W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1];
-        const double* rl = a.q_line + 3 * (s0 + grp.x);
-        GroupCtx G;
-        G.ar = (float)rl[0]; G.br = (float)rl[1]; G.cr = (float)rl[2];
-        G.R = P.R;
-        {
-            const double hs2 = D * D - 0.25 * a.d * a.d;
-            G.hsure = hs2 > 0 ? (float)(sqrt(hs2) - 0.075) : -1.0f;
-        }
-        G.pax = P.pax; G.pay = P.pay; G.pbx64 = P.pbx; G.pby64 = P.pby;
-        G.pbx = (float)P.pbx; G.pby = (float)P.pby;
-        G.dxf = (float)(P.pax - P.pbx); G.dyf = (float)(P.pay - P.pby);
-        G.len = (float)P.len;
-        G.dirx = P.len > 0 ? (float)((P.pax - P.pbx) / P.len) : 0.f;
-        G.diry = P.len > 0 ? (float)((P.pay - P.pby) / P.len) : 0.f;
-        G.K = P.K;
-        G.invK = 1.0f / (float)P.K;
-        G.spacing = fmaxf((float)(P.len / P.K), 1e-6f);
-        G.slack = (float)(4e-6 * ((double)W + (double)H + 4.0 * a.d) / D) + 1e-4f;
-        G.Wd = (double)W; G.Hd = (double)H;
-        const double singleton[3] = {P.sl0, P.sl1, P.sl2};
-
-        // ---- strip enumeration: rows of buckets along the minor direction
-        const bool horiz = fabsf(G.br) >= fabsf(G.ar);
-        const float alpha = horiz ? G.ar : G.br, beta = horiz ? G.br : G.ar;
-        const float Pmax = horiz ? (float)W : (float)H, Qmax = horiz ? (float)H : (float)W;
-        const int nbx = a.dims[2 * ti], nby = a.dims[2 * ti + 1];
-        const int nalong = horiz ? nbx : nby, nrows = horiz ? nby : nbx;
-        const int64_t toffb = horiz ? a.roff[ti] : a.coff[ti];
-        const int32_t* start = horiz ? a.rstart : a.cstart;
-        const int32_t* mem = horiz ? a.rmem : a.cmem;
-        const float Df = (float)D;
-        float qlo, qhi;
-        {
-            const float q00 = (-G.R - G.cr) / beta, q01 = (G.R - G.cr) / beta;
-            const float q10 = (-G.R - G.cr - alpha * Pmax) / beta, q11 = (G.R - G.cr - alpha * Pmax) / beta;
-            qlo = fminf(fminf(q00, q01), fminf(q10, q11));
-            qhi = fmaxf(fmaxf(q00, q01), fmaxf(q10, q11));
-        }
-        int rlo = (int)floorf((fmaxf(qlo, 0.f) - 0.01f) / Df), rhi = (int)floorf((fminf(qhi, Qmax) + 0.01f) / Df);
-        rlo = max(rlo, 0);
-        rhi = min(rhi, nrows - 1);
+        const int nalong = G.horiz ? a.dims[2 * ti] : a.dims[2 * ti + 1];
+        const int64_t toffb = G.horiz ? a.roff[ti] : a.coff[ti];
+        const int32_t* start = G.horiz ? a.rstart : a.cstart;
+        const int32_t* mem = G.horiz ? a.rmem : a.cmem;
         int n = 0;
         bool first_round = true;
         int cols_total = 0;
         if (lane < CAP / 32) S.valid[lane] = 0;
         __syncwarp();
-        for (int r0 = rlo; r0 <= rhi; r0 += 32) {
+        // ---- strip gather: bucket rows of the strip |dist_rep| <= R, filtered
+        for (int r0 = G.rlo; r0 <= G.rhi; r0 += 32) {
             const int r = r0 + lane;
             int bs = 0, len = 0;
-            if (r <= rhi) {
+            if (r <= G.rhi) {
                 int blo = 0, bhi = nalong - 1;
-                if (fabsf(alpha) > 1e-6f) {
+                if (G.inv_alpha != 0.f) {
                     const float y0 = r * Df - 0.01f, y1 = (r + 1) * Df + 0.01f;
-                    const float e00 = (-G.R - beta * y0 - G.cr) / alpha, e01 = (G.R - beta * y0 - G.cr) / alpha;
-                    const float e10 = (-G.R - beta * y1 - G.cr) / alpha, e11 = (G.R - beta * y1 - G.cr) / alpha;
+                    const float e00 = (-G.R - G.beta * y0 - G.cr) * G.inv_alpha;
+                    const float e01 = (G.R - G.beta * y0 - G.cr) * G.inv_alpha;
+                    const float e10 = (-G.R - G.beta * y1 - G.cr) * G.inv_alpha;
+                    const float e11 = (G.R - G.beta * y1 - G.cr) * G.inv_alpha;
                     const float plo = fminf(fminf(e00, e01), fminf(e10, e11));
                     const float phi = fmaxf(fmaxf(e00, e01), fmaxf(e10, e11));
-                    blo = max(blo, (int)floorf(fmaxf(plo - 0.01f, -1.f) / Df));
-                    bhi = min(bhi, (int)floorf(fminf(phi + 0.01f, Pmax + 1.f) / Df));
+                    blo = max(blo, (int)floorf(fmaxf(plo - 0.02f, -1.f) * G.invD));
+                    bhi = min(bhi, (int)floorf(fminf(phi + 0.02f, G.Pmax + 1.f) * G.invD));
                 }
                 if (blo <= bhi) {
                     const int64_t cb = toffb + (int64_t)r * nalong;
@@ -934,8 +951,7 @@ __global__ void __launch_bounds__(WARPS * 32) match_kernel(ChunkArgs a) {
                 if (j < tot) {
                     f = mem[ob + (j - oex)];
                     const float2 p2 = a.xy[toff + f];
-                    const float dr = fmaf(G.ar, p2.x, fmaf(G.br, p2.y, G.cr));
-                    const float adr = fabsf(dr);
+                    const float adr = fabsf(fmaf(G.ar, p2.x, fmaf(G.br, p2.y, G.cr)));
                     pass = adr <= G.R;
                     const float tau = (p2.x - G.pbx) * G.dirx + (p2.y - G.pby) * G.diry;
                     sure = adr <= G.hsure && tau >= 0.05f && tau <= G.len - 0.05f;
@@ -944,7 +960,7 @@ __global__ void __launch_bounds__(WARPS * 32) match_kernel(ChunkArgs a) {
                 const int cnt = __popc(bal);
                 if (n + cnt > CAP) {
                     __syncwarp();
-                    process_round<STATS>(a, G, S, n, grp, toff, qoff, q0 - s0, singleton, first_round, cols_total);
+                    process_round<STATS>(a, G, S, n, toff, qoff, first_round, cols_total);
                     first_round = false;
                     n = 0;
                     if (lane < CAP / 32) S.valid[lane] = 0;
@@ -965,44 +981,45 @@ __global__ void __launch_bounds__(WARPS * 32) match_kernel(ChunkArgs a) {
         }
         if (n > 0) {
             __syncwarp();
-            process_round<STATS>(a, G, S, n, grp, toff, qoff, q0 - s0, singleton, first_round, cols_total);
+            process_round<STATS>(a, G, S, n, toff, qoff, first_round, cols_total);
             first_round = false;
         }
         __syncwarp();
         // ---- ratio test + dedupe per member (ratio_filter / _dedupe_targets)
         if (!first_round) {
-            for (int j = lane; j < grp.y; j += 32) {
-                const int slot = a.members[grp.z + j];
+            for (int j = lane; j < G.cnt; j += 32) {
+                const MemberRec& M = a.mrec[G.moff + j];
+                const int slot = M.slot;
                 const unsigned long long best = a.mstate[slot];
                 const unsigned sec = a.mstate2[slot];
                 if (best == ~0ull) continue;
                 const unsigned bd2 = (unsigned)(best >> 32);
                 const int tid = (int)(best & 0xffffffffu);
                 const float db = sqrtf((float)bd2);
-                float r;
+                float rr;
                 bool acc;
                 if (sec == NONE) {
                     acc = db < a.single_cap;
-                    r = 0.0f;
+                    rr = 0.0f;
                 } else {
                     const float ds = sqrtf((float)sec);
-                    r = ds > 0.0f ? db / ds : 1.0f;
-                    acc = r < a.ratio;
+                    rr = ds > 0.0f ? db / ds : 1.0f;
+                    acc = rr < a.ratio;
                 }
                 if (!acc) continue;
-                const int qid = a.qlist[q0 - s0 + slot];
                 a.res_tid[slot] = tid;
                 a.res_dist[slot] = db;
-                a.res_ratio[slot] = r;
+                a.res_ratio[slot] = rr;
                 const unsigned long long key =
-                    ((unsigned long long)__float_as_uint(db) << 32) | (unsigned)qid;
-                atomicMin(&a.dedupe[a.tbase[p] + tid], key);
+                    ((unsigned long long)__float_as_uint(db) << 32) | (unsigned)M.fid;
+                atomicMin(&a.dedupe[a.tbase[G.p] + tid], key);
             }
         }
         if (STATS && lane == 0 && cols_total > 0) {
-            atomicAdd(&a.stats[2 * pg], (unsigned long long)grp.y);
-            atomicAdd(&a.stats[2 * pg + 1], (unsigned long long)grp.y * (unsigned long long)cols_total);
+            atomicAdd(&a.stats[2 * pg], (unsigned long long)G.cnt);
+            atomicAdd(&a.stats[2 * pg + 1], (unsigned long long)G.cnt * (unsigned long long)cols_total);
         }
+        __syncwarp();
     }
 }
 
@@ -1058,7 +1075,8 @@ size_t chunk_bytes(const ChunkSizes& c) {
     b += aligned_bytes<double>(3 * c.Q);               // q_line
     b += aligned_bytes<int4>(c.Q);                     // grec
     b += aligned_bytes<int32_t>(c.Q) * 2;              // gfill, members
-    b += aligned_bytes<GroupPrep>(c.Q);                // prep
+    b += aligned_bytes<GroupRec>(c.Q);                 // grp
+    b += aligned_bytes<MemberRec>(c.Q);                // mrec
     b += aligned_bytes<unsigned long long>(c.Q);       // mstate
     b += aligned_bytes<unsigned>(c.Q);                 // mstate2
     b += aligned_bytes<int32_t>(c.Q) * 3;              // res_tid/dist/ratio
@@ -1079,6 +1097,7 @@ extern "C" int msfm_feature_norms(const uint8_t* d_desc, int64_t n, int32_t* d_n
     if (n == 0) return MSFM_OK;
     norms_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(d_desc, n, d_norm2);
     MSFM_LAUNCH_CHECK();
+    count_launches(1);
     return MSFM_OK;
 }
 
@@ -1124,12 +1143,14 @@ extern "C" int msfm_grid_build(const msfm_bank* bank, const int32_t* d_dims, con
                     d_rmem, d_cmem, D};
     grid_count_kernel<<<bank->n_images, 256, 0, st>>>(a);
     MSFM_LAUNCH_CHECK();
+    count_launches(1);
     int rc = exclusive_scan(d_rstart, n_buckets_total + 1, rcur, bsum, st);
     if (rc) return rc;
     rc = exclusive_scan(d_cstart, n_buckets_total + 1, ccur, bsum, st);
     if (rc) return rc;
     grid_scatter_kernel<<<bank->n_images, 256, 0, st>>>(a);
     MSFM_LAUNCH_CHECK();
+    count_launches(1);
     return MSFM_OK;
 }
 
@@ -1220,7 +1241,8 @@ extern "C" int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids,
     a.q_tab = ar.take<int32_t>(w.Q); a.q_line = ar.take<double>(3 * w.Q);
     a.grec = ar.take<int4>(w.Q);
     a.gfill = ar.take<int32_t>(w.Q); a.members = ar.take<int32_t>(w.Q);
-    a.prep = ar.take<GroupPrep>(w.Q);
+    a.grp = ar.take<GroupRec>(w.Q);
+    a.mrec = ar.take<MemberRec>(w.Q);
     a.mstate = ar.take<unsigned long long>(w.Q); a.mstate2 = ar.take<unsigned>(w.Q);
     a.res_tid = ar.take<int32_t>(w.Q); a.res_dist = ar.take<float>(w.Q); a.res_ratio = ar.take<float>(w.Q);
     a.dedupe = ar.take<unsigned long long>(w.NT);
@@ -1242,10 +1264,14 @@ extern "C" int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids,
         gscan_kernel<<<1, SCAN_T, 0, st>>>(a);
         scatter_kernel<<<a.npairs, 256, 0, st>>>(a);
         if (Q > 0) prep_kernel<<<(unsigned)((Q + 127) / 128), 128, 0, st>>>(a, (int)Q);
-        if (d_stats) match_kernel<true><<<nsm * 4, WARPS * 32, 0, st>>>(a);
-        else         match_kernel<false><<<nsm * 4, WARPS * 32, 0, st>>>(a);
+        {
+            ProfScope ps("match_kernel", st);
+            if (d_stats) match_kernel<true><<<nsm * 3, WARPS * 32, 0, st>>>(a);
+            else         match_kernel<false><<<nsm * 3, WARPS * 32, 0, st>>>(a);
+        }
         compact_kernel<<<a.npairs, 256, 0, st>>>(a);
         MSFM_LAUNCH_CHECK();
+        count_launches(7 + (Q > 0 ? 1 : 0));
     }
     return MSFM_OK;
 }
