@@ -146,6 +146,17 @@ int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids, int32_t n_
                       int32_t* d_out_count, int64_t* d_stats,
                       void* d_workspace, size_t workspace_bytes, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Host-only: RANSAC hypothesis sets.  Emits `count` consecutive draws of
+ * numpy's `rng.choice(n, size=sample_size, replace=False)` starting from the
+ * PCG64 state of a numpy Generator (state hi/lo, inc hi/lo, has_uint32,
+ * uinteger = rng.bit_generator.state), exactly as pnp_ransac consumes them
+ * (reconstruct.py:185-194).  out: [count][sample_size] int32.
+ * ---------------------------------------------------------------------- */
+int msfm_ransac_samples(const uint64_t state_inc[4], int32_t has_uint32, uint32_t uinteger,
+                        int64_t n, int32_t sample_size, int32_t count, int32_t* out,
+                        uint64_t state_out[4]);
+
 #ifdef __cplusplus
 }
 #endif

@@ -48,6 +48,8 @@ _SIGS = {
     "msfm_grid_build": (ctypes.c_int, [ctypes.POINTER(Bank), VP, VP, VP, ctypes.c_int64,
                                        ctypes.c_int64, ctypes.c_double, VP, VP, VP, VP, VP,
                                        VP, ctypes.c_size_t, VP]),
+    "msfm_ransac_samples": (ctypes.c_int, [VP, ctypes.c_int32, ctypes.c_uint32, ctypes.c_int64,
+                                           ctypes.c_int32, ctypes.c_int32, VP, VP]),
     "msfm_guided_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int32, VP,
                                                       ctypes.POINTER(MatchParams)]),
     "msfm_guided_match": (ctypes.c_int, [ctypes.POINTER(Bank), ctypes.POINTER(Grids),

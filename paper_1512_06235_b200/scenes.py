@@ -51,11 +51,13 @@ def tier_counts(sets: dict, eta: float = 20.0) -> dict:
     return out
 
 
-def coarse_snapshot(scene, registered, eta: float = 20.0) -> Snapshot:
+def coarse_snapshot(scene, registered, eta: float | None = 20.0) -> Snapshot:
+    """GT points restricted to the registered cameras' refs (and to each image's
+    coarse tier when eta is given), >= 2 refs, ids in ascending GT order."""
     registered = np.array(sorted(int(i) for i in registered), dtype=np.int64)
     reg_mask = np.zeros(len(scene.cameras), dtype=bool)
     reg_mask[registered] = True
-    tiers = tier_counts(scene.feature_sets, eta)
+    tiers = tier_counts(scene.feature_sets, eta if eta is not None else 100.0)
     n_pts = len(scene.points)
     # observation table of every (image, fid) that sees a world point
     obs_img, obs_fid, obs_pid = [], [], []
@@ -67,7 +69,8 @@ def coarse_snapshot(scene, registered, eta: float = 20.0) -> Snapshot:
     obs_pid = np.concatenate(obs_pid)
     # triangulable = seen in >= 2 images (GT model membership, synth.py:86-116)
     seen = np.bincount(obs_pid, minlength=n_pts)
-    tier_arr = np.array([tiers[i] for i in range(len(scene.cameras))], dtype=np.int64)
+    tier_arr = np.array([tiers[i] if eta is not None else 1 << 40
+                         for i in range(len(scene.cameras))], dtype=np.int64)
     tier_of = tier_arr[obs_img]
     keep = reg_mask[obs_img] & (obs_fid < tier_of) & (seen[obs_pid] >= 2)
     k_img, k_fid, k_pid = obs_img[keep], obs_fid[keep], obs_pid[keep]
@@ -196,3 +199,16 @@ def build(config: str, n_cameras: int | None = None):
     scene = generate_scene(spec)
     snap = coarse_snapshot(scene, registered_for(config, spec.n_cameras))
     return scene, snap
+
+
+def track_sums(scene, snap: Snapshot):
+    """Per point: S = sum of track descriptors (int32, <= 255*n) and n = track
+    length — the exact form of mean_descriptor (localize.py:51-59)."""
+    M = len(snap.point_xyz)
+    S = np.zeros((M, 128), dtype=np.int64)
+    pid = np.repeat(np.arange(M), np.diff(snap.track_ptr))
+    for i in np.unique(snap.track_img):
+        sel = np.flatnonzero(snap.track_img == i)
+        np.add.at(S, pid[sel], scene.feature_sets[int(i)].descriptors[snap.track_fid[sel]].astype(np.int64))
+    n = np.diff(snap.track_ptr).astype(np.int32)
+    return S.astype(np.int32), n

@@ -40,3 +40,19 @@ def load(name):
 
 
 GUIDED_FIXTURES = sorted(f for f in os.listdir(GOLDEN) if f.startswith("guided_") and f.endswith(".npz"))
+
+
+def load_localize(name):
+    """(spec kw, scene, snapshot, npz) of a localization fixture."""
+    from paper_1512_06235_b200 import scenes
+
+    z = np.load(os.path.join(GOLDEN, name), allow_pickle=False)
+    kw = ast.literal_eval(str(z["spec"]))
+    key = repr(sorted(kw.items()))
+    if key not in _SCENES:
+        _SCENES[key] = generate_scene(SceneSpec(**kw))
+    scene = _SCENES[key]
+    eta = float(z["eta"])
+    snap = scenes.coarse_snapshot(scene, [int(i) for i in z["registered"]],
+                                  eta=None if eta < 0 else eta)
+    return kw, scene, snap, z

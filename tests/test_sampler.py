@@ -1,0 +1,30 @@
+"""The native hypothesis generator reproduces numpy's Generator.choice stream."""
+
+import numpy as np
+import pytest
+
+from paper_1512_06235_b200.sampling import ransac_samples
+
+
+@pytest.mark.parametrize("seed,n", [(0, 6), (1, 7), (5, 40), (17, 1500), (123, 6000), (99, 9999),
+                                    (7, 10000), (3, 65535), (11, 2**20)])
+def test_matches_numpy_choice(seed, n):
+    if n > 10000:
+        pytest.skip("tail-shuffle branch not needed for pnp populations")
+    count = 300
+    rng = np.random.default_rng(seed)
+    ref = np.stack([rng.choice(n, size=6, replace=False) for _ in range(count)])
+    np.testing.assert_array_equal(ransac_samples(seed, n, count), ref)
+
+
+def test_many_seeds_small_populations():
+    for seed in range(200):
+        n = 6 + seed * 37 % 3000
+        rng = np.random.default_rng(seed)
+        ref = np.stack([rng.choice(n, size=6, replace=False) for _ in range(20)])
+        np.testing.assert_array_equal(ransac_samples(seed, n, 20), ref)
+
+
+def test_rejects_bad_population():
+    with pytest.raises(ValueError):
+        ransac_samples(0, 5, 3)
