@@ -60,6 +60,7 @@ typedef struct {
     const int32_t* d_img_n;
     const int32_t* d_img_wh;
     int32_t n_images;
+    int64_t n_total;          /* total features (rows of d_xy / d_desc) */
 } msfm_bank;
 
 /* |desc|^2 per feature (exact int32). */
@@ -156,6 +157,39 @@ int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids, int32_t n_
 int msfm_ransac_samples(const uint64_t state_inc[4], int32_t has_uint32, uint32_t uinteger,
                         int64_t n, int32_t sample_size, int32_t count, int32_t* out,
                         uint64_t state_out[4]);
+
+/* ------------------------------------------------------------------------
+ * 3D-2D localization kNN (DescriptorIndex.knn2 exact path, descriptors.py:35-72,
+ * for the mean-descriptor queries of direct_3d2d_search, localize.py:99-122).
+ * Points are given exactly: S [n_points][128] int32 track-descriptor sums and
+ * n [n_points] track lengths (mean = S/n, localize.py:51-59).  For every query
+ * image d_images[s] (bank image index) and point p the result is the top-2 of
+ *     key = n_p |f|^2 - 2 S_p.f     (N = |S - n f|^2 = n_p*key + |S_p|^2)
+ * over the image's features, lowest feature index winning ties:
+ *     k1[s][p], i1[s][p] (image-local feature id, -1 if none), k2[s][p]
+ * (INT32_MAX when the image has < 2 features).  Row stride = n_points rounded
+ * up to 128.  S.f runs on tcgen05 kind::i8 (two u8 digit planes of S).
+ * Requires max track length <= 100 (int32 keys).
+ * ---------------------------------------------------------------------- */
+size_t msfm_knn_workspace_bytes(int32_t n_points);
+int msfm_knn2_tracks(const msfm_bank* bank, int32_t n_points, const int32_t* d_S,
+                     const int32_t* d_n, int32_t n_images, const int32_t* d_images,
+                     int32_t max_track, int32_t* d_k1, int32_t* d_i1, int32_t* d_k2,
+                     void* d_workspace, size_t workspace_bytes, void* stream);
+
+/* direct_3d2d_search post-processing (localize.py:108-122 + ratio_filter
+ * matching.py:82-103) on the knn2 output: ratio test sqrt(N_b/N_s) < p/q
+ * evaluated exactly (q^2 N_b < p^2 N_s), single-feature images: sqrt(N_b)/n <
+ * single_cap; then one point per feature (smallest exact distance N/n^2, lower
+ * point row wins ties).  Output per image slot s: rows d_corr_row[s*stride ..]
+ * (ascending point row) and d_corr_fid, count d_corr_n[s].  d_win is scratch of
+ * sum over query images of their feature counts (int32), offsets d_win_off[s]. */
+int msfm_direct_3d2d(const msfm_bank* bank, int32_t n_points, const int32_t* d_n,
+                     const int64_t* d_SS, int32_t n_images, const int32_t* d_images,
+                     const int32_t* d_k1, const int32_t* d_i1, const int32_t* d_k2,
+                     int64_t ratio_p, int64_t ratio_q, double single_cap,
+                     int32_t* d_win, const int64_t* d_win_off, int32_t* d_corr_row,
+                     int32_t* d_corr_fid, int32_t* d_corr_n, void* stream);
 
 #ifdef __cplusplus
 }

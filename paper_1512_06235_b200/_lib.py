@@ -20,7 +20,8 @@ VP = ctypes.c_void_p
 
 class Bank(ctypes.Structure):
     _fields_ = [("d_xy", VP), ("d_desc", VP), ("d_norm2", VP), ("d_img_off", VP),
-                ("d_img_n", VP), ("d_img_wh", VP), ("n_images", ctypes.c_int32)]
+                ("d_img_n", VP), ("d_img_wh", VP), ("n_images", ctypes.c_int32),
+                ("n_total", ctypes.c_int64)]
 
 
 class Grids(ctypes.Structure):
@@ -50,6 +51,12 @@ _SIGS = {
                                        VP, ctypes.c_size_t, VP]),
     "msfm_ransac_samples": (ctypes.c_int, [VP, ctypes.c_int32, ctypes.c_uint32, ctypes.c_int64,
                                            ctypes.c_int32, ctypes.c_int32, VP, VP]),
+    "msfm_knn_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int32]),
+    "msfm_knn2_tracks": (ctypes.c_int, [ctypes.POINTER(Bank), ctypes.c_int32, VP, VP, ctypes.c_int32,
+                                        VP, ctypes.c_int32, VP, VP, VP, VP, ctypes.c_size_t, VP]),
+    "msfm_direct_3d2d": (ctypes.c_int, [ctypes.POINTER(Bank), ctypes.c_int32, VP, VP, ctypes.c_int32,
+                                        VP, VP, VP, VP, ctypes.c_int64, ctypes.c_int64,
+                                        ctypes.c_double, VP, VP, VP, VP, VP, VP]),
     "msfm_guided_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int32, VP,
                                                       ctypes.POINTER(MatchParams)]),
     "msfm_guided_match": (ctypes.c_int, [ctypes.POINTER(Bank), ctypes.POINTER(Grids),

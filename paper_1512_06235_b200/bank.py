@@ -85,7 +85,7 @@ class FeatureBank:
     def cstruct(self) -> _lib.Bank:
         return _lib.Bank(_lib.ptr(self.xy), _lib.ptr(self.desc), _lib.ptr(self.norm2),
                          _lib.ptr(self.img_off), _lib.ptr(self.img_n), _lib.ptr(self.img_wh),
-                         len(self.image_ids))
+                         len(self.image_ids), self.n_total)
 
     def grid(self, D: float, stream=None) -> "SpatialIndex":
         key = float(D)

@@ -1,0 +1,584 @@
+// 3D-2D localization kNN on the 5th-gen tensor cores (tcgen05, kind::i8).
+//
+// Native body of DescriptorIndex.knn2's exact path (descriptors.py:35-72) for the
+// queries of direct_3d2d_search (localize.py:99-122), batched over points x
+// images.  A point is its track-descriptor sum S (<= 255 n) and track length n
+// (mean = S/n, localize.py:51-59); against feature f the exact rank key is
+//     key = n |f|^2 - 2 S.f            (N = |S - n f|^2 = n*key + |S|^2)
+// S.f is computed exactly as two u8 x u8 -> s32 GEMMs over the digit planes
+// S = S_lo + 256 S_hi.  Per (point, image) the epilogue keeps the running top-2
+// (lowest feature index wins ties), so no distance matrix is ever stored.
+//
+// CTA (persistent, 1 per SM, 384 threads):
+//   warp 0      TMA producer: A planes (128 points x 128 B, once per unit) and
+//               B tiles (128 features x 128 B, 4-stage ring), SWIZZLE_128B
+//   warp 1      MMA issuer: tcgen05.mma M=128 N=128 K=32 x 4 per plane,
+//               accumulators in TMEM (2 stages x 2 planes x 128 columns)
+//   warp 2      TMEM allocator
+//   warps 4-11  epilogue: tcgen05.ld -> key -> top-2, 2 warps per lane quadrant
+// unit = (128-point tile, image); tile = 128 features of that image.
+#include <cuda.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace msfm {
+namespace {
+
+constexpr int KN_THREADS = 384;
+constexpr int KN_STAGES = 4;
+constexpr int TILE_M = 128, TILE_N = 128, KB = 128;   // K = 128 bytes per plane
+constexpr int EPI_WARP0 = 4, EPI_WARPS = 8;
+constexpr uint32_t B_TILE_BYTES = TILE_N * KB;          // 16 KB
+constexpr uint32_t A_PLANE_BYTES = TILE_M * KB;         // 16 KB
+constexpr int INT_BIG = 0x7fffffff;
+
+struct KnnSmem {
+    uint8_t a[2][A_PLANE_BYTES];            // lo, hi planes (1024-B aligned)
+    uint8_t b[KN_STAGES][B_TILE_BYTES];
+    uint64_t full[KN_STAGES], empty[KN_STAGES];
+    uint64_t a_full, a_empty;
+    uint64_t t_full[2], t_empty[2];
+    uint32_t tmem_base;
+    int merge_k1[TILE_M], merge_i1[TILE_M], merge_k2[TILE_M];
+};
+
+struct KnnArgs {
+    const int32_t* n;          // [M_pad] track length (0 for padding rows)
+    const int32_t* fnorm;      // bank |f|^2
+    const int64_t* img_off;    // bank image offsets
+    const int32_t* img_n;      // bank image sizes
+    const int32_t* images;     // [n_img] bank image index of each query image
+    int n_img;
+    int m_tiles;
+    int M;                     // real points
+    int32_t* out_k1;           // [n_img][M_pad]
+    int32_t* out_i1;
+    int32_t* out_k2;
+    int M_pad;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+// Bounded wait: a protocol bug traps instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    const uint32_t addr = smem_u32(b);
+    uint32_t done = 0;
+    for (long long it = 0; it < (1LL << 31); it++) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(addr), "r"(parity)
+            : "memory");
+        if (done) return;
+    }
+    __trap();
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+// K-major, 128-byte swizzle UMMA shared-memory descriptor (8 rows x 128 B atoms)
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;                 // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;       // SBO: 8-row group stride
+    d |= (uint64_t)1 << 46;                 // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
+    return d;
+}
+
+// instruction descriptor: kind::i8, D = s32, A/B unsigned 8-bit, K-major, M=128, N=128
+constexpr uint32_t IDESC = (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(TILE_N >> 3) << 17) |
+                           ((uint32_t)(TILE_M >> 4) << 24);
+
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"
+        " [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_wait_ld() {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ int unit_tiles(const KnnArgs& a, int u, int& img, int& mt, int64_t& off,
+                                          int& n) {
+    mt = u / a.n_img;
+    const int s = u - mt * a.n_img;
+    img = a.images[s];
+    off = a.img_off[img];
+    n = a.img_n[img];
+    return (n + TILE_N - 1) / TILE_N;
+}
+
+__global__ void __launch_bounds__(KN_THREADS, 1)
+knn_tc_kernel(const __grid_constant__ CUtensorMap map_lo, const __grid_constant__ CUtensorMap map_hi,
+              const __grid_constant__ CUtensorMap map_b, KnnArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    KnnSmem& S = *reinterpret_cast<KnnSmem*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_units = a.m_tiles * a.n_img;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < KN_STAGES; s++) {
+            mbar_init(&S.full[s], 1);
+            mbar_init(&S.empty[s], 1);
+        }
+        mbar_init(&S.a_full, 1);
+        mbar_init(&S.a_empty, 1);
+        for (int s = 0; s < 2; s++) {
+            mbar_init(&S.t_full[s], 1);
+            mbar_init(&S.t_empty[s], EPI_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            smem_u32(&S.tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = S.tmem_base;
+
+    if (warp == 0) {
+        // ---------------- TMA producer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0, a_phase = 0;
+            int first = 1;
+            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+                int img, mt, n;
+                int64_t off;
+                const int nt = unit_tiles(a, u, img, mt, off, n);
+                if (nt == 0) continue;
+                if (!first) {
+                    mbar_wait(&S.a_empty, a_phase);
+                    a_phase ^= 1;
+                }
+                first = 0;
+                mbar_expect_tx(&S.a_full, 2 * A_PLANE_BYTES);
+                tma_load_2d(S.a[0], &map_lo, &S.a_full, 0, mt * TILE_M);
+                tma_load_2d(S.a[1], &map_hi, &S.a_full, 0, mt * TILE_M);
+                for (int j = 0; j < nt; j++) {
+                    mbar_wait(&S.empty[stage], phase ^ 1);
+                    mbar_expect_tx(&S.full[stage], B_TILE_BYTES);
+                    tma_load_2d(S.b[stage], &map_b, &S.full[stage], 0, (int)(off + (int64_t)j * TILE_N));
+                    if (++stage == KN_STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        if (lane == 0) {
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, a_phase = 0, acc_phase = 0;
+            const uint32_t a_lo = smem_u32(S.a[0]), a_hi = smem_u32(S.a[1]);
+            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+                int img, mt, n;
+                int64_t off;
+                const int nt = unit_tiles(a, u, img, mt, off, n);
+                if (nt == 0) continue;
+                mbar_wait(&S.a_full, a_phase);
+                a_phase ^= 1;
+                tc_fence_after();
+                for (int j = 0; j < nt; j++) {
+                    mbar_wait(&S.t_empty[acc], acc_phase ^ 1);
+                    mbar_wait(&S.full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t b_addr = smem_u32(S.b[stage]);
+                    const uint32_t d_lo = tbase + (uint32_t)(acc * 256);
+                    const uint32_t d_hi = d_lo + 128;
+#pragma unroll
+                    for (int k = 0; k < KB / 32; k++) {
+                        umma_i8(d_lo, umma_desc_sw128(a_lo + 32 * k), umma_desc_sw128(b_addr + 32 * k), k > 0);
+                    }
+#pragma unroll
+                    for (int k = 0; k < KB / 32; k++) {
+                        umma_i8(d_hi, umma_desc_sw128(a_hi + 32 * k), umma_desc_sw128(b_addr + 32 * k), k > 0);
+                    }
+                    umma_commit(&S.empty[stage]);     // B stage reusable once these MMAs retire
+                    umma_commit(&S.t_full[acc]);      // accumulator ready for the epilogue
+                    if (++stage == KN_STAGES) { stage = 0; phase ^= 1; }
+                    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                }
+                umma_commit(&S.a_empty);              // A planes reusable after this unit
+            }
+        }
+    } else if (warp >= EPI_WARP0) {
+        // ---------------- epilogue
+        const int ew = warp - EPI_WARP0;          // 0..7
+        const int quad = warp & 3;                // TMEM lane quadrant this warp may access
+        const int half = ew >> 2;                 // column half
+        const int row = quad * 32 + lane;         // point row within the tile
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+            int img, mt, n;
+            int64_t off;
+            const int nt = unit_tiles(a, u, img, mt, off, n);
+            const int grow = mt * TILE_M + row;
+            const int np = grow < a.M_pad ? a.n[grow] : 0;
+            int k1 = INT_BIG, i1 = -1, k2 = INT_BIG;
+            for (int j = 0; j < nt; j++) {
+                mbar_wait(&S.t_full[acc], acc_phase);
+                tc_fence_after();
+                const uint32_t t_lo = tbase + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * 256 + half * 64);
+                const int cbase = j * TILE_N + half * 64;
+#pragma unroll
+                for (int c0 = 0; c0 < 64; c0 += 16) {
+                    uint32_t lo[16], hi[16];
+                    tmem_ld16(t_lo + c0, lo);
+                    tmem_ld16(t_lo + 128 + c0, hi);
+                    tmem_wait_ld();
+                    const int col0 = cbase + c0;
+#pragma unroll
+                    for (int c = 0; c < 16; c++) {
+                        const int col = col0 + c;
+                        const int fv = col < n ? __ldg(a.fnorm + off + col) : 0;
+                        const int dot = (int)lo[c] + ((int)hi[c] << 8);
+                        const int key = np * fv - 2 * dot;
+                        if (key < k2 && col < n) {
+                            if (key < k1) { k2 = k1; k1 = key; i1 = col; }
+                            else k2 = key;
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&S.t_empty[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+            // merge the two column halves of each row
+            if (half == 1) {
+                S.merge_k1[row] = k1; S.merge_i1[row] = i1; S.merge_k2[row] = k2;
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(EPI_WARPS * 32));
+            if (half == 0) {
+                const int ok1 = S.merge_k1[row], oi1 = S.merge_i1[row], ok2 = S.merge_k2[row];
+                // best = min by (key, index); second = 2nd smallest key value
+                const bool other_first = (ok1 < k1) || (ok1 == k1 && oi1 >= 0 && (i1 < 0 || oi1 < i1));
+                const int nk1 = other_first ? ok1 : k1;
+                const int ni1 = other_first ? oi1 : i1;
+                const int hi_k = other_first ? k1 : ok1;
+                const int nk2 = min(hi_k, min(k2, ok2));
+                const int slot = u - mt * a.n_img;
+                if (grow < a.M_pad) {
+                    const int64_t o = (int64_t)slot * a.M_pad + grow;
+                    a.out_k1[o] = nk1; a.out_i1[o] = ni1; a.out_k2[o] = nk2;
+                }
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(EPI_WARPS * 32));
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
+    }
+}
+
+// ------------------------------------------------------------------ helpers
+__global__ void digit_planes_kernel(const int32_t* __restrict__ S, const int32_t* __restrict__ n,
+                                    int64_t M, int64_t M_pad, uint8_t* __restrict__ lo,
+                                    uint8_t* __restrict__ hi, int32_t* __restrict__ npad) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M_pad * 128) return;
+    const int64_t r = i >> 7;
+    const int v = r < M ? S[i] : 0;
+    lo[i] = (uint8_t)(v & 255);
+    hi[i] = (uint8_t)(v >> 8);
+    if ((i & 127) == 0) npad[r] = r < M ? n[r] : 0;
+}
+
+// ratio test + one point per feature (localize.py:108-122, matching.py:82-103)
+struct DirectArgs {
+    const int32_t* n; const int64_t* SS; const int32_t* k1; const int32_t* i1; const int32_t* k2;
+    const int32_t* images; const int32_t* img_n;
+    int32_t* win; const int64_t* win_off; int32_t* row_out; int32_t* fid_out; int32_t* cnt_out;
+    int M, M_pad, n_img;
+    long long p, q;
+    double cap;
+};
+
+__device__ __forceinline__ long long exact_N(const DirectArgs& a, int s, int r, int32_t k) {
+    return (long long)a.n[r] * k + a.SS[r];
+}
+
+__device__ __forceinline__ bool accepted(const DirectArgs& a, int s, int r, long long& Nb) {
+    const int64_t o = (int64_t)s * a.M_pad + r;
+    const int i1 = a.i1[o];
+    if (i1 < 0) return false;
+    Nb = exact_N(a, s, r, a.k1[o]);
+    const int k2 = a.k2[o];
+    if (k2 == INT_BIG) return sqrt((double)Nb) / (double)a.n[r] < a.cap;
+    const long long Ns = exact_N(a, s, r, k2);
+    return (__int128)a.q * a.q * Nb < (__int128)a.p * a.p * Ns;
+}
+
+// total order on (N/n^2, row): true if row r beats row c
+__device__ __forceinline__ bool closer(const DirectArgs& a, int s, int r, long long Nr, int c) {
+    const int64_t oc = (int64_t)s * a.M_pad + c;
+    const long long Nc = exact_N(a, s, c, a.k1[oc]);
+    const __int128 lhs = (__int128)Nr * a.n[c] * a.n[c];
+    const __int128 rhs = (__int128)Nc * a.n[r] * a.n[r];
+    return lhs < rhs || (lhs == rhs && r < c);
+}
+
+__global__ void direct_claim_kernel(DirectArgs a) {
+    const int s = blockIdx.y;
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= a.M) return;
+    long long Nb;
+    if (!accepted(a, s, r, Nb)) return;
+    const int f = a.i1[(int64_t)s * a.M_pad + r];
+    int* w = a.win + a.win_off[s] + f;
+    int cur = *w;
+    while (cur < 0 || closer(a, s, r, Nb, cur)) {
+        const int prev = atomicCAS(w, cur, r);
+        if (prev == cur) break;
+        cur = prev;
+    }
+}
+
+__global__ void direct_init_kernel(DirectArgs a) {
+    const int s = blockIdx.y;
+    const int n = a.img_n[a.images[s]];
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < n; f += gridDim.x * blockDim.x)
+        a.win[a.win_off[s] + f] = -1;
+}
+
+__global__ void __launch_bounds__(1024) direct_compact_kernel(DirectArgs a) {
+    __shared__ int wsum[33];
+    const int s = blockIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int carry = 0;
+    for (int r0 = 0; r0 < a.M; r0 += 1024) {
+        const int r = r0 + threadIdx.x;
+        bool keep = false;
+        int f = -1;
+        if (r < a.M) {
+            long long Nb;
+            if (accepted(a, s, r, Nb)) {
+                f = a.i1[(int64_t)s * a.M_pad + r];
+                keep = a.win[a.win_off[s] + f] == r;
+            }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) wsum[wid] = __popc(bal);
+        __syncthreads();
+        if (wid == 0) {
+            int v = wsum[lane], x = v;
+            for (int o = 1; o < 32; o <<= 1) {
+                int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            wsum[lane] = x - v;
+            if (lane == 31) wsum[32] = x;
+        }
+        __syncthreads();
+        if (keep) {
+            const int pos = carry + wsum[wid] + __popc(bal & ((1u << lane) - 1u));
+            a.row_out[(int64_t)s * a.M_pad + pos] = r;
+            a.fid_out[(int64_t)s * a.M_pad + pos] = f;
+        }
+        carry += wsum[32];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) a.cnt_out[s] = carry;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int make_rows128_map(CUtensorMap* map, const void* base, int64_t rows) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+                cudaSuccess || !p) {
+            set_error("cuTensorMapEncodeTiled unavailable");
+            return MSFM_ECUDA;
+        }
+        fn = (EncodeTiledFn)p;
+    }
+    cuuint64_t dims[2] = {128, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {128, 128};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+        return MSFM_ECUDA;
+    }
+    return MSFM_OK;
+}
+
+}  // namespace
+}  // namespace msfm
+
+using namespace msfm;
+
+extern "C" size_t msfm_knn_workspace_bytes(int32_t n_points) {
+    const int64_t M_pad = ((int64_t)n_points + TILE_M - 1) / TILE_M * TILE_M;
+    return aligned_bytes<uint8_t>(M_pad * 128) * 2 + aligned_bytes<int32_t>(M_pad) + 4096;
+}
+
+extern "C" int msfm_direct_3d2d(const msfm_bank* bank, int32_t n_points, const int32_t* d_n,
+                                const int64_t* d_SS, int32_t n_images, const int32_t* d_images,
+                                const int32_t* d_k1, const int32_t* d_i1, const int32_t* d_k2,
+                                int64_t ratio_p, int64_t ratio_q, double single_cap,
+                                int32_t* d_win, const int64_t* d_win_off, int32_t* d_corr_row,
+                                int32_t* d_corr_fid, int32_t* d_corr_n, void* stream) {
+    if (!bank || n_points < 0 || n_images < 0 || ratio_p <= 0 || ratio_q <= 0 ||
+        ratio_p > (1 << 20) || ratio_q > (1 << 20)) {
+        set_error("msfm_direct_3d2d: bad arguments");
+        return MSFM_EINVAL;
+    }
+    if (n_images == 0) return MSFM_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    DirectArgs a;
+    a.n = d_n; a.SS = d_SS; a.k1 = d_k1; a.i1 = d_i1; a.k2 = d_k2;
+    a.images = d_images; a.img_n = bank->d_img_n;
+    a.win = d_win; a.win_off = d_win_off; a.row_out = d_corr_row; a.fid_out = d_corr_fid;
+    a.cnt_out = d_corr_n;
+    a.M = n_points;
+    a.M_pad = (int)(((int64_t)n_points + TILE_M - 1) / TILE_M * TILE_M);
+    a.n_img = n_images;
+    a.p = ratio_p; a.q = ratio_q; a.cap = single_cap;
+    if (n_points == 0) {
+        MSFM_CUDA_TRY(cudaMemsetAsync(d_corr_n, 0, sizeof(int32_t) * n_images, st));
+        return MSFM_OK;
+    }
+    direct_init_kernel<<<dim3(16, n_images), 256, 0, st>>>(a);
+    direct_claim_kernel<<<dim3((n_points + 255) / 256, n_images), 256, 0, st>>>(a);
+    direct_compact_kernel<<<n_images, 1024, 0, st>>>(a);
+    MSFM_LAUNCH_CHECK();
+    count_launches(3);
+    return MSFM_OK;
+}
+
+extern "C" int msfm_knn2_tracks(const msfm_bank* bank, int32_t n_points, const int32_t* d_S,
+                                const int32_t* d_n, int32_t n_images, const int32_t* d_images,
+                                int32_t max_track, int32_t* d_k1, int32_t* d_i1, int32_t* d_k2,
+                                void* d_workspace, size_t workspace_bytes, void* stream) {
+    if (!bank || n_points < 0 || n_images < 0 || (n_points > 0 && (!d_S || !d_n))) {
+        set_error("msfm_knn2_tracks: bad arguments");
+        return MSFM_EINVAL;
+    }
+    if (max_track > 100) {
+        set_error("msfm_knn2_tracks: track length %d > 100 overflows the int32 rank key", max_track);
+        return MSFM_EINVAL;
+    }
+    if (n_points == 0 || n_images == 0) return MSFM_OK;
+    if (workspace_bytes < msfm_knn_workspace_bytes(n_points)) {
+        set_error("msfm_knn2_tracks: workspace too small");
+        return MSFM_EWORKSPACE;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t M_pad = ((int64_t)n_points + TILE_M - 1) / TILE_M * TILE_M;
+    Arena ar(d_workspace, workspace_bytes);
+    uint8_t* lo = ar.take<uint8_t>(M_pad * 128);
+    uint8_t* hi = ar.take<uint8_t>(M_pad * 128);
+    int32_t* npad = ar.take<int32_t>(M_pad);
+    digit_planes_kernel<<<(unsigned)((M_pad * 128 + 255) / 256), 256, 0, st>>>(d_S, d_n, n_points,
+                                                                             M_pad, lo, hi, npad);
+    MSFM_LAUNCH_CHECK();
+    const int64_t n_total = bank->n_total;
+    if (n_total <= 0) {
+        set_error("msfm_knn2_tracks: empty feature bank");
+        return MSFM_EINVAL;
+    }
+    CUtensorMap mlo, mhi, mb;
+    int rc;
+    if ((rc = make_rows128_map(&mlo, lo, M_pad))) return rc;
+    if ((rc = make_rows128_map(&mhi, hi, M_pad))) return rc;
+    if ((rc = make_rows128_map(&mb, bank->d_desc, n_total))) return rc;
+    KnnArgs a;
+    a.n = npad;
+    a.fnorm = bank->d_norm2;
+    a.img_off = bank->d_img_off;
+    a.img_n = bank->d_img_n;
+    a.images = d_images;
+    a.n_img = n_images;
+    a.m_tiles = (int)(M_pad / TILE_M);
+    a.M = n_points;
+    a.M_pad = (int)M_pad;
+    a.out_k1 = d_k1;
+    a.out_i1 = d_i1;
+    a.out_k2 = d_k2;
+    const size_t smem = sizeof(KnnSmem) + 1024;
+    MSFM_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int units = a.m_tiles * n_images;
+    const int grid = units < nsm ? units : nsm;
+    {
+        ProfScope ps("knn_tc_kernel", st);
+        knn_tc_kernel<<<grid, KN_THREADS, smem, st>>>(mlo, mhi, mb, a);
+    }
+    MSFM_LAUNCH_CHECK();
+    count_launches(2);
+    return MSFM_OK;
+}

@@ -1,0 +1,67 @@
+"""GPU parity of the tcgen05 kNN and the direct 3D-2D search (through the C-ABI)."""
+
+import numpy as np
+import pytest
+
+from golden_io import load_localize
+from oracle import localize as ol
+
+pytestmark = pytest.mark.gpu
+
+
+def _random_case(rng, M, sizes, max_n=10, dup=False):
+    from paper_1512_06235_b200.types import FeatureSet
+    sets = {}
+    for i, nf in enumerate(sizes):
+        desc = rng.integers(0, 256, size=(nf, 128), dtype=np.uint8)
+        if dup and nf > 4:
+            desc[3] = desc[1]          # exact ties: lowest index must win
+        sets[i] = FeatureSet(image_id=i, width=640, height=480,
+                             xy=rng.uniform(0, 400, size=(nf, 2)).astype(np.float32),
+                             scale=np.ones(nf, np.float32), orientation=np.zeros(nf, np.float32),
+                             descriptors=desc)
+    n = rng.integers(1, max_n + 1, size=M).astype(np.int32)
+    S = (rng.integers(0, 256, size=(M, 128)) * n[:, None]).astype(np.int32)
+    if dup and M > 3:
+        S[2] = S[0] if n[2] == n[0] else S[2]
+    return sets, S, n
+
+
+@pytest.mark.parametrize("M,sizes,max_n", [(1, [1], 1), (5, [3, 1, 0, 130], 4), (128, [128], 10),
+                                           (300, [257, 1000, 5], 10), (1000, [2000, 129], 100)])
+def test_knn_topk_matches_exact_oracle(M, sizes, max_n):
+    from paper_1512_06235_b200.bank import FeatureBank
+    from paper_1512_06235_b200.localize import PointSet, knn2_tracks
+
+    rng = np.random.default_rng(M + len(sizes))
+    sets, S, n = _random_case(rng, M, sizes, max_n, dup=True)
+    bank = FeatureBank(sets)
+    pts = PointSet(S=S, n=n, ids=np.arange(M))
+    imgs = [i for i in sets]
+    res = knn2_tracks(bank, pts, imgs)
+    for s, i in enumerate(imgs):
+        F = sets[i].descriptors
+        idx, nb, ns = res.host(pts, s)
+        if len(F) == 0:
+            assert (idx == -1).all()
+            continue
+        oi, onb, ons = ol.knn2_exact(S, n, F)
+        np.testing.assert_array_equal(idx, oi)
+        np.testing.assert_array_equal(nb, onb)
+        np.testing.assert_array_equal(ns, ons)
+
+
+@pytest.mark.parametrize("name", ["localize_holdout.npz", "localize_c2mini.npz"])
+def test_direct_search_equals_reference(name):
+    from paper_1512_06235_b200.bank import FeatureBank
+    from paper_1512_06235_b200.localize import PointSet, direct_search
+    from paper_1512_06235_b200 import scenes
+
+    kw, scene, snap, z = load_localize(name)
+    S, n = scenes.track_sums(scene, snap)
+    pts = PointSet(S=S, n=n, ids=np.arange(len(S)))
+    bank = FeatureBank(scene.feature_sets)
+    qs = [int(q) for q in z["queries"]]
+    got = direct_search(bank, pts, qs)
+    for s, q in enumerate(qs):
+        np.testing.assert_array_equal(got[s], z[f"q{q}_corr"])
