@@ -152,11 +152,13 @@ int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids, int32_t n_
  * numpy's `rng.choice(n, size=sample_size, replace=False)` starting from the
  * PCG64 state of a numpy Generator (state hi/lo, inc hi/lo, has_uint32,
  * uinteger = rng.bit_generator.state), exactly as pnp_ransac consumes them
- * (reconstruct.py:185-194).  out: [count][sample_size] int32.
+ * (reconstruct.py:185-194).  out: [count][sample_size] int32.  state_out
+ * (optional) receives the generator state after the draws: state hi/lo,
+ * inc hi/lo, has_uint32, uinteger — to continue the stream in a later call.
  * ---------------------------------------------------------------------- */
 int msfm_ransac_samples(const uint64_t state_inc[4], int32_t has_uint32, uint32_t uinteger,
                         int64_t n, int32_t sample_size, int32_t count, int32_t* out,
-                        uint64_t state_out[4]);
+                        uint64_t state_out[6]);
 
 /* ------------------------------------------------------------------------
  * 3D-2D localization kNN (DescriptorIndex.knn2 exact path, descriptors.py:35-72,
@@ -190,6 +192,30 @@ int msfm_direct_3d2d(const msfm_bank* bank, int32_t n_points, const int32_t* d_n
                      int64_t ratio_p, int64_t ratio_q, double single_cap,
                      int32_t* d_win, const int64_t* d_win_off, int32_t* d_corr_row,
                      int32_t* d_corr_fid, int32_t* d_corr_n, void* stream);
+
+/* ------------------------------------------------------------------------
+ * PnP-RANSAC (reconstruct.py:168-226), batched over images.  Correspondences of
+ * image s: X [off[s]..off[s+1])[3] f64 world points, uv [..][2] f64 pixels,
+ * K [s][9].  msfm_pnp_hypotheses scores n_hyp host-supplied 6-point samples per
+ * image (d_samples [s][h][6], image-local indices; see msfm_ransac_samples):
+ * d_hyp [s][h][12] = R (row-major) | t of dlt_pose (reconstruct.py:53-103),
+ * d_count [s][h] = inliers (err < threshold, z > 0), -1 when the DLT fails.
+ * The caller replays the adaptive stop (reconstruct.py:192-211) on the counts
+ * and passes the winning pose to msfm_pnp_refit, which recomputes the inlier
+ * mask, refits dlt_pose on it, runs refine_pose_lm (<= lm_iters LM iterations)
+ * and writes the final R, t, mask (d_mask[off[s]..]) and inlier count;
+ * d_ok[s] = final inliers >= min_inliers and the refit succeeded.  Only images
+ * with d_status[s] != 0 are processed.
+ * ---------------------------------------------------------------------- */
+int msfm_pnp_hypotheses(const double* d_X, const double* d_uv, const int64_t* d_off,
+                        const double* d_K, int32_t n_images, const int32_t* d_samples,
+                        int32_t n_hyp, double threshold, double* d_hyp, int32_t* d_count,
+                        void* stream);
+int msfm_pnp_refit(const double* d_X, const double* d_uv, const int64_t* d_off, const double* d_K,
+                   int32_t n_images, const double* d_hyp_best, const int32_t* d_status,
+                   double threshold, int32_t min_inliers, int32_t lm_iters, double* d_R,
+                   double* d_t, uint8_t* d_mask, int32_t* d_n_inliers, int32_t* d_ok,
+                   void* stream);
 
 #ifdef __cplusplus
 }

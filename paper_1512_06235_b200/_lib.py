@@ -57,6 +57,10 @@ _SIGS = {
     "msfm_direct_3d2d": (ctypes.c_int, [ctypes.POINTER(Bank), ctypes.c_int32, VP, VP, ctypes.c_int32,
                                         VP, VP, VP, VP, ctypes.c_int64, ctypes.c_int64,
                                         ctypes.c_double, VP, VP, VP, VP, VP, VP]),
+    "msfm_pnp_hypotheses": (ctypes.c_int, [VP, VP, VP, VP, ctypes.c_int32, VP, ctypes.c_int32,
+                                           ctypes.c_double, VP, VP, VP]),
+    "msfm_pnp_refit": (ctypes.c_int, [VP, VP, VP, VP, ctypes.c_int32, VP, VP, ctypes.c_double,
+                                      ctypes.c_int32, ctypes.c_int32, VP, VP, VP, VP, VP, VP]),
     "msfm_guided_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int32, VP,
                                                       ctypes.POINTER(MatchParams)]),
     "msfm_guided_match": (ctypes.c_int, [ctypes.POINTER(Bank), ctypes.POINTER(Grids),

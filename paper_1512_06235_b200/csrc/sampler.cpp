@@ -112,7 +112,7 @@ namespace msfm { void set_error(const char* fmt, ...); }
 
 extern "C" int msfm_ransac_samples(const uint64_t state_inc[4], int32_t has_uint32,
                                    uint32_t uinteger, int64_t n, int32_t sample_size,
-                                   int32_t count, int32_t* out, uint64_t state_out[4]) {
+                                   int32_t count, int32_t* out, uint64_t state_out[6]) {
     if (!state_inc || !out || n < sample_size || sample_size < 1 || sample_size > 48 || count < 0) {
         msfm::set_error("msfm_ransac_samples: bad arguments (n=%lld, size=%d)", (long long)n,
                         sample_size);
@@ -137,6 +137,8 @@ extern "C" int msfm_ransac_samples(const uint64_t state_inc[4], int32_t has_uint
         state_out[1] = (uint64_t)g.state;
         state_out[2] = (uint64_t)(g.inc >> 64);
         state_out[3] = (uint64_t)g.inc;
+        state_out[4] = (uint64_t)g.has32;
+        state_out[5] = (uint64_t)g.u32;
     }
     return MSFM_OK;
 }

@@ -1,0 +1,60 @@
+"""GPU PnP-RANSAC vs the reference's outputs: identical inlier masks, poses within tolerance."""
+
+import numpy as np
+import pytest
+
+from golden_io import GOLDEN, load_localize
+
+pytestmark = pytest.mark.gpu
+
+R_TOL = 1e-6     # stated tolerance (relative/absolute on rotation entries); expected ~1e-10
+T_TOL = 1e-6
+
+
+def _check(res, R, t, mask):
+    assert res is not None
+    gR, gt, gm = res
+    np.testing.assert_array_equal(gm, mask)
+    np.testing.assert_allclose(gR, R, atol=R_TOL)
+    np.testing.assert_allclose(gt, t, rtol=T_TOL, atol=T_TOL)
+
+
+def test_pnp_cases_match_reference():
+    from paper_1512_06235_b200.pnp import pnp_ransac
+
+    z = np.load(f"{GOLDEN}/pnp_cases.npz")
+    for k in range(int(z["n_cases"])):
+        X, uv, K, seed = z[f"c{k}_X"], z[f"c{k}_uv"], z[f"c{k}_K"], int(z[f"c{k}_seed"])
+        status = str(z[f"c{k}_status"])
+        if status == "overflow":
+            with pytest.raises(OverflowError):
+                pnp_ransac(X, uv, K, seed=seed)
+        elif status == "none":
+            assert pnp_ransac(X, uv, K, seed=seed) is None
+        else:
+            _check(pnp_ransac(X, uv, K, seed=seed), z[f"c{k}_R"], z[f"c{k}_t"], z[f"c{k}_mask"])
+
+
+@pytest.mark.parametrize("name", ["localize_holdout.npz", "localize_c2mini.npz"])
+def test_batched_pnp_on_reference_correspondences(name):
+    from paper_1512_06235_b200.pnp import pnp_batch
+
+    kw, scene, snap, z = load_localize(name)
+    qs = [int(q) for q in z["queries"] if str(z[f"q{int(q)}_status"]) != "below_gate"]
+    X = [snap.point_xyz[z[f"q{q}_corr"][:, 0]] for q in qs]
+    uv = [scene.feature_sets[q].xy[z[f"q{q}_corr"][:, 1]].astype(np.float64) for q in qs]
+    K = [scene.cameras[q].K for q in qs]
+    res = pnp_batch(X, uv, K, qs)
+    for q, r in zip(qs, res):
+        status = str(z[f"q{q}_status"])
+        assert r.status == status, (q, r.status, status)
+        if status == "ok":
+            _check((r.R, r.t, r.mask), z[f"q{q}_R"], z[f"q{q}_t"], z[f"q{q}_mask"])
+
+
+def test_insufficient_raises():
+    from paper_1512_06235_b200.pnp import pnp_ransac
+    from paper_1512_06235_b200.types import InsufficientDataError
+
+    with pytest.raises(InsufficientDataError):
+        pnp_ransac(np.zeros((5, 3)), np.zeros((5, 2)), np.eye(3))

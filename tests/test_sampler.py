@@ -28,3 +28,24 @@ def test_many_seeds_small_populations():
 def test_rejects_bad_population():
     with pytest.raises(ValueError):
         ransac_samples(0, 5, 3)
+
+
+def test_stream_continuation():
+    """state_out continues the stream exactly (used for a second RANSAC round)."""
+    from paper_1512_06235_b200 import _lib
+    from paper_1512_06235_b200.sampling import rng_state
+
+    lib = _lib.load(require_device=False)
+    seed, n = 42, 777
+    words, has32, u32 = rng_state(seed)
+    a = np.zeros((10, 6), np.int32)
+    st = np.zeros(6, np.uint64)
+    _lib.check(lib.msfm_ransac_samples(words.ctypes.data, has32, u32, n, 6, 10, a.ctypes.data,
+                                       st.ctypes.data), "s")
+    b = np.zeros((15, 6), np.int32)
+    w2 = np.ascontiguousarray(st[:4])
+    _lib.check(lib.msfm_ransac_samples(w2.ctypes.data, int(st[4]), int(st[5]), n, 6, 15,
+                                       b.ctypes.data, None), "s")
+    rng = np.random.default_rng(seed)
+    ref = np.stack([rng.choice(n, 6, replace=False) for _ in range(25)])
+    np.testing.assert_array_equal(np.vstack([a, b]), ref)
