@@ -165,3 +165,279 @@ def direct_search(bank: FeatureBank, pts: PointSet, image_ids, *, ratio: float =
         return [np.stack([pts.ids[rows[s, :c[s]].cpu().numpy()], fids[s, :c[s]].cpu().numpy()], 1)
                 .astype(np.int64) for s in range(len(slots))]
     return res
+
+
+# ---------------------------------------------------------------------------
+# reference-shaped stage API (localize.py:33-281)
+# ---------------------------------------------------------------------------
+
+SET_COVER_K = 400
+SET_COVER_ENGAGE_POINTS = 100_000
+RANKED_TOP_K = 10
+
+
+@dataclass
+class LocalizationResult:
+    image_id: int
+    method: str
+    correspondences: list = field(default_factory=list)
+    pose: object = None
+    inliers: int = 0
+    inlier_refs: list = field(default_factory=list)
+    reason: str = ""
+
+
+@dataclass
+class SetCover:
+    selected: list
+    k: int
+    coverage: dict
+
+
+def compute_set_cover(model, k: int = SET_COVER_K) -> SetCover:
+    """Lazy-greedy k-cover (localize.py:62-96): host side, off the per-image path."""
+    import heapq
+
+    if k < 1:
+        raise ValueError(f"coverage target must be >= 1, got {k}")
+    remaining = {i: k for i in model.cameras}
+    coverage = {i: 0 for i in model.cameras}
+    selected = []
+
+    def score(pid):
+        return sum(1 for i in model.points[pid].track if remaining.get(i, 0) > 0)
+
+    heap = [(-score(p), -len(model.points[p].track), p) for p in sorted(model.points)]
+    heapq.heapify(heap)
+    while heap:
+        neg_s, neg_len, pid = heapq.heappop(heap)
+        s = score(pid)
+        if s == 0:
+            continue
+        if -neg_s != s:
+            heapq.heappush(heap, (-s, neg_len, pid))
+            continue
+        selected.append(pid)
+        for i in model.points[pid].track:
+            if remaining.get(i, 0) > 0:
+                remaining[i] -= 1
+            coverage[i] = coverage.get(i, 0) + 1
+        if all(v == 0 for v in remaining.values()):
+            break
+    return SetCover(selected=selected, k=k, coverage=coverage)
+
+
+def model_points(model, feature_store, point_ids) -> PointSet:
+    """Exact track sums of the listed points (mean_descriptor, localize.py:51-59)."""
+    pids = np.asarray(sorted(point_ids), dtype=np.int64)
+    S = np.zeros((len(pids), 128), dtype=np.int32)
+    n = np.zeros(len(pids), dtype=np.int32)
+    by_img: dict = {}
+    for r, p in enumerate(pids):
+        tr = model.points[int(p)].track
+        n[r] = len(tr)
+        for i, f in tr.items():
+            by_img.setdefault(i, ([], []))
+            by_img[i][0].append(r)
+            by_img[i][1].append(f)
+    for i, (rows, fids) in by_img.items():
+        d = np.asarray(feature_store.sets[i].descriptors)[np.asarray(fids)].astype(np.int32)
+        np.add.at(S, np.asarray(rows), d)
+    return PointSet(S=S, n=n, ids=pids)
+
+
+def direct_3d2d_search(model, point_ids, image_fs, feature_store, *, ratio=RATIO_UNGUIDED,
+                       single_cap=SINGLE_CANDIDATE_CAP, index=None, stats=None):
+    """Drop-in for localize.py:99-122 (exact kNN on the device)."""
+    pids = sorted(point_ids)
+    if not pids or len(image_fs) == 0:
+        return []
+    pts = model_points(model, feature_store, pids)
+    bank = FeatureBank({int(image_fs.image_id): image_fs})
+    if stats is not None:
+        stats.add(len(pids), len(pids) * len(image_fs))
+    corr = direct_search(bank, pts, [int(image_fs.image_id)], ratio=ratio, single_cap=single_cap)[0]
+    return [(int(p), int(f)) for p, f in corr]
+
+
+def _knn_u8(bank, image_id, queries_u8):
+    """knn2 of u8 query descriptors (track length 1): exact f32 distances as the
+    reference computes them (descriptors.py:55-69, all partials < 2^24)."""
+    q = np.asarray(queries_u8, dtype=np.int32).reshape(-1, 128)
+    pts = PointSet(S=q, n=np.ones(len(q), np.int32), ids=np.arange(len(q)))
+    res = knn2_tracks(bank, pts, [image_id])
+    idx, nb, ns = res.host(pts, 0)
+    d0 = np.sqrt(nb.astype(np.float32)).astype(np.float64)
+    d1 = np.where(ns < 0, np.inf, np.sqrt(np.maximum(ns, 0).astype(np.float32)).astype(np.float64))
+    i1 = np.where(ns < 0, -1, 0)
+    return np.stack([d0, d1], 1), np.stack([idx, i1], 1)
+
+
+def _ratio_filter(dist, idx, ratio, single_cap):
+    """matching.py:82-103 on float64 distances."""
+    out = []
+    for row in range(len(dist)):
+        best, second = dist[row]
+        if idx[row, 0] < 0:
+            continue
+        if idx[row, 1] < 0 or not np.isfinite(second):
+            if best < single_cap:
+                out.append((row, int(idx[row, 0]), float(best), 0.0))
+            continue
+        r = best / second if second > 0 else 1.0
+        if r < ratio:
+            out.append((row, int(idx[row, 0]), float(best), float(r)))
+    return out
+
+
+def ranked_2d2d_search(model, graph, image_id, image_fs, feature_store, *, top_k=RANKED_TOP_K,
+                       ratio=RATIO_UNGUIDED, single_cap=SINGLE_CANDIDATE_CAP,
+                       min_correspondences=MIN_CORRESPONDENCES, index=None, stats=None):
+    """Drop-in for localize.py:125-176 (u8 proxy queries through the device kNN)."""
+    from .types import InsufficientDataError
+
+    neighbors = [(graph.match_count(image_id, o), -o, o) for o in graph.neighbors(image_id)
+                 if model.is_registered(o)]
+    if not neighbors:
+        raise InsufficientDataError(f"image {image_id} has no localized neighbours")
+    neighbors.sort(reverse=True)
+    bank = FeatureBank({int(image_id): image_fs})
+    best: dict = {}
+    for _, _, other in neighbors[:top_k]:
+        proxy = [(pid, model.points[pid].track[other]) for pid in sorted(model.points_visible_in(other))]
+        if not proxy:
+            continue
+        qd = np.stack([feature_store.descriptor(other, f) for _, f in proxy])
+        if stats is not None:
+            stats.add(len(proxy), len(proxy) * len(image_fs))
+        dist, idx = _knn_u8(bank, int(image_id), qd)
+        for row, feat, d, _ in _ratio_filter(dist, idx, ratio, single_cap):
+            pid = proxy[row][0]
+            cur = best.get(pid)
+            if cur is None or d < cur[0]:
+                best[pid] = (d, feat)
+    by_feature: dict = {}
+    for pid, (d, feat) in best.items():
+        cur = by_feature.get(feat)
+        if cur is None or d < cur[0]:
+            by_feature[feat] = (d, pid)
+    corr = sorted((pid, feat) for feat, (d, pid) in by_feature.items())
+    if len(corr) <= min_correspondences:
+        return []
+    return corr
+
+
+def _camera(K, R, t, image_id):
+    try:  # the caller's own Camera class when running inside msfm
+        from msfm.model import Camera as RefCamera  # noqa: F401
+        return RefCamera(K=K, R=R, t=t, image_id=image_id)
+    except Exception:
+        from .types import Camera
+        return Camera(K=K, R=R, t=t, image_id=image_id)
+
+
+def _ref(image_id, fid):
+    try:
+        from msfm.model import FeatureRef as RefFR
+        return RefFR(image_id, fid)
+    except Exception:
+        from .types import FeatureRef
+        return FeatureRef(image_id, fid)
+
+
+def localize_images(model, graph, image_ids, feature_store, intrinsics, *, cover_points=None,
+                    ratio=RATIO_UNGUIDED, min_correspondences=MIN_CORRESPONDENCES,
+                    pnp_threshold=4.0, pnp_min_inliers=16, seed=0, stats=None):
+    """localize_image (localize.py:179-222) for many images in one device pass.
+    Raises OverflowError where the reference's pnp_ransac does."""
+    from .pnp import pnp_batch
+    from .types import InsufficientDataError
+
+    image_ids = [int(i) for i in image_ids]
+    points = cover_points if cover_points is not None else sorted(model.points)
+    pts = model_points(model, feature_store, points)
+    bank = FeatureBank({i: feature_store.sets[i] for i in image_ids})
+    if stats is not None:
+        for i in image_ids:
+            stats.add(len(points), len(points) * len(feature_store.sets[i]))
+    corrs = direct_search(bank, pts, image_ids, ratio=ratio) if len(points) else \
+        [np.zeros((0, 2), np.int64) for _ in image_ids]
+    methods, corr_lists = {}, {}
+    for i, c in zip(image_ids, corrs):
+        corr = [(int(p), int(f)) for p, f in c]
+        methods[i] = "direct3d2d"
+        if len(corr) <= min_correspondences:
+            try:
+                corr = ranked_2d2d_search(model, graph, i, feature_store.sets[i], feature_store,
+                                          ratio=ratio, min_correspondences=min_correspondences,
+                                          stats=stats)
+            except InsufficientDataError:
+                corr = []
+            methods[i] = "ranked2d2d"
+        corr_lists[i] = corr
+    todo = [i for i in image_ids if len(corr_lists[i]) > min_correspondences]
+    X = [np.stack([model.points[p].position for p, _ in corr_lists[i]]) for i in todo]
+    uv = [np.stack([feature_store.sets[i].xy[f] for _, f in corr_lists[i]]).astype(np.float64)
+          for i in todo]
+    res = pnp_batch(X, uv, [intrinsics[i] for i in todo], [seed + i for i in todo],
+                    threshold=pnp_threshold, min_inliers=pnp_min_inliers) if todo else []
+    pnp = dict(zip(todo, res))
+    out = []
+    for i in image_ids:
+        corr = corr_lists[i]
+        if i not in pnp:
+            out.append(LocalizationResult(image_id=i, method=methods[i],
+                                          reason="below correspondence gate"))
+            continue
+        r = pnp[i]
+        if r.status == "overflow":
+            raise OverflowError("cannot convert float infinity to integer")
+        if r.status != "ok":
+            out.append(LocalizationResult(image_id=i, method=methods[i], correspondences=corr,
+                                          reason="resection failed"))
+            continue
+        pose = _camera(intrinsics[i], r.R, r.t, i)
+        refs = [(corr[k][0], _ref(i, corr[k][1])) for k in range(len(corr)) if r.mask[k]]
+        out.append(LocalizationResult(image_id=i, method=methods[i], correspondences=corr,
+                                      pose=pose, inliers=int(r.mask.sum()), inlier_refs=refs))
+    return out
+
+
+def localize_image(model, graph, image_id, feature_store, intrinsics, *, cover_points=None,
+                   ratio=RATIO_UNGUIDED, min_correspondences=MIN_CORRESPONDENCES,
+                   pnp_threshold=4.0, pnp_min_inliers=16, seed=0, stats=None):
+    """Drop-in for localize.py:179-222."""
+    return localize_images(model, graph, [image_id], feature_store, {image_id: intrinsics},
+                           cover_points=cover_points, ratio=ratio,
+                           min_correspondences=min_correspondences, pnp_threshold=pnp_threshold,
+                           pnp_min_inliers=pnp_min_inliers, seed=seed, stats=stats)[0]
+
+
+def localize_all(model, feature_store, graph, intrinsics, *, iteration=1, set_cover_k=SET_COVER_K,
+                 set_cover_engage=SET_COVER_ENGAGE_POINTS, force_set_cover=False,
+                 ratio=RATIO_UNGUIDED, min_correspondences=MIN_CORRESPONDENCES,
+                 pnp_threshold=4.0, pnp_min_inliers=16, seed=0, threads=1, order=None):
+    """Drop-in for localize.py:225-281: one batched device pass over every
+    unregistered image, then the image-id-ordered merge."""
+    unregistered = [i for i in sorted(feature_store.sets) if not model.is_registered(i)]
+    if order is not None:
+        wanted = set(unregistered)
+        unregistered = [i for i in order if i in wanted]
+    if not unregistered:
+        model.stage_tag = f"after_localize({iteration})"
+        return [], []
+    cover = None
+    if force_set_cover or len(model.points) > set_cover_engage:
+        cover = compute_set_cover(model, set_cover_k).selected
+    results = localize_images(model, graph, unregistered, feature_store, intrinsics,
+                              cover_points=cover, ratio=ratio,
+                              min_correspondences=min_correspondences, pnp_threshold=pnp_threshold,
+                              pnp_min_inliers=pnp_min_inliers, seed=seed)
+    newly = []
+    for r in sorted(results, key=lambda r: r.image_id):
+        if r.pose is None:
+            continue
+        model.attach_camera(r.pose, r.inlier_refs)
+        newly.append(r.image_id)
+    model.stage_tag = f"after_localize({iteration})"
+    return newly, results

@@ -65,3 +65,45 @@ def test_direct_search_equals_reference(name):
     got = direct_search(bank, pts, qs)
     for s, q in enumerate(qs):
         np.testing.assert_array_equal(got[s], z[f"q{q}_corr"])
+
+
+class _NoGraph:
+    def neighbors(self, image_id):
+        return []
+
+    def match_count(self, a, b):
+        return 0
+
+
+def test_localize_all_equals_reference_holdout():
+    from paper_1512_06235_b200 import scenes
+    from paper_1512_06235_b200.localize import localize_all
+
+    kw, scene, snap, z = load_localize("localize_holdout.npz")
+    model = scenes.snapshot_to_model(scene, snap)
+    store = scene.store()
+    K = {i: scene.cameras[i].K for i in store.sets}
+    newly, results = localize_all(model, store, _NoGraph(), K)
+    qs = [int(q) for q in z["queries"]]
+    assert newly == [q for q in qs if str(z[f"q{q}_status"]) == "ok"]
+    for r in results:
+        q = r.image_id
+        assert [tuple(c) for c in z[f"q{q}_corr"].tolist()] == r.correspondences
+        np.testing.assert_allclose(r.pose.R, z[f"q{q}_R"], atol=1e-6)
+        np.testing.assert_allclose(r.pose.t, z[f"q{q}_t"], atol=1e-6, rtol=1e-6)
+        assert r.inliers == int(z[f"q{q}_mask"].sum())
+        assert model.is_registered(q)
+    assert model.stage_tag == "after_localize(1)"
+
+
+def test_localize_all_raises_like_reference_on_overflow():
+    from paper_1512_06235_b200 import scenes
+    from paper_1512_06235_b200.localize import localize_all
+
+    kw, scene, snap, z = load_localize("localize_c2mini.npz")
+    model = scenes.snapshot_to_model(scene, snap)
+    store = scene.store()
+    store.sets = {q: store.sets[q] for q in list(z["registered"]) + [int(x) for x in z["queries"]]}
+    K = {i: scene.cameras[i].K for i in store.sets}
+    with pytest.raises(OverflowError):
+        localize_all(model, store, _NoGraph(), K)
