@@ -217,6 +217,20 @@ int msfm_pnp_refit(const double* d_X, const double* d_uv, const int64_t* d_off, 
                    double* d_t, uint8_t* d_mask, int32_t* d_n_inliers, int32_t* d_ok,
                    void* stream);
 
+/* ------------------------------------------------------------------------
+ * Multi-view DLT triangulation (geometry.py:276-357) of n_tracks tracks.
+ * Cameras: K [c][9], R [c][9], t [c][3] (x ~ K (R X + t)).  Track k has the
+ * observations [ptr[k], ptr[k+1]): camera index d_cam[i], pixel d_pix[i][2].
+ * Output X [k][3], mean reprojection error err [k], status [k]:
+ *   1 accepted, 0 rejected by a gate (the reference returns None),
+ *  -1 DegenerateGeometryError (shared centre / parallel rays),
+ *  -2 InsufficientDataError (< 2 observations).
+ * ---------------------------------------------------------------------- */
+int msfm_triangulate_batch(const double* d_K, const double* d_R, const double* d_t,
+                           int32_t n_tracks, const int64_t* d_ptr, const int32_t* d_cam,
+                           const double* d_pix, double max_error, double min_angle_deg,
+                           double* d_X, double* d_err, int32_t* d_status, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -61,6 +61,8 @@ _SIGS = {
                                            ctypes.c_double, VP, VP, VP]),
     "msfm_pnp_refit": (ctypes.c_int, [VP, VP, VP, VP, ctypes.c_int32, VP, VP, ctypes.c_double,
                                       ctypes.c_int32, ctypes.c_int32, VP, VP, VP, VP, VP, VP]),
+    "msfm_triangulate_batch": (ctypes.c_int, [VP, VP, VP, ctypes.c_int32, VP, VP, VP,
+                                              ctypes.c_double, ctypes.c_double, VP, VP, VP, VP]),
     "msfm_guided_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int32, VP,
                                                       ctypes.POINTER(MatchParams)]),
     "msfm_guided_match": (ctypes.c_int, [ctypes.POINTER(Bank), ctypes.POINTER(Grids),
