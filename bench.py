@@ -186,28 +186,21 @@ def run_reference(args, rank, world):
 
 
 def gather_to_rank0(res, world, dev):
-    """Variable-length gather of this rank's match arrays to rank 0 (NCCL)."""
+    """Variable-length gather of this rank's matches (device-packed rows) over NCCL."""
     import torch
-    import torch.distributed as dist
+
+    from paper_1512_06235_b200.dist import gather_rows
 
     cnt = res.count.to(torch.int64)
     qoff = torch.from_numpy(res.qoff[:-1]).to(dev)
-    # compact this rank's per-pair segments into one contiguous block
+    # compact this rank's per-pair segments into one contiguous block on the device
     idx_pairs = torch.repeat_interleave(torch.arange(cnt.numel(), device=dev), cnt)
     starts = torch.cumsum(cnt, 0) - cnt
     pos = torch.arange(idx_pairs.numel(), device=dev) - starts[idx_pairs] + qoff[idx_pairs]
-    packed = torch.stack([res.q[pos].to(torch.int64), res.t[pos].to(torch.int64),
-                          res.dist[pos].view(torch.int32).to(torch.int64),
-                          res.ratio[pos].view(torch.int32).to(torch.int64)], 1)
-    m = torch.tensor([packed.shape[0]], device=dev, dtype=torch.int64)
-    sizes = [torch.zeros_like(m) for _ in range(world)]
-    dist.all_gather(sizes, m)
-    mx = int(max(s.item() for s in sizes))
-    buf = torch.zeros((mx, 4), dtype=torch.int64, device=dev)
-    buf[:packed.shape[0]] = packed
-    out = [torch.zeros_like(buf) for _ in range(world)]
-    dist.all_gather(out, buf)
-    return out, sizes
+    rows = torch.stack([idx_pairs, res.q[pos].to(torch.int64), res.t[pos].to(torch.int64),
+                        res.dist[pos].view(torch.int32).to(torch.int64),
+                        res.ratio[pos].view(torch.int32).to(torch.int64)], 1)
+    return gather_rows(rows, world)
 
 
 def run_b200(args, rank, world):
