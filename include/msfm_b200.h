@@ -42,6 +42,10 @@ int64_t msfm_launch_count(void);
  * read() synchronises on the recorded events and sums their durations. */
 int msfm_profile_enable(int on);
 int msfm_profile_read(const char* kernel_name, double* total_ms, int64_t* launches);
+/* Diagnostics: enable(1) allocates 16 device counters the matcher increments
+ * (super-groups, members, gathered, passing, sure, unsure, exact-C' tests,
+ * m-tiles, groups, rounds); read copies them to out16 and resets; enable(0) frees. */
+int msfm_debug_counters(int enable, int64_t* out16);
 
 /* ------------------------------------------------------------------------
  * Feature bank: all images' features concatenated (SoA, HBM-resident).

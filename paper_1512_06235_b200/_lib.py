@@ -41,6 +41,7 @@ _SIGS = {
     "msfm_version": (ctypes.c_int, []),
     "msfm_launch_count": (ctypes.c_int64, []),
     "msfm_profile_enable": (ctypes.c_int, [ctypes.c_int]),
+    "msfm_debug_counters": (ctypes.c_int, [ctypes.c_int, VP]),
     "msfm_profile_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double),
                                          ctypes.POINTER(ctypes.c_int64)]),
     "msfm_feature_norms": (ctypes.c_int, [VP, ctypes.c_int64, VP, VP]),

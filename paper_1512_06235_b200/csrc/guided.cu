@@ -17,6 +17,7 @@
 //                      fp32 band prefilter (+exact fp64 fallback), top-2, ratio, dedupe
 //   compact  CTA/pair   ordered compaction of dedupe winners
 #include <math.h>
+#include <stdlib.h>
 
 #include <vector>
 
@@ -28,7 +29,7 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr unsigned long long EMPTY = 0xffffffffffffffffull;
 constexpr int CAP = 512;       // candidates per round (9-bit local index in keys)
-constexpr int WARPS = 8;       // match kernel warps per CTA
+constexpr int WARPS = 4;       // match kernel warps per CTA
 constexpr unsigned NONE = 0xffffffffu;
 
 // ------------------------------------------------------------------ geometry
@@ -294,23 +295,38 @@ int exclusive_scan(int32_t* data, int64_t n, int32_t* copy, int32_t* bsum, cudaS
 // warp-per-group match kernel starts from fp32 values and never divides in fp64.
 struct GroupRec {
     int p, rep, cnt, moff;                 // chunk-local pair, rep slot, members, member offset
-    float ar, br, cr, R;                   // rep line (fp32) and strip half-width
-    float hsure, pbx, pby, dirx;           // sure-in-C' radius, padded segment origin (pb) + dir
-    float diry, len, spacing, invK;
-    float dxf, dyf, slack, invD;
-    int K, horiz, rlo, rhi;                // K<0: C' empty; strip orientation and bucket-row range
-    float alpha, beta, inv_alpha, Pmax;    // strip row math in the chosen orientation
+    float ar, br, cr, hsure;               // rep line (fp32), sure-in-C' radius
+    float pbx, pby, dirx, diry;            // padded segment origin (pb) and direction
+    float len, spacing, invK, invD;
+    float dxf, dyf, slack, maxdev;         // maxdev: max member-band deviation from the rep line
+    int K, pad1, pad2, pad3;               // K<0: the rep line misses the padded image (C' empty)
     double pax, pay, pbx64, pby64;         // exact sample interpolation (guided.py:187)
     double sl0, sl1, sl2, spare;           // singleton member's own (dgemv) line
 };
 
-// Per-member epilogue constants (written by prep_kernel, indexed like members[]).
+// Per-member epilogue constants (prep_kernel), indexed like members[].
 struct MemberRec {
     float a, b, c, lo;    // member line (fp32) and sure-in-band threshold d - eps
     float hi;             // d + eps: above it the fp32 value is surely out of band
     unsigned qn9;         // |q|^2 << 9
-    int fid, slot;        // query feature id, chunk-local slot
+    int fid;              // query feature id
+    int slotgi;           // chunk-local slot | (group index within its super-group << 24)
 };
+
+// A super-group: up to SG_MEMBERS consecutive members (groups ordered by line
+// angle) that share one strip gather and full n8 tiles (sg_prep_kernel).
+struct alignas(16) SGRec {
+    int p, m0, mcnt, g0;                   // pair, member range, first group (dense gid)
+    int gcnt, horiz, rlo, rhi;             // groups, strip orientation, bucket-row range
+    float ar, br, cr, R;                   // base line (fp32) and strip half-width
+    float delta, hsure, border, invD;      // max rep-vs-base deviation, sure radius, border
+    float alpha, beta, inv_alpha, Pmax;    // strip row math in the chosen orientation
+    float W, H, pad0, pad1;
+};
+
+constexpr int SG_MEMBERS = 16;
+constexpr float SG_TAU = 16.0f;
+constexpr int SG_MAX_GROUPS = 16;
 
 struct ChunkArgs {
     // bank
@@ -321,20 +337,25 @@ struct ChunkArgs {
     const int32_t* rstart; const int32_t* cstart; const int32_t* rmem; const int32_t* cmem;
     double D, d;
     float ratio, single_cap;
+    int stats_mode;              // 1: one super-group per group (exact SearchStats)
+    float sg_tau;                // super-group line tolerance (px)
     // pairs
     const int32_t* pair_q; const int32_t* pair_t; const double* pair_F;
     const int64_t* qlist_off; const int32_t* qlist;
     int32_t p0, npairs; int64_t qbase;
     // chunk workspace
-    int64_t* tab_off; int64_t* tbase; int32_t* ngroups; int32_t* gstart;
+    int64_t* tab_off; int64_t* tbase; int32_t* ngroups; int32_t* gstart; int32_t* nmem;
+    int32_t* sgstart; int32_t* sg_next; int32_t* nsg;
     unsigned long long* tab_key; unsigned* tab_rep; unsigned* tab_cnt;
     int32_t* q_tab; double* q_line;
-    int4* grec; int32_t* gfill; int32_t* members; GroupRec* grp; MemberRec* mrec;
+    int2* gtmp; float* gkey; int32_t* gpos; float4* gline; float4* gend; int2* sglist;
+    int4* grec; int32_t* gfill; int32_t* members; GroupRec* grp; MemberRec* mrec; SGRec* sg;
     unsigned long long* mstate;  // per member slot: best (d2<<32 | tid)
     unsigned* mstate2;           // per member slot: second d2
     int32_t* res_tid; float* res_dist; float* res_ratio;
     unsigned long long* dedupe;
     unsigned long long* stats;   // [2*n_pairs] (global pair index) or null
+    unsigned long long* dbg;     // optional workload counters (msfm_debug_counters)
     // outputs
     int32_t* out_q; int32_t* out_t; float* out_dist; float* out_ratio; int32_t* out_count;
 };
@@ -393,7 +414,7 @@ __global__ void __launch_bounds__(256) lines_kernel(ChunkArgs a) {
         a.res_tid[s0 + i] = -1;
         a.gfill[s0 + i] = 0;
     }
-    if (threadIdx.x == 0) a.ngroups[p] = 0;
+    if (threadIdx.x == 0) { a.ngroups[p] = 0; a.nmem[p] = 0; }
     __syncthreads();
     double F[9];
 #pragma unroll
@@ -434,13 +455,23 @@ __global__ void __launch_bounds__(256) lines_kernel(ChunkArgs a) {
     }
 }
 
+// Groups of a pair: compact the occupied hash slots, then order the groups by
+// the angle of their representative line (adaptive 4096-bucket counting sort)
+// so consecutive groups have nearly identical lines, and lay out their member
+// ranges in that order.  The order only affects how members are packed into
+// super-groups, never any result.
+constexpr int GB = 4096;
 __global__ void __launch_bounds__(256) groups_kernel(ChunkArgs a) {
     __shared__ int sm[256 / 32 + 1];
+    __shared__ int hist[GB];
+    __shared__ float fmin_s[8], fmax_s[8];
     const int p = blockIdx.x, pg = a.p0 + p;
     const int64_t s0 = a.qlist_off[pg] - a.qbase;
     const int64_t t0 = a.tab_off[p];
     const int tsize = (int)(a.tab_off[p + 1] - t0);
-    int gcarry = 0, mcarry = 0;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int gcarry = 0;
+    float lo = 1e30f, hi = -1e30f;
     for (int e0 = 0; e0 < tsize; e0 += 256) {
         const int e = e0 + threadIdx.x;
         bool occ = false;
@@ -449,32 +480,165 @@ __global__ void __launch_bounds__(256) groups_kernel(ChunkArgs a) {
             occ = a.tab_key[t0 + e] != EMPTY;
             if (occ) { cnt = a.tab_cnt[t0 + e]; rep = a.tab_rep[t0 + e]; }
         }
-        int gtot, mtot;
-        int lg = block_exclusive_scan<256>(occ ? 1 : 0, &gtot, sm);
-        int mo = block_exclusive_scan<256>((int)cnt, &mtot, sm);
+        int gtot;
+        const int lg = block_exclusive_scan<256>(occ ? 1 : 0, &gtot, sm);
         if (occ) {
             const int g = gcarry + lg;
-            a.grec[s0 + g] = make_int4((int)rep, (int)cnt, (int)(s0 + mcarry + mo), 0);
+            a.gtmp[s0 + g] = make_int2((int)rep, (int)cnt);
+            const double* L = a.q_line + 3 * (s0 + rep);
+            float la = (float)L[0], lb = (float)L[1];
+            if (la < 0.f || (la == 0.f && lb < 0.f)) { la = -la; lb = -lb; }
+            const float ang = atan2f(lb, la);
+            a.gkey[s0 + g] = ang;
+            lo = fminf(lo, ang);
+            hi = fmaxf(hi, ang);
             a.tab_rep[t0 + e] = (unsigned)g;
         }
         gcarry += gtot;
-        mcarry += mtot;
     }
-    if (threadIdx.x == 0) a.ngroups[p] = gcarry;
+    const int ng = gcarry;
+    for (int o = 16; o; o >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(FULL, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(FULL, hi, o));
+    }
+    if (lane == 0) { fmin_s[wid] = lo; fmax_s[wid] = hi; }
+    for (int b = threadIdx.x; b < GB; b += 256) hist[b] = 0;
+    __syncthreads();
+    lo = fmin_s[0]; hi = fmax_s[0];
+    for (int w = 1; w < 8; w++) { lo = fminf(lo, fmin_s[w]); hi = fmaxf(hi, fmax_s[w]); }
+    const float scale = (float)GB / fmaxf(hi - lo, 1e-20f);
+    for (int g = threadIdx.x; g < ng; g += 256) {
+        const int b = min(GB - 1, max(0, (int)((a.gkey[s0 + g] - lo) * scale)));
+        atomicAdd(&hist[b], 1);
+    }
+    __syncthreads();
+    // exclusive scan of the histogram (16 buckets per thread)
+    {
+        int v[GB / 256];
+        int s = 0;
+        for (int k = 0; k < GB / 256; k++) { v[k] = hist[threadIdx.x * (GB / 256) + k]; s += v[k]; }
+        int tot;
+        int ex = block_exclusive_scan<256>(s, &tot, sm);
+        for (int k = 0; k < GB / 256; k++) { hist[threadIdx.x * (GB / 256) + k] = ex; ex += v[k]; }
+    }
+    __syncthreads();
+    for (int g = threadIdx.x; g < ng; g += 256) {
+        const int b = min(GB - 1, max(0, (int)((a.gkey[s0 + g] - lo) * scale)));
+        a.gpos[s0 + g] = atomicAdd(&hist[b], 1);
+    }
+    __syncthreads();
+    int mcarry = 0;
+    // write grec in sorted order (scatter by gpos), then scan counts in that order
+    for (int g = threadIdx.x; g < ng; g += 256) {
+        const int2 r = a.gtmp[s0 + g];
+        a.grec[s0 + a.gpos[s0 + g]] = make_int4(r.x, r.y, 0, 0);
+    }
+    __syncthreads();
+    for (int i0 = 0; i0 < ng; i0 += 256) {
+        const int i = i0 + threadIdx.x;
+        const int cnt = i < ng ? a.grec[s0 + i].y : 0;
+        int tot;
+        const int ex = block_exclusive_scan<256>(cnt, &tot, sm);
+        if (i < ng) a.grec[s0 + i].z = (int)(s0 + mcarry + ex);
+        mcarry += tot;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < tsize; e += 256) {
+        if (a.tab_key[t0 + e] != EMPTY) a.tab_rep[t0 + e] = (unsigned)a.gpos[s0 + a.tab_rep[t0 + e]];
+    }
+    // boundary endpoints of every representative line (in sorted order)
+    const int ti = a.pair_t[pg];
+    const double W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1];
+    for (int g = threadIdx.x; g < ng; g += 256) {
+        const int4 gr = a.grec[s0 + g];
+        const double* L = a.q_line + 3 * (s0 + gr.x);
+        const double l[3] = {L[0], L[1], L[2]};
+        double pa[2] = {0, 0}, pb[2] = {0, 0};
+        clip_batch(l, W, H, pa, pb);
+        a.gline[s0 + g] = make_float4((float)l[0], (float)l[1], (float)l[2], 0.f);
+        a.gend[s0 + g] = make_float4((float)pa[0], (float)pa[1], (float)pb[0], (float)pb[1]);
+    }
+    __syncthreads();
+    // super-groups: greedy walk over the angle-ordered groups; a super-group holds
+    // at most SG_MEMBERS members and closes when the next group's line leaves the
+    // base line by more than SG_TAU px inside the image (stats mode: one per group)
+    if (threadIdx.x < 32) {
+        int nsg = 0;
+        if (a.stats_mode) {
+            for (int g = lane; g < ng; g += 32) {
+                const int4 gr = a.grec[s0 + g];
+                a.sglist[s0 + g] = make_int2(gr.z, gr.y);
+            }
+            nsg = ng;
+        } else {
+            float ba = 0.f, bb = 0.f, bc = 0.f;
+            int cur_m0 = 0, cur_cnt = 0;
+            bool open = false;
+            for (int g0 = 0; g0 < ng; g0 += 32) {
+                const int g = g0 + lane;
+                int4 gr = make_int4(0, 0, 0, 0);
+                float4 ln = make_float4(0.f, 0.f, 0.f, 0.f), en = ln;
+                if (g < ng) { gr = a.grec[s0 + g]; ln = a.gline[s0 + g]; en = a.gend[s0 + g]; }
+                const int lim = min(32, ng - g0);
+                for (int i = 0; i < lim; i++) {
+                    const int cnt = __shfl_sync(FULL, gr.y, i), moff = __shfl_sync(FULL, gr.z, i);
+                    const float la = __shfl_sync(FULL, ln.x, i), lb = __shfl_sync(FULL, ln.y, i);
+                    const float lc = __shfl_sync(FULL, ln.z, i);
+                    const float pax = __shfl_sync(FULL, en.x, i), pay = __shfl_sync(FULL, en.y, i);
+                    const float pbx = __shfl_sync(FULL, en.z, i), pby = __shfl_sync(FULL, en.w, i);
+                    bool fits = false;
+                    if (open && cur_cnt < SG_MEMBERS) {
+                        const float d1 = fabsf(fmaf(ba, pax, fmaf(bb, pay, bc)));
+                        const float d2 = fabsf(fmaf(ba, pbx, fmaf(bb, pby, bc)));
+                        fits = fmaxf(d1, d2) <= a.sg_tau;
+                    }
+                    int rem = cnt, pos = moff;
+                    if (fits) {
+                        const int take = min(SG_MEMBERS - cur_cnt, rem);
+                        cur_cnt += take; rem -= take; pos += take;
+                    }
+                    while (rem > 0) {
+                        if (open) {
+                            if (lane == 0) a.sglist[s0 + nsg] = make_int2(cur_m0, cur_cnt);
+                            nsg++;
+                        }
+                        open = true;
+                        ba = la; bb = lb; bc = lc;
+                        const int take = min(SG_MEMBERS, rem);
+                        cur_m0 = pos; cur_cnt = take; rem -= take; pos += take;
+                    }
+                }
+            }
+            if (open) {
+                if (lane == 0) a.sglist[s0 + nsg] = make_int2(cur_m0, cur_cnt);
+                nsg++;
+            }
+        }
+        if (lane == 0) a.nsg[p] = nsg;
+    }
+    if (threadIdx.x == 0) { a.ngroups[p] = ng; a.nmem[p] = mcarry; }
 }
 
 __global__ void gscan_kernel(ChunkArgs a) {
     __shared__ int sm[SCAN_T / 32 + 1];
-    int carry = 0;
+    int carry = 0, carry_sg = 0;
     for (int b0 = 0; b0 < a.npairs; b0 += SCAN_T) {
         int p = b0 + threadIdx.x;
         int v = p < a.npairs ? a.ngroups[p] : 0;
-        int total;
+        int vs = 0;
+        if (p < a.npairs) vs = a.nsg[p];
+        int total, total_sg;
         int ex = block_exclusive_scan<SCAN_T>(v, &total, sm);
-        if (p < a.npairs) a.gstart[p] = carry + ex;
+        int exs = block_exclusive_scan<SCAN_T>(vs, &total_sg, sm);
+        if (p < a.npairs) { a.gstart[p] = carry + ex; a.sgstart[p] = carry_sg + exs; }
         carry += total;
+        carry_sg += total_sg;
     }
-    if (threadIdx.x == 0) a.gstart[a.npairs] = carry;
+    if (threadIdx.x == 0) {
+        a.gstart[a.npairs] = carry;
+        a.sgstart[a.npairs] = carry_sg;
+        *a.sg_next = 0;
+    }
 }
 
 __global__ void __launch_bounds__(256) scatter_kernel(ChunkArgs a) {
@@ -502,8 +666,8 @@ __device__ __forceinline__ int find_pair(const int32_t* gstart, int npairs, int 
     return lo;
 }
 
-// Upper bound of |dist_m(f) - dist_rep(f)| over the image rectangle restricted
-// to the member's band (|dist_m| <= d + 0.5): the difference is affine, so its
+// Upper bound of |dist_m(f) - dist_r(f)| over the image rectangle restricted to
+// the member's band (|dist_m| <= d + 0.5): the difference is affine, so its
 // maximum over that convex polygon sits at one of its vertices.
 __device__ double band_deviation(const double m[3], const double r[3], double W, double H,
                                  double d) {
@@ -516,7 +680,6 @@ __device__ double band_deviation(const double m[3], const double r[3], double W,
         if (fabs(dm) <= B) dev = fmax(dev, fabs(da * cx[k] + db * cy[k] + dc));
     }
     for (int s = -1; s <= 1; s += 2) {
-        // m0 x + m1 y + m2 = s*B  intersected with the four edges
         if (fabs(m[1]) > 1e-12) {
             for (int e = 0; e < 2; e++) {
                 double x = e ? W : 0.0;
@@ -535,6 +698,17 @@ __device__ double band_deviation(const double m[3], const double r[3], double W,
     return dev;
 }
 
+// |dist_g - dist_base| over the whole image rectangle (affine -> max at a corner)
+__device__ double rect_deviation(const double g[3], const double r[3], double W, double H) {
+    const double da = g[0] - r[0], db = g[1] - r[1], dc = g[2] - r[2];
+    double dev = fabs(dc);
+    dev = fmax(dev, fabs(da * W + dc));
+    dev = fmax(dev, fabs(db * H + dc));
+    dev = fmax(dev, fabs(da * W + db * H + dc));
+    return dev;
+}
+
+// Per group: the C' geometry of its representative line + member constants.
 __global__ void __launch_bounds__(128) prep_kernel(ChunkArgs a, int max_groups) {
     const int gid = blockIdx.x * blockDim.x + threadIdx.x;
     const int total = a.gstart[a.npairs];
@@ -545,14 +719,15 @@ __global__ void __launch_bounds__(128) prep_kernel(ChunkArgs a, int max_groups) 
     const int64_t s0 = q0 - a.qbase;
     const int4 g = a.grec[s0 + (gid - a.gstart[p])];
     const int ti = a.pair_t[pg], qi = a.pair_q[pg];
-    const int Wi = a.img_wh[2 * ti], Hi = a.img_wh[2 * ti + 1];
-    const double W = Wi, H = Hi, D = a.D, d = a.d;
+    const double W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1], D = a.D, d = a.d;
     const int64_t qoff = a.img_off[qi];
     const double* rl = a.q_line + 3 * (s0 + g.x);
     const double r[3] = {rl[0], rl[1], rl[2]};
     GroupRec o;
     o.p = p; o.rep = (int)(s0 + g.x); o.cnt = g.y; o.moff = g.z;
     o.sl0 = r[0]; o.sl1 = r[1]; o.sl2 = r[2]; o.spare = 0.0;
+    o.pad1 = o.pad2 = o.pad3 = 0;
+    double maxdev = 0.0;
     double pa[2] = {0, 0}, pb[2] = {0, 0}, len = 0.0;
     o.K = -1;
     if (clip_scalar(r[0], r[1], r[2], W, H, d, pa, pb)) {
@@ -561,9 +736,6 @@ __global__ void __launch_bounds__(128) prep_kernel(ChunkArgs a, int max_groups) 
         o.K = (int)(K < 1 ? 1 : K);
     }
     o.pax = pa[0]; o.pay = pa[1]; o.pbx64 = pb[0]; o.pby64 = pb[1];
-    // members: own line (dgemv rounding for a singleton, guided.py:443-446), band
-    // deviation from the rep line, fp32 epilogue constants
-    double dev = 0.0;
     double F[9];
     if (g.y == 1)
         for (int j = 0; j < 9; j++) F[j] = a.pair_F[9 * (int64_t)pg + j];
@@ -572,6 +744,7 @@ __global__ void __launch_bounds__(128) prep_kernel(ChunkArgs a, int max_groups) 
         const int fid = a.qlist[a.qbase + slot];
         double m[3];
         if (g.y == 1) {
+            // a singleton's own band uses the dgemv-rounded line (guided.py:443-446, m == 1)
             const float2 p2 = a.xy[qoff + fid];
             epiline(F, (double)p2.x, (double)p2.y, true, m);
             double nrm = fmax(np_hypot(m[0], m[1]), 1e-15);
@@ -581,7 +754,7 @@ __global__ void __launch_bounds__(128) prep_kernel(ChunkArgs a, int max_groups) 
             const double* ml = a.q_line + 3 * (int64_t)slot;
             m[0] = ml[0]; m[1] = ml[1]; m[2] = ml[2];
         }
-        dev = fmax(dev, band_deviation(m, r, W, H, d));
+        maxdev = fmax(maxdev, band_deviation(m, r, W, H, d));
         MemberRec mr;
         mr.a = (float)m[0]; mr.b = (float)m[1]; mr.c = (float)m[2];
         const float eps = (float)((fabs(m[0]) * W + fabs(m[1]) * H + fabs(m[2])) * 0x1p-20) + 1e-6f;
@@ -589,13 +762,11 @@ __global__ void __launch_bounds__(128) prep_kernel(ChunkArgs a, int max_groups) 
         mr.hi = (float)d + eps;
         mr.qn9 = (unsigned)a.norm2[qoff + fid] << 9;
         mr.fid = fid;
-        mr.slot = slot;
+        mr.slotgi = slot;
         a.mrec[g.z + j] = mr;
     }
-    const double reach = 2.0 * sqrt(2.0) * D + 0.05;   // C' never reaches further
-    double R = d + dev + 0.05;
-    R = R < reach ? R : reach;
-    o.ar = (float)r[0]; o.br = (float)r[1]; o.cr = (float)r[2]; o.R = (float)R;
+    o.ar = (float)r[0]; o.br = (float)r[1]; o.cr = (float)r[2];
+    o.maxdev = (float)(maxdev + 0.05);
     const double hs2 = D * D - 0.25 * d * d;
     o.hsure = hs2 > 0 ? (float)(sqrt(hs2) - 0.075) : -1.0f;
     o.pbx = (float)pb[0]; o.pby = (float)pb[1];
@@ -607,7 +778,85 @@ __global__ void __launch_bounds__(128) prep_kernel(ChunkArgs a, int max_groups) 
     o.dxf = (float)(pa[0] - pb[0]); o.dyf = (float)(pa[1] - pb[1]);
     o.slack = (float)(4e-6 * (W + H + 4.0 * d) / D) + 1e-4f;
     o.invD = (float)(1.0 / D);
-    // strip rows: buckets along the minor direction of the line
+    a.grp[gid] = o;
+}
+
+// Per super-group: member window, its groups, the base line and strip.
+__global__ void __launch_bounds__(128) sg_prep_kernel(ChunkArgs a, int max_sg) {
+    const int sid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int total = a.sgstart[a.npairs];
+    if (sid >= total || sid >= max_sg) return;
+    const int p = find_pair(a.sgstart, a.npairs, sid);
+    const int ls = sid - a.sgstart[p];
+    const int pg = a.p0 + p;
+    const int64_t s0 = a.qlist_off[pg] - a.qbase;
+    const int ng = a.ngroups[p];
+    const int ti = a.pair_t[pg];
+    const double W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1], D = a.D, d = a.d;
+    SGRec o;
+    o.p = p;
+    int lg0, lg1;                       // group range [lg0, lg1] (sorted order)
+    const int2 sgm = a.sglist[s0 + ls];
+    o.m0 = sgm.x; o.mcnt = sgm.y;
+    if (a.stats_mode) {
+        lg0 = lg1 = ls;
+    } else {
+        // groups containing the first and last member (member offsets ascend with lg)
+        auto group_of = [&](int m) {
+            int lo = 0, hi = ng - 1;
+            while (lo < hi) {
+                int mid = (lo + hi + 1) >> 1;
+                if (a.grec[s0 + mid].z <= m) lo = mid; else hi = mid - 1;
+            }
+            return lo;
+        };
+        lg0 = group_of(o.m0);
+        lg1 = group_of(o.m0 + o.mcnt - 1);
+    }
+    o.g0 = a.gstart[p] + lg0;
+    o.gcnt = lg1 - lg0 + 1;
+    // base line: the middle group's representative
+    const int gb = a.gstart[p] + (lg0 + lg1) / 2;
+    const GroupRec& B = a.grp[gb];
+    const double* bl = a.q_line + 3 * (int64_t)B.rep;
+    const double r[3] = {bl[0], bl[1], bl[2]};
+    bool all_k = true;
+    double dev = 0.0;
+    for (int j = 0; j < o.mcnt; j++) {
+        const int pos = o.m0 + j;
+        // group of this member within the super-group
+        int gi = 0;
+        while (gi + 1 < o.gcnt && a.grp[o.g0 + gi + 1].moff <= pos) gi++;
+        const GroupRec& G = a.grp[o.g0 + gi];
+        MemberRec& mr = a.mrec[pos];
+        const int slot = mr.slotgi & 0xFFFFFF;
+        double m[3];
+        if (G.cnt == 1) { m[0] = G.sl0; m[1] = G.sl1; m[2] = G.sl2; }
+        else {
+            const double* ml = a.q_line + 3 * (int64_t)slot;
+            m[0] = ml[0]; m[1] = ml[1]; m[2] = ml[2];
+        }
+        dev = fmax(dev, band_deviation(m, r, W, H, d));
+        mr.slotgi = slot | (gi << 24);
+    }
+    const double R = d + dev + 0.05;
+    double delta = 0.0;
+    for (int g = o.g0; g < o.g0 + o.gcnt; g++) {
+        const GroupRec& G = a.grp[g];
+        const double* gl = a.q_line + 3 * (int64_t)G.rep;
+        const double gr[3] = {gl[0], gl[1], gl[2]};
+        // |dist_g - dist_base| over the strip |dist_base| <= R inside the image
+        delta = fmax(delta, band_deviation(r, gr, W, H, R));
+        all_k = all_k && G.K >= 0;
+    }
+    o.ar = (float)r[0]; o.br = (float)r[1]; o.cr = (float)r[2]; o.R = (float)R;
+    const double hs2 = D * D - 0.25 * d * d;
+    const double hs = hs2 > 0 ? sqrt(hs2) - 0.075 : -1.0;
+    o.hsure = (float)hs;
+    o.delta = all_k ? (float)(delta + 0.01) : 1e30f;
+    o.border = (float)(fmax(0.0, hs - d) + 0.05);
+    o.invD = (float)(1.0 / D);
+    o.W = (float)W; o.H = (float)H; o.pad0 = o.pad1 = 0.f;
     const bool horiz = fabs(r[1]) >= fabs(r[0]);
     const double al = horiz ? r[0] : r[1], be = horiz ? r[1] : r[0];
     const double Pm = horiz ? W : H, Qm = horiz ? H : W;
@@ -622,10 +871,10 @@ __global__ void __launch_bounds__(128) prep_kernel(ChunkArgs a, int max_groups) 
     o.alpha = (float)al; o.beta = (float)be;
     o.inv_alpha = fabs(al) > 1e-6 ? (float)(1.0 / al) : 0.f;
     o.Pmax = (float)Pm;
-    a.grp[gid] = o;
+    a.sg[sid] = o;
 }
 
-// mma.sync m16n8k32 u8 x u8 -> s32 (legacy IMMA path; rows = candidates, cols = members)
+// mma.sync m16n8k32 u8 x u8 -> s32 (rows = candidates, cols = members)
 __device__ __forceinline__ void mma_u8(int (&c)[4], unsigned a0, unsigned a1, unsigned a2,
                                        unsigned a3, unsigned b0, unsigned b1) {
     asm volatile(
@@ -647,7 +896,7 @@ __device__ __forceinline__ void top2_merge(unsigned& b1, unsigned& b2, unsigned 
     b2 = min(hi, min(b2, o2));
 }
 
-// Exact subcell of sample k of the rep line (guided.py:173-187 + cell_indices):
+// Exact subcell of sample k of a rep line (guided.py:173-187 + cell_indices):
 // fp32 interpolation, exact fp64 evaluation only near a subcell boundary.
 __device__ __forceinline__ void sample_subcell(const GroupRec& G, double D, int k, int& u, int& v) {
     const float t = (float)k * G.invK;
@@ -666,7 +915,7 @@ __device__ __forceinline__ void sample_subcell(const GroupRec& G, double D, int 
     v = exact_subcell(ey, D);
 }
 
-// f in C'(rep) <=> some sample subcell is within Chebyshev distance 1 of f's.
+// f in C'(rep): some sample subcell is within Chebyshev distance 1 of f's.
 __device__ bool in_cprime_exact(const GroupRec& G, double D, float fx, float fy, int fu, int fv) {
     if (G.K < 0) return false;
     const float tau = (fx - G.pbx) * G.dirx + (fy - G.pby) * G.diry;
@@ -684,12 +933,26 @@ __device__ bool in_cprime_exact(const GroupRec& G, double D, float fx, float fy,
     return false;
 }
 
-struct WarpSmem {
+// C' membership of f for group G, using the sure zone first
+__device__ __forceinline__ bool in_cprime(const ChunkArgs& a, const GroupRec& G, const SGRec& S,
+                                          float fx, float fy, int64_t toff, int f) {
+    if (G.K < 0) return false;
+    const float dg = fabsf(fmaf(G.ar, fx, fmaf(G.br, fy, G.cr)));
+    if (dg <= S.hsure && fx >= S.border && fx <= S.W - S.border && fy >= S.border &&
+        fy <= S.H - S.border)
+        return true;
+    const int su = a.sub[toff + f];
+    return in_cprime_exact(G, a.D, fx, fy, (short)(su & 0xffff), su >> 16);
+}
+
+struct alignas(16) WarpSmem {
     unsigned short list[CAP];    // candidate feature ids (target-local)
-    unsigned short ulist[CAP];   // positions whose C' membership is not yet decided
-    unsigned valid[CAP / 32];    // candidate in C'
+    unsigned short cmask[CAP];   // per candidate: groups (bit gi) whose C' contains it
+    unsigned short ulist[CAP];   // positions still to decide
+    unsigned sure[CAP / 32];     // candidate in C' of every group of the super-group
     unsigned anyb[CAP / 8];      // stats: candidate inside some member band
-    GroupRec grec;               // this warp's group context (broadcast reads)
+    SGRec sg;                    // this warp's super-group (broadcast reads)
+    int gbeg[SG_MAX_GROUPS + 1]; // member range of each group within the super-group
 };
 
 // the reference's float64 band value for one (member, target) element, guided.py:447
@@ -706,122 +969,181 @@ __device__ __forceinline__ bool member_band(const ChunkArgs& a, const GroupRec& 
     if (v <= M.lo) return true;
     if (v > M.hi) return false;
     if (G.cnt == 1) return band_exact(G.sl0, G.sl1, G.sl2, true, x, y, a.d);
-    const double* L = a.q_line + 3 * (int64_t)M.slot;
+    const double* L = a.q_line + 3 * (int64_t)(M.slotgi & 0xFFFFFF);
     return band_exact(L[0], L[1], L[2], false, x, y, a.d);
 }
 
 template <bool STATS>
-__device__ void process_round(const ChunkArgs& a, const GroupRec& G, WarpSmem& S, int n,
-                              int64_t toff, int64_t qoff, bool first_round, int& cols_total) {
+__device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t toff, int64_t qoff,
+                              bool first_round, int& cols_total) {
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-    const double D = a.D;
-    const int m = G.cnt;
-    const MemberRec* MR = a.mrec + G.moff;
-    // ---- C' membership of the candidates outside the sure zone that some member
-    //      band actually contains (compacted so every lane does useful work)
+    const SGRec& SG = S.sg;
+    const int m = SG.mcnt;
+    const MemberRec* MR = a.mrec + SG.m0;
+    const unsigned all_groups = (1u << SG.gcnt) - 1u;
+    // ---- per-group C' bits of the candidates not surely inside every group's C'
     int nu = 0;
     for (int j0 = 0; j0 < n; j0 += 32) {
         const int j = j0 + lane;
-        const bool need = j < n && !((S.valid[j >> 5] >> (j & 31)) & 1u);
+        const bool sure = j < n && ((S.sure[j >> 5] >> (j & 31)) & 1u);
+        if (j < n) S.cmask[j] = sure ? (unsigned short)all_groups : 0;
+        const bool need = j < n && !sure;
         const unsigned bal = __ballot_sync(FULL, need);
         if (need) S.ulist[nu + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)j;
         nu += __popc(bal);
     }
     __syncwarp();
+    if (a.dbg && lane == 0) {
+        atomicAdd(&a.dbg[5], (unsigned long long)nu);
+        atomicAdd(&a.dbg[7], (unsigned long long)((n + 15) >> 4) * ((m + 15) >> 4));
+        atomicAdd(&a.dbg[9], 1ull);
+    }
     for (int u0 = 0; u0 < nu; u0 += 32) {
         const int uj = u0 + lane;
         if (uj < nu) {
             const int j = S.ulist[uj];
             const int f = S.list[j];
             const float2 p2 = a.xy[toff + f];
-            bool any = false;
-            for (int k = 0; k < m && !any; k++) any = member_band(a, G, MR[k], p2.x, p2.y);
-            if (any) {
-                const int su = a.sub[toff + f];
-                if (in_cprime_exact(G, D, p2.x, p2.y, (short)(su & 0xffff), su >> 16))
-                    atomicOr(&S.valid[j >> 5], 1u << (j & 31));
+            const bool inner = p2.x >= SG.border && p2.x <= SG.W - SG.border &&
+                               p2.y >= SG.border && p2.y <= SG.H - SG.border;
+            unsigned bits = 0;
+            for (int gi = 0; gi < SG.gcnt; gi++) {
+                const GroupRec& G = a.grp[SG.g0 + gi];
+                if (G.K < 0) continue;
+                const float dg = fabsf(fmaf(G.ar, p2.x, fmaf(G.br, p2.y, G.cr)));
+                if (dg <= SG.hsure && inner) { bits |= 1u << gi; continue; }
+                // outside every member band of this group: the bit is never consulted
+                if (dg > (float)a.d + G.maxdev + 0.05f) continue;
+                bool any = false;
+                for (int k = S.gbeg[gi]; k < S.gbeg[gi + 1] && !any; k++)
+                    any = member_band(a, G, MR[k], p2.x, p2.y);
+                if (any && a.dbg) atomicAdd(&a.dbg[6], 1ull);
+                if (any && in_cprime(a, G, SG, p2.x, p2.y, toff, f)) bits |= 1u << gi;
             }
+            S.cmask[j] = (unsigned short)bits;
         }
     }
     if (STATS) {
         for (int w = lane; w < CAP / 8; w += 32) S.anyb[w] = 0;
     }
     __syncwarp();
-    const bool gemv_band = (m == 1);
     const int ntiles = (n + 15) >> 4;
-    for (int mt0 = 0; mt0 < m; mt0 += 8) {
-        // B fragment: member mt0+g, bytes [32t, 32t+32) (K permuted consistently with A)
-        unsigned bw[8];
-        {
-            const int j = mt0 + g;
+    for (int mt0 = 0; mt0 < m; mt0 += 16) {
+        // B fragments: members mt0+g (n-tile 0) and mt0+8+g (n-tile 1), bytes [32t, 32t+32)
+        unsigned bw[2][8];
+#pragma unroll
+        for (int nt = 0; nt < 2; nt++) {
+            const int j = mt0 + nt * 8 + g;
             if (j < m) {
                 const int fid = MR[j].fid;
                 const uint4* row = reinterpret_cast<const uint4*>(a.desc + (qoff + fid) * 128) + 2 * t;
                 const uint4 v0 = __ldg(row), v1 = __ldg(row + 1);
-                bw[0] = v0.x; bw[1] = v0.y; bw[2] = v0.z; bw[3] = v0.w;
-                bw[4] = v1.x; bw[5] = v1.y; bw[6] = v1.z; bw[7] = v1.w;
+                bw[nt][0] = v0.x; bw[nt][1] = v0.y; bw[nt][2] = v0.z; bw[nt][3] = v0.w;
+                bw[nt][4] = v1.x; bw[nt][5] = v1.y; bw[nt][6] = v1.z; bw[nt][7] = v1.w;
             } else {
 #pragma unroll
-                for (int k = 0; k < 8; k++) bw[k] = 0;
+                for (int k = 0; k < 8; k++) bw[nt][k] = 0;
             }
         }
-        // epilogue columns 2t, 2t+1
-        float la[2], lb[2], lc[2], lo[2], hi[2];
-        unsigned qn9[2];
-        int mslot[2];
+        // epilogue columns: (nt, 2t + c) -> member mt0 + 8 nt + 2t + c
+        float la[4], lb[4], lc[4], lo[4], hi[4];
+        unsigned qn9[4];
+        int mslot[4], mgi[4];
 #pragma unroll
-        for (int c = 0; c < 2; c++) {
-            const int j = mt0 + 2 * t + c;
+        for (int c = 0; c < 4; c++) {
+            const int j = mt0 + (c >> 1) * 8 + 2 * t + (c & 1);
             if (j < m) {
                 const MemberRec M = MR[j];
                 la[c] = M.a; lb[c] = M.b; lc[c] = M.c; lo[c] = M.lo; hi[c] = M.hi;
                 qn9[c] = M.qn9;
-                mslot[c] = M.slot;
+                mslot[c] = M.slotgi & 0xFFFFFF;
+                mgi[c] = M.slotgi >> 24;
             } else {
                 la[c] = 0.f; lb[c] = 0.f; lc[c] = 1e30f; lo[c] = -1.f; hi[c] = -1.f;
                 qn9[c] = 0;
                 mslot[c] = -1;
+                mgi[c] = 0;
             }
         }
-        unsigned b1[2] = {NONE, NONE}, b2[2] = {NONE, NONE};
-        for (int mt = 0; mt < ntiles; mt++) {
+        unsigned b1[4] = {NONE, NONE, NONE, NONE}, b2[4] = {NONE, NONE, NONE, NONE};
+        // candidate tile loads, double-buffered in registers so the next tile's
+        // L2 traffic overlaps this tile's mma + epilogue
+        struct Tile {
+            uint4 x00, x01, x10, x11;
+            float2 p0, p1;
+            unsigned tb0, tb1, cm0, cm1;
+        };
+        auto load_tile = [&](int mt, Tile& T) {
             const int r0 = mt * 16 + g, r1 = r0 + 8;
-            const bool v0 = r0 < n && ((S.valid[r0 >> 5] >> (r0 & 31)) & 1u);
-            const bool v1 = r1 < n && ((S.valid[r1 >> 5] >> (r1 & 31)) & 1u);
+            T.cm0 = r0 < n ? S.cmask[r0] : 0u;
+            T.cm1 = r1 < n ? S.cmask[r1] : 0u;
             const int f0 = r0 < n ? S.list[r0] : 0, f1 = r1 < n ? S.list[r1] : 0;
             const uint4* row0 = reinterpret_cast<const uint4*>(a.desc + (toff + f0) * 128) + 2 * t;
             const uint4* row1 = reinterpret_cast<const uint4*>(a.desc + (toff + f1) * 128) + 2 * t;
-            const uint4 x00 = __ldg(row0), x01 = __ldg(row0 + 1);
-            const uint4 x10 = __ldg(row1), x11 = __ldg(row1 + 1);
-            float2 p0 = a.xy[toff + f0], p1 = a.xy[toff + f1];
-            if (!v0) { p0.x = 1e30f; p0.y = 1e30f; }
-            if (!v1) { p1.x = 1e30f; p1.y = 1e30f; }
-            const unsigned tb0 = ((unsigned)a.norm2[toff + f0] << 9) | (unsigned)r0;
-            const unsigned tb1 = ((unsigned)a.norm2[toff + f1] << 9) | (unsigned)r1;
-            int acc[4] = {0, 0, 0, 0};
-            mma_u8(acc, x00.x, x10.x, x00.y, x10.y, bw[0], bw[1]);
-            mma_u8(acc, x00.z, x10.z, x00.w, x10.w, bw[2], bw[3]);
-            mma_u8(acc, x01.x, x11.x, x01.y, x11.y, bw[4], bw[5]);
-            mma_u8(acc, x01.z, x11.z, x01.w, x11.w, bw[6], bw[7]);
-            bool inb[4];
+            T.x00 = __ldg(row0); T.x01 = __ldg(row0 + 1);
+            T.x10 = __ldg(row1); T.x11 = __ldg(row1 + 1);
+            T.p0 = a.xy[toff + f0]; T.p1 = a.xy[toff + f1];
+            T.tb0 = ((unsigned)a.norm2[toff + f0] << 9) | (unsigned)r0;
+            T.tb1 = ((unsigned)a.norm2[toff + f1] << 9) | (unsigned)r1;
+        };
+        Tile nxt;
+        if (ntiles > 0) load_tile(0, nxt);
+        for (int mt = 0; mt < ntiles; mt++) {
+            const Tile cur = nxt;
+            if (mt + 1 < ntiles) load_tile(mt + 1, nxt);
+            const uint4 x00 = cur.x00, x01 = cur.x01, x10 = cur.x10, x11 = cur.x11;
+            const unsigned cm0 = cur.cm0, cm1 = cur.cm1, tb0 = cur.tb0, tb1 = cur.tb1;
+            float2 p0 = cur.p0, p1 = cur.p1;
+            if (!cm0) { p0.x = 1e30f; p0.y = 1e30f; }
+            if (!cm1) { p1.x = 1e30f; p1.y = 1e30f; }
+            int acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
 #pragma unroll
-            for (int e = 0; e < 4; e++) {
-                const int c = e & 1;
-                const float2 P = (e < 2) ? p0 : p1;
+            for (int nt = 0; nt < 2; nt++) {
+                mma_u8(acc[nt], x00.x, x10.x, x00.y, x10.y, bw[nt][0], bw[nt][1]);
+                mma_u8(acc[nt], x00.z, x10.z, x00.w, x10.w, bw[nt][2], bw[nt][3]);
+                mma_u8(acc[nt], x01.x, x11.x, x01.y, x11.y, bw[nt][4], bw[nt][5]);
+                mma_u8(acc[nt], x01.z, x11.z, x01.w, x11.w, bw[nt][6], bw[nt][7]);
+            }
+            // band test for all 8 elements first (straight-line code); the exact
+            // fp64 value is needed only inside [d - eps, d + eps] (rare, warp-uniform check)
+            bool inb[8], unc[8];
+            bool any_unc = false;
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+                const int c = (e >> 2) * 2 + (e & 1);
+                const float2 P = (e & 2) ? p1 : p0;
                 const float av = fabsf(fmaf(la[c], P.x, fmaf(lb[c], P.y, lc[c])));
-                bool in = av <= lo[c];
-                if (!in && av <= hi[c]) {
-                    const double* L = gemv_band ? &G.sl0 : a.q_line + 3 * (int64_t)mslot[c];
-                    in = band_exact(L[0], L[1], L[2], gemv_band, (double)P.x, (double)P.y, a.d);
+                inb[e] = av <= lo[c];
+                unc[e] = !inb[e] && av <= hi[c];
+                any_unc |= unc[e];
+            }
+            if (__any_sync(FULL, any_unc)) {
+#pragma unroll
+                for (int e = 0; e < 8; e++) {
+                    if (!unc[e]) continue;
+                    const int c = (e >> 2) * 2 + (e & 1);
+                    const float2 P = (e & 2) ? p1 : p0;
+                    const GroupRec& Gc = a.grp[SG.g0 + mgi[c]];
+                    const bool gemv = Gc.cnt == 1;
+                    const double* L = gemv ? &Gc.sl0 : a.q_line + 3 * (int64_t)mslot[c];
+                    inb[e] = band_exact(L[0], L[1], L[2], gemv, (double)P.x, (double)P.y, a.d);
                 }
-                inb[e] = in;
-                const unsigned base = ((e < 2) ? tb0 : tb1) + qn9[c];
-                const unsigned key = in ? base - ((unsigned)acc[e] << 10) : NONE;
+            }
+            bool any0 = false, any1 = false;
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+                const int nt = e >> 2, q = e & 3, c = nt * 2 + (q & 1);
+                const bool rowhi = q >= 2;
+                const unsigned cm = rowhi ? cm1 : cm0;
+                const bool in = inb[e] && ((cm >> mgi[c]) & 1u);
+                if (rowhi) any1 |= in; else any0 |= in;
+                const unsigned base = (rowhi ? tb1 : tb0) + qn9[c];
+                const unsigned key = in ? base - ((unsigned)acc[nt][q] << 10) : NONE;
                 top2_push(key, b1[c], b2[c]);
             }
             if (STATS) {
-                unsigned m0 = __ballot_sync(FULL, inb[0] || inb[1]);
-                unsigned m1 = __ballot_sync(FULL, inb[2] || inb[3]);
+                unsigned m0 = __ballot_sync(FULL, any0);
+                unsigned m1 = __ballot_sync(FULL, any1);
                 if (lane == 0) {
                     m0 |= m0 >> 1; m0 |= m0 >> 2;
                     m1 |= m1 >> 1; m1 |= m1 >> 2;
@@ -832,7 +1154,7 @@ __device__ void process_round(const ChunkArgs& a, const GroupRec& G, WarpSmem& S
         }
         // reduce across the 8 lanes sharing t
 #pragma unroll
-        for (int c = 0; c < 2; c++) {
+        for (int c = 0; c < 4; c++) {
 #pragma unroll
             for (int o = 4; o < 32; o <<= 1) {
                 unsigned o1 = __shfl_xor_sync(FULL, b1[c], o);
@@ -842,7 +1164,7 @@ __device__ void process_round(const ChunkArgs& a, const GroupRec& G, WarpSmem& S
         }
         if (g == 0) {
 #pragma unroll
-            for (int c = 0; c < 2; c++) {
+            for (int c = 0; c < 4; c++) {
                 if (mslot[c] < 0) continue;
                 unsigned long long best = ~0ull;
                 unsigned sec = NONE;
@@ -878,50 +1200,60 @@ __device__ void process_round(const ChunkArgs& a, const GroupRec& G, WarpSmem& S
 }
 
 template <bool STATS>
-__global__ void __launch_bounds__(WARPS * 32, 3) match_kernel(ChunkArgs a) {
+__global__ void __launch_bounds__(WARPS * 32, 4) match_kernel(ChunkArgs a) {
     __shared__ WarpSmem smem[WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpSmem& S = smem[warp];
-    const int total = a.gstart[a.npairs];
+    const int total = a.sgstart[a.npairs];
     const float Df = (float)a.D;
-    for (int gid = blockIdx.x * WARPS + warp; gid < total; gid += gridDim.x * WARPS) {
+    for (int sid = 0;;) {
+        if (lane == 0) sid = atomicAdd(a.sg_next, 1);
+        sid = __shfl_sync(FULL, sid, 0);
+        if (sid >= total) break;
         {
-            static_assert(sizeof(GroupRec) % 16 == 0, "GroupRec must be 16-byte granular");
-            const uint4* src = reinterpret_cast<const uint4*>(a.grp + gid);
-            uint4* dst = reinterpret_cast<uint4*>(&S.grec);
-            if (lane < (int)(sizeof(GroupRec) / 16)) dst[lane] = __ldg(src + lane);
+            static_assert(sizeof(SGRec) % 16 == 0, "SGRec must be 16-byte granular");
+            const uint4* src = reinterpret_cast<const uint4*>(a.sg + sid);
+            uint4* dst = reinterpret_cast<uint4*>(&S.sg);
+            if (lane < (int)(sizeof(SGRec) / 16)) dst[lane] = __ldg(src + lane);
             __syncwarp();
         }
-        const GroupRec& G = S.grec;
-        if (G.K < 0) { __syncwarp(); continue; }   // rep line misses the padded image: C' is empty
-        const int pg = a.p0 + G.p;
+        const SGRec& SG = S.sg;
+        if (a.dbg && lane == 0) {
+            atomicAdd(&a.dbg[0], 1ull);
+            atomicAdd(&a.dbg[1], (unsigned long long)SG.mcnt);
+            atomicAdd(&a.dbg[8], (unsigned long long)SG.gcnt);
+        }
+        if (lane <= SG.gcnt)
+            S.gbeg[lane] = lane < SG.gcnt ? max(a.grp[SG.g0 + lane].moff - SG.m0, 0) : SG.mcnt;
+        __syncwarp();
+        const int pg = a.p0 + SG.p;
         const int ti = a.pair_t[pg], qi = a.pair_q[pg];
         const int64_t toff = a.img_off[ti], qoff = a.img_off[qi];
-        const int nalong = G.horiz ? a.dims[2 * ti] : a.dims[2 * ti + 1];
-        const int64_t toffb = G.horiz ? a.roff[ti] : a.coff[ti];
-        const int32_t* start = G.horiz ? a.rstart : a.cstart;
-        const int32_t* mem = G.horiz ? a.rmem : a.cmem;
+        const int nalong = SG.horiz ? a.dims[2 * ti] : a.dims[2 * ti + 1];
+        const int64_t toffb = SG.horiz ? a.roff[ti] : a.coff[ti];
+        const int32_t* start = SG.horiz ? a.rstart : a.cstart;
+        const int32_t* mem = SG.horiz ? a.rmem : a.cmem;
         int n = 0;
         bool first_round = true;
         int cols_total = 0;
-        if (lane < CAP / 32) S.valid[lane] = 0;
+        if (lane < CAP / 32) S.sure[lane] = 0;
         __syncwarp();
-        // ---- strip gather: bucket rows of the strip |dist_rep| <= R, filtered
-        for (int r0 = G.rlo; r0 <= G.rhi; r0 += 32) {
+        // ---- strip gather: bucket rows of the strip |dist_base| <= R
+        for (int r0 = SG.rlo; r0 <= SG.rhi; r0 += 32) {
             const int r = r0 + lane;
             int bs = 0, len = 0;
-            if (r <= G.rhi) {
+            if (r <= SG.rhi) {
                 int blo = 0, bhi = nalong - 1;
-                if (G.inv_alpha != 0.f) {
+                if (SG.inv_alpha != 0.f) {
                     const float y0 = r * Df - 0.01f, y1 = (r + 1) * Df + 0.01f;
-                    const float e00 = (-G.R - G.beta * y0 - G.cr) * G.inv_alpha;
-                    const float e01 = (G.R - G.beta * y0 - G.cr) * G.inv_alpha;
-                    const float e10 = (-G.R - G.beta * y1 - G.cr) * G.inv_alpha;
-                    const float e11 = (G.R - G.beta * y1 - G.cr) * G.inv_alpha;
+                    const float e00 = (-SG.R - SG.beta * y0 - SG.cr) * SG.inv_alpha;
+                    const float e01 = (SG.R - SG.beta * y0 - SG.cr) * SG.inv_alpha;
+                    const float e10 = (-SG.R - SG.beta * y1 - SG.cr) * SG.inv_alpha;
+                    const float e11 = (SG.R - SG.beta * y1 - SG.cr) * SG.inv_alpha;
                     const float plo = fminf(fminf(e00, e01), fminf(e10, e11));
                     const float phi = fmaxf(fmaxf(e00, e01), fmaxf(e10, e11));
-                    blo = max(blo, (int)floorf(fmaxf(plo - 0.02f, -1.f) * G.invD));
-                    bhi = min(bhi, (int)floorf(fminf(phi + 0.02f, G.Pmax + 1.f) * G.invD));
+                    blo = max(blo, (int)floorf(fmaxf(plo - 0.02f, -1.f) * SG.invD));
+                    bhi = min(bhi, (int)floorf(fminf(phi + 0.02f, SG.Pmax + 1.f) * SG.invD));
                 }
                 if (blo <= bhi) {
                     const int64_t cb = toffb + (int64_t)r * nalong;
@@ -936,6 +1268,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) match_kernel(ChunkArgs a) {
                 if (lane >= o) incl += y;
             }
             const int tot = __shfl_sync(FULL, incl, 31);
+            if (a.dbg && lane == 0) atomicAdd(&a.dbg[2], (unsigned long long)tot);
             for (int j0 = 0; j0 < tot; j0 += 32) {
                 const int j = j0 + lane;
                 int o = 0;
@@ -951,29 +1284,34 @@ __global__ void __launch_bounds__(WARPS * 32, 3) match_kernel(ChunkArgs a) {
                 if (j < tot) {
                     f = mem[ob + (j - oex)];
                     const float2 p2 = a.xy[toff + f];
-                    const float adr = fabsf(fmaf(G.ar, p2.x, fmaf(G.br, p2.y, G.cr)));
-                    pass = adr <= G.R;
-                    const float tau = (p2.x - G.pbx) * G.dirx + (p2.y - G.pby) * G.diry;
-                    sure = adr <= G.hsure && tau >= 0.05f && tau <= G.len - 0.05f;
+                    const float adr = fabsf(fmaf(SG.ar, p2.x, fmaf(SG.br, p2.y, SG.cr)));
+                    pass = adr <= SG.R;
+                    sure = adr + SG.delta <= SG.hsure && p2.x >= SG.border &&
+                           p2.x <= SG.W - SG.border && p2.y >= SG.border && p2.y <= SG.H - SG.border;
                 }
                 const unsigned bal = __ballot_sync(FULL, pass);
                 const int cnt = __popc(bal);
+                if (a.dbg && lane == 0) {
+                    atomicAdd(&a.dbg[3], (unsigned long long)cnt);
+                    atomicAdd(&a.dbg[4], (unsigned long long)__popc(__ballot_sync(FULL, pass && sure)));
+                } else if (a.dbg) {
+                    __ballot_sync(FULL, pass && sure);
+                }
                 if (n + cnt > CAP) {
                     __syncwarp();
-                    process_round<STATS>(a, G, S, n, toff, qoff, first_round, cols_total);
+                    process_round<STATS>(a, S, n, toff, qoff, first_round, cols_total);
                     first_round = false;
                     n = 0;
-                    if (lane < CAP / 32) S.valid[lane] = 0;
+                    if (lane < CAP / 32) S.sure[lane] = 0;
                     __syncwarp();
                 }
                 const int k = __popc(bal & ((1u << lane) - 1u));
                 if (pass) S.list[n + k] = (unsigned short)f;
-                // sure bits, compacted to list order (positions n .. n+cnt-1)
                 const unsigned bits = __reduce_or_sync(FULL, (pass && sure) ? (1u << k) : 0u);
                 if (lane == 0 && cnt) {
                     const int w = n >> 5, sh = n & 31;
-                    S.valid[w] |= bits << sh;
-                    if (sh && sh + cnt > 32) S.valid[w + 1] |= bits >> (32 - sh);
+                    S.sure[w] |= bits << sh;
+                    if (sh && sh + cnt > 32) S.sure[w + 1] |= bits >> (32 - sh);
                 }
                 n += cnt;
                 __syncwarp();
@@ -981,15 +1319,15 @@ __global__ void __launch_bounds__(WARPS * 32, 3) match_kernel(ChunkArgs a) {
         }
         if (n > 0) {
             __syncwarp();
-            process_round<STATS>(a, G, S, n, toff, qoff, first_round, cols_total);
+            process_round<STATS>(a, S, n, toff, qoff, first_round, cols_total);
             first_round = false;
         }
         __syncwarp();
         // ---- ratio test + dedupe per member (ratio_filter / _dedupe_targets)
         if (!first_round) {
-            for (int j = lane; j < G.cnt; j += 32) {
-                const MemberRec& M = a.mrec[G.moff + j];
-                const int slot = M.slot;
+            for (int j = lane; j < SG.mcnt; j += 32) {
+                const MemberRec& M = a.mrec[SG.m0 + j];
+                const int slot = M.slotgi & 0xFFFFFF;
                 const unsigned long long best = a.mstate[slot];
                 const unsigned sec = a.mstate2[slot];
                 if (best == ~0ull) continue;
@@ -1012,12 +1350,12 @@ __global__ void __launch_bounds__(WARPS * 32, 3) match_kernel(ChunkArgs a) {
                 a.res_ratio[slot] = rr;
                 const unsigned long long key =
                     ((unsigned long long)__float_as_uint(db) << 32) | (unsigned)M.fid;
-                atomicMin(&a.dedupe[a.tbase[G.p] + tid], key);
+                atomicMin(&a.dedupe[a.tbase[SG.p] + tid], key);
             }
         }
         if (STATS && lane == 0 && cols_total > 0) {
-            atomicAdd(&a.stats[2 * pg], (unsigned long long)G.cnt);
-            atomicAdd(&a.stats[2 * pg + 1], (unsigned long long)G.cnt * (unsigned long long)cols_total);
+            atomicAdd(&a.stats[2 * pg], (unsigned long long)SG.mcnt);
+            atomicAdd(&a.stats[2 * pg + 1], (unsigned long long)SG.mcnt * (unsigned long long)cols_total);
         }
         __syncwarp();
     }
@@ -1068,7 +1406,8 @@ struct ChunkSizes {
 size_t chunk_bytes(const ChunkSizes& c) {
     size_t b = 0;
     b += aligned_bytes<int64_t>(c.P + 1) * 2;          // tab_off, tbase
-    b += aligned_bytes<int32_t>(c.P + 1) * 2;          // ngroups, gstart
+    b += aligned_bytes<int32_t>(c.P + 1) * 5 + 256;    // ngroups, gstart, nmem, sgstart, nsg, sg_next
+    b += aligned_bytes<float4>(c.Q) * 2 + aligned_bytes<int2>(c.Q);   // gline, gend, sglist
     b += aligned_bytes<unsigned long long>(c.T);       // tab_key
     b += aligned_bytes<unsigned>(c.T) * 2;             // tab_rep, tab_cnt
     b += aligned_bytes<int32_t>(c.Q);                  // q_tab
@@ -1077,6 +1416,8 @@ size_t chunk_bytes(const ChunkSizes& c) {
     b += aligned_bytes<int32_t>(c.Q) * 2;              // gfill, members
     b += aligned_bytes<GroupRec>(c.Q);                 // grp
     b += aligned_bytes<MemberRec>(c.Q);                // mrec
+    b += aligned_bytes<SGRec>(c.Q);                    // sg
+    b += aligned_bytes<int2>(c.Q) + aligned_bytes<float>(c.Q) + aligned_bytes<int32_t>(c.Q);  // gtmp, gkey, gpos
     b += aligned_bytes<unsigned long long>(c.Q);       // mstate
     b += aligned_bytes<unsigned>(c.Q);                 // mstate2
     b += aligned_bytes<int32_t>(c.Q) * 3;              // res_tid/dist/ratio
@@ -1088,6 +1429,24 @@ size_t chunk_bytes(const ChunkSizes& c) {
 }  // namespace msfm
 
 using namespace msfm;
+
+static unsigned long long* g_dbg = nullptr;
+
+extern "C" int msfm_debug_counters(int enable, int64_t* out16) {
+    if (enable && !g_dbg) {
+        MSFM_CUDA_TRY(cudaMalloc(&g_dbg, 16 * sizeof(unsigned long long)));
+        MSFM_CUDA_TRY(cudaMemset(g_dbg, 0, 16 * sizeof(unsigned long long)));
+    }
+    if (out16 && g_dbg) {
+        MSFM_CUDA_TRY(cudaMemcpy(out16, g_dbg, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        MSFM_CUDA_TRY(cudaMemset(g_dbg, 0, 16 * sizeof(unsigned long long)));
+    }
+    if (!enable && g_dbg) {
+        cudaFree(g_dbg);
+        g_dbg = nullptr;
+    }
+    return MSFM_OK;
+}
 
 extern "C" int msfm_feature_norms(const uint8_t* d_desc, int64_t n, int32_t* d_norm2, void* stream) {
     if (n < 0 || (n > 0 && (!d_desc || !d_norm2))) {
@@ -1156,13 +1515,17 @@ extern "C" int msfm_grid_build(const msfm_bank* bank, const int32_t* d_dims, con
 
 static void plan_chunks(int32_t n_pairs, const int64_t* h_qlist_off, const msfm_match_params* prm,
                         std::vector<int>& bounds, ChunkSizes& worst) {
-    const int cp = prm->chunk_pairs > 0 ? prm->chunk_pairs : 256;
+    // pairs per chunk, and at most 8M query slots per chunk (member records pack the
+    // chunk-local slot into 24 bits)
+    const int cp = prm->chunk_pairs > 0 ? prm->chunk_pairs : 1024;
+    const int64_t qmax = 8 << 20;
     bounds.clear();
     worst = {0, 0, 0, 0};
     int p = 0;
     bounds.push_back(0);
     while (p < n_pairs) {
-        int e = p + cp < n_pairs ? p + cp : n_pairs;
+        int e = p + 1;
+        while (e < n_pairs && e - p < cp && h_qlist_off[e + 1] - h_qlist_off[p] <= qmax) e++;
         ChunkSizes c;
         c.P = e - p;
         c.Q = h_qlist_off[e] - h_qlist_off[p];
@@ -1232,10 +1595,19 @@ extern "C" int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids,
     a.sub = grids->d_sub; a.dims = grids->d_dims; a.roff = grids->d_roff; a.coff = grids->d_coff;
     a.rstart = grids->d_rstart; a.cstart = grids->d_cstart; a.rmem = grids->d_rmem; a.cmem = grids->d_cmem;
     a.D = grids->D; a.d = prm->d; a.ratio = prm->ratio; a.single_cap = prm->single_cap;
+    a.stats_mode = d_stats ? 1 : 0;
+    {
+        const char* e = getenv("MSFM_SG_TAU");
+        a.sg_tau = e ? (float)atof(e) : SG_TAU;
+    }
     a.pair_q = d_pair_q; a.pair_t = d_pair_t; a.pair_F = d_pair_F;
     a.qlist_off = d_qlist_off; a.qlist = d_qlist;
     a.tab_off = ar.take<int64_t>(w.P + 1); a.tbase = ar.take<int64_t>(w.P + 1);
     a.ngroups = ar.take<int32_t>(w.P + 1); a.gstart = ar.take<int32_t>(w.P + 1);
+    a.nmem = ar.take<int32_t>(w.P + 1); a.sgstart = ar.take<int32_t>(w.P + 1);
+    a.sg_next = ar.take<int32_t>(1);
+    a.nsg = ar.take<int32_t>(w.P + 1);
+    a.gline = ar.take<float4>(w.Q); a.gend = ar.take<float4>(w.Q); a.sglist = ar.take<int2>(w.Q);
     a.tab_key = ar.take<unsigned long long>(w.T);
     a.tab_rep = ar.take<unsigned>(w.T); a.tab_cnt = ar.take<unsigned>(w.T);
     a.q_tab = ar.take<int32_t>(w.Q); a.q_line = ar.take<double>(3 * w.Q);
@@ -1243,10 +1615,13 @@ extern "C" int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids,
     a.gfill = ar.take<int32_t>(w.Q); a.members = ar.take<int32_t>(w.Q);
     a.grp = ar.take<GroupRec>(w.Q);
     a.mrec = ar.take<MemberRec>(w.Q);
+    a.sg = ar.take<SGRec>(w.Q);
+    a.gtmp = ar.take<int2>(w.Q); a.gkey = ar.take<float>(w.Q); a.gpos = ar.take<int32_t>(w.Q);
     a.mstate = ar.take<unsigned long long>(w.Q); a.mstate2 = ar.take<unsigned>(w.Q);
     a.res_tid = ar.take<int32_t>(w.Q); a.res_dist = ar.take<float>(w.Q); a.res_ratio = ar.take<float>(w.Q);
     a.dedupe = ar.take<unsigned long long>(w.NT);
     a.stats = reinterpret_cast<unsigned long long*>(d_stats);
+    a.dbg = g_dbg;
     a.out_q = d_out_q; a.out_t = d_out_t; a.out_dist = d_out_dist; a.out_ratio = d_out_ratio;
     a.out_count = d_out_count;
     int dev = 0, nsm = 148;
@@ -1263,15 +1638,18 @@ extern "C" int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids,
         groups_kernel<<<a.npairs, 256, 0, st>>>(a);
         gscan_kernel<<<1, SCAN_T, 0, st>>>(a);
         scatter_kernel<<<a.npairs, 256, 0, st>>>(a);
-        if (Q > 0) prep_kernel<<<(unsigned)((Q + 127) / 128), 128, 0, st>>>(a, (int)Q);
+        if (Q > 0) {
+            prep_kernel<<<(unsigned)((Q + 127) / 128), 128, 0, st>>>(a, (int)Q);
+            sg_prep_kernel<<<(unsigned)((Q + 127) / 128), 128, 0, st>>>(a, (int)Q);
+        }
         {
             ProfScope ps("match_kernel", st);
-            if (d_stats) match_kernel<true><<<nsm * 3, WARPS * 32, 0, st>>>(a);
-            else         match_kernel<false><<<nsm * 3, WARPS * 32, 0, st>>>(a);
+            if (d_stats) match_kernel<true><<<nsm * 4, WARPS * 32, 0, st>>>(a);
+            else         match_kernel<false><<<nsm * 4, WARPS * 32, 0, st>>>(a);
         }
         compact_kernel<<<a.npairs, 256, 0, st>>>(a);
         MSFM_LAUNCH_CHECK();
-        count_launches(7 + (Q > 0 ? 1 : 0));
+        count_launches(7 + (Q > 0 ? 2 : 0));
     }
     return MSFM_OK;
 }
