@@ -175,13 +175,14 @@ int msfm_ransac_samples(const uint64_t state_inc[4], int32_t has_uint32, uint32_
  *     k1[s][p], i1[s][p] (image-local feature id, -1 if none), k2[s][p]
  * (INT32_MAX when the image has < 2 features).  Row stride = n_points rounded
  * up to 128.  S.f runs on tcgen05 kind::i8 (two u8 digit planes of S).
- * Requires max track length <= 100 (int32 keys).
+ * Requires max track length <= 100 (int32 keys); max_image_features bounds the
+ * feature count of every query image.
  * ---------------------------------------------------------------------- */
-size_t msfm_knn_workspace_bytes(int32_t n_points);
+size_t msfm_knn_workspace_bytes(int32_t n_points, int32_t n_images, int32_t max_image_features);
 int msfm_knn2_tracks(const msfm_bank* bank, int32_t n_points, const int32_t* d_S,
                      const int32_t* d_n, int32_t n_images, const int32_t* d_images,
-                     int32_t max_track, int32_t* d_k1, int32_t* d_i1, int32_t* d_k2,
-                     void* d_workspace, size_t workspace_bytes, void* stream);
+                     int32_t max_track, int32_t max_image_features, int32_t* d_k1, int32_t* d_i1,
+                     int32_t* d_k2, void* d_workspace, size_t workspace_bytes, void* stream);
 
 /* direct_3d2d_search post-processing (localize.py:108-122 + ratio_filter
  * matching.py:82-103) on the knn2 output: ratio test sqrt(N_b/N_s) < p/q

@@ -25,10 +25,11 @@
 namespace msfm {
 namespace {
 
-constexpr int KN_THREADS = 384;
+constexpr int KN_THREADS = 640;
 constexpr int KN_STAGES = 4;
 constexpr int TILE_M = 128, TILE_N = 128, KB = 128;   // K = 128 bytes per plane
-constexpr int EPI_WARP0 = 4, EPI_WARPS = 8;
+constexpr int EPI_WARP0 = 4, EPI_WARPS = 16;
+constexpr int EPI_COLS = TILE_N / (EPI_WARPS / 4);   // columns per epilogue warp per tile
 constexpr uint32_t B_TILE_BYTES = TILE_N * KB;          // 16 KB
 constexpr uint32_t A_PLANE_BYTES = TILE_M * KB;         // 16 KB
 constexpr int INT_BIG = 0x7fffffff;
@@ -40,12 +41,14 @@ struct KnnSmem {
     uint64_t a_full, a_empty;
     uint64_t t_full[2], t_empty[2];
     uint32_t tmem_base;
-    int merge_k1[TILE_M], merge_i1[TILE_M], merge_k2[TILE_M];
+    int merge_k1[EPI_WARPS / 4][TILE_M], merge_i1[EPI_WARPS / 4][TILE_M], merge_k2[EPI_WARPS / 4][TILE_M];
 };
 
 struct KnnArgs {
     const int32_t* n;          // [M_pad] track length (0 for padding rows)
     const int32_t* fnorm;      // bank |f|^2
+    const int32_t* fn_pad;     // [n_img][fn_stride] |f|^2 per query image, 16-B aligned tiles
+    int fn_stride;
     const int64_t* img_off;    // bank image offsets
     const int32_t* img_n;      // bank image sizes
     const int32_t* images;     // [n_img] bank image index of each query image
@@ -260,9 +263,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_lo, const __grid_constant_
         }
     } else if (warp >= EPI_WARP0) {
         // ---------------- epilogue
-        const int ew = warp - EPI_WARP0;          // 0..7
+        const int ew = warp - EPI_WARP0;          // 0..EPI_WARPS-1
         const int quad = warp & 3;                // TMEM lane quadrant this warp may access
-        const int half = ew >> 2;                 // column half
+        const int half = ew >> 2;                 // column slice
         const int row = quad * 32 + lane;         // point row within the tile
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -276,24 +279,39 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_lo, const __grid_constant_
             for (int j = 0; j < nt; j++) {
                 mbar_wait(&S.t_full[acc], acc_phase);
                 tc_fence_after();
-                const uint32_t t_lo = tbase + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * 256 + half * 64);
-                const int cbase = j * TILE_N + half * 64;
+                const uint32_t t_lo = tbase + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * 256 + half * EPI_COLS);
+                const int cbase = j * TILE_N + half * EPI_COLS;
+                const int slot = u - mt * a.n_img;
+                const int4* fp = reinterpret_cast<const int4*>(a.fn_pad + (int64_t)slot * a.fn_stride + cbase);
+                const bool full = cbase + EPI_COLS <= n;
 #pragma unroll
-                for (int c0 = 0; c0 < 64; c0 += 16) {
+                for (int c0 = 0; c0 < EPI_COLS; c0 += 16) {
                     uint32_t lo[16], hi[16];
                     tmem_ld16(t_lo + c0, lo);
                     tmem_ld16(t_lo + 128 + c0, hi);
+                    int fv[16];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const int4 f4 = __ldg(fp + (c0 >> 2) + q);
+                        fv[4 * q] = f4.x; fv[4 * q + 1] = f4.y; fv[4 * q + 2] = f4.z; fv[4 * q + 3] = f4.w;
+                    }
                     tmem_wait_ld();
                     const int col0 = cbase + c0;
+                    // keys first (straight-line), then one warp vote: after the first
+                    // tiles almost no key beats the running second best
+                    int key[16];
+                    bool hit = false;
 #pragma unroll
                     for (int c = 0; c < 16; c++) {
-                        const int col = col0 + c;
-                        const int fv = col < n ? __ldg(a.fnorm + off + col) : 0;
-                        const int dot = (int)lo[c] + ((int)hi[c] << 8);
-                        const int key = np * fv - 2 * dot;
-                        if (key < k2 && col < n) {
-                            if (key < k1) { k2 = k1; k1 = key; i1 = col; }
-                            else k2 = key;
+                        key[c] = np * fv[c] - 2 * ((int)lo[c] + ((int)hi[c] << 8));
+                        hit |= key[c] < k2;
+                    }
+                    if (__any_sync(0xffffffffu, hit) && hit) {
+                        for (int c = 0; c < 16; c++) {
+                            if (key[c] < k2 && (full || col0 + c < n)) {
+                                if (key[c] < k1) { k2 = k1; k1 = key[c]; i1 = col0 + c; }
+                                else k2 = key[c];
+                            }
                         }
                     }
                 }
@@ -302,23 +320,22 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_lo, const __grid_constant_
                 if (lane == 0) mbar_arrive(&S.t_empty[acc]);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
-            // merge the two column halves of each row
-            if (half == 1) {
-                S.merge_k1[row] = k1; S.merge_i1[row] = i1; S.merge_k2[row] = k2;
-            }
+            // merge the column slices of each row
+            S.merge_k1[half][row] = k1; S.merge_i1[half][row] = i1; S.merge_k2[half][row] = k2;
             asm volatile("bar.sync 1, %0;" ::"r"(EPI_WARPS * 32));
             if (half == 0) {
-                const int ok1 = S.merge_k1[row], oi1 = S.merge_i1[row], ok2 = S.merge_k2[row];
-                // best = min by (key, index); second = 2nd smallest key value
-                const bool other_first = (ok1 < k1) || (ok1 == k1 && oi1 >= 0 && (i1 < 0 || oi1 < i1));
-                const int nk1 = other_first ? ok1 : k1;
-                const int ni1 = other_first ? oi1 : i1;
-                const int hi_k = other_first ? k1 : ok1;
-                const int nk2 = min(hi_k, min(k2, ok2));
+                for (int h = 1; h < EPI_WARPS / 4; h++) {
+                    const int ok1 = S.merge_k1[h][row], oi1 = S.merge_i1[h][row], ok2 = S.merge_k2[h][row];
+                    // best = min by (key, index); second = 2nd smallest key value
+                    const bool other_first = (ok1 < k1) || (ok1 == k1 && oi1 >= 0 && (i1 < 0 || oi1 < i1));
+                    const int hi_k = other_first ? k1 : ok1;
+                    if (other_first) { k1 = ok1; i1 = oi1; }
+                    k2 = min(hi_k, min(k2, ok2));
+                }
                 const int slot = u - mt * a.n_img;
                 if (grow < a.M_pad) {
                     const int64_t o = (int64_t)slot * a.M_pad + grow;
-                    a.out_k1[o] = nk1; a.out_i1[o] = ni1; a.out_k2[o] = nk2;
+                    a.out_k1[o] = k1; a.out_i1[o] = i1; a.out_k2[o] = k2;
                 }
             }
             asm volatile("bar.sync 1, %0;" ::"r"(EPI_WARPS * 32));
@@ -333,6 +350,17 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_lo, const __grid_constant_
 }
 
 // ------------------------------------------------------------------ helpers
+__global__ void fn_pad_kernel(const int32_t* __restrict__ fnorm, const int64_t* __restrict__ img_off,
+                              const int32_t* __restrict__ img_n, const int32_t* __restrict__ images,
+                              int stride, int32_t* __restrict__ out) {
+    const int s = blockIdx.y;
+    const int img = images[s];
+    const int64_t off = img_off[img];
+    const int n = img_n[img];
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < stride; j += gridDim.x * blockDim.x)
+        out[(int64_t)s * stride + j] = j < n ? fnorm[off + j] : 0;
+}
+
 __global__ void digit_planes_kernel(const int32_t* __restrict__ S, const int32_t* __restrict__ n,
                                     int64_t M, int64_t M_pad, uint8_t* __restrict__ lo,
                                     uint8_t* __restrict__ hi, int32_t* __restrict__ npad) {
@@ -478,9 +506,14 @@ int make_rows128_map(CUtensorMap* map, const void* base, int64_t rows) {
 
 using namespace msfm;
 
-extern "C" size_t msfm_knn_workspace_bytes(int32_t n_points) {
+static int64_t fn_stride_of(int32_t max_n) {
+    return ((int64_t)(max_n > 0 ? max_n : 1) + TILE_N - 1) / TILE_N * TILE_N;
+}
+
+extern "C" size_t msfm_knn_workspace_bytes(int32_t n_points, int32_t n_images, int32_t max_n) {
     const int64_t M_pad = ((int64_t)n_points + TILE_M - 1) / TILE_M * TILE_M;
-    return aligned_bytes<uint8_t>(M_pad * 128) * 2 + aligned_bytes<int32_t>(M_pad) + 4096;
+    return aligned_bytes<uint8_t>(M_pad * 128) * 2 + aligned_bytes<int32_t>(M_pad) +
+           aligned_bytes<int32_t>((int64_t)(n_images > 0 ? n_images : 1) * fn_stride_of(max_n)) + 4096;
 }
 
 extern "C" int msfm_direct_3d2d(const msfm_bank* bank, int32_t n_points, const int32_t* d_n,
@@ -519,8 +552,9 @@ extern "C" int msfm_direct_3d2d(const msfm_bank* bank, int32_t n_points, const i
 
 extern "C" int msfm_knn2_tracks(const msfm_bank* bank, int32_t n_points, const int32_t* d_S,
                                 const int32_t* d_n, int32_t n_images, const int32_t* d_images,
-                                int32_t max_track, int32_t* d_k1, int32_t* d_i1, int32_t* d_k2,
-                                void* d_workspace, size_t workspace_bytes, void* stream) {
+                                int32_t max_track, int32_t max_n, int32_t* d_k1, int32_t* d_i1,
+                                int32_t* d_k2, void* d_workspace, size_t workspace_bytes,
+                                void* stream) {
     if (!bank || n_points < 0 || n_images < 0 || (n_points > 0 && (!d_S || !d_n))) {
         set_error("msfm_knn2_tracks: bad arguments");
         return MSFM_EINVAL;
@@ -530,7 +564,7 @@ extern "C" int msfm_knn2_tracks(const msfm_bank* bank, int32_t n_points, const i
         return MSFM_EINVAL;
     }
     if (n_points == 0 || n_images == 0) return MSFM_OK;
-    if (workspace_bytes < msfm_knn_workspace_bytes(n_points)) {
+    if (workspace_bytes < msfm_knn_workspace_bytes(n_points, n_images, max_n)) {
         set_error("msfm_knn2_tracks: workspace too small");
         return MSFM_EWORKSPACE;
     }
@@ -540,6 +574,11 @@ extern "C" int msfm_knn2_tracks(const msfm_bank* bank, int32_t n_points, const i
     uint8_t* lo = ar.take<uint8_t>(M_pad * 128);
     uint8_t* hi = ar.take<uint8_t>(M_pad * 128);
     int32_t* npad = ar.take<int32_t>(M_pad);
+    const int64_t fstride = fn_stride_of(max_n);
+    int32_t* fpad = ar.take<int32_t>((int64_t)n_images * fstride);
+    fn_pad_kernel<<<dim3(8, n_images), 256, 0, st>>>(bank->d_norm2, bank->d_img_off, bank->d_img_n,
+                                                    d_images, (int)fstride, fpad);
+    MSFM_LAUNCH_CHECK();
     digit_planes_kernel<<<(unsigned)((M_pad * 128 + 255) / 256), 256, 0, st>>>(d_S, d_n, n_points,
                                                                              M_pad, lo, hi, npad);
     MSFM_LAUNCH_CHECK();
@@ -556,6 +595,8 @@ extern "C" int msfm_knn2_tracks(const msfm_bank* bank, int32_t n_points, const i
     KnnArgs a;
     a.n = npad;
     a.fnorm = bank->d_norm2;
+    a.fn_pad = fpad;
+    a.fn_stride = (int)fstride;
     a.img_off = bank->d_img_off;
     a.img_n = bank->d_img_n;
     a.images = d_images;
@@ -579,6 +620,6 @@ extern "C" int msfm_knn2_tracks(const msfm_bank* bank, int32_t n_points, const i
         knn_tc_kernel<<<grid, KN_THREADS, smem, st>>>(mlo, mhi, mb, a);
     }
     MSFM_LAUNCH_CHECK();
-    count_launches(2);
+    count_launches(3);
     return MSFM_OK;
 }

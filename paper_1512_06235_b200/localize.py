@@ -89,12 +89,13 @@ def knn2_tracks(bank: FeatureBank, pts: PointSet, image_ids, stream=None,
     k1 = torch.empty((max(len(slots), 1), M_pad), dtype=torch.int32, device=dev)
     i1 = torch.empty_like(k1)
     k2 = torch.empty_like(k1)
-    ws_bytes = lib.msfm_knn_workspace_bytes(M)
+    max_feat = int(bank.counts[slots].max()) if len(slots) else 0
+    ws_bytes = lib.msfm_knn_workspace_bytes(M, len(slots), max_feat)
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
     b = bank.cstruct()
     maxn = int(pts.n.max()) if M else 0
     _lib.check(lib.msfm_knn2_tracks(ctypes.byref(b), M, _lib.ptr(dS), _lib.ptr(dn), len(slots),
-                                    _lib.ptr(d_slots), maxn, _lib.ptr(k1), _lib.ptr(i1),
+                                    _lib.ptr(d_slots), maxn, max_feat, _lib.ptr(k1), _lib.ptr(i1),
                                     _lib.ptr(k2), _lib.ptr(ws), ws_bytes,
                                     _lib.stream_handle(stream)), "msfm_knn2_tracks")
     return DeviceKnn(k1, i1, k2, M_pad, keep=(ws, d_slots))
