@@ -121,7 +121,10 @@ int msfm_grid_build(const msfm_bank* bank, const int32_t* d_dims, const int64_t*
  * Pair k: query image d_pair_q[k], target image d_pair_t[k], fundamental
  * matrix d_pair_F[9k..9k+8] (row-major, p_t^T F p_q = 0, from
  * fundamental_from_poses geometry.py:69-83), query feature ids
- * d_qlist[d_qlist_off[k] .. d_qlist_off[k+1]) in ascending order.
+ * d_qlist[d_qlist_off[k] .. d_qlist_off[k+1]) in ascending order.  When
+ * d_qlist_src (optional, [n_pairs] int64) is given, pair k's list is read from
+ * d_qlist[d_qlist_src[k] ..] instead (pairs sharing a query image share one
+ * list); d_qlist_off still sizes the lists and places the output segments.
  * A pair whose F row starts with NaN is skipped (degenerate geometry,
  * densify.py:161-165).
  *
@@ -141,12 +144,20 @@ typedef struct {
     int32_t chunk_pairs; /* pairs per internal chunk (workspace bound), 0 = auto  */
 } msfm_match_params;
 
+/* Pack the per-pair segments of msfm_guided_match's output into contiguous
+ * 16-byte rows (pair index, q_fid | t_fid << 16, f32 dist bits, f32 ratio bits)
+ * in pair order; d_out_off [n_pairs+1] receives the row offsets (total last).
+ * d_rows capacity: 4 * total queries int32. */
+int msfm_pack_matches(int32_t n_pairs, const int64_t* d_qlist_off, const int32_t* d_count,
+                      const int32_t* d_q, const int32_t* d_t, const float* d_dist,
+                      const float* d_ratio, int64_t* d_out_off, int32_t* d_rows, void* stream);
+
 size_t msfm_guided_workspace_bytes(int32_t n_pairs, const int64_t* h_qlist_off,
                                    const msfm_match_params* prm);
 int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids, int32_t n_pairs,
                       const int32_t* d_pair_q, const int32_t* d_pair_t, const double* d_pair_F,
                       const int64_t* d_qlist_off, const int32_t* d_qlist,
-                      const int64_t* h_qlist_off, const msfm_match_params* prm,
+                      const int64_t* d_qlist_src, const int64_t* h_qlist_off, const msfm_match_params* prm,
                       int32_t* d_out_q, int32_t* d_out_t, float* d_out_dist, float* d_out_ratio,
                       int32_t* d_out_count, int64_t* d_stats,
                       void* d_workspace, size_t workspace_bytes, void* stream);

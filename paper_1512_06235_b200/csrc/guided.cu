@@ -324,9 +324,14 @@ struct alignas(16) SGRec {
     float W, H, pad0, pad1;
 };
 
-constexpr int SG_MEMBERS = 16;
+#ifndef MSFM_SG_NT
+#define MSFM_SG_NT 2
+#endif
+constexpr int SG_NT = MSFM_SG_NT;          // n8 member tiles per super-group
+constexpr int SG_MEMBERS = 8 * SG_NT;
+constexpr int MATCH_MINB = SG_NT == 1 ? 6 : 4;   // resident CTAs (4 warps) per SM
 constexpr float SG_TAU = 16.0f;
-constexpr int SG_MAX_GROUPS = 16;
+constexpr int SG_MAX_GROUPS = SG_MEMBERS;
 
 struct ChunkArgs {
     // bank
@@ -342,6 +347,8 @@ struct ChunkArgs {
     // pairs
     const int32_t* pair_q; const int32_t* pair_t; const double* pair_F;
     const int64_t* qlist_off; const int32_t* qlist;
+    const int64_t* qlist_src;    // optional: per-pair start of its list inside qlist
+    int32_t* q_fid;              // chunk-local query feature ids (filled by lines_kernel)
     int32_t p0, npairs; int64_t qbase;
     // chunk workspace
     int64_t* tab_off; int64_t* tbase; int32_t* ngroups; int32_t* gstart; int32_t* nmem;
@@ -426,8 +433,10 @@ __global__ void __launch_bounds__(256) lines_kernel(ChunkArgs a) {
     const double W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1];
     const int64_t qoff = a.img_off[qi];
     const unsigned mask = (unsigned)tsize - 1;
+    const int64_t qs = a.qlist_src ? a.qlist_src[pg] : q0;
     for (int i = threadIdx.x; i < nq; i += blockDim.x) {
-        const int fid = a.qlist[q0 + i];
+        const int fid = a.qlist[qs + i];
+        a.q_fid[s0 + i] = fid;
         const float2 p2 = a.xy[qoff + fid];
         double l[3];
         epiline(F, (double)p2.x, (double)p2.y, nq == 1, l);
@@ -741,7 +750,7 @@ __global__ void __launch_bounds__(128) prep_kernel(ChunkArgs a, int max_groups) 
         for (int j = 0; j < 9; j++) F[j] = a.pair_F[9 * (int64_t)pg + j];
     for (int j = 0; j < g.y; j++) {
         const int slot = a.members[g.z + j];
-        const int fid = a.qlist[a.qbase + slot];
+        const int fid = a.q_fid[slot];
         double m[3];
         if (g.y == 1) {
             // a singleton's own band uses the dgemv-rounded line (guided.py:443-446, m == 1)
@@ -1028,11 +1037,11 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
     }
     __syncwarp();
     const int ntiles = (n + 15) >> 4;
-    for (int mt0 = 0; mt0 < m; mt0 += 16) {
-        // B fragments: members mt0+g (n-tile 0) and mt0+8+g (n-tile 1), bytes [32t, 32t+32)
-        unsigned bw[2][8];
+    for (int mt0 = 0; mt0 < m; mt0 += SG_MEMBERS) {
+        // B fragments: member mt0 + 8 nt + g of n-tile nt, bytes [32t, 32t+32)
+        unsigned bw[SG_NT][8];
 #pragma unroll
-        for (int nt = 0; nt < 2; nt++) {
+        for (int nt = 0; nt < SG_NT; nt++) {
             const int j = mt0 + nt * 8 + g;
             if (j < m) {
                 const int fid = MR[j].fid;
@@ -1046,11 +1055,12 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
             }
         }
         // epilogue columns: (nt, 2t + c) -> member mt0 + 8 nt + 2t + c
-        float la[4], lb[4], lc[4], lo[4], hi[4];
-        unsigned qn9[4];
-        int mslot[4], mgi[4];
+        constexpr int NC = 2 * SG_NT;    // epilogue columns per lane
+        float la[NC], lb[NC], lc[NC], lo[NC], hi[NC];
+        unsigned qn9[NC];
+        int mslot[NC], mgi[NC];
 #pragma unroll
-        for (int c = 0; c < 4; c++) {
+        for (int c = 0; c < NC; c++) {
             const int j = mt0 + (c >> 1) * 8 + 2 * t + (c & 1);
             if (j < m) {
                 const MemberRec M = MR[j];
@@ -1065,7 +1075,9 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
                 mgi[c] = 0;
             }
         }
-        unsigned b1[4] = {NONE, NONE, NONE, NONE}, b2[4] = {NONE, NONE, NONE, NONE};
+        unsigned b1[NC], b2[NC];
+#pragma unroll
+        for (int c = 0; c < NC; c++) { b1[c] = NONE; b2[c] = NONE; }
         // candidate tile loads, double-buffered in registers so the next tile's
         // L2 traffic overlaps this tile's mma + epilogue
         struct Tile {
@@ -1096,9 +1108,10 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
             float2 p0 = cur.p0, p1 = cur.p1;
             if (!cm0) { p0.x = 1e30f; p0.y = 1e30f; }
             if (!cm1) { p1.x = 1e30f; p1.y = 1e30f; }
-            int acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+            int acc[SG_NT][4];
 #pragma unroll
-            for (int nt = 0; nt < 2; nt++) {
+            for (int nt = 0; nt < SG_NT; nt++) {
+                acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0;
                 mma_u8(acc[nt], x00.x, x10.x, x00.y, x10.y, bw[nt][0], bw[nt][1]);
                 mma_u8(acc[nt], x00.z, x10.z, x00.w, x10.w, bw[nt][2], bw[nt][3]);
                 mma_u8(acc[nt], x01.x, x11.x, x01.y, x11.y, bw[nt][4], bw[nt][5]);
@@ -1106,10 +1119,11 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
             }
             // band test for all 8 elements first (straight-line code); the exact
             // fp64 value is needed only inside [d - eps, d + eps] (rare, warp-uniform check)
-            bool inb[8], unc[8];
+            constexpr int NE = 4 * SG_NT;
+            bool inb[NE], unc[NE];
             bool any_unc = false;
 #pragma unroll
-            for (int e = 0; e < 8; e++) {
+            for (int e = 0; e < NE; e++) {
                 const int c = (e >> 2) * 2 + (e & 1);
                 const float2 P = (e & 2) ? p1 : p0;
                 const float av = fabsf(fmaf(la[c], P.x, fmaf(lb[c], P.y, lc[c])));
@@ -1119,7 +1133,7 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
             }
             if (__any_sync(FULL, any_unc)) {
 #pragma unroll
-                for (int e = 0; e < 8; e++) {
+                for (int e = 0; e < NE; e++) {
                     if (!unc[e]) continue;
                     const int c = (e >> 2) * 2 + (e & 1);
                     const float2 P = (e & 2) ? p1 : p0;
@@ -1131,7 +1145,7 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
             }
             bool any0 = false, any1 = false;
 #pragma unroll
-            for (int e = 0; e < 8; e++) {
+            for (int e = 0; e < NE; e++) {
                 const int nt = e >> 2, q = e & 3, c = nt * 2 + (q & 1);
                 const bool rowhi = q >= 2;
                 const unsigned cm = rowhi ? cm1 : cm0;
@@ -1154,7 +1168,7 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
         }
         // reduce across the 8 lanes sharing t
 #pragma unroll
-        for (int c = 0; c < 4; c++) {
+        for (int c = 0; c < NC; c++) {
 #pragma unroll
             for (int o = 4; o < 32; o <<= 1) {
                 unsigned o1 = __shfl_xor_sync(FULL, b1[c], o);
@@ -1164,7 +1178,7 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
         }
         if (g == 0) {
 #pragma unroll
-            for (int c = 0; c < 4; c++) {
+            for (int c = 0; c < NC; c++) {
                 if (mslot[c] < 0) continue;
                 unsigned long long best = ~0ull;
                 unsigned sec = NONE;
@@ -1200,7 +1214,7 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
 }
 
 template <bool STATS>
-__global__ void __launch_bounds__(WARPS * 32, 4) match_kernel(ChunkArgs a) {
+__global__ void __launch_bounds__(WARPS * 32, MATCH_MINB) match_kernel(ChunkArgs a) {
     __shared__ WarpSmem smem[WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpSmem& S = smem[warp];
@@ -1377,7 +1391,7 @@ __global__ void __launch_bounds__(256) compact_kernel(ChunkArgs a) {
         if (i < nq) {
             tid = a.res_tid[s0 + i];
             if (tid >= 0) {
-                qid = a.qlist[q0 + i];
+                qid = a.q_fid[s0 + i];
                 dist = a.res_dist[s0 + i];
                 const unsigned long long key =
                     ((unsigned long long)__float_as_uint(dist) << 32) | (unsigned)qid;
@@ -1398,6 +1412,35 @@ __global__ void __launch_bounds__(256) compact_kernel(ChunkArgs a) {
     if (threadIdx.x == 0) a.out_count[pg] = carry;
 }
 
+// pack the per-pair match segments into contiguous 16-B rows:
+// (pair, q | t << 16, dist bits, ratio bits)
+__global__ void pack_scan_kernel(const int32_t* __restrict__ count, int n_pairs,
+                                 int64_t* __restrict__ out_off) {
+    __shared__ int sm[SCAN_T / 32 + 1];
+    long long carry = 0;
+    for (int b0 = 0; b0 < n_pairs; b0 += SCAN_T) {
+        const int p = b0 + threadIdx.x;
+        const int v = p < n_pairs ? count[p] : 0;
+        int tot;
+        const int ex = block_exclusive_scan<SCAN_T>(v, &tot, sm);
+        if (p < n_pairs) out_off[p] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) out_off[n_pairs] = carry;
+}
+
+__global__ void pack_kernel(const int64_t* __restrict__ qlist_off, const int32_t* __restrict__ count,
+                            const int64_t* __restrict__ out_off, const int32_t* __restrict__ q,
+                            const int32_t* __restrict__ t, const float* __restrict__ dist,
+                            const float* __restrict__ ratio, int4* __restrict__ rows) {
+    const int p = blockIdx.x;
+    const int64_t src = qlist_off[p], dst = out_off[p];
+    const int c = count[p];
+    for (int i = threadIdx.x; i < c; i += blockDim.x)
+        rows[dst + i] = make_int4(p, (q[src + i] & 0xffff) | (t[src + i] << 16),
+                                  __float_as_int(dist[src + i]), __float_as_int(ratio[src + i]));
+}
+
 // workspace plan for one chunk
 struct ChunkSizes {
     int64_t P, Q, T, NT;
@@ -1410,7 +1453,7 @@ size_t chunk_bytes(const ChunkSizes& c) {
     b += aligned_bytes<float4>(c.Q) * 2 + aligned_bytes<int2>(c.Q);   // gline, gend, sglist
     b += aligned_bytes<unsigned long long>(c.T);       // tab_key
     b += aligned_bytes<unsigned>(c.T) * 2;             // tab_rep, tab_cnt
-    b += aligned_bytes<int32_t>(c.Q);                  // q_tab
+    b += aligned_bytes<int32_t>(c.Q) * 2;              // q_tab, q_fid
     b += aligned_bytes<double>(3 * c.Q);               // q_line
     b += aligned_bytes<int4>(c.Q);                     // grec
     b += aligned_bytes<int32_t>(c.Q) * 2;              // gfill, members
@@ -1457,6 +1500,24 @@ extern "C" int msfm_feature_norms(const uint8_t* d_desc, int64_t n, int32_t* d_n
     norms_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(d_desc, n, d_norm2);
     MSFM_LAUNCH_CHECK();
     count_launches(1);
+    return MSFM_OK;
+}
+
+extern "C" int msfm_pack_matches(int32_t n_pairs, const int64_t* d_qlist_off,
+                                 const int32_t* d_count, const int32_t* d_q, const int32_t* d_t,
+                                 const float* d_dist, const float* d_ratio, int64_t* d_out_off,
+                                 int32_t* d_rows, void* stream) {
+    if (n_pairs < 0) {
+        set_error("msfm_pack_matches: bad arguments");
+        return MSFM_EINVAL;
+    }
+    if (n_pairs == 0) return MSFM_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    pack_scan_kernel<<<1, SCAN_T, 0, st>>>(d_count, n_pairs, d_out_off);
+    pack_kernel<<<n_pairs, 128, 0, st>>>(d_qlist_off, d_count, d_out_off, d_q, d_t, d_dist, d_ratio,
+                                         reinterpret_cast<int4*>(d_rows));
+    MSFM_LAUNCH_CHECK();
+    count_launches(2);
     return MSFM_OK;
 }
 
@@ -1552,7 +1613,8 @@ extern "C" size_t msfm_guided_workspace_bytes(int32_t n_pairs, const int64_t* h_
 extern "C" int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids, int32_t n_pairs,
                                  const int32_t* d_pair_q, const int32_t* d_pair_t,
                                  const double* d_pair_F, const int64_t* d_qlist_off,
-                                 const int32_t* d_qlist, const int64_t* h_qlist_off,
+                                 const int32_t* d_qlist, const int64_t* d_qlist_src,
+                                 const int64_t* h_qlist_off,
                                  const msfm_match_params* prm, int32_t* d_out_q, int32_t* d_out_t,
                                  float* d_out_dist, float* d_out_ratio, int32_t* d_out_count,
                                  int64_t* d_stats, void* d_workspace, size_t workspace_bytes,
@@ -1601,7 +1663,8 @@ extern "C" int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids,
         a.sg_tau = e ? (float)atof(e) : SG_TAU;
     }
     a.pair_q = d_pair_q; a.pair_t = d_pair_t; a.pair_F = d_pair_F;
-    a.qlist_off = d_qlist_off; a.qlist = d_qlist;
+    a.qlist_off = d_qlist_off; a.qlist = d_qlist; a.qlist_src = d_qlist_src;
+    a.q_fid = ar.take<int32_t>(w.Q);
     a.tab_off = ar.take<int64_t>(w.P + 1); a.tbase = ar.take<int64_t>(w.P + 1);
     a.ngroups = ar.take<int32_t>(w.P + 1); a.gstart = ar.take<int32_t>(w.P + 1);
     a.nmem = ar.take<int32_t>(w.P + 1); a.sgstart = ar.take<int32_t>(w.P + 1);
@@ -1644,8 +1707,8 @@ extern "C" int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids,
         }
         {
             ProfScope ps("match_kernel", st);
-            if (d_stats) match_kernel<true><<<nsm * 4, WARPS * 32, 0, st>>>(a);
-            else         match_kernel<false><<<nsm * 4, WARPS * 32, 0, st>>>(a);
+            if (d_stats) match_kernel<true><<<nsm * MATCH_MINB, WARPS * 32, 0, st>>>(a);
+            else         match_kernel<false><<<nsm * MATCH_MINB, WARPS * 32, 0, st>>>(a);
         }
         compact_kernel<<<a.npairs, 256, 0, st>>>(a);
         MSFM_LAUNCH_CHECK();

@@ -24,6 +24,10 @@ RATIO_GUIDED = 0.8       # matching.py:22
 SINGLE_CANDIDATE_CAP = 45.0  # matching.py:27
 
 
+# one packed match row (msfm_pack_matches): 16 bytes, little-endian
+MATCH_ROW = np.dtype([("pair", "<i4"), ("q", "<u2"), ("t", "<u2"), ("dist", "<f4"), ("ratio", "<f4")])
+
+
 @dataclass
 class PairMatches:
     """Device-resident output of ``match_pairs`` (per-pair segments)."""
@@ -36,17 +40,44 @@ class PairMatches:
     qoff: np.ndarray  # host int64 (n_pairs+1,)
     stats: "object"   # int64 (n_pairs, 2) or None
 
-    def to_host(self):
-        """Concatenated (pair_index, q, t, dist, ratio) numpy arrays in pair order."""
+    def packed(self, stream=None):
+        """Device (rows int32 (total, 4), total): contiguous 16-B match rows in pair order
+        (pair, q | t << 16, dist bits, ratio bits), packed on the device."""
         import torch
 
-        cnt = self.count.cpu().numpy().astype(np.int64)
-        idx = np.concatenate([np.arange(self.qoff[k], self.qoff[k] + cnt[k])
-                              for k in range(len(cnt))]) if len(cnt) else np.zeros(0, np.int64)
-        sel = torch.from_numpy(idx).to(self.q.device)
-        pair = np.repeat(np.arange(len(cnt)), cnt)
-        return (pair, self.q[sel].cpu().numpy(), self.t[sel].cpu().numpy(),
-                self.dist[sel].cpu().numpy(), self.ratio[sel].cpu().numpy())
+        lib = _lib.load()
+        P = self.count.numel()
+        dev = self.q.device
+        off = torch.empty(P + 1, dtype=torch.int64, device=dev)
+        rows = torch.empty((max(self.q.numel(), 1), 4), dtype=torch.int32, device=dev)
+        _lib.check(lib.msfm_pack_matches(P, _lib.ptr(self._qoff_d), _lib.ptr(self.count),
+                                         _lib.ptr(self.q), _lib.ptr(self.t), _lib.ptr(self.dist),
+                                         _lib.ptr(self.ratio), _lib.ptr(off), _lib.ptr(rows),
+                                         _lib.stream_handle(stream)), "msfm_pack_matches")
+        total = int(off[P].item())
+        return rows[:total], total
+
+    def rows_host(self, pinned=None):
+        """Host structured array (MATCH_ROW: pair, q, t, dist, ratio) in pair order:
+        one device-side pack and one D2H copy.  With ``pinned`` (int32 (>=total, 4),
+        pinned) the result is a zero-copy view of that buffer."""
+        import torch
+
+        if self.count.numel() == 0:
+            return np.zeros(0, MATCH_ROW)
+        rows, total = self.packed()
+        if pinned is None or pinned.shape[0] < total:
+            pinned = torch.empty((max(total, 1), 4), dtype=torch.int32, pin_memory=True)
+        host = pinned[:total]
+        host.copy_(rows, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return host.numpy().view(MATCH_ROW).reshape(total)
+
+    def to_host(self, pinned=None):
+        """Concatenated (pair_index, q, t, dist, ratio) numpy arrays in pair order."""
+        r = self.rows_host(pinned)
+        return (r["pair"].astype(np.int64), r["q"].astype(np.int32), r["t"].astype(np.int32),
+                r["dist"].copy(), r["ratio"].copy())
 
 
 def match_pairs(bank: FeatureBank, q_img, t_img, F, query_lists, *, d: float = BAND_D_PX,
@@ -70,7 +101,8 @@ def match_pairs(bank: FeatureBank, q_img, t_img, F, query_lists, *, d: float = B
     dev = bank.device
     if device_inputs is None:
         device_inputs = prepare_pairs(bank, q_img, t_img, F, query_lists)
-    pq, pt, pF, qoff_d, qlist_d, qoff = device_inputs
+    pq, pt, pF, qoff_d, qlist_d, qoff = device_inputs[:6]
+    qsrc_d = device_inputs[6] if len(device_inputs) > 6 else None
     nq_total = int(qoff[-1]) if P else 0
     grid = bank.grid(D, stream)
     prm = _lib.MatchParams(float(d), float(np.float32(ratio)), float(np.float32(single_cap)),
@@ -88,18 +120,22 @@ def match_pairs(bank: FeatureBank, q_img, t_img, F, query_lists, *, d: float = B
     b, g = bank.cstruct(), grid.cstruct()
     _lib.check(lib.msfm_guided_match(ctypes.byref(b), ctypes.byref(g), P, _lib.ptr(pq), _lib.ptr(pt),
                                      _lib.ptr(pF), _lib.ptr(qoff_d), _lib.ptr(qlist_d),
-                                     qoff_c.ctypes.data, ctypes.byref(prm), _lib.ptr(out_q),
+                                     _lib.ptr(qsrc_d), qoff_c.ctypes.data, ctypes.byref(prm), _lib.ptr(out_q),
                                      _lib.ptr(out_t), _lib.ptr(out_d), _lib.ptr(out_r),
                                      _lib.ptr(out_c), _lib.ptr(stats), _lib.ptr(ws), ws_bytes,
                                      _lib.stream_handle(stream)),
                "msfm_guided_match")
     res = PairMatches(out_q, out_t, out_d, out_r, out_c[:P], qoff, stats)
+    res._qoff_d = qoff_d
     res._keep = (ws, device_inputs)
     return res
 
 
 def prepare_pairs(bank: FeatureBank, q_img, t_img, F, query_lists):
-    """Stage the pair table on the device (index translation + one copy per array)."""
+    """Stage the pair table on the device (index translation + one copy per array).
+
+    Query lists passed as the same object for several pairs (every pair of one
+    query image, densify.py:150-158) are uploaded once and shared."""
     import torch
 
     P = len(q_img)
@@ -109,16 +145,22 @@ def prepare_pairs(bank: FeatureBank, q_img, t_img, F, query_lists):
     lens = np.array([len(x) for x in query_lists], dtype=np.int64)
     qoff = np.zeros(P + 1, dtype=np.int64)
     np.cumsum(lens, out=qoff[1:])
-    qlist = np.concatenate([np.asarray(x, dtype=np.int32) for x in query_lists]) \
-        if P else np.zeros(0, np.int32)
+    uniq, src = {}, np.zeros(max(P, 1), dtype=np.int64)
+    parts, n = [], 0
+    for k, x in enumerate(query_lists):
+        s = uniq.get(id(x))
+        if s is None:
+            s = uniq[id(x)] = n
+            parts.append(np.asarray(x, dtype=np.int32))
+            n += len(x)
+        src[k] = s
+    qlist = np.concatenate(parts) if n else np.zeros(1, np.int32)
     dev = bank.device
 
     def up(a):
         return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().to(dev, non_blocking=True)
 
-    return (up(qi), up(ti), up(Fh), up(qoff), up(qlist if len(qlist) else np.zeros(1, np.int32)),
-            qoff)
-
+    return (up(qi), up(ti), up(Fh), up(qoff), up(qlist), qoff, up(src))
 
 # ---------------------------------------------------------------------------
 # drop-in for msfm.guided.guided_match_pair

@@ -133,3 +133,30 @@ def test_8k_scene_matches_oracle(n_cams, seed_pairs):
         np.testing.assert_array_equal(stats[j], ost)
         total += len(oq)
     assert total > 1000
+
+
+def test_shared_query_lists_and_packed_rows():
+    """Pairs that pass one list object share its upload (d_qlist_src); the
+    result, packed on the device into 16-B rows, must not depend on it."""
+    from paper_1512_06235_b200 import scenes
+    from paper_1512_06235_b200.guided import MATCH_ROW, match_pairs
+
+    scene, snap = scenes.build("C1", n_cameras=10)
+    wl = scenes.pair_workload(scene, snap)
+    ok = np.flatnonzero(wl.valid)
+    bank = _bank(scene.feature_sets)
+    shared = [wl.untracked[int(wl.q_img[k])] for k in ok]
+    copied = [np.array(x, copy=True) for x in shared]
+    a = match_pairs(bank, wl.q_img[ok], wl.t_img[ok], wl.F[ok], shared, chunk_pairs=3)
+    b = match_pairs(bank, wl.q_img[ok], wl.t_img[ok], wl.F[ok], copied)
+    ra, rb = a.rows_host(), b.rows_host()
+    assert ra.dtype == MATCH_ROW and len(ra) > 100
+    np.testing.assert_array_equal(ra.view(np.int32), rb.view(np.int32))
+    pk, q, t, d, r = b.to_host()
+    np.testing.assert_array_equal(pk, ra["pair"])
+    np.testing.assert_array_equal(q, ra["q"])
+    np.testing.assert_array_equal(t, ra["t"])
+    np.testing.assert_array_equal(d, ra["dist"])
+    assert np.all(np.diff(pk) >= 0)
+    cnt = b.count.cpu().numpy()
+    np.testing.assert_array_equal(np.bincount(pk, minlength=len(ok)), cnt)
