@@ -10,6 +10,7 @@ same kernels on a two-image bank.
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -167,6 +168,7 @@ def prepare_pairs(bank: FeatureBank, q_img, t_img, F, query_lists):
 # ---------------------------------------------------------------------------
 
 _BANK_CACHE: dict = {}
+_DROPIN_LOCK = threading.Lock()   # densify.py:232-236 may call from a thread pool
 
 
 def _pair_bank(query_fs, target_fs):
@@ -220,11 +222,12 @@ def guided_match_pair(query_fs, target_fs, geom, *, d: float = BAND_D_PX,
         tfs = _Sub(target_fs, ti)
         bank = FeatureBank({0: query_fs, 1: tfs})
     F = np.asarray(geom.F if hasattr(geom, "F") else geom, dtype=np.float64).reshape(1, 3, 3)
-    res = match_pairs(bank, [0], [1], F, [qi.astype(np.int32)], d=d, ratio=ratio,
-                      grid_d=D, single_cap=single_cap, with_stats=stats is not None)
-    _, q, t, dist, rat = res.to_host()
+    with _DROPIN_LOCK:
+        res = match_pairs(bank, [0], [1], F, [qi.astype(np.int32)], d=d, ratio=ratio,
+                          grid_d=D, single_cap=single_cap, with_stats=stats is not None)
+        _, q, t, dist, rat = res.to_host()
+        s = res.stats.cpu().numpy() if stats is not None else None
     if stats is not None:
-        s = res.stats.cpu().numpy()
         stats.add(int(s[0, 0]), int(s[0, 1]))
     qimg, timg = query_fs.image_id, target_fs.image_id
     return [Match(query=FeatureRef(qimg, int(a)), target=FeatureRef(timg, int(ti[b])),

@@ -122,7 +122,50 @@ def pnp_cases():
     np.savez_compressed(os.path.join(HERE, "pnp_cases.npz"), **out)
 
 
+def ranked_cases():
+    """ranked_2d2d_search (localize.py:125-176) on the hold-out recipe of
+    test_localize.py:18-38, exact index, plus the copied-image case of
+    test_localize.py:201-221 and the below-gate case."""
+    import dataclasses
+
+    from msfm.matching import Edge, Match, MatchGraph, build_coarse_matchgraph
+    from msfm.localize import ranked_2d2d_search
+
+    kw = dict(n_cameras=12, n_points=700, visibility_fraction=0.7, pixel_noise=0.3,
+              descriptor_noise=3.0, seed=77)
+    scene = generate_scene(SceneSpec(**kw))
+    store = scene.store()
+    graph = build_coarse_matchgraph(store.sets)
+    model = partial_model(scene, range(9))
+    out = {"spec": np.array(repr(kw)), "registered": np.arange(9), "eta": np.array(-1.0)}
+    edges = sorted(graph.edges)
+    out["edges"] = np.array([[a, b, len(graph.edges[(a, b)].matches)] for a, b in edges], np.int64)
+    for q in (9, 10, 11):
+        fs = store.sets[q]
+        idx = DescriptorIndex(fs.descriptors_f32(), exact_threshold=10**9)
+        corr = ranked_2d2d_search(model, graph, q, fs, store, index=idx)
+        out[f"r{q}_corr"] = np.array(corr, dtype=np.int32).reshape(-1, 2)
+        strict = ranked_2d2d_search(model, graph, q, fs, store, ratio=1e-6,
+                                    index=DescriptorIndex(fs.descriptors_f32(), exact_threshold=10**9))
+        out[f"r{q}_strict_n"] = np.array(len(strict))
+    source = model.image_ids()[0]
+    fs = dataclasses.replace(store[source], image_id=97)
+    g = MatchGraph()
+    key = (min(97, source), max(97, source))
+    g.edges[key] = Edge(matches=[Match(query=FeatureRef(key[0], i), target=FeatureRef(key[1], i),
+                                       distance=0.0, ratio=0.0) for i in range(40)])
+    corr = ranked_2d2d_search(model, g, 97, fs, store,
+                              index=DescriptorIndex(fs.descriptors_f32(), exact_threshold=10**9))
+    out["copy_source"] = np.array(source)
+    out["copy_corr"] = np.array(corr, dtype=np.int32).reshape(-1, 2)
+    np.savez_compressed(os.path.join(HERE, "localize_ranked.npz"), **out)
+    print("ranked", {q: len(out[f"r{q}_corr"]) for q in (9, 10, 11)}, "copy", len(corr))
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["ranked"]:
+        ranked_cases()
+        sys.exit(0)
     # reference unit-test style hold-out (test_localize.py:18-38): last 3 cameras removed
     run("localize_holdout.npz", dict(n_cameras=12, n_points=700, visibility_fraction=0.7,
                                      pixel_noise=0.3, descriptor_noise=3.0, seed=77),

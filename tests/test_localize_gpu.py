@@ -107,3 +107,44 @@ def test_localize_all_raises_like_reference_on_overflow():
     K = {i: scene.cameras[i].K for i in store.sets}
     with pytest.raises(OverflowError):
         localize_all(model, store, _NoGraph(), K)
+
+
+class _EdgeGraph:
+    """MatchGraph stand-in carrying the reference graph's edge counts."""
+
+    def __init__(self, edges):
+        self.count = {(int(a), int(b)): int(c) for a, b, c in edges}
+
+    def neighbors(self, image_id):
+        return sorted([b for a, b in self.count if a == image_id] +
+                      [a for a, b in self.count if b == image_id])
+
+    def match_count(self, a, b):
+        return self.count.get((min(a, b), max(a, b)), 0)
+
+
+def test_ranked_2d2d_equals_reference():
+    """ranked_2d2d_search (localize.py:125-176) through the device kNN: same
+    correspondences as the reference with its exact index."""
+    import dataclasses
+
+    from paper_1512_06235_b200 import scenes
+    from paper_1512_06235_b200.localize import ranked_2d2d_search
+    from paper_1512_06235_b200.types import InsufficientDataError
+
+    kw, scene, snap, z = load_localize("localize_ranked.npz")
+    model = scenes.snapshot_to_model(scene, snap)
+    store = scene.store()
+    graph = _EdgeGraph(z["edges"])
+    for q in (9, 10, 11):
+        corr = ranked_2d2d_search(model, graph, q, store.sets[q], store)
+        assert [tuple(c) for c in z[f"r{q}_corr"].tolist()] == corr
+        strict = ranked_2d2d_search(model, graph, q, store.sets[q], store, ratio=1e-6)
+        assert len(strict) == int(z[f"r{q}_strict_n"]) == 0
+    src = int(z["copy_source"])
+    fs = dataclasses.replace(store.sets[src], image_id=97)
+    g = _EdgeGraph([(min(97, src), max(97, src), 40)])
+    corr = ranked_2d2d_search(model, g, 97, fs, store)
+    assert [tuple(c) for c in z["copy_corr"].tolist()] == corr
+    with pytest.raises(InsufficientDataError):
+        ranked_2d2d_search(model, _EdgeGraph([]), 9, store.sets[9], store)

@@ -23,5 +23,6 @@ for r in rows:
     a[0] += ex; a[1] += smp
 tot_i = sum(v[0] for v in agg.values()) or 1; tot_s = sum(v[1] for v in agg.values()) or 1
 print(f"total warp-instr {tot_i}, stall samples {tot_s}")
-for (ln, src), (i, s) in sorted(agg.items(), key=lambda x: -x[1][1])[:int(sys.argv[2]) if len(sys.argv) > 2 else 45]:
+KEY = 0 if "--by-instr" in sys.argv else 1
+for (ln, src), (i, s) in sorted(agg.items(), key=lambda x: -x[1][KEY])[:45]:
     print(f"{ln:5d} instr {i/tot_i*100:5.1f}%  stall {s/tot_s*100:5.1f}%  {src}")
