@@ -12,7 +12,7 @@ import os
 from .types import DeviceUnavailableError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmsfm_b200.so")
+LIB_PATH = os.environ.get("MSFM_LIB_VARIANT") or os.path.join(_HERE, "libmsfm_b200.so")
 
 c_int32_p = ctypes.POINTER(ctypes.c_int32)
 VP = ctypes.c_void_p
@@ -27,7 +27,7 @@ class Bank(ctypes.Structure):
 class Grids(ctypes.Structure):
     _fields_ = [("d_sub", VP), ("d_dims", VP), ("d_roff", VP), ("d_coff", VP),
                 ("d_rstart", VP), ("d_cstart", VP), ("d_rmem", VP), ("d_cmem", VP),
-                ("D", ctypes.c_double)]
+                ("d_rxy", VP), ("d_cxy", VP), ("D", ctypes.c_double)]
 
 
 class MatchParams(ctypes.Structure):
@@ -49,7 +49,7 @@ _SIGS = {
     "msfm_grid_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int64]),
     "msfm_grid_build": (ctypes.c_int, [ctypes.POINTER(Bank), VP, VP, VP, ctypes.c_int64,
                                        ctypes.c_int64, ctypes.c_double, VP, VP, VP, VP, VP,
-                                       VP, ctypes.c_size_t, VP]),
+                                       VP, VP, VP, ctypes.c_size_t, VP]),
     "msfm_ransac_samples": (ctypes.c_int, [VP, ctypes.c_int32, ctypes.c_uint32, ctypes.c_int64,
                                            ctypes.c_int32, ctypes.c_int32, VP, VP]),
     "msfm_knn_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),

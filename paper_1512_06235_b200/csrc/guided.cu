@@ -188,7 +188,7 @@ struct GridBuildArgs {
     const float2* xy; const int64_t* img_off; const int32_t* img_n; const int32_t* img_wh;
     const int32_t* dims; const int64_t* roff; const int64_t* coff;
     int32_t* sub; int32_t* rcount; int32_t* ccount; int32_t* rcur; int32_t* ccur;
-    int32_t* rmem; int32_t* cmem; double D;
+    int32_t* rmem; int32_t* cmem; float2* rxy; float2* cxy; double D;
 };
 
 __device__ __forceinline__ int bucket_of(float v, double D, int nb) {
@@ -223,6 +223,8 @@ __global__ void grid_scatter_kernel(GridBuildArgs a) {
         int c = atomicAdd(&a.ccur[a.coff[img] + (int64_t)bx * nby + by], 1);
         a.rmem[r] = f;
         a.cmem[c] = f;
+        a.rxy[r] = p;
+        a.cxy[c] = p;
     }
 }
 
@@ -340,6 +342,7 @@ struct ChunkArgs {
     // index
     const int32_t* sub; const int32_t* dims; const int64_t* roff; const int64_t* coff;
     const int32_t* rstart; const int32_t* cstart; const int32_t* rmem; const int32_t* cmem;
+    const float2* rxy; const float2* cxy;
     double D, d;
     float ratio, single_cap;
     int stats_mode;              // 1: one super-group per group (exact SearchStats)
@@ -955,12 +958,15 @@ __device__ __forceinline__ bool in_cprime(const ChunkArgs& a, const GroupRec& G,
 }
 
 struct alignas(16) WarpSmem {
+    float2 xy[CAP];              // candidate positions (from the bucket-ordered copy)
     unsigned short list[CAP];    // candidate feature ids (target-local)
     unsigned short cmask[CAP];   // per candidate: groups (bit gi) whose C' contains it
     unsigned short ulist[CAP];   // positions still to decide
     unsigned sure[CAP / 32];     // candidate in C' of every group of the super-group
     unsigned anyb[CAP / 8];      // stats: candidate inside some member band
     SGRec sg;                    // this warp's super-group (broadcast reads)
+    float4 gl[SG_MAX_GROUPS];    // per group: rep line (fp32), member-band reach
+    MemberRec mr[SG_MEMBERS];    // the super-group's members (when mcnt <= SG_MEMBERS)
     int gbeg[SG_MAX_GROUPS + 1]; // member range of each group within the super-group
 };
 
@@ -972,11 +978,12 @@ __device__ __forceinline__ bool band_exact(double A, double B, double C, bool ge
     return fabs(v) <= d;
 }
 
-__device__ __forceinline__ bool member_band(const ChunkArgs& a, const GroupRec& G,
-                                            const MemberRec& M, float x, float y) {
+__device__ __forceinline__ bool member_band(const ChunkArgs& a, int gid, const MemberRec& M,
+                                            float x, float y) {
     const float v = fabsf(fmaf(M.a, x, fmaf(M.b, y, M.c)));
     if (v <= M.lo) return true;
     if (v > M.hi) return false;
+    const GroupRec& G = a.grp[gid];
     if (G.cnt == 1) return band_exact(G.sl0, G.sl1, G.sl2, true, x, y, a.d);
     const double* L = a.q_line + 3 * (int64_t)(M.slotgi & 0xFFFFFF);
     return band_exact(L[0], L[1], L[2], false, x, y, a.d);
@@ -988,7 +995,7 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const SGRec& SG = S.sg;
     const int m = SG.mcnt;
-    const MemberRec* MR = a.mrec + SG.m0;
+    const MemberRec* MR = m <= SG_MEMBERS ? S.mr : a.mrec + SG.m0;
     const unsigned all_groups = (1u << SG.gcnt) - 1u;
     // ---- per-group C' bits of the candidates not surely inside every group's C'
     int nu = 0;
@@ -1012,22 +1019,24 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
         if (uj < nu) {
             const int j = S.ulist[uj];
             const int f = S.list[j];
-            const float2 p2 = a.xy[toff + f];
+            const float2 p2 = S.xy[j];
             const bool inner = p2.x >= SG.border && p2.x <= SG.W - SG.border &&
                                p2.y >= SG.border && p2.y <= SG.H - SG.border;
             unsigned bits = 0;
             for (int gi = 0; gi < SG.gcnt; gi++) {
-                const GroupRec& G = a.grp[SG.g0 + gi];
-                if (G.K < 0) continue;
-                const float dg = fabsf(fmaf(G.ar, p2.x, fmaf(G.br, p2.y, G.cr)));
+                // gl: rep line and member reach; a group whose line misses the image
+                // (K < 0) has gl = (0, 0, 1e30) and is never taken
+                const float4 gl = S.gl[gi];
+                const float dg = fabsf(fmaf(gl.x, p2.x, fmaf(gl.y, p2.y, gl.z)));
                 if (dg <= SG.hsure && inner) { bits |= 1u << gi; continue; }
                 // outside every member band of this group: the bit is never consulted
-                if (dg > (float)a.d + G.maxdev + 0.05f) continue;
+                if (dg > gl.w) continue;
                 bool any = false;
                 for (int k = S.gbeg[gi]; k < S.gbeg[gi + 1] && !any; k++)
-                    any = member_band(a, G, MR[k], p2.x, p2.y);
+                    any = member_band(a, SG.g0 + gi, MR[k], p2.x, p2.y);
                 if (any && a.dbg) atomicAdd(&a.dbg[6], 1ull);
-                if (any && in_cprime(a, G, SG, p2.x, p2.y, toff, f)) bits |= 1u << gi;
+                if (any && in_cprime(a, a.grp[SG.g0 + gi], SG, p2.x, p2.y, toff, f))
+                    bits |= 1u << gi;
             }
             S.cmask[j] = (unsigned short)bits;
         }
@@ -1085,24 +1094,23 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
             float2 p0, p1;
             unsigned tb0, tb1, cm0, cm1;
         };
+        const uint4* tdesc = reinterpret_cast<const uint4*>(a.desc + toff * 128) + 2 * t;
+        const int32_t* tnorm = a.norm2 + toff;
         auto load_tile = [&](int mt, Tile& T) {
             const int r0 = mt * 16 + g, r1 = r0 + 8;
-            T.cm0 = r0 < n ? S.cmask[r0] : 0u;
-            T.cm1 = r1 < n ? S.cmask[r1] : 0u;
-            const int f0 = r0 < n ? S.list[r0] : 0, f1 = r1 < n ? S.list[r1] : 0;
-            const uint4* row0 = reinterpret_cast<const uint4*>(a.desc + (toff + f0) * 128) + 2 * t;
-            const uint4* row1 = reinterpret_cast<const uint4*>(a.desc + (toff + f1) * 128) + 2 * t;
+            const bool v0 = r0 < n, v1 = r1 < n;
+            T.cm0 = v0 ? S.cmask[r0] : 0u;
+            T.cm1 = v1 ? S.cmask[r1] : 0u;
+            const int f0 = v0 ? S.list[r0] : 0, f1 = v1 ? S.list[r1] : 0;
+            const uint4* row0 = tdesc + 8 * f0;
+            const uint4* row1 = tdesc + 8 * f1;
             T.x00 = __ldg(row0); T.x01 = __ldg(row0 + 1);
             T.x10 = __ldg(row1); T.x11 = __ldg(row1 + 1);
-            T.p0 = a.xy[toff + f0]; T.p1 = a.xy[toff + f1];
-            T.tb0 = ((unsigned)a.norm2[toff + f0] << 9) | (unsigned)r0;
-            T.tb1 = ((unsigned)a.norm2[toff + f1] << 9) | (unsigned)r1;
+            T.p0 = S.xy[v0 ? r0 : 0]; T.p1 = S.xy[v1 ? r1 : 0];
+            T.tb0 = ((unsigned)__ldg(tnorm + f0) << 9) | (unsigned)r0;
+            T.tb1 = ((unsigned)__ldg(tnorm + f1) << 9) | (unsigned)r1;
         };
-        Tile nxt;
-        if (ntiles > 0) load_tile(0, nxt);
-        for (int mt = 0; mt < ntiles; mt++) {
-            const Tile cur = nxt;
-            if (mt + 1 < ntiles) load_tile(mt + 1, nxt);
+        auto do_tile = [&](int mt, const Tile& cur) {
             const uint4 x00 = cur.x00, x01 = cur.x01, x10 = cur.x10, x11 = cur.x11;
             const unsigned cm0 = cur.cm0, cm1 = cur.cm1, tb0 = cur.tb0, tb1 = cur.tb1;
             float2 p0 = cur.p0, p1 = cur.p1;
@@ -1165,6 +1173,14 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
                     S.anyb[2 * mt + 1] |= m1 & 0x11111111u;
                 }
             }
+        };
+        // two register tiles in flight: tile mt+1's loads overlap tile mt's mma + epilogue
+        Tile nxt;
+        if (ntiles > 0) load_tile(0, nxt);
+        for (int mt = 0; mt < ntiles; mt++) {
+            const Tile cur = nxt;
+            if (mt + 1 < ntiles) load_tile(mt + 1, nxt);
+            do_tile(mt, cur);
         }
         // reduce across the 8 lanes sharing t
 #pragma unroll
@@ -1237,8 +1253,15 @@ __global__ void __launch_bounds__(WARPS * 32, MATCH_MINB) match_kernel(ChunkArgs
             atomicAdd(&a.dbg[1], (unsigned long long)SG.mcnt);
             atomicAdd(&a.dbg[8], (unsigned long long)SG.gcnt);
         }
-        if (lane <= SG.gcnt)
+        if (lane <= SG.gcnt) {
             S.gbeg[lane] = lane < SG.gcnt ? max(a.grp[SG.g0 + lane].moff - SG.m0, 0) : SG.mcnt;
+            if (lane < SG.gcnt) {
+                const GroupRec& G = a.grp[SG.g0 + lane];
+                S.gl[lane] = G.K < 0 ? make_float4(0.f, 0.f, 1e30f, -1.f)
+                                     : make_float4(G.ar, G.br, G.cr, (float)a.d + G.maxdev + 0.05f);
+            }
+        }
+        if (SG.mcnt <= SG_MEMBERS && lane < SG.mcnt) S.mr[lane] = a.mrec[SG.m0 + lane];
         __syncwarp();
         const int pg = a.p0 + SG.p;
         const int ti = a.pair_t[pg], qi = a.pair_q[pg];
@@ -1247,6 +1270,7 @@ __global__ void __launch_bounds__(WARPS * 32, MATCH_MINB) match_kernel(ChunkArgs
         const int64_t toffb = SG.horiz ? a.roff[ti] : a.coff[ti];
         const int32_t* start = SG.horiz ? a.rstart : a.cstart;
         const int32_t* mem = SG.horiz ? a.rmem : a.cmem;
+        const float2* mxy = SG.horiz ? a.rxy : a.cxy;
         int n = 0;
         bool first_round = true;
         int cols_total = 0;
@@ -1295,9 +1319,11 @@ __global__ void __launch_bounds__(WARPS * 32, MATCH_MINB) match_kernel(ChunkArgs
                 const int oex = __shfl_sync(FULL, incl - len, o & 31);
                 bool pass = false, sure = false;
                 int f = 0;
+                float2 p2 = make_float2(0.f, 0.f);
                 if (j < tot) {
-                    f = mem[ob + (j - oex)];
-                    const float2 p2 = a.xy[toff + f];
+                    const int e = ob + (j - oex);
+                    f = mem[e];
+                    p2 = mxy[e];
                     const float adr = fabsf(fmaf(SG.ar, p2.x, fmaf(SG.br, p2.y, SG.cr)));
                     pass = adr <= SG.R;
                     sure = adr + SG.delta <= SG.hsure && p2.x >= SG.border &&
@@ -1320,7 +1346,10 @@ __global__ void __launch_bounds__(WARPS * 32, MATCH_MINB) match_kernel(ChunkArgs
                     __syncwarp();
                 }
                 const int k = __popc(bal & ((1u << lane) - 1u));
-                if (pass) S.list[n + k] = (unsigned short)f;
+                if (pass) {
+                    S.list[n + k] = (unsigned short)f;
+                    S.xy[n + k] = p2;
+                }
                 const unsigned bits = __reduce_or_sync(FULL, (pass && sure) ? (1u << k) : 0u);
                 if (lane == 0 && cnt) {
                     const int w = n >> 5, sh = n & 31;
@@ -1539,7 +1568,8 @@ extern "C" size_t msfm_grid_workspace_bytes(int64_t n_buckets_total) {
 extern "C" int msfm_grid_build(const msfm_bank* bank, const int32_t* d_dims, const int64_t* d_roff,
                                const int64_t* d_coff, int64_t n_buckets_total, int64_t n_total,
                                double D, int32_t* d_sub, int32_t* d_rstart, int32_t* d_cstart,
-                               int32_t* d_rmem, int32_t* d_cmem, void* d_workspace,
+                               int32_t* d_rmem, int32_t* d_cmem, float* d_rxy, float* d_cxy,
+                               void* d_workspace,
                                size_t workspace_bytes, void* stream) {
     if (!bank || !(D > 0) || n_buckets_total < 0 || n_total < 0) {
         set_error("msfm_grid_build: bad arguments (D=%g)", D);
@@ -1560,7 +1590,8 @@ extern "C" int msfm_grid_build(const msfm_bank* bank, const int32_t* d_dims, con
     if (bank->n_images == 0) return MSFM_OK;
     GridBuildArgs a{reinterpret_cast<const float2*>(bank->d_xy), bank->d_img_off, bank->d_img_n,
                     bank->d_img_wh, d_dims, d_roff, d_coff, d_sub, d_rstart, d_cstart, rcur, ccur,
-                    d_rmem, d_cmem, D};
+                    d_rmem, d_cmem, reinterpret_cast<float2*>(d_rxy),
+                    reinterpret_cast<float2*>(d_cxy), D};
     grid_count_kernel<<<bank->n_images, 256, 0, st>>>(a);
     MSFM_LAUNCH_CHECK();
     count_launches(1);
@@ -1656,6 +1687,8 @@ extern "C" int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids,
     a.img_off = bank->d_img_off; a.img_n = bank->d_img_n; a.img_wh = bank->d_img_wh;
     a.sub = grids->d_sub; a.dims = grids->d_dims; a.roff = grids->d_roff; a.coff = grids->d_coff;
     a.rstart = grids->d_rstart; a.cstart = grids->d_cstart; a.rmem = grids->d_rmem; a.cmem = grids->d_cmem;
+    a.rxy = reinterpret_cast<const float2*>(grids->d_rxy);
+    a.cxy = reinterpret_cast<const float2*>(grids->d_cxy);
     a.D = grids->D; a.d = prm->d; a.ratio = prm->ratio; a.single_cap = prm->single_cap;
     a.stats_mode = d_stats ? 1 : 0;
     {
