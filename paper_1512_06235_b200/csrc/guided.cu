@@ -331,7 +331,10 @@ struct alignas(16) SGRec {
 #endif
 constexpr int SG_NT = MSFM_SG_NT;          // n8 member tiles per super-group
 constexpr int SG_MEMBERS = 8 * SG_NT;
-constexpr int MATCH_MINB = SG_NT == 1 ? 6 : 4;   // resident CTAs (4 warps) per SM
+#ifndef MSFM_MATCH_MINB
+#define MSFM_MATCH_MINB (SG_NT == 1 ? 6 : 4)
+#endif
+constexpr int MATCH_MINB = MSFM_MATCH_MINB;   // resident CTAs (4 warps) per SM
 constexpr float SG_TAU = 16.0f;
 constexpr int SG_MAX_GROUPS = SG_MEMBERS;
 
@@ -969,6 +972,8 @@ struct alignas(16) WarpSmem {
     MemberRec mr[SG_MEMBERS];    // the super-group's members (when mcnt <= SG_MEMBERS)
     int gbeg[SG_MAX_GROUPS + 1]; // member range of each group within the super-group
 };
+static_assert(offsetof(WarpSmem, mr) % 16 == 0, "member records must be 16-B aligned");
+static_assert(sizeof(MemberRec) == 32, "MemberRec is read as two 16-B shared loads");
 
 // the reference's float64 band value for one (member, target) element, guided.py:447
 __device__ __forceinline__ bool band_exact(double A, double B, double C, bool gemv, double x,
@@ -987,6 +992,39 @@ __device__ __forceinline__ bool member_band(const ChunkArgs& a, int gid, const M
     if (G.cnt == 1) return band_exact(G.sl0, G.sl1, G.sl2, true, x, y, a.d);
     const double* L = a.q_line + 3 * (int64_t)(M.slotgi & 0xFFFFFF);
     return band_exact(L[0], L[1], L[2], false, x, y, a.d);
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// volatile shared loads: re-read per tile instead of pinning registers across the loop
+__device__ __forceinline__ float4 lds_f4(const void* p) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(smem_addr(p)));
+    return v;
+}
+__device__ __forceinline__ uint4 lds_u4(const void* p) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(smem_addr(p)));
+    return v;
+}
+
+// member block [mt0, mt0 + SG_MEMBERS) of the super-group into S.mr; columns past the
+// last member get a line that never passes the band test
+__device__ __forceinline__ void stage_members(const ChunkArgs& a, WarpSmem& S, int m0, int m, int mt0) {
+    const int lane = threadIdx.x & 31;
+    if (lane < SG_MEMBERS) {
+        MemberRec M;
+        if (mt0 + lane < m) {
+            M = a.mrec[m0 + mt0 + lane];
+        } else {
+            M.a = 0.f; M.b = 0.f; M.c = 1e30f; M.lo = -1.f; M.hi = -1.f;
+            M.qn9 = 0; M.fid = 0; M.slotgi = 0;
+        }
+        S.mr[lane] = M;
+    }
 }
 
 template <bool STATS>
@@ -1047,13 +1085,18 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
     __syncwarp();
     const int ntiles = (n + 15) >> 4;
     for (int mt0 = 0; mt0 < m; mt0 += SG_MEMBERS) {
+        if (m > SG_MEMBERS) {
+            __syncwarp();
+            stage_members(a, S, SG.m0, m, mt0);
+            __syncwarp();
+        }
         // B fragments: member mt0 + 8 nt + g of n-tile nt, bytes [32t, 32t+32)
         unsigned bw[SG_NT][8];
 #pragma unroll
         for (int nt = 0; nt < SG_NT; nt++) {
             const int j = mt0 + nt * 8 + g;
             if (j < m) {
-                const int fid = MR[j].fid;
+                const int fid = S.mr[nt * 8 + g].fid;
                 const uint4* row = reinterpret_cast<const uint4*>(a.desc + (qoff + fid) * 128) + 2 * t;
                 const uint4 v0 = __ldg(row), v1 = __ldg(row + 1);
                 bw[nt][0] = v0.x; bw[nt][1] = v0.y; bw[nt][2] = v0.z; bw[nt][3] = v0.w;
@@ -1063,27 +1106,9 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
                 for (int k = 0; k < 8; k++) bw[nt][k] = 0;
             }
         }
-        // epilogue columns: (nt, 2t + c) -> member mt0 + 8 nt + 2t + c
+        // epilogue columns: (nt, 2t + c) -> member mt0 + 8 nt + 2t + c; their constants
+        // are re-read from S.mr every tile (two 16-B shared loads per column)
         constexpr int NC = 2 * SG_NT;    // epilogue columns per lane
-        float la[NC], lb[NC], lc[NC], lo[NC], hi[NC];
-        unsigned qn9[NC];
-        int mslot[NC], mgi[NC];
-#pragma unroll
-        for (int c = 0; c < NC; c++) {
-            const int j = mt0 + (c >> 1) * 8 + 2 * t + (c & 1);
-            if (j < m) {
-                const MemberRec M = MR[j];
-                la[c] = M.a; lb[c] = M.b; lc[c] = M.c; lo[c] = M.lo; hi[c] = M.hi;
-                qn9[c] = M.qn9;
-                mslot[c] = M.slotgi & 0xFFFFFF;
-                mgi[c] = M.slotgi >> 24;
-            } else {
-                la[c] = 0.f; lb[c] = 0.f; lc[c] = 1e30f; lo[c] = -1.f; hi[c] = -1.f;
-                qn9[c] = 0;
-                mslot[c] = -1;
-                mgi[c] = 0;
-            }
-        }
         unsigned b1[NC], b2[NC];
 #pragma unroll
         for (int c = 0; c < NC; c++) { b1[c] = NONE; b2[c] = NONE; }
@@ -1091,29 +1116,35 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
         // L2 traffic overlaps this tile's mma + epilogue
         struct Tile {
             uint4 x00, x01, x10, x11;
-            float2 p0, p1;
-            unsigned tb0, tb1, cm0, cm1;
+            unsigned tb0, tb1;
         };
         const uint4* tdesc = reinterpret_cast<const uint4*>(a.desc + toff * 128) + 2 * t;
         const int32_t* tnorm = a.norm2 + toff;
         auto load_tile = [&](int mt, Tile& T) {
             const int r0 = mt * 16 + g, r1 = r0 + 8;
             const bool v0 = r0 < n, v1 = r1 < n;
-            T.cm0 = v0 ? S.cmask[r0] : 0u;
-            T.cm1 = v1 ? S.cmask[r1] : 0u;
             const int f0 = v0 ? S.list[r0] : 0, f1 = v1 ? S.list[r1] : 0;
             const uint4* row0 = tdesc + 8 * f0;
             const uint4* row1 = tdesc + 8 * f1;
             T.x00 = __ldg(row0); T.x01 = __ldg(row0 + 1);
             T.x10 = __ldg(row1); T.x11 = __ldg(row1 + 1);
-            T.p0 = S.xy[v0 ? r0 : 0]; T.p1 = S.xy[v1 ? r1 : 0];
             T.tb0 = ((unsigned)__ldg(tnorm + f0) << 9) | (unsigned)r0;
             T.tb1 = ((unsigned)__ldg(tnorm + f1) << 9) | (unsigned)r1;
         };
         auto do_tile = [&](int mt, const Tile& cur) {
             const uint4 x00 = cur.x00, x01 = cur.x01, x10 = cur.x10, x11 = cur.x11;
-            const unsigned cm0 = cur.cm0, cm1 = cur.cm1, tb0 = cur.tb0, tb1 = cur.tb1;
-            float2 p0 = cur.p0, p1 = cur.p1;
+            const unsigned tb0 = cur.tb0, tb1 = cur.tb1;
+            const int r0 = mt * 16 + g, r1 = r0 + 8;
+            const unsigned cm0 = r0 < n ? S.cmask[r0] : 0u, cm1 = r1 < n ? S.cmask[r1] : 0u;
+            float2 p0 = S.xy[r0 < n ? r0 : 0], p1 = S.xy[r1 < n ? r1 : 0];
+            float4 ML[NC];
+            uint4 MH[NC];
+#pragma unroll
+            for (int c = 0; c < NC; c++) {
+                const MemberRec* Mc = &S.mr[(c >> 1) * 8 + 2 * t + (c & 1)];
+                ML[c] = lds_f4(&Mc->a);      // a, b, c, lo
+                MH[c] = lds_u4(&Mc->hi);     // hi, qn9, fid, slotgi
+            }
             if (!cm0) { p0.x = 1e30f; p0.y = 1e30f; }
             if (!cm1) { p1.x = 1e30f; p1.y = 1e30f; }
             int acc[SG_NT][4];
@@ -1134,9 +1165,9 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
             for (int e = 0; e < NE; e++) {
                 const int c = (e >> 2) * 2 + (e & 1);
                 const float2 P = (e & 2) ? p1 : p0;
-                const float av = fabsf(fmaf(la[c], P.x, fmaf(lb[c], P.y, lc[c])));
-                inb[e] = av <= lo[c];
-                unc[e] = !inb[e] && av <= hi[c];
+                const float av = fabsf(fmaf(ML[c].x, P.x, fmaf(ML[c].y, P.y, ML[c].z)));
+                inb[e] = av <= ML[c].w;
+                unc[e] = !inb[e] && av <= __uint_as_float(MH[c].x);
                 any_unc |= unc[e];
             }
             if (__any_sync(FULL, any_unc)) {
@@ -1145,9 +1176,9 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
                     if (!unc[e]) continue;
                     const int c = (e >> 2) * 2 + (e & 1);
                     const float2 P = (e & 2) ? p1 : p0;
-                    const GroupRec& Gc = a.grp[SG.g0 + mgi[c]];
+                    const GroupRec& Gc = a.grp[SG.g0 + (int)(MH[c].w >> 24)];
                     const bool gemv = Gc.cnt == 1;
-                    const double* L = gemv ? &Gc.sl0 : a.q_line + 3 * (int64_t)mslot[c];
+                    const double* L = gemv ? &Gc.sl0 : a.q_line + 3 * (int64_t)(MH[c].w & 0xFFFFFFu);
                     inb[e] = band_exact(L[0], L[1], L[2], gemv, (double)P.x, (double)P.y, a.d);
                 }
             }
@@ -1157,9 +1188,9 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
                 const int nt = e >> 2, q = e & 3, c = nt * 2 + (q & 1);
                 const bool rowhi = q >= 2;
                 const unsigned cm = rowhi ? cm1 : cm0;
-                const bool in = inb[e] && ((cm >> mgi[c]) & 1u);
+                const bool in = inb[e] && ((cm >> (MH[c].w >> 24)) & 1u);
                 if (rowhi) any1 |= in; else any0 |= in;
-                const unsigned base = (rowhi ? tb1 : tb0) + qn9[c];
+                const unsigned base = (rowhi ? tb1 : tb0) + MH[c].y;
                 const unsigned key = in ? base - ((unsigned)acc[nt][q] << 10) : NONE;
                 top2_push(key, b1[c], b2[c]);
             }
@@ -1195,7 +1226,9 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
         if (g == 0) {
 #pragma unroll
             for (int c = 0; c < NC; c++) {
-                if (mslot[c] < 0) continue;
+                const int jj = (c >> 1) * 8 + 2 * t + (c & 1);
+                if (mt0 + jj >= m) continue;
+                const int mslot = S.mr[jj].slotgi & 0xFFFFFF;
                 unsigned long long best = ~0ull;
                 unsigned sec = NONE;
                 if (b1[c] != NONE) {
@@ -1205,16 +1238,16 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
                 }
                 if (b2[c] != NONE) sec = b2[c] >> 9;
                 if (!first_round) {
-                    const unsigned long long ob = a.mstate[mslot[c]];
-                    const unsigned os = a.mstate2[mslot[c]];
+                    const unsigned long long ob = a.mstate[mslot];
+                    const unsigned os = a.mstate2[mslot];
                     const unsigned bd = (unsigned)(best >> 32), od = (unsigned)(ob >> 32);
                     const unsigned nh = max(bd, od);
                     const unsigned long long nbest = (bd < od) ? best : ob;
                     sec = min(nh, min(sec, os));
                     best = nbest;
                 }
-                a.mstate[mslot[c]] = best;
-                a.mstate2[mslot[c]] = sec;
+                a.mstate[mslot] = best;
+                a.mstate2[mslot] = sec;
             }
         }
     }
@@ -1261,7 +1294,7 @@ __global__ void __launch_bounds__(WARPS * 32, MATCH_MINB) match_kernel(ChunkArgs
                                      : make_float4(G.ar, G.br, G.cr, (float)a.d + G.maxdev + 0.05f);
             }
         }
-        if (SG.mcnt <= SG_MEMBERS && lane < SG.mcnt) S.mr[lane] = a.mrec[SG.m0 + lane];
+        stage_members(a, S, SG.m0, SG.mcnt, 0);
         __syncwarp();
         const int pg = a.p0 + SG.p;
         const int ti = a.pair_t[pg], qi = a.pair_q[pg];
