@@ -363,6 +363,10 @@ struct ChunkArgs {
     int32_t* q_tab; double* q_line;
     int2* gtmp; float* gkey; int32_t* gpos; float4* gline; float4* gend; int2* sglist;
     int4* grec; int32_t* gfill; int32_t* members; GroupRec* grp; MemberRec* mrec; SGRec* sg;
+    int32_t* mgid;               // per member position: dense group id (-1: unused position)
+    int32_t* msg;                // per member position: super-group id
+    unsigned* gfit;              // per sorted group: bit i = group g+1+i fits g's line (tau)
+    unsigned long long* sgdev;   // per super-group: max member-band deviation (f64 bits)
     unsigned long long* mstate;  // per member slot: best (d2<<32 | tid)
     unsigned* mstate2;           // per member slot: second d2
     int32_t* res_tid; float* res_dist; float* res_ratio;
@@ -426,6 +430,7 @@ __global__ void __launch_bounds__(256) lines_kernel(ChunkArgs a) {
     for (int i = threadIdx.x; i < nq; i += blockDim.x) {
         a.res_tid[s0 + i] = -1;
         a.gfill[s0 + i] = 0;
+        a.mgid[s0 + i] = -1;
     }
     if (threadIdx.x == 0) { a.ngroups[p] = 0; a.nmem[p] = 0; }
     __syncthreads();
@@ -476,6 +481,7 @@ __global__ void __launch_bounds__(256) lines_kernel(ChunkArgs a) {
 // ranges in that order.  The order only affects how members are packed into
 // super-groups, never any result.
 constexpr int GB = 4096;
+constexpr int WALK_T = GB;   // groups staged per walk step (2 x u16 in the 4*GB-byte histogram)
 __global__ void __launch_bounds__(256) groups_kernel(ChunkArgs a) {
     __shared__ int sm[256 / 32 + 1];
     __shared__ int hist[GB];
@@ -576,60 +582,70 @@ __global__ void __launch_bounds__(256) groups_kernel(ChunkArgs a) {
     __syncthreads();
     // super-groups: greedy walk over the angle-ordered groups; a super-group holds
     // at most SG_MEMBERS members and closes when the next group's line leaves the
-    // base line by more than SG_TAU px inside the image (stats mode: one per group)
-    if (threadIdx.x < 32) {
-        int nsg = 0;
-        if (a.stats_mode) {
-            for (int g = lane; g < ng; g += 32) {
-                const int4 gr = a.grec[s0 + g];
-                a.sglist[s0 + g] = make_int2(gr.z, gr.y);
+    // base line by more than SG_TAU px inside the image (stats mode: one per group).
+    // The tau tests run in parallel (gfit bit i: group g+1+i fits group g's line);
+    // one thread then walks the groups with integer work only.
+    if (a.stats_mode) {
+        for (int g = threadIdx.x; g < ng; g += 256) {
+            const int4 gr = a.grec[s0 + g];
+            a.sglist[s0 + g] = make_int2(gr.z, gr.y);
+        }
+        if (threadIdx.x == 0) a.nsg[p] = ng;
+    } else {
+        for (int g = threadIdx.x; g < ng; g += 256) {
+            const float4 ln = a.gline[s0 + g];
+            unsigned bits = 0;
+            const int lim = min(SG_MEMBERS, ng - 1 - g);
+            for (int i = 0; i < lim; i++) {
+                const float4 en = a.gend[s0 + g + 1 + i];
+                const float d1 = fabsf(fmaf(ln.x, en.x, fmaf(ln.y, en.y, ln.z)));
+                const float d2 = fabsf(fmaf(ln.x, en.z, fmaf(ln.y, en.w, ln.z)));
+                if (fmaxf(d1, d2) <= a.sg_tau) bits |= 1u << i;
             }
-            nsg = ng;
-        } else {
-            float ba = 0.f, bb = 0.f, bc = 0.f;
-            int cur_m0 = 0, cur_cnt = 0;
-            bool open = false;
-            for (int g0 = 0; g0 < ng; g0 += 32) {
-                const int g = g0 + lane;
-                int4 gr = make_int4(0, 0, 0, 0);
-                float4 ln = make_float4(0.f, 0.f, 0.f, 0.f), en = ln;
-                if (g < ng) { gr = a.grec[s0 + g]; ln = a.gline[s0 + g]; en = a.gend[s0 + g]; }
-                const int lim = min(32, ng - g0);
-                for (int i = 0; i < lim; i++) {
-                    const int cnt = __shfl_sync(FULL, gr.y, i), moff = __shfl_sync(FULL, gr.z, i);
-                    const float la = __shfl_sync(FULL, ln.x, i), lb = __shfl_sync(FULL, ln.y, i);
-                    const float lc = __shfl_sync(FULL, ln.z, i);
-                    const float pax = __shfl_sync(FULL, en.x, i), pay = __shfl_sync(FULL, en.y, i);
-                    const float pbx = __shfl_sync(FULL, en.z, i), pby = __shfl_sync(FULL, en.w, i);
-                    bool fits = false;
-                    if (open && cur_cnt < SG_MEMBERS) {
-                        const float d1 = fabsf(fmaf(ba, pax, fmaf(bb, pay, bc)));
-                        const float d2 = fabsf(fmaf(ba, pbx, fmaf(bb, pby, bc)));
-                        fits = fmaxf(d1, d2) <= a.sg_tau;
-                    }
-                    int rem = cnt, pos = moff;
-                    if (fits) {
+            a.gfit[s0 + g] = bits;
+        }
+        __syncthreads();
+        // the walk reads counts and fit masks from shared memory, WALK_T groups at a time
+        // (the histogram buffer is free again)
+        unsigned short* wcnt = reinterpret_cast<unsigned short*>(hist);
+        unsigned short* wfit = wcnt + WALK_T;
+        int nsg = 0, base = 0, cur_m0 = 0, cur_cnt = 0;
+        unsigned bmask = 0;
+        bool open = false;
+        for (int c0 = 0; c0 < ng; c0 += WALK_T) {
+            const int cn = min(WALK_T, ng - c0);
+            for (int i = threadIdx.x; i < cn; i += 256) {
+                wcnt[i] = (unsigned short)a.grec[s0 + c0 + i].y;
+                wfit[i] = (unsigned short)a.gfit[s0 + c0 + i];
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int pos = a.grec[s0 + c0].z;    // member offsets are the prefix of the counts
+#pragma unroll 4
+                for (int i = 0; i < cn; i++) {
+                    const int g = c0 + i;
+                    int rem = wcnt[i];
+                    const int dg = g - base;
+                    if (open && cur_cnt < SG_MEMBERS && dg <= SG_MEMBERS && ((bmask >> (dg - 1)) & 1u)) {
                         const int take = min(SG_MEMBERS - cur_cnt, rem);
                         cur_cnt += take; rem -= take; pos += take;
                     }
                     while (rem > 0) {
-                        if (open) {
-                            if (lane == 0) a.sglist[s0 + nsg] = make_int2(cur_m0, cur_cnt);
-                            nsg++;
-                        }
+                        if (open) a.sglist[s0 + nsg++] = make_int2(cur_m0, cur_cnt);
                         open = true;
-                        ba = la; bb = lb; bc = lc;
+                        base = g;
+                        bmask = wfit[i];
                         const int take = min(SG_MEMBERS, rem);
                         cur_m0 = pos; cur_cnt = take; rem -= take; pos += take;
                     }
                 }
             }
-            if (open) {
-                if (lane == 0) a.sglist[s0 + nsg] = make_int2(cur_m0, cur_cnt);
-                nsg++;
-            }
+            __syncthreads();
         }
-        if (lane == 0) a.nsg[p] = nsg;
+        if (threadIdx.x == 0) {
+            if (open) a.sglist[s0 + nsg++] = make_int2(cur_m0, cur_cnt);
+            a.nsg[p] = nsg;
+        }
     }
     if (threadIdx.x == 0) { a.ngroups[p] = ng; a.nmem[p] = mcarry; }
 }
@@ -669,6 +685,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(ChunkArgs a) {
         const int4 g = a.grec[s0 + lg];
         const int pos = g.z + atomicAdd(&a.gfill[s0 + lg], 1);
         a.members[pos] = (int)(s0 + i);
+        a.mgid[pos] = a.gstart[p] + lg;
     }
 }
 
@@ -694,18 +711,20 @@ __device__ double band_deviation(const double m[3], const double r[3], double W,
         double dm = m[0] * cx[k] + m[1] * cy[k] + m[2];
         if (fabs(dm) <= B) dev = fmax(dev, fabs(da * cx[k] + db * cy[k] + dc));
     }
+    const double i1 = fabs(m[1]) > 1e-12 ? 1.0 / m[1] : 0.0;
+    const double i0 = fabs(m[0]) > 1e-12 ? 1.0 / m[0] : 0.0;
     for (int s = -1; s <= 1; s += 2) {
-        if (fabs(m[1]) > 1e-12) {
+        if (i1 != 0.0) {
             for (int e = 0; e < 2; e++) {
                 double x = e ? W : 0.0;
-                double y = (s * B - m[2] - m[0] * x) / m[1];
+                double y = (s * B - m[2] - m[0] * x) * i1;
                 if (y >= -1e-6 && y <= H + 1e-6) dev = fmax(dev, fabs(da * x + db * y + dc));
             }
         }
-        if (fabs(m[0]) > 1e-12) {
+        if (i0 != 0.0) {
             for (int e = 0; e < 2; e++) {
                 double y = e ? H : 0.0;
-                double x = (s * B - m[2] - m[1] * y) / m[0];
+                double x = (s * B - m[2] - m[1] * y) * i0;
                 if (x >= -1e-6 && x <= W + 1e-6) dev = fmax(dev, fabs(da * x + db * y + dc));
             }
         }
@@ -735,7 +754,6 @@ __global__ void __launch_bounds__(128) prep_kernel(ChunkArgs a, int max_groups) 
     const int4 g = a.grec[s0 + (gid - a.gstart[p])];
     const int ti = a.pair_t[pg], qi = a.pair_q[pg];
     const double W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1], D = a.D, d = a.d;
-    const int64_t qoff = a.img_off[qi];
     const double* rl = a.q_line + 3 * (s0 + g.x);
     const double r[3] = {rl[0], rl[1], rl[2]};
     GroupRec o;
@@ -751,37 +769,8 @@ __global__ void __launch_bounds__(128) prep_kernel(ChunkArgs a, int max_groups) 
         o.K = (int)(K < 1 ? 1 : K);
     }
     o.pax = pa[0]; o.pay = pa[1]; o.pbx64 = pb[0]; o.pby64 = pb[1];
-    double F[9];
-    if (g.y == 1)
-        for (int j = 0; j < 9; j++) F[j] = a.pair_F[9 * (int64_t)pg + j];
-    for (int j = 0; j < g.y; j++) {
-        const int slot = a.members[g.z + j];
-        const int fid = a.q_fid[slot];
-        double m[3];
-        if (g.y == 1) {
-            // a singleton's own band uses the dgemv-rounded line (guided.py:443-446, m == 1)
-            const float2 p2 = a.xy[qoff + fid];
-            epiline(F, (double)p2.x, (double)p2.y, true, m);
-            double nrm = fmax(np_hypot(m[0], m[1]), 1e-15);
-            m[0] /= nrm; m[1] /= nrm; m[2] /= nrm;
-            o.sl0 = m[0]; o.sl1 = m[1]; o.sl2 = m[2];
-        } else {
-            const double* ml = a.q_line + 3 * (int64_t)slot;
-            m[0] = ml[0]; m[1] = ml[1]; m[2] = ml[2];
-        }
-        maxdev = fmax(maxdev, band_deviation(m, r, W, H, d));
-        MemberRec mr;
-        mr.a = (float)m[0]; mr.b = (float)m[1]; mr.c = (float)m[2];
-        const float eps = (float)((fabs(m[0]) * W + fabs(m[1]) * H + fabs(m[2])) * 0x1p-20) + 1e-6f;
-        mr.lo = (float)d - eps;
-        mr.hi = (float)d + eps;
-        mr.qn9 = (unsigned)a.norm2[qoff + fid] << 9;
-        mr.fid = fid;
-        mr.slotgi = slot;
-        a.mrec[g.z + j] = mr;
-    }
     o.ar = (float)r[0]; o.br = (float)r[1]; o.cr = (float)r[2];
-    o.maxdev = (float)(maxdev + 0.05);
+    o.maxdev = (float)(maxdev + 0.05);   // raised by member_kernel (atomic max of f32 bits)
     const double hs2 = D * D - 0.25 * d * d;
     o.hsure = hs2 > 0 ? (float)(sqrt(hs2) - 0.075) : -1.0f;
     o.pbx = (float)pb[0]; o.pby = (float)pb[1];
@@ -797,7 +786,8 @@ __global__ void __launch_bounds__(128) prep_kernel(ChunkArgs a, int max_groups) 
 }
 
 // Per super-group: member window, its groups, the base line and strip.
-__global__ void __launch_bounds__(128) sg_prep_kernel(ChunkArgs a, int max_sg) {
+// Super-group shape (thread per super-group): group range and base line.
+__global__ void __launch_bounds__(128) sg_shape_kernel(ChunkArgs a, int max_sg) {
     const int sid = blockIdx.x * blockDim.x + threadIdx.x;
     const int total = a.sgstart[a.npairs];
     if (sid >= total || sid >= max_sg) return;
@@ -806,9 +796,7 @@ __global__ void __launch_bounds__(128) sg_prep_kernel(ChunkArgs a, int max_sg) {
     const int pg = a.p0 + p;
     const int64_t s0 = a.qlist_off[pg] - a.qbase;
     const int ng = a.ngroups[p];
-    const int ti = a.pair_t[pg];
-    const double W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1], D = a.D, d = a.d;
-    SGRec o;
+    SGRec o = {};
     o.p = p;
     int lg0, lg1;                       // group range [lg0, lg1] (sorted order)
     const int2 sgm = a.sglist[s0 + ls];
@@ -830,30 +818,76 @@ __global__ void __launch_bounds__(128) sg_prep_kernel(ChunkArgs a, int max_sg) {
     }
     o.g0 = a.gstart[p] + lg0;
     o.gcnt = lg1 - lg0 + 1;
-    // base line: the middle group's representative
-    const int gb = a.gstart[p] + (lg0 + lg1) / 2;
-    const GroupRec& B = a.grp[gb];
-    const double* bl = a.q_line + 3 * (int64_t)B.rep;
-    const double r[3] = {bl[0], bl[1], bl[2]};
-    bool all_k = true;
-    double dev = 0.0;
-    for (int j = 0; j < o.mcnt; j++) {
-        const int pos = o.m0 + j;
-        // group of this member within the super-group
-        int gi = 0;
-        while (gi + 1 < o.gcnt && a.grp[o.g0 + gi + 1].moff <= pos) gi++;
-        const GroupRec& G = a.grp[o.g0 + gi];
-        MemberRec& mr = a.mrec[pos];
-        const int slot = mr.slotgi & 0xFFFFFF;
-        double m[3];
-        if (G.cnt == 1) { m[0] = G.sl0; m[1] = G.sl1; m[2] = G.sl2; }
-        else {
-            const double* ml = a.q_line + 3 * (int64_t)slot;
-            m[0] = ml[0]; m[1] = ml[1]; m[2] = ml[2];
-        }
-        dev = fmax(dev, band_deviation(m, r, W, H, d));
-        mr.slotgi = slot | (gi << 24);
+    // base line: the middle group's representative (its chunk-local slot in rlo)
+    o.rlo = a.grp[a.gstart[p] + (lg0 + lg1) / 2].rep;
+    for (int j = 0; j < o.mcnt; j++) a.msg[o.m0 + j] = sid;
+    a.sgdev[sid] = 0ull;
+    a.sg[sid] = o;
+}
+
+// Per member (thread per member position): epilogue constants, the member band's
+// deviation from its group's representative line (-> GroupRec.maxdev) and from its
+// super-group's base line (-> sgdev), both as atomic maxima.
+__global__ void __launch_bounds__(128) member_kernel(ChunkArgs a, int max_pos) {
+    const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pos >= max_pos) return;
+    const int gid = a.mgid[pos];
+    if (gid < 0) return;
+    GroupRec& G = a.grp[gid];
+    const int p = G.p, pg = a.p0 + p;
+    const int ti = a.pair_t[pg], qi = a.pair_q[pg];
+    const double W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1], d = a.d;
+    const int64_t qoff = a.img_off[qi];
+    const int slot = a.members[pos];
+    const int fid = a.q_fid[slot];
+    double m[3];
+    if (G.cnt == 1) {
+        // a singleton's own band uses the dgemv-rounded line (guided.py:443-446, m == 1)
+        double F[9];
+        for (int j = 0; j < 9; j++) F[j] = a.pair_F[9 * (int64_t)pg + j];
+        const float2 p2 = a.xy[qoff + fid];
+        epiline(F, (double)p2.x, (double)p2.y, true, m);
+        double nrm = fmax(np_hypot(m[0], m[1]), 1e-15);
+        m[0] /= nrm; m[1] /= nrm; m[2] /= nrm;
+        G.sl0 = m[0]; G.sl1 = m[1]; G.sl2 = m[2];
+    } else {
+        const double* ml = a.q_line + 3 * (int64_t)slot;
+        m[0] = ml[0]; m[1] = ml[1]; m[2] = ml[2];
     }
+    const double* rl = a.q_line + 3 * (int64_t)G.rep;
+    const double r[3] = {rl[0], rl[1], rl[2]};
+    const float gdev = (float)(band_deviation(m, r, W, H, d) + 0.05);
+    atomicMax(reinterpret_cast<unsigned*>(&G.maxdev), __float_as_uint(gdev));
+    const int sid = a.msg[pos];
+    const SGRec& SG = a.sg[sid];
+    const double* bl = a.q_line + 3 * (int64_t)SG.rlo;
+    const double b[3] = {bl[0], bl[1], bl[2]};
+    const double sdev = band_deviation(m, b, W, H, d);
+    atomicMax(&a.sgdev[sid], (unsigned long long)__double_as_longlong(sdev));
+    MemberRec mr;
+    mr.a = (float)m[0]; mr.b = (float)m[1]; mr.c = (float)m[2];
+    const float eps = (float)((fabs(m[0]) * W + fabs(m[1]) * H + fabs(m[2])) * 0x1p-20) + 1e-6f;
+    mr.lo = (float)d - eps;
+    mr.hi = (float)d + eps;
+    mr.qn9 = (unsigned)a.norm2[qoff + fid] << 9;
+    mr.fid = fid;
+    mr.slotgi = slot | ((gid - SG.g0) << 24);
+    a.mrec[pos] = mr;
+}
+
+// Super-group strip geometry (thread per super-group), after member_kernel.
+__global__ void __launch_bounds__(128) sg_prep_kernel(ChunkArgs a, int max_sg) {
+    const int sid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int total = a.sgstart[a.npairs];
+    if (sid >= total || sid >= max_sg) return;
+    SGRec o = a.sg[sid];
+    const int pg = a.p0 + o.p;
+    const int ti = a.pair_t[pg];
+    const double W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1], D = a.D, d = a.d;
+    const double* bl = a.q_line + 3 * (int64_t)o.rlo;
+    const double r[3] = {bl[0], bl[1], bl[2]};
+    const double dev = __longlong_as_double((long long)a.sgdev[sid]);
+    bool all_k = true;
     const double R = d + dev + 0.05;
     double delta = 0.0;
     for (int g = o.g0; g < o.g0 + o.gcnt; g++) {
@@ -1516,6 +1550,9 @@ size_t chunk_bytes(const ChunkSizes& c) {
     b += aligned_bytes<unsigned long long>(c.T);       // tab_key
     b += aligned_bytes<unsigned>(c.T) * 2;             // tab_rep, tab_cnt
     b += aligned_bytes<int32_t>(c.Q) * 2;              // q_tab, q_fid
+    b += aligned_bytes<int32_t>(c.Q) * 2;              // mgid, msg
+    b += aligned_bytes<unsigned>(c.Q);                 // gfit
+    b += aligned_bytes<unsigned long long>(c.Q);       // sgdev
     b += aligned_bytes<double>(3 * c.Q);               // q_line
     b += aligned_bytes<int4>(c.Q);                     // grec
     b += aligned_bytes<int32_t>(c.Q) * 2;              // gfill, members
@@ -1731,6 +1768,8 @@ extern "C" int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids,
     a.pair_q = d_pair_q; a.pair_t = d_pair_t; a.pair_F = d_pair_F;
     a.qlist_off = d_qlist_off; a.qlist = d_qlist; a.qlist_src = d_qlist_src;
     a.q_fid = ar.take<int32_t>(w.Q);
+    a.mgid = ar.take<int32_t>(w.Q); a.msg = ar.take<int32_t>(w.Q);
+    a.gfit = ar.take<unsigned>(w.Q); a.sgdev = ar.take<unsigned long long>(w.Q);
     a.tab_off = ar.take<int64_t>(w.P + 1); a.tbase = ar.take<int64_t>(w.P + 1);
     a.ngroups = ar.take<int32_t>(w.P + 1); a.gstart = ar.take<int32_t>(w.P + 1);
     a.nmem = ar.take<int32_t>(w.P + 1); a.sgstart = ar.take<int32_t>(w.P + 1);
@@ -1763,22 +1802,25 @@ extern "C" int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids,
         a.qbase = h_qlist_off[p0];
         const int64_t Q = h_qlist_off[p1] - h_qlist_off[p0];
         plan_kernel<<<1, SCAN_T, 0, st>>>(a);
-        lines_kernel<<<a.npairs, 256, 0, st>>>(a);
-        groups_kernel<<<a.npairs, 256, 0, st>>>(a);
+        { ProfScope ps("lines_kernel", st); lines_kernel<<<a.npairs, 256, 0, st>>>(a); }
+        { ProfScope ps("groups_kernel", st); groups_kernel<<<a.npairs, 256, 0, st>>>(a); }
         gscan_kernel<<<1, SCAN_T, 0, st>>>(a);
-        scatter_kernel<<<a.npairs, 256, 0, st>>>(a);
+        { ProfScope ps("scatter_kernel", st); scatter_kernel<<<a.npairs, 256, 0, st>>>(a); }
         if (Q > 0) {
-            prep_kernel<<<(unsigned)((Q + 127) / 128), 128, 0, st>>>(a, (int)Q);
-            sg_prep_kernel<<<(unsigned)((Q + 127) / 128), 128, 0, st>>>(a, (int)Q);
+            const unsigned nb = (unsigned)((Q + 127) / 128);
+            { ProfScope ps("prep_kernel", st); prep_kernel<<<nb, 128, 0, st>>>(a, (int)Q); }
+            { ProfScope ps("sg_shape_kernel", st); sg_shape_kernel<<<nb, 128, 0, st>>>(a, (int)Q); }
+            { ProfScope ps("member_kernel", st); member_kernel<<<nb, 128, 0, st>>>(a, (int)Q); }
+            { ProfScope ps("sg_prep_kernel", st); sg_prep_kernel<<<nb, 128, 0, st>>>(a, (int)Q); }
         }
         {
             ProfScope ps("match_kernel", st);
             if (d_stats) match_kernel<true><<<nsm * MATCH_MINB, WARPS * 32, 0, st>>>(a);
             else         match_kernel<false><<<nsm * MATCH_MINB, WARPS * 32, 0, st>>>(a);
         }
-        compact_kernel<<<a.npairs, 256, 0, st>>>(a);
+        { ProfScope ps("compact_kernel", st); compact_kernel<<<a.npairs, 256, 0, st>>>(a); }
         MSFM_LAUNCH_CHECK();
-        count_launches(7 + (Q > 0 ? 2 : 0));
+        count_launches(7 + (Q > 0 ? 4 : 0));
     }
     return MSFM_OK;
 }
