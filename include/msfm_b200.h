@@ -191,7 +191,8 @@ int msfm_ransac_samples(const uint64_t state_inc[4], int32_t has_uint32, uint32_
  * over the image's features, lowest feature index winning ties:
  *     k1[s][p], i1[s][p] (image-local feature id, -1 if none), k2[s][p]
  * (INT32_MAX when the image has < 2 features).  Row stride = n_points rounded
- * up to 128.  S.f runs on tcgen05 kind::i8 (two u8 digit planes of S).
+ * up to 128.  2 S.f runs on tcgen05 kind::i8 over two u8 digit planes
+ * (2S = lo + 256 hi, lo = 2 (S mod 128), hi = S >> 7).
  * Requires max track length <= 100 (int32 keys); max_image_features bounds the
  * feature count of every query image.
  * ---------------------------------------------------------------------- */

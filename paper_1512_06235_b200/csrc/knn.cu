@@ -5,8 +5,8 @@
 // images.  A point is its track-descriptor sum S (<= 255 n) and track length n
 // (mean = S/n, localize.py:51-59); against feature f the exact rank key is
 //     key = n |f|^2 - 2 S.f            (N = |S - n f|^2 = n*key + |S|^2)
-// S.f is computed exactly as two u8 x u8 -> s32 GEMMs over the digit planes
-// S = S_lo + 256 S_hi.  Per (point, image) the epilogue keeps the running top-2
+// 2 S.f is computed exactly as two u8 x u8 -> s32 GEMMs over the digit planes
+// 2S = lo + 256 hi (lo = 2 (S mod 128), hi = S >> 7).  Per (point, image) the epilogue keeps the running top-2
 // (lowest feature index wins ties), so no distance matrix is ever stored.
 //
 // CTA (persistent, 1 per SM, 384 threads):
@@ -25,10 +25,13 @@
 namespace msfm {
 namespace {
 
-constexpr int KN_THREADS = 640;
+#ifndef MSFM_KNN_EPI_WARPS
+#define MSFM_KNN_EPI_WARPS 16
+#endif
 constexpr int KN_STAGES = 4;
 constexpr int TILE_M = 128, TILE_N = 128, KB = 128;   // K = 128 bytes per plane
-constexpr int EPI_WARP0 = 4, EPI_WARPS = 16;
+constexpr int EPI_WARP0 = 4, EPI_WARPS = MSFM_KNN_EPI_WARPS;
+constexpr int KN_THREADS = (EPI_WARP0 + EPI_WARPS) * 32;
 constexpr int EPI_COLS = TILE_N / (EPI_WARPS / 4);   // columns per epilogue warp per tile
 constexpr uint32_t B_TILE_BYTES = TILE_N * KB;          // 16 KB
 constexpr uint32_t A_PLANE_BYTES = TILE_M * KB;         // 16 KB
@@ -77,6 +80,26 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+// Bounded wait with back-off (epilogue warps waiting for the next accumulator
+// should not steal issue slots from the warps still draining the current one).
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, uint32_t parity) {
+    const uint32_t addr = smem_u32(b);
+    uint32_t done = 0;
+    for (long long it = 0; it < (1LL << 28); it++) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(addr), "r"(parity)
+            : "memory");
+        if (done) return;
+#ifndef MSFM_KNN_NO_BACKOFF
+        __nanosleep(64);
+#endif
+    }
+    __trap();
 }
 
 // Bounded wait: a protocol bug traps instead of hanging the GPU.
@@ -275,9 +298,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_lo, const __grid_constant_
             const int nt = unit_tiles(a, u, img, mt, off, n);
             const int grow = mt * TILE_M + row;
             const int np = grow < a.M_pad ? a.n[grow] : 0;
-            int k1 = INT_BIG, i1 = -1, k2 = INT_BIG;
+            // running top-2 of this row over its column slice: k1 (best key), k2 (second
+            // smallest key value), best column = ibase + il.  Branch-free per score:
+            // two ops for the key, five for the update.
+            int k1 = INT_BIG, k2 = INT_BIG, il = 0, ibase = 0;
             for (int j = 0; j < nt; j++) {
-                mbar_wait(&S.t_full[acc], acc_phase);
+                mbar_wait_backoff(&S.t_full[acc], acc_phase);
                 tc_fence_after();
                 const uint32_t t_lo = tbase + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * 256 + half * EPI_COLS);
                 const int cbase = j * TILE_N + half * EPI_COLS;
@@ -296,30 +322,31 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_lo, const __grid_constant_
                         fv[4 * q] = f4.x; fv[4 * q + 1] = f4.y; fv[4 * q + 2] = f4.z; fv[4 * q + 3] = f4.w;
                     }
                     tmem_wait_ld();
-                    const int col0 = cbase + c0;
-                    // keys first (straight-line), then one warp vote: after the first
-                    // tiles almost no key beats the running second best
-                    int key[16];
-                    bool hit = false;
+                    const int k1_in = k1;
+                    if (full) {
 #pragma unroll
-                    for (int c = 0; c < 16; c++) {
-                        key[c] = np * fv[c] - 2 * ((int)lo[c] + ((int)hi[c] << 8));
-                        hit |= key[c] < k2;
-                    }
-                    if (__any_sync(0xffffffffu, hit) && hit) {
                         for (int c = 0; c < 16; c++) {
-                            if (key[c] < k2 && (full || col0 + c < n)) {
-                                if (key[c] < k1) { k2 = k1; k1 = key[c]; i1 = col0 + c; }
-                                else k2 = key[c];
-                            }
+                            const int key = np * fv[c] - ((int)lo[c] + ((int)hi[c] << 8));
+                            k2 = min(k2, max(k1, key));
+                            if (key < k1) { k1 = key; il = c; }
+                        }
+                    } else {
+                        const int lim = n - (cbase + c0);
+#pragma unroll
+                        for (int c = 0; c < 16; c++) {
+                            const int key = c < lim ? np * fv[c] - ((int)lo[c] + ((int)hi[c] << 8)) : INT_BIG;
+                            k2 = min(k2, max(k1, key));
+                            if (key < k1) { k1 = key; il = c; }
                         }
                     }
+                    if (k1 != k1_in) ibase = cbase + c0;
                 }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&S.t_empty[acc]);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
+            int i1 = k1 == INT_BIG ? -1 : ibase + il;
             // merge the column slices of each row
             S.merge_k1[half][row] = k1; S.merge_i1[half][row] = i1; S.merge_k2[half][row] = k2;
             asm volatile("bar.sync 1, %0;" ::"r"(EPI_WARPS * 32));
@@ -368,8 +395,10 @@ __global__ void digit_planes_kernel(const int32_t* __restrict__ S, const int32_t
     if (i >= M_pad * 128) return;
     const int64_t r = i >> 7;
     const int v = r < M ? S[i] : 0;
-    lo[i] = (uint8_t)(v & 255);
-    hi[i] = (uint8_t)(v >> 8);
+    // 2S = lo + 256 hi with lo = 2 (S mod 128), hi = S >> 7 (S <= 32767, n <= 128):
+    // the planes' GEMMs give 2 S.f directly
+    lo[i] = (uint8_t)((v & 127) << 1);
+    hi[i] = (uint8_t)(v >> 7);
     if ((i & 127) == 0) npad[r] = r < M ? n[r] : 0;
 }
 

@@ -162,9 +162,13 @@ def direct_search(bank: FeatureBank, pts: PointSet, image_ids, *, ratio: float =
     res = Correspondences(rows, fids, cnt, knn.M_pad)
     res._keep = (win, d_win_off, d_slots, knn)
     if to_host:
+        # three copies in total (counts, then the used prefix of both tables)
         c = cnt.cpu().numpy()
-        return [np.stack([pts.ids[rows[s, :c[s]].cpu().numpy()], fids[s, :c[s]].cpu().numpy()], 1)
-                .astype(np.int64) for s in range(len(slots))]
+        w = int(c.max()) if len(c) else 0
+        rh = rows[:, :w].cpu().numpy()
+        fh = fids[:, :w].cpu().numpy()
+        return [np.stack([pts.ids[rh[s, :c[s]]], fh[s, :c[s]]], 1).astype(np.int64)
+                for s in range(len(slots))]
     return res
 
 

@@ -105,7 +105,6 @@ def pnp_batch(X_list, uv_list, K_list, seeds, *, threshold=PNP_THRESHOLD_PX,
     A = len(active)
     H1 = min(max_iters, first_round)
     counts = np.full((A, max_iters), -2, np.int64)
-    hyps = np.zeros((A, max_iters, 12))
     states = []
     samples = np.zeros((A, H1, 6), np.int32)
     for k, i in enumerate(active):
@@ -115,7 +114,9 @@ def pnp_batch(X_list, uv_list, K_list, seeds, *, threshold=PNP_THRESHOLD_PX,
                                            samples[k].ctypes.data, out_state.ctypes.data),
                    "msfm_ransac_samples")
         states.append((out_state, has32, u32))
-    _score(lib, batch, samples, H1, threshold, counts, hyps, 0, st, dev, list(range(A)))
+    # hypotheses stay on the device; only the inlier counts come back for the replay
+    d_hyp1, c1 = _score(lib, batch, samples, H1, threshold, st, dev)
+    counts[:, :H1] = c1
     best = [None] * A
     pending = []
     for k in range(A):
@@ -128,6 +129,7 @@ def pnp_batch(X_list, uv_list, K_list, seeds, *, threshold=PNP_THRESHOLD_PX,
             best[k] = r
         else:
             pending.append(k)
+    d_hyp2 = None
     if pending:
         # second round: continue each stream up to the current `needed` bound
         H2 = max_iters - H1
@@ -141,21 +143,20 @@ def pnp_batch(X_list, uv_list, K_list, seeds, *, threshold=PNP_THRESHOLD_PX,
         sub = _Batch(dev, [np.asarray(X_list[active[k]]) for k in pending],
                      [np.asarray(uv_list[active[k]]) for k in pending],
                      [K_list[active[k]] for k in pending])
-        c2 = np.full((len(pending), H2), -2, np.int64)
-        h2 = np.zeros((len(pending), H2, 12))
-        _score(lib, sub, samples2, H2, threshold, c2, h2, 0, st, dev, list(range(len(pending))))
+        d_hyp2, c2 = _score(lib, sub, samples2, H2, threshold, st, dev)
         for j, k in enumerate(pending):
             counts[k, H1:] = c2[j]
-            hyps[k, H1:] = h2[j]
             try:
                 r = _replay(counts[k], max_iters, int(batch.n[k]), max_iters, confidence)
             except OverflowError:
                 best[k] = "overflow"
                 continue
             best[k] = r
-    # refit the winners
+    # refit the winners: gather each winning hypothesis on the device
+    import torch
+
     status = np.zeros(A, np.int32)
-    hyp_best = np.zeros((A, 12))
+    src1, src2 = [], []
     for k in range(A):
         if best[k] == "overflow":
             results[active[k]] = PnpResult("overflow")
@@ -165,33 +166,45 @@ def pnp_batch(X_list, uv_list, K_list, seeds, *, threshold=PNP_THRESHOLD_PX,
             results[active[k]] = PnpResult("none", iterations=it)
             continue
         status[k] = 1
-        hyp_best[k] = hyps[k, bh]
+        if bh < H1:
+            src1.append((k, bh))
+        else:
+            src2.append((k, pending.index(k), bh - H1))
     if status.any():
-        _refit(lib, batch, status, hyp_best, threshold, min_inliers, st, dev, results, active, best)
+        d_best = torch.zeros((A, 12), dtype=torch.float64, device=dev)
+        if src1:
+            ks = torch.tensor([x[0] for x in src1], device=dev)
+            hs = torch.tensor([x[1] for x in src1], device=dev)
+            d_best[ks] = d_hyp1[ks, hs]
+        if src2:
+            ks = torch.tensor([x[0] for x in src2], device=dev)
+            js = torch.tensor([x[1] for x in src2], device=dev)
+            hs = torch.tensor([x[2] for x in src2], device=dev)
+            d_best[ks] = d_hyp2[js, hs]
+        _refit(lib, batch, status, d_best, threshold, min_inliers, st, dev, results, active, best)
     return results
 
 
-def _score(lib, batch, samples, H, threshold, counts, hyps, h0, st, dev, rows):
+def _score(lib, batch, samples, H, threshold, st, dev):
+    """Device hypotheses (A, H, 12) and host inlier counts (A, H)."""
     import torch
 
     A = samples.shape[0]
-    d_samples = torch.from_numpy(np.ascontiguousarray(samples)).to(dev)
+    d_samples = torch.from_numpy(np.ascontiguousarray(samples)).pin_memory().to(dev, non_blocking=True)
     d_hyp = torch.empty((A, H, 12), dtype=torch.float64, device=dev)
     d_count = torch.empty((A, H), dtype=torch.int32, device=dev)
     _lib.check(lib.msfm_pnp_hypotheses(_lib.ptr(batch.X), _lib.ptr(batch.uv), _lib.ptr(batch.off),
                                        _lib.ptr(batch.K), A, _lib.ptr(d_samples), H,
                                        float(threshold), _lib.ptr(d_hyp), _lib.ptr(d_count), st),
                "msfm_pnp_hypotheses")
-    counts[rows, h0:h0 + H] = d_count.cpu().numpy()
-    hyps[rows, h0:h0 + H] = d_hyp.cpu().numpy()
+    return d_hyp, d_count.cpu().numpy()
 
 
-def _refit(lib, batch, status, hyp_best, threshold, min_inliers, st, dev, results, active, best):
+def _refit(lib, batch, status, d_best, threshold, min_inliers, st, dev, results, active, best):
     import torch
 
     A = len(status)
     d_status = torch.from_numpy(status).to(dev)
-    d_best = torch.from_numpy(np.ascontiguousarray(hyp_best)).to(dev)
     d_R = torch.zeros((A, 9), dtype=torch.float64, device=dev)
     d_t = torch.zeros((A, 3), dtype=torch.float64, device=dev)
     d_mask = torch.zeros(max(int(batch.off_h[-1]), 1), dtype=torch.uint8, device=dev)
