@@ -19,6 +19,7 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "common.cuh"
@@ -481,7 +482,6 @@ __global__ void __launch_bounds__(256) lines_kernel(ChunkArgs a) {
 // ranges in that order.  The order only affects how members are packed into
 // super-groups, never any result.
 constexpr int GB = 4096;
-constexpr int WALK_T = GB;   // groups staged per walk step (2 x u16 in the 4*GB-byte histogram)
 __global__ void __launch_bounds__(256) groups_kernel(ChunkArgs a) {
     __shared__ int sm[256 / 32 + 1];
     __shared__ int hist[GB];
@@ -605,45 +605,44 @@ __global__ void __launch_bounds__(256) groups_kernel(ChunkArgs a) {
             a.gfit[s0 + g] = bits;
         }
         __syncthreads();
-        // the walk reads counts and fit masks from shared memory, WALK_T groups at a time
-        // (the histogram buffer is free again)
-        unsigned short* wcnt = reinterpret_cast<unsigned short*>(hist);
-        unsigned short* wfit = wcnt + WALK_T;
-        int nsg = 0, base = 0, cur_m0 = 0, cur_cnt = 0;
-        unsigned bmask = 0;
-        bool open = false;
-        for (int c0 = 0; c0 < ng; c0 += WALK_T) {
-            const int cn = min(WALK_T, ng - c0);
-            for (int i = threadIdx.x; i < cn; i += 256) {
-                wcnt[i] = (unsigned short)a.grec[s0 + c0 + i].y;
-                wfit[i] = (unsigned short)a.gfit[s0 + c0 + i];
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                int pos = a.grec[s0 + c0].z;    // member offsets are the prefix of the counts
-#pragma unroll 4
-                for (int i = 0; i < cn; i++) {
-                    const int g = c0 + i;
-                    int rem = wcnt[i];
-                    const int dg = g - base;
-                    if (open && cur_cnt < SG_MEMBERS && dg <= SG_MEMBERS && ((bmask >> (dg - 1)) & 1u)) {
-                        const int take = min(SG_MEMBERS - cur_cnt, rem);
-                        cur_cnt += take; rem -= take; pos += take;
+        // The super-groups partition the member sequence into contiguous ranges, so the
+        // greedy walk is a chain over member positions: end[q] = where the super-group
+        // opened at position q closes (all q in parallel), then one thread follows the
+        // chain from 0 through shared memory.
+        extern __shared__ unsigned short send[];
+        const int nm = mcarry;
+        for (int g = threadIdx.x; g < ng; g += 256) {
+            const int4 gr = a.grec[s0 + g];
+            const int cnt = gr.y, rel0 = (int)(gr.z - s0);
+            const unsigned fit = a.gfit[s0 + g];
+            for (int k = 0; k < cnt; k++) {
+                const int q = rel0 + k, r = cnt - k;
+                int e;
+                if (r > SG_MEMBERS) {
+                    e = q + SG_MEMBERS;
+                } else {
+                    int cur = r, j = g + 1;
+                    e = -1;
+                    while (j < ng && cur < SG_MEMBERS && ((fit >> (j - g - 1)) & 1u)) {
+                        const int4 gj = a.grec[s0 + j];
+                        const int take = min(SG_MEMBERS - cur, gj.y);
+                        cur += take;
+                        if (take < gj.y) { e = (int)(gj.z - s0) + take; break; }
+                        j++;
                     }
-                    while (rem > 0) {
-                        if (open) a.sglist[s0 + nsg++] = make_int2(cur_m0, cur_cnt);
-                        open = true;
-                        base = g;
-                        bmask = wfit[i];
-                        const int take = min(SG_MEMBERS, rem);
-                        cur_m0 = pos; cur_cnt = take; rem -= take; pos += take;
-                    }
+                    if (e < 0) e = j < ng ? (int)(a.grec[s0 + j].z - s0) : nm;
                 }
+                send[q] = (unsigned short)e;
             }
-            __syncthreads();
         }
+        __syncthreads();
         if (threadIdx.x == 0) {
-            if (open) a.sglist[s0 + nsg++] = make_int2(cur_m0, cur_cnt);
+            int nsg = 0;
+            for (int q = 0; q < nm;) {
+                const int e = send[q];
+                a.sglist[s0 + nsg++] = make_int2((int)s0 + q, e - q);
+                q = e;
+            }
             a.nsg[p] = nsg;
         }
     }
@@ -1795,6 +1794,8 @@ extern "C" int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids,
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    MSFM_CUDA_TRY(cudaFuncSetAttribute(groups_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       2 * 65536 + 16));
     for (size_t c = 0; c + 1 < bounds.size(); c++) {
         const int p0 = bounds[c], p1 = bounds[c + 1];
         a.p0 = p0;
@@ -1803,7 +1804,12 @@ extern "C" int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids,
         const int64_t Q = h_qlist_off[p1] - h_qlist_off[p0];
         plan_kernel<<<1, SCAN_T, 0, st>>>(a);
         { ProfScope ps("lines_kernel", st); lines_kernel<<<a.npairs, 256, 0, st>>>(a); }
-        { ProfScope ps("groups_kernel", st); groups_kernel<<<a.npairs, 256, 0, st>>>(a); }
+        {
+            int64_t max_nq = 1;
+            for (int k = p0; k < p1; k++) max_nq = std::max(max_nq, h_qlist_off[k + 1] - h_qlist_off[k]);
+            ProfScope ps("groups_kernel", st);
+            groups_kernel<<<a.npairs, 256, (size_t)(2 * max_nq + 16), st>>>(a);
+        }
         gscan_kernel<<<1, SCAN_T, 0, st>>>(a);
         { ProfScope ps("scatter_kernel", st); scatter_kernel<<<a.npairs, 256, 0, st>>>(a); }
         if (Q > 0) {
