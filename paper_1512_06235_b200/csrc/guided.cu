@@ -324,7 +324,10 @@ struct alignas(16) SGRec {
     float ar, br, cr, R;                   // base line (fp32) and strip half-width
     float delta, hsure, border, invD;      // max rep-vs-base deviation, sure radius, border
     float alpha, beta, inv_alpha, Pmax;    // strip row math in the chosen orientation
-    float W, H, pad0, pad1;
+    float W, H;
+    int nalong, pad0;                      // buckets along a strip row
+    long long toff, qoff;                  // first bank feature of the target / query image
+    long long toffb, dbase;                // first bucket of the strip table, dedupe base
 };
 
 #ifndef MSFM_SG_NT
@@ -368,6 +371,8 @@ struct ChunkArgs {
     int32_t* msg;                // per member position: super-group id
     unsigned* gfit;              // per sorted group: bit i = group g+1+i fits g's line (tau)
     unsigned long long* sgdev;   // per super-group: max member-band deviation (f64 bits)
+    float4* gl4;                 // per dense group: rep line (fp32) + member-band reach
+    int32_t* gmoff;              // per dense group: first member position
     unsigned long long* mstate;  // per member slot: best (d2<<32 | tid)
     unsigned* mstate2;           // per member slot: second d2
     int32_t* res_tid; float* res_dist; float* res_ratio;
@@ -896,6 +901,11 @@ __global__ void __launch_bounds__(128) sg_prep_kernel(ChunkArgs a, int max_sg) {
         // |dist_g - dist_base| over the strip |dist_base| <= R inside the image
         delta = fmax(delta, band_deviation(r, gr, W, H, R));
         all_k = all_k && G.K >= 0;
+        // compact per-group view for the match kernel (groups shared by two
+        // super-groups get the same values twice)
+        a.gl4[g] = G.K < 0 ? make_float4(0.f, 0.f, 1e30f, -1.f)
+                           : make_float4(G.ar, G.br, G.cr, (float)a.d + G.maxdev + 0.05f);
+        a.gmoff[g] = G.moff;
     }
     o.ar = (float)r[0]; o.br = (float)r[1]; o.cr = (float)r[2]; o.R = (float)R;
     const double hs2 = D * D - 0.25 * d * d;
@@ -904,8 +914,13 @@ __global__ void __launch_bounds__(128) sg_prep_kernel(ChunkArgs a, int max_sg) {
     o.delta = all_k ? (float)(delta + 0.01) : 1e30f;
     o.border = (float)(fmax(0.0, hs - d) + 0.05);
     o.invD = (float)(1.0 / D);
-    o.W = (float)W; o.H = (float)H; o.pad0 = o.pad1 = 0.f;
+    o.W = (float)W; o.H = (float)H; o.pad0 = 0;
     const bool horiz = fabs(r[1]) >= fabs(r[0]);
+    const int qi = a.pair_q[pg];
+    o.toff = a.img_off[ti]; o.qoff = a.img_off[qi];
+    o.nalong = horiz ? a.dims[2 * ti] : a.dims[2 * ti + 1];
+    o.toffb = horiz ? a.roff[ti] : a.coff[ti];
+    o.dbase = a.tbase[o.p];
     const double al = horiz ? r[0] : r[1], be = horiz ? r[1] : r[0];
     const double Pm = horiz ? W : H, Qm = horiz ? H : W;
     const int nrows = horiz ? a.dims[2 * ti + 1] : a.dims[2 * ti];
@@ -1320,20 +1335,15 @@ __global__ void __launch_bounds__(WARPS * 32, MATCH_MINB) match_kernel(ChunkArgs
             atomicAdd(&a.dbg[8], (unsigned long long)SG.gcnt);
         }
         if (lane <= SG.gcnt) {
-            S.gbeg[lane] = lane < SG.gcnt ? max(a.grp[SG.g0 + lane].moff - SG.m0, 0) : SG.mcnt;
-            if (lane < SG.gcnt) {
-                const GroupRec& G = a.grp[SG.g0 + lane];
-                S.gl[lane] = G.K < 0 ? make_float4(0.f, 0.f, 1e30f, -1.f)
-                                     : make_float4(G.ar, G.br, G.cr, (float)a.d + G.maxdev + 0.05f);
-            }
+            S.gbeg[lane] = lane < SG.gcnt ? max(a.gmoff[SG.g0 + lane] - SG.m0, 0) : SG.mcnt;
+            if (lane < SG.gcnt) S.gl[lane] = a.gl4[SG.g0 + lane];
         }
         stage_members(a, S, SG.m0, SG.mcnt, 0);
         __syncwarp();
         const int pg = a.p0 + SG.p;
-        const int ti = a.pair_t[pg], qi = a.pair_q[pg];
-        const int64_t toff = a.img_off[ti], qoff = a.img_off[qi];
-        const int nalong = SG.horiz ? a.dims[2 * ti] : a.dims[2 * ti + 1];
-        const int64_t toffb = SG.horiz ? a.roff[ti] : a.coff[ti];
+        const int64_t toff = SG.toff, qoff = SG.qoff;
+        const int nalong = SG.nalong;
+        const int64_t toffb = SG.toffb;
         const int32_t* start = SG.horiz ? a.rstart : a.cstart;
         const int32_t* mem = SG.horiz ? a.rmem : a.cmem;
         const float2* mxy = SG.horiz ? a.rxy : a.cxy;
@@ -1342,10 +1352,10 @@ __global__ void __launch_bounds__(WARPS * 32, MATCH_MINB) match_kernel(ChunkArgs
         int cols_total = 0;
         if (lane < CAP / 32) S.sure[lane] = 0;
         __syncwarp();
-        // ---- strip gather: bucket rows of the strip |dist_base| <= R
-        for (int r0 = SG.rlo; r0 <= SG.rhi; r0 += 32) {
-            const int r = r0 + lane;
-            int bs = 0, len = 0;
+        // ---- strip gather: bucket rows of the strip |dist_base| <= R.  The CSR starts of
+        // the next 32 rows are loaded while the current rows' entries are processed.
+        auto row_span = [&](int r, int& bs, int& e1) {
+            bs = 0; e1 = 0;
             if (r <= SG.rhi) {
                 int blo = 0, bhi = nalong - 1;
                 if (SG.inv_alpha != 0.f) {
@@ -1361,10 +1371,16 @@ __global__ void __launch_bounds__(WARPS * 32, MATCH_MINB) match_kernel(ChunkArgs
                 }
                 if (blo <= bhi) {
                     const int64_t cb = toffb + (int64_t)r * nalong;
-                    bs = start[cb + blo];
-                    len = start[cb + bhi + 1] - bs;
+                    bs = __ldg(start + cb + blo);
+                    e1 = __ldg(start + cb + bhi + 1);
                 }
             }
+        };
+        int nbs, ne1;
+        row_span(SG.rlo + lane, nbs, ne1);
+        for (int r0 = SG.rlo; r0 <= SG.rhi; r0 += 32) {
+            const int bs = nbs, len = ne1 - nbs;
+            row_span(r0 + 32 + lane, nbs, ne1);
             int incl = len;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -1459,7 +1475,7 @@ __global__ void __launch_bounds__(WARPS * 32, MATCH_MINB) match_kernel(ChunkArgs
                 a.res_ratio[slot] = rr;
                 const unsigned long long key =
                     ((unsigned long long)__float_as_uint(db) << 32) | (unsigned)M.fid;
-                atomicMin(&a.dedupe[a.tbase[SG.p] + tid], key);
+                atomicMin(&a.dedupe[SG.dbase + tid], key);
             }
         }
         if (STATS && lane == 0 && cols_total > 0) {
@@ -1552,6 +1568,7 @@ size_t chunk_bytes(const ChunkSizes& c) {
     b += aligned_bytes<int32_t>(c.Q) * 2;              // mgid, msg
     b += aligned_bytes<unsigned>(c.Q);                 // gfit
     b += aligned_bytes<unsigned long long>(c.Q);       // sgdev
+    b += aligned_bytes<float4>(c.Q) + aligned_bytes<int32_t>(c.Q);   // gl4, gmoff
     b += aligned_bytes<double>(3 * c.Q);               // q_line
     b += aligned_bytes<int4>(c.Q);                     // grec
     b += aligned_bytes<int32_t>(c.Q) * 2;              // gfill, members
@@ -1769,6 +1786,7 @@ extern "C" int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids,
     a.q_fid = ar.take<int32_t>(w.Q);
     a.mgid = ar.take<int32_t>(w.Q); a.msg = ar.take<int32_t>(w.Q);
     a.gfit = ar.take<unsigned>(w.Q); a.sgdev = ar.take<unsigned long long>(w.Q);
+    a.gl4 = ar.take<float4>(w.Q); a.gmoff = ar.take<int32_t>(w.Q);
     a.tab_off = ar.take<int64_t>(w.P + 1); a.tbase = ar.take<int64_t>(w.P + 1);
     a.ngroups = ar.take<int32_t>(w.P + 1); a.gstart = ar.take<int32_t>(w.P + 1);
     a.nmem = ar.take<int32_t>(w.P + 1); a.sgstart = ar.take<int32_t>(w.P + 1);
