@@ -1184,7 +1184,7 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
             const unsigned tb0 = cur.tb0, tb1 = cur.tb1;
             const int r0 = mt * 16 + g, r1 = r0 + 8;
             const unsigned cm0 = r0 < n ? S.cmask[r0] : 0u, cm1 = r1 < n ? S.cmask[r1] : 0u;
-            float2 p0 = S.xy[r0 < n ? r0 : 0], p1 = S.xy[r1 < n ? r1 : 0];
+            const float2 p0 = S.xy[r0 < n ? r0 : 0], p1 = S.xy[r1 < n ? r1 : 0];
             float4 ML[NC];
             uint4 MH[NC];
 #pragma unroll
@@ -1193,8 +1193,6 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
                 ML[c] = lds_f4(&Mc->a);      // a, b, c, lo
                 MH[c] = lds_u4(&Mc->hi);     // hi, qn9, fid, slotgi
             }
-            if (!cm0) { p0.x = 1e30f; p0.y = 1e30f; }
-            if (!cm1) { p1.x = 1e30f; p1.y = 1e30f; }
             int acc[SG_NT][4];
 #pragma unroll
             for (int nt = 0; nt < SG_NT; nt++) {
@@ -1204,43 +1202,42 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
                 mma_u8(acc[nt], x01.x, x11.x, x01.y, x11.y, bw[nt][4], bw[nt][5]);
                 mma_u8(acc[nt], x01.z, x11.z, x01.w, x11.w, bw[nt][6], bw[nt][7]);
             }
-            // band test for all 8 elements first (straight-line code); the exact
-            // fp64 value is needed only inside [d - eps, d + eps] (rare, warp-uniform check)
+            // Fast path: elements surely inside the member band (fp32 value <= d - eps) and
+            // inside the group's C' go straight into the top-2; elements within eps of the
+            // band edge are collected in ucm and decided with the reference's fp64 value
+            // afterwards (rare; top-2 is insensitive to the push order).
             constexpr int NE = 4 * SG_NT;
-            bool inb[NE], unc[NE];
-            bool any_unc = false;
-#pragma unroll
-            for (int e = 0; e < NE; e++) {
-                const int c = (e >> 2) * 2 + (e & 1);
-                const float2 P = (e & 2) ? p1 : p0;
-                const float av = fabsf(fmaf(ML[c].x, P.x, fmaf(ML[c].y, P.y, ML[c].z)));
-                inb[e] = av <= ML[c].w;
-                unc[e] = !inb[e] && av <= __uint_as_float(MH[c].x);
-                any_unc |= unc[e];
-            }
-            if (__any_sync(FULL, any_unc)) {
-#pragma unroll
-                for (int e = 0; e < NE; e++) {
-                    if (!unc[e]) continue;
-                    const int c = (e >> 2) * 2 + (e & 1);
-                    const float2 P = (e & 2) ? p1 : p0;
-                    const GroupRec& Gc = a.grp[SG.g0 + (int)(MH[c].w >> 24)];
-                    const bool gemv = Gc.cnt == 1;
-                    const double* L = gemv ? &Gc.sl0 : a.q_line + 3 * (int64_t)(MH[c].w & 0xFFFFFFu);
-                    inb[e] = band_exact(L[0], L[1], L[2], gemv, (double)P.x, (double)P.y, a.d);
-                }
-            }
+            unsigned ucm = 0;
             bool any0 = false, any1 = false;
 #pragma unroll
             for (int e = 0; e < NE; e++) {
                 const int nt = e >> 2, q = e & 3, c = nt * 2 + (q & 1);
                 const bool rowhi = q >= 2;
-                const unsigned cm = rowhi ? cm1 : cm0;
-                const bool in = inb[e] && ((cm >> (MH[c].w >> 24)) & 1u);
-                if (rowhi) any1 |= in; else any0 |= in;
-                const unsigned base = (rowhi ? tb1 : tb0) + MH[c].y;
-                const unsigned key = in ? base - ((unsigned)acc[nt][q] << 10) : NONE;
-                top2_push(key, b1[c], b2[c]);
+                const float2 P = rowhi ? p1 : p0;
+                const float av = fabsf(fmaf(ML[c].x, P.x, fmaf(ML[c].y, P.y, ML[c].z)));
+                const bool cbit = ((rowhi ? cm1 : cm0) >> (MH[c].w >> 24)) & 1u;
+                const bool sure_in = av <= ML[c].w && cbit;
+                if (!(av <= ML[c].w) && av <= __uint_as_float(MH[c].x) && cbit) ucm |= 1u << e;
+                if (STATS) { if (rowhi) any1 |= sure_in; else any0 |= sure_in; }
+                const unsigned key = (rowhi ? tb1 : tb0) + MH[c].y - ((unsigned)acc[nt][q] << 10);
+                top2_push(sure_in ? key : NONE, b1[c], b2[c]);
+            }
+            if (__any_sync(FULL, ucm != 0)) {
+#pragma unroll
+                for (int e = 0; e < NE; e++) {
+                    if (!((ucm >> e) & 1u)) continue;
+                    const int nt = e >> 2, q = e & 3, c = nt * 2 + (q & 1);
+                    const bool rowhi = q >= 2;
+                    const float2 P = rowhi ? p1 : p0;
+                    const GroupRec& Gc = a.grp[SG.g0 + (int)(MH[c].w >> 24)];
+                    const bool gemv = Gc.cnt == 1;
+                    const double* L = gemv ? &Gc.sl0 : a.q_line + 3 * (int64_t)(MH[c].w & 0xFFFFFFu);
+                    if (band_exact(L[0], L[1], L[2], gemv, (double)P.x, (double)P.y, a.d)) {
+                        if (STATS) { if (rowhi) any1 = true; else any0 = true; }
+                        const unsigned key = (rowhi ? tb1 : tb0) + MH[c].y - ((unsigned)acc[nt][q] << 10);
+                        top2_push(key, b1[c], b2[c]);
+                    }
+                }
             }
             if (STATS) {
                 unsigned m0 = __ballot_sync(FULL, any0);
