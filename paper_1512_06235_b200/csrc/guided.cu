@@ -417,7 +417,10 @@ __global__ void plan_kernel(ChunkArgs a) {
     }
 }
 
-__global__ void __launch_bounds__(256) lines_kernel(ChunkArgs a) {
+#ifndef MSFM_LINES_T
+#define MSFM_LINES_T 1024
+#endif
+__global__ void __launch_bounds__(MSFM_LINES_T) lines_kernel(ChunkArgs a) {
     const int p = blockIdx.x, pg = a.p0 + p;
     const int64_t q0 = a.qlist_off[pg];
     const int nq = (int)(a.qlist_off[pg + 1] - q0);
@@ -487,10 +490,11 @@ __global__ void __launch_bounds__(256) lines_kernel(ChunkArgs a) {
 // ranges in that order.  The order only affects how members are packed into
 // super-groups, never any result.
 constexpr int GB = 4096;
-__global__ void __launch_bounds__(256) groups_kernel(ChunkArgs a) {
-    __shared__ int sm[256 / 32 + 1];
+constexpr int GT = 1024;   // groups_kernel threads per pair
+__global__ void __launch_bounds__(GT) groups_kernel(ChunkArgs a) {
+    __shared__ int sm[GT / 32 + 1];
     __shared__ int hist[GB];
-    __shared__ float fmin_s[8], fmax_s[8];
+    __shared__ float fmin_s[GT / 32], fmax_s[GT / 32];
     const int p = blockIdx.x, pg = a.p0 + p;
     const int64_t s0 = a.qlist_off[pg] - a.qbase;
     const int64_t t0 = a.tab_off[p];
@@ -498,7 +502,7 @@ __global__ void __launch_bounds__(256) groups_kernel(ChunkArgs a) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int gcarry = 0;
     float lo = 1e30f, hi = -1e30f;
-    for (int e0 = 0; e0 < tsize; e0 += 256) {
+    for (int e0 = 0; e0 < tsize; e0 += GT) {
         const int e = e0 + threadIdx.x;
         bool occ = false;
         unsigned cnt = 0, rep = 0;
@@ -507,7 +511,7 @@ __global__ void __launch_bounds__(256) groups_kernel(ChunkArgs a) {
             if (occ) { cnt = a.tab_cnt[t0 + e]; rep = a.tab_rep[t0 + e]; }
         }
         int gtot;
-        const int lg = block_exclusive_scan<256>(occ ? 1 : 0, &gtot, sm);
+        const int lg = block_exclusive_scan<GT>(occ ? 1 : 0, &gtot, sm);
         if (occ) {
             const int g = gcarry + lg;
             a.gtmp[s0 + g] = make_int2((int)rep, (int)cnt);
@@ -528,54 +532,54 @@ __global__ void __launch_bounds__(256) groups_kernel(ChunkArgs a) {
         hi = fmaxf(hi, __shfl_xor_sync(FULL, hi, o));
     }
     if (lane == 0) { fmin_s[wid] = lo; fmax_s[wid] = hi; }
-    for (int b = threadIdx.x; b < GB; b += 256) hist[b] = 0;
+    for (int b = threadIdx.x; b < GB; b += GT) hist[b] = 0;
     __syncthreads();
     lo = fmin_s[0]; hi = fmax_s[0];
-    for (int w = 1; w < 8; w++) { lo = fminf(lo, fmin_s[w]); hi = fmaxf(hi, fmax_s[w]); }
+    for (int w = 1; w < GT / 32; w++) { lo = fminf(lo, fmin_s[w]); hi = fmaxf(hi, fmax_s[w]); }
     const float scale = (float)GB / fmaxf(hi - lo, 1e-20f);
-    for (int g = threadIdx.x; g < ng; g += 256) {
+    for (int g = threadIdx.x; g < ng; g += GT) {
         const int b = min(GB - 1, max(0, (int)((a.gkey[s0 + g] - lo) * scale)));
         atomicAdd(&hist[b], 1);
     }
     __syncthreads();
     // exclusive scan of the histogram (16 buckets per thread)
     {
-        int v[GB / 256];
+        int v[GB / GT];
         int s = 0;
-        for (int k = 0; k < GB / 256; k++) { v[k] = hist[threadIdx.x * (GB / 256) + k]; s += v[k]; }
+        for (int k = 0; k < GB / GT; k++) { v[k] = hist[threadIdx.x * (GB / GT) + k]; s += v[k]; }
         int tot;
-        int ex = block_exclusive_scan<256>(s, &tot, sm);
-        for (int k = 0; k < GB / 256; k++) { hist[threadIdx.x * (GB / 256) + k] = ex; ex += v[k]; }
+        int ex = block_exclusive_scan<GT>(s, &tot, sm);
+        for (int k = 0; k < GB / GT; k++) { hist[threadIdx.x * (GB / GT) + k] = ex; ex += v[k]; }
     }
     __syncthreads();
-    for (int g = threadIdx.x; g < ng; g += 256) {
+    for (int g = threadIdx.x; g < ng; g += GT) {
         const int b = min(GB - 1, max(0, (int)((a.gkey[s0 + g] - lo) * scale)));
         a.gpos[s0 + g] = atomicAdd(&hist[b], 1);
     }
     __syncthreads();
     int mcarry = 0;
     // write grec in sorted order (scatter by gpos), then scan counts in that order
-    for (int g = threadIdx.x; g < ng; g += 256) {
+    for (int g = threadIdx.x; g < ng; g += GT) {
         const int2 r = a.gtmp[s0 + g];
         a.grec[s0 + a.gpos[s0 + g]] = make_int4(r.x, r.y, 0, 0);
     }
     __syncthreads();
-    for (int i0 = 0; i0 < ng; i0 += 256) {
+    for (int i0 = 0; i0 < ng; i0 += GT) {
         const int i = i0 + threadIdx.x;
         const int cnt = i < ng ? a.grec[s0 + i].y : 0;
         int tot;
-        const int ex = block_exclusive_scan<256>(cnt, &tot, sm);
+        const int ex = block_exclusive_scan<GT>(cnt, &tot, sm);
         if (i < ng) a.grec[s0 + i].z = (int)(s0 + mcarry + ex);
         mcarry += tot;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < tsize; e += 256) {
+    for (int e = threadIdx.x; e < tsize; e += GT) {
         if (a.tab_key[t0 + e] != EMPTY) a.tab_rep[t0 + e] = (unsigned)a.gpos[s0 + a.tab_rep[t0 + e]];
     }
     // boundary endpoints of every representative line (in sorted order)
     const int ti = a.pair_t[pg];
     const double W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1];
-    for (int g = threadIdx.x; g < ng; g += 256) {
+    for (int g = threadIdx.x; g < ng; g += GT) {
         const int4 gr = a.grec[s0 + g];
         const double* L = a.q_line + 3 * (s0 + gr.x);
         const double l[3] = {L[0], L[1], L[2]};
@@ -591,13 +595,13 @@ __global__ void __launch_bounds__(256) groups_kernel(ChunkArgs a) {
     // The tau tests run in parallel (gfit bit i: group g+1+i fits group g's line);
     // one thread then walks the groups with integer work only.
     if (a.stats_mode) {
-        for (int g = threadIdx.x; g < ng; g += 256) {
+        for (int g = threadIdx.x; g < ng; g += GT) {
             const int4 gr = a.grec[s0 + g];
             a.sglist[s0 + g] = make_int2(gr.z, gr.y);
         }
         if (threadIdx.x == 0) a.nsg[p] = ng;
     } else {
-        for (int g = threadIdx.x; g < ng; g += 256) {
+        for (int g = threadIdx.x; g < ng; g += GT) {
             const float4 ln = a.gline[s0 + g];
             unsigned bits = 0;
             const int lim = min(SG_MEMBERS, ng - 1 - g);
@@ -616,7 +620,7 @@ __global__ void __launch_bounds__(256) groups_kernel(ChunkArgs a) {
         // chain from 0 through shared memory.
         extern __shared__ unsigned short send[];
         const int nm = mcarry;
-        for (int g = threadIdx.x; g < ng; g += 256) {
+        for (int g = threadIdx.x; g < ng; g += GT) {
             const int4 gr = a.grec[s0 + g];
             const int cnt = gr.y, rel0 = (int)(gr.z - s0);
             const unsigned fit = a.gfit[s0 + g];
@@ -676,7 +680,7 @@ __global__ void gscan_kernel(ChunkArgs a) {
     }
 }
 
-__global__ void __launch_bounds__(256) scatter_kernel(ChunkArgs a) {
+__global__ void __launch_bounds__(MSFM_LINES_T) scatter_kernel(ChunkArgs a) {
     const int p = blockIdx.x, pg = a.p0 + p;
     const int64_t q0 = a.qlist_off[pg];
     const int nq = (int)(a.qlist_off[pg + 1] - q0);
@@ -737,14 +741,6 @@ __device__ double band_deviation(const double m[3], const double r[3], double W,
 }
 
 // |dist_g - dist_base| over the whole image rectangle (affine -> max at a corner)
-__device__ double rect_deviation(const double g[3], const double r[3], double W, double H) {
-    const double da = g[0] - r[0], db = g[1] - r[1], dc = g[2] - r[2];
-    double dev = fabs(dc);
-    dev = fmax(dev, fabs(da * W + dc));
-    dev = fmax(dev, fabs(db * H + dc));
-    dev = fmax(dev, fabs(da * W + db * H + dc));
-    return dev;
-}
 
 // Per group: the C' geometry of its representative line + member constants.
 __global__ void __launch_bounds__(128) prep_kernel(ChunkArgs a, int max_groups) {
@@ -756,7 +752,7 @@ __global__ void __launch_bounds__(128) prep_kernel(ChunkArgs a, int max_groups) 
     const int64_t q0 = a.qlist_off[pg];
     const int64_t s0 = q0 - a.qbase;
     const int4 g = a.grec[s0 + (gid - a.gstart[p])];
-    const int ti = a.pair_t[pg], qi = a.pair_q[pg];
+    const int ti = a.pair_t[pg];
     const double W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1], D = a.D, d = a.d;
     const double* rl = a.q_line + 3 * (s0 + g.x);
     const double r[3] = {rl[0], rl[1], rl[2]};
@@ -1818,15 +1814,15 @@ extern "C" int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids,
         a.qbase = h_qlist_off[p0];
         const int64_t Q = h_qlist_off[p1] - h_qlist_off[p0];
         plan_kernel<<<1, SCAN_T, 0, st>>>(a);
-        { ProfScope ps("lines_kernel", st); lines_kernel<<<a.npairs, 256, 0, st>>>(a); }
+        { ProfScope ps("lines_kernel", st); lines_kernel<<<a.npairs, MSFM_LINES_T, 0, st>>>(a); }
         {
             int64_t max_nq = 1;
             for (int k = p0; k < p1; k++) max_nq = std::max(max_nq, h_qlist_off[k + 1] - h_qlist_off[k]);
             ProfScope ps("groups_kernel", st);
-            groups_kernel<<<a.npairs, 256, (size_t)(2 * max_nq + 16), st>>>(a);
+            groups_kernel<<<a.npairs, GT, (size_t)(2 * max_nq + 16), st>>>(a);
         }
         gscan_kernel<<<1, SCAN_T, 0, st>>>(a);
-        { ProfScope ps("scatter_kernel", st); scatter_kernel<<<a.npairs, 256, 0, st>>>(a); }
+        { ProfScope ps("scatter_kernel", st); scatter_kernel<<<a.npairs, MSFM_LINES_T, 0, st>>>(a); }
         if (Q > 0) {
             const unsigned nb = (unsigned)((Q + 127) / 128);
             { ProfScope ps("prep_kernel", st); prep_kernel<<<nb, 128, 0, st>>>(a, (int)Q); }
