@@ -148,6 +148,10 @@ typedef struct {
     float single_cap;    /* single-candidate cap (SINGLE_CANDIDATE_CAP = 45)     */
     int32_t max_nt;      /* max target feature count over the batch (<= 65536)   */
     int32_t chunk_pairs; /* pairs per internal chunk (workspace bound), 0 = auto  */
+    int32_t strategy;    /* candidate strategy of guided_match_pair (guided.py:425-431):
+                          * 0 grid (cells of the samples, default), 1 linear
+                          * (|rep line| <= d, guided.py:190-194), 2 radial (disks of
+                          * radius d*sqrt(2) around the samples, guided.py:273-285) */
 } msfm_match_params;
 
 /* Pack the per-pair segments of msfm_guided_match's output into contiguous

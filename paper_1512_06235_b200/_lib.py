@@ -33,7 +33,7 @@ class Grids(ctypes.Structure):
 class MatchParams(ctypes.Structure):
     _fields_ = [("d", ctypes.c_double), ("ratio", ctypes.c_float),
                 ("single_cap", ctypes.c_float), ("max_nt", ctypes.c_int32),
-                ("chunk_pairs", ctypes.c_int32)]
+                ("chunk_pairs", ctypes.c_int32), ("strategy", ctypes.c_int32)]
 
 
 _SIGS = {

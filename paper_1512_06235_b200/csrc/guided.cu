@@ -353,6 +353,8 @@ struct ChunkArgs {
     double D, d;
     float ratio, single_cap;
     int stats_mode;              // 1: one super-group per group (exact SearchStats)
+    int strategy;                // 0 grid, 1 linear, 2 radial (msfm_match_params)
+    double r2;                   // radial: (d * sqrt(2))^2 as the reference rounds it
     float sg_tau;                // super-group line tolerance (px)
     // pairs
     const int32_t* pair_q; const int32_t* pair_t; const double* pair_F;
@@ -899,16 +901,20 @@ __global__ void __launch_bounds__(128) sg_prep_kernel(ChunkArgs a, int max_sg) {
         all_k = all_k && G.K >= 0;
         // compact per-group view for the match kernel (groups shared by two
         // super-groups get the same values twice)
-        a.gl4[g] = G.K < 0 ? make_float4(0.f, 0.f, 1e30f, -1.f)
+        a.gl4[g] = (G.K < 0 && a.strategy != 1) ? make_float4(0.f, 0.f, 1e30f, -1.f)
                            : make_float4(G.ar, G.br, G.cr, (float)a.d + G.maxdev + 0.05f);
         a.gmoff[g] = G.moff;
     }
     o.ar = (float)r[0]; o.br = (float)r[1]; o.cr = (float)r[2]; o.R = (float)R;
-    const double hs2 = D * D - 0.25 * d * d;
-    const double hs = hs2 > 0 ? sqrt(hs2) - 0.075 : -1.0;
+    // sure-in-C' radius around the base line: grid, the 3x3 subcell block of the
+    // nearest sample (half-size D); radial, the disk of radius r around it; both with the
+    // sample spacing <= d.  Linear: the rep-line band itself (fp32 error << 0.05 px).
+    const double DC = a.strategy == 2 ? sqrt(a.r2) : D;
+    const double hs2 = DC * DC - 0.25 * d * d;
+    const double hs = a.strategy == 1 ? d - 0.05 : (hs2 > 0 ? sqrt(hs2) - 0.075 : -1.0);
     o.hsure = (float)hs;
-    o.delta = all_k ? (float)(delta + 0.01) : 1e30f;
-    o.border = (float)(fmax(0.0, hs - d) + 0.05);
+    o.delta = (all_k || a.strategy == 1) ? (float)(delta + 0.01) : 1e30f;
+    o.border = a.strategy == 1 ? -1e30f : (float)(fmax(0.0, hs - d) + 0.05);
     o.invD = (float)(1.0 / D);
     o.W = (float)W; o.H = (float)H; o.pad0 = 0;
     const bool horiz = fabs(r[1]) >= fabs(r[0]);
@@ -993,13 +999,51 @@ __device__ bool in_cprime_exact(const GroupRec& G, double D, float fx, float fy,
 }
 
 // C' membership of f for group G, using the sure zone first
+// the reference's float64 band value for one (member, target) element, guided.py:447
+__device__ __forceinline__ bool band_exact(double A, double B, double C, bool gemv, double x,
+                                           double y, double d) {
+    double v = gemv ? fma(A, x, B * y) : fma(B, y, A * x);
+    v = v + C;
+    return fabs(v) <= d;
+}
+
+// radial (guided.py:273-285): some sample within r of f, squared distance in f64
+// exactly as scipy's cKDTree.query_ball_point compares it (dx*dx + dy*dy <= r*r)
+__device__ bool in_radial_exact(const GroupRec& G, double r2, float fx, float fy) {
+    if (G.K < 0) return false;
+    const float tau = (fx - G.pbx) * G.dirx + (fy - G.pby) * G.diry;
+    const float reach = (float)sqrt(r2) + 1.0f;
+    const float inv_sp = 1.0f / G.spacing;
+    int klo = (int)floorf((tau - reach) * inv_sp) - 1;
+    int khi = (int)ceilf((tau + reach) * inv_sp) + 1;
+    if (klo < 0) klo = 0;
+    if (khi > G.K) khi = G.K;
+    const double x = (double)fx, y = (double)fy, Kd = (double)G.K;
+    for (int k = klo; k <= khi; k++) {
+        const double kd = (double)k, rk = (double)(G.K - k);
+        const double sx = (kd * G.pax + rk * G.pbx64) / Kd;
+        const double sy = (kd * G.pay + rk * G.pby64) / Kd;
+        const double dx = x - sx, dy = y - sy;
+        if (dx * dx + dy * dy <= r2) return true;
+    }
+    return false;
+}
+
 __device__ __forceinline__ bool in_cprime(const ChunkArgs& a, const GroupRec& G, const SGRec& S,
                                           float fx, float fy, int64_t toff, int f) {
+    if (a.strategy == 1) {
+        // linear (guided.py:190-194): |xy @ [a, b] + c| <= d, a dgemv (fma(a, x, b*y))
+        const float dg = fabsf(fmaf(G.ar, fx, fmaf(G.br, fy, G.cr)));
+        if (dg <= S.hsure) return true;
+        const double* L = a.q_line + 3 * (int64_t)G.rep;
+        return band_exact(L[0], L[1], L[2], true, (double)fx, (double)fy, a.d);
+    }
     if (G.K < 0) return false;
     const float dg = fabsf(fmaf(G.ar, fx, fmaf(G.br, fy, G.cr)));
     if (dg <= S.hsure && fx >= S.border && fx <= S.W - S.border && fy >= S.border &&
         fy <= S.H - S.border)
         return true;
+    if (a.strategy == 2) return in_radial_exact(G, a.r2, fx, fy);
     const int su = a.sub[toff + f];
     return in_cprime_exact(G, a.D, fx, fy, (short)(su & 0xffff), su >> 16);
 }
@@ -1019,13 +1063,6 @@ struct alignas(16) WarpSmem {
 static_assert(offsetof(WarpSmem, mr) % 16 == 0, "member records must be 16-B aligned");
 static_assert(sizeof(MemberRec) == 32, "MemberRec is read as two 16-B shared loads");
 
-// the reference's float64 band value for one (member, target) element, guided.py:447
-__device__ __forceinline__ bool band_exact(double A, double B, double C, bool gemv, double x,
-                                           double y, double d) {
-    double v = gemv ? fma(A, x, B * y) : fma(B, y, A * x);
-    v = v + C;
-    return fabs(v) <= d;
-}
 
 __device__ __forceinline__ bool member_band(const ChunkArgs& a, int gid, const MemberRec& M,
                                             float x, float y) {
@@ -1769,6 +1806,15 @@ extern "C" int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids,
     a.rxy = reinterpret_cast<const float2*>(grids->d_rxy);
     a.cxy = reinterpret_cast<const float2*>(grids->d_cxy);
     a.D = grids->D; a.d = prm->d; a.ratio = prm->ratio; a.single_cap = prm->single_cap;
+    if (prm->strategy < 0 || prm->strategy > 2) {
+        set_error("msfm_guided_match: unknown strategy %d", prm->strategy);
+        return MSFM_EINVAL;
+    }
+    a.strategy = prm->strategy;
+    {
+        const double r = prm->d * sqrt(2.0);      // guided.py:275 radius_factor=np.sqrt(2.0)
+        a.r2 = r * r;
+    }
     a.stats_mode = d_stats ? 1 : 0;
     {
         const char* e = getenv("MSFM_SG_TAU");

@@ -23,6 +23,7 @@ BAND_D_PX = 8.0          # guided.py:39
 GRID_INFLATION = 1.25    # guided.py:40
 RATIO_GUIDED = 0.8       # matching.py:22
 SINGLE_CANDIDATE_CAP = 45.0  # matching.py:27
+STRATEGIES = {"grid": 0, "linear": 1, "radial": 2}   # guided.py:425-431
 
 
 # one packed match row (msfm_pack_matches): 16 bytes, little-endian
@@ -85,7 +86,7 @@ def match_pairs(bank: FeatureBank, q_img, t_img, F, query_lists, *, d: float = B
                 ratio: float = RATIO_GUIDED, inflation: float = GRID_INFLATION,
                 grid_d: float | None = None, single_cap: float = SINGLE_CANDIDATE_CAP,
                 with_stats: bool = False, chunk_pairs: int = 0, stream=None,
-                device_inputs=None) -> PairMatches:
+                device_inputs=None, strategy: str = "grid") -> PairMatches:
     """Match every pair k: query image q_img[k] against target t_img[k].
 
     ``F`` is (P,3,3) float64 (NaN rows mark degenerate pairs, skipped as
@@ -97,6 +98,8 @@ def match_pairs(bank: FeatureBank, q_img, t_img, F, query_lists, *, d: float = B
     lib = _lib.load()
     if d <= 0:
         raise ValueError(f"cell half-size d must be positive, got {d}")
+    if strategy not in STRATEGIES:
+        raise ValueError(f"unknown strategy {strategy!r}")
     D = float(grid_d) if grid_d is not None else float(d) * float(inflation)
     P = len(q_img)
     dev = bank.device
@@ -107,7 +110,7 @@ def match_pairs(bank: FeatureBank, q_img, t_img, F, query_lists, *, d: float = B
     nq_total = int(qoff[-1]) if P else 0
     grid = bank.grid(D, stream)
     prm = _lib.MatchParams(float(d), float(np.float32(ratio)), float(np.float32(single_cap)),
-                           max(bank.max_n, 1), int(chunk_pairs))
+                           max(bank.max_n, 1), int(chunk_pairs), STRATEGIES[strategy])
     qoff_c = np.ascontiguousarray(qoff, dtype=np.int64)
     ws_bytes = lib.msfm_guided_workspace_bytes(P, qoff_c.ctypes.data, ctypes.byref(prm))
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
@@ -206,13 +209,13 @@ def guided_match_pair(query_fs, target_fs, geom, *, d: float = BAND_D_PX,
     ti = np.arange(len(target_fs)) if target_indices is None else np.asarray(target_indices)
     if len(ti) == 0:
         return []
-    if strategy != "grid":
-        if strategy in ("linear", "radial"):
-            raise NotImplementedError(f"strategy {strategy!r} has no B200 kernel yet")
+    if strategy not in STRATEGIES:
         raise ValueError(f"unknown strategy {strategy!r}")
     D = float(grid.d) if grid is not None and hasattr(grid, "d") else d * inflation
-    if D <= 0:
+    if D <= 0 and strategy == "grid":
         raise ValueError(f"cell half-size d must be positive, got {D}")
+    if strategy != "grid":
+        D = max(D, 1.0)   # the index is built but only grid mode consults its cells
     qi = np.arange(len(query_fs)) if query_indices is None else np.asarray(query_indices)
     qi = np.unique(qi.astype(np.int64))  # duplicates cannot change the match set
     if target_indices is None:
@@ -224,7 +227,8 @@ def guided_match_pair(query_fs, target_fs, geom, *, d: float = BAND_D_PX,
     F = np.asarray(geom.F if hasattr(geom, "F") else geom, dtype=np.float64).reshape(1, 3, 3)
     with _DROPIN_LOCK:
         res = match_pairs(bank, [0], [1], F, [qi.astype(np.int32)], d=d, ratio=ratio,
-                          grid_d=D, single_cap=single_cap, with_stats=stats is not None)
+                          grid_d=D, single_cap=single_cap, with_stats=stats is not None,
+                          strategy=strategy)
         _, q, t, dist, rat = res.to_host()
         s = res.stats.cpu().numpy() if stats is not None else None
     if stats is not None:

@@ -143,5 +143,40 @@ def main():
     save("guided_8k.npz", kw, sc, run_pairs(sc, items))
 
 
+def strategies():
+    """guided_match_pair with strategy="linear" / "radial" (guided.py:190-194,
+    273-285, 425-431) on the unit scenes, the edge cases, C1 pairs and two 8k pairs."""
+    for strat in ("linear", "radial"):
+        rows_all = []
+        scenes_kw = []
+        for seed in (9, 10):
+            kw = dict(n_cameras=2, layout="grid", ring_radius=1.2, cloud_radius=2.0,
+                      n_points=600, seed=seed)
+            sc = generate_scene(SceneSpec(**kw))
+            save(f"strategy_{strat}_s{seed}.npz", kw, sc,
+                 run_pairs(sc, [(0, 1, None), (1, 0, None)], strategy=strat))
+        sc = generate_scene(SceneSpec(n_cameras=3, n_points=400, seed=5))
+        items = [(0, 1, np.array([7])), (0, 1, np.array([], np.int64)),
+                 (1, 2, np.arange(0, 60, 3)), (2, 0, np.array([0, 1])), (1, 0, None)]
+        save(f"strategy_{strat}_edges.npz", dict(n_cameras=3, n_points=400, seed=5), sc,
+             run_pairs(sc, items, strategy=strat))
+        kw = dict(n_cameras=20, n_points=2000, visibility_fraction=0.6, pixel_noise=0.5,
+                  descriptor_noise=4.0, seed=1)
+        sc = generate_scene(SceneSpec(**kw))
+        model = coarse_model(sc, range(20))
+        items = densify_inputs(model, sc)[::4]
+        save(f"strategy_{strat}_C1.npz", kw, sc, run_pairs(sc, items, strategy=strat))
+        kw = dict(n_cameras=10, n_points=12000, image_width=3072, image_height=2304, focal=2600.0,
+                  visibility_fraction=0.55, clutter_per_image=2700, pixel_noise=0.5,
+                  descriptor_noise=4.0, seed=2)
+        sc = generate_scene(SceneSpec(**kw))
+        model = coarse_model(sc, range(10))
+        items = densify_inputs(model, sc)[:2]
+        save(f"strategy_{strat}_8k.npz", kw, sc, run_pairs(sc, items, strategy=strat))
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["strategies"]:
+        strategies()
+    else:
+        main()

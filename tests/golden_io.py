@@ -40,6 +40,8 @@ def load(name):
 
 
 GUIDED_FIXTURES = sorted(f for f in os.listdir(GOLDEN) if f.startswith("guided_") and f.endswith(".npz"))
+STRATEGY_FIXTURES = sorted(f for f in os.listdir(GOLDEN)
+                           if f.startswith("strategy_") and f.endswith(".npz"))
 
 
 def load_localize(name):

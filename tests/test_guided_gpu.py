@@ -5,7 +5,7 @@ f32 distances, f32 ratios and SearchStats."""
 import numpy as np
 import pytest
 
-from golden_io import GUIDED_FIXTURES, load
+from golden_io import GUIDED_FIXTURES, STRATEGY_FIXTURES, load
 
 pytestmark = pytest.mark.gpu
 
@@ -160,3 +160,53 @@ def test_shared_query_lists_and_packed_rows():
     assert np.all(np.diff(pk) >= 0)
     cnt = b.count.cpu().numpy()
     np.testing.assert_array_equal(np.bincount(pk, minlength=len(ok)), cnt)
+
+
+@pytest.mark.parametrize("name", STRATEGY_FIXTURES)
+def test_linear_and_radial_strategies_equal_reference(name):
+    """strategy="linear" (rep-line band, guided.py:190-194) and "radial" (disks of
+    radius d*sqrt(2) around the samples, guided.py:273-285): match sets and
+    SearchStats identical to the reference's."""
+    from paper_1512_06235_b200.geometry import fundamental_from_poses
+    from paper_1512_06235_b200.guided import match_pairs
+
+    strategy = name.split("_")[1]
+    _, scene, _, pairs = load(name)
+    bank = _bank(scene.feature_sets)
+    F = np.stack([fundamental_from_poses(scene.cameras[p["q"]], scene.cameras[p["t"]]).F
+                  for p in pairs])
+    ql = [np.arange(len(scene.feature_sets[p["q"]]), dtype=np.int32) if p["qi"] is None
+          else p["qi"] for p in pairs]
+    res = match_pairs(bank, [p["q"] for p in pairs], [p["t"] for p in pairs], F, ql,
+                      with_stats=True, strategy=strategy)
+    pk, q, t, d, r = res.to_host()
+    stats = res.stats.cpu().numpy()
+    for k, p in enumerate(pairs):
+        sel = pk == k
+        _assert_same(p, q[sel], t[sel], d[sel], r[sel])
+        np.testing.assert_array_equal(stats[k], p["stats"])
+    # and without stats (super-group path)
+    res = match_pairs(bank, [p["q"] for p in pairs], [p["t"] for p in pairs], F, ql,
+                      strategy=strategy)
+    pk, q, t, d, r = res.to_host()
+    for k, p in enumerate(pairs):
+        sel = pk == k
+        _assert_same(p, q[sel], t[sel], d[sel], r[sel])
+
+
+def test_dropin_strategies_and_errors():
+    from paper_1512_06235_b200.geometry import fundamental_from_poses
+    from paper_1512_06235_b200.guided import guided_match_pair
+    from paper_1512_06235_b200.types import SearchStats
+
+    _, scene, _, pairs = load("strategy_radial_s9.npz")
+    p = pairs[0]
+    geom = fundamental_from_poses(scene.cameras[p["q"]], scene.cameras[p["t"]])
+    st = SearchStats()
+    ms = guided_match_pair(scene.feature_sets[p["q"]], scene.feature_sets[p["t"]], geom,
+                           strategy="radial", stats=st)
+    np.testing.assert_array_equal([m.query.feature_id for m in ms], p["mq"])
+    assert (st.queries, st.candidates) == tuple(p["stats"])
+    with pytest.raises(ValueError):
+        guided_match_pair(scene.feature_sets[p["q"]], scene.feature_sets[p["t"]], geom,
+                          strategy="bogus")
