@@ -45,6 +45,7 @@ struct KnnSmem {
     uint64_t t_full[2], t_empty[2];
     uint32_t tmem_base;
     int merge_k1[EPI_WARPS / 4][TILE_M], merge_i1[EPI_WARPS / 4][TILE_M], merge_k2[EPI_WARPS / 4][TILE_M];
+    alignas(16) int fvs[];   // |f|^2 of the current unit's image (fn_stride ints)
 };
 
 struct KnnArgs {
@@ -298,6 +299,14 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_lo, const __grid_constant_
             const int nt = unit_tiles(a, u, img, mt, off, n);
             const int grow = mt * TILE_M + row;
             const int np = grow < a.M_pad ? a.n[grow] : 0;
+            {
+                // stage the image's |f|^2 row in shared memory (broadcast reads per chunk)
+                const int slot = u - mt * a.n_img;
+                const int4* src = reinterpret_cast<const int4*>(a.fn_pad + (int64_t)slot * a.fn_stride);
+                int4* dst = reinterpret_cast<int4*>(S.fvs);
+                for (int i = ew * 32 + lane; i < a.fn_stride / 4; i += EPI_WARPS * 32) dst[i] = __ldg(src + i);
+                asm volatile("bar.sync 1, %0;" ::"r"(EPI_WARPS * 32));
+            }
             // running top-2 of this row over its column slice: k1 (best key), k2 (second
             // smallest key value), best column = ibase + il.  Branch-free per score:
             // two ops for the key, five for the update.
@@ -307,8 +316,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_lo, const __grid_constant_
                 tc_fence_after();
                 const uint32_t t_lo = tbase + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * 256 + half * EPI_COLS);
                 const int cbase = j * TILE_N + half * EPI_COLS;
-                const int slot = u - mt * a.n_img;
-                const int4* fp = reinterpret_cast<const int4*>(a.fn_pad + (int64_t)slot * a.fn_stride + cbase);
+                const int4* fp = reinterpret_cast<const int4*>(S.fvs + cbase);
                 const bool full = cbase + EPI_COLS <= n;
 #pragma unroll
                 for (int c0 = 0; c0 < EPI_COLS; c0 += 16) {
@@ -318,7 +326,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_lo, const __grid_constant_
                     int fv[16];
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
-                        const int4 f4 = __ldg(fp + (c0 >> 2) + q);
+                        const int4 f4 = fp[(c0 >> 2) + q];
                         fv[4 * q] = f4.x; fv[4 * q + 1] = f4.y; fv[4 * q + 2] = f4.z; fv[4 * q + 3] = f4.w;
                     }
                     tmem_wait_ld();
@@ -636,7 +644,12 @@ extern "C" int msfm_knn2_tracks(const msfm_bank* bank, int32_t n_points, const i
     a.out_k1 = d_k1;
     a.out_i1 = d_i1;
     a.out_k2 = d_k2;
-    const size_t smem = sizeof(KnnSmem) + 1024;
+    const size_t smem = sizeof(KnnSmem) + (size_t)fstride * sizeof(int32_t) + 1024;
+    if (smem > 227 * 1024) {
+        set_error("msfm_knn2_tracks: %d features per image exceed the shared-memory |f|^2 row",
+                  max_n);
+        return MSFM_EINVAL;
+    }
     MSFM_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
     int dev = 0, nsm = 148;
