@@ -258,6 +258,26 @@ int msfm_triangulate_batch(const double* d_K, const double* d_R, const double* d
                            const double* d_pix, double max_error, double min_angle_deg,
                            double* d_X, double* d_err, int32_t* d_status, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Track merge of densify_stage (densify.py:68-158): connected components over
+ * one stage's matches plus the model tracks, with the reference's conflict
+ * rules (two owning points: dropped; an image holding an owner ref keeps the
+ * ref; otherwise one node per image, smallest (support distance, key)).
+ * Nodes are bank feature rows (bank images in ascending id: node order is the
+ * reference's (image, feature) key order).
+ *   d_u, d_v, d_dist [n_edges]      matched nodes and f32 distances
+ *   d_track_ptr [n_points+1], d_track_node  model tracks as bank nodes
+ * Output: fresh nodes grouped per emitting component (ascending smallest node),
+ * ascending inside: d_out_node [<= 2 n_edges]; per segment d_seg_owner (track
+ * row extended, -1 = new track) and d_seg_off [n_seg+1]; d_counts = {n_seg, n_out}.
+ * ---------------------------------------------------------------------- */
+size_t msfm_merge_workspace_bytes(int64_t n_nodes, int64_t n_edges);
+int msfm_merge_tracks(const msfm_bank* bank, int64_t n_edges, const int32_t* d_u,
+                      const int32_t* d_v, const float* d_dist, int32_t n_points,
+                      const int64_t* d_track_ptr, const int32_t* d_track_node,
+                      int32_t* d_out_node, int32_t* d_seg_owner, int64_t* d_seg_off,
+                      int64_t* d_counts, void* d_workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -2,10 +2,10 @@
 
 Pairs come from covisibility (a sparse V·Vᵀ instead of per-pair set
 intersections), all pairs are matched in one batched ``match_pairs`` call,
-tracks are merged on the host (``merge_tracks``: the reference's connected
-components and conflict rules, densify.py:68-158, over integer feature keys
-with union-find), and all new / grown tracks are triangulated in one batched
-kernel launch.  The model is then updated in the reference's order.
+tracks are merged on the device (``merge_tracks_device``: the reference's
+connected components and conflict rules, densify.py:68-158, as a lock-free
+union-find over bank feature rows), and all new / grown tracks are triangulated
+in one batched kernel launch.  The model is then updated in the reference's order.
 """
 
 from __future__ import annotations
@@ -67,97 +67,65 @@ def candidate_pairs(model, query_images, threshold, k_limit):
     return sorted(pairs)
 
 
-def merge_tracks(q_img, q_fid, t_img, t_fid, dist, model):
-    """Connected components over feature keys seeded with the touched model
-    tracks, conflict rules of densify.py:121-157.  Returns (new_tracks,
-    extensions) as lists of (image, fid) tuples, in the reference's order."""
-    nodes = {}
-    parent = []
+def model_tracks(model, bank):
+    """(pids, CSR ptr, bank nodes) of every model point's refs inside the bank."""
+    pids = sorted(model.points)
+    ptr = np.zeros(len(pids) + 1, np.int64)
+    nodes = []
+    for r, pid in enumerate(pids):
+        for ref in model.points[pid].refs():
+            k = bank.index_of.get(int(ref.image_id))
+            if k is not None:
+                nodes.append(int(bank.offsets[k]) + int(ref.feature_id))
+        ptr[r + 1] = len(nodes)
+    return pids, ptr, np.asarray(nodes, np.int32)
 
-    def node(k):
-        j = nodes.get(k)
-        if j is None:
-            j = len(parent)
-            nodes[k] = j
-            parent.append(j)
-        return j
 
-    def find(x):
-        while parent[x] != x:
-            parent[x] = parent[parent[x]]
-            x = parent[x]
-        return x
+def merge_tracks_device(bank, u, v, dist, model, stream=None):
+    """Track merge on the device (msfm_merge_tracks, densify.py:68-158).
 
-    def union(a, b):
-        ra, rb = find(a), find(b)
-        if ra != rb:
-            parent[max(ra, rb)] = min(ra, rb)
+    ``u``, ``v`` are bank node ids (device int32), ``dist`` the f32 match
+    distances (device).  Returns (new_tracks, extensions) like the reference:
+    lists of (image << 32 | feature) keys in component order."""
+    import ctypes
 
-    edge = {}
-    adj = {}
-    for qi, qf, ti, tf, d in zip(q_img, q_fid, t_img, t_fid, dist):
-        u, v = _key(qi, qf), _key(ti, tf)
-        a, b = node(u), node(v)
-        union(a, b)
-        e = (u, v) if u < v else (v, u)
-        cur = edge.get(e)
-        if cur is None or d < cur:
-            edge[e] = float(d)
-        adj.setdefault(u, []).append(v)
-        adj.setdefault(v, []).append(u)
-    FR = _ref_type()
-    owner_of = {}
-    touched = set()
-    for k in list(nodes):
-        pid = model.owner(FR(k >> 32, k & 0xFFFFFFFF))
-        if pid is not None:
-            owner_of[k] = pid
-            touched.add(pid)
-    existing = {}
-    for pid in touched:
-        refs = [_key(r.image_id, r.feature_id) for r in model.points[pid].refs()]
-        existing[pid] = set(refs)
-        for k in refs:
-            owner_of[k] = pid
-            node(k)
-        for k in refs[1:]:
-            union(nodes[refs[0]], nodes[k])
-    comps = {}
-    for k, j in nodes.items():
-        comps.setdefault(find(j), []).append(k)
+    import torch
+
+    from . import _lib
+
+    lib = _lib.load()
+    dev = bank.device
+    pids, ptr, tnode = model_tracks(model, bank)
+    d_ptr = torch.from_numpy(ptr).to(dev)
+    d_tnode = torch.from_numpy(tnode if len(tnode) else np.zeros(1, np.int32)).to(dev)
+    E = int(u.numel())
+    cap = max(2 * E, 1)
+    out_node = torch.empty(cap, dtype=torch.int32, device=dev)
+    seg_owner = torch.empty(cap, dtype=torch.int32, device=dev)
+    seg_off = torch.empty(cap + 1, dtype=torch.int64, device=dev)
+    counts = torch.zeros(2, dtype=torch.int64, device=dev)
+    ws_bytes = lib.msfm_merge_workspace_bytes(bank.n_total, E)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    b = bank.cstruct()
+    _lib.check(lib.msfm_merge_tracks(ctypes.byref(b), E, _lib.ptr(u), _lib.ptr(v), _lib.ptr(dist),
+                                     len(pids), _lib.ptr(d_ptr), _lib.ptr(d_tnode),
+                                     _lib.ptr(out_node), _lib.ptr(seg_owner), _lib.ptr(seg_off),
+                                     _lib.ptr(counts), _lib.ptr(ws), ws_bytes,
+                                     _lib.stream_handle(stream)), "msfm_merge_tracks")
+    nseg, nout = (int(x) for x in counts.cpu().numpy())
+    nodes = out_node[:nout].cpu().numpy().astype(np.int64)
+    owners = seg_owner[:nseg].cpu().numpy()
+    offs = seg_off[:nseg + 1].cpu().numpy()
+    slot = np.searchsorted(bank.offsets, nodes, side="right") - 1
+    ids = np.asarray(bank.image_ids, np.int64)
+    keys = ((ids[slot] << 32) | (nodes - bank.offsets[slot])).tolist()
     new_tracks, extensions = [], {}
-    for comp in sorted(comps.values(), key=min):
-        comp.sort()
-        owners = {owner_of[k] for k in comp if k in owner_of}
-        if len(owners) >= 2:
-            continue        # bridges two points: ambiguous, dropped
-        owner = owners.pop() if owners else None
-        ex = existing.get(owner, set())
-
-        def support(k):
-            ds = [edge[(min(k, o), max(k, o))] for o in adj.get(k, ())]
-            return min(ds) if ds else np.inf
-
-        by_image = {}
-        for k in comp:
-            by_image.setdefault(k >> 32, []).append(k)
-        keep = []
-        for img in sorted(by_image):
-            ks = by_image[img]
-            pinned = [k for k in ks if k in ex]
-            if pinned:
-                keep.extend(pinned)
-                continue
-            if owner is not None and img in model.points[owner].track:
-                continue
-            ks.sort(key=lambda k: (support(k), k))
-            keep.append(ks[0])
-        fresh = [k for k in keep if k not in ex]
-        if owner is not None:
-            if fresh:
-                extensions.setdefault(owner, []).extend(fresh)
-        elif len(fresh) >= 2 and len({k >> 32 for k in fresh}) >= 2:
-            new_tracks.append(fresh)
+    for s in range(nseg):
+        seg = keys[offs[s]:offs[s + 1]]
+        if owners[s] < 0:
+            new_tracks.append(seg)
+        else:
+            extensions[pids[owners[s]]] = seg
     return new_tracks, extensions
 
 
@@ -193,19 +161,29 @@ def densify_stage(model, feature_store, *, iteration=1, query_images=None, d=BAN
         t_img.append(t)
         Fs.append(F if F is not None else np.full((3, 3), np.nan))
         ok.append(F is not None)
-    all_q, all_qf, all_t, all_tf, all_d = [], [], [], [], []
+    n_matches = 0
+    new_tracks, extensions = [], {}
     if pairs:
+        import torch
+
         bank = FeatureBank({i: feature_store.sets[i] for i in imgs})
         res = match_pairs(bank, q_img, t_img, np.stack(Fs), [untracked[q] for q in q_img], d=d,
                           ratio=ratio, inflation=inflation, with_stats=stats is not None)
-        pk, mq, mt, md, _ = res.to_host()
         if stats is not None:
             s = res.stats.cpu().numpy()
             stats.add(int(s[:, 0].sum()), int(s[:, 1].sum()))
-        qa, ta = np.asarray(q_img), np.asarray(t_img)
-        all_q, all_qf, all_t, all_tf, all_d = qa[pk], mq, ta[pk], mt, md.astype(np.float64)
-    n_matches = len(all_q)
-    new_tracks, extensions = merge_tracks(all_q, all_qf, all_t, all_tf, all_d, model)
+        rows, n_matches = res.packed()
+        # bank nodes of both ends of every match, on the device
+        qoff = torch.from_numpy(np.array([bank.offsets[bank.index_of[q]] for q in q_img],
+                                         np.int64)).to(bank.device)
+        toff = torch.from_numpy(np.array([bank.offsets[bank.index_of[t]] for t in t_img],
+                                         np.int64)).to(bank.device)
+        pk = rows[:, 0].long()
+        qt = rows[:, 1]
+        u = (qoff[pk] + (qt & 0xFFFF).long()).to(torch.int32).contiguous()
+        v = (toff[pk] + ((qt >> 16) & 0xFFFF).long()).to(torch.int32).contiguous()
+        dist = rows[:, 2].contiguous().view(torch.float32)
+        new_tracks, extensions = merge_tracks_device(bank, u, v, dist, model)
     # grown tracks: reference order, fresh refs against the current ownership
     ext_jobs = []
     for pid in sorted(extensions):
