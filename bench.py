@@ -47,12 +47,14 @@ def parse():
 
 # ---------------------------------------------------------------- workload --
 
-def build_workload(n_cameras):
+def build_workload(n_cameras, with_snapshot=False):
     from paper_1512_06235_b200 import scenes
 
     scene, snap = scenes.build("C3", n_cameras=n_cameras)
     wl = scenes.pair_workload(scene, snap)
     ok = np.flatnonzero(wl.valid)
+    if with_snapshot:
+        return scene, wl, ok, snap
     return scene, wl, ok
 
 
@@ -213,7 +215,7 @@ def run_b200(args, rank, world):
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
-    scene, wl, ok = build_workload(args.cameras)
+    scene, wl, ok, snap = build_workload(args.cameras, with_snapshot=True)
     mine = ok[rank::world]                     # round-robin over pair order (weak scaling)
     ql = [wl.untracked[int(wl.q_img[k])] for k in mine]
     host = HostBank(scene.feature_sets)
@@ -270,6 +272,9 @@ def run_b200(args, rank, world):
     achieved = alg / (k_ms / 1e3) / 1e9 if k_ms > 0 else 0.0
     step_ms = ms / args.steps
     tpp = ncu_traffic_per_pair()
+
+    # ---- the stage's next step on the same matches: device track merge (densify.py:68-158)
+    merge = track_merge_leg(bank, wl, mine, res, snap, dev)
 
     # ---- e2e through the public API with host buffers (pinned H2D + D2H every step)
     torch.cuda.synchronize()
@@ -331,10 +336,42 @@ def run_b200(args, rank, world):
         "gpu_launches": int(launches),
         "clocks": sampler.summary(),
         "matches_per_step": n_matches_local if world == 1 else None,
+        "track_merge": merge,
     }
     if not args.no_localize:
         line["localization"] = run_localization(args, dev)
     print(json.dumps(line), flush=True)
+
+
+def track_merge_leg(bank, wl, mine, res, snap, dev):
+    """msfm_merge_tracks over this rank's matches + the coarse tracks (bank nodes)."""
+    import torch
+
+    from paper_1512_06235_b200 import _lib
+    from paper_1512_06235_b200.densify import merge_tracks_nodes
+
+    rows, n = res.packed()
+    qoff = torch.from_numpy(bank.offsets[[bank.index_of[int(q)] for q in wl.q_img[mine]]]).to(dev)
+    toff = torch.from_numpy(bank.offsets[[bank.index_of[int(t)] for t in wl.t_img[mine]]]).to(dev)
+    pk = rows[:, 0].long()
+    u = (qoff[pk] + (rows[:, 1] & 0xFFFF).long()).to(torch.int32).contiguous()
+    v = (toff[pk] + ((rows[:, 1] >> 16) & 0xFFFF).long()).to(torch.int32).contiguous()
+    dist = rows[:, 2].contiguous().view(torch.float32)
+    slot = np.array([bank.index_of[int(i)] for i in snap.track_img], np.int64)
+    tnode = (bank.offsets[slot] + snap.track_fid).astype(np.int32)
+    for _ in range(2):
+        merge_tracks_nodes(bank, u, v, dist, snap.track_ptr, tnode)
+    torch.cuda.synchronize()
+    _lib.profile_enable(True)
+    nodes, owners, offs = merge_tracks_nodes(bank, u, v, dist, snap.track_ptr, tnode)
+    torch.cuda.synchronize()
+    ms, _ = _lib.profile_read("merge_tracks")
+    _lib.profile_enable(False)
+    return {"what": "msfm_merge_tracks (densify.py:68-158) over the step's matches + the coarse "
+                    "tracks, union-find over bank feature rows", "matches": int(n),
+            "nodes": int(bank.n_total), "tracks": int(len(snap.track_ptr) - 1), "ms": ms,
+            "edges_per_s": n / (ms / 1e3) if ms > 0 else None,
+            "new_tracks": int((owners < 0).sum()), "extended_tracks": int((owners >= 0).sum())}
 
 
 # ------------------------------------------------------- localization leg ---

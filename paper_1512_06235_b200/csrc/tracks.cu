@@ -302,6 +302,7 @@ extern "C" int msfm_merge_tracks(const msfm_bank* bank, int64_t n_edges, const i
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const int grid = nsm * 8;
+    ProfScope ps("merge_tracks", st);
     merge_init_kernel<<<grid, 256, 0, st>>>(a);
     if (n_edges > 0) merge_edges_kernel<<<grid, 256, 0, st>>>(a);
     if (n_points > 0) merge_tracks_kernel<<<(n_points + 255) / 256, 256, 0, st>>>(a);

@@ -81,12 +81,12 @@ def model_tracks(model, bank):
     return pids, ptr, np.asarray(nodes, np.int32)
 
 
-def merge_tracks_device(bank, u, v, dist, model, stream=None):
-    """Track merge on the device (msfm_merge_tracks, densify.py:68-158).
-
-    ``u``, ``v`` are bank node ids (device int32), ``dist`` the f32 match
-    distances (device).  Returns (new_tracks, extensions) like the reference:
-    lists of (image << 32 | feature) keys in component order."""
+def merge_tracks_nodes(bank, u, v, dist, track_ptr, track_node, stream=None):
+    """msfm_merge_tracks on bank nodes: ``u``, ``v`` (device int32) and ``dist``
+    (device f32) are the matches, ``track_ptr`` / ``track_node`` (host CSR) the
+    model tracks.  Returns host arrays (nodes, segment owners, segment offsets):
+    fresh nodes grouped per component in the reference's order, owner = track row
+    being extended or -1 for a new track."""
     import ctypes
 
     import torch
@@ -95,9 +95,9 @@ def merge_tracks_device(bank, u, v, dist, model, stream=None):
 
     lib = _lib.load()
     dev = bank.device
-    pids, ptr, tnode = model_tracks(model, bank)
-    d_ptr = torch.from_numpy(ptr).to(dev)
-    d_tnode = torch.from_numpy(tnode if len(tnode) else np.zeros(1, np.int32)).to(dev)
+    d_ptr = torch.from_numpy(np.ascontiguousarray(track_ptr, np.int64)).to(dev)
+    tn = np.ascontiguousarray(track_node, np.int32)
+    d_tnode = torch.from_numpy(tn if len(tn) else np.zeros(1, np.int32)).to(dev)
     E = int(u.numel())
     cap = max(2 * E, 1)
     out_node = torch.empty(cap, dtype=torch.int32, device=dev)
@@ -108,19 +108,28 @@ def merge_tracks_device(bank, u, v, dist, model, stream=None):
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
     b = bank.cstruct()
     _lib.check(lib.msfm_merge_tracks(ctypes.byref(b), E, _lib.ptr(u), _lib.ptr(v), _lib.ptr(dist),
-                                     len(pids), _lib.ptr(d_ptr), _lib.ptr(d_tnode),
+                                     len(track_ptr) - 1, _lib.ptr(d_ptr), _lib.ptr(d_tnode),
                                      _lib.ptr(out_node), _lib.ptr(seg_owner), _lib.ptr(seg_off),
                                      _lib.ptr(counts), _lib.ptr(ws), ws_bytes,
                                      _lib.stream_handle(stream)), "msfm_merge_tracks")
     nseg, nout = (int(x) for x in counts.cpu().numpy())
-    nodes = out_node[:nout].cpu().numpy().astype(np.int64)
-    owners = seg_owner[:nseg].cpu().numpy()
-    offs = seg_off[:nseg + 1].cpu().numpy()
+    return (out_node[:nout].cpu().numpy().astype(np.int64), seg_owner[:nseg].cpu().numpy(),
+            seg_off[:nseg + 1].cpu().numpy())
+
+
+def merge_tracks_device(bank, u, v, dist, model, stream=None):
+    """Track merge on the device (msfm_merge_tracks, densify.py:68-158).
+
+    ``u``, ``v`` are bank node ids (device int32), ``dist`` the f32 match
+    distances (device).  Returns (new_tracks, extensions) like the reference:
+    lists of (image << 32 | feature) keys in component order."""
+    pids, ptr, tnode = model_tracks(model, bank)
+    nodes, owners, offs = merge_tracks_nodes(bank, u, v, dist, ptr, tnode, stream)
     slot = np.searchsorted(bank.offsets, nodes, side="right") - 1
     ids = np.asarray(bank.image_ids, np.int64)
     keys = ((ids[slot] << 32) | (nodes - bank.offsets[slot])).tolist()
     new_tracks, extensions = [], {}
-    for s in range(nseg):
+    for s in range(len(owners)):
         seg = keys[offs[s]:offs[s + 1]]
         if owners[s] < 0:
             new_tracks.append(seg)
