@@ -259,6 +259,27 @@ int msfm_triangulate_batch(const double* d_K, const double* d_R, const double* d
                            double* d_X, double* d_err, int32_t* d_status, void* stream);
 
 /* ------------------------------------------------------------------------
+ * Two-view geometry of the coarse match graph: estimate_fundamental_ransac
+ * (geometry.py:153-198) batched over image pairs.  Pair p's correspondences
+ * are rows [off[p], off[p+1]) of d_q (query pixels) and d_c (target pixels),
+ * f64 [..][2].  msfm_fundamental_hypotheses fits the normalized 8-point F of
+ * n_hyp host-supplied samples per pair (d_samples [p][h][8], pair-local rows;
+ * msfm_ransac_samples with sample_size 8) into d_F [p][h][9] and counts the
+ * Sampson inliers (< threshold) into d_count [p][h] (-1: non-finite fit).
+ * The caller replays the adaptive stop (geometry.py:176-191, w**8) and passes
+ * the winner to msfm_fundamental_refit, which refits on its inliers (pairs
+ * with d_status[p] != 0) and writes F, the final inlier mask (d_mask, per row),
+ * the inlier count and the design-matrix gap s[-2]/s[0] (0 below 9 rows).
+ * ---------------------------------------------------------------------- */
+int msfm_fundamental_hypotheses(const double* d_q, const double* d_c, const int64_t* d_off,
+                                int32_t n_pairs, const int32_t* d_samples, int32_t n_hyp,
+                                double threshold, double* d_F, int32_t* d_count, void* stream);
+int msfm_fundamental_refit(const double* d_q, const double* d_c, const int64_t* d_off,
+                           int32_t n_pairs, const double* d_F_best, const int32_t* d_status,
+                           double threshold, double* d_F, uint8_t* d_mask, int32_t* d_count,
+                           double* d_gap, void* stream);
+
+/* ------------------------------------------------------------------------
  * Track merge of densify_stage (densify.py:68-158): connected components over
  * one stage's matches plus the model tracks, with the reference's conflict
  * rules (two owning points: dropped; an image holding an owner ref keeps the

@@ -34,10 +34,10 @@ class PnpResult:
     iterations: int = 0
 
 
-def _replay(counts, evaluated, n, max_iters, confidence):
-    """The reference's while-loop over hypothesis outcomes (reconstruct.py:190-211).
-    Returns (best_h, best_count, it, needed); stops early when it runs past the
-    evaluated hypotheses."""
+def _replay(counts, evaluated, n, max_iters, confidence, power=6):
+    """The reference's while-loop over hypothesis outcomes (reconstruct.py:190-211;
+    geometry.py:176-191 with power 8).  Returns (best_h, best_count, it, needed,
+    complete); stops early when it runs past the evaluated hypotheses."""
     best_count, best_h, needed, it = 0, -1, max_iters, 0
     while it < needed and it < max_iters:
         if it >= evaluated:
@@ -52,7 +52,7 @@ def _replay(counts, evaluated, n, max_iters, confidence):
             w = c / n
             if w > 0:
                 with np.errstate(divide="ignore"):
-                    denom = np.log(max(1.0 - w ** 6, 1e-15))
+                    denom = np.log(max(1.0 - w ** power, 1e-15))
                     needed = min(max_iters, int(np.ceil(np.log(1.0 - confidence) / denom)))
     return best_h, best_count, it, needed, True
 
