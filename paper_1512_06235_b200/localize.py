@@ -60,6 +60,18 @@ class DeviceKnn:
     M_pad: int
     keep: tuple = field(default=())
 
+    def host_all(self, pts: PointSet):
+        """(idx, N_best, N_second) of every query slot: (S, M) arrays, three copies."""
+        M = len(pts.n)
+        k1 = self.k1[:, :M].cpu().numpy().astype(np.int64)
+        i1 = self.i1[:, :M].cpu().numpy().astype(np.int64)
+        k2 = self.k2[:, :M].cpu().numpy().astype(np.int64)
+        n = pts.n.astype(np.int64)[None, :]
+        SS = pts.SS[None, :]
+        Nb = n * k1 + SS
+        Ns = np.where(k2 == INT_BIG, -1, n * k2 + SS)
+        return i1, Nb, Ns
+
     def host(self, pts: PointSet, s: int):
         """(idx, N_best, N_second) of query slot s, N_second=-1 if undefined."""
         M = len(pts.n)
@@ -74,7 +86,9 @@ class DeviceKnn:
 
 
 def knn2_tracks(bank: FeatureBank, pts: PointSet, image_ids, stream=None,
-                device_points=None) -> DeviceKnn:
+                device_points=None, counts=None) -> DeviceKnn:
+    """Top-2 over each image's features; ``counts`` (per bank image, optional)
+    restricts image k to its first counts[k] features (a coarse tier)."""
     import torch
 
     lib = _lib.load()
@@ -89,16 +103,21 @@ def knn2_tracks(bank: FeatureBank, pts: PointSet, image_ids, stream=None,
     k1 = torch.empty((max(len(slots), 1), M_pad), dtype=torch.int32, device=dev)
     i1 = torch.empty_like(k1)
     k2 = torch.empty_like(k1)
-    max_feat = int(bank.counts[slots].max()) if len(slots) else 0
+    cnt = bank.counts if counts is None else np.asarray(counts, np.int64)
+    max_feat = int(cnt[slots].max()) if len(slots) else 0
     ws_bytes = lib.msfm_knn_workspace_bytes(M, len(slots), max_feat)
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
     b = bank.cstruct()
+    d_cnt = None
+    if counts is not None:
+        d_cnt = torch.from_numpy(cnt.astype(np.int32)).to(dev)
+        b.d_img_n = _lib.ptr(d_cnt)
     maxn = int(pts.n.max()) if M else 0
     _lib.check(lib.msfm_knn2_tracks(ctypes.byref(b), M, _lib.ptr(dS), _lib.ptr(dn), len(slots),
                                     _lib.ptr(d_slots), maxn, max_feat, _lib.ptr(k1), _lib.ptr(i1),
                                     _lib.ptr(k2), _lib.ptr(ws), ws_bytes,
                                     _lib.stream_handle(stream)), "msfm_knn2_tracks")
-    return DeviceKnn(k1, i1, k2, M_pad, keep=(ws, d_slots))
+    return DeviceKnn(k1, i1, k2, M_pad, keep=(ws, d_slots, d_cnt))
 
 
 def upload_points(pts: PointSet, dev):

@@ -291,6 +291,44 @@ class TwoViewGeometry:
     degenerate_planar: bool = False
 
 
+@dataclass
+class Edge:
+    """matching.py:46-56"""
+    matches: list
+    geometry: TwoViewGeometry | None = None
+    inlier_mask: np.ndarray | None = None
+
+    def inlier_matches(self) -> list:
+        if self.inlier_mask is None:
+            return list(self.matches)
+        return [m for m, keep in zip(self.matches, self.inlier_mask) if keep]
+
+
+@dataclass
+class MatchGraph:
+    """matching.py:59-79"""
+    edges: dict = field(default_factory=dict)
+
+    def pair_key(self, a: int, b: int):
+        return (a, b) if a < b else (b, a)
+
+    def get(self, a: int, b: int):
+        return self.edges.get(self.pair_key(a, b))
+
+    def neighbors(self, image_id: int) -> list:
+        out = []
+        for a, b in self.edges:
+            if a == image_id:
+                out.append(b)
+            elif b == image_id:
+                out.append(a)
+        return sorted(out)
+
+    def match_count(self, a: int, b: int) -> int:
+        edge = self.get(a, b)
+        return len(edge.matches) if edge else 0
+
+
 @dataclass(frozen=True)
 class EpipolarLine:
     a: float
