@@ -340,7 +340,39 @@ def run_b200(args, rank, world):
     }
     if not args.no_localize:
         line["localization"] = run_localization(args, dev)
+        line["coarse_graph"] = coarse_graph_leg(dev)
     print(json.dumps(line), flush=True)
+
+
+def coarse_graph_leg(dev, n_cameras=40):
+    """build_coarse_matchgraph (matching.py:208-249) on the C2 recipe's first
+    n_cameras images at eta = 20 tiers: all pairs, hybrid matching on the tcgen05
+    kNN, batched device F-RANSAC.  Wall clock (host orchestration included)."""
+    import torch
+
+    from paper_1512_06235_b200 import _lib, scenes
+    from paper_1512_06235_b200.coarse import build_coarse_matchgraph
+
+    scene, _ = scenes.build("C2", n_cameras=n_cameras)
+    store = scene.store()
+    store.apply_eta(20.0)
+    build_coarse_matchgraph(store.sets, on_overflow="drop")
+    torch.cuda.synchronize()
+    _lib.profile_enable(True)
+    t0 = time.perf_counter()
+    g = build_coarse_matchgraph(store.sets, on_overflow="drop")
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    kern = {k: _lib.profile_read(k)[0] for k in ("knn_tc_kernel", "f_hyp_kernel",
+                                                  "f_score_kernel", "f_refit_kernel")}
+    _lib.profile_enable(False)
+    P = n_cameras * (n_cameras - 1) // 2
+    return {"metric": "coarse match-graph pairs/sec", "value": P / dt, "unit": "pairs/s",
+            "workload": f"C2 recipe, {n_cameras} cameras, eta=20 tiers "
+                        f"(~{int(np.mean([fs.coarse_count for fs in store.sets.values()]))} "
+                        "features), all pairs",
+            "pairs": P, "edges": len(g.edges), "overflow_pairs_dropped": len(g.overflow_pairs),
+            "wall_ms": dt * 1e3, "kernel_ms": kern}
 
 
 def track_merge_leg(bank, wl, mine, res, snap, dev):

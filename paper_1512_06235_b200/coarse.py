@@ -109,11 +109,6 @@ def _matches(types, qid, tid, rows, tgts, d, r, qmap=None, tmap=None):
             for a, b, c, e in zip(qm, tm, d, r)]
 
 
-def _bank_for(feature_sets):
-    key = tuple(sorted((i, id(fs)) for i, fs in feature_sets.items()))
-    return key, FeatureBank(feature_sets)
-
-
 def match_pair(query_fs, target_fs, *, ratio=RATIO_UNGUIDED, query_indices=None,
                target_indices=None, single_cap=SINGLE_CANDIDATE_CAP, index=None, stats=None):
     """Drop-in for msfm.matching.match_pair (matching.py:116-140), exact index."""
@@ -183,10 +178,16 @@ def preemptive_pair_filter(feature_sets, *, n_top=PREEMPTIVE_TOP,
 
 def build_coarse_matchgraph(feature_sets, *, ratio=RATIO_UNGUIDED, preemptive=False,
                             min_edge_matches=MIN_EDGE_MATCHES, min_edge_inliers=MIN_EDGE_INLIERS,
-                            early_stop=HYBRID_EARLY_STOP, seed=0, threads=1, stats=None):
+                            early_stop=HYBRID_EARLY_STOP, seed=0, threads=1, stats=None,
+                            on_overflow="raise"):
     """Drop-in for msfm.matching.build_coarse_matchgraph (matching.py:208-249):
     one kNN launch per query image over all its candidate partners, the hybrid
-    schedule per pair, then one batched device RANSAC over every surviving pair."""
+    schedule per pair, then one batched device RANSAC over every surviving pair.
+
+    A pair whose RANSAC hits the reference's OverflowError (geometry.py:189, a
+    best inlier fraction below ~1%) raises it, as the reference does;
+    ``on_overflow="drop"`` (not the reference's behaviour) drops such pairs and
+    counts them in ``graph.overflow_pairs`` instead."""
     FR, M, E, MG, G = _ref_types()
     ids = sorted(feature_sets)
     if preemptive:
@@ -225,8 +226,12 @@ def build_coarse_matchgraph(feature_sets, *, ratio=RATIO_UNGUIDED, preemptive=Fa
         seeds.append(seed + a * 100003 + b)
     geo = fransac_batch(q_list, c_list, seeds) if cand else []
     graph = MG()
+    dropped = []
     for (a, b), g in zip(cand, geo):
         if g.status == "overflow":
+            if on_overflow == "drop":
+                dropped.append((a, b))
+                continue
             raise OverflowError("cannot convert float infinity to integer")   # geometry.py:189
         if int(g.mask.sum()) < min_edge_inliers:
             continue
@@ -235,4 +240,6 @@ def build_coarse_matchgraph(feature_sets, *, ratio=RATIO_UNGUIDED, preemptive=Fa
               for x, y, c, e in zip(rows, tg, dd, rr)]
         geom = G(F=g.F, inlier_count=g.inlier_count, degenerate_planar=g.degenerate_planar)
         graph.edges[(a, b)] = E(matches=ms, geometry=geom, inlier_mask=g.mask)
+    if on_overflow == "drop":
+        graph.overflow_pairs = dropped
     return graph
