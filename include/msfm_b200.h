@@ -293,6 +293,12 @@ int msfm_fundamental_refit(const double* d_q, const double* d_c, const int64_t* 
  * row extended, -1 = new track) and d_seg_off [n_seg+1]; d_counts = {n_seg, n_out}.
  * ---------------------------------------------------------------------- */
 size_t msfm_merge_workspace_bytes(int64_t n_nodes, int64_t n_edges);
+/* Covisibility of all image pairs (len(model.covisible_points(a, b)),
+ * model.py:105-110, used by candidate_images densify.py:37-56): d_counts
+ * [n_images][n_images] int32 (zeroed here) counts the points whose track
+ * (d_track_img [track_ptr[p] .. track_ptr[p+1]), image slots) holds both. */
+int msfm_covisibility(int32_t n_points, const int64_t* d_track_ptr, const int32_t* d_track_img,
+                      int32_t n_images, int32_t* d_counts, void* stream);
 int msfm_merge_tracks(const msfm_bank* bank, int64_t n_edges, const int32_t* d_u,
                       const int32_t* d_v, const float* d_dist, int32_t n_points,
                       const int64_t* d_track_ptr, const int32_t* d_track_node,

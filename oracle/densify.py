@@ -118,3 +118,22 @@ def merge_tracks(q_img, q_fid, t_img, t_fid, dist, model):
     return new_tracks, extensions
 
 
+
+
+def covisibility_counts(model, ids):
+    """Host restatement (checker): len(model.covisible_points(a, b)), model.py:105-110."""
+    pos = {i: k for k, i in enumerate(ids)}
+    rows, cols = [], []
+    for pid, pt in model.points.items():
+        for i in pt.track:
+            if i in pos:
+                rows.append(pos[i])
+                cols.append(pid)
+    if not rows:
+        return np.zeros((len(ids), len(ids)), np.int64)
+    pids = np.unique(cols)
+    V = np.zeros((len(ids), len(pids)), np.float32)
+    V[np.array(rows), np.searchsorted(pids, np.array(cols))] = 1.0
+    return (V @ V.T).astype(np.int64)
+
+

@@ -69,6 +69,7 @@ _SIGS = {
                                                    ctypes.c_double, VP, VP, VP]),
     "msfm_fundamental_refit": (ctypes.c_int, [VP, VP, VP, ctypes.c_int32, VP, VP, ctypes.c_double,
                                               VP, VP, VP, VP, VP]),
+"msfm_covisibility": (ctypes.c_int, [ctypes.c_int32, VP, VP, ctypes.c_int32, VP, VP]),
     "msfm_merge_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int64]),
     "msfm_merge_tracks": (ctypes.c_int, [ctypes.POINTER(Bank), ctypes.c_int64, VP, VP, VP,
                                          ctypes.c_int32, VP, VP, VP, VP, VP, VP, VP,

@@ -241,6 +241,23 @@ __global__ void merge_sort_kernel(MergeArgs a) {
     }
 }
 
+// covisibility counts (model.py:105-110 for every image pair): one thread per
+// point adds 1 to C[a][b] for every ordered pair of distinct images on its track
+__global__ void covis_kernel(int32_t n_points, const int64_t* __restrict__ ptr,
+                            const int32_t* __restrict__ img, int32_t n_images,
+                            int32_t* __restrict__ C) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n_points) return;
+    const int64_t b = ptr[p], e = ptr[p + 1];
+    for (int64_t i = b; i < e; i++)
+        for (int64_t j = i + 1; j < e; j++) {
+            const int x = img[i], y = img[j];
+            if (x == y) continue;
+            atomicAdd(C + (int64_t)x * n_images + y, 1);
+            atomicAdd(C + (int64_t)y * n_images + x, 1);
+        }
+}
+
 int64_t hash_size(int64_t n_edges) {
     int64_t h = 1024;
     while (h < 4 * n_edges) h <<= 1;
@@ -251,6 +268,25 @@ int64_t hash_size(int64_t n_edges) {
 }  // namespace msfm
 
 using namespace msfm;
+
+extern "C" int msfm_covisibility(int32_t n_points, const int64_t* d_track_ptr,
+                                 const int32_t* d_track_img, int32_t n_images, int32_t* d_counts,
+                                 void* stream) {
+    if (n_points < 0 || n_images < 0 || (n_points > 0 && (!d_track_ptr || !d_track_img)) ||
+        (n_images > 0 && !d_counts)) {
+        set_error("msfm_covisibility: bad arguments");
+        return MSFM_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_images == 0) return MSFM_OK;
+    MSFM_CUDA_TRY(cudaMemsetAsync(d_counts, 0, sizeof(int32_t) * (size_t)n_images * n_images, st));
+    if (n_points == 0) return MSFM_OK;
+    covis_kernel<<<(n_points + 255) / 256, 256, 0, st>>>(n_points, d_track_ptr, d_track_img,
+                                                         n_images, d_counts);
+    MSFM_LAUNCH_CHECK();
+    count_launches(1);
+    return MSFM_OK;
+}
 
 extern "C" size_t msfm_merge_workspace_bytes(int64_t n_nodes, int64_t n_edges) {
     const int64_t n = n_nodes > 0 ? n_nodes : 1;

@@ -35,21 +35,31 @@ def _ref_type():
         return FeatureRef
 
 
-def covisibility_counts(model, ids):
-    """len(model.covisible_points(a, b)) for all registered pairs (model.py:105-110)."""
+def covisibility_counts(model, ids, device=None):
+    """len(model.covisible_points(a, b)) for all registered pairs (model.py:105-110),
+    counted on the device (msfm_covisibility): int64 (N, N), N = len(ids)."""
+    import torch
+
+    from . import _lib
+
+    lib = _lib.load()
+    dev = torch.device(device or "cuda")
     pos = {i: k for k, i in enumerate(ids)}
-    rows, cols = [], []
-    for pid, pt in model.points.items():
-        for i in pt.track:
-            if i in pos:
-                rows.append(pos[i])
-                cols.append(pid)
-    if not rows:
-        return np.zeros((len(ids), len(ids)), np.int64)
-    pids = np.unique(cols)
-    V = np.zeros((len(ids), len(pids)), np.float32)
-    V[np.array(rows), np.searchsorted(pids, np.array(cols))] = 1.0
-    return (V @ V.T).astype(np.int64)
+    ptr = [0]
+    img = []
+    for pid in sorted(model.points):
+        for i in model.points[pid].track:
+            k = pos.get(i)
+            if k is not None:
+                img.append(k)
+        ptr.append(len(img))
+    N = len(ids)
+    d_ptr = torch.tensor(ptr, dtype=torch.int64, device=dev)
+    d_img = torch.tensor(img if img else [0], dtype=torch.int32, device=dev)
+    C = torch.empty((max(N, 1), max(N, 1)), dtype=torch.int32, device=dev)
+    _lib.check(lib.msfm_covisibility(len(ptr) - 1, _lib.ptr(d_ptr), _lib.ptr(d_img), N,
+                                     _lib.ptr(C), _lib.stream_handle(None)), "msfm_covisibility")
+    return C[:N, :N].cpu().numpy().astype(np.int64)
 
 
 def candidate_pairs(model, query_images, threshold, k_limit):

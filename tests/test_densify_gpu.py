@@ -89,3 +89,21 @@ def test_device_track_merge_equals_host_restatement(seed):
     assert got_new == [sorted(t) for t in want_new]
     assert {k: sorted(v) for k, v in got_ext.items()} == {k: sorted(v) for k, v in want_ext.items()}
     assert list(got_ext) == list(want_ext)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_device_covisibility_equals_host(seed):
+    """msfm_covisibility == len(model.covisible_points(a, b)) for every pair."""
+    from oracle.densify import covisibility_counts as host_counts
+    from paper_1512_06235_b200.densify import covisibility_counts
+
+    _, model, _ = _random_merge_case(seed, n_img=[3, 8, 20, 2][seed], n_points=[5, 60, 300, 0][seed])
+    ids = model.image_ids()
+    got = covisibility_counts(model, ids)
+    want = host_counts(model, ids)
+    off = ~np.eye(len(ids), dtype=bool)          # the diagonal is not a pair
+    np.testing.assert_array_equal(got[off], want[off])
+    for a in ids[:5]:
+        for b in ids[:5]:
+            if a != b:
+                assert got[ids.index(a), ids.index(b)] == len(model.covisible_points(a, b))
