@@ -211,7 +211,7 @@ def run_b200(args, rank, world):
 
     from paper_1512_06235_b200 import _lib
     from paper_1512_06235_b200.bank import FeatureBank, HostBank
-    from paper_1512_06235_b200.guided import match_pairs, prepare_pairs
+    from paper_1512_06235_b200.guided import match_pairs, match_pairs_rows, prepare_pairs
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
@@ -289,15 +289,16 @@ def run_b200(args, rank, world):
         b2 = FeatureBank(host=host, device=dev)
         b2.grid(D)
         inp = prepare_pairs(b2, wl.q_img[mine], wl.t_img[mine], wl.F[mine], ql)
-        r2 = match_pairs(b2, wl.q_img[mine], wl.t_img[mine], wl.F[mine], ql, device_inputs=inp,
-                         chunk_pairs=args.chunk_pairs)
-        rows = r2.rows_host(pinned)
+        # matching with each chunk's packed rows copied to pinned memory while the
+        # next chunk computes (msfm_guided_match_rows)
+        rows = match_pairs_rows(b2, wl.q_img[mine], wl.t_img[mine], wl.F[mine], ql,
+                                device_inputs=inp, chunk_pairs=args.chunk_pairs, pinned=pinned)
         a1.record()
         torch.cuda.synchronize()
         if i >= args.warmup:
             e2e_ms.append(a0.elapsed_time(a1))
         h2d = host.nbytes + sum(int(x.numel() * x.element_size()) for x in inp[:5] + inp[6:])
-        d2h = int(rows.nbytes + 8)   # packed 16-B rows + the row total
+        d2h = int(rows.nbytes + 16 * 6)   # packed 16-B rows + per-chunk (base, count)
     te = torch.tensor([float(np.mean(e2e_ms))], device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)

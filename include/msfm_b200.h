@@ -172,6 +172,23 @@ int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids, int32_t n_
                       int32_t* d_out_count, int64_t* d_stats,
                       void* d_workspace, size_t workspace_bytes, void* stream);
 
+/* msfm_guided_match followed by the packing of msfm_pack_matches, pipelined with
+ * the device-to-host copy: after every internal chunk its packed rows are copied
+ * on `copy_stream` into the pinned host buffer h_rows (16-B rows, pair order)
+ * while the next chunk computes.  Scratch: d_out_off [n_pairs+1], d_rows
+ * (4 * total queries int32), d_meta / h_meta (pinned) [2 * (n_pairs + 1)] int64.
+ * Returns after the last copy; *h_total = rows written.  No SearchStats. */
+int msfm_guided_match_rows(const msfm_bank* bank, const msfm_grids* grids, int32_t n_pairs,
+                           const int32_t* d_pair_q, const int32_t* d_pair_t,
+                           const double* d_pair_F, const int64_t* d_qlist_off,
+                           const int32_t* d_qlist, const int64_t* d_qlist_src,
+                           const int64_t* h_qlist_off, const msfm_match_params* prm,
+                           int32_t* d_out_q, int32_t* d_out_t, float* d_out_dist,
+                           float* d_out_ratio, int32_t* d_out_count, int64_t* d_out_off,
+                           int32_t* d_rows, int64_t* d_meta, int64_t* h_meta, int32_t* h_rows,
+                           int64_t* h_total, void* d_workspace, size_t workspace_bytes,
+                           void* stream, void* copy_stream);
+
 /* ------------------------------------------------------------------------
  * Host-only: RANSAC hypothesis sets.  Emits `count` consecutive draws of
  * numpy's `rng.choice(n, size=sample_size, replace=False)` starting from the

@@ -77,6 +77,10 @@ _SIGS = {
     "msfm_pack_matches": (ctypes.c_int, [ctypes.c_int32, VP, VP, VP, VP, VP, VP, VP, VP, VP]),
     "msfm_guided_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int32, VP,
                                                       ctypes.POINTER(MatchParams)]),
+    "msfm_guided_match_rows": (ctypes.c_int, [ctypes.POINTER(Bank), ctypes.POINTER(Grids),
+                                              ctypes.c_int32, VP, VP, VP, VP, VP, VP, VP,
+                                              ctypes.POINTER(MatchParams), VP, VP, VP, VP, VP,
+                                              VP, VP, VP, VP, VP, VP, VP, ctypes.c_size_t, VP, VP]),
     "msfm_guided_match": (ctypes.c_int, [ctypes.POINTER(Bank), ctypes.POINTER(Grids),
                                          ctypes.c_int32, VP, VP, VP, VP, VP, VP, VP,
                                          ctypes.POINTER(MatchParams), VP, VP, VP, VP, VP, VP,

@@ -1481,11 +1481,29 @@ __global__ void pack_scan_kernel(const int32_t* __restrict__ count, int n_pairs,
     if (threadIdx.x == 0) out_off[n_pairs] = carry;
 }
 
+// chunk c of a pipelined packing: pairs [p0, p0 + np); meta[2c] = first row of the
+// chunk (after chunk c-1), meta[2c+1] = rows in the chunk
+__global__ void pack_chunk_scan_kernel(const int32_t* __restrict__ count, int p0, int np, int c,
+                                       int64_t* __restrict__ out_off, int64_t* __restrict__ meta) {
+    __shared__ int sm[SCAN_T / 32 + 1];
+    const long long base = c > 0 ? meta[2 * (c - 1)] + meta[2 * (c - 1) + 1] : 0;
+    long long carry = 0;
+    for (int b0 = 0; b0 < np; b0 += SCAN_T) {
+        const int k = b0 + threadIdx.x;
+        const int v = k < np ? count[p0 + k] : 0;
+        int tot;
+        const int ex = block_exclusive_scan<SCAN_T>(v, &tot, sm);
+        if (k < np) out_off[p0 + k] = base + carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) { meta[2 * c] = base; meta[2 * c + 1] = carry; }
+}
+
 __global__ void pack_kernel(const int64_t* __restrict__ qlist_off, const int32_t* __restrict__ count,
                             const int64_t* __restrict__ out_off, const int32_t* __restrict__ q,
                             const int32_t* __restrict__ t, const float* __restrict__ dist,
-                            const float* __restrict__ ratio, int4* __restrict__ rows) {
-    const int p = blockIdx.x;
+                            const float* __restrict__ ratio, int4* __restrict__ rows, int p0 = 0) {
+    const int p = p0 + blockIdx.x;
     const int64_t src = qlist_off[p], dst = out_off[p];
     const int c = count[p];
     for (int i = threadIdx.x; i < c; i += blockDim.x)
@@ -1668,15 +1686,18 @@ extern "C" size_t msfm_guided_workspace_bytes(int32_t n_pairs, const int64_t* h_
     return chunk_bytes(w);
 }
 
-extern "C" int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids, int32_t n_pairs,
-                                 const int32_t* d_pair_q, const int32_t* d_pair_t,
-                                 const double* d_pair_F, const int64_t* d_qlist_off,
-                                 const int32_t* d_qlist, const int64_t* d_qlist_src,
-                                 const int64_t* h_qlist_off,
-                                 const msfm_match_params* prm, int32_t* d_out_q, int32_t* d_out_t,
-                                 float* d_out_dist, float* d_out_ratio, int32_t* d_out_count,
-                                 int64_t* d_stats, void* d_workspace, size_t workspace_bytes,
-                                 void* stream) {
+// after each chunk: hook(chunk index, first pair, end pair) -> status
+typedef int (*ChunkHookFn)(void* ctx, int c, int p0, int p1);
+
+static int guided_match_impl(const msfm_bank* bank, const msfm_grids* grids, int32_t n_pairs,
+                             const int32_t* d_pair_q, const int32_t* d_pair_t,
+                             const double* d_pair_F, const int64_t* d_qlist_off,
+                             const int32_t* d_qlist, const int64_t* d_qlist_src,
+                             const int64_t* h_qlist_off,
+                             const msfm_match_params* prm, int32_t* d_out_q, int32_t* d_out_t,
+                             float* d_out_dist, float* d_out_ratio, int32_t* d_out_count,
+                             int64_t* d_stats, void* d_workspace, size_t workspace_bytes,
+                             void* stream, ChunkHookFn hook, void* hook_ctx) {
     if (!bank || !grids || !prm || n_pairs < 0 || !h_qlist_off) {
         set_error("msfm_guided_match: null argument");
         return MSFM_EINVAL;
@@ -1795,6 +1816,111 @@ extern "C" int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids,
         { ProfScope ps("compact_kernel", st); compact_kernel<<<a.npairs, 256, 0, st>>>(a); }
         MSFM_LAUNCH_CHECK();
         count_launches(7 + (Q > 0 ? 4 : 0));
+        if (hook) {
+            const int rc = hook(hook_ctx, (int)c, p0, p1);
+            if (rc) return rc;
+        }
     }
     return MSFM_OK;
+}
+
+extern "C" int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids, int32_t n_pairs,
+                                 const int32_t* d_pair_q, const int32_t* d_pair_t,
+                                 const double* d_pair_F, const int64_t* d_qlist_off,
+                                 const int32_t* d_qlist, const int64_t* d_qlist_src,
+                                 const int64_t* h_qlist_off,
+                                 const msfm_match_params* prm, int32_t* d_out_q, int32_t* d_out_t,
+                                 float* d_out_dist, float* d_out_ratio, int32_t* d_out_count,
+                                 int64_t* d_stats, void* d_workspace, size_t workspace_bytes,
+                                 void* stream) {
+    return guided_match_impl(bank, grids, n_pairs, d_pair_q, d_pair_t, d_pair_F, d_qlist_off,
+                             d_qlist, d_qlist_src, h_qlist_off, prm, d_out_q, d_out_t, d_out_dist,
+                             d_out_ratio, d_out_count, d_stats, d_workspace, workspace_bytes,
+                             stream, nullptr, nullptr);
+}
+
+namespace {
+// pipelined packing + device-to-host copy of every finished chunk
+struct RowsCtx {
+    cudaStream_t st, copy;
+    const int64_t* qlist_off; const int32_t* count;
+    const int32_t* q; const int32_t* t; const float* dist; const float* ratio;
+    int64_t* out_off; int32_t* d_rows; int32_t* h_rows;
+    int64_t* d_meta; int64_t* h_meta;
+    std::vector<cudaEvent_t> ev;
+    int flushed;
+};
+
+int rows_flush(RowsCtx& x, int c) {
+    MSFM_CUDA_TRY(cudaEventSynchronize(x.ev[c]));
+    const int64_t base = x.h_meta[2 * c], tot = x.h_meta[2 * c + 1];
+    if (tot > 0) {
+        MSFM_CUDA_TRY(cudaStreamWaitEvent(x.copy, x.ev[c], 0));
+        MSFM_CUDA_TRY(cudaMemcpyAsync(x.h_rows + 4 * base, x.d_rows + 4 * base,
+                                      (size_t)tot * 16, cudaMemcpyDeviceToHost, x.copy));
+    }
+    x.flushed = c + 1;
+    return MSFM_OK;
+}
+
+int rows_hook(void* ctx, int c, int p0, int p1) {
+    RowsCtx& x = *static_cast<RowsCtx*>(ctx);
+    const int np = p1 - p0;
+    pack_chunk_scan_kernel<<<1, SCAN_T, 0, x.st>>>(x.count, p0, np, c, x.out_off, x.d_meta);
+    pack_kernel<<<np, 128, 0, x.st>>>(x.qlist_off, x.count, x.out_off, x.q, x.t, x.dist, x.ratio,
+                                      reinterpret_cast<int4*>(x.d_rows), p0);
+    MSFM_LAUNCH_CHECK();
+    count_launches(2);
+    MSFM_CUDA_TRY(cudaMemcpyAsync(x.h_meta + 2 * c, x.d_meta + 2 * c, 2 * sizeof(int64_t),
+                                  cudaMemcpyDeviceToHost, x.st));
+    cudaEvent_t e;
+    MSFM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    MSFM_CUDA_TRY(cudaEventRecord(e, x.st));
+    x.ev.push_back(e);
+    // the previous chunk's rows go out while this chunk computes
+    if (c > 0) return rows_flush(x, c - 1);
+    return MSFM_OK;
+}
+}  // namespace
+
+extern "C" int msfm_guided_match_rows(const msfm_bank* bank, const msfm_grids* grids,
+                                      int32_t n_pairs, const int32_t* d_pair_q,
+                                      const int32_t* d_pair_t, const double* d_pair_F,
+                                      const int64_t* d_qlist_off, const int32_t* d_qlist,
+                                      const int64_t* d_qlist_src, const int64_t* h_qlist_off,
+                                      const msfm_match_params* prm, int32_t* d_out_q,
+                                      int32_t* d_out_t, float* d_out_dist, float* d_out_ratio,
+                                      int32_t* d_out_count, int64_t* d_out_off, int32_t* d_rows,
+                                      int64_t* d_meta, int64_t* h_meta, int32_t* h_rows,
+                                      int64_t* h_total, void* d_workspace,
+                                      size_t workspace_bytes, void* stream, void* copy_stream) {
+    if (!d_out_off || !d_rows || !d_meta || !h_meta || !h_rows || !h_total || !copy_stream) {
+        set_error("msfm_guided_match_rows: null argument");
+        return MSFM_EINVAL;
+    }
+    *h_total = 0;
+    RowsCtx x;
+    x.st = (cudaStream_t)stream; x.copy = (cudaStream_t)copy_stream;
+    x.qlist_off = d_qlist_off; x.count = d_out_count;
+    x.q = d_out_q; x.t = d_out_t; x.dist = d_out_dist; x.ratio = d_out_ratio;
+    x.out_off = d_out_off; x.d_rows = d_rows; x.h_rows = h_rows;
+    x.d_meta = d_meta; x.h_meta = h_meta; x.flushed = 0;
+    int rc = guided_match_impl(bank, grids, n_pairs, d_pair_q, d_pair_t, d_pair_F, d_qlist_off,
+                               d_qlist, d_qlist_src, h_qlist_off, prm, d_out_q, d_out_t,
+                               d_out_dist, d_out_ratio, d_out_count, nullptr, d_workspace,
+                               workspace_bytes, stream, rows_hook, &x);
+    if (rc == MSFM_OK && !x.ev.empty()) rc = rows_flush(x, (int)x.ev.size() - 1);
+    if (rc == MSFM_OK) {
+        cudaError_t e = cudaStreamSynchronize(x.copy);
+        if (e != cudaSuccess) {
+            set_error("msfm_guided_match_rows: %s", cudaGetErrorString(e));
+            rc = MSFM_ECUDA;
+        }
+    }
+    if (rc == MSFM_OK && !x.ev.empty()) {
+        const int last = (int)x.ev.size() - 1;
+        *h_total = h_meta[2 * last] + h_meta[2 * last + 1];
+    }
+    for (cudaEvent_t e : x.ev) cudaEventDestroy(e);
+    return rc;
 }

@@ -135,6 +135,66 @@ def match_pairs(bank: FeatureBank, q_img, t_img, F, query_lists, *, d: float = B
     return res
 
 
+def match_pairs_rows(bank: FeatureBank, q_img, t_img, F, query_lists, *, d: float = BAND_D_PX,
+                     ratio: float = RATIO_GUIDED, inflation: float = GRID_INFLATION,
+                     grid_d: float | None = None, single_cap: float = SINGLE_CANDIDATE_CAP,
+                     chunk_pairs: int = 0, stream=None, device_inputs=None,
+                     strategy: str = "grid", pinned=None):
+    """``match_pairs`` + packing + one pinned host copy per internal chunk, the
+    copy of chunk c overlapping the compute of chunk c+1 (msfm_guided_match_rows).
+    Returns the host rows as a MATCH_ROW structured array (a view of ``pinned``
+    when given: int32 (>= total queries, 4), pinned)."""
+    import torch
+
+    lib = _lib.load()
+    if d <= 0:
+        raise ValueError(f"cell half-size d must be positive, got {d}")
+    if strategy not in STRATEGIES:
+        raise ValueError(f"unknown strategy {strategy!r}")
+    D = float(grid_d) if grid_d is not None else float(d) * float(inflation)
+    P = len(q_img)
+    dev = bank.device
+    if device_inputs is None:
+        device_inputs = prepare_pairs(bank, q_img, t_img, F, query_lists)
+    pq, pt, pF, qoff_d, qlist_d, qoff = device_inputs[:6]
+    qsrc_d = device_inputs[6] if len(device_inputs) > 6 else None
+    nq_total = int(qoff[-1]) if P else 0
+    if P == 0:
+        return np.zeros(0, MATCH_ROW)
+    grid = bank.grid(D, stream)
+    prm = _lib.MatchParams(float(d), float(np.float32(ratio)), float(np.float32(single_cap)),
+                           max(bank.max_n, 1), int(chunk_pairs), STRATEGIES[strategy])
+    qoff_c = np.ascontiguousarray(qoff, dtype=np.int64)
+    ws_bytes = lib.msfm_guided_workspace_bytes(P, qoff_c.ctypes.data, ctypes.byref(prm))
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    cap = max(nq_total, 1)
+    out_q = torch.empty(cap, dtype=torch.int32, device=dev)
+    out_t = torch.empty(cap, dtype=torch.int32, device=dev)
+    out_d = torch.empty(cap, dtype=torch.float32, device=dev)
+    out_r = torch.empty(cap, dtype=torch.float32, device=dev)
+    out_c = torch.zeros(P, dtype=torch.int32, device=dev)
+    out_off = torch.empty(P + 1, dtype=torch.int64, device=dev)
+    d_rows = torch.empty((cap, 4), dtype=torch.int32, device=dev)
+    d_meta = torch.zeros(2 * (P + 1), dtype=torch.int64, device=dev)
+    h_meta = torch.zeros(2 * (P + 1), dtype=torch.int64, pin_memory=True)
+    if pinned is None or pinned.shape[0] < cap:
+        pinned = torch.empty((cap, 4), dtype=torch.int32, pin_memory=True)
+    total = ctypes.c_int64(0)
+    copy_stream = torch.cuda.Stream(device=dev)
+    b, g = bank.cstruct(), grid.cstruct()
+    _lib.check(lib.msfm_guided_match_rows(ctypes.byref(b), ctypes.byref(g), P, _lib.ptr(pq),
+                                          _lib.ptr(pt), _lib.ptr(pF), _lib.ptr(qoff_d),
+                                          _lib.ptr(qlist_d), _lib.ptr(qsrc_d), qoff_c.ctypes.data,
+                                          ctypes.byref(prm), _lib.ptr(out_q), _lib.ptr(out_t),
+                                          _lib.ptr(out_d), _lib.ptr(out_r), _lib.ptr(out_c),
+                                          _lib.ptr(out_off), _lib.ptr(d_rows), _lib.ptr(d_meta),
+                                          h_meta.data_ptr(), pinned.data_ptr(), ctypes.byref(total),
+                                          _lib.ptr(ws), ws_bytes, _lib.stream_handle(stream),
+                                          copy_stream.cuda_stream), "msfm_guided_match_rows")
+    n = int(total.value)
+    return pinned[:n].numpy().view(MATCH_ROW).reshape(n)
+
+
 def prepare_pairs(bank: FeatureBank, q_img, t_img, F, query_lists):
     """Stage the pair table on the device (index translation + one copy per array).
 

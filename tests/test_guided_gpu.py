@@ -210,3 +210,20 @@ def test_dropin_strategies_and_errors():
     with pytest.raises(ValueError):
         guided_match_pair(scene.feature_sets[p["q"]], scene.feature_sets[p["t"]], geom,
                           strategy="bogus")
+
+
+@pytest.mark.parametrize("chunk", [1, 3, 0])
+def test_pipelined_host_rows_equal_device_packing(chunk):
+    """msfm_guided_match_rows (chunk-pipelined pack + D2H) == match_pairs + packing."""
+    from paper_1512_06235_b200 import scenes
+    from paper_1512_06235_b200.guided import match_pairs, match_pairs_rows
+
+    scene, snap = scenes.build("C1", n_cameras=10)
+    wl = scenes.pair_workload(scene, snap)
+    ok = np.flatnonzero(wl.valid)
+    bank = _bank(scene.feature_sets)
+    ql = [wl.untracked[int(wl.q_img[k])] for k in ok]
+    want = match_pairs(bank, wl.q_img[ok], wl.t_img[ok], wl.F[ok], ql).rows_host()
+    got = match_pairs_rows(bank, wl.q_img[ok], wl.t_img[ok], wl.F[ok], ql, chunk_pairs=chunk)
+    assert len(got) == len(want) > 100
+    np.testing.assert_array_equal(got.view(np.int32), want.view(np.int32))
