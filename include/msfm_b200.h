@@ -201,6 +201,15 @@ int msfm_guided_match_rows(const msfm_bank* bank, const msfm_grids* grids, int32
 int msfm_ransac_samples(const uint64_t state_inc[4], int32_t has_uint32, uint32_t uinteger,
                         int64_t n, int32_t sample_size, int32_t count, int32_t* out,
                         uint64_t state_out[6]);
+/* PCG64 state (layout of state_out above) of np.random.default_rng(seed):
+ * numpy's SeedSequence -> PCG64 seeding restated (0 <= seed < 2^64). */
+int msfm_rng_seed_state(uint64_t seed, uint64_t state_out[6]);
+/* msfm_ransac_samples for n_items independent streams default_rng(seeds[i])
+ * over populations n[i]: out [n_items][count][sample_size], state_out
+ * (optional) [n_items][6] after the draws. */
+int msfm_ransac_samples_seeded(int32_t n_items, const uint64_t* seeds, const int64_t* n,
+                               int32_t sample_size, int32_t count, int32_t* out,
+                               uint64_t* state_out);
 
 /* ------------------------------------------------------------------------
  * 3D-2D localization kNN (DescriptorIndex.knn2 exact path, descriptors.py:35-72,

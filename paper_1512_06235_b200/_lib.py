@@ -52,6 +52,9 @@ _SIGS = {
                                        VP, VP, VP, ctypes.c_size_t, VP]),
     "msfm_ransac_samples": (ctypes.c_int, [VP, ctypes.c_int32, ctypes.c_uint32, ctypes.c_int64,
                                            ctypes.c_int32, ctypes.c_int32, VP, VP]),
+    "msfm_rng_seed_state": (ctypes.c_int, [ctypes.c_uint64, VP]),
+    "msfm_ransac_samples_seeded": (ctypes.c_int, [ctypes.c_int32, VP, VP, ctypes.c_int32,
+                                                  ctypes.c_int32, VP, VP]),
     "msfm_knn_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
     "msfm_knn2_tracks": (ctypes.c_int, [ctypes.POINTER(Bank), ctypes.c_int32, VP, VP, ctypes.c_int32,
                                         VP, ctypes.c_int32, ctypes.c_int32, VP, VP, VP, VP,

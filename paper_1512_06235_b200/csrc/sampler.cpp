@@ -5,8 +5,10 @@
 // buffered next_uint32, Lemire bounded ints (random_bounded_uint64 with
 // use_masked=0), Generator.choice's Floyd branch with a linear-probing hash
 // set of size nextpow2(1.2*size), then the in-place Fisher-Yates _shuffle_int.
-// The initial state comes from numpy itself (rng.bit_generator.state), so
-// SeedSequence is not restated.  Validated draw-for-draw in tests/test_sampler.py.
+// The initial state is either numpy's own (rng.bit_generator.state) or, for the
+// batched entry, numpy's SeedSequence(seed) -> PCG64 seeding restated below
+// (bit_generator.pyx hashmix/mix/generate_state, pcg64_set_seed).  Validated
+// draw-for-draw and state-for-state in tests/test_sampler.py.
 #include <stdint.h>
 #include <string.h>
 
@@ -108,7 +110,116 @@ bool choice_floyd(Pcg64& g, int64_t pop, int size, int64_t* out) {
 }
 }  // namespace
 
+namespace {
+// numpy SeedSequence (bit_generator.pyx), pool size 4, 32-bit words
+constexpr uint32_t INIT_A = 0x43b0d7e5u, MULT_A = 0x931e8875u;
+constexpr uint32_t INIT_B = 0x8b51f9ddu, MULT_B = 0x58f38dedu;
+constexpr uint32_t MIX_MULT_L = 0xca01f9ddu, MIX_MULT_R = 0x4973f715u;
+
+inline uint32_t hashmix(uint32_t value, uint32_t& hash_const) {
+    value ^= hash_const;
+    hash_const *= MULT_A;
+    value *= hash_const;
+    value ^= value >> 16;
+    return value;
+}
+
+inline uint32_t mixw(uint32_t x, uint32_t y) {
+    uint32_t r = MIX_MULT_L * x - MIX_MULT_R * y;
+    r ^= r >> 16;
+    return r;
+}
+
+// PCG64 state of np.random.default_rng(seed) for 0 <= seed < 2^64
+void seed_pcg64(uint64_t seed, Pcg64& g) {
+    uint32_t ent[2];
+    int ne = 0;
+    if (seed == 0) ent[ne++] = 0;
+    while (seed > 0) { ent[ne++] = (uint32_t)(seed & 0xffffffffu); seed >>= 32; }
+    uint32_t pool[4];
+    uint32_t hc = INIT_A;
+    for (int i = 0; i < 4; i++) pool[i] = hashmix(i < ne ? ent[i] : 0u, hc);
+    for (int s = 0; s < 4; s++)
+        for (int d = 0; d < 4; d++)
+            if (s != d) pool[d] = mixw(pool[d], hashmix(pool[s], hc));
+    // generate_state(4, uint64): 8 words, cycling the pool
+    uint32_t w[8];
+    uint32_t hb = INIT_B;
+    for (int i = 0; i < 8; i++) {
+        uint32_t v = pool[i % 4];
+        v ^= hb;
+        hb *= MULT_B;
+        v *= hb;
+        v ^= v >> 16;
+        w[i] = v;
+    }
+    uint64_t v64[4];
+    for (int i = 0; i < 4; i++) v64[i] = (uint64_t)w[2 * i] | ((uint64_t)w[2 * i + 1] << 32);
+    const u128 initstate = ((u128)v64[0] << 64) | v64[1];
+    const u128 initseq = ((u128)v64[2] << 64) | v64[3];
+    const u128 mult = ((u128)0x2360ED051FC65DA4ULL << 64) | 0x4385DF649FCCF645ULL;
+    g.state = 0;
+    g.inc = (initseq << 1) | 1u;
+    g.state = g.state * mult + g.inc;
+    g.state += initstate;
+    g.state = g.state * mult + g.inc;
+    g.has32 = 0;
+    g.u32 = 0;
+}
+}  // namespace
+
 namespace msfm { void set_error(const char* fmt, ...); }
+
+extern "C" int msfm_rng_seed_state(uint64_t seed, uint64_t state_out[6]) {
+    if (!state_out) return MSFM_EINVAL;
+    Pcg64 g;
+    seed_pcg64(seed, g);
+    state_out[0] = (uint64_t)(g.state >> 64);
+    state_out[1] = (uint64_t)g.state;
+    state_out[2] = (uint64_t)(g.inc >> 64);
+    state_out[3] = (uint64_t)g.inc;
+    state_out[4] = 0;
+    state_out[5] = 0;
+    return MSFM_OK;
+}
+
+extern "C" int msfm_ransac_samples_seeded(int32_t n_items, const uint64_t* seeds, const int64_t* n,
+                                          int32_t sample_size, int32_t count, int32_t* out,
+                                          uint64_t* state_out) {
+    if (n_items < 0 || !seeds || !n || !out || sample_size < 1 || sample_size > 48 || count < 0) {
+        msfm::set_error("msfm_ransac_samples_seeded: bad arguments");
+        return MSFM_EINVAL;
+    }
+    int64_t tmp[48];
+    for (int32_t it = 0; it < n_items; it++) {
+        if (n[it] < sample_size) {
+            msfm::set_error("msfm_ransac_samples_seeded: item %d has %lld < %d rows", it,
+                            (long long)n[it], sample_size);
+            return MSFM_EINVAL;
+        }
+        Pcg64 g;
+        seed_pcg64(seeds[it], g);
+        int32_t* o = out + (int64_t)it * count * sample_size;
+        for (int32_t h = 0; h < count; h++) {
+            if (!choice_floyd(g, n[it], sample_size, tmp)) {
+                msfm::set_error("msfm_ransac_samples_seeded: population %lld outside the Floyd "
+                                "branch", (long long)n[it]);
+                return MSFM_EINVAL;
+            }
+            for (int k = 0; k < sample_size; k++) o[(int64_t)h * sample_size + k] = (int32_t)tmp[k];
+        }
+        if (state_out) {
+            uint64_t* so = state_out + 6 * (int64_t)it;
+            so[0] = (uint64_t)(g.state >> 64);
+            so[1] = (uint64_t)g.state;
+            so[2] = (uint64_t)(g.inc >> 64);
+            so[3] = (uint64_t)g.inc;
+            so[4] = (uint64_t)g.has32;
+            so[5] = (uint64_t)g.u32;
+        }
+    }
+    return MSFM_OK;
+}
 
 extern "C" int msfm_ransac_samples(const uint64_t state_inc[4], int32_t has_uint32,
                                    uint32_t uinteger, int64_t n, int32_t sample_size,

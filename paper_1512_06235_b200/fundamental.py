@@ -17,7 +17,6 @@ import numpy as np
 
 from . import _lib
 from .pnp import _replay
-from .sampling import rng_state
 from .types import InsufficientDataError, TwoViewGeometry
 
 SAMPSON_THRESHOLD_PX = 2.0     # geometry.py:19
@@ -90,14 +89,15 @@ def fransac_batch(q_list, c_list, seeds, *, threshold=SAMPSON_THRESHOLD_PX,
     H1 = min(max_iters, first_round)
     counts = np.full((A, max_iters), -2, np.int64)
     samples = np.zeros((A, H1, 8), np.int32)
-    states = []
-    for k, i in enumerate(active):
-        words, has32, u32 = rng_state(int(seeds[i]))
-        out_state = np.zeros(6, np.uint64)
-        _lib.check(lib.msfm_ransac_samples(words.ctypes.data, has32, u32, int(pairs.n[k]), 8, H1,
-                                           samples[k].ctypes.data, out_state.ctypes.data),
-                   "msfm_ransac_samples")
-        states.append(out_state)
+    st_all = np.zeros((A, 6), np.uint64)
+    if any(int(seeds[i]) < 0 for i in active):
+        raise ValueError("expected non-negative integer seeds")   # as np.random.default_rng
+    seed_arr = np.array([int(seeds[i]) for i in active], np.uint64)
+    n_arr = np.ascontiguousarray(pairs.n, np.int64)
+    _lib.check(lib.msfm_ransac_samples_seeded(A, seed_arr.ctypes.data, n_arr.ctypes.data, 8, H1,
+                                              samples.ctypes.data, st_all.ctypes.data),
+               "msfm_ransac_samples_seeded")
+    states = [st_all[k] for k in range(A)]
     d_F1, c1 = _score(lib, pairs, samples, H1, threshold, st, dev)
     counts[:, :H1] = c1
     best = [None] * A

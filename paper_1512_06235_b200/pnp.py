@@ -15,7 +15,6 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .sampling import rng_state
 from .types import InsufficientDataError
 
 PNP_THRESHOLD_PX = 4.0
@@ -105,15 +104,17 @@ def pnp_batch(X_list, uv_list, K_list, seeds, *, threshold=PNP_THRESHOLD_PX,
     A = len(active)
     H1 = min(max_iters, first_round)
     counts = np.full((A, max_iters), -2, np.int64)
-    states = []
+    # all streams default_rng(seed) at once (SeedSequence restated natively)
     samples = np.zeros((A, H1, 6), np.int32)
-    for k, i in enumerate(active):
-        words, has32, u32 = rng_state(int(seeds[i]))
-        out_state = np.zeros(6, np.uint64)
-        _lib.check(lib.msfm_ransac_samples(words.ctypes.data, has32, u32, int(batch.n[k]), 6, H1,
-                                           samples[k].ctypes.data, out_state.ctypes.data),
-                   "msfm_ransac_samples")
-        states.append((out_state, has32, u32))
+    st_all = np.zeros((A, 6), np.uint64)
+    if any(int(seeds[i]) < 0 for i in active):
+        raise ValueError("expected non-negative integer seeds")   # as np.random.default_rng
+    seed_arr = np.array([int(seeds[i]) for i in active], np.uint64)
+    n_arr = np.ascontiguousarray(batch.n, np.int64)
+    _lib.check(lib.msfm_ransac_samples_seeded(A, seed_arr.ctypes.data, n_arr.ctypes.data, 6, H1,
+                                              samples.ctypes.data, st_all.ctypes.data),
+               "msfm_ransac_samples_seeded")
+    states = [(st_all[k],) for k in range(A)]
     # hypotheses stay on the device; only the inlier counts come back for the replay
     d_hyp1, c1 = _score(lib, batch, samples, H1, threshold, st, dev)
     counts[:, :H1] = c1

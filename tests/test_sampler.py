@@ -49,3 +49,40 @@ def test_stream_continuation():
     rng = np.random.default_rng(seed)
     ref = np.stack([rng.choice(n, 6, replace=False) for _ in range(25)])
     np.testing.assert_array_equal(np.vstack([a, b]), ref)
+
+
+def test_seedsequence_restatement_matches_numpy():
+    """msfm_rng_seed_state == np.random.default_rng(seed).bit_generator.state."""
+    from paper_1512_06235_b200 import _lib
+    from paper_1512_06235_b200.sampling import rng_state
+
+    lib = _lib.load(require_device=False)
+    seeds = list(range(0, 300)) + [2**32 - 1, 2**32, 2**32 + 5, 123456789012, 2**63 + 11,
+                                   2**64 - 1, 100003 * 19 + 18, 31337]
+    out = np.zeros(6, np.uint64)
+    for seed in seeds:
+        words, has32, u32 = rng_state(seed)
+        assert lib.msfm_rng_seed_state(seed, out.ctypes.data) == 0
+        np.testing.assert_array_equal(out[:4], words, err_msg=str(seed))
+        assert has32 == 0 and u32 == 0
+
+
+@pytest.mark.parametrize("size", [6, 8])
+def test_batched_seeded_samples(size):
+    from paper_1512_06235_b200 import _lib
+
+    lib = _lib.load(require_device=False)
+    seeds = np.array([3, 1000, 100003 * 4 + 9, 7], np.uint64)
+    n = np.array([50, 8, 3000, 123], np.int64)
+    count = 40
+    out = np.zeros((len(seeds), count, size), np.int32)
+    st = np.zeros((len(seeds), 6), np.uint64)
+    assert lib.msfm_ransac_samples_seeded(len(seeds), seeds.ctypes.data, n.ctypes.data, size,
+                                          count, out.ctypes.data, st.ctypes.data) == 0
+    for i in range(len(seeds)):
+        rng = np.random.default_rng(int(seeds[i]))
+        ref = np.stack([rng.choice(int(n[i]), size=size, replace=False) for _ in range(count)])
+        np.testing.assert_array_equal(out[i], ref)
+        s = rng.bit_generator.state
+        assert int(st[i, 0]) == s["state"]["state"] >> 64
+        assert int(st[i, 4]) == s["has_uint32"]
