@@ -331,6 +331,37 @@ int msfm_merge_tracks(const msfm_bank* bank, int64_t n_edges, const int32_t* d_u
                       int32_t* d_out_node, int32_t* d_seg_owner, int64_t* d_seg_off,
                       int64_t* d_counts, void* d_workspace, size_t workspace_bytes, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Host-only staging of .msft feature files (features.py:98-130): the
+ * reference's header / size / bounds validation (status codes below, with the
+ * first offending record), then the records in np.argsort(-scale, "stable")
+ * order written to caller buffers (xy [n][2], scale, orientation [n] f32,
+ * desc [n][128] u8; scale / orientation may be NULL; xy = NULL probes the
+ * header only).  msfm_msft_load_many loads n_files into one set of buffers
+ * at rows row_off[i] (e.g. the pinned host bank) on n_threads host threads.
+ * ---------------------------------------------------------------------- */
+#define MSFM_MSFT_OK 0
+#define MSFM_MSFT_TRUNCATED 1     /* shorter than the 24-byte header */
+#define MSFM_MSFT_BAD_MAGIC 2
+#define MSFM_MSFT_BAD_VERSION 3
+#define MSFM_MSFT_BAD_SIZE 4      /* payload != count * 144 bytes */
+#define MSFM_MSFT_BOUNDS 5        /* x, y outside the image or scale <= 0 */
+#define MSFM_MSFT_IO 6
+typedef struct {
+    int32_t status;
+    char magic[4];
+    uint32_t version;
+    int32_t image_id, width, height;
+    int64_t count, file_bytes;
+    int64_t bad_record;
+    float bad_x, bad_y, bad_scale;
+} msfm_msft_info;
+int msfm_msft_load(const char* path, msfm_msft_info* info, float* xy, float* scale,
+                   float* orientation, uint8_t* desc);
+int msfm_msft_load_many(int32_t n_files, const char* const* paths, const int64_t* row_off,
+                        msfm_msft_info* infos, float* xy, float* scale, float* orientation,
+                        uint8_t* desc, int32_t n_threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,6 +30,15 @@ class Grids(ctypes.Structure):
                 ("d_rxy", VP), ("d_cxy", VP), ("D", ctypes.c_double)]
 
 
+class MsftInfo(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("magic", ctypes.c_char * 4),
+                ("version", ctypes.c_uint32), ("image_id", ctypes.c_int32),
+                ("width", ctypes.c_int32), ("height", ctypes.c_int32),
+                ("count", ctypes.c_int64), ("file_bytes", ctypes.c_int64),
+                ("bad_record", ctypes.c_int64), ("bad_x", ctypes.c_float),
+                ("bad_y", ctypes.c_float), ("bad_scale", ctypes.c_float)]
+
+
 class MatchParams(ctypes.Structure):
     _fields_ = [("d", ctypes.c_double), ("ratio", ctypes.c_float),
                 ("single_cap", ctypes.c_float), ("max_nt", ctypes.c_int32),
@@ -52,6 +61,9 @@ _SIGS = {
                                        VP, VP, VP, ctypes.c_size_t, VP]),
     "msfm_ransac_samples": (ctypes.c_int, [VP, ctypes.c_int32, ctypes.c_uint32, ctypes.c_int64,
                                            ctypes.c_int32, ctypes.c_int32, VP, VP]),
+    "msfm_msft_load": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(MsftInfo), VP, VP, VP, VP]),
+    "msfm_msft_load_many": (ctypes.c_int, [ctypes.c_int32, VP, VP, VP, VP, VP, VP, VP,
+                                           ctypes.c_int32]),
     "msfm_rng_seed_state": (ctypes.c_int, [ctypes.c_uint64, VP]),
     "msfm_ransac_samples_seeded": (ctypes.c_int, [ctypes.c_int32, VP, VP, ctypes.c_int32,
                                                   ctypes.c_int32, VP, VP]),

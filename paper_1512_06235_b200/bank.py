@@ -44,6 +44,24 @@ class HostBank:
         self.img_n = torch.from_numpy(self.counts.astype(np.int32)).pin_memory()
         self.img_wh = torch.from_numpy(self.wh.copy()).pin_memory()
 
+    @classmethod
+    def from_buffers(cls, image_ids, counts, wh, xy, desc):
+        """A bank over already-filled pinned buffers (staging.host_bank_from_dir)."""
+        import torch
+
+        self = cls.__new__(cls)
+        self.image_ids = list(image_ids)
+        self.counts = np.asarray(counts, np.int64)
+        self.offsets = np.zeros(len(self.counts), dtype=np.int64)
+        if len(self.counts) > 1:
+            np.cumsum(self.counts[:-1], out=self.offsets[1:])
+        self.wh = np.asarray(wh, np.int32).reshape(-1, 2)
+        self.xy, self.desc = xy, desc
+        self.img_off = torch.from_numpy(self.offsets.copy()).pin_memory()
+        self.img_n = torch.from_numpy(self.counts.astype(np.int32)).pin_memory()
+        self.img_wh = torch.from_numpy(self.wh.copy()).pin_memory()
+        return self
+
     @property
     def nbytes(self) -> int:
         return sum(int(t.numel() * t.element_size())

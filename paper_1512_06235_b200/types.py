@@ -28,6 +28,10 @@ class MsfmError(Exception):
     pass
 
 
+class FormatError(MsfmError):
+    """Malformed input file (errors.py:12-13)."""
+
+
 class DegenerateGeometryError(MsfmError):
     pass
 
@@ -98,6 +102,8 @@ class FeatureSet:
 
 def select_top_scale(fs, eta: float = 20.0):
     """Coarse-tier boundary at the top eta percent (features.py:149-161)."""
+    if not 0 < eta <= 100:
+        raise ValueError(f"eta must be in (0, 100], got {eta}")
     n = len(fs)
     count = n if n < 1000 else int(np.ceil(eta / 100.0 * n))
     return replace(fs, coarse_count=count)
