@@ -188,20 +188,11 @@ def run_reference(args, rank, world):
 
 
 def gather_to_rank0(res, world, dev):
-    """Variable-length gather of this rank's matches (device-packed rows) over NCCL."""
-    import torch
-
+    """Variable-length gather of this rank's matches over NCCL: the device-packed
+    16-B rows (pair index local to the rank: global = rank + world * local)."""
     from paper_1512_06235_b200.dist import gather_rows
 
-    cnt = res.count.to(torch.int64)
-    qoff = torch.from_numpy(res.qoff[:-1]).to(dev)
-    # compact this rank's per-pair segments into one contiguous block on the device
-    idx_pairs = torch.repeat_interleave(torch.arange(cnt.numel(), device=dev), cnt)
-    starts = torch.cumsum(cnt, 0) - cnt
-    pos = torch.arange(idx_pairs.numel(), device=dev) - starts[idx_pairs] + qoff[idx_pairs]
-    rows = torch.stack([idx_pairs, res.q[pos].to(torch.int64), res.t[pos].to(torch.int64),
-                        res.dist[pos].view(torch.int32).to(torch.int64),
-                        res.ratio[pos].view(torch.int32).to(torch.int64)], 1)
+    rows, _ = res.packed()
     return gather_rows(rows, world)
 
 
