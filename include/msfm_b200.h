@@ -87,9 +87,10 @@ int msfm_feature_norms(const uint8_t* d_desc, int64_t n, int32_t* d_norm2, void*
  *   d_roff/d_coff [n_images] first bucket of image i in the row/col tables
  *   d_rstart/d_cstart [n_buckets_total+1] CSR starts (global feature index)
  *   d_rmem/d_cmem [n_total]  image-local feature ids in bucket order
- *   d_rxy/d_cxy [n_total][2] the same features' positions (f32) in bucket
- *                            order, so a strip gather reads id and position
- *                            side by side instead of through the id
+ *   d_rrec/d_crec [n_total][4] int32 records in bucket order: x, y (f32
+ *                            bits), |desc|^2, feature id, so a strip gather
+ *                            reads one 16-B record per entry instead of
+ *                            chasing the id
  * ---------------------------------------------------------------------- */
 typedef struct {
     const int32_t* d_sub;        /* short2 packed: (u & 0xffff) | (v << 16)      */
@@ -100,8 +101,8 @@ typedef struct {
     const int32_t* d_cstart;
     const int32_t* d_rmem;
     const int32_t* d_cmem;
-    const float* d_rxy;
-    const float* d_cxy;
+    const int32_t* d_rrec;
+    const int32_t* d_crec;
     double D;                    /* cell half-size = d * inflation (grid.d)      */
 } msfm_grids;
 
@@ -115,7 +116,7 @@ size_t msfm_grid_workspace_bytes(int64_t n_buckets_total);
 int msfm_grid_build(const msfm_bank* bank, const int32_t* d_dims, const int64_t* d_roff,
                     const int64_t* d_coff, int64_t n_buckets_total, int64_t n_total, double D,
                     int32_t* d_sub, int32_t* d_rstart, int32_t* d_cstart, int32_t* d_rmem,
-                    int32_t* d_cmem, float* d_rxy, float* d_cxy, void* d_workspace,
+                    int32_t* d_cmem, int32_t* d_rrec, int32_t* d_crec, void* d_workspace,
                     size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------------

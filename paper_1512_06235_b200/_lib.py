@@ -27,7 +27,7 @@ class Bank(ctypes.Structure):
 class Grids(ctypes.Structure):
     _fields_ = [("d_sub", VP), ("d_dims", VP), ("d_roff", VP), ("d_coff", VP),
                 ("d_rstart", VP), ("d_cstart", VP), ("d_rmem", VP), ("d_cmem", VP),
-                ("d_rxy", VP), ("d_cxy", VP), ("D", ctypes.c_double)]
+                ("d_rrec", VP), ("d_crec", VP), ("D", ctypes.c_double)]
 
 
 class MsftInfo(ctypes.Structure):

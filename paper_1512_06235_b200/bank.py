@@ -143,8 +143,8 @@ class SpatialIndex:
         self.cstart = torch.empty(nb + 1, dtype=torch.int32, device=dev)
         self.rmem = torch.empty(max(bank.n_total, 1), dtype=torch.int32, device=dev)
         self.cmem = torch.empty(max(bank.n_total, 1), dtype=torch.int32, device=dev)
-        self.rxy = torch.empty((max(bank.n_total, 1), 2), dtype=torch.float32, device=dev)
-        self.cxy = torch.empty((max(bank.n_total, 1), 2), dtype=torch.float32, device=dev)
+        self.rrec = torch.empty((max(bank.n_total, 1), 4), dtype=torch.int32, device=dev)
+        self.crec = torch.empty((max(bank.n_total, 1), 4), dtype=torch.int32, device=dev)
         ws_bytes = lib.msfm_grid_workspace_bytes(nb)
         ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
         st = _lib.stream_handle(stream)
@@ -153,16 +153,16 @@ class SpatialIndex:
                                        _lib.ptr(self.coff), nb, bank.n_total, self.D,
                                        _lib.ptr(self.sub), _lib.ptr(self.rstart),
                                        _lib.ptr(self.cstart), _lib.ptr(self.rmem),
-                                       _lib.ptr(self.cmem), _lib.ptr(self.rxy),
-                                       _lib.ptr(self.cxy), _lib.ptr(ws), ws_bytes, st),
+                                       _lib.ptr(self.cmem), _lib.ptr(self.rrec),
+                                       _lib.ptr(self.crec), _lib.ptr(ws), ws_bytes, st),
                    "msfm_grid_build")
         self._ws = ws  # keep alive until the stream has consumed it
 
     def cstruct(self) -> _lib.Grids:
         return _lib.Grids(_lib.ptr(self.sub), _lib.ptr(self.dims), _lib.ptr(self.roff),
                           _lib.ptr(self.coff), _lib.ptr(self.rstart), _lib.ptr(self.cstart),
-                          _lib.ptr(self.rmem), _lib.ptr(self.cmem), _lib.ptr(self.rxy),
-                          _lib.ptr(self.cxy), self.D)
+                          _lib.ptr(self.rmem), _lib.ptr(self.cmem), _lib.ptr(self.rrec),
+                          _lib.ptr(self.crec), self.D)
 
 
 def _to_device(a: np.ndarray, device):

@@ -163,7 +163,7 @@ struct GridBuildArgs {
     const float2* xy; const int64_t* img_off; const int32_t* img_n; const int32_t* img_wh;
     const int32_t* dims; const int64_t* roff; const int64_t* coff;
     int32_t* sub; int32_t* rcount; int32_t* ccount; int32_t* rcur; int32_t* ccur;
-    int32_t* rmem; int32_t* cmem; float2* rxy; float2* cxy; double D;
+    int32_t* rmem; int32_t* cmem; int4* rrec; int4* crec; const int32_t* norm2; double D;
 };
 
 __device__ __forceinline__ int bucket_of(float v, double D, int nb) {
@@ -198,8 +198,9 @@ __global__ void grid_scatter_kernel(GridBuildArgs a) {
         int c = atomicAdd(&a.ccur[a.coff[img] + (int64_t)bx * nby + by], 1);
         a.rmem[r] = f;
         a.cmem[c] = f;
-        a.rxy[r] = p;
-        a.cxy[c] = p;
+        const int4 rec = make_int4(__float_as_int(p.x), __float_as_int(p.y), a.norm2[off + f], f);
+        a.rrec[r] = rec;
+        a.crec[c] = rec;
     }
 }
 
@@ -260,7 +261,7 @@ struct ChunkArgs {
     // index
     const int32_t* sub; const int32_t* dims; const int64_t* roff; const int64_t* coff;
     const int32_t* rstart; const int32_t* cstart; const int32_t* rmem; const int32_t* cmem;
-    const float2* rxy; const float2* cxy;
+    const int4* rrec; const int4* crec;   // bucket-ordered (x, y, |desc|^2, id)
     double D, d;
     float ratio, single_cap;
     int stats_mode;              // 1: one super-group per group (exact SearchStats)
@@ -960,7 +961,8 @@ __device__ __forceinline__ bool in_cprime(const ChunkArgs& a, const GroupRec& G,
 }
 
 struct alignas(16) WarpSmem {
-    float2 xy[CAP];              // candidate positions (from the bucket-ordered copy)
+    float2 xy[CAP];              // candidate positions (from the bucket-ordered records)
+    unsigned nrm[CAP];           // candidate |desc|^2
     unsigned short list[CAP];    // candidate feature ids (target-local)
     unsigned short cmask[CAP];   // per candidate: groups (bit gi) whose C' contains it
     unsigned short ulist[CAP];   // positions still to decide
@@ -1111,7 +1113,6 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
             unsigned tb0, tb1;
         };
         const uint4* tdesc = reinterpret_cast<const uint4*>(a.desc + toff * 128) + 2 * t;
-        const int32_t* tnorm = a.norm2 + toff;
         auto load_tile = [&](int mt, Tile& T) {
             const int r0 = mt * 16 + g, r1 = r0 + 8;
             const bool v0 = r0 < n, v1 = r1 < n;
@@ -1120,8 +1121,8 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
             const uint4* row1 = tdesc + 8 * f1;
             T.x00 = __ldg(row0); T.x01 = __ldg(row0 + 1);
             T.x10 = __ldg(row1); T.x11 = __ldg(row1 + 1);
-            T.tb0 = ((unsigned)__ldg(tnorm + f0) << 9) | (unsigned)r0;
-            T.tb1 = ((unsigned)__ldg(tnorm + f1) << 9) | (unsigned)r1;
+            T.tb0 = (S.nrm[v0 ? r0 : 0] << 9) | (unsigned)r0;
+            T.tb1 = (S.nrm[v1 ? r1 : 0] << 9) | (unsigned)r1;
         };
         auto do_tile = [&](int mt, const Tile& cur) {
             const uint4 x00 = cur.x00, x01 = cur.x01, x10 = cur.x10, x11 = cur.x11;
@@ -1286,8 +1287,7 @@ __global__ void __launch_bounds__(WARPS * 32, MATCH_MINB) match_kernel(ChunkArgs
         const int nalong = SG.nalong;
         const int64_t toffb = SG.toffb;
         const int32_t* start = SG.horiz ? a.rstart : a.cstart;
-        const int32_t* mem = SG.horiz ? a.rmem : a.cmem;
-        const float2* mxy = SG.horiz ? a.rxy : a.cxy;
+        const int4* mrec4 = SG.horiz ? a.rrec : a.crec;
         int n = 0;
         bool first_round = true;
         int cols_total = 0;
@@ -1342,11 +1342,13 @@ __global__ void __launch_bounds__(WARPS * 32, MATCH_MINB) match_kernel(ChunkArgs
                 const int oex = __shfl_sync(FULL, incl - len, o & 31);
                 bool pass = false, sure = false;
                 int f = 0;
+                unsigned nrm = 0;
                 float2 p2 = make_float2(0.f, 0.f);
                 if (j < tot) {
-                    const int e = ob + (j - oex);
-                    f = mem[e];
-                    p2 = mxy[e];
+                    const int4 rec = __ldg(mrec4 + ob + (j - oex));
+                    f = rec.w;
+                    p2 = make_float2(__int_as_float(rec.x), __int_as_float(rec.y));
+                    nrm = (unsigned)rec.z;
                     const float adr = fabsf(fmaf(SG.ar, p2.x, fmaf(SG.br, p2.y, SG.cr)));
                     pass = adr <= SG.R;
                     sure = adr + SG.delta <= SG.hsure && p2.x >= SG.border &&
@@ -1372,6 +1374,7 @@ __global__ void __launch_bounds__(WARPS * 32, MATCH_MINB) match_kernel(ChunkArgs
                 if (pass) {
                     S.list[n + k] = (unsigned short)f;
                     S.xy[n + k] = p2;
+                    S.nrm[n + k] = nrm;
                 }
                 const unsigned bits = __reduce_or_sync(FULL, (pass && sure) ? (1u << k) : 0u);
                 if (lane == 0 && cnt) {
@@ -1613,7 +1616,7 @@ extern "C" size_t msfm_grid_workspace_bytes(int64_t n_buckets_total) {
 extern "C" int msfm_grid_build(const msfm_bank* bank, const int32_t* d_dims, const int64_t* d_roff,
                                const int64_t* d_coff, int64_t n_buckets_total, int64_t n_total,
                                double D, int32_t* d_sub, int32_t* d_rstart, int32_t* d_cstart,
-                               int32_t* d_rmem, int32_t* d_cmem, float* d_rxy, float* d_cxy,
+                               int32_t* d_rmem, int32_t* d_cmem, int32_t* d_rrec, int32_t* d_crec,
                                void* d_workspace,
                                size_t workspace_bytes, void* stream) {
     if (!bank || !(D > 0) || n_buckets_total < 0 || n_total < 0) {
@@ -1635,8 +1638,8 @@ extern "C" int msfm_grid_build(const msfm_bank* bank, const int32_t* d_dims, con
     if (bank->n_images == 0) return MSFM_OK;
     GridBuildArgs a{reinterpret_cast<const float2*>(bank->d_xy), bank->d_img_off, bank->d_img_n,
                     bank->d_img_wh, d_dims, d_roff, d_coff, d_sub, d_rstart, d_cstart, rcur, ccur,
-                    d_rmem, d_cmem, reinterpret_cast<float2*>(d_rxy),
-                    reinterpret_cast<float2*>(d_cxy), D};
+                    d_rmem, d_cmem, reinterpret_cast<int4*>(d_rrec),
+                    reinterpret_cast<int4*>(d_crec), bank->d_norm2, D};
     grid_count_kernel<<<bank->n_images, 256, 0, st>>>(a);
     MSFM_LAUNCH_CHECK();
     count_launches(1);
@@ -1735,8 +1738,8 @@ static int guided_match_impl(const msfm_bank* bank, const msfm_grids* grids, int
     a.img_off = bank->d_img_off; a.img_n = bank->d_img_n; a.img_wh = bank->d_img_wh;
     a.sub = grids->d_sub; a.dims = grids->d_dims; a.roff = grids->d_roff; a.coff = grids->d_coff;
     a.rstart = grids->d_rstart; a.cstart = grids->d_cstart; a.rmem = grids->d_rmem; a.cmem = grids->d_cmem;
-    a.rxy = reinterpret_cast<const float2*>(grids->d_rxy);
-    a.cxy = reinterpret_cast<const float2*>(grids->d_cxy);
+    a.rrec = reinterpret_cast<const int4*>(grids->d_rrec);
+    a.crec = reinterpret_cast<const int4*>(grids->d_crec);
     a.D = grids->D; a.d = prm->d; a.ratio = prm->ratio; a.single_cap = prm->single_cap;
     if (prm->strategy < 0 || prm->strategy > 2) {
         set_error("msfm_guided_match: unknown strategy %d", prm->strategy);
