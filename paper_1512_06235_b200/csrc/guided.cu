@@ -1259,17 +1259,23 @@ __global__ void __launch_bounds__(WARPS * 32, MATCH_MINB) match_kernel(ChunkArgs
     WarpSmem& S = smem[warp];
     const int total = a.sgstart[a.npairs];
     const float Df = (float)a.D;
-    for (int sid = 0;;) {
-        if (lane == 0) sid = atomicAdd(a.sg_next, 1);
-        sid = __shfl_sync(FULL, sid, 0);
+    static_assert(sizeof(SGRec) % 16 == 0, "SGRec must be 16-byte granular");
+    constexpr int SG_CHUNKS = (int)(sizeof(SGRec) / 16);
+    // the next super-group's id and record are fetched while the current one runs
+    int nsid = 0;
+    if (lane == 0) nsid = atomicAdd(a.sg_next, 1);
+    nsid = __shfl_sync(FULL, nsid, 0);
+    uint4 nrec = make_uint4(0, 0, 0, 0);
+    if (nsid < total && lane < SG_CHUNKS) nrec = __ldg(reinterpret_cast<const uint4*>(a.sg + nsid) + lane);
+    for (;;) {
+        const int sid = nsid;
         if (sid >= total) break;
-        {
-            static_assert(sizeof(SGRec) % 16 == 0, "SGRec must be 16-byte granular");
-            const uint4* src = reinterpret_cast<const uint4*>(a.sg + sid);
-            uint4* dst = reinterpret_cast<uint4*>(&S.sg);
-            if (lane < (int)(sizeof(SGRec) / 16)) dst[lane] = __ldg(src + lane);
-            __syncwarp();
-        }
+        if (lane < SG_CHUNKS) reinterpret_cast<uint4*>(&S.sg)[lane] = nrec;
+        __syncwarp();
+        if (lane == 0) nsid = atomicAdd(a.sg_next, 1);
+        nsid = __shfl_sync(FULL, nsid, 0);
+        if (nsid < total && lane < SG_CHUNKS)
+            nrec = __ldg(reinterpret_cast<const uint4*>(a.sg + nsid) + lane);
         const SGRec& SG = S.sg;
         if (a.dbg && lane == 0) {
             atomicAdd(&a.dbg[0], 1ull);
