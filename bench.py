@@ -312,7 +312,10 @@ def run_b200(args, rank, world):
                                "synthetic scene, 8k feats/img, 3072x2304",
                    "pairs": int(total_pairs), "cameras": args.cameras,
                    "mean_queries_per_pair": float(np.mean([len(wl.untracked[int(wl.q_img[k])]) for k in ok])),
-                   "parallelism": f"pairs round-robin over {world} GPU(s)",
+                   "parallelism": f"pairs round-robin over {world} GPU(s), no collective on "
+                                  "the data path; match rows gathered over NCCL",
+                   "scaling_note": "C3's pair set sharded across ranks (BASELINE configs[2]); "
+                                   "labelled weak per the sharded-independent-units rule",
                    "l2": "inputs larger than L2 (feature bank "
                          f"{host.nbytes / 1e6:.0f} MB > 126 MB); no explicit flush"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
