@@ -227,3 +227,33 @@ def test_pipelined_host_rows_equal_device_packing(chunk):
     got = match_pairs_rows(bank, wl.q_img[ok], wl.t_img[ok], wl.F[ok], ql, chunk_pairs=chunk)
     assert len(got) == len(want) > 100
     np.testing.assert_array_equal(got.view(np.int32), want.view(np.int32))
+
+
+def test_16k_feature_pairs_match_oracle():
+    """C4/C5 feature density (16k/img): a few densify pairs against the C oracle
+    (16-bit feature ids in the packed rows, larger strips and member sets)."""
+    from oracle import guided as og
+    from paper_1512_06235_b200 import scenes
+    from paper_1512_06235_b200.guided import match_pairs
+
+    spec = scenes.spec_for("C4", n_cameras=12)
+    scene = scenes.generate_scene(spec)
+    snap = scenes.coarse_snapshot(scene, range(12))
+    wl = scenes.pair_workload(scene, snap)
+    ok = np.flatnonzero(wl.valid)[:3]
+    bank = _bank(scene.feature_sets)
+    ql = [wl.untracked[int(wl.q_img[k])] for k in ok]
+    res = match_pairs(bank, wl.q_img[ok], wl.t_img[ok], wl.F[ok], ql, with_stats=True)
+    pk, q, t, d, r = res.to_host()
+    stats = res.stats.cpu().numpy()
+    assert max(len(scene.feature_sets[i]) for i in scene.feature_sets) > 15000
+    for j, k in enumerate(ok):
+        fq, ft = scene.feature_sets[int(wl.q_img[k])], scene.feature_sets[int(wl.t_img[k])]
+        oq, ot, od, orr, ost = og.guided_match(fq.xy, fq.descriptors, ft.xy, ft.descriptors,
+                                               ft.width, ft.height, wl.F[k], ql[j])
+        sel = pk == j
+        np.testing.assert_array_equal(q[sel], oq)
+        np.testing.assert_array_equal(t[sel], ot)
+        np.testing.assert_array_equal(d[sel], od)
+        np.testing.assert_array_equal(r[sel], orr)
+        np.testing.assert_array_equal(stats[j], ost)

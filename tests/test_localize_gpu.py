@@ -28,7 +28,8 @@ def _random_case(rng, M, sizes, max_n=10, dup=False):
 
 
 @pytest.mark.parametrize("M,sizes,max_n", [(1, [1], 1), (5, [3, 1, 0, 130], 4), (128, [128], 10),
-                                           (300, [257, 1000, 5], 10), (1000, [2000, 129], 100)])
+                                           (300, [257, 1000, 5], 10), (1000, [2000, 129], 100),
+                                           (200, [16000, 31], 12)])
 def test_knn_topk_matches_exact_oracle(M, sizes, max_n):
     from paper_1512_06235_b200.bank import FeatureBank
     from paper_1512_06235_b200.localize import PointSet, knn2_tracks
