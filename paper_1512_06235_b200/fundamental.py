@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .pnp import _replay
+from .pnp import _replay_batch
 from .types import InsufficientDataError, TwoViewGeometry
 
 SAMPSON_THRESHOLD_PX = 2.0     # geometry.py:19
@@ -100,18 +100,8 @@ def fransac_batch(q_list, c_list, seeds, *, threshold=SAMPSON_THRESHOLD_PX,
     states = [st_all[k] for k in range(A)]
     d_F1, c1 = _score(lib, pairs, samples, H1, threshold, st, dev)
     counts[:, :H1] = c1
-    best = [None] * A
-    pending = []
-    for k in range(A):
-        try:
-            r = _replay(counts[k], H1, int(pairs.n[k]), max_iters, confidence, power=8)
-        except OverflowError:
-            best[k] = "overflow"
-            continue
-        if r[4]:
-            best[k] = r
-        else:
-            pending.append(k)
+    best = _replay_batch(counts, H1, pairs.n, max_iters, confidence, power=8)
+    pending = [k for k in range(A) if best[k] != "overflow" and not best[k][4]]
     d_F2 = None
     if pending:
         H2 = max_iters - H1
@@ -124,13 +114,10 @@ def fransac_batch(q_list, c_list, seeds, *, threshold=SAMPSON_THRESHOLD_PX,
                                                None), "msfm_ransac_samples")
         sub = _Pairs(dev, [q_list[active[k]] for k in pending], [c_list[active[k]] for k in pending])
         d_F2, c2 = _score(lib, sub, samples2, H2, threshold, st, dev)
-        for j, k in enumerate(pending):
-            counts[k, H1:] = c2[j]
-            try:
-                best[k] = _replay(counts[k], max_iters, int(pairs.n[k]), max_iters, confidence,
-                                  power=8)
-            except OverflowError:
-                best[k] = "overflow"
+        counts[pending, H1:] = c2
+        for k, r in zip(pending, _replay_batch(counts[pending], max_iters, pairs.n[pending],
+                                               max_iters, confidence, power=8)):
+            best[k] = r
     status = np.zeros(A, np.int32)
     d_best = torch.zeros((A, 9), dtype=torch.float64, device=dev)
     src1, src2 = [], []

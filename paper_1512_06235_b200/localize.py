@@ -148,7 +148,8 @@ class Correspondences:
 
 def direct_search(bank: FeatureBank, pts: PointSet, image_ids, *, ratio: float = RATIO_UNGUIDED,
                   single_cap: float = SINGLE_CANDIDATE_CAP, stream=None, device_points=None,
-                  knn: DeviceKnn | None = None, to_host: bool = True):
+                  knn: DeviceKnn | None = None, to_host: bool = True, flat: bool = False,
+                  device_flat: bool = False):
     """direct_3d2d_search for many images: kNN + ratio + one point per feature."""
     import torch
 
@@ -180,12 +181,26 @@ def direct_search(bank: FeatureBank, pts: PointSet, image_ids, *, ratio: float =
                                     _lib.ptr(cnt), _lib.stream_handle(stream)), "msfm_direct_3d2d")
     res = Correspondences(rows, fids, cnt, knn.M_pad)
     res._keep = (win, d_win_off, d_slots, knn)
+    if device_flat:
+        # (point rows, feature ids) on the device, offsets on the host: image s owns
+        # [off[s], off[s+1]); one small copy (the counts)
+        c = cnt[:len(slots)].cpu().numpy()
+        off = np.zeros(len(slots) + 1, np.int64)
+        np.cumsum(c, out=off[1:])
+        keep = torch.arange(knn.M_pad, device=dev)[None, :] < cnt[:len(slots), None]
+        return rows[:len(slots)][keep].long(), fids[:len(slots)][keep].long(), off
     if to_host:
         # three copies in total (counts, then the used prefix of both tables)
         c = cnt.cpu().numpy()
         w = int(c.max()) if len(c) else 0
         rh = rows[:, :w].cpu().numpy()
         fh = fids[:, :w].cpu().numpy()
+        if flat:
+            # (point ids, feature ids, offsets): image s owns [off[s], off[s+1])
+            off = np.zeros(len(slots) + 1, np.int64)
+            np.cumsum(c[:len(slots)], out=off[1:])
+            keep = np.arange(w)[None, :] < c[:len(slots), None]
+            return pts.ids[rh[keep]].astype(np.int64), fh[keep].astype(np.int64), off
         return [np.stack([pts.ids[rh[s, :c[s]]], fh[s, :c[s]]], 1).astype(np.int64)
                 for s in range(len(slots))]
     return res

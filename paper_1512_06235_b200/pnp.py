@@ -56,33 +56,133 @@ def _replay(counts, evaluated, n, max_iters, confidence, power=6):
     return best_h, best_count, it, needed, True
 
 
+def _replay_records(counts, evaluated, n, max_iters, confidence, power=6):
+    """_replay visiting only the improving hypotheses ("records"): the loop state
+    changes nowhere else, so the same scalar numpy expressions are evaluated in
+    the same order and the result (including the OverflowError) is identical."""
+    c = np.asarray(counts[:evaluated], np.int64)
+    prev = np.maximum.accumulate(np.concatenate([[0], np.maximum(c, 0)]))[:-1]
+    recs = np.flatnonzero(c > prev)
+    best_count, best_h, needed = 0, -1, max_iters
+    for h in recs.tolist():
+        if h >= needed or h >= max_iters:
+            break                                   # the loop stopped before h
+        cnt = int(c[h])
+        best_count, best_h = cnt, h
+        w = cnt / n
+        if w > 0:
+            with np.errstate(divide="ignore"):
+                denom = np.log(max(1.0 - w ** power, 1e-15))
+                needed = min(max_iters, int(np.ceil(np.log(1.0 - confidence) / denom)))
+    stop = min(needed, max_iters)
+    last = best_h + 1
+    it = max(stop, last) if best_h >= 0 and last > stop else stop
+    if it > evaluated:
+        return best_h, best_count, evaluated, needed, False
+    return best_h, best_count, it, needed, True
+
+
+def _replay_batch(counts, evaluated, n, max_iters, confidence, power=6):
+    """_replay_records for every row of ``counts`` (A, >= evaluated): the record
+    positions of all rows come from one vectorized pass; per row the same scalar
+    numpy expressions run at the records.  Returns, per row, the _replay tuple or
+    "overflow"."""
+    C = np.asarray(counts)[:, :evaluated].astype(np.int64)
+    A = C.shape[0]
+    prev = np.maximum.accumulate(np.concatenate([np.zeros((A, 1), np.int64), np.maximum(C, 0)],
+                                                axis=1), axis=1)[:, :-1]
+    rr, cc = np.nonzero(C > prev)
+    starts = np.searchsorted(rr, np.arange(A + 1))
+    cc_l, cnt_l = cc.tolist(), C[rr, cc].tolist()
+    out = []
+    for k in range(A):
+        nk = int(n[k])
+        best_count, best_h, needed = 0, -1, max_iters
+        try:
+            for j in range(starts[k], starts[k + 1]):
+                h = cc_l[j]
+                if h >= needed or h >= max_iters:
+                    break
+                best_count, best_h = cnt_l[j], h
+                w = best_count / nk
+                if w > 0:
+                    with np.errstate(divide="ignore"):
+                        denom = np.log(max(1.0 - w ** power, 1e-15))
+                        needed = min(max_iters, int(np.ceil(np.log(1.0 - confidence) / denom)))
+        except OverflowError:
+            out.append("overflow")
+            continue
+        stop = min(needed, max_iters)
+        last = best_h + 1
+        it = max(stop, last) if best_h >= 0 and last > stop else stop
+        if it > evaluated:
+            out.append((best_h, best_count, evaluated, needed, False))
+        else:
+            out.append((best_h, best_count, it, needed, True))
+    return out
+
+
 class _Batch:
-    def __init__(self, dev, X_list, uv_list, K_list):
+    def __init__(self, dev, X_list, uv_list, K_list, flat=None):
+        """Correspondences of many images as one device batch: per-image lists, or
+        ``flat`` = (X (N,3), uv (N,2), offsets (B+1,)) already concatenated."""
         import torch
 
-        self.n = np.array([len(x) for x in X_list], dtype=np.int64)
-        off = np.zeros(len(X_list) + 1, np.int64)
-        np.cumsum(self.n, out=off[1:])
+        if flat is not None:
+            X, uv, off = flat
+            off = np.asarray(off, np.int64)
+            self.n = np.diff(off)
+        else:
+            self.n = np.array([len(x) for x in X_list], dtype=np.int64)
+            off = np.zeros(len(X_list) + 1, np.int64)
+            np.cumsum(self.n, out=off[1:])
+            X = np.concatenate([np.asarray(x, np.float64).reshape(-1, 3) for x in X_list]) \
+                if len(X_list) else np.zeros((0, 3))
+            uv = np.concatenate([np.asarray(u, np.float64).reshape(-1, 2) for u in uv_list]) \
+                if len(uv_list) else np.zeros((0, 2))
         self.off_h = off
-        X = np.concatenate([np.asarray(x, np.float64).reshape(-1, 3) for x in X_list]) \
-            if len(X_list) else np.zeros((0, 3))
-        uv = np.concatenate([np.asarray(u, np.float64).reshape(-1, 2) for u in uv_list]) \
-            if len(uv_list) else np.zeros((0, 2))
         K = np.stack([np.asarray(k, np.float64).reshape(9) for k in K_list]) \
             if len(K_list) else np.zeros((0, 9))
 
-        def up(a):
+        def up(a, cols):
+            if isinstance(a, torch.Tensor):          # already on the device (e.g. gathered there)
+                a = a.to(device=dev, dtype=torch.float64).reshape(-1, cols).contiguous()
+                return a if a.numel() else torch.zeros((1, cols), dtype=torch.float64, device=dev)
+            a = np.ascontiguousarray(a, np.float64).reshape(-1, cols)
+            if a.size == 0:
+                a = np.zeros((1, cols), a.dtype)
+            return torch.from_numpy(a).pin_memory().to(dev, non_blocking=True)
+
+        def up_i(a):
             a = np.ascontiguousarray(a)
             if a.size == 0:
                 a = np.zeros(1, a.dtype)
             return torch.from_numpy(a).pin_memory().to(dev, non_blocking=True)
 
-        self.X, self.uv, self.off, self.K = up(X), up(uv), up(off), up(K)
+        self.X, self.uv = up(X, 3), up(uv, 2)
+        self.off, self.K = up_i(off), up_i(K)
+
+    def subset(self, dev, rows, K_list):
+        import torch
+
+        sel = np.concatenate([np.arange(self.off_h[k], self.off_h[k + 1]) for k in rows]) \
+            if len(rows) else np.zeros(0, np.int64)
+        off = np.zeros(len(rows) + 1, np.int64)
+        np.cumsum(self.n[rows], out=off[1:])
+        d_sel = torch.from_numpy(sel).to(dev)
+        return _Batch(dev, None, None, K_list, flat=(self.X[d_sel], self.uv[d_sel], off))
+
+
+def pnp_batch_flat(X, uv, off, K_list, seeds, **kw):
+    """pnp_batch over concatenated correspondences: image k owns rows
+    [off[k], off[k+1]) of X (N,3) and uv (N,2)."""
+    return pnp_batch(None, None, K_list, seeds, flat=(X, uv, off), **kw)
 
 
 def pnp_batch(X_list, uv_list, K_list, seeds, *, threshold=PNP_THRESHOLD_PX,
               min_inliers=PNP_MIN_INLIERS, max_iters=PNP_MAX_ITERS,
-              confidence=PNP_CONFIDENCE, device=None, stream=None, first_round=FIRST_ROUND):
+              confidence=PNP_CONFIDENCE, device=None, stream=None, first_round=FIRST_ROUND,
+              flat=None):
     """pnp_ransac for many images; returns a PnpResult per image.  Images with
     fewer than 6 correspondences get status "insufficient" (the reference raises
     InsufficientDataError there)."""
@@ -90,16 +190,25 @@ def pnp_batch(X_list, uv_list, K_list, seeds, *, threshold=PNP_THRESHOLD_PX,
 
     lib = _lib.load()
     dev = torch.device(device or "cuda")
-    B = len(X_list)
+    if flat is not None:
+        sizes = np.diff(np.asarray(flat[2], np.int64))
+    else:
+        sizes = np.array([len(x) for x in X_list], np.int64)
+    B = len(sizes)
     results = [None] * B
-    active = [i for i in range(B) if len(X_list[i]) >= 6]
+    active = [i for i in range(B) if sizes[i] >= 6]
     for i in range(B):
-        if len(X_list[i]) < 6:
+        if sizes[i] < 6:
             results[i] = PnpResult("insufficient")
     if not active:
         return results
-    batch = _Batch(dev, [X_list[i] for i in active], [uv_list[i] for i in active],
-                   [K_list[i] for i in active])
+    if flat is not None:
+        full = _Batch(dev, None, None, K_list, flat=flat) if len(active) == B else None
+        batch = full if full is not None else \
+            _Batch(dev, None, None, [], flat=flat).subset(dev, active, [K_list[i] for i in active])
+    else:
+        batch = _Batch(dev, [X_list[i] for i in active], [uv_list[i] for i in active],
+                       [K_list[i] for i in active])
     st = _lib.stream_handle(stream)
     A = len(active)
     H1 = min(max_iters, first_round)
@@ -118,18 +227,8 @@ def pnp_batch(X_list, uv_list, K_list, seeds, *, threshold=PNP_THRESHOLD_PX,
     # hypotheses stay on the device; only the inlier counts come back for the replay
     d_hyp1, c1 = _score(lib, batch, samples, H1, threshold, st, dev)
     counts[:, :H1] = c1
-    best = [None] * A
-    pending = []
-    for k in range(A):
-        try:
-            r = _replay(counts[k], H1, int(batch.n[k]), max_iters, confidence)
-        except OverflowError:
-            best[k] = "overflow"
-            continue
-        if r[4]:
-            best[k] = r
-        else:
-            pending.append(k)
+    best = _replay_batch(counts, H1, batch.n, max_iters, confidence)
+    pending = [k for k in range(A) if best[k] != "overflow" and not best[k][4]]
     d_hyp2 = None
     if pending:
         # second round: continue each stream up to the current `needed` bound
@@ -141,17 +240,11 @@ def pnp_batch(X_list, uv_list, K_list, seeds, *, threshold=PNP_THRESHOLD_PX,
             _lib.check(lib.msfm_ransac_samples(words.ctypes.data, int(st6[4]), int(st6[5]),
                                                int(batch.n[k]), 6, H2, samples2[j].ctypes.data,
                                                None), "msfm_ransac_samples")
-        sub = _Batch(dev, [np.asarray(X_list[active[k]]) for k in pending],
-                     [np.asarray(uv_list[active[k]]) for k in pending],
-                     [K_list[active[k]] for k in pending])
+        sub = batch.subset(dev, pending, [K_list[active[k]] for k in pending])
         d_hyp2, c2 = _score(lib, sub, samples2, H2, threshold, st, dev)
-        for j, k in enumerate(pending):
-            counts[k, H1:] = c2[j]
-            try:
-                r = _replay(counts[k], max_iters, int(batch.n[k]), max_iters, confidence)
-            except OverflowError:
-                best[k] = "overflow"
-                continue
+        counts[pending, H1:] = c2
+        for k, r in zip(pending, _replay_batch(counts[pending], max_iters, batch.n[pending],
+                                               max_iters, confidence)):
             best[k] = r
     # refit the winners: gather each winning hypothesis on the device
     import torch

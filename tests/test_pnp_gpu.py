@@ -58,3 +58,28 @@ def test_insufficient_raises():
 
     with pytest.raises(InsufficientDataError):
         pnp_ransac(np.zeros((5, 3)), np.zeros((5, 2)), np.eye(3))
+
+
+def test_flat_batch_equals_list_batch():
+    """pnp_batch_flat (concatenated correspondences) == pnp_batch (lists), incl.
+    images under the 6-correspondence floor."""
+    import os
+
+    from golden_io import GOLDEN
+    from paper_1512_06235_b200.pnp import pnp_batch, pnp_batch_flat
+
+    z = np.load(os.path.join(GOLDEN, "pnp_cases.npz"))
+    ks = list(range(int(z["n_cases"])))
+    X = [z[f"c{k}_X"] for k in ks] + [z["c0_X"][:4]]
+    uv = [z[f"c{k}_uv"] for k in ks] + [z["c0_uv"][:4]]
+    K = [z[f"c{k}_K"] for k in ks] + [z["c0_K"]]
+    seeds = [int(z[f"c{k}_seed"]) for k in ks] + [1]
+    a = pnp_batch(X, uv, K, seeds)
+    off = np.zeros(len(X) + 1, np.int64)
+    np.cumsum([len(x) for x in X], out=off[1:])
+    b = pnp_batch_flat(np.concatenate(X), np.concatenate(uv), off, K, seeds)
+    for ra, rb in zip(a, b):
+        assert ra.status == rb.status
+        if ra.status == "ok":
+            np.testing.assert_array_equal(ra.mask, rb.mask)
+            np.testing.assert_array_equal(ra.R, rb.R)

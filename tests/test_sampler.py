@@ -86,3 +86,51 @@ def test_batched_seeded_samples(size):
         s = rng.bit_generator.state
         assert int(st[i, 0]) == s["state"]["state"] >> 64
         assert int(st[i, 4]) == s["has_uint32"]
+
+
+def test_record_replay_equals_loop_replay():
+    """The record-only replay of the RANSAC stopping rule equals the literal loop
+    (reconstruct.py:190-211 / geometry.py:176-191), OverflowError included."""
+    from paper_1512_06235_b200.pnp import _replay, _replay_records
+
+    rng = np.random.default_rng(0)
+    for _ in range(3000):
+        H = int(rng.choice([8, 64, 256, 2048]))
+        n = int(rng.integers(6, 3000))
+        mode = int(rng.integers(0, 3))
+        if mode == 0:
+            c = rng.integers(-1, n + 1, size=H)
+        elif mode == 1:
+            c = rng.integers(0, max(2, n // 50), size=H)
+        else:
+            c = np.sort(rng.integers(-1, n + 1, size=H))
+        ev = int(rng.integers(1, H + 1))
+        power = int(rng.choice([6, 8]))
+        out = []
+        for f in (_replay, _replay_records):
+            try:
+                out.append(f(c, ev, n, H, 0.999, power))
+            except OverflowError:
+                out.append("overflow")
+        assert out[0] == out[1]
+
+
+def test_batched_replay_equals_loop_replay():
+    from paper_1512_06235_b200.pnp import _replay, _replay_batch
+
+    rng = np.random.default_rng(1)
+    for _ in range(60):
+        A, H = int(rng.integers(1, 40)), int(rng.choice([64, 256, 2048]))
+        n = rng.integers(6, 3000, size=A)
+        C = np.where(rng.random((A, H)) < 0.5, rng.integers(-1, 5, size=(A, H)),
+                     rng.integers(-1, 3000, size=(A, H)))
+        C = np.minimum(C, n[:, None])
+        ev = int(rng.integers(1, H + 1))
+        power = int(rng.choice([6, 8]))
+        got = _replay_batch(C, ev, n, H, 0.999, power)
+        for k in range(A):
+            try:
+                want = _replay(C[k], ev, int(n[k]), H, 0.999, power)
+            except OverflowError:
+                want = "overflow"
+            assert got[k] == want
