@@ -415,9 +415,15 @@ def localize_images(model, graph, image_ids, feature_store, intrinsics, *, cover
             methods[i] = "ranked2d2d"
         corr_lists[i] = corr
     todo = [i for i in image_ids if len(corr_lists[i]) > min_correspondences]
-    X = [np.stack([model.points[p].position for p, _ in corr_lists[i]]) for i in todo]
-    uv = [np.stack([feature_store.sets[i].xy[f] for _, f in corr_lists[i]]).astype(np.float64)
-          for i in todo]
+    # positions of every point once, then vectorized gathers per image
+    pids_all = np.asarray(sorted({p for i in todo for p, _ in corr_lists[i]}), np.int64)
+    pos_all = np.stack([model.points[int(p)].position for p in pids_all]) if len(pids_all) \
+        else np.zeros((0, 3))
+    X, uv = [], []
+    for i in todo:
+        c = np.asarray(corr_lists[i], np.int64).reshape(-1, 2)
+        X.append(pos_all[np.searchsorted(pids_all, c[:, 0])])
+        uv.append(np.asarray(feature_store.sets[i].xy)[c[:, 1]].astype(np.float64))
     res = pnp_batch(X, uv, [intrinsics[i] for i in todo], [seed + i for i in todo],
                     threshold=pnp_threshold, min_inliers=pnp_min_inliers) if todo else []
     pnp = dict(zip(todo, res))
