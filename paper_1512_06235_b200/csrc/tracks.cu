@@ -34,6 +34,7 @@ struct MergeArgs {
     int32_t* fresh_cnt; int32_t* fresh; int32_t* seg_idx; int32_t* seg_off; int32_t* fill;
     unsigned long long* hkey; unsigned long long* hval; int64_t hmask;
     int32_t* out_node; int32_t* seg_owner; int64_t* seg_off_out; int64_t* counts;
+    int32_t* tmp_node;           // scratch for the segment sort (2 * n_edges)
 };
 
 __device__ __forceinline__ int find_root(int32_t* parent, int x) {
@@ -226,18 +227,25 @@ __global__ void merge_emit_kernel(MergeArgs a) {
     }
 }
 
-// ascending node order inside every segment (segments are short: one node per image)
+// ascending node order inside every segment (one node per image: short segments):
+// one warp per segment, every element placed at its rank (node ids are distinct)
 __global__ void merge_sort_kernel(MergeArgs a) {
     const int64_t nseg = a.counts[0];
-    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg;
-         s += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t s = w0; s < nseg; s += nw) {
         const int64_t b = a.seg_off_out[s], e = a.seg_off_out[s + 1];
-        for (int64_t i = b + 1; i < e; i++) {
-            const int x = a.out_node[i];
-            int64_t j = i - 1;
-            while (j >= b && a.out_node[j] > x) { a.out_node[j + 1] = a.out_node[j]; j--; }
-            a.out_node[j + 1] = x;
+        const int L = (int)(e - b);
+        for (int i = lane; i < L; i += 32) {
+            const int x = a.out_node[b + i];
+            int r = 0;
+            for (int j = 0; j < L; j++) r += a.out_node[b + j] < x;
+            a.tmp_node[b + r] = x;
         }
+        __syncwarp();
+        for (int i = lane; i < L; i += 32) a.out_node[b + i] = a.tmp_node[b + i];
+        __syncwarp();
     }
 }
 
@@ -292,7 +300,8 @@ extern "C" size_t msfm_merge_workspace_bytes(int64_t n_nodes, int64_t n_edges) {
     const int64_t n = n_nodes > 0 ? n_nodes : 1;
     const int64_t nb = (n + SCAN_T * SCAN_PER - 1) / (SCAN_T * SCAN_PER) + 1;
     return aligned_bytes<int32_t>(n) * 10 + aligned_bytes<int32_t>(nb) +
-           aligned_bytes<unsigned long long>(hash_size(n_edges)) * 2 + 4096;
+           aligned_bytes<unsigned long long>(hash_size(n_edges)) * 2 +
+           aligned_bytes<int32_t>(2 * (n_edges > 0 ? n_edges : 1)) + 4096;
 }
 
 extern "C" int msfm_merge_tracks(const msfm_bank* bank, int64_t n_edges, const int32_t* d_u,
@@ -333,6 +342,7 @@ extern "C" int msfm_merge_tracks(const msfm_bank* bank, int64_t n_edges, const i
     const int64_t hs = hash_size(n_edges);
     a.hkey = ar.take<unsigned long long>(hs); a.hval = ar.take<unsigned long long>(hs);
     a.hmask = hs - 1;
+    a.tmp_node = ar.take<int32_t>(2 * (n_edges > 0 ? n_edges : 1));
     a.out_node = d_out_node; a.seg_owner = d_seg_owner; a.seg_off_out = d_seg_off; a.counts = d_counts;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
