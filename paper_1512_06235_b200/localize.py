@@ -37,8 +37,13 @@ class PointSet:
 
     @property
     def SS(self) -> np.ndarray:
-        S = self.S.astype(np.int64)
-        return (S * S).sum(1)
+        """|S|^2 per point (int64), computed once."""
+        ss = self.__dict__.get("_ss")
+        if ss is None or len(ss) != len(self.S):
+            S = self.S.astype(np.int64)
+            ss = (S * S).sum(1)
+            self.__dict__["_ss"] = ss
+        return ss
 
 
 def points_from_snapshot(scene_sets, snap, ids=None) -> PointSet:
