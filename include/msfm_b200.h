@@ -233,6 +233,14 @@ int msfm_knn2_tracks(const msfm_bank* bank, int32_t n_points, const int32_t* d_S
                      int32_t max_track, int32_t max_image_features, int32_t* d_k1, int32_t* d_i1,
                      int32_t* d_k2, void* d_workspace, size_t workspace_bytes, void* stream);
 
+/* Index of the second neighbour of msfm_knn2_tracks' output (the lowest feature
+ * index other than i1 whose key equals k2, descriptors.py:61-63), -1 when there
+ * is none: d_i2 [n_images][n_points rounded up to 128]. */
+int msfm_knn2_second_index(const msfm_bank* bank, int32_t n_points, const int32_t* d_S,
+                           const int32_t* d_n, int32_t n_images, const int32_t* d_images,
+                           const int32_t* d_k1, const int32_t* d_i1, const int32_t* d_k2,
+                           int32_t* d_i2, void* stream);
+
 /* direct_3d2d_search post-processing (localize.py:108-122 + ratio_filter
  * matching.py:82-103) on the knn2 output: ratio test sqrt(N_b/N_s) < p/q
  * evaluated exactly (q^2 N_b < p^2 N_s), single-feature images: sqrt(N_b)/n <

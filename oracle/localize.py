@@ -47,6 +47,31 @@ def knn2_exact(S, n, F):
     return best.astype(np.int64), nb, ns
 
 
+def two_nearest(Q, T):
+    """(dist f64 (n,2), idx i64 (n,2)) of descriptors.py:35-72 for integer-valued
+    descriptors: integer squared distances (exact, as the reference's f32 BLAS
+    form is for uint8 rows), argmin with the lowest index winning, the best
+    column masked for the second, dist = sqrt in f32; +inf / -1 with one target."""
+    Q = np.asarray(Q, np.int64).reshape(-1, 128)
+    T = np.asarray(T, np.int64).reshape(-1, 128)
+    nq, nt = len(Q), len(T)
+    dist = np.full((nq, 2), np.inf)
+    idx = np.full((nq, 2), -1, dtype=np.int64)
+    if nq == 0 or nt == 0:
+        return dist, idx
+    d2 = (Q * Q).sum(1)[:, None] + (T * T).sum(1)[None, :] - 2 * (Q @ T.T)
+    rows = np.arange(nq)
+    best = np.argmin(d2, axis=1)
+    dist[:, 0] = np.sqrt(d2[rows, best].astype(np.float32))
+    idx[:, 0] = best
+    if nt > 1:
+        d2[rows, best] = np.iinfo(np.int64).max
+        second = np.argmin(d2, axis=1)
+        dist[:, 1] = np.sqrt(d2[rows, second].astype(np.float32))
+        idx[:, 1] = second
+    return dist, idx
+
+
 def ratio_pq(ratio: float):
     f = Fraction(ratio).limit_denominator(1 << 20)
     return f.numerator, f.denominator

@@ -507,6 +507,44 @@ __global__ void __launch_bounds__(1024) direct_compact_kernel(DirectArgs a) {
     if (threadIdx.x == 0) a.cnt_out[s] = carry;
 }
 
+// index of the second neighbour (lowest feature index with key == k2, other than
+// i1): one warp per (query image slot, point), lanes over features, early exit
+__global__ void knn_second_kernel(const uint8_t* __restrict__ desc, const int32_t* __restrict__ fnorm,
+                                  const int64_t* __restrict__ img_off, const int32_t* __restrict__ img_n,
+                                  const int32_t* __restrict__ images, int n_img, int M, int M_pad,
+                                  const int32_t* __restrict__ S, const int32_t* __restrict__ n,
+                                  const int32_t* __restrict__ k1, const int32_t* __restrict__ i1,
+                                  const int32_t* __restrict__ k2, int32_t* __restrict__ i2) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= n_img * M) return;
+    const int s = warp / M, r = warp - s * M;
+    const int64_t o = (int64_t)s * M_pad + r;
+    const int want = k2[o], best = i1[o];
+    if (lane == 0) i2[o] = -1;
+    if (best < 0 || want == INT_BIG) return;
+    const int img = images[s];
+    const int64_t off = img_off[img];
+    const int nf = img_n[img];
+    const int np = n[r];
+    const int32_t* Sr = S + (int64_t)r * 128;
+    for (int f0 = 0; f0 < nf; f0 += 32) {
+        const int f = f0 + lane;
+        bool hit = false;
+        if (f < nf && f != best) {
+            const uint8_t* d = desc + (off + f) * 128;
+            long long dot = 0;
+            for (int k = 0; k < 128; k++) dot += (long long)Sr[k] * d[k];
+            const long long key = (long long)np * fnorm[off + f] - 2 * dot;
+            hit = (int32_t)key == want;
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, hit);
+        if (b) {
+            if (lane == 0) i2[o] = f0 + __ffs(b) - 1;
+            return;
+        }
+    }
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -551,6 +589,25 @@ extern "C" size_t msfm_knn_workspace_bytes(int32_t n_points, int32_t n_images, i
     const int64_t M_pad = ((int64_t)n_points + TILE_M - 1) / TILE_M * TILE_M;
     return aligned_bytes<uint8_t>(M_pad * 128) * 2 + aligned_bytes<int32_t>(M_pad) +
            aligned_bytes<int32_t>((int64_t)(n_images > 0 ? n_images : 1) * fn_stride_of(max_n)) + 4096;
+}
+
+extern "C" int msfm_knn2_second_index(const msfm_bank* bank, int32_t n_points, const int32_t* d_S,
+                                      const int32_t* d_n, int32_t n_images, const int32_t* d_images,
+                                      const int32_t* d_k1, const int32_t* d_i1, const int32_t* d_k2,
+                                      int32_t* d_i2, void* stream) {
+    if (!bank || n_points < 0 || n_images < 0) {
+        set_error("msfm_knn2_second_index: bad arguments");
+        return MSFM_EINVAL;
+    }
+    if (n_points == 0 || n_images == 0) return MSFM_OK;
+    const int M_pad = (int)(((int64_t)n_points + TILE_M - 1) / TILE_M * TILE_M);
+    const int64_t warps = (int64_t)n_images * n_points;
+    knn_second_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        bank->d_desc, bank->d_norm2, bank->d_img_off, bank->d_img_n, d_images, n_images, n_points,
+        M_pad, d_S, d_n, d_k1, d_i1, d_k2, d_i2);
+    MSFM_LAUNCH_CHECK();
+    count_launches(1);
+    return MSFM_OK;
 }
 
 extern "C" int msfm_direct_3d2d(const msfm_bank* bank, int32_t n_points, const int32_t* d_n,

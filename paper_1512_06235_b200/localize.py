@@ -64,6 +64,7 @@ class DeviceKnn:
     k2: object
     M_pad: int
     keep: tuple = field(default=())
+    i2: object = None          # second neighbour's index (knn2_tracks(second=True))
 
     def host_all(self, pts: PointSet):
         """(idx, N_best, N_second) of every query slot: (S, M) arrays, three copies."""
@@ -91,9 +92,10 @@ class DeviceKnn:
 
 
 def knn2_tracks(bank: FeatureBank, pts: PointSet, image_ids, stream=None,
-                device_points=None, counts=None) -> DeviceKnn:
+                device_points=None, counts=None, second: bool = False) -> DeviceKnn:
     """Top-2 over each image's features; ``counts`` (per bank image, optional)
-    restricts image k to its first counts[k] features (a coarse tier)."""
+    restricts image k to its first counts[k] features (a coarse tier); ``second``
+    also resolves the second neighbour's index (lowest index at the second key)."""
     import torch
 
     lib = _lib.load()
@@ -122,7 +124,15 @@ def knn2_tracks(bank: FeatureBank, pts: PointSet, image_ids, stream=None,
                                     _lib.ptr(d_slots), maxn, max_feat, _lib.ptr(k1), _lib.ptr(i1),
                                     _lib.ptr(k2), _lib.ptr(ws), ws_bytes,
                                     _lib.stream_handle(stream)), "msfm_knn2_tracks")
-    return DeviceKnn(k1, i1, k2, M_pad, keep=(ws, d_slots, d_cnt))
+    out = DeviceKnn(k1, i1, k2, M_pad, keep=(ws, d_slots, d_cnt))
+    if second:
+        out.i2 = torch.empty_like(k1)
+        _lib.check(lib.msfm_knn2_second_index(ctypes.byref(b), M, _lib.ptr(dS), _lib.ptr(dn),
+                                              len(slots), _lib.ptr(d_slots), _lib.ptr(k1),
+                                              _lib.ptr(i1), _lib.ptr(k2), _lib.ptr(out.i2),
+                                              _lib.stream_handle(stream)),
+                   "msfm_knn2_second_index")
+    return out
 
 
 def upload_points(pts: PointSet, dev):
