@@ -41,6 +41,10 @@ def parse():
     p.add_argument("--cpu-pairs", type=int, default=0, help="CPU sample size (0 = auto)")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--chunk-pairs", type=int, default=0)
+    p.add_argument("--segment-images", type=int, default=8,
+                   help="e2e: bank images per staged upload range")
+    p.add_argument("--e2e-resident", action="store_true",
+                   help="e2e: upload + index the whole bank before matching (no staging)")
     p.add_argument("--no-localize", action="store_true")
     return p.parse_args()
 
@@ -202,7 +206,8 @@ def run_b200(args, rank, world):
 
     from paper_1512_06235_b200 import _lib
     from paper_1512_06235_b200.bank import FeatureBank, HostBank
-    from paper_1512_06235_b200.guided import match_pairs, match_pairs_rows, prepare_pairs
+    from paper_1512_06235_b200.guided import (HostPairs, match_pairs, match_pairs_rows,
+                                              match_pairs_rows_staged, prepare_pairs)
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
@@ -273,17 +278,31 @@ def run_b200(args, rank, world):
     h2d = d2h = 0
     pinned = torch.empty((max(int(sum(len(x) for x in ql)), 1), 4), dtype=torch.int32,
                          pin_memory=True)
+    b2 = None
+    hp = HostPairs(host, wl.q_img[mine], wl.t_img[mine], wl.F[mine], ql)   # pinned pair table
     for i in range(args.warmup + args.steps):
         barrier(); torch.cuda.synchronize()
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record()
-        b2 = FeatureBank(host=host, device=dev)
-        b2.grid(D)
-        inp = prepare_pairs(b2, wl.q_img[mine], wl.t_img[mine], wl.F[mine], ql)
-        # matching with each chunk's packed rows copied to pinned memory while the
-        # next chunk computes (msfm_guided_match_rows)
-        rows = match_pairs_rows(b2, wl.q_img[mine], wl.t_img[mine], wl.F[mine], ql,
-                                device_inputs=inp, chunk_pairs=args.chunk_pairs, pinned=pinned)
+        if args.e2e_resident:
+            b2 = FeatureBank(host=host, device=dev)
+            b2.grid(D)
+            inp = prepare_pairs(b2, wl.q_img[mine], wl.t_img[mine], wl.F[mine], ql)
+            # matching with each chunk's packed rows copied to pinned memory while the
+            # next chunk computes (msfm_guided_match_rows)
+            rows = match_pairs_rows(b2, wl.q_img[mine], wl.t_img[mine], wl.F[mine], ql,
+                                    device_inputs=inp, chunk_pairs=args.chunk_pairs,
+                                    pinned=pinned)
+        else:
+            # the bank goes up range by range in the order the chunks need it, each
+            # range indexed as it lands, chunk c starting once its ranges are ready;
+            # packed rows of chunk c copied out while chunk c+1 computes
+            rows, b2 = match_pairs_rows_staged(host, wl.q_img[mine], wl.t_img[mine],
+                                               wl.F[mine], ql, device=dev,
+                                               chunk_pairs=args.chunk_pairs, pinned=pinned,
+                                               segment_images=args.segment_images, bank=b2,
+                                               host_pairs=hp)
+            inp = b2.pair_inputs
         a1.record()
         torch.cuda.synchronize()
         if i >= args.warmup:

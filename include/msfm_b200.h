@@ -119,6 +119,19 @@ int msfm_grid_build(const msfm_bank* bank, const int32_t* d_dims, const int64_t*
                     int32_t* d_cmem, int32_t* d_rrec, int32_t* d_crec, void* d_workspace,
                     size_t workspace_bytes, void* stream);
 
+/* The same for the contiguous image range [img0, img1) only (bucket range
+ * [bucket0, bucket1) = [roff[img0], roff[img1]), first feature row feat0 =
+ * img_off[img0]; d_coff must equal d_roff): lets a bank be indexed range by range
+ * as its rows arrive (staged uploads).  Writes the CSR starts [bucket0, bucket1]
+ * and never rewrites a start another range published.  Ranges built on one stream
+ * share one workspace. */
+int msfm_grid_build_range(const msfm_bank* bank, const int32_t* d_dims, const int64_t* d_roff,
+                          const int64_t* d_coff, int64_t n_buckets_total, int32_t img0,
+                          int32_t img1, int64_t bucket0, int64_t bucket1, int64_t feat0,
+                          double D, int32_t* d_sub, int32_t* d_rstart, int32_t* d_cstart,
+                          int32_t* d_rmem, int32_t* d_cmem, int32_t* d_rrec, int32_t* d_crec,
+                          void* d_workspace, size_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------------------------
  * Geometry-aware (epipolar-guided) matching of a batch of image pairs.
  * Replaces msfm.guided.guided_match_pair(strategy="grid") (guided.py:393-480)
@@ -153,6 +166,8 @@ typedef struct {
                           * 0 grid (cells of the samples, default), 1 linear
                           * (|rep line| <= d, guided.py:190-194), 2 radial (disks of
                           * radius d*sqrt(2) around the samples, guided.py:273-285) */
+    int32_t first_chunk_pairs; /* pairs of the first chunk when > 0 (a short first
+                          * chunk starts matching sooner on a staged bank)       */
 } msfm_match_params;
 
 /* Pack the per-pair segments of msfm_guided_match's output into contiguous
@@ -173,12 +188,40 @@ int msfm_guided_match(const msfm_bank* bank, const msfm_grids* grids, int32_t n_
                       int32_t* d_out_count, int64_t* d_stats,
                       void* d_workspace, size_t workspace_bytes, void* stream);
 
+/* Staged bank for msfm_guided_match_rows: the bank rows of image range r arrive
+ * (uploaded by the caller on its own stream, event landed[r]) while earlier
+ * chunks match; just before chunk chunk[r] the matcher's stream waits on
+ * landed[r] and computes the range's |desc|^2 and spatial index
+ * (msfm_grid_build_range with img0/img1, bucket0/bucket1, feat0), so the index
+ * build never queues behind a running chunk.  chunk[] is non-decreasing. */
+typedef struct {
+    int32_t n_ranges;
+    const int32_t* chunk;
+    const int32_t* img0;
+    const int32_t* img1;
+    const int64_t* bucket0;
+    const int64_t* bucket1;
+    const int64_t* feat0;         /* first bank row of the range */
+    const int64_t* feat1;         /* end bank row of the range */
+    void* const* landed;          /* cudaEvent_t per range, or NULL entries */
+    int64_t n_buckets_total;
+    void* grid_workspace;         /* msfm_grid_workspace_bytes(n_buckets_total) */
+    size_t grid_workspace_bytes;
+} msfm_stage_plan;
+
+/* The matcher's internal chunking: writes the first pair of every chunk and the
+ * end (n_chunks + 1 values, at most `capacity`) and returns n_chunks. */
+int32_t msfm_guided_chunk_bounds(int32_t n_pairs, const int64_t* h_qlist_off,
+                                 const msfm_match_params* prm, int32_t* out_bounds,
+                                 int32_t capacity);
+
 /* msfm_guided_match followed by the packing of msfm_pack_matches, pipelined with
  * the device-to-host copy: after every internal chunk its packed rows are copied
  * on `copy_stream` into the pinned host buffer h_rows (16-B rows, pair order)
  * while the next chunk computes.  Scratch: d_out_off [n_pairs+1], d_rows
  * (4 * total queries int32), d_meta / h_meta (pinned) [2 * (n_pairs + 1)] int64.
- * Returns after the last copy; *h_total = rows written.  No SearchStats. */
+ * Returns after the last copy; *h_total = rows written.  No SearchStats.
+ * plan (optional): the bank is still arriving; see msfm_stage_plan. */
 int msfm_guided_match_rows(const msfm_bank* bank, const msfm_grids* grids, int32_t n_pairs,
                            const int32_t* d_pair_q, const int32_t* d_pair_t,
                            const double* d_pair_F, const int64_t* d_qlist_off,
@@ -188,7 +231,7 @@ int msfm_guided_match_rows(const msfm_bank* bank, const msfm_grids* grids, int32
                            float* d_out_ratio, int32_t* d_out_count, int64_t* d_out_off,
                            int32_t* d_rows, int64_t* d_meta, int64_t* h_meta, int32_t* h_rows,
                            int64_t* h_total, void* d_workspace, size_t workspace_bytes,
-                           void* stream, void* copy_stream);
+                           void* stream, void* copy_stream, const msfm_stage_plan* plan);
 
 /* ------------------------------------------------------------------------
  * Host-only: RANSAC hypothesis sets.  Emits `count` consecutive draws of

@@ -42,7 +42,15 @@ class MsftInfo(ctypes.Structure):
 class MatchParams(ctypes.Structure):
     _fields_ = [("d", ctypes.c_double), ("ratio", ctypes.c_float),
                 ("single_cap", ctypes.c_float), ("max_nt", ctypes.c_int32),
-                ("chunk_pairs", ctypes.c_int32), ("strategy", ctypes.c_int32)]
+                ("chunk_pairs", ctypes.c_int32), ("strategy", ctypes.c_int32),
+                ("first_chunk_pairs", ctypes.c_int32)]
+
+
+class StagePlan(ctypes.Structure):
+    _fields_ = [("n_ranges", ctypes.c_int32), ("chunk", VP), ("img0", VP), ("img1", VP),
+                ("bucket0", VP), ("bucket1", VP), ("feat0", VP), ("feat1", VP),
+                ("landed", VP), ("n_buckets_total", ctypes.c_int64),
+                ("grid_workspace", VP), ("grid_workspace_bytes", ctypes.c_size_t)]
 
 
 _SIGS = {
@@ -59,6 +67,12 @@ _SIGS = {
     "msfm_grid_build": (ctypes.c_int, [ctypes.POINTER(Bank), VP, VP, VP, ctypes.c_int64,
                                        ctypes.c_int64, ctypes.c_double, VP, VP, VP, VP, VP,
                                        VP, VP, VP, ctypes.c_size_t, VP]),
+    "msfm_grid_build_range": (ctypes.c_int, [ctypes.POINTER(Bank), VP, VP, VP, ctypes.c_int64,
+                                             ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
+                                             ctypes.c_int64, ctypes.c_int64, ctypes.c_double, VP,
+                                             VP, VP, VP, VP, VP, VP, VP, ctypes.c_size_t, VP]),
+    "msfm_guided_chunk_bounds": (ctypes.c_int32, [ctypes.c_int32, VP, ctypes.POINTER(MatchParams),
+                                                  VP, ctypes.c_int32]),
     "msfm_ransac_samples": (ctypes.c_int, [VP, ctypes.c_int32, ctypes.c_uint32, ctypes.c_int64,
                                            ctypes.c_int32, ctypes.c_int32, VP, VP]),
     "msfm_msft_load": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(MsftInfo), VP, VP, VP, VP]),
@@ -97,7 +111,8 @@ _SIGS = {
     "msfm_guided_match_rows": (ctypes.c_int, [ctypes.POINTER(Bank), ctypes.POINTER(Grids),
                                               ctypes.c_int32, VP, VP, VP, VP, VP, VP, VP,
                                               ctypes.POINTER(MatchParams), VP, VP, VP, VP, VP,
-                                              VP, VP, VP, VP, VP, VP, VP, ctypes.c_size_t, VP, VP]),
+                                              VP, VP, VP, VP, VP, VP, VP, ctypes.c_size_t, VP, VP,
+                                              ctypes.POINTER(StagePlan)]),
     "msfm_guided_match": (ctypes.c_int, [ctypes.POINTER(Bank), ctypes.POINTER(Grids),
                                          ctypes.c_int32, VP, VP, VP, VP, VP, VP, VP,
                                          ctypes.POINTER(MatchParams), VP, VP, VP, VP, VP, VP,

@@ -17,8 +17,29 @@ import numpy as np
 from . import _lib
 
 
+def _slots(bank, image_ids) -> np.ndarray:
+    ids = np.asarray(image_ids, dtype=np.int64).reshape(-1)
+    if "_ids_sorted" not in bank.__dict__:
+        keys = np.array(bank.image_ids, dtype=np.int64)
+        order = np.argsort(keys, kind="stable")
+        bank.__dict__["_ids_sorted"], bank.__dict__["_ids_order"] = keys[order], order
+    srt, order = bank.__dict__["_ids_sorted"], bank.__dict__["_ids_order"]
+    if len(ids) == 0:
+        return np.zeros(0, np.int64)
+    pos = np.searchsorted(srt, ids)
+    pos_c = np.minimum(pos, max(len(srt) - 1, 0))
+    bad = (pos >= len(srt)) | (srt[pos_c] != ids)
+    if np.any(bad):
+        raise KeyError(int(ids[np.flatnonzero(bad)[0]]))
+    return order[pos_c].astype(np.int64)
+
+
 class HostBank:
     """Concatenated feature arrays in pinned host memory (the H2D staging area)."""
+
+    def slots(self, image_ids) -> np.ndarray:
+        """Bank index of every image id (int64), KeyError for ids not in the bank."""
+        return _slots(self, image_ids)
 
     def __init__(self, feature_sets, image_ids=None):
         import torch
@@ -71,7 +92,11 @@ class HostBank:
 class FeatureBank:
     """Feature sets of many images, resident on one CUDA device."""
 
-    def __init__(self, feature_sets=None, device=None, image_ids=None, stream=None, host=None):
+    def __init__(self, feature_sets=None, device=None, image_ids=None, stream=None, host=None,
+                 staged: bool = False):
+        """``staged``: allocate the device rows without copying them; the caller
+        fills image ranges with ``stage_range`` (and indexes them with
+        ``SpatialIndex.build_range``) on streams of its choice."""
         import torch
 
         lib = _lib.load()
@@ -83,18 +108,49 @@ class FeatureBank:
         self.counts, self.offsets, self.wh = host.counts, host.offsets, host.wh
         self.n_total = int(self.counts.sum())
         dev = self.device
-        self.xy = host.xy.to(dev, non_blocking=True)
-        self.desc = host.desc.to(dev, non_blocking=True)
+        self.host = host
+        if staged:
+            self.xy = torch.empty(tuple(host.xy.shape), dtype=torch.float32, device=dev)
+            self.desc = torch.empty(tuple(host.desc.shape), dtype=torch.uint8, device=dev)
+        else:
+            self.xy = host.xy.to(dev, non_blocking=True)
+            self.desc = host.desc.to(dev, non_blocking=True)
         self.img_off = host.img_off.to(dev, non_blocking=True)
         self.img_n = host.img_n.to(dev, non_blocking=True)
         self.img_wh = host.img_wh.to(dev, non_blocking=True)
         self.norm2 = torch.empty(self.n_total, dtype=torch.int32, device=dev)
-        st = _lib.stream_handle(stream)
-        _lib.check(lib.msfm_feature_norms(_lib.ptr(self.desc), self.n_total,
-                                          _lib.ptr(self.norm2), st), "msfm_feature_norms")
+        self.staged = staged
+        if not staged:
+            st = _lib.stream_handle(stream)
+            _lib.check(lib.msfm_feature_norms(_lib.ptr(self.desc), self.n_total,
+                                              _lib.ptr(self.norm2), st), "msfm_feature_norms")
         self.max_n = int(self.counts.max()) if len(self.counts) else 0
         self._grids = {}
 
+    def slots(self, image_ids) -> np.ndarray:
+        """Bank index of every image id (int64), KeyError for ids not in the bank."""
+        return _slots(self, image_ids)
+
+    def row_range(self, k0: int, k1: int):
+        """Bank rows [a, b) of images [k0, k1)."""
+        a = int(self.offsets[k0]) if k0 < len(self.offsets) else self.n_total
+        b = int(self.offsets[k1]) if k1 < len(self.offsets) else self.n_total
+        return a, b
+
+    def upload_range(self, k0: int, k1: int, copy_stream):
+        """(staged bank) Copy the rows of images [k0, k1) on ``copy_stream``;
+        returns the event that marks them landed.  |desc|^2 and the spatial index
+        of the range are computed by whoever consumes them (msfm_stage_plan)."""
+        import torch
+
+        a, b = self.row_range(k0, k1)
+        if b > a:
+            with torch.cuda.stream(copy_stream):
+                self.xy[a:b].copy_(self.host.xy[a:b], non_blocking=True)
+                self.desc[a:b].copy_(self.host.desc[a:b], non_blocking=True)
+        landed = torch.cuda.Event()
+        landed.record(copy_stream)
+        return landed
     @property
     def h2d_bytes(self) -> int:
         return int(self.xy.numel() * 4 + self.desc.numel() + self.img_off.numel() * 8
@@ -105,17 +161,17 @@ class FeatureBank:
                          _lib.ptr(self.img_off), _lib.ptr(self.img_n), _lib.ptr(self.img_wh),
                          len(self.image_ids), self.n_total)
 
-    def grid(self, D: float, stream=None) -> "SpatialIndex":
+    def grid(self, D: float, stream=None, build: bool = True) -> "SpatialIndex":
         key = float(D)
         if key not in self._grids:
-            self._grids[key] = SpatialIndex(self, key, stream)
+            self._grids[key] = SpatialIndex(self, key, stream, build=build)
         return self._grids[key]
 
 
 class SpatialIndex:
     """Subcell ids + row/column bucket CSR tables of every image (msfm_grid_build)."""
 
-    def __init__(self, bank: FeatureBank, D: float, stream=None):
+    def __init__(self, bank: FeatureBank, D: float, stream=None, build: bool = True):
         import torch
 
         lib = _lib.load()
@@ -147,6 +203,10 @@ class SpatialIndex:
         self.crec = torch.empty((max(bank.n_total, 1), 4), dtype=torch.int32, device=dev)
         ws_bytes = lib.msfm_grid_workspace_bytes(nb)
         ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        self._bank, self._nb, self._roff_h = bank, nb, roff
+        self._ws, self._ws_bytes = ws, ws_bytes
+        if not build:
+            return
         st = _lib.stream_handle(stream)
         b = bank.cstruct()
         _lib.check(lib.msfm_grid_build(ctypes.byref(b), _lib.ptr(self.dims), _lib.ptr(self.roff),
@@ -156,7 +216,30 @@ class SpatialIndex:
                                        _lib.ptr(self.cmem), _lib.ptr(self.rrec),
                                        _lib.ptr(self.crec), _lib.ptr(ws), ws_bytes, st),
                    "msfm_grid_build")
-        self._ws = ws  # keep alive until the stream has consumed it
+
+    def bucket_range(self, k0: int, k1: int):
+        """Bucket rows [b0, b1) of images [k0, k1) (row and column tables alike)."""
+        nimg = len(self._bank.image_ids)
+        b0 = int(self._roff_h[k0]) if k0 < nimg else self._nb
+        b1 = int(self._roff_h[k1]) if k1 < nimg else self._nb
+        return b0, b1
+
+    def build_range(self, k0: int, k1: int, stream=None):
+        """Index bank images [k0, k1) only (their rows must be on the device,
+        in stream order); ranges built on one stream may come in any order."""
+        lib = _lib.load()
+        bank = self._bank
+        b0, b1 = self.bucket_range(k0, k1)
+        f0 = bank.row_range(k0, k1)[0]
+        b = bank.cstruct()
+        _lib.check(lib.msfm_grid_build_range(ctypes.byref(b), _lib.ptr(self.dims),
+                                             _lib.ptr(self.roff), _lib.ptr(self.coff), self._nb,
+                                             k0, k1, b0, b1, f0, self.D, _lib.ptr(self.sub),
+                                             _lib.ptr(self.rstart), _lib.ptr(self.cstart),
+                                             _lib.ptr(self.rmem), _lib.ptr(self.cmem),
+                                             _lib.ptr(self.rrec), _lib.ptr(self.crec),
+                                             _lib.ptr(self._ws), self._ws_bytes,
+                                             _lib.stream_handle(stream)), "msfm_grid_build_range")
 
     def cstruct(self) -> _lib.Grids:
         return _lib.Grids(_lib.ptr(self.sub), _lib.ptr(self.dims), _lib.ptr(self.roff),

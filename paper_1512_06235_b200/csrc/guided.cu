@@ -164,6 +164,7 @@ struct GridBuildArgs {
     const int32_t* dims; const int64_t* roff; const int64_t* coff;
     int32_t* sub; int32_t* rcount; int32_t* ccount; int32_t* rcur; int32_t* ccur;
     int32_t* rmem; int32_t* cmem; int4* rrec; int4* crec; const int32_t* norm2; double D;
+    int img0;             // first image of the range this launch builds (blockIdx.x + img0)
 };
 
 __device__ __forceinline__ int bucket_of(float v, double D, int nb) {
@@ -172,7 +173,7 @@ __device__ __forceinline__ int bucket_of(float v, double D, int nb) {
 }
 
 __global__ void grid_count_kernel(GridBuildArgs a) {
-    const int img = blockIdx.x;
+    const int img = a.img0 + blockIdx.x;
     const int64_t off = a.img_off[img];
     const int n = a.img_n[img];
     const int nbx = a.dims[2 * img], nby = a.dims[2 * img + 1];
@@ -187,7 +188,7 @@ __global__ void grid_count_kernel(GridBuildArgs a) {
 }
 
 __global__ void grid_scatter_kernel(GridBuildArgs a) {
-    const int img = blockIdx.x;
+    const int img = a.img0 + blockIdx.x;
     const int64_t off = a.img_off[img];
     const int n = a.img_n[img];
     const int nbx = a.dims[2 * img], nby = a.dims[2 * img + 1];
@@ -1619,14 +1620,18 @@ extern "C" size_t msfm_grid_workspace_bytes(int64_t n_buckets_total) {
     return aligned_bytes<int32_t>(n_buckets_total + 1) * 2 + aligned_bytes<int32_t>(nb) + 1024;
 }
 
-extern "C" int msfm_grid_build(const msfm_bank* bank, const int32_t* d_dims, const int64_t* d_roff,
-                               const int64_t* d_coff, int64_t n_buckets_total, int64_t n_total,
-                               double D, int32_t* d_sub, int32_t* d_rstart, int32_t* d_cstart,
-                               int32_t* d_rmem, int32_t* d_cmem, int32_t* d_rrec, int32_t* d_crec,
-                               void* d_workspace,
-                               size_t workspace_bytes, void* stream) {
-    if (!bank || !(D > 0) || n_buckets_total < 0 || n_total < 0) {
-        set_error("msfm_grid_build: bad arguments (D=%g)", D);
+extern "C" int msfm_grid_build_range(const msfm_bank* bank, const int32_t* d_dims,
+                                     const int64_t* d_roff, const int64_t* d_coff,
+                                     int64_t n_buckets_total, int32_t img0, int32_t img1,
+                                     int64_t bucket0, int64_t bucket1, int64_t feat0, double D,
+                                     int32_t* d_sub, int32_t* d_rstart, int32_t* d_cstart,
+                                     int32_t* d_rmem, int32_t* d_cmem, int32_t* d_rrec,
+                                     int32_t* d_crec, void* d_workspace, size_t workspace_bytes,
+                                     void* stream) {
+    if (!bank || !(D > 0) || n_buckets_total < 0 || img0 < 0 || img1 < img0 ||
+        img1 > bank->n_images || bucket0 < 0 || bucket1 < bucket0 || bucket1 > n_buckets_total ||
+        feat0 < 0 || feat0 > INT32_MAX) {
+        set_error("msfm_grid_build_range: bad arguments (D=%g, images [%d, %d))", D, img0, img1);
         return MSFM_EINVAL;
     }
     if (workspace_bytes < msfm_grid_workspace_bytes(n_buckets_total)) {
@@ -1639,24 +1644,46 @@ extern "C" int msfm_grid_build(const msfm_bank* bank, const int32_t* d_dims, con
     int32_t* ccur = ar.take<int32_t>(n_buckets_total + 1);
     int64_t nb = (n_buckets_total + 1 + SCAN_T * SCAN_PER - 1) / (SCAN_T * SCAN_PER) + 1;
     int32_t* bsum = ar.take<int32_t>(nb);
-    MSFM_CUDA_TRY(cudaMemsetAsync(d_rstart, 0, sizeof(int32_t) * (n_buckets_total + 1), st));
-    MSFM_CUDA_TRY(cudaMemsetAsync(d_cstart, 0, sizeof(int32_t) * (n_buckets_total + 1), st));
-    if (bank->n_images == 0) return MSFM_OK;
+    // counts go to the cursor arrays; the scan writes the CSR starts [bucket0, bucket1]
+    // (the closing start included, = the next range's first start) without ever
+    // touching a start another range already published
+    const int64_t n = bucket1 - bucket0 + 1;
+    MSFM_CUDA_TRY(cudaMemsetAsync(rcur + bucket0, 0, sizeof(int32_t) * n, st));
+    MSFM_CUDA_TRY(cudaMemsetAsync(ccur + bucket0, 0, sizeof(int32_t) * n, st));
     GridBuildArgs a{reinterpret_cast<const float2*>(bank->d_xy), bank->d_img_off, bank->d_img_n,
-                    bank->d_img_wh, d_dims, d_roff, d_coff, d_sub, d_rstart, d_cstart, rcur, ccur,
+                    bank->d_img_wh, d_dims, d_roff, d_coff, d_sub, rcur, ccur, rcur, ccur,
                     d_rmem, d_cmem, reinterpret_cast<int4*>(d_rrec),
-                    reinterpret_cast<int4*>(d_crec), bank->d_norm2, D};
-    grid_count_kernel<<<bank->n_images, 256, 0, st>>>(a);
-    MSFM_LAUNCH_CHECK();
-    count_launches(1);
-    int rc = exclusive_scan(d_rstart, n_buckets_total + 1, rcur, bsum, st);
+                    reinterpret_cast<int4*>(d_crec), bank->d_norm2, D, img0};
+    if (img1 > img0) {
+        grid_count_kernel<<<img1 - img0, 256, 0, st>>>(a);
+        MSFM_LAUNCH_CHECK();
+        count_launches(1);
+    }
+    int rc = exclusive_scan(rcur + bucket0, n, d_rstart + bucket0, bsum, st, (int32_t)feat0);
     if (rc) return rc;
-    rc = exclusive_scan(d_cstart, n_buckets_total + 1, ccur, bsum, st);
+    rc = exclusive_scan(ccur + bucket0, n, d_cstart + bucket0, bsum, st, (int32_t)feat0);
     if (rc) return rc;
-    grid_scatter_kernel<<<bank->n_images, 256, 0, st>>>(a);
-    MSFM_LAUNCH_CHECK();
-    count_launches(1);
+    if (img1 > img0) {
+        grid_scatter_kernel<<<img1 - img0, 256, 0, st>>>(a);
+        MSFM_LAUNCH_CHECK();
+        count_launches(1);
+    }
     return MSFM_OK;
+}
+
+extern "C" int msfm_grid_build(const msfm_bank* bank, const int32_t* d_dims, const int64_t* d_roff,
+                               const int64_t* d_coff, int64_t n_buckets_total, int64_t n_total,
+                               double D, int32_t* d_sub, int32_t* d_rstart, int32_t* d_cstart,
+                               int32_t* d_rmem, int32_t* d_cmem, int32_t* d_rrec, int32_t* d_crec,
+                               void* d_workspace,
+                               size_t workspace_bytes, void* stream) {
+    if (!bank || !(D > 0) || n_buckets_total < 0 || n_total < 0) {
+        set_error("msfm_grid_build: bad arguments (D=%g)", D);
+        return MSFM_EINVAL;
+    }
+    return msfm_grid_build_range(bank, d_dims, d_roff, d_coff, n_buckets_total, 0, bank->n_images,
+                                 0, n_buckets_total, 0, D, d_sub, d_rstart, d_cstart, d_rmem,
+                                 d_cmem, d_rrec, d_crec, d_workspace, workspace_bytes, stream);
 }
 
 static void plan_chunks(int32_t n_pairs, const int64_t* h_qlist_off, const msfm_match_params* prm,
@@ -1671,7 +1698,8 @@ static void plan_chunks(int32_t n_pairs, const int64_t* h_qlist_off, const msfm_
     bounds.push_back(0);
     while (p < n_pairs) {
         int e = p + 1;
-        while (e < n_pairs && e - p < cp && h_qlist_off[e + 1] - h_qlist_off[p] <= qmax) e++;
+        const int cap = (p == 0 && prm->first_chunk_pairs > 0) ? std::min(cp, prm->first_chunk_pairs) : cp;
+        while (e < n_pairs && e - p < cap && h_qlist_off[e + 1] - h_qlist_off[p] <= qmax) e++;
         ChunkSizes c;
         c.P = e - p;
         c.Q = h_qlist_off[e] - h_qlist_off[p];
@@ -1684,6 +1712,19 @@ static void plan_chunks(int32_t n_pairs, const int64_t* h_qlist_off, const msfm_
         bounds.push_back(e);
         p = e;
     }
+}
+
+extern "C" int32_t msfm_guided_chunk_bounds(int32_t n_pairs, const int64_t* h_qlist_off,
+                                            const msfm_match_params* prm, int32_t* out_bounds,
+                                            int32_t capacity) {
+    if (!prm || !h_qlist_off || n_pairs < 0) return -1;
+    std::vector<int> bounds;
+    ChunkSizes w;
+    plan_chunks(n_pairs, h_qlist_off, prm, bounds, w);
+    const int32_t nc = (int32_t)bounds.size() - 1;
+    if (out_bounds)
+        for (int32_t k = 0; k <= nc && k < capacity; k++) out_bounds[k] = bounds[k];
+    return nc < 0 ? 0 : nc;
 }
 
 extern "C" size_t msfm_guided_workspace_bytes(int32_t n_pairs, const int64_t* h_qlist_off,
@@ -1706,7 +1747,8 @@ static int guided_match_impl(const msfm_bank* bank, const msfm_grids* grids, int
                              const msfm_match_params* prm, int32_t* d_out_q, int32_t* d_out_t,
                              float* d_out_dist, float* d_out_ratio, int32_t* d_out_count,
                              int64_t* d_stats, void* d_workspace, size_t workspace_bytes,
-                             void* stream, ChunkHookFn hook, void* hook_ctx) {
+                             void* stream, ChunkHookFn hook, void* hook_ctx,
+                             const msfm_stage_plan* plan = nullptr) {
     if (!bank || !grids || !prm || n_pairs < 0 || !h_qlist_off) {
         set_error("msfm_guided_match: null argument");
         return MSFM_EINVAL;
@@ -1794,12 +1836,41 @@ static int guided_match_impl(const msfm_bank* bank, const msfm_grids* grids, int
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     MSFM_CUDA_TRY(cudaFuncSetAttribute(groups_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        2 * 65536 + 16));
+    int next_range = 0;
     for (size_t c = 0; c + 1 < bounds.size(); c++) {
         const int p0 = bounds[c], p1 = bounds[c + 1];
         a.p0 = p0;
         a.npairs = p1 - p0;
         a.qbase = h_qlist_off[p0];
         const int64_t Q = h_qlist_off[p1] - h_qlist_off[p0];
+        // bank ranges first read by this chunk: wait for their rows, then index them
+        for (; plan && next_range < plan->n_ranges && plan->chunk[next_range] <= (int32_t)c;
+             next_range++) {
+            const int r = next_range;
+            if (plan->landed && plan->landed[r])
+                MSFM_CUDA_TRY(cudaStreamWaitEvent(st, (cudaEvent_t)plan->landed[r], 0));
+            const int64_t f0 = plan->feat0[r], f1 = plan->feat1[r];
+            const int i1 = plan->img1[r];
+            if (f1 < f0 || f1 > bank->n_total) {
+                set_error("msfm_guided_match_rows: stage range %d rows [%lld, %lld)", r,
+                          (long long)f0, (long long)f1);
+                return MSFM_EINVAL;
+            }
+            // a plan hands the matcher the (otherwise read-only) |desc|^2 and index
+            // arrays of its ranges to fill
+            auto w32 = [](const int32_t* p) { return const_cast<int32_t*>(p); };
+            int rc = msfm_feature_norms(bank->d_desc + 128 * f0, f1 - f0,
+                                        w32(bank->d_norm2) + f0, st);
+            if (rc) return rc;
+            rc = msfm_grid_build_range(bank, grids->d_dims, grids->d_roff, grids->d_coff,
+                                       plan->n_buckets_total, plan->img0[r], i1,
+                                       plan->bucket0[r], plan->bucket1[r], f0, grids->D,
+                                       w32(grids->d_sub), w32(grids->d_rstart),
+                                       w32(grids->d_cstart), w32(grids->d_rmem),
+                                       w32(grids->d_cmem), w32(grids->d_rrec), w32(grids->d_crec),
+                                       plan->grid_workspace, plan->grid_workspace_bytes, st);
+            if (rc) return rc;
+        }
         plan_kernel<<<1, SCAN_T, 0, st>>>(a);
         { ProfScope ps("lines_kernel", st); lines_kernel<<<a.npairs, MSFM_LINES_T, 0, st>>>(a); }
         {
@@ -1902,7 +1973,8 @@ extern "C" int msfm_guided_match_rows(const msfm_bank* bank, const msfm_grids* g
                                       int32_t* d_out_count, int64_t* d_out_off, int32_t* d_rows,
                                       int64_t* d_meta, int64_t* h_meta, int32_t* h_rows,
                                       int64_t* h_total, void* d_workspace,
-                                      size_t workspace_bytes, void* stream, void* copy_stream) {
+                                      size_t workspace_bytes, void* stream, void* copy_stream,
+                                      const msfm_stage_plan* plan) {
     if (!d_out_off || !d_rows || !d_meta || !h_meta || !h_rows || !h_total || !copy_stream) {
         set_error("msfm_guided_match_rows: null argument");
         return MSFM_EINVAL;
@@ -1917,7 +1989,7 @@ extern "C" int msfm_guided_match_rows(const msfm_bank* bank, const msfm_grids* g
     int rc = guided_match_impl(bank, grids, n_pairs, d_pair_q, d_pair_t, d_pair_F, d_qlist_off,
                                d_qlist, d_qlist_src, h_qlist_off, prm, d_out_q, d_out_t,
                                d_out_dist, d_out_ratio, d_out_count, nullptr, d_workspace,
-                               workspace_bytes, stream, rows_hook, &x);
+                               workspace_bytes, stream, rows_hook, &x, plan);
     if (rc == MSFM_OK && !x.ev.empty()) rc = rows_flush(x, (int)x.ev.size() - 1);
     if (rc == MSFM_OK) {
         cudaError_t e = cudaStreamSynchronize(x.copy);

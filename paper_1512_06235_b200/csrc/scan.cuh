@@ -65,7 +65,8 @@ __global__ void scan_bsum_kernel(int32_t* bsum, int64_t nb) {
     }
 }
 
-__global__ void scan_apply_kernel(int32_t* data, int64_t n, const int32_t* bsum, int32_t* copy) {
+__global__ void scan_apply_kernel(int32_t* data, int64_t n, const int32_t* bsum, int32_t* copy,
+                                  int32_t base0) {
     __shared__ int sm[SCAN_T / 32 + 1];
     int64_t base = (int64_t)blockIdx.x * SCAN_T * SCAN_PER;
     int v[SCAN_PER];
@@ -77,7 +78,7 @@ __global__ void scan_apply_kernel(int32_t* data, int64_t n, const int32_t* bsum,
         s += v[k];
     }
     int total;
-    int ex = block_exclusive_scan<SCAN_T>(s, &total, sm) + bsum[blockIdx.x];
+    int ex = block_exclusive_scan<SCAN_T>(s, &total, sm) + bsum[blockIdx.x] + base0;
 #pragma unroll
     for (int k = 0; k < SCAN_PER; k++) {
         int64_t i = base + (int64_t)threadIdx.x * SCAN_PER + k;
@@ -89,12 +90,14 @@ __global__ void scan_apply_kernel(int32_t* data, int64_t n, const int32_t* bsum,
     }
 }
 
-int exclusive_scan(int32_t* data, int64_t n, int32_t* copy, int32_t* bsum, cudaStream_t st) {
+// exclusive prefix sums of data[0, n) in place (+ base0), mirrored into copy if given
+int exclusive_scan(int32_t* data, int64_t n, int32_t* copy, int32_t* bsum, cudaStream_t st,
+                   int32_t base0 = 0) {
     int64_t nb = (n + SCAN_T * SCAN_PER - 1) / (SCAN_T * SCAN_PER);
     if (nb == 0) return MSFM_OK;
     scan_tiles_kernel<<<(unsigned)nb, SCAN_T, 0, st>>>(data, n, bsum);
     scan_bsum_kernel<<<1, SCAN_T, 0, st>>>(bsum, nb);
-    scan_apply_kernel<<<(unsigned)nb, SCAN_T, 0, st>>>(data, n, bsum, copy);
+    scan_apply_kernel<<<(unsigned)nb, SCAN_T, 0, st>>>(data, n, bsum, copy, base0);
     MSFM_LAUNCH_CHECK();
     count_launches(3);
     return MSFM_OK;

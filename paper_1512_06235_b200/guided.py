@@ -139,11 +139,13 @@ def match_pairs_rows(bank: FeatureBank, q_img, t_img, F, query_lists, *, d: floa
                      ratio: float = RATIO_GUIDED, inflation: float = GRID_INFLATION,
                      grid_d: float | None = None, single_cap: float = SINGLE_CANDIDATE_CAP,
                      chunk_pairs: int = 0, stream=None, device_inputs=None,
-                     strategy: str = "grid", pinned=None):
+                     strategy: str = "grid", pinned=None, stage_plan=None,
+                     first_chunk_pairs: int = 0):
     """``match_pairs`` + packing + one pinned host copy per internal chunk, the
     copy of chunk c overlapping the compute of chunk c+1 (msfm_guided_match_rows).
     Returns the host rows as a MATCH_ROW structured array (a view of ``pinned``
-    when given: int32 (>= total queries, 4), pinned)."""
+    when given: int32 (>= total queries, 4), pinned).  ``stage_plan``: the bank
+    is still arriving (see match_pairs_rows_staged)."""
     import torch
 
     lib = _lib.load()
@@ -163,7 +165,8 @@ def match_pairs_rows(bank: FeatureBank, q_img, t_img, F, query_lists, *, d: floa
         return np.zeros(0, MATCH_ROW)
     grid = bank.grid(D, stream)
     prm = _lib.MatchParams(float(d), float(np.float32(ratio)), float(np.float32(single_cap)),
-                           max(bank.max_n, 1), int(chunk_pairs), STRATEGIES[strategy])
+                           max(bank.max_n, 1), int(chunk_pairs), STRATEGIES[strategy],
+                           int(first_chunk_pairs))
     qoff_c = np.ascontiguousarray(qoff, dtype=np.int64)
     ws_bytes = lib.msfm_guided_workspace_bytes(P, qoff_c.ctypes.data, ctypes.byref(prm))
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
@@ -190,9 +193,184 @@ def match_pairs_rows(bank: FeatureBank, q_img, t_img, F, query_lists, *, d: floa
                                           _lib.ptr(out_off), _lib.ptr(d_rows), _lib.ptr(d_meta),
                                           h_meta.data_ptr(), pinned.data_ptr(), ctypes.byref(total),
                                           _lib.ptr(ws), ws_bytes, _lib.stream_handle(stream),
-                                          copy_stream.cuda_stream), "msfm_guided_match_rows")
+                                          copy_stream.cuda_stream,
+                                          ctypes.byref(stage_plan) if stage_plan else None),
+               "msfm_guided_match_rows")
     n = int(total.value)
     return pinned[:n].numpy().view(MATCH_ROW).reshape(n)
+
+
+def chunk_bounds(qoff, chunk_pairs: int = 0, max_nt: int = 1, first_chunk_pairs: int = 0):
+    """The matcher's internal chunking (first pair of every chunk, then the end)."""
+    lib = _lib.load(require_device=False)
+    qoff_c = np.ascontiguousarray(qoff, dtype=np.int64)
+    P = len(qoff_c) - 1
+    prm = _lib.MatchParams(1.0, 1.0, 1.0, max(max_nt, 1), int(chunk_pairs), 0,
+                           int(first_chunk_pairs))
+    out = np.zeros(P + 2, np.int32)
+    nc = lib.msfm_guided_chunk_bounds(P, qoff_c.ctypes.data, ctypes.byref(prm), out.ctypes.data,
+                                      len(out))
+    return out[:nc + 1].astype(np.int64)
+
+
+def match_pairs_rows_staged(host, q_img, t_img, F, query_lists, *, device=None,
+                            segment_images: int = 8, d: float = BAND_D_PX,
+                            ratio: float = RATIO_GUIDED, inflation: float = GRID_INFLATION,
+                            grid_d: float | None = None, single_cap: float = SINGLE_CANDIDATE_CAP,
+                            chunk_pairs: int = 0, strategy: str = "grid", pinned=None,
+                            first_chunk_pairs: int = 64, bank: FeatureBank | None = None,
+                            host_pairs: HostPairs | None = None):
+    """``match_pairs_rows`` straight from a pinned ``HostBank``, the upload
+    pipelined into the matching: the bank goes up on a copy stream in ranges of
+    ``segment_images`` images, in the order the matcher's chunks first read them;
+    just before a chunk the matcher's stream waits for the ranges it first reads
+    and indexes them (|desc|^2 + spatial index, msfm_stage_plan), so chunk c
+    computes while later ranges are still in flight; a short first chunk
+    (``first_chunk_pairs``) needs few ranges to start.  ``bank``: a staged bank
+    from an earlier call over the same host bank, whose device buffers (rows,
+    norms, spatial index) are refilled instead of allocated.  ``host_pairs``: the
+    pair table already in pinned memory (``HostPairs``).  Returns (rows, bank)."""
+    import torch
+
+    lib = _lib.load()
+    if d <= 0:
+        raise ValueError(f"cell half-size d must be positive, got {d}")
+    D = float(grid_d) if grid_d is not None else float(d) * float(inflation)
+    P = len(q_img)
+    if bank is None or not getattr(bank, "staged", False) or bank.host is not host:
+        bank = FeatureBank(host=host, device=device, staged=True)
+    nimg = len(bank.image_ids)
+    seg = max(int(segment_images), 1)
+    nseg = (nimg + seg - 1) // seg
+    # H2D copies of all streams go through one copy engine in issue order: small
+    # tables first, then the ranges the first chunk reads, then the pair tables
+    # (prepared on the host while those land), then every other range
+    grid = bank.grid(D, build=False)
+    if host_pairs is not None:
+        qoff = host_pairs.qoff
+    else:
+        lens = np.fromiter((len(x) for x in query_lists), dtype=np.int64, count=P)
+        qoff = np.zeros(P + 1, dtype=np.int64)
+        np.cumsum(lens, out=qoff[1:])
+    # ranges in the order of the first chunk that reads them (host-only planning)
+    bounds = (chunk_bounds(qoff, chunk_pairs, bank.max_n, first_chunk_pairs) if P
+              else np.zeros(1, np.int64))
+    nck = len(bounds) - 1
+    qi, ti = bank.slots(q_img), bank.slots(t_img)
+    first = np.full(nseg, max(nck - 1, 0), np.int64)      # unread ranges: before the last chunk
+    for c in range(nck - 1, -1, -1):
+        p0, p1 = int(bounds[c]), int(bounds[c + 1])
+        first[np.unique(np.concatenate([qi[p0:p1], ti[p0:p1]]) // seg)] = c
+    order = np.lexsort((np.arange(nseg), first))
+    # neighbouring segments first read by the same chunk travel and index as one range
+    k0l, k1l, chk = [], [], []
+    for s in order:
+        a, b = int(s) * seg, min((int(s) + 1) * seg, nimg)
+        if k1l and k1l[-1] == a and chk[-1] == first[s]:
+            k1l[-1] = b
+        else:
+            k0l.append(a)
+            k1l.append(b)
+            chk.append(int(first[s]))
+    k0 = np.array(k0l, np.int32)
+    k1 = np.array(k1l, np.int32)
+    copy_s = torch.cuda.Stream(device=bank.device)
+    copy_s.wait_stream(torch.cuda.current_stream(bank.device))
+    bank.xy.record_stream(copy_s)
+    bank.desc.record_stream(copy_s)
+    n0 = int(np.searchsorted(np.array(chk), 1))           # ranges chunk 0 reads
+    landed = [bank.upload_range(int(a), int(b), copy_s) for a, b in zip(k0[:n0], k1[:n0])]
+    # the pair tables on the copy stream too, right behind chunk 0's ranges (the
+    # matcher's stream waits for them: by then chunk 0's rows have landed as well)
+    hp = host_pairs if host_pairs is not None else HostPairs(bank, q_img, t_img, F, query_lists)
+    inp = hp.upload(bank.device, copy_s)
+    landed += [bank.upload_range(int(a), int(b), copy_s) for a, b in zip(k0[n0:], k1[n0:])]
+    br = np.array([grid.bucket_range(int(a), int(b)) for a, b in zip(k0, k1)],
+                  np.int64).reshape(-1, 2)
+    fr = np.array([bank.row_range(int(a), int(b)) for a, b in zip(k0, k1)],
+                  np.int64).reshape(-1, 2)
+    arrs = dict(chunk=np.array(chk, np.int32), img0=k0, img1=k1,
+                bucket0=np.ascontiguousarray(br[:, 0]), bucket1=np.ascontiguousarray(br[:, 1]),
+                feat0=np.ascontiguousarray(fr[:, 0]), feat1=np.ascontiguousarray(fr[:, 1]))
+    ev = (ctypes.c_void_p * max(len(landed), 1))(*[e._as_parameter_ for e in landed])
+    plan = _lib.StagePlan(len(k0), *[arrs[k].ctypes.data for k in
+                                         ("chunk", "img0", "img1", "bucket0", "bucket1",
+                                          "feat0", "feat1")],
+                          ctypes.cast(ev, ctypes.c_void_p), grid._nb, _lib.ptr(grid._ws),
+                          grid._ws_bytes)
+    plan._keep = (arrs, ev)
+    if P == 0:
+        # nothing to match: index the whole bank here so it is complete on return
+        torch.cuda.current_stream(bank.device).wait_stream(copy_s)
+        _lib.check(lib.msfm_feature_norms(_lib.ptr(bank.desc), bank.n_total, _lib.ptr(bank.norm2),
+                                          _lib.stream_handle()), "msfm_feature_norms")
+        grid.build_range(0, nimg)
+        bank.pair_inputs = inp
+        return np.zeros(0, MATCH_ROW), bank
+    rows = match_pairs_rows(bank, q_img, t_img, F, query_lists, d=d, ratio=ratio,
+                            inflation=inflation, grid_d=grid_d, single_cap=single_cap,
+                            chunk_pairs=chunk_pairs, device_inputs=inp, strategy=strategy,
+                            pinned=pinned, stage_plan=plan, first_chunk_pairs=first_chunk_pairs)
+    bank.pair_inputs = inp
+    bank._staging = copy_s
+    return rows, bank
+
+
+class HostPairs:
+    """A matching step's pair table in pinned host memory (the H2D staging area
+    next to ``HostBank``): bank slots of the query and target images, F, the
+    query-list offsets, the query lists (a list object shared by several pairs —
+    every pair of one query image, densify.py:150-158 — stored once) and each
+    pair's list start.  ``upload`` is one copy per array."""
+
+    def __init__(self, bank, q_img, t_img, F, query_lists):
+        import torch
+
+        P = len(q_img)
+        self.n_pairs = P
+        qi = bank.slots(q_img).astype(np.int32)
+        ti = bank.slots(t_img).astype(np.int32)
+        Fh = np.ascontiguousarray(np.asarray(F, dtype=np.float64).reshape(P, 9))
+        lens = np.fromiter((len(x) for x in query_lists), dtype=np.int64, count=P)
+        qoff = np.zeros(P + 1, dtype=np.int64)
+        np.cumsum(lens, out=qoff[1:])
+        uniq, src = {}, np.zeros(max(P, 1), dtype=np.int64)
+        parts, n = [], 0
+        for k, x in enumerate(query_lists):
+            s = uniq.get(id(x))
+            if s is None:
+                s = uniq[id(x)] = n
+                parts.append(np.asarray(x, dtype=np.int32))
+                n += len(x)
+            src[k] = s
+        qlist = np.concatenate(parts) if n else np.zeros(1, np.int32)
+        self.qoff = qoff
+
+        def pin(a):
+            return torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+
+        self.tensors = (pin(qi), pin(ti), pin(Fh), pin(qoff), pin(qlist), pin(src))
+
+    @property
+    def nbytes(self) -> int:
+        return sum(int(t.numel() * t.element_size()) for t in self.tensors)
+
+    def upload(self, dev, stream=None):
+        """(q slots, t slots, F, qoff, qlist, qoff on the host, list starts) on ``dev``;
+        with ``stream``: copied on that stream, and the current stream waits for them."""
+        import torch
+
+        if stream is None:
+            qi, ti, Fh, qoff, qlist, src = (t.to(dev, non_blocking=True) for t in self.tensors)
+            return (qi, ti, Fh, qoff, qlist, self.qoff, src)
+        cur = torch.cuda.current_stream(dev)
+        with torch.cuda.stream(stream):
+            out = [t.to(dev, non_blocking=True) for t in self.tensors]
+        for t in out:
+            t.record_stream(cur)
+        cur.wait_stream(stream)
+        qi, ti, Fh, qoff, qlist, src = out
+        return (qi, ti, Fh, qoff, qlist, self.qoff, src)
 
 
 def prepare_pairs(bank: FeatureBank, q_img, t_img, F, query_lists):
@@ -200,31 +378,7 @@ def prepare_pairs(bank: FeatureBank, q_img, t_img, F, query_lists):
 
     Query lists passed as the same object for several pairs (every pair of one
     query image, densify.py:150-158) are uploaded once and shared."""
-    import torch
-
-    P = len(q_img)
-    qi = np.array([bank.index_of[int(i)] for i in q_img], dtype=np.int32)
-    ti = np.array([bank.index_of[int(i)] for i in t_img], dtype=np.int32)
-    Fh = np.ascontiguousarray(np.asarray(F, dtype=np.float64).reshape(P, 9))
-    lens = np.array([len(x) for x in query_lists], dtype=np.int64)
-    qoff = np.zeros(P + 1, dtype=np.int64)
-    np.cumsum(lens, out=qoff[1:])
-    uniq, src = {}, np.zeros(max(P, 1), dtype=np.int64)
-    parts, n = [], 0
-    for k, x in enumerate(query_lists):
-        s = uniq.get(id(x))
-        if s is None:
-            s = uniq[id(x)] = n
-            parts.append(np.asarray(x, dtype=np.int32))
-            n += len(x)
-        src[k] = s
-    qlist = np.concatenate(parts) if n else np.zeros(1, np.int32)
-    dev = bank.device
-
-    def up(a):
-        return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().to(dev, non_blocking=True)
-
-    return (up(qi), up(ti), up(Fh), up(qoff), up(qlist), qoff, up(src))
+    return HostPairs(bank, q_img, t_img, F, query_lists).upload(bank.device)
 
 # ---------------------------------------------------------------------------
 # drop-in for msfm.guided.guided_match_pair

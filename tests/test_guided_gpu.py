@@ -229,6 +229,63 @@ def test_pipelined_host_rows_equal_device_packing(chunk):
     np.testing.assert_array_equal(got.view(np.int32), want.view(np.int32))
 
 
+@pytest.mark.parametrize("seg,chunk,first", [(1, 7, 0), (3, 16, 5), (2, 0, 3), (64, 0, 128)])
+def test_staged_upload_rows_equal_resident_bank(seg, chunk, first):
+    """match_pairs_rows_staged (bank uploaded and indexed range by range while the
+    chunks match) == match_pairs_rows over a fully resident bank."""
+    import torch
+
+    from paper_1512_06235_b200 import scenes
+    from paper_1512_06235_b200.bank import HostBank
+    from paper_1512_06235_b200.guided import match_pairs_rows, match_pairs_rows_staged
+
+    scene, snap = scenes.build("C1", n_cameras=10)
+    wl = scenes.pair_workload(scene, snap)
+    ok = np.flatnonzero(wl.valid)
+    bank = _bank(scene.feature_sets)
+    ql = [wl.untracked[int(wl.q_img[k])] for k in ok]
+    want = match_pairs_rows(bank, wl.q_img[ok], wl.t_img[ok], wl.F[ok], ql, chunk_pairs=chunk)
+    host = HostBank(scene.feature_sets)
+    got, b2 = match_pairs_rows_staged(host, wl.q_img[ok], wl.t_img[ok], wl.F[ok], ql,
+                                      segment_images=seg, chunk_pairs=chunk,
+                                      first_chunk_pairs=first)
+    torch.cuda.synchronize()
+    assert len(got) == len(want) > 100
+    np.testing.assert_array_equal(got.view(np.int32), want.view(np.int32))
+    # the staged bank ends complete: rows, norms, CSR starts identical
+    assert torch.equal(b2.desc, bank.desc) and torch.equal(b2.norm2, bank.norm2)
+    g1, g2 = bank.grid(10.0), b2.grid(10.0)        # D = d * inflation = 8 * 1.25
+    for name in ("sub", "rstart", "cstart"):
+        assert torch.equal(getattr(g1, name), getattr(g2, name)), name
+
+
+def test_grid_build_ranges_any_order_equal_full_build():
+    """msfm_grid_build_range over shuffled image ranges == msfm_grid_build (bucket
+    members compared as sets: the scatter order inside a bucket is atomic)."""
+    import torch
+
+    from paper_1512_06235_b200 import scenes
+    from paper_1512_06235_b200.bank import SpatialIndex
+
+    scene, _ = scenes.build("C1", n_cameras=9)
+    bank = _bank(scene.feature_sets)
+    full = bank.grid(10.0)
+    part = SpatialIndex(bank, 10.0, build=False)
+    cuts = [0, 1, 4, 5, 9]
+    for k in [2, 0, 3, 1]:
+        part.build_range(cuts[k], cuts[k + 1])
+    torch.cuda.synchronize()
+    for name in ("sub", "rstart", "cstart"):
+        assert torch.equal(getattr(full, name), getattr(part, name)), name
+    rs = full.rstart.cpu().numpy()
+    for mem in ("rmem", "cmem"):
+        a, b = getattr(full, mem).cpu().numpy(), getattr(part, mem).cpu().numpy()
+        st = rs if mem == "rmem" else full.cstart.cpu().numpy()
+        key = np.repeat(np.arange(len(st) - 1), np.diff(st))
+        assert np.array_equal(np.sort(a + key.astype(np.int64) * 100000),
+                              np.sort(b + key.astype(np.int64) * 100000))
+
+
 def test_16k_feature_pairs_match_oracle():
     """C4/C5 feature density (16k/img): a few densify pairs against the C oracle
     (16-bit feature ids in the packed rows, larger strips and member sets)."""

@@ -1,0 +1,90 @@
+"""Where does the time of the staged e2e path go?  (C3 bench workload)"""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import bench
+from paper_1512_06235_b200.bank import FeatureBank, HostBank
+from paper_1512_06235_b200.guided import match_pairs_rows, match_pairs_rows_staged, prepare_pairs
+
+dev = torch.device("cuda", 0)
+scene, wl, ok, snap = bench.build_workload(320, with_snapshot=True)
+ql = [wl.untracked[int(wl.q_img[k])] for k in ok]
+host = HostBank(scene.feature_sets)
+pinned = torch.empty((int(sum(len(x) for x in ql)), 4), dtype=torch.int32, pin_memory=True)
+args = (wl.q_img[ok], wl.t_img[ok], wl.F[ok], ql)
+
+
+def timed(name, fn, n=6):
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(n):
+        t0 = time.perf_counter()
+        fn()
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    print(f"{name:40s} {1e3 * np.median(ts):8.2f} ms  (all: "
+          f"{' '.join(f'{1e3 * t:.1f}' for t in ts)})", flush=True)
+
+
+def up():
+    b = FeatureBank(host=host, device=dev)
+    return b
+
+
+timed("bank H2D (resident)", up)
+from torch.profiler import ProfilerActivity, profile
+with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA], with_stack=True) as prof0:
+    timed("bank H2D + grid", lambda: up().grid(10.0))
+os.makedirs("gpurun_out", exist_ok=True)
+prof0.export_chrome_trace("gpurun_out/grid_trace.json")
+timed("staged bank alloc", lambda: FeatureBank(host=host, device=dev, staged=True))
+
+
+bank = up()
+bank.grid(10.0)
+inp = prepare_pairs(bank, *args)
+timed("match_pairs_rows resident", lambda: match_pairs_rows(bank, *args, device_inputs=inp,
+                                                            pinned=pinned))
+timed("resident e2e", lambda: match_pairs_rows(up(), *args, pinned=pinned))
+timed("staged e2e (first chunk 128)", lambda: match_pairs_rows_staged(host, *args, device=dev, pinned=pinned))
+_sb = [None]
+from paper_1512_06235_b200.guided import HostPairs
+hp = HostPairs(host, *args)
+
+
+def staged_reuse(**kw):
+    rows, _sb[0] = match_pairs_rows_staged(host, *args, device=dev, pinned=pinned, bank=_sb[0],
+                                         host_pairs=hp, **kw)
+    return rows
+
+
+timed("staged e2e, device buffers reused", staged_reuse)
+for fcp in (0, 32, 64, 256):
+    timed(f"staged reuse first chunk {fcp}", lambda: staged_reuse(first_chunk_pairs=fcp))
+for seg in (8, 32):
+    timed(f"staged reuse seg {seg}", lambda: staged_reuse(segment_images=seg))
+for fcp in ():
+    timed(f"staged e2e first chunk {fcp}", lambda: match_pairs_rows_staged(
+        host, *args, device=dev, pinned=pinned, first_chunk_pairs=fcp))
+for seg in ():
+    timed(f"staged e2e seg={seg}", lambda: match_pairs_rows_staged(host, *args, device=dev,
+                                                                    pinned=pinned,
+                                                                    segment_images=seg))
+
+
+
+# ---- one staged call under the CUDA activity profiler (kernel + memcpy timeline)
+for _ in range(2):
+    staged_reuse()
+torch.cuda.synchronize()
+with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+    staged_reuse()
+    torch.cuda.synchronize()
+prof.export_chrome_trace("gpurun_out/staged_trace.json")
