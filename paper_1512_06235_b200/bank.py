@@ -131,6 +131,21 @@ class FeatureBank:
         """Bank index of every image id (int64), KeyError for ids not in the bank."""
         return _slots(self, image_ids)
 
+    def refill(self, stream=None):
+        """Copy every host row into this bank's device buffers again and recompute
+        |desc|^2 (a step of a pipeline whose inputs arrive in the same pinned host
+        bank: no device allocation).  Spatial indexes are dropped."""
+        import torch
+
+        lib = _lib.load()
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(s):
+            self.xy.copy_(self.host.xy, non_blocking=True)
+            self.desc.copy_(self.host.desc, non_blocking=True)
+        _lib.check(lib.msfm_feature_norms(_lib.ptr(self.desc), self.n_total, _lib.ptr(self.norm2),
+                                          _lib.stream_handle(s)), "msfm_feature_norms")
+        self._grids = {}
+
     def row_range(self, k0: int, k1: int):
         """Bank rows [a, b) of images [k0, k1)."""
         a = int(self.offsets[k0]) if k0 < len(self.offsets) else self.n_total

@@ -9,6 +9,10 @@
 // batched entry, numpy's SeedSequence(seed) -> PCG64 seeding restated below
 // (bit_generator.pyx hashmix/mix/generate_state, pcg64_set_seed).  Validated
 // draw-for-draw and state-for-state in tests/test_sampler.py.
+#include <algorithm>
+#include <atomic>
+#include <thread>
+#include <vector>
 #include <stdint.h>
 #include <string.h>
 
@@ -190,33 +194,54 @@ extern "C" int msfm_ransac_samples_seeded(int32_t n_items, const uint64_t* seeds
         msfm::set_error("msfm_ransac_samples_seeded: bad arguments");
         return MSFM_EINVAL;
     }
-    int64_t tmp[48];
     for (int32_t it = 0; it < n_items; it++) {
         if (n[it] < sample_size) {
             msfm::set_error("msfm_ransac_samples_seeded: item %d has %lld < %d rows", it,
                             (long long)n[it], sample_size);
             return MSFM_EINVAL;
         }
-        Pcg64 g;
-        seed_pcg64(seeds[it], g);
-        int32_t* o = out + (int64_t)it * count * sample_size;
-        for (int32_t h = 0; h < count; h++) {
-            if (!choice_floyd(g, n[it], sample_size, tmp)) {
-                msfm::set_error("msfm_ransac_samples_seeded: population %lld outside the Floyd "
-                                "branch", (long long)n[it]);
-                return MSFM_EINVAL;
+    }
+    // items are independent streams: host threads over items (output order fixed)
+    std::atomic<int32_t> next{0};
+    std::atomic<int64_t> bad_n{-1};
+    auto work = [&]() {
+        int64_t tmp[48];
+        for (;;) {
+            const int32_t it = next.fetch_add(1);
+            if (it >= n_items) return;
+            Pcg64 g;
+            seed_pcg64(seeds[it], g);
+            int32_t* o = out + (int64_t)it * count * sample_size;
+            for (int32_t h = 0; h < count; h++) {
+                if (!choice_floyd(g, n[it], sample_size, tmp)) {
+                    bad_n.store(n[it]);
+                    return;
+                }
+                for (int k = 0; k < sample_size; k++) o[(int64_t)h * sample_size + k] = (int32_t)tmp[k];
             }
-            for (int k = 0; k < sample_size; k++) o[(int64_t)h * sample_size + k] = (int32_t)tmp[k];
+            if (state_out) {
+                uint64_t* so = state_out + 6 * (int64_t)it;
+                so[0] = (uint64_t)(g.state >> 64);
+                so[1] = (uint64_t)g.state;
+                so[2] = (uint64_t)(g.inc >> 64);
+                so[3] = (uint64_t)g.inc;
+                so[4] = (uint64_t)g.has32;
+                so[5] = (uint64_t)g.u32;
+            }
         }
-        if (state_out) {
-            uint64_t* so = state_out + 6 * (int64_t)it;
-            so[0] = (uint64_t)(g.state >> 64);
-            so[1] = (uint64_t)g.state;
-            so[2] = (uint64_t)(g.inc >> 64);
-            so[3] = (uint64_t)g.inc;
-            so[4] = (uint64_t)g.has32;
-            so[5] = (uint64_t)g.u32;
-        }
+    };
+    const int64_t draws = (int64_t)n_items * count;
+    int nt = (int)std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), 16);
+    nt = (int)std::min<int64_t>(nt, std::max<int64_t>(1, draws / 2048));
+    nt = std::min(nt, std::max(n_items, 1));
+    std::vector<std::thread> pool;
+    for (int k = 1; k < nt; k++) pool.emplace_back(work);
+    work();
+    for (auto& th : pool) th.join();
+    if (bad_n.load() >= 0) {
+        msfm::set_error("msfm_ransac_samples_seeded: population %lld outside the Floyd branch",
+                        (long long)bad_n.load());
+        return MSFM_EINVAL;
     }
     return MSFM_OK;
 }

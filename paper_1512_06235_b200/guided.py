@@ -169,21 +169,37 @@ def match_pairs_rows(bank: FeatureBank, q_img, t_img, F, query_lists, *, d: floa
                            int(first_chunk_pairs))
     qoff_c = np.ascontiguousarray(qoff, dtype=np.int64)
     ws_bytes = lib.msfm_guided_workspace_bytes(P, qoff_c.ctypes.data, ctypes.byref(prm))
-    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    # scratch kept on the bank between calls of the same shape (a staged bank reused
+    # step after step allocates nothing here after the first step)
+    bufs = bank.__dict__.setdefault("_rows_bufs", {})
+
+    def buf(name, shape, dtype, zero=False, pin=False):
+        t = bufs.get(name)
+        if t is None or tuple(t.shape) != tuple(shape) or t.dtype != dtype:
+            t = (torch.empty(shape, dtype=dtype, pin_memory=True) if pin
+                 else torch.empty(shape, dtype=dtype, device=dev))
+            bufs[name] = t
+        if zero:
+            t.zero_()
+        return t
+
+    ws = buf("ws", (max(ws_bytes, 1),), torch.uint8)
     cap = max(nq_total, 1)
-    out_q = torch.empty(cap, dtype=torch.int32, device=dev)
-    out_t = torch.empty(cap, dtype=torch.int32, device=dev)
-    out_d = torch.empty(cap, dtype=torch.float32, device=dev)
-    out_r = torch.empty(cap, dtype=torch.float32, device=dev)
-    out_c = torch.zeros(P, dtype=torch.int32, device=dev)
-    out_off = torch.empty(P + 1, dtype=torch.int64, device=dev)
-    d_rows = torch.empty((cap, 4), dtype=torch.int32, device=dev)
-    d_meta = torch.zeros(2 * (P + 1), dtype=torch.int64, device=dev)
-    h_meta = torch.zeros(2 * (P + 1), dtype=torch.int64, pin_memory=True)
+    out_q = buf("q", (cap,), torch.int32)
+    out_t = buf("t", (cap,), torch.int32)
+    out_d = buf("d", (cap,), torch.float32)
+    out_r = buf("r", (cap,), torch.float32)
+    out_c = buf("c", (P,), torch.int32, zero=True)
+    out_off = buf("off", (P + 1,), torch.int64)
+    d_rows = buf("rows", (cap, 4), torch.int32)
+    d_meta = buf("meta", (2 * (P + 1),), torch.int64, zero=True)
+    h_meta = buf("hmeta", (2 * (P + 1),), torch.int64, zero=True, pin=True)
     if pinned is None or pinned.shape[0] < cap:
         pinned = torch.empty((cap, 4), dtype=torch.int32, pin_memory=True)
     total = ctypes.c_int64(0)
-    copy_stream = torch.cuda.Stream(device=dev)
+    copy_stream = bank.__dict__.get("_d2h_stream")
+    if copy_stream is None:
+        copy_stream = bank.__dict__["_d2h_stream"] = torch.cuda.Stream(device=dev)
     b, g = bank.cstruct(), grid.cstruct()
     _lib.check(lib.msfm_guided_match_rows(ctypes.byref(b), ctypes.byref(g), P, _lib.ptr(pq),
                                           _lib.ptr(pt), _lib.ptr(pF), _lib.ptr(qoff_d),
@@ -274,16 +290,25 @@ def match_pairs_rows_staged(host, q_img, t_img, F, query_lists, *, device=None,
             chk.append(int(first[s]))
     k0 = np.array(k0l, np.int32)
     k1 = np.array(k1l, np.int32)
-    copy_s = torch.cuda.Stream(device=bank.device)
+    # one H2D stream per bank (torch's stream pool hands out a different stream per
+    # call, each with its own allocator pool)
+    copy_s = bank.__dict__.get("_h2d_stream")
+    if copy_s is None:
+        copy_s = bank.__dict__["_h2d_stream"] = torch.cuda.Stream(device=bank.device)
     copy_s.wait_stream(torch.cuda.current_stream(bank.device))
-    bank.xy.record_stream(copy_s)
-    bank.desc.record_stream(copy_s)
+    if not bank.__dict__.get("_recorded"):
+        bank.xy.record_stream(copy_s)
+        bank.desc.record_stream(copy_s)
+        bank.__dict__["_recorded"] = True
     n0 = int(np.searchsorted(np.array(chk), 1))           # ranges chunk 0 reads
     landed = [bank.upload_range(int(a), int(b), copy_s) for a, b in zip(k0[:n0], k1[:n0])]
     # the pair tables on the copy stream too, right behind chunk 0's ranges (the
     # matcher's stream waits for them: by then chunk 0's rows have landed as well)
     hp = host_pairs if host_pairs is not None else HostPairs(bank, q_img, t_img, F, query_lists)
-    inp = hp.upload(bank.device, copy_s)
+    prev = bank.__dict__.get("_pairs_dev")
+    reuse = prev[1] if prev is not None and prev[0] is hp else None
+    inp = hp.upload(bank.device, copy_s, out=reuse)
+    bank.__dict__["_pairs_dev"] = (hp, [inp[k] for k in (0, 1, 2, 3, 4, 6)])
     landed += [bank.upload_range(int(a), int(b), copy_s) for a, b in zip(k0[n0:], k1[n0:])]
     br = np.array([grid.bucket_range(int(a), int(b)) for a, b in zip(k0, k1)],
                   np.int64).reshape(-1, 2)
@@ -355,20 +380,25 @@ class HostPairs:
     def nbytes(self) -> int:
         return sum(int(t.numel() * t.element_size()) for t in self.tensors)
 
-    def upload(self, dev, stream=None):
+    def upload(self, dev, stream=None, out=None):
         """(q slots, t slots, F, qoff, qlist, qoff on the host, list starts) on ``dev``;
-        with ``stream``: copied on that stream, and the current stream waits for them."""
+        with ``stream``: copied on that stream, and the current stream waits for them;
+        ``out``: device tensors of an earlier upload of this table, refilled."""
         import torch
 
-        if stream is None:
+        if stream is None and out is None:
             qi, ti, Fh, qoff, qlist, src = (t.to(dev, non_blocking=True) for t in self.tensors)
             return (qi, ti, Fh, qoff, qlist, self.qoff, src)
         cur = torch.cuda.current_stream(dev)
-        with torch.cuda.stream(stream):
-            out = [t.to(dev, non_blocking=True) for t in self.tensors]
-        for t in out:
-            t.record_stream(cur)
-        cur.wait_stream(stream)
+        if out is None:
+            # allocated in the current stream's pool (the one that consumes them)
+            out = [torch.empty(tuple(t.shape), dtype=t.dtype, device=dev) for t in self.tensors]
+        s = stream if stream is not None else cur
+        with torch.cuda.stream(s):
+            for d, h in zip(out, self.tensors):
+                d.copy_(h, non_blocking=True)
+        if s is not cur:
+            cur.wait_stream(s)
         qi, ti, Fh, qoff, qlist, src = out
         return (qi, ti, Fh, qoff, qlist, self.qoff, src)
 

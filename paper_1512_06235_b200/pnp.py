@@ -83,33 +83,42 @@ def _replay_records(counts, evaluated, n, max_iters, confidence, power=6):
 
 
 def _replay_batch(counts, evaluated, n, max_iters, confidence, power=6):
-    """_replay_records for every row of ``counts`` (A, >= evaluated): the record
-    positions of all rows come from one vectorized pass; per row the same scalar
-    numpy expressions run at the records.  Returns, per row, the _replay tuple or
-    "overflow"."""
+    """_replay_records for every row of ``counts`` (A, >= evaluated).  The record
+    positions of all rows come from one vectorized pass; the reference's
+    ``needed`` at every record is evaluated once for all rows: ``1 - w**power``
+    and the max with 1e-15 as the Python float expressions, then np.log / divide
+    / ceil on one array (numpy's float64 ufunc loop is the one its scalar calls
+    run, so the values are the reference's bit for bit; a non-finite quotient is
+    the reference's OverflowError).  Per row only the integer scan remains.
+    Returns, per row, the _replay tuple or "overflow"."""
     C = np.asarray(counts)[:, :evaluated].astype(np.int64)
     A = C.shape[0]
     prev = np.maximum.accumulate(np.concatenate([np.zeros((A, 1), np.int64), np.maximum(C, 0)],
                                                 axis=1), axis=1)[:, :-1]
     rr, cc = np.nonzero(C > prev)
-    starts = np.searchsorted(rr, np.arange(A + 1))
+    starts = np.searchsorted(rr, np.arange(A + 1)).tolist()
     cc_l, cnt_l = cc.tolist(), C[rr, cc].tolist()
+    n_l = np.asarray(n, np.int64)[rr].tolist()
+    # records have count >= 1, so w > 0 and the reference always evaluates needed
+    arg = np.array([max(1.0 - (c / m) ** power, 1e-15) for c, m in zip(cnt_l, n_l)], np.float64)
+    with np.errstate(divide="ignore"):
+        quo = np.ceil(np.log(1.0 - confidence) / np.log(arg))
+    ovf_l = (~np.isfinite(quo)).tolist()
+    need_l = np.where(np.isfinite(quo), np.minimum(np.nan_to_num(quo, posinf=0.0, neginf=0.0),
+                                                   max_iters), 0).astype(np.int64).tolist()
     out = []
     for k in range(A):
-        nk = int(n[k])
-        best_count, best_h, needed = 0, -1, max_iters
-        try:
-            for j in range(starts[k], starts[k + 1]):
-                h = cc_l[j]
-                if h >= needed or h >= max_iters:
-                    break
-                best_count, best_h = cnt_l[j], h
-                w = best_count / nk
-                if w > 0:
-                    with np.errstate(divide="ignore"):
-                        denom = np.log(max(1.0 - w ** power, 1e-15))
-                        needed = min(max_iters, int(np.ceil(np.log(1.0 - confidence) / denom)))
-        except OverflowError:
+        best_count, best_h, needed, ovf = 0, -1, max_iters, False
+        for j in range(starts[k], starts[k + 1]):
+            h = cc_l[j]
+            if h >= needed or h >= max_iters:
+                break
+            best_count, best_h = cnt_l[j], h
+            if ovf_l[j]:
+                ovf = True
+                break
+            needed = need_l[j]
+        if ovf:
             out.append("overflow")
             continue
         stop = min(needed, max_iters)
@@ -182,7 +191,7 @@ def pnp_batch_flat(X, uv, off, K_list, seeds, **kw):
 def pnp_batch(X_list, uv_list, K_list, seeds, *, threshold=PNP_THRESHOLD_PX,
               min_inliers=PNP_MIN_INLIERS, max_iters=PNP_MAX_ITERS,
               confidence=PNP_CONFIDENCE, device=None, stream=None, first_round=FIRST_ROUND,
-              flat=None):
+              flat=None, timing=None):
     """pnp_ransac for many images; returns a PnpResult per image.  Images with
     fewer than 6 correspondences get status "insufficient" (the reference raises
     InsufficientDataError there)."""
@@ -190,6 +199,17 @@ def pnp_batch(X_list, uv_list, K_list, seeds, *, threshold=PNP_THRESHOLD_PX,
 
     lib = _lib.load()
     dev = torch.device(device or "cuda")
+
+    def mark(name):
+        # optional phase timing (tools/probe_localize.py): device synchronized
+        if timing is not None:
+            import time
+            torch.cuda.synchronize(dev)
+            t = time.perf_counter()
+            timing[name] = timing.get(name, 0.0) + (t - timing.get("_t", t))
+            timing["_t"] = t
+
+    mark("_start")
     if flat is not None:
         sizes = np.diff(np.asarray(flat[2], np.int64))
     else:
@@ -212,9 +232,12 @@ def pnp_batch(X_list, uv_list, K_list, seeds, *, threshold=PNP_THRESHOLD_PX,
     st = _lib.stream_handle(stream)
     A = len(active)
     H1 = min(max_iters, first_round)
+    mark("batch upload")
     counts = np.full((A, max_iters), -2, np.int64)
     # all streams default_rng(seed) at once (SeedSequence restated natively)
-    samples = np.zeros((A, H1, 6), np.int32)
+    # written straight into pinned memory: the upload is one async copy
+    samples_t = torch.empty((A, H1, 6), dtype=torch.int32, pin_memory=True)
+    samples = samples_t.numpy()
     st_all = np.zeros((A, 6), np.uint64)
     if any(int(seeds[i]) < 0 for i in active):
         raise ValueError("expected non-negative integer seeds")   # as np.random.default_rng
@@ -224,10 +247,13 @@ def pnp_batch(X_list, uv_list, K_list, seeds, *, threshold=PNP_THRESHOLD_PX,
                                               samples.ctypes.data, st_all.ctypes.data),
                "msfm_ransac_samples_seeded")
     states = [(st_all[k],) for k in range(A)]
+    mark("samples (host)")
     # hypotheses stay on the device; only the inlier counts come back for the replay
-    d_hyp1, c1 = _score(lib, batch, samples, H1, threshold, st, dev)
+    d_hyp1, c1 = _score(lib, batch, samples_t, H1, threshold, st, dev)
     counts[:, :H1] = c1
+    mark("round 1 score")
     best = _replay_batch(counts, H1, batch.n, max_iters, confidence)
+    mark("round 1 replay")
     pending = [k for k in range(A) if best[k] != "overflow" and not best[k][4]]
     d_hyp2 = None
     if pending:
@@ -246,6 +272,7 @@ def pnp_batch(X_list, uv_list, K_list, seeds, *, threshold=PNP_THRESHOLD_PX,
         for k, r in zip(pending, _replay_batch(counts[pending], max_iters, batch.n[pending],
                                                max_iters, confidence)):
             best[k] = r
+        mark(f"round 2 ({len(pending)} images)")
     # refit the winners: gather each winning hypothesis on the device
     import torch
 
@@ -276,6 +303,7 @@ def pnp_batch(X_list, uv_list, K_list, seeds, *, threshold=PNP_THRESHOLD_PX,
             hs = torch.tensor([x[2] for x in src2], device=dev)
             d_best[ks] = d_hyp2[js, hs]
         _refit(lib, batch, status, d_best, threshold, min_inliers, st, dev, results, active, best)
+    mark("refit + results")
     return results
 
 
@@ -284,7 +312,9 @@ def _score(lib, batch, samples, H, threshold, st, dev):
     import torch
 
     A = samples.shape[0]
-    d_samples = torch.from_numpy(np.ascontiguousarray(samples)).pin_memory().to(dev, non_blocking=True)
+    if not isinstance(samples, torch.Tensor):
+        samples = torch.from_numpy(np.ascontiguousarray(samples)).pin_memory()
+    d_samples = samples.to(dev, non_blocking=True)
     d_hyp = torch.empty((A, H, 12), dtype=torch.float64, device=dev)
     d_count = torch.empty((A, H), dtype=torch.int32, device=dev)
     _lib.check(lib.msfm_pnp_hypotheses(_lib.ptr(batch.X), _lib.ptr(batch.uv), _lib.ptr(batch.off),
@@ -309,7 +339,10 @@ def _refit(lib, batch, status, d_best, threshold, min_inliers, st, dev, results,
                                   float(threshold), int(min_inliers), 20, _lib.ptr(d_R),
                                   _lib.ptr(d_t), _lib.ptr(d_mask), _lib.ptr(d_ni), _lib.ptr(d_ok), st),
                "msfm_pnp_refit")
-    R, t, mask, ok = d_R.cpu().numpy(), d_t.cpu().numpy(), d_mask.cpu().numpy(), d_ok.cpu().numpy()
+    # two copies back: (R | t | ok) rows and the inlier masks
+    pose = torch.cat([d_R, d_t, d_ok.to(torch.float64)[:, None]], dim=1).cpu().numpy()
+    mask = d_mask.cpu().numpy()
+    R, t, ok = pose[:, :9], pose[:, 9:12], pose[:, 12] != 0
     for k in range(A):
         if not status[k]:
             continue

@@ -1,4 +1,5 @@
-"""Localization-step probe (not the bench): C2 workload, wall-clock breakdown."""
+"""Localization-step probe (not the bench): the bench's C2 step (device-flat
+correspondences + pnp_batch_flat), wall-clock split + cProfile + CUDA timeline."""
 import cProfile, os, pstats, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -6,7 +7,7 @@ import bench
 from paper_1512_06235_b200 import scenes
 from paper_1512_06235_b200.bank import FeatureBank, HostBank
 from paper_1512_06235_b200.localize import PointSet, direct_search, upload_points
-from paper_1512_06235_b200.pnp import pnp_batch
+from paper_1512_06235_b200.pnp import pnp_batch_flat
 
 scene, snap, queries = bench.build_localization()
 S, n = scenes.track_sums(scene, snap)
@@ -16,29 +17,58 @@ Ks = [scene.cameras[q].K for q in queries]
 dev = torch.device("cuda")
 bank = FeatureBank(host=host, device=dev)
 dp = upload_points(pts, dev)
+d_xyz = torch.from_numpy(snap.point_xyz).to(dev)
+T = {}
+PT = {}
+
+
+def tick(name, t0):
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    T.setdefault(name, []).append((t - t0) * 1e3)
+    return t
 
 
 def step():
     t0 = time.perf_counter()
-    corrs = direct_search(bank, pts, queries, device_points=dp)
-    t1 = time.perf_counter()
-    todo = [k for k, c in enumerate(corrs) if len(c) > 16]
-    X = [snap.point_xyz[corrs[k][:, 0]] for k in todo]
-    uv = [scene.feature_sets[queries[k]].xy[corrs[k][:, 1]].astype(np.float64) for k in todo]
-    t2 = time.perf_counter()
-    res = pnp_batch(X, uv, [Ks[k] for k in todo], [queries[k] for k in todo], device=dev)
-    torch.cuda.synchronize()
-    t3 = time.perf_counter()
-    return (t1 - t0) * 1e3, (t2 - t1) * 1e3, (t3 - t2) * 1e3
+    prow, fid, off = direct_search(bank, pts, queries, device_points=dp, device_flat=True)
+    t0 = tick("direct_search (kNN + ratio + dedupe, counts D2H)", t0)
+    cnt = np.diff(off)
+    todo = np.flatnonzero(cnt > 16)
+    sel = np.concatenate([np.arange(off[k], off[k + 1]) for k in todo])
+    img_of = np.repeat(np.arange(len(queries)), cnt)[sel]
+    d_sel = torch.from_numpy(sel).to(dev)
+    d_row = torch.from_numpy(bank.offsets[img_of]).to(dev) + fid[d_sel]
+    X = d_xyz[prow[d_sel]]
+    uv = bank.xy[d_row].to(torch.float64)
+    toff = np.zeros(len(todo) + 1, np.int64)
+    np.cumsum(cnt[todo], out=toff[1:])
+    t0 = tick("gather", t0)
+    res = pnp_batch_flat(X, uv, toff, [Ks[k] for k in todo], [queries[k] for k in todo], device=dev,
+                         timing=PT)
+    tick("pnp_batch_flat", t0)
+    return res
 
 
 for _ in range(3):
     step()
-ts = np.array([step() for _ in range(5)])
-print("direct_search %.2f ms  gather %.2f ms  pnp_batch %.2f ms" % tuple(ts.mean(0)))
+T.clear()
+for _ in range(10):
+    step()
+for k, v in T.items():
+    print(f"{k:52s} {np.median(v):7.2f} ms")
+PT.pop("_t", None)
+for k, v in PT.items():
+    print(f"   pnp {k:46s} {v * 1e3 / 13:7.2f} ms")
 pr = cProfile.Profile()
 pr.enable()
-for _ in range(3):
+for _ in range(5):
     step()
 pr.disable()
-pstats.Stats(pr).sort_stats("cumulative").print_stats(25)
+pstats.Stats(pr).sort_stats("tottime").print_stats(22)
+from torch.profiler import ProfilerActivity, profile
+with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+    step()
+    torch.cuda.synchronize()
+os.makedirs("gpurun_out", exist_ok=True)
+prof.export_chrome_trace("gpurun_out/loc_trace.json")
