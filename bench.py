@@ -471,7 +471,8 @@ def run_localization(args, dev):
 
     from paper_1512_06235_b200 import _lib, scenes
     from paper_1512_06235_b200.bank import FeatureBank, HostBank
-    from paper_1512_06235_b200.localize import PointSet, direct_search, knn2_tracks, upload_points
+    from paper_1512_06235_b200.localize import (PointSet, direct_search, gather_pnp_inputs,
+                                                knn2_tracks, upload_points)
     from paper_1512_06235_b200.pnp import pnp_batch_flat
 
     scene, snap, queries = build_localization()
@@ -484,21 +485,11 @@ def run_localization(args, dev):
         # device-resident flat correspondences: image k owns [off[k], off[k+1]); the
         # gate of localize.py:203 (> 16) selects the images that go to PnP, and their
         # 3D-2D pairs are gathered on the device
-        prow, fid, off = direct_search(bank, pts, queries, device_points=dp, device_flat=True)
-        cnt = np.diff(off)
-        todo = np.flatnonzero(cnt > 16)
-        sel = np.concatenate([np.arange(off[k], off[k + 1]) for k in todo]) if len(todo) else \
-            np.zeros(0, np.int64)
-        img_of = np.repeat(np.arange(len(queries)), cnt)[sel]
-        d_sel = torch.from_numpy(sel).to(dev)
-        d_row = torch.from_numpy(bank.offsets[img_of]).to(dev) + fid[d_sel]
-        X = d_xyz[prow[d_sel]]
-        uv = bank.xy[d_row].to(torch.float64)
-        toff = np.zeros(len(todo) + 1, np.int64)
-        np.cumsum(cnt[todo], out=toff[1:])
+        corr = direct_search(bank, pts, queries, device_points=dp, to_host=False)
+        X, uv, toff, todo = gather_pnp_inputs(bank, corr, queries, d_xyz)
         res = pnp_batch_flat(X, uv, toff, [Ks[k] for k in todo], [queries[k] for k in todo],
                              device=dev)
-        return off, res
+        return toff, res
 
     bank = FeatureBank(host=host, device=dev)
     dp = upload_points(pts, dev)
@@ -551,7 +542,7 @@ def run_localization(args, dev):
            "ms_per_step": dt * 1e3, "status_counts": status,
            "e2e": {"value": len(queries) / float(np.mean(e2e)), "unit": "images/s",
                    "h2d_bytes_per_step": int(host.nbytes + S.nbytes + n.nbytes + 8 * M + 24 * M),
-                   "d2h_bytes_per_step": int(corrs.nbytes + 1 * len(res) +
+                   "d2h_bytes_per_step": int(4 * len(queries) + 13 * 8 * len(res) +
                                              sum(r.mask.nbytes for r in res if r.mask is not None))},
            "roofline": {"bound": "tensor", "kernel": "knn_tc_kernel", "achieved": ach,
                         "peak": peak, "unit": "TOPS (int8)", "frac": ach / peak,

@@ -298,6 +298,16 @@ int msfm_direct_3d2d(const msfm_bank* bank, int32_t n_points, const int32_t* d_n
                      int32_t* d_win, const int64_t* d_win_off, int32_t* d_corr_row,
                      int32_t* d_corr_fid, int32_t* d_corr_n, void* stream);
 
+/* The PnP inputs of selected images straight from msfm_direct_3d2d's output
+ * (localize.py:203-211: X = the points' positions, uv = the features' pixels as
+ * f64).  Selected image k: correspondence table row d_sel[k] (stride m_pad),
+ * bank row of its feature 0 d_row0[k], output rows [d_out_off[k], d_out_off[k+1]):
+ * d_X [.][3] = d_xyz[point row], d_uv [.][2] = bank xy[d_row0[k] + fid]. */
+int msfm_gather_3d2d(const int32_t* d_corr_row, const int32_t* d_corr_fid, int32_t m_pad,
+                     int32_t n_sel, const int64_t* d_sel, const int64_t* d_row0,
+                     const int64_t* d_out_off, const double* d_xyz, const float* d_bank_xy,
+                     double* d_X, double* d_uv, void* stream);
+
 /* ------------------------------------------------------------------------
  * PnP-RANSAC (reconstruct.py:168-226), batched over images.  Correspondences of
  * image s: X [off[s]..off[s+1])[3] f64 world points, uv [..][2] f64 pixels,

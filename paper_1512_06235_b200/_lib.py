@@ -87,6 +87,8 @@ _SIGS = {
                                         ctypes.c_size_t, VP]),
     "msfm_knn2_second_index": (ctypes.c_int, [ctypes.POINTER(Bank), ctypes.c_int32, VP, VP,
                                               ctypes.c_int32, VP, VP, VP, VP, VP, VP]),
+    "msfm_gather_3d2d": (ctypes.c_int, [VP, VP, ctypes.c_int32, ctypes.c_int32, VP, VP, VP, VP,
+                                        VP, VP, VP, VP]),
     "msfm_direct_3d2d": (ctypes.c_int, [ctypes.POINTER(Bank), ctypes.c_int32, VP, VP, ctypes.c_int32,
                                         VP, VP, VP, VP, ctypes.c_int64, ctypes.c_int64,
                                         ctypes.c_double, VP, VP, VP, VP, VP, VP]),

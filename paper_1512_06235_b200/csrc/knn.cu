@@ -610,6 +610,42 @@ extern "C" int msfm_knn2_second_index(const msfm_bank* bank, int32_t n_points, c
     return MSFM_OK;
 }
 
+// one CTA per selected image, threads over its correspondences
+__global__ void gather_3d2d_kernel(const int32_t* __restrict__ crow, const int32_t* __restrict__ cfid,
+                                   int m_pad, const int64_t* __restrict__ sel,
+                                   const int64_t* __restrict__ row0, const int64_t* __restrict__ out_off,
+                                   const double* __restrict__ xyz, const float2* __restrict__ bxy,
+                                   double* __restrict__ X, double* __restrict__ uv) {
+    const int k = blockIdx.x;
+    const int64_t src = (int64_t)sel[k] * m_pad, o = out_off[k], n = out_off[k + 1] - o;
+    const int64_t r0 = row0[k];
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const int64_t p = crow[src + i];
+        const float2 q = bxy[r0 + cfid[src + i]];
+        double* x = X + 3 * (o + i);
+        x[0] = xyz[3 * p]; x[1] = xyz[3 * p + 1]; x[2] = xyz[3 * p + 2];
+        uv[2 * (o + i)] = (double)q.x;
+        uv[2 * (o + i) + 1] = (double)q.y;
+    }
+}
+
+extern "C" int msfm_gather_3d2d(const int32_t* d_corr_row, const int32_t* d_corr_fid, int32_t m_pad,
+                                int32_t n_sel, const int64_t* d_sel, const int64_t* d_row0,
+                                const int64_t* d_out_off, const double* d_xyz,
+                                const float* d_bank_xy, double* d_X, double* d_uv, void* stream) {
+    if (n_sel < 0 || m_pad < 0) {
+        set_error("msfm_gather_3d2d: bad arguments");
+        return MSFM_EINVAL;
+    }
+    if (n_sel == 0) return MSFM_OK;
+    gather_3d2d_kernel<<<n_sel, 256, 0, (cudaStream_t)stream>>>(
+        d_corr_row, d_corr_fid, m_pad, d_sel, d_row0, d_out_off, d_xyz,
+        reinterpret_cast<const float2*>(d_bank_xy), d_X, d_uv);
+    MSFM_LAUNCH_CHECK();
+    count_launches(1);
+    return MSFM_OK;
+}
+
 extern "C" int msfm_direct_3d2d(const msfm_bank* bank, int32_t n_points, const int32_t* d_n,
                                 const int64_t* d_SS, int32_t n_images, const int32_t* d_images,
                                 const int32_t* d_k1, const int32_t* d_i1, const int32_t* d_k2,

@@ -221,6 +221,38 @@ def direct_search(bank: FeatureBank, pts: PointSet, image_ids, *, ratio: float =
     return res
 
 
+def gather_pnp_inputs(bank: FeatureBank, corr: Correspondences, image_ids, d_xyz,
+                      gate: int = MIN_CORRESPONDENCES, stream=None):
+    """The PnP inputs of the images with more than ``gate`` correspondences
+    (localize.py:203-211) straight from ``direct_search(to_host=False)``: X (N, 3)
+    and uv (N, 2) f64 on the device (msfm_gather_3d2d, one launch), per-image
+    offsets (host) and the selected positions in ``image_ids``.  One small copy
+    each way (the counts back, the selection out)."""
+    import torch
+
+    lib = _lib.load()
+    dev = bank.device
+    B = len(image_ids)
+    c = corr.counts[:B].cpu().numpy().astype(np.int64)
+    todo = np.flatnonzero(c > gate)
+    off = np.zeros(len(todo) + 1, np.int64)
+    np.cumsum(c[todo], out=off[1:])
+    N = int(off[-1])
+    row0 = bank.offsets[bank.slots(np.asarray(image_ids)[todo])] if len(todo) else \
+        np.zeros(0, np.int64)
+    meta = torch.from_numpy(np.concatenate([todo.astype(np.int64), row0, off])).pin_memory()
+    d_meta = meta.to(dev, non_blocking=True)
+    k = len(todo)
+    X = torch.empty((max(N, 1), 3), dtype=torch.float64, device=dev)
+    uv = torch.empty((max(N, 1), 2), dtype=torch.float64, device=dev)
+    base = _lib.ptr(d_meta)
+    _lib.check(lib.msfm_gather_3d2d(_lib.ptr(corr.rows), _lib.ptr(corr.fids), corr.M_pad, k, base,
+                                    base + 8 * k, base + 16 * k, _lib.ptr(d_xyz),
+                                    _lib.ptr(bank.xy), _lib.ptr(X), _lib.ptr(uv),
+                                    _lib.stream_handle(stream)), "msfm_gather_3d2d")
+    return X[:N], uv[:N], off, todo
+
+
 # ---------------------------------------------------------------------------
 # reference-shaped stage API (localize.py:33-281)
 # ---------------------------------------------------------------------------

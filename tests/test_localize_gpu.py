@@ -68,6 +68,35 @@ def test_direct_search_equals_reference(name):
         np.testing.assert_array_equal(got[s], z[f"q{q}_corr"])
 
 
+@pytest.mark.parametrize("name", ["localize_holdout.npz", "localize_c2mini.npz"])
+def test_gather_pnp_inputs_equals_host_gather(name):
+    """msfm_gather_3d2d: X / uv of the gated images == the host gather of the
+    reference's correspondences (localize.py:203-211)."""
+    import torch
+
+    from paper_1512_06235_b200.bank import FeatureBank
+    from paper_1512_06235_b200.localize import PointSet, direct_search, gather_pnp_inputs
+    from paper_1512_06235_b200 import scenes
+
+    kw, scene, snap, z = load_localize(name)
+    S, n = scenes.track_sums(scene, snap)
+    pts = PointSet(S=S, n=n, ids=np.arange(len(S)))
+    qs = [int(q) for q in z["queries"]]
+    bank = FeatureBank({q: scene.feature_sets[q] for q in qs})
+    corr = direct_search(bank, pts, qs, to_host=False)
+    d_xyz = torch.from_numpy(np.ascontiguousarray(snap.point_xyz)).cuda()
+    for gate in (16, 0, 10**9):
+        X, uv, off, todo = gather_pnp_inputs(bank, corr, qs, d_xyz, gate=gate)
+        want = [k for k, q in enumerate(qs) if len(z[f"q{q}_corr"]) > gate]
+        assert todo.tolist() == want
+        X, uv = X.cpu().numpy(), uv.cpu().numpy()
+        for j, k in enumerate(todo):
+            c = z[f"q{qs[k]}_corr"]
+            np.testing.assert_array_equal(X[off[j]:off[j + 1]], snap.point_xyz[c[:, 0]])
+            np.testing.assert_array_equal(uv[off[j]:off[j + 1]],
+                                          scene.feature_sets[qs[k]].xy[c[:, 1]].astype(np.float64))
+
+
 class _NoGraph:
     def neighbors(self, image_id):
         return []

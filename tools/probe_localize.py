@@ -6,7 +6,7 @@ import numpy as np, torch
 import bench
 from paper_1512_06235_b200 import scenes
 from paper_1512_06235_b200.bank import FeatureBank, HostBank
-from paper_1512_06235_b200.localize import PointSet, direct_search, upload_points
+from paper_1512_06235_b200.localize import PointSet, direct_search, gather_pnp_inputs, upload_points
 from paper_1512_06235_b200.pnp import pnp_batch_flat
 
 scene, snap, queries = bench.build_localization()
@@ -31,18 +31,9 @@ def tick(name, t0):
 
 def step():
     t0 = time.perf_counter()
-    prow, fid, off = direct_search(bank, pts, queries, device_points=dp, device_flat=True)
-    t0 = tick("direct_search (kNN + ratio + dedupe, counts D2H)", t0)
-    cnt = np.diff(off)
-    todo = np.flatnonzero(cnt > 16)
-    sel = np.concatenate([np.arange(off[k], off[k + 1]) for k in todo])
-    img_of = np.repeat(np.arange(len(queries)), cnt)[sel]
-    d_sel = torch.from_numpy(sel).to(dev)
-    d_row = torch.from_numpy(bank.offsets[img_of]).to(dev) + fid[d_sel]
-    X = d_xyz[prow[d_sel]]
-    uv = bank.xy[d_row].to(torch.float64)
-    toff = np.zeros(len(todo) + 1, np.int64)
-    np.cumsum(cnt[todo], out=toff[1:])
+    corr = direct_search(bank, pts, queries, device_points=dp, to_host=False)
+    t0 = tick("direct_search (kNN + ratio + dedupe)", t0)
+    X, uv, toff, todo = gather_pnp_inputs(bank, corr, queries, d_xyz)
     t0 = tick("gather", t0)
     res = pnp_batch_flat(X, uv, toff, [Ks[k] for k in todo], [queries[k] for k in todo], device=dev,
                          timing=PT)
