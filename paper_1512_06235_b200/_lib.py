@@ -163,6 +163,15 @@ def ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
 
+def h2d(a, dev):
+    """A small host array on the device through pinned memory, asynchronously
+    (a pageable copy would block the host until the stream drains)."""
+    import numpy as np
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().to(dev, non_blocking=True)
+
+
 def stream_handle(stream=None) -> int:
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()

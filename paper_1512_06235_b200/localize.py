@@ -106,7 +106,7 @@ def knn2_tracks(bank: FeatureBank, pts: PointSet, image_ids, stream=None,
         device_points = upload_points(pts, dev)
     dS, dn, dSS = device_points
     slots = np.array([bank.index_of[int(i)] for i in image_ids], dtype=np.int32)
-    d_slots = torch.from_numpy(slots).to(dev)
+    d_slots = _lib.h2d(slots, dev)
     k1 = torch.empty((max(len(slots), 1), M_pad), dtype=torch.int32, device=dev)
     i1 = torch.empty_like(k1)
     k2 = torch.empty_like(k1)
@@ -117,7 +117,7 @@ def knn2_tracks(bank: FeatureBank, pts: PointSet, image_ids, stream=None,
     b = bank.cstruct()
     d_cnt = None
     if counts is not None:
-        d_cnt = torch.from_numpy(cnt.astype(np.int32)).to(dev)
+        d_cnt = _lib.h2d(cnt.astype(np.int32), dev)
         b.d_img_n = _lib.ptr(d_cnt)
     maxn = int(pts.n.max()) if M else 0
     _lib.check(lib.msfm_knn2_tracks(ctypes.byref(b), M, _lib.ptr(dS), _lib.ptr(dn), len(slots),
@@ -177,12 +177,12 @@ def direct_search(bank: FeatureBank, pts: PointSet, image_ids, *, ratio: float =
     dS, dn, dSS = device_points
     M = len(pts.n)
     slots = np.array([bank.index_of[int(i)] for i in image_ids], dtype=np.int32)
-    d_slots = torch.from_numpy(slots).to(dev)
+    d_slots = _lib.h2d(slots, dev)
     nfeat = bank.counts[slots].astype(np.int64)
     win_off = np.zeros(len(slots), np.int64)
     if len(slots) > 1:
         np.cumsum(nfeat[:-1], out=win_off[1:])
-    d_win_off = torch.from_numpy(win_off).to(dev)
+    d_win_off = _lib.h2d(win_off, dev)
     win = torch.empty(max(int(nfeat.sum()), 1), dtype=torch.int32, device=dev)
     rows = torch.empty((max(len(slots), 1), knn.M_pad), dtype=torch.int32, device=dev)
     fids = torch.empty_like(rows)

@@ -178,7 +178,7 @@ class _Batch:
             if len(rows) else np.zeros(0, np.int64)
         off = np.zeros(len(rows) + 1, np.int64)
         np.cumsum(self.n[rows], out=off[1:])
-        d_sel = torch.from_numpy(sel).to(dev)
+        d_sel = _lib.h2d(sel, dev)
         return _Batch(dev, None, None, K_list, flat=(self.X[d_sel], self.uv[d_sel], off))
 
 
@@ -294,14 +294,13 @@ def pnp_batch(X_list, uv_list, K_list, seeds, *, threshold=PNP_THRESHOLD_PX,
     if status.any():
         d_best = torch.zeros((A, 12), dtype=torch.float64, device=dev)
         if src1:
-            ks = torch.tensor([x[0] for x in src1], device=dev)
-            hs = torch.tensor([x[1] for x in src1], device=dev)
-            d_best[ks] = d_hyp1[ks, hs]
+            s1 = np.array(src1, np.int64).reshape(-1, 2)
+            ks = _lib.h2d(s1[:, 0], dev)
+            d_best[ks] = d_hyp1.reshape(-1, 12)[_lib.h2d(s1[:, 0] * H1 + s1[:, 1], dev)]
         if src2:
-            ks = torch.tensor([x[0] for x in src2], device=dev)
-            js = torch.tensor([x[1] for x in src2], device=dev)
-            hs = torch.tensor([x[2] for x in src2], device=dev)
-            d_best[ks] = d_hyp2[js, hs]
+            s2 = np.array(src2, np.int64).reshape(-1, 3)
+            ks = _lib.h2d(s2[:, 0], dev)
+            d_best[ks] = d_hyp2.reshape(-1, 12)[_lib.h2d(s2[:, 1] * d_hyp2.shape[1] + s2[:, 2], dev)]
         _refit(lib, batch, status, d_best, threshold, min_inliers, st, dev, results, active, best)
     mark("refit + results")
     return results
@@ -328,7 +327,7 @@ def _refit(lib, batch, status, d_best, threshold, min_inliers, st, dev, results,
     import torch
 
     A = len(status)
-    d_status = torch.from_numpy(status).to(dev)
+    d_status = _lib.h2d(status, dev)
     d_R = torch.zeros((A, 9), dtype=torch.float64, device=dev)
     d_t = torch.zeros((A, 3), dtype=torch.float64, device=dev)
     d_mask = torch.zeros(max(int(batch.off_h[-1]), 1), dtype=torch.uint8, device=dev)
