@@ -1154,6 +1154,9 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
             // afterwards (rare; top-2 is insensitive to the push order).
             constexpr int NE = 4 * SG_NT;
             unsigned ucm = 0;
+#ifdef MSFM_MATCH_TILE_STATS
+            unsigned inb = 0;
+#endif
             bool any0 = false, any1 = false;
 #pragma unroll
             for (int e = 0; e < NE; e++) {
@@ -1161,6 +1164,9 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
                 const bool rowhi = q >= 2;
                 const float2 P = rowhi ? p1 : p0;
                 const float av = fabsf(fmaf(ML[c].x, P.x, fmaf(ML[c].y, P.y, ML[c].z)));
+#ifdef MSFM_MATCH_TILE_STATS
+                if (a.dbg && av <= __uint_as_float(MH[c].x) && (rowhi ? r1 : r0) < n) inb |= 1u << e;
+#endif
                 const bool cbit = ((rowhi ? cm1 : cm0) >> (MH[c].w >> 24)) & 1u;
                 const bool sure_in = av <= ML[c].w && cbit;
                 if (!(av <= ML[c].w) && av <= __uint_as_float(MH[c].x) && cbit) ucm |= 1u << e;
@@ -1168,6 +1174,29 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
                 const unsigned key = (rowhi ? tb1 : tb0) + MH[c].y - ((unsigned)acc[nt][q] << 10);
                 top2_push(sure_in ? key : NONE, b1[c], b2[c]);
             }
+#ifdef MSFM_MATCH_TILE_STATS
+            if (a.dbg) {
+                // band-reach occupancy of the tile: elements near some member band, and
+                // (tile, 8-member block)s with none (MMA + epilogue work a skip could save)
+                int blk_empty = 0, blk = 0;
+#pragma unroll
+                for (int nt = 0; nt < SG_NT; nt++) {
+                    if (mt0 + nt * 8 >= m) continue;
+                    blk++;
+                    if (!__any_sync(FULL, ((inb >> (4 * nt)) & 0xFu) != 0)) blk_empty++;
+                }
+                unsigned ne = __popc(inb);
+#pragma unroll
+                for (int o = 16; o; o >>= 1) ne += __shfl_xor_sync(FULL, ne, o);
+                if (lane == 0) {
+                    const int rv = min(16, n - mt * 16), cv = min(16, m - mt0);
+                    atomicAdd(&a.dbg[10], (unsigned long long)(rv * cv));
+                    atomicAdd(&a.dbg[11], (unsigned long long)ne);
+                    atomicAdd(&a.dbg[12], (unsigned long long)blk_empty);
+                    atomicAdd(&a.dbg[13], (unsigned long long)blk);
+                }
+            }
+#endif
             if (__any_sync(FULL, ucm != 0)) {
 #pragma unroll
                 for (int e = 0; e < NE; e++) {
