@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(MSFM_LINES_T) lines_kernel(ChunkArgs a) {
 // super-groups, never any result.
 constexpr int GB = 4096;
 constexpr int GT = 1024;   // groups_kernel threads per pair
-__global__ void __launch_bounds__(GT) groups_kernel(ChunkArgs a) {
+__global__ void __launch_bounds__(GT, 2) groups_kernel(ChunkArgs a) {
     __shared__ int sm[GT / 32 + 1];
     __shared__ int hist[GB];
     __shared__ float fmin_s[GT / 32], fmax_s[GT / 32];
@@ -743,7 +743,7 @@ __global__ void __launch_bounds__(128) sg_shape_kernel(ChunkArgs a, int max_sg) 
 // Per member (thread per member position): epilogue constants, the member band's
 // deviation from its group's representative line (-> GroupRec.maxdev) and from its
 // super-group's base line (-> sgdev), both as atomic maxima.
-__global__ void __launch_bounds__(128) member_kernel(ChunkArgs a, int max_pos) {
+__global__ void __launch_bounds__(128, 12) member_kernel(ChunkArgs a, int max_pos) {
     const int pos = blockIdx.x * blockDim.x + threadIdx.x;
     if (pos >= max_pos) return;
     const int gid = a.mgid[pos];
