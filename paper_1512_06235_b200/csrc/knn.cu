@@ -16,7 +16,7 @@
 //               accumulators in TMEM (2 stages x 2 planes x 128 columns)
 //   warp 2      TMEM allocator
 //   warps 4-11  epilogue: tcgen05.ld -> key -> top-2, 2 warps per lane quadrant
-// unit = (128-point tile, image); tile = 128 features of that image.
+// unit = (image, 128-point tile), image-major; tile = 128 features of that image.
 #include <cuda.h>
 #include <stdint.h>
 
@@ -180,8 +180,10 @@ __device__ __forceinline__ void tc_fence_after() {
 
 __device__ __forceinline__ int unit_tiles(const KnnArgs& a, int u, int& img, int& mt, int64_t& off,
                                           int& n) {
-    mt = u / a.n_img;
-    const int s = u - mt * a.n_img;
+    // image-major: the CTAs running at one time share a few images' feature tiles
+    // (L2 hits) instead of streaming every image once per point tile
+    const int s = u / a.m_tiles;
+    mt = u - s * a.m_tiles;
     img = a.images[s];
     off = a.img_off[img];
     n = a.img_n[img];
@@ -301,7 +303,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_lo, const __grid_constant_
             const int np = grow < a.M_pad ? a.n[grow] : 0;
             {
                 // stage the image's |f|^2 row in shared memory (broadcast reads per chunk)
-                const int slot = u - mt * a.n_img;
+                const int slot = u / a.m_tiles;     // image slot of the unit (unit_tiles)
                 const int4* src = reinterpret_cast<const int4*>(a.fn_pad + (int64_t)slot * a.fn_stride);
                 int4* dst = reinterpret_cast<int4*>(S.fvs);
                 for (int i = ew * 32 + lane; i < a.fn_stride / 4; i += EPI_WARPS * 32) dst[i] = __ldg(src + i);
@@ -367,7 +369,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_lo, const __grid_constant_
                     if (other_first) { k1 = ok1; i1 = oi1; }
                     k2 = min(hi_k, min(k2, ok2));
                 }
-                const int slot = u - mt * a.n_img;
+                const int slot = u / a.m_tiles;     // image slot of the unit (unit_tiles)
                 if (grow < a.M_pad) {
                     const int64_t o = (int64_t)slot * a.M_pad + grow;
                     a.out_k1[o] = k1; a.out_i1[o] = i1; a.out_k2[o] = k2;
