@@ -105,8 +105,10 @@ def _matches(types, qid, tid, rows, tgts, d, r, qmap=None, tmap=None):
     FR, M = types[0], types[1]
     qm = rows if qmap is None else qmap[rows]
     tm = tgts if tmap is None else tmap[tgts]
-    return [M(query=FR(qid, int(a)), target=FR(tid, int(b)), distance=float(c), ratio=float(e))
-            for a, b, c, e in zip(qm, tm, d, r)]
+    return [M(query=FR(qid, a), target=FR(tid, b), distance=c, ratio=e)
+            for a, b, c, e in zip(np.asarray(qm).tolist(), np.asarray(tm).tolist(),
+                                  np.asarray(d, np.float64).tolist(),
+                                  np.asarray(r, np.float64).tolist())]
 
 
 def match_pair(query_fs, target_fs, *, ratio=RATIO_UNGUIDED, query_indices=None,
@@ -215,14 +217,22 @@ def build_coarse_matchgraph(feature_sets, *, ratio=RATIO_UNGUIDED, preemptive=Fa
                                      HYBRID_BATCH_FRACTION, HYBRID_CONTINUE_MIN, early_stop,
                                      SINGLE_CANDIDATE_CAP, int(tiers[pos[b]]), stats)
     cand, q_list, c_list, seeds = [], [], [], []
+    xy64 = {}
+
+    def xy_of(i):
+        v = xy64.get(i)
+        if v is None:
+            v = xy64[i] = np.asarray(feature_sets[i].xy, np.float64)
+        return v
+
     for a, b in pairs:
         h = hybrid.get((a, b))
         if h is None or len(h[0]) < min_edge_matches:
             continue
         rows, tg = h[0], h[1]
         cand.append((a, b))
-        q_list.append(np.asarray(feature_sets[a].xy, np.float64)[rows])
-        c_list.append(np.asarray(feature_sets[b].xy, np.float64)[tg])
+        q_list.append(xy_of(a)[rows])
+        c_list.append(xy_of(b)[tg])
         seeds.append(seed + a * 100003 + b)
     geo = fransac_batch(q_list, c_list, seeds) if cand else []
     graph = MG()
@@ -236,8 +246,9 @@ def build_coarse_matchgraph(feature_sets, *, ratio=RATIO_UNGUIDED, preemptive=Fa
         if int(g.mask.sum()) < min_edge_inliers:
             continue
         rows, tg, dd, rr = hybrid[(a, b)]
-        ms = [M(query=FR(a, int(x)), target=FR(b, int(y)), distance=float(c), ratio=float(e))
-              for x, y, c, e in zip(rows, tg, dd, rr)]
+        # Python scalars first (.tolist()): the objects are built without numpy scalars
+        ms = [M(query=FR(a, x), target=FR(b, y), distance=c, ratio=e)
+              for x, y, c, e in zip(rows.tolist(), tg.tolist(), dd.tolist(), rr.tolist())]
         geom = G(F=g.F, inlier_count=g.inlier_count, degenerate_planar=g.degenerate_planar)
         graph.edges[(a, b)] = E(matches=ms, geometry=geom, inlier_mask=g.mask)
     if on_overflow == "drop":

@@ -23,3 +23,11 @@ _lib.profile_enable(False)
 P = n * (n - 1) // 2
 print(f"cams={n} pairs={P} edges={len(g.edges)} overflow={len(g.overflow_pairs)} wall {dt*1e3:.1f} ms ({P/dt:.0f} pairs/s)  " +
       "  ".join(f"{nm} {v[0]:.2f}ms/{v[1]}" for nm, v in k.items()))
+
+import cProfile, pstats
+pr = cProfile.Profile()
+pr.enable()
+build_coarse_matchgraph(store.sets, on_overflow="drop")
+torch.cuda.synchronize()
+pr.disable()
+pstats.Stats(pr).sort_stats("tottime").print_stats(25)
