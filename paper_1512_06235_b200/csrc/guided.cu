@@ -1131,14 +1131,6 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
             const int r0 = mt * 16 + g, r1 = r0 + 8;
             const unsigned cm0 = r0 < n ? S.cmask[r0] : 0u, cm1 = r1 < n ? S.cmask[r1] : 0u;
             const float2 p0 = S.xy[r0 < n ? r0 : 0], p1 = S.xy[r1 < n ? r1 : 0];
-            float4 ML[NC];
-            uint4 MH[NC];
-#pragma unroll
-            for (int c = 0; c < NC; c++) {
-                const MemberRec* Mc = &S.mr[(c >> 1) * 8 + 2 * t + (c & 1)];
-                ML[c] = lds_f4(&Mc->a);      // a, b, c, lo
-                MH[c] = lds_u4(&Mc->hi);     // hi, qn9, fid, slotgi
-            }
             int acc[SG_NT][4];
 #pragma unroll
             for (int nt = 0; nt < SG_NT; nt++) {
@@ -1158,21 +1150,29 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
             unsigned inb = 0;
 #endif
             bool any0 = false, any1 = false;
+            // column by column: one member's constants (two 16-B shared loads) live at a
+            // time, used by its two elements of this lane
 #pragma unroll
-            for (int e = 0; e < NE; e++) {
-                const int nt = e >> 2, q = e & 3, c = nt * 2 + (q & 1);
-                const bool rowhi = q >= 2;
+            for (int c = 0; c < NC; c++) {
+              const MemberRec* Mc = &S.mr[(c >> 1) * 8 + 2 * t + (c & 1)];
+              const float4 MLc = lds_f4(&Mc->a);      // a, b, c, lo
+              const uint4 MHc = lds_u4(&Mc->hi);      // hi, qn9, fid, slotgi
+#pragma unroll
+              for (int rh = 0; rh < 2; rh++) {
+                const int nt = c >> 1, q = (c & 1) + 2 * rh, e = nt * 4 + q;
+                const bool rowhi = rh != 0;
                 const float2 P = rowhi ? p1 : p0;
-                const float av = fabsf(fmaf(ML[c].x, P.x, fmaf(ML[c].y, P.y, ML[c].z)));
+                const float av = fabsf(fmaf(MLc.x, P.x, fmaf(MLc.y, P.y, MLc.z)));
 #ifdef MSFM_MATCH_TILE_STATS
-                if (a.dbg && av <= __uint_as_float(MH[c].x) && (rowhi ? r1 : r0) < n) inb |= 1u << e;
+                if (a.dbg && av <= __uint_as_float(MHc.x) && (rowhi ? r1 : r0) < n) inb |= 1u << e;
 #endif
-                const bool cbit = ((rowhi ? cm1 : cm0) >> (MH[c].w >> 24)) & 1u;
-                const bool sure_in = av <= ML[c].w && cbit;
-                if (!(av <= ML[c].w) && av <= __uint_as_float(MH[c].x) && cbit) ucm |= 1u << e;
+                const bool cbit = ((rowhi ? cm1 : cm0) >> (MHc.w >> 24)) & 1u;
+                const bool sure_in = av <= MLc.w && cbit;
+                if (!(av <= MLc.w) && av <= __uint_as_float(MHc.x) && cbit) ucm |= 1u << e;
                 if (STATS) { if (rowhi) any1 |= sure_in; else any0 |= sure_in; }
-                const unsigned key = (rowhi ? tb1 : tb0) + MH[c].y - ((unsigned)acc[nt][q] << 10);
+                const unsigned key = (rowhi ? tb1 : tb0) + MHc.y - ((unsigned)acc[nt][q] << 10);
                 top2_push(sure_in ? key : NONE, b1[c], b2[c]);
+              }
             }
 #ifdef MSFM_MATCH_TILE_STATS
             if (a.dbg) {
@@ -1204,12 +1204,13 @@ __device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t to
                     const int nt = e >> 2, q = e & 3, c = nt * 2 + (q & 1);
                     const bool rowhi = q >= 2;
                     const float2 P = rowhi ? p1 : p0;
-                    const GroupRec& Gc = a.grp[SG.g0 + (int)(MH[c].w >> 24)];
+                    const uint4 MHc = lds_u4(&S.mr[(c >> 1) * 8 + 2 * t + (c & 1)].hi);
+                    const GroupRec& Gc = a.grp[SG.g0 + (int)(MHc.w >> 24)];
                     const bool gemv = Gc.cnt == 1;
-                    const double* L = gemv ? &Gc.sl0 : a.q_line + 3 * (int64_t)(MH[c].w & 0xFFFFFFu);
+                    const double* L = gemv ? &Gc.sl0 : a.q_line + 3 * (int64_t)(MHc.w & 0xFFFFFFu);
                     if (band_exact(L[0], L[1], L[2], gemv, (double)P.x, (double)P.y, a.d)) {
                         if (STATS) { if (rowhi) any1 = true; else any0 = true; }
-                        const unsigned key = (rowhi ? tb1 : tb0) + MH[c].y - ((unsigned)acc[nt][q] << 10);
+                        const unsigned key = (rowhi ? tb1 : tb0) + MHc.y - ((unsigned)acc[nt][q] << 10);
                         top2_push(key, b1[c], b2[c]);
                     }
                 }
