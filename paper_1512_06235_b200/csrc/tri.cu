@@ -200,7 +200,11 @@ __global__ void __launch_bounds__(128) tri_kernel(TriArgs a) {
     Xo[0] = X[0]; Xo[1] = X[1]; Xo[2] = X[2];
     a.err[k] = err;
     if (!isfinite(err) || !depth_ok || err > a.max_error) { a.status[k] = 0; return; }
-    // widest pairwise ray angle >= min_angle (geometry.py:350-356)
+    // widest pairwise ray angle >= min_angle (geometry.py:350-356).  The gate only
+    // asks whether the widest angle reaches min_angle: the first pair whose own
+    // angle (the same acos formula, monotone in the cosine) reaches it settles the
+    // status, so well-spread tracks stop after a few pairs instead of n^2/2
+    const double deg = 180.0 / 3.141592653589793;
     double minc = 1.0;
     for (int i = 0; i < n; i++) {
         double ri[3];
@@ -220,10 +224,16 @@ __global__ void __launch_bounds__(128) tri_kernel(TriArgs a) {
             for (int j = 0; j < 3; j++) rj[j] = X[j] + (R[j] * t[0] + R[3 + j] * t[1] + R[6 + j] * t[2]);
             const double nr = fmax(sqrt(rj[0] * rj[0] + rj[1] * rj[1] + rj[2] * rj[2]), 1e-15);
             const double cs = (ri[0] * rj[0] + ri[1] * rj[1] + ri[2] * rj[2]) / nr;
-            minc = fmin(minc, cs);
+            if (cs < minc) {
+                minc = cs;
+                if (!(acos(fmin(fmax(minc, -1.0), 1.0)) * deg < a.min_angle_deg)) {
+                    a.status[k] = 1;
+                    return;
+                }
+            }
         }
     }
-    const double ang = acos(fmin(fmax(minc, -1.0), 1.0)) * (180.0 / 3.141592653589793);
+    const double ang = acos(fmin(fmax(minc, -1.0), 1.0)) * deg;
     a.status[k] = ang < a.min_angle_deg ? 0 : 1;
 }
 

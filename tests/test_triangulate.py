@@ -82,3 +82,52 @@ def test_device_dropin_edge_cases():
             assert abs(r.mean_error - float(Z[f"e{k}_err"])) < 1e-6
     with pytest.raises(InsufficientDataError):
         triangulate_track(obs[:1])
+
+
+@pytest.mark.gpu
+def test_device_angle_gate_on_long_narrow_tracks():
+    """The widest-ray-angle gate (geometry.py:350-356) around its threshold on long
+    tracks (the kernel stops at the first pair that reaches min_angle): statuses,
+    points and errors equal to the oracle's full pairwise scan."""
+    from paper_1512_06235_b200.triangulation import triangulate_batch
+
+    rng = np.random.default_rng(7)
+    C = 240
+    ang = np.radians(np.arange(C) * 0.06)                 # 0.06 deg between neighbours
+    K = np.tile(np.array([[2600.0, 0, 1536], [0, 2600.0, 1152], [0, 0, 1]]), (C, 1, 1))
+    R = np.zeros((C, 3, 3))
+    t = np.zeros((C, 3))
+    for c in range(C):
+        cen = np.array([8 * np.cos(ang[c]), 0.0, 8 * np.sin(ang[c])])
+        z = -cen / np.linalg.norm(cen)
+        x = np.cross([0, 1.0, 0], z)
+        x /= np.linalg.norm(x)
+        R[c] = np.stack([x, np.cross(z, x), z])
+        t[c] = -R[c] @ cen
+    T = 400
+    lens = rng.integers(2, 60, size=T)
+    ptr = np.zeros(T + 1, np.int64)
+    np.cumsum(lens, out=ptr[1:])
+    cam = np.empty(ptr[-1], np.int32)
+    pix = np.empty((ptr[-1], 2))
+    for k in range(T):
+        c0 = int(rng.integers(0, C - lens[k]))
+        cs = c0 + rng.permutation(lens[k])               # shuffled view order
+        cam[ptr[k]:ptr[k + 1]] = cs
+        Xw = rng.normal(size=3) * 0.5
+        xc = np.einsum("cij,j->ci", R[cs], Xw) + t[cs]
+        uv = np.einsum("cij,cj->ci", K[cs], xc)
+        pix[ptr[k]:ptr[k + 1]] = uv[:, :2] / uv[:, 2:3] + rng.normal(size=(lens[k], 2)) * 0.2
+    st, X, err = triangulate_batch(K, R, t, ptr, cam, pix)
+    code = {"ok": 1, "rejected": 0, "degenerate": -1}
+    n_rej = 0
+    for k in range(T):
+        lo, hi = ptr[k], ptr[k + 1]
+        c = cam[lo:hi]
+        s, Xo, eo = otri.triangulate(K[c], R[c], t[c], pix[lo:hi])
+        assert st[k] == code[s], k
+        n_rej += s == "rejected"
+        if s == "ok":
+            np.testing.assert_allclose(X[k], Xo, rtol=1e-6, atol=1e-9)
+            np.testing.assert_allclose(err[k], eo, atol=1e-6)
+    assert 0 < n_rej < T                                  # both sides of the gate exercised
