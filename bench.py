@@ -270,7 +270,7 @@ def run_b200(args, rank, world):
     tpp = ncu_traffic_per_pair()
 
     # ---- the stage's next step on the same matches: device track merge (densify.py:68-158)
-    merge = track_merge_leg(bank, wl, mine, res, snap, dev)
+    merge = track_merge_leg(bank, wl, mine, res, snap, dev, scene)
 
     # ---- e2e through the public API with host buffers (pinned H2D + D2H every step)
     torch.cuda.synchronize()
@@ -389,7 +389,7 @@ def coarse_graph_leg(dev, n_cameras=40):
             "wall_ms": dt * 1e3, "kernel_ms": kern}
 
 
-def track_merge_leg(bank, wl, mine, res, snap, dev):
+def track_merge_leg(bank, wl, mine, res, snap, dev, scene=None):
     """msfm_merge_tracks over this rank's matches + the coarse tracks (bank nodes)."""
     import torch
 
@@ -417,7 +417,46 @@ def track_merge_leg(bank, wl, mine, res, snap, dev):
                     "tracks, union-find over bank feature rows", "matches": int(n),
             "nodes": int(bank.n_total), "tracks": int(len(snap.track_ptr) - 1), "ms": ms,
             "edges_per_s": n / (ms / 1e3) if ms > 0 else None,
-            "new_tracks": int((owners < 0).sum()), "extended_tracks": int((owners >= 0).sum())}
+            "new_tracks": int((owners < 0).sum()), "extended_tracks": int((owners >= 0).sum()),
+            "triangulation": triangulation_leg(scene, bank, nodes, owners, offs)}
+
+
+def triangulation_leg(scene, bank, nodes, owners, offs):
+    """Batched multi-view DLT triangulation (geometry.py:276-357) of the new tracks
+    the merge produced: one msfm_triangulate_batch launch (C3 cameras = images)."""
+    import torch
+
+    from paper_1512_06235_b200 import _lib
+    from paper_1512_06235_b200.triangulation import triangulate_batch
+
+    if scene is None:
+        return None
+    new = np.flatnonzero(np.asarray(owners) < 0)
+    seg = np.diff(offs)[new]
+    ptr = np.zeros(len(new) + 1, np.int64)
+    np.cumsum(seg, out=ptr[1:])
+    sel = np.concatenate([np.arange(offs[s], offs[s + 1]) for s in new]) if len(new) else \
+        np.zeros(0, np.int64)
+    nd = np.asarray(nodes)[sel]
+    slot = np.searchsorted(bank.offsets, nd, "right") - 1
+    cam = np.asarray(bank.image_ids, np.int64)[slot].astype(np.int32)
+    pix = bank.host.xy.numpy()[nd].astype(np.float64)
+    K = np.stack([c.K for c in scene.cameras])
+    R = np.stack([c.R for c in scene.cameras])
+    t = np.stack([np.asarray(c.t).reshape(3) for c in scene.cameras])
+    triangulate_batch(K, R, t, ptr, cam, pix)
+    torch.cuda.synchronize()
+    _lib.profile_enable(True)
+    t0 = time.perf_counter()
+    st, X, err = triangulate_batch(K, R, t, ptr, cam, pix)
+    wall = time.perf_counter() - t0
+    ms, _ = _lib.profile_read("tri_kernel")
+    _lib.profile_enable(False)
+    return {"what": "msfm_triangulate_batch over the merge's new tracks (DLT, Gauss-Newton, "
+                    "depth / reprojection / angle gates)", "tracks": int(len(new)),
+            "views": int(ptr[-1]), "kernel_ms": ms, "call_ms": wall * 1e3,
+            "tracks_per_s": len(new) / (ms / 1e3) if ms > 0 else None,
+            "accepted": int((st == 1).sum())}
 
 
 # ------------------------------------------------------- localization leg ---
