@@ -624,6 +624,50 @@ __device__ __forceinline__ int find_pair(const int32_t* gstart, int npairs, int 
 // Upper bound of |dist_m(f) - dist_r(f)| over the image rectangle restricted to
 // the member's band (|dist_m| <= d + 0.5): the difference is affine, so its
 // maximum over that convex polygon sits at one of its vertices.
+// band_deviation of one member line against two lines at once: the points where
+// the member band is extremal (corners, band-edge / border crossings, with their
+// divisions) depend only on m and are evaluated once for both.
+__device__ void band_deviation2(const double m[3], const double r[3], const double b[3],
+                                double W, double H, double d, double& dev_r, double& dev_b) {
+    const double ra = m[0] - r[0], rb = m[1] - r[1], rc = m[2] - r[2];
+    const double ba = m[0] - b[0], bb = m[1] - b[1], bc = m[2] - b[2];
+    const double B = d + 0.5;
+    dev_r = 0.0;
+    dev_b = 0.0;
+    const double cx[4] = {0.0, W, 0.0, W}, cy[4] = {0.0, 0.0, H, H};
+    for (int k = 0; k < 4; k++) {
+        double dm = m[0] * cx[k] + m[1] * cy[k] + m[2];
+        if (fabs(dm) <= B) {
+            dev_r = fmax(dev_r, fabs(ra * cx[k] + rb * cy[k] + rc));
+            dev_b = fmax(dev_b, fabs(ba * cx[k] + bb * cy[k] + bc));
+        }
+    }
+    const double i1 = fabs(m[1]) > 1e-12 ? 1.0 / m[1] : 0.0;
+    const double i0 = fabs(m[0]) > 1e-12 ? 1.0 / m[0] : 0.0;
+    for (int s = -1; s <= 1; s += 2) {
+        if (i1 != 0.0) {
+            for (int e = 0; e < 2; e++) {
+                double x = e ? W : 0.0;
+                double y = (s * B - m[2] - m[0] * x) * i1;
+                if (y >= -1e-6 && y <= H + 1e-6) {
+                    dev_r = fmax(dev_r, fabs(ra * x + rb * y + rc));
+                    dev_b = fmax(dev_b, fabs(ba * x + bb * y + bc));
+                }
+            }
+        }
+        if (i0 != 0.0) {
+            for (int e = 0; e < 2; e++) {
+                double y = e ? H : 0.0;
+                double x = (s * B - m[2] - m[1] * y) * i0;
+                if (x >= -1e-6 && x <= W + 1e-6) {
+                    dev_r = fmax(dev_r, fabs(ra * x + rb * y + rc));
+                    dev_b = fmax(dev_b, fabs(ba * x + bb * y + bc));
+                }
+            }
+        }
+    }
+}
+
 __device__ double band_deviation(const double m[3], const double r[3], double W, double H,
                                  double d) {
     const double da = m[0] - r[0], db = m[1] - r[1], dc = m[2] - r[2];
@@ -771,13 +815,14 @@ __global__ void __launch_bounds__(128, 12) member_kernel(ChunkArgs a, int max_po
     }
     const double* rl = a.q_line + 3 * (int64_t)G.rep;
     const double r[3] = {rl[0], rl[1], rl[2]};
-    const float gdev = (float)(band_deviation(m, r, W, H, d) + 0.05);
-    atomicMax(reinterpret_cast<unsigned*>(&G.maxdev), __float_as_uint(gdev));
     const int sid = a.msg[pos];
     const SGRec& SG = a.sg[sid];
     const double* bl = a.q_line + 3 * (int64_t)SG.rlo;
     const double b[3] = {bl[0], bl[1], bl[2]};
-    const double sdev = band_deviation(m, b, W, H, d);
+    double rdev, sdev;
+    band_deviation2(m, r, b, W, H, d, rdev, sdev);
+    const float gdev = (float)(rdev + 0.05);
+    atomicMax(reinterpret_cast<unsigned*>(&G.maxdev), __float_as_uint(gdev));
     atomicMax(&a.sgdev[sid], (unsigned long long)__double_as_longlong(sdev));
     MemberRec mr;
     mr.a = (float)m[0]; mr.b = (float)m[1]; mr.c = (float)m[2];
