@@ -101,6 +101,54 @@ def _hybrid(idx, d0, d1, n_query_all, n_tier, ratio, batch_fraction, continue_mi
     return _dedupe(rows[sel], tg[sel], dd[sel], rr[sel])
 
 
+def _hybrid_all(idx, d0, d1, n_query_all, n_tier, ratio, batch_fraction, continue_min,
+                early_stop, single_cap, n_target_tiers, stats):
+    """_hybrid for every target slot of one query image at once (rows = target
+    slots of the kNN result): the ratio filter, the batch schedule (accepted counts
+    from one cumulative sum) and the per-target dedupe are array operations over
+    all slots; returns the per-slot (rows, targets, dist, ratio) in slot order."""
+    S = idx.shape[0]
+    has = idx >= 0
+    single = ~np.isfinite(d1)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        r = np.where(d1 > 0, d0 / np.where(d1 > 0, d1, 1.0), 1.0)
+    acc = has & np.where(single, d0 < single_cap, r < ratio)
+    batch = max(1, int(np.ceil(batch_fraction * n_query_all)))
+    csum = np.cumsum(acc, axis=1)
+    accepted = np.zeros(S, np.int64)
+    end = np.zeros(S, np.int64)
+    active = np.ones(S, bool)
+    tiers = np.asarray(n_target_tiers, np.int64)
+    first_done = False
+    for start in range(0, n_tier, batch):
+        if first_done:
+            active &= ~(accepted <= continue_min)
+        active &= ~(accepted >= early_stop)
+        if not active.any():
+            break
+        stop = min(start + batch, n_tier)
+        accepted[active] = csum[active, stop - 1]
+        if stats is not None:
+            na = int(active.sum())
+            stats.add((stop - start) * na, (stop - start) * int(tiers[active].sum()))
+        end[active] = stop
+        first_done = True
+    sel = acc & (np.arange(acc.shape[1])[None, :] < end[:, None])
+    ss, rows = np.nonzero(sel)
+    tg, dd = idx[ss, rows], d0[ss, rows]
+    rr = np.where(single[ss, rows], 0.0, r[ss, rows])
+    if len(rows):
+        order = np.lexsort((rows, dd, tg, ss))
+        first = np.ones(len(order), bool)
+        first[1:] = (ss[order][1:] != ss[order][:-1]) | (tg[order][1:] != tg[order][:-1])
+        keep = order[first]
+        keep = keep[np.lexsort((rows[keep], ss[keep]))]
+        ss, rows, tg, dd, rr = ss[keep], rows[keep], tg[keep], dd[keep], rr[keep]
+    bnd = np.searchsorted(ss, np.arange(S + 1))
+    return [(rows[bnd[s]:bnd[s + 1]], tg[bnd[s]:bnd[s + 1]], dd[bnd[s]:bnd[s + 1]],
+             rr[bnd[s]:bnd[s + 1]]) for s in range(S)]
+
+
 def _matches(types, qid, tid, rows, tgts, d, r, qmap=None, tmap=None):
     FR, M = types[0], types[1]
     qm = rows if qmap is None else qmap[rows]
@@ -212,10 +260,11 @@ def build_coarse_matchgraph(feature_sets, *, ratio=RATIO_UNGUIDED, preemptive=Fa
         if n_tier == 0 or not targets:
             continue
         idx, d0, d1 = _knn_rows(bank, np.asarray(fa.descriptors)[:n_tier], targets, tiers)
-        for s, b in enumerate(targets):
-            hybrid[(a, b)] = _hybrid(idx[s], d0[s], d1[s], len(fa), n_tier, ratio,
-                                     HYBRID_BATCH_FRACTION, HYBRID_CONTINUE_MIN, early_stop,
-                                     SINGLE_CANDIDATE_CAP, int(tiers[pos[b]]), stats)
+        per = _hybrid_all(idx, d0, d1, len(fa), n_tier, ratio, HYBRID_BATCH_FRACTION,
+                          HYBRID_CONTINUE_MIN, early_stop, SINGLE_CANDIDATE_CAP,
+                          [int(tiers[pos[b]]) for b in targets], stats)
+        for b, h in zip(targets, per):
+            hybrid[(a, b)] = h
     cand, q_list, c_list, seeds = [], [], [], []
     xy64 = {}
 

@@ -31,3 +31,10 @@ build_coarse_matchgraph(store.sets, on_overflow="drop")
 torch.cuda.synchronize()
 pr.disable()
 pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+
+from torch.profiler import ProfilerActivity, profile
+with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+    build_coarse_matchgraph(store.sets, on_overflow="drop")
+    torch.cuda.synchronize()
+os.makedirs("gpurun_out", exist_ok=True)
+prof.export_chrome_trace("gpurun_out/coarse_trace.json")
