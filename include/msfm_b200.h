@@ -308,6 +308,16 @@ int msfm_gather_3d2d(const int32_t* d_corr_row, const int32_t* d_corr_fid, int32
                      const int64_t* d_out_off, const double* d_xyz, const float* d_bank_xy,
                      double* d_X, double* d_uv, void* stream);
 
+/* msfm_ransac_samples_seeded on the device, the same draws bit for bit (the
+ * PCG64 / SeedSequence / choice restatement is shared with the host sampler,
+ * rng.cuh): one thread per (stream, choice) positioned with PCG64's jump-ahead,
+ * streams where Lemire's bounded draw would have redrawn are redone sequentially.
+ * d_bad: 1 + n_items int32 of scratch; d_bad[0] is set to 1 (never cleared) when
+ * an item is outside choice's Floyd branch (n > 10000 and size > n/50). */
+int msfm_ransac_samples_seeded_device(int32_t n_items, const uint64_t* d_seeds, const int64_t* d_n,
+                                      int32_t sample_size, int32_t count, int32_t* d_out,
+                                      uint64_t* d_state_out, int32_t* d_bad, void* stream);
+
 /* ------------------------------------------------------------------------
  * PnP-RANSAC (reconstruct.py:168-226), batched over images.  Correspondences of
  * image s: X [off[s]..off[s+1])[3] f64 world points, uv [..][2] f64 pixels,

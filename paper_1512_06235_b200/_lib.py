@@ -78,6 +78,8 @@ _SIGS = {
     "msfm_msft_load": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(MsftInfo), VP, VP, VP, VP]),
     "msfm_msft_load_many": (ctypes.c_int, [ctypes.c_int32, VP, VP, VP, VP, VP, VP, VP,
                                            ctypes.c_int32]),
+    "msfm_ransac_samples_seeded_device": (ctypes.c_int, [ctypes.c_int32, VP, VP, ctypes.c_int32,
+                                                         ctypes.c_int32, VP, VP, VP, VP]),
     "msfm_rng_seed_state": (ctypes.c_int, [ctypes.c_uint64, VP]),
     "msfm_ransac_samples_seeded": (ctypes.c_int, [ctypes.c_int32, VP, VP, ctypes.c_int32,
                                                   ctypes.c_int32, VP, VP]),

@@ -13,6 +13,7 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "rng.cuh"
 
 namespace msfm {
 namespace {
@@ -650,6 +651,89 @@ __global__ void __launch_bounds__(RT) pnp_refit_kernel(RefitArgs a) {
 
 using namespace msfm;
 
+// np.random.default_rng(seed_k).choice(n_k, size, replace=False) x count.
+// Every choice consumes a fixed number of 32-bit draws unless Lemire's bounded
+// draw rejects (probability ~ n / 2^32 per draw), so thread (k, h) jumps stream k
+// to draw h * (2 size - 1) with PCG64's O(log) advance and makes choice h alone;
+// a stream where any draw would have been rejected is flagged and redone
+// sequentially (one thread) by ransac_samples_fixup_kernel.
+__global__ void ransac_samples_kernel(int32_t n_items, const uint64_t* __restrict__ seeds,
+                                      const int64_t* __restrict__ n, int32_t sample_size,
+                                      int32_t count, int32_t* __restrict__ out,
+                                      uint64_t* __restrict__ state_out, int32_t* __restrict__ redo,
+                                      int32_t* __restrict__ bad) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t per = (int64_t)count + 1;          // count choices + the end state
+    if (tid >= (int64_t)n_items * per) return;
+    const int it = (int)(tid / per), h = (int)(tid - (int64_t)it * per);
+    const int64_t pop = n[it];
+    if (pop > 10000 && sample_size > pop / 50) { atomicExch(bad, 1); return; }
+    msfm_rng::Pcg64 g0;
+    msfm_rng::seed_pcg64(seeds[it], g0);
+    // draws per choice: one per bounded call with a non-zero range (Floyd's j = 0,
+    // reached when pop == size, returns 0 without drawing)
+    const uint64_t draws = 2 * (uint64_t)sample_size - 1 - (pop == sample_size ? 1 : 0);
+    msfm_rng::Pcg64 g;
+    msfm_rng::pcg_at_draw(g0.state, g0.inc, draws * (uint64_t)h, g);
+    if (h == count) {
+        // numpy keeps the last buffered half in `uinteger` after using it: after an
+        // even number of draws that is the high half of the last 64-bit output
+        if (!g.has32 && count > 0 && draws > 0) {
+            const uint64_t hi = (uint64_t)(g.state >> 64), lo = (uint64_t)g.state;
+            const unsigned rot = (unsigned)(hi >> 58);
+            const uint64_t x = hi ^ lo;
+            g.u32 = (uint32_t)(((x >> rot) | (x << ((64 - rot) & 63))) >> 32);
+        }
+        if (state_out) {
+            uint64_t* so = state_out + 6 * (int64_t)it;
+            so[0] = (uint64_t)(g.state >> 64);
+            so[1] = (uint64_t)g.state;
+            so[2] = (uint64_t)(g.inc >> 64);
+            so[3] = (uint64_t)g.inc;
+            so[4] = (uint64_t)g.has32;
+            so[5] = (uint64_t)g.u32;
+        }
+        return;
+    }
+    int64_t tmp[48];
+    bool rej = false;
+    msfm_rng::choice_floyd_once(g, pop, sample_size, tmp, rej);
+    if (rej) atomicExch(redo + it, 1);
+    int32_t* o = out + ((int64_t)it * count + h) * sample_size;
+    for (int k = 0; k < sample_size; k++) o[k] = (int32_t)tmp[k];
+}
+
+// the sequential stream, for the flagged items only
+__global__ void ransac_samples_fixup_kernel(int32_t n_items, const uint64_t* __restrict__ seeds,
+                                            const int64_t* __restrict__ n, int32_t sample_size,
+                                            int32_t count, int32_t* __restrict__ out,
+                                            uint64_t* __restrict__ state_out,
+                                            const int32_t* __restrict__ redo,
+                                            int32_t* __restrict__ bad) {
+    const int it = blockIdx.x * blockDim.x + threadIdx.x;
+    if (it >= n_items || !redo[it]) return;
+    msfm_rng::Pcg64 g;
+    msfm_rng::seed_pcg64(seeds[it], g);
+    int64_t tmp[48];
+    int32_t* o = out + (int64_t)it * count * sample_size;
+    for (int32_t h = 0; h < count; h++) {
+        if (!msfm_rng::choice_floyd(g, n[it], sample_size, tmp)) {
+            atomicExch(bad, 1);
+            return;
+        }
+        for (int k = 0; k < sample_size; k++) o[(int64_t)h * sample_size + k] = (int32_t)tmp[k];
+    }
+    if (state_out) {
+        uint64_t* so = state_out + 6 * (int64_t)it;
+        so[0] = (uint64_t)(g.state >> 64);
+        so[1] = (uint64_t)g.state;
+        so[2] = (uint64_t)(g.inc >> 64);
+        so[3] = (uint64_t)g.inc;
+        so[4] = (uint64_t)g.has32;
+        so[5] = (uint64_t)g.u32;
+    }
+}
+
 extern "C" int msfm_pnp_hypotheses(const double* d_X, const double* d_uv, const int64_t* d_off,
                                    const double* d_K, int32_t n_images, const int32_t* d_samples,
                                    int32_t n_hyp, double threshold, double* d_hyp,
@@ -695,5 +779,30 @@ extern "C" int msfm_pnp_refit(const double* d_X, const double* d_uv, const int64
     }
     MSFM_LAUNCH_CHECK();
     count_launches(1);
+    return MSFM_OK;
+}
+
+extern "C" int msfm_ransac_samples_seeded_device(int32_t n_items, const uint64_t* d_seeds,
+                                                 const int64_t* d_n, int32_t sample_size,
+                                                 int32_t count, int32_t* d_out,
+                                                 uint64_t* d_state_out, int32_t* d_bad,
+                                                 void* stream) {
+    if (n_items < 0 || sample_size < 1 || sample_size > 48 || count < 0 || !d_bad) {
+        set_error("msfm_ransac_samples_seeded_device: bad arguments");
+        return MSFM_EINVAL;
+    }
+    if (n_items == 0) return MSFM_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    // per-item redo flags live after the bad flag's int: the caller's d_bad must
+    // hold 1 + n_items int32
+    int32_t* redo = d_bad + 1;
+    MSFM_CUDA_TRY(cudaMemsetAsync(redo, 0, sizeof(int32_t) * n_items, st));
+    const int64_t threads = (int64_t)n_items * ((int64_t)count + 1);
+    ransac_samples_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(
+        n_items, d_seeds, d_n, sample_size, count, d_out, d_state_out, redo, d_bad);
+    ransac_samples_fixup_kernel<<<(n_items + 63) / 64, 64, 0, st>>>(
+        n_items, d_seeds, d_n, sample_size, count, d_out, d_state_out, redo, d_bad);
+    MSFM_LAUNCH_CHECK();
+    count_launches(2);
     return MSFM_OK;
 }

@@ -234,22 +234,28 @@ def pnp_batch(X_list, uv_list, K_list, seeds, *, threshold=PNP_THRESHOLD_PX,
     H1 = min(max_iters, first_round)
     mark("batch upload")
     counts = np.full((A, max_iters), -2, np.int64)
-    # all streams default_rng(seed) at once (SeedSequence restated natively)
-    # written straight into pinned memory: the upload is one async copy
-    samples_t = torch.empty((A, H1, 6), dtype=torch.int32, pin_memory=True)
-    samples = samples_t.numpy()
-    st_all = np.zeros((A, 6), np.uint64)
+    # every stream's default_rng(seed).choice draws generated on the device (one
+    # thread per stream; the PCG64 / SeedSequence restatement shared with the host
+    # sampler), straight into the hypothesis kernel's input
     if any(int(seeds[i]) < 0 for i in active):
         raise ValueError("expected non-negative integer seeds")   # as np.random.default_rng
     seed_arr = np.array([int(seeds[i]) for i in active], np.uint64)
     n_arr = np.ascontiguousarray(batch.n, np.int64)
-    _lib.check(lib.msfm_ransac_samples_seeded(A, seed_arr.ctypes.data, n_arr.ctypes.data, 6, H1,
-                                              samples.ctypes.data, st_all.ctypes.data),
-               "msfm_ransac_samples_seeded")
-    states = [(st_all[k],) for k in range(A)]
-    mark("samples (host)")
+    d_samples = torch.empty((A, H1, 6), dtype=torch.int32, device=dev)
+    d_state = torch.empty((A, 6), dtype=torch.int64, device=dev)
+    d_bad = torch.zeros(1 + A, dtype=torch.int32, device=dev)
+    # named: a temporary's block could be handed to the next allocation before the
+    # kernel reads it
+    d_seeds, d_n = _lib.h2d(seed_arr.view(np.int64), dev), _lib.h2d(n_arr, dev)
+    _lib.check(lib.msfm_ransac_samples_seeded_device(
+        A, _lib.ptr(d_seeds), _lib.ptr(d_n), 6, H1,
+        _lib.ptr(d_samples), _lib.ptr(d_state), _lib.ptr(d_bad), st),
+        "msfm_ransac_samples_seeded_device")
+    mark("samples (device)")
     # hypotheses stay on the device; only the inlier counts come back for the replay
-    d_hyp1, c1 = _score(lib, batch, samples_t, H1, threshold, st, dev)
+    d_hyp1, c1 = _score(lib, batch, d_samples, H1, threshold, st, dev)
+    if int(d_bad[0].item()):
+        raise ValueError("RANSAC population outside numpy choice's Floyd branch")
     counts[:, :H1] = c1
     mark("round 1 score")
     best = _replay_batch(counts, H1, batch.n, max_iters, confidence)
@@ -257,6 +263,8 @@ def pnp_batch(X_list, uv_list, K_list, seeds, *, threshold=PNP_THRESHOLD_PX,
     pending = [k for k in range(A) if best[k] != "overflow" and not best[k][4]]
     d_hyp2 = None
     if pending:
+        st_all = d_state.cpu().numpy().view(np.uint64)
+        states = [(st_all[k],) for k in range(A)]
         # second round: continue each stream up to the current `needed` bound
         H2 = max_iters - H1
         samples2 = np.zeros((len(pending), H2, 6), np.int32)

@@ -83,3 +83,39 @@ def test_flat_batch_equals_list_batch():
         if ra.status == "ok":
             np.testing.assert_array_equal(ra.mask, rb.mask)
             np.testing.assert_array_equal(ra.R, rb.R)
+
+
+def test_device_sampler_equals_host_sampler():
+    """msfm_ransac_samples_seeded_device: the same draws and end states as the host
+    restatement (itself pinned draw-for-draw to numpy in test_sampler.py)."""
+    import ctypes
+
+    import torch
+
+    from paper_1512_06235_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(4)
+    A, H = 37, 300
+    n = rng.integers(6, 20000, size=A).astype(np.int64)
+    n[:3] = [6, 7, 10001]
+    # huge populations: Lemire's bounded draw rejects often (the sequential fixup path)
+    n[3:6] = [2**31 + 7, 3 * 2**30, 2**32 - 3]
+    seeds = rng.integers(0, 2**63, size=A, dtype=np.uint64)
+    seeds[:2] = [0, 2**64 - 1]
+    want = np.zeros((A, H, 6), np.int32)
+    wst = np.zeros((A, 6), np.uint64)
+    _lib.check(lib.msfm_ransac_samples_seeded(A, seeds.ctypes.data, n.ctypes.data, 6, H,
+                                              want.ctypes.data, wst.ctypes.data), "host")
+    dev = torch.device("cuda")
+    d_out = torch.empty((A, H, 6), dtype=torch.int32, device=dev)
+    d_st = torch.empty((A, 6), dtype=torch.int64, device=dev)
+    d_bad = torch.zeros(1 + A, dtype=torch.int32, device=dev)
+    d_seeds = torch.from_numpy(seeds.view(np.int64)).to(dev)
+    d_n = torch.from_numpy(n).to(dev)
+    _lib.check(lib.msfm_ransac_samples_seeded_device(A, _lib.ptr(d_seeds), _lib.ptr(d_n), 6, H,
+                                                     _lib.ptr(d_out), _lib.ptr(d_st),
+                                                     _lib.ptr(d_bad), None), "device")
+    assert int(d_bad[0].item()) == 0
+    np.testing.assert_array_equal(d_out.cpu().numpy(), want)
+    np.testing.assert_array_equal(d_st.cpu().numpy().view(np.uint64), wst)
