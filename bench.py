@@ -188,6 +188,16 @@ def run_reference(args, rank, world):
                              "sample": f"{n} seeded-random C3 pairs per step (oracle/guided_oracle.c, "
                                        f"C restatement of guided_match_pair)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if not args.no_localize:
+        # the metric's second half: localized images/s of the CPU restatement on C2
+        lscene, lsnap, queries = build_localization()
+        lr, lcores, ln, ldt = cpu_localize_rate(lscene, lsnap, queries, max(cpu_cores(), 8))
+        line["localization"] = {
+            "metric": "localized images/sec", "value": lr, "unit": "images/s",
+            "cpu_baseline": {"value": lr, "unit": "images/s", "cores": lcores, "kind": "port",
+                             "sample": f"{ln} C2 query images in {ldt:.1f}s (oracle/localize.py: "
+                                       "exact direct 3D-2D + pnp_ransac restatement), one "
+                                       "process per core"}}
     print(json.dumps(line), flush=True)
 
 
