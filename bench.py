@@ -521,7 +521,7 @@ def run_localization(args, dev):
     from paper_1512_06235_b200 import _lib, scenes
     from paper_1512_06235_b200.bank import FeatureBank, HostBank
     from paper_1512_06235_b200.localize import (PointSet, direct_search, gather_pnp_inputs,
-                                                knn2_tracks, upload_points)
+                                                knn2_tracks, knn2_tracks_staged, upload_points)
     from paper_1512_06235_b200.pnp import pnp_batch_flat
 
     scene, snap, queries = build_localization()
@@ -530,11 +530,11 @@ def run_localization(args, dev):
     host = HostBank({q: scene.feature_sets[q] for q in queries})
     Ks = [scene.cameras[q].K for q in queries]
 
-    def step(bank, dp, d_xyz):
+    def step(bank, dp, d_xyz, knn=None):
         # device-resident flat correspondences: image k owns [off[k], off[k+1]); the
         # gate of localize.py:203 (> 16) selects the images that go to PnP, and their
         # 3D-2D pairs are gathered on the device
-        corr = direct_search(bank, pts, queries, device_points=dp, to_host=False)
+        corr = direct_search(bank, pts, queries, device_points=dp, to_host=False, knn=knn)
         X, uv, toff, todo = gather_pnp_inputs(bank, corr, queries, d_xyz)
         res = pnp_batch_flat(X, uv, toff, [Ks[k] for k in todo], [queries[k] for k in todo],
                              device=dev)
@@ -578,9 +578,10 @@ def run_localization(args, dev):
     for i in range(args.warmup + args.steps):
         torch.cuda.synchronize()
         t1 = time.perf_counter()
-        b2.refill()
+        # the query bank goes up in eight ranges, each range's kNN starting as it lands
         dp2 = upload_points(pts, dev)
-        step(b2, dp2, pin_xyz.to(dev, non_blocking=True))
+        knn = knn2_tracks_staged(b2, pts, queries, dp2)
+        step(b2, dp2, pin_xyz.to(dev, non_blocking=True), knn=knn)
         torch.cuda.synchronize()
         if i >= args.warmup:
             e2e.append(time.perf_counter() - t1)

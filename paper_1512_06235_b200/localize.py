@@ -92,7 +92,7 @@ class DeviceKnn:
 
 
 def knn2_tracks(bank: FeatureBank, pts: PointSet, image_ids, stream=None,
-                device_points=None, counts=None, second: bool = False) -> DeviceKnn:
+                device_points=None, counts=None, second: bool = False, into=None) -> DeviceKnn:
     """Top-2 over each image's features; ``counts`` (per bank image, optional)
     restricts image k to its first counts[k] features (a coarse tier); ``second``
     also resolves the second neighbour's index (lowest index at the second key)."""
@@ -107,9 +107,13 @@ def knn2_tracks(bank: FeatureBank, pts: PointSet, image_ids, stream=None,
     dS, dn, dSS = device_points
     slots = np.array([bank.index_of[int(i)] for i in image_ids], dtype=np.int32)
     d_slots = _lib.h2d(slots, dev)
-    k1 = torch.empty((max(len(slots), 1), M_pad), dtype=torch.int32, device=dev)
-    i1 = torch.empty_like(k1)
-    k2 = torch.empty_like(k1)
+    if into is not None:
+        # (k1, i1, k2) rows of these images inside larger tables (row views)
+        k1, i1, k2 = into
+    else:
+        k1 = torch.empty((max(len(slots), 1), M_pad), dtype=torch.int32, device=dev)
+        i1 = torch.empty_like(k1)
+        k2 = torch.empty_like(k1)
     cnt = bank.counts if counts is None else np.asarray(counts, np.int64)
     max_feat = int(cnt[slots].max()) if len(slots) else 0
     ws_bytes = lib.msfm_knn_workspace_bytes(M, len(slots), max_feat)
@@ -135,16 +139,62 @@ def knn2_tracks(bank: FeatureBank, pts: PointSet, image_ids, stream=None,
     return out
 
 
-def upload_points(pts: PointSet, dev):
+def knn2_tracks_staged(bank: FeatureBank, pts: PointSet, image_ids, device_points,
+                       groups: int = 8) -> DeviceKnn:
+    """knn2_tracks on a staged bank (FeatureBank(staged=True)) whose rows are
+    still in pinned host memory: the images go up in ``groups`` contiguous ranges
+    on a copy stream, and the kNN of range g (with its |desc|^2) runs as soon as
+    it has landed, while range g + 1 is in flight.  ``image_ids`` must be the
+    bank's images in bank order."""
     import torch
 
-    def up(a):
-        return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().to(dev, non_blocking=True)
+    lib = _lib.load()
+    dev = bank.device
+    ids = list(image_ids)
+    S = len(ids)
+    assert list(bank.slots(ids)) == list(range(S)), "image_ids must be the bank's images in order"
+    M_pad = (len(pts.n) + 127) // 128 * 128
+    k1 = torch.empty((max(S, 1), M_pad), dtype=torch.int32, device=dev)
+    i1 = torch.empty_like(k1)
+    k2 = torch.empty_like(k1)
+    cs = bank.__dict__.get("_h2d_stream")
+    if cs is None:
+        cs = bank.__dict__["_h2d_stream"] = torch.cuda.Stream(device=dev)
+    cur = torch.cuda.current_stream(dev)
+    cs.wait_stream(cur)
+    edges = np.linspace(0, S, max(1, min(groups, S)) + 1).round().astype(int)
+    keep = []
+    for g0, g1 in zip(edges[:-1], edges[1:]):
+        if g1 <= g0:
+            continue
+        landed = bank.upload_range(int(g0), int(g1), cs)
+        cur.wait_event(landed)
+        a, b = bank.row_range(int(g0), int(g1))
+        _lib.check(lib.msfm_feature_norms(_lib.ptr(bank.desc) + 128 * a, b - a,
+                                          _lib.ptr(bank.norm2) + 4 * a, _lib.stream_handle(cur)),
+                   "msfm_feature_norms")
+        keep.append(knn2_tracks(bank, pts, ids[g0:g1], device_points=device_points,
+                                into=(k1[g0:g1], i1[g0:g1], k2[g0:g1])))
+    return DeviceKnn(k1, i1, k2, M_pad, keep=tuple(keep))
 
-    M = len(pts.n)
-    return (up(pts.S.astype(np.int32) if M else np.zeros((1, 128), np.int32)),
-            up(pts.n.astype(np.int32) if M else np.zeros(1, np.int32)),
-            up(pts.SS if M else np.zeros(1, np.int64)))
+
+def upload_points(pts: PointSet, dev):
+    """(S, n, |S|^2) on the device; the pinned host copies are made once per
+    PointSet, so repeated uploads are three async copies."""
+    import torch
+
+    pinned = pts.__dict__.get("_pinned")
+    if pinned is None or pinned[0] is not pts.S:
+        M = len(pts.n)
+
+        def pin(a):
+            return torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+
+        pinned = (pts.S, pin(pts.S.astype(np.int32) if M else np.zeros((1, 128), np.int32)),
+                  pin(pts.n.astype(np.int32) if M else np.zeros(1, np.int32)),
+                  pin(pts.SS if M else np.zeros(1, np.int64)))
+        pts.__dict__["_pinned"] = pinned
+    return tuple(t.to(dev, non_blocking=True) for t in pinned[1:])
 
 
 @dataclass

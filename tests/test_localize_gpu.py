@@ -178,3 +178,27 @@ def test_ranked_2d2d_equals_reference():
     assert [tuple(c) for c in z["copy_corr"].tolist()] == corr
     with pytest.raises(InsufficientDataError):
         ranked_2d2d_search(model, _EdgeGraph([]), 9, store.sets[9], store)
+
+
+def test_staged_knn_equals_resident_knn():
+    """knn2_tracks_staged (query bank uploaded in ranges, kNN per range as it lands)
+    == knn2_tracks over a resident bank."""
+    import torch
+
+    from paper_1512_06235_b200.bank import FeatureBank, HostBank
+    from paper_1512_06235_b200.localize import PointSet, knn2_tracks, knn2_tracks_staged, upload_points
+
+    rng = np.random.default_rng(11)
+    sets = {}
+    for i in range(7):
+        sets[i] = _random_case(rng, 1, [int(rng.integers(50, 900))])[0][0]
+    S = rng.integers(0, 256, size=(300, 128)).astype(np.int32) * 2
+    pts = PointSet(S=S, n=np.full(300, 2, np.int32), ids=np.arange(300))
+    full = FeatureBank(sets)
+    want = knn2_tracks(full, pts, list(range(7)))
+    for groups in (1, 3, 7):
+        b = FeatureBank(host=HostBank(sets), staged=True)
+        got = knn2_tracks_staged(b, pts, list(range(7)), upload_points(pts, b.device), groups)
+        torch.cuda.synchronize()
+        for name in ("k1", "i1", "k2"):
+            assert torch.equal(getattr(got, name)[:, :300], getattr(want, name)[:, :300]), (groups, name)

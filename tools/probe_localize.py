@@ -63,3 +63,38 @@ with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
     torch.cuda.synchronize()
 os.makedirs("gpurun_out", exist_ok=True)
 prof.export_chrome_trace("gpurun_out/loc_trace.json")
+
+# ---- e2e variants: bank refilled then stepped vs staged (4 ranges, kNN per range)
+from paper_1512_06235_b200.localize import knn2_tracks_staged
+pin_xyz = torch.from_numpy(snap.point_xyz).pin_memory()
+b2 = FeatureBank(host=host, device=dev, staged=True)
+
+
+def e2e(staged, groups=4):
+    dp2 = upload_points(pts, dev)
+    if staged:
+        knn = knn2_tracks_staged(b2, pts, queries, dp2, groups)
+    else:
+        b2.refill()
+        knn = None
+    corr = direct_search(b2, pts, queries, device_points=dp2, to_host=False, knn=knn)
+    X, uv, toff, todo = gather_pnp_inputs(b2, corr, queries, pin_xyz.to(dev, non_blocking=True))
+    return pnp_batch_flat(X, uv, toff, [Ks[k] for k in todo], [queries[k] for k in todo], device=dev)
+
+
+for name, fn in (("e2e refill", lambda: e2e(False)), ("e2e staged 4", lambda: e2e(True, 4)),
+                 ("e2e staged 2", lambda: e2e(True, 2)), ("e2e staged 8", lambda: e2e(True, 8))):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(10):
+        t0 = time.perf_counter()
+        fn()
+        torch.cuda.synchronize()
+        ts.append((time.perf_counter() - t0) * 1e3)
+    print(f"{name:20s} {np.median(ts):7.2f} ms", flush=True)
+with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+    e2e(True, 4)
+    torch.cuda.synchronize()
+prof.export_chrome_trace("gpurun_out/loc_e2e_trace.json")
