@@ -162,6 +162,11 @@ def knn2_tracks_staged(bank: FeatureBank, pts: PointSet, image_ids, device_point
         cs = bank.__dict__["_h2d_stream"] = torch.cuda.Stream(device=dev)
     cur = torch.cuda.current_stream(dev)
     cs.wait_stream(cur)
+    if not bank.__dict__.get("_recorded"):
+        # the rows are written on `cs`: the allocator must not recycle them early
+        bank.xy.record_stream(cs)
+        bank.desc.record_stream(cs)
+        bank.__dict__["_recorded"] = True
     edges = np.linspace(0, S, max(1, min(groups, S)) + 1).round().astype(int)
     keep = []
     for g0, g1 in zip(edges[:-1], edges[1:]):
