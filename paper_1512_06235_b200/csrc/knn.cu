@@ -334,11 +334,19 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_lo, const __grid_constant_
                     tmem_wait_ld();
                     const int k1_in = k1;
                     if (full) {
+                        // values only in the loop (three min/max per score); the
+                        // column of a new best is found afterwards, rarely
+                        int key[16];
 #pragma unroll
                         for (int c = 0; c < 16; c++) {
-                            const int key = np * fv[c] - ((int)lo[c] + ((int)hi[c] << 8));
-                            k2 = min(k2, max(k1, key));
-                            if (key < k1) { k1 = key; il = c; }
+                            key[c] = np * fv[c] - ((int)lo[c] + ((int)hi[c] << 8));
+                            k2 = min(k2, max(k1, key[c]));
+                            k1 = min(k1, key[c]);
+                        }
+                        if (k1 != k1_in) {
+#pragma unroll
+                            for (int c = 15; c >= 0; c--)
+                                if (key[c] == k1) il = c;     // lowest column at the best
                         }
                     } else {
                         const int lim = n - (cbase + c0);
