@@ -478,6 +478,9 @@ def guided_match_pair(query_fs, target_fs, geom, *, d: float = BAND_D_PX,
     if stats is not None:
         stats.add(int(s[0, 0]), int(s[0, 1]))
     qimg, timg = query_fs.image_id, target_fs.image_id
-    return [Match(query=FeatureRef(qimg, int(a)), target=FeatureRef(timg, int(ti[b])),
-                  distance=float(c), ratio=float(r))
-            for a, b, c, r in zip(q, t, dist, rat)]
+    # Python scalars first (.tolist()): f32 values widen exactly to float
+    return [Match(query=FeatureRef(qimg, a), target=FeatureRef(timg, b), distance=c, ratio=r)
+            for a, b, c, r in zip(np.asarray(q, np.int64).tolist(),
+                                  np.asarray(ti)[np.asarray(t, np.int64)].astype(np.int64).tolist(),
+                                  np.asarray(dist, np.float32).astype(np.float64).tolist(),
+                                  np.asarray(rat, np.float32).astype(np.float64).tolist())]
