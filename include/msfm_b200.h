@@ -387,7 +387,7 @@ int msfm_fundamental_refit(const double* d_q, const double* d_c, const int64_t* 
  *   d_u, d_v, d_dist [n_edges]      matched nodes and f32 distances
  *   d_track_ptr [n_points+1], d_track_node  model tracks as bank nodes
  * Output: fresh nodes grouped per emitting component (ascending smallest node),
- * ascending inside: d_out_node [<= 2 n_edges]; per segment d_seg_owner (track
+ * ascending inside: d_out_node [<= min(2 n_edges, bank rows)]; per segment d_seg_owner (track
  * row extended, -1 = new track) and d_seg_off [n_seg+1]; d_counts = {n_seg, n_out}.
  * ---------------------------------------------------------------------- */
 size_t msfm_merge_workspace_bytes(int64_t n_nodes, int64_t n_edges);

@@ -34,7 +34,7 @@ struct MergeArgs {
     int32_t* fresh_cnt; int32_t* fresh; int32_t* seg_idx; int32_t* seg_off; int32_t* fill;
     unsigned long long* hkey; unsigned long long* hval; int64_t hmask;
     int32_t* out_node; int32_t* seg_owner; int64_t* seg_off_out; int64_t* counts;
-    int32_t* tmp_node;           // scratch for the segment sort (2 * n_edges)
+    int32_t* tmp_node;           // scratch for the segment sort (touched_bound)
 };
 
 __device__ __forceinline__ int find_root(int32_t* parent, int x) {
@@ -266,9 +266,18 @@ __global__ void covis_kernel(int32_t n_points, const int64_t* __restrict__ ptr,
         }
 }
 
-int64_t hash_size(int64_t n_edges) {
+// nodes the merge can emit: every fresh node is a distinct bank row touched by an
+// edge, so min(2 * edges, nodes) bounds the (component, image) keys, the output
+// nodes and their segments alike
+int64_t touched_bound(int64_t n_nodes, int64_t n_edges) {
+    const int64_t b = 2 * n_edges < n_nodes ? 2 * n_edges : n_nodes;
+    return b > 0 ? b : 1;
+}
+
+// open addressing at load <= 1/2 over at most `keys` keys
+int64_t hash_size(int64_t keys) {
     int64_t h = 1024;
-    while (h < 4 * n_edges) h <<= 1;
+    while (h < 2 * keys) h <<= 1;
     return h;
 }
 
@@ -300,8 +309,8 @@ extern "C" size_t msfm_merge_workspace_bytes(int64_t n_nodes, int64_t n_edges) {
     const int64_t n = n_nodes > 0 ? n_nodes : 1;
     const int64_t nb = (n + SCAN_T * SCAN_PER - 1) / (SCAN_T * SCAN_PER) + 1;
     return aligned_bytes<int32_t>(n) * 10 + aligned_bytes<int32_t>(nb) +
-           aligned_bytes<unsigned long long>(hash_size(n_edges)) * 2 +
-           aligned_bytes<int32_t>(2 * (n_edges > 0 ? n_edges : 1)) + 4096;
+           aligned_bytes<unsigned long long>(hash_size(touched_bound(n, n_edges))) * 2 +
+           aligned_bytes<int32_t>(touched_bound(n, n_edges)) + 4096;
 }
 
 extern "C" int msfm_merge_tracks(const msfm_bank* bank, int64_t n_edges, const int32_t* d_u,
@@ -339,10 +348,10 @@ extern "C" int msfm_merge_tracks(const msfm_bank* bank, int64_t n_edges, const i
     a.seg_idx = ar.take<int32_t>(n); a.seg_off = ar.take<int32_t>(n); a.fill = ar.take<int32_t>(n);
     const int64_t nb = (n + SCAN_T * SCAN_PER - 1) / (SCAN_T * SCAN_PER) + 1;
     int32_t* bsum = ar.take<int32_t>(nb);
-    const int64_t hs = hash_size(n_edges);
+    const int64_t hs = hash_size(touched_bound(n, n_edges));
     a.hkey = ar.take<unsigned long long>(hs); a.hval = ar.take<unsigned long long>(hs);
     a.hmask = hs - 1;
-    a.tmp_node = ar.take<int32_t>(2 * (n_edges > 0 ? n_edges : 1));
+    a.tmp_node = ar.take<int32_t>(touched_bound(n, n_edges));
     a.out_node = d_out_node; a.seg_owner = d_seg_owner; a.seg_off_out = d_seg_off; a.counts = d_counts;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);

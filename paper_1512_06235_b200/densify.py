@@ -109,7 +109,8 @@ def merge_tracks_nodes(bank, u, v, dist, track_ptr, track_node, stream=None):
     tn = np.ascontiguousarray(track_node, np.int32)
     d_tnode = torch.from_numpy(tn if len(tn) else np.zeros(1, np.int32)).to(dev)
     E = int(u.numel())
-    cap = max(2 * E, 1)
+    # fresh nodes are distinct bank rows touched by the edges
+    cap = max(min(2 * E, int(bank.n_total)), 1)
     out_node = torch.empty(cap, dtype=torch.int32, device=dev)
     seg_owner = torch.empty(cap, dtype=torch.int32, device=dev)
     seg_off = torch.empty(cap + 1, dtype=torch.int64, device=dev)
