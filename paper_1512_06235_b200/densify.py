@@ -128,14 +128,17 @@ def merge_tracks_nodes(bank, u, v, dist, track_ptr, track_node, stream=None):
             seg_off[:nseg + 1].cpu().numpy())
 
 
-def merge_tracks_device(bank, u, v, dist, model, stream=None):
+def merge_tracks_device(bank, u, v, dist, model, stream=None, arrays=None):
     """Track merge on the device (msfm_merge_tracks, densify.py:68-158).
 
     ``u``, ``v`` are bank node ids (device int32), ``dist`` the f32 match
     distances (device).  Returns (new_tracks, extensions) like the reference:
-    lists of (image << 32 | feature) keys in component order."""
+    lists of (image << 32 | feature) keys in component order.  ``arrays`` (a
+    dict, optional) receives the raw (nodes, owners, offsets)."""
     pids, ptr, tnode = model_tracks(model, bank)
     nodes, owners, offs = merge_tracks_nodes(bank, u, v, dist, ptr, tnode, stream)
+    if arrays is not None:
+        arrays.update(nodes=nodes, owners=owners, offs=offs)
     slot = np.searchsorted(bank.offsets, nodes, side="right") - 1
     ids = np.asarray(bank.image_ids, np.int64)
     keys = ((ids[slot] << 32) | (nodes - bank.offsets[slot])).tolist()
@@ -183,6 +186,7 @@ def densify_stage(model, feature_store, *, iteration=1, query_images=None, d=BAN
         ok.append(F is not None)
     n_matches = 0
     new_tracks, extensions = [], {}
+    merged = {}
     if pairs:
         import torch
 
@@ -203,7 +207,7 @@ def densify_stage(model, feature_store, *, iteration=1, query_images=None, d=BAN
         u = (qoff[pk] + (qt & 0xFFFF).long()).to(torch.int32).contiguous()
         v = (toff[pk] + ((qt >> 16) & 0xFFFF).long()).to(torch.int32).contiguous()
         dist = rows[:, 2].contiguous().view(torch.float32)
-        new_tracks, extensions = merge_tracks_device(bank, u, v, dist, model)
+        new_tracks, extensions = merge_tracks_device(bank, u, v, dist, model, arrays=merged)
     # grown tracks: reference order, fresh refs against the current ownership
     ext_jobs = []
     for pid in sorted(extensions):
@@ -213,18 +217,38 @@ def densify_stage(model, feature_store, *, iteration=1, query_images=None, d=BAN
         if fresh:
             cand = [_key(r.image_id, r.feature_id) for r in model.points[pid].refs()] + fresh
             ext_jobs.append((pid, fresh, cand))
-    tracks = [t for t in new_tracks] + [c for _, _, c in ext_jobs]
     cams = sorted(model.cameras)
-    cpos = {c: k for k, c in enumerate(cams)}
     K = np.stack([model.cameras[c].K for c in cams]) if cams else np.zeros((0, 3, 3))
     R = np.stack([model.cameras[c].R for c in cams]) if cams else np.zeros((0, 3, 3))
     t = np.stack([model.cameras[c].t for c in cams]) if cams else np.zeros((0, 3))
-    ptr = np.zeros(len(tracks) + 1, np.int64)
-    np.cumsum([len(x) for x in tracks], out=ptr[1:])
-    flat = [k for x in tracks for k in x]
-    cam = np.array([cpos[k >> 32] for k in flat], np.int32)
-    pix = np.array([feature_store.position(k >> 32, k & 0xFFFFFFFF) for k in flat],
-                   np.float64).reshape(-1, 2)
+    # triangulation input as arrays: the new tracks straight from the merge's
+    # segments (bank rows), then the grown tracks' candidate refs
+    n_tr = len(new_tracks) + len(ext_jobs)
+    lens = [len(x) for x in new_tracks] + [len(c) for _, _, c in ext_jobs]
+    ptr = np.zeros(n_tr + 1, np.int64)
+    np.cumsum(lens, out=ptr[1:])
+    if merged:
+        nodes, owners, offs = (np.asarray(merged[k]) for k in ("nodes", "owners", "offs"))
+        sel = np.flatnonzero(owners < 0)
+        new_rows = (np.concatenate([nodes[offs[s]:offs[s + 1]] for s in sel]).astype(np.int64)
+                    if len(sel) else np.zeros(0, np.int64))
+    else:
+        new_rows = np.zeros(0, np.int64)
+    # grown tracks keep refs in images outside this stage's bank: positions from
+    # the feature store for those (few) keys
+    ext_keys = np.fromiter((k for _, _, c in ext_jobs for k in c), np.int64)
+    cam_ids = np.asarray(cams, np.int64)
+    if len(new_rows):
+        slot = np.searchsorted(bank.offsets, new_rows, side="right") - 1
+        new_img = np.asarray(bank.image_ids, np.int64)[slot]
+        new_pix = bank.host.xy.numpy()[new_rows].astype(np.float64).reshape(-1, 2)
+    else:
+        new_img, new_pix = np.zeros(0, np.int64), np.zeros((0, 2))
+    ext_pix = np.array([feature_store.position(int(k) >> 32, int(k) & 0xFFFFFFFF)
+                        for k in ext_keys], np.float64).reshape(-1, 2)
+    cam = np.searchsorted(cam_ids, np.concatenate([new_img, ext_keys >> 32])).astype(np.int32)
+    pix = np.concatenate([new_pix, ext_pix]).reshape(-1, 2)
+    tracks = n_tr
     if tracks:
         st, X, _ = triangulate_batch(K, R, t, ptr, cam, pix, max_error=tri_max_error_px,
                                      min_angle_deg=tri_min_angle_deg)
