@@ -327,7 +327,9 @@ def run_b200(args, rank, world):
     if rank != 0:
         return
     cpu = None
-    if not args.no_cpu:
+    # the CPU baseline is an N = 1 figure (rank 0 alone would share the host cores
+    # with the other ranks' processes)
+    if not args.no_cpu and world == 1:
         sample = args.cpu_pairs or max(8 * cpu_cores(), 96)
         r, cores, n, dt = cpu_oracle_rate(scene, wl, ok, sample)
         cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "port",
@@ -363,7 +365,7 @@ def run_b200(args, rank, world):
         "track_merge": merge,
     }
     if not args.no_localize:
-        line["localization"] = run_localization(args, dev)
+        line["localization"] = run_localization(args, dev, world)
         line["coarse_graph"] = coarse_graph_leg(dev)
     print(json.dumps(line), flush=True)
 
@@ -515,7 +517,7 @@ def cpu_localize_rate(scene, snap, queries, sample, seed=0):
     return len(jobs) / dt, min(cores, len(jobs)), len(jobs), dt
 
 
-def run_localization(args, dev):
+def run_localization(args, dev, world=1):
     import torch
 
     from paper_1512_06235_b200 import _lib, scenes
@@ -600,7 +602,8 @@ def run_localization(args, dev):
                         "ops_per_launch_hw": ops_hw, "ops_per_launch_alg": ops_alg,
                         "kernel_ms": k_ms, "alg_frac": (ops_alg / (k_ms / 1e3) / 1e12) / peak
                         if k_ms > 0 else 0.0}}
-    if not args.no_cpu:
+    out["n_gpus"] = 1        # this leg runs on rank 0's GPU
+    if not args.no_cpu and world == 1:
         r, cores, ns, cdt = cpu_localize_rate(scene, snap, queries, max(cpu_cores(), 8))
         out["cpu_baseline"] = {"value": r, "unit": "images/s", "cores": cores, "kind": "port",
                                "sample": f"{ns} query images in {cdt:.1f}s (oracle/localize.py: "
