@@ -155,6 +155,29 @@ def measured_peaks():
     return HBM_FALLBACK_GBS, "fallback"
 
 
+def ncu_unit_utilization(name):
+    """Pipe / issue utilizations of a kernel from its committed ncu capture: which
+    unit (if any) bounds it."""
+    path = os.path.join(REPO, "profiles", name)
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        j = json.load(f)
+    pick = {"issue_active_pct": "sm__issue_active.avg.pct_of_peak_sustained_elapsed",
+            "alu_pipe_pct": "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+            "fma_pipe_pct": "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+            "tensor_pipe_pct": "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+            "l2_sector_pct": "lts__t_sectors.sum.pct_of_peak_sustained_elapsed",
+            "dram_pct": "dram__throughput.avg.pct_of_peak_sustained_elapsed"}
+    out = {}
+    for k, m in pick.items():
+        v = j.get(m)
+        if isinstance(v, dict):
+            out[k] = round(float(v["value"]), 2)
+    out["source"] = f"profiles/{name}"
+    return out
+
+
 def ncu_traffic_per_pair():
     """dram read+write bytes per pair of match_kernel from the committed ncu capture."""
     path = os.path.join(REPO, "profiles", "ncu_match_kernel.json")
@@ -355,7 +378,8 @@ def run_b200(args, rank, world):
                      "traffic": (tpp * len(mine) / max(k_n, 1)) if tpp else None,
                      "algorithmic_bytes_per_launch": alg / max(k_n, 1),
                      "launches": k_n, "kernel_ms_per_step": k_ms,
-                     "step_frac": (alg / (step_ms / 1e3) / 1e9) / peak},
+                     "step_frac": (alg / (step_ms / 1e3) / 1e9) / peak,
+                     "units": ncu_unit_utilization("ncu_match_kernel.json")},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "steps_ms": [round(x, 2) for x in e2e_ms]},
@@ -601,7 +625,8 @@ def run_localization(args, dev, world=1):
                         "peak_kind": "2x measured bf16 (int8 dense rate)",
                         "ops_per_launch_hw": ops_hw, "ops_per_launch_alg": ops_alg,
                         "kernel_ms": k_ms, "alg_frac": (ops_alg / (k_ms / 1e3) / 1e12) / peak
-                        if k_ms > 0 else 0.0}}
+                        if k_ms > 0 else 0.0,
+                        "units": ncu_unit_utilization("ncu_knn_tc_kernel.json")}}
     out["n_gpus"] = 1        # this leg runs on rank 0's GPU
     if not args.no_cpu and world == 1:
         r, cores, ns, cdt = cpu_localize_rate(scene, snap, queries, max(cpu_cores(), 8))
