@@ -314,3 +314,34 @@ def test_16k_feature_pairs_match_oracle():
         np.testing.assert_array_equal(d[sel], od)
         np.testing.assert_array_equal(r[sel], orr)
         np.testing.assert_array_equal(stats[j], ost)
+
+
+def test_bench_workload_sample_matches_oracle():
+    """The bench's own C3 step (all 5,401 pairs of the 320-camera scene in one call):
+    a seeded sample of pairs equals the C oracle (tools/parity_sweep.py does 256)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import guided as og
+    from paper_1512_06235_b200 import scenes
+    from paper_1512_06235_b200.guided import match_pairs
+
+    scene, snap = scenes.build("C3", n_cameras=320)
+    wl = scenes.pair_workload(scene, snap)
+    ok = np.flatnonzero(wl.valid)
+    bank = _bank(scene.feature_sets)
+    ql = [wl.untracked[int(wl.q_img[k])] for k in ok]
+    pk, q, t, d, r = match_pairs(bank, wl.q_img[ok], wl.t_img[ok], wl.F[ok], ql).to_host()
+    pick = np.random.default_rng(7).choice(len(ok), size=48, replace=False)
+
+    def one(j):
+        k = int(ok[j])
+        qi, ti = int(wl.q_img[k]), int(wl.t_img[k])
+        fq, ft = scene.feature_sets[qi], scene.feature_sets[ti]
+        oq, ot, od, orr, _ = og.guided_match(fq.xy, fq.descriptors, ft.xy, ft.descriptors,
+                                             ft.width, ft.height, wl.F[k], wl.untracked[qi])
+        sel = pk == j
+        return (np.array_equal(q[sel], oq) and np.array_equal(t[sel], ot)
+                and np.array_equal(d[sel], od) and np.array_equal(r[sel], orr))
+
+    with ThreadPoolExecutor(8) as ex:
+        assert all(ex.map(one, pick))
