@@ -112,7 +112,31 @@ class ClockSampler:
     def __init__(self, device_index=0):
         self.samples, self.stop, self.dev = [], threading.Event(), device_index
 
+    def _run_nvml(self):
+        """NVML sampling every ~5 ms (the timed region is a few hundred ms)."""
+        import pynvml as nv
+
+        nv.nvmlInit()
+        try:
+            h = nv.nvmlDeviceGetHandleByIndex(self.dev)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+            while not self.stop.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append([str(sm), str(mx)] +
+                                    ["Active" if r & b else "Not Active" for b in bits])
+                self.stop.wait(0.005)
+        finally:
+            nv.nvmlShutdown()
+
     def _run(self):
+        try:
+            self._run_nvml()
+            return
+        except Exception:
+            self.samples.clear()
         while not self.stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", f"--id={self.dev}",
