@@ -327,7 +327,10 @@ def run_b200(args, rank, world):
     tpp = ncu_traffic_per_pair()
 
     # ---- the stage's next step on the same matches: device track merge (densify.py:68-158)
-    merge = track_merge_leg(bank, wl, mine, res, snap, dev, scene)
+    try:
+        merge = track_merge_leg(bank, wl, mine, res, snap, dev, scene, world, rank, ok)
+    except Exception as exc:                        # never lose the step's line over it
+        merge = {"error": f"{type(exc).__name__}: {exc}"}
 
     # ---- e2e through the public API with host buffers (pinned H2D + D2H every step)
     torch.cuda.synchronize()
@@ -449,16 +452,29 @@ def coarse_graph_leg(dev, n_cameras=40):
             "wall_ms": dt * 1e3, "kernel_ms": kern}
 
 
-def track_merge_leg(bank, wl, mine, res, snap, dev, scene=None):
-    """msfm_merge_tracks over this rank's matches + the coarse tracks (bank nodes)."""
+def track_merge_leg(bank, wl, mine, res, snap, dev, scene=None, world=1, rank=0, ok=None):
+    """msfm_merge_tracks over the step's matches + the coarse tracks (bank nodes).
+    With several ranks every rank's rows are gathered (NCCL) and rank 0 merges all
+    of them — the gather of tracks of an N-GPU run; other ranks return None."""
     import torch
 
     from paper_1512_06235_b200 import _lib
     from paper_1512_06235_b200.densify import merge_tracks_nodes
 
     rows, n = res.packed()
-    qoff = torch.from_numpy(bank.offsets[[bank.index_of[int(q)] for q in wl.q_img[mine]]]).to(dev)
-    toff = torch.from_numpy(bank.offsets[[bank.index_of[int(t)] for t in wl.t_img[mine]]]).to(dev)
+    pairs = mine
+    if world > 1:
+        from paper_1512_06235_b200.dist import gather_rows
+
+        g = rows.clone()
+        g[:, 0] = rank + world * g[:, 0]            # rank-local pair -> index into `ok`
+        rows = gather_rows(g, world)
+        if rank != 0:
+            return None
+        pairs = ok
+        n = int(rows.shape[0])
+    qoff = torch.from_numpy(bank.offsets[bank.slots(wl.q_img[pairs])]).to(dev)
+    toff = torch.from_numpy(bank.offsets[bank.slots(wl.t_img[pairs])]).to(dev)
     pk = rows[:, 0].long()
     u = (qoff[pk] + (rows[:, 1] & 0xFFFF).long()).to(torch.int32).contiguous()
     v = (toff[pk] + ((rows[:, 1] >> 16) & 0xFFFF).long()).to(torch.int32).contiguous()

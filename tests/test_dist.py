@@ -69,3 +69,43 @@ def test_gloo_gather_restores_pair_order(tmp_path):
         ref[0] += [k] * m; ref[1] += list(q); ref[2] += list(t)
         ref[3] += list(np.float32(d)); ref[4] += list(np.float32(r))
     np.testing.assert_array_equal(got, np.array(ref, np.float64))
+
+
+def _merge_gather_worker(rank, world, port, n_pairs, out_path):
+    """bench.track_merge_leg's N > 1 gather: each rank's rows carry rank-local pair
+    indices (its call over ok[rank::world]); mapped to rank + world * local they
+    index the global pair list on rank 0."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1512_06235_b200.dist import gather_rows
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mine = shard(n_pairs, rank, world)
+    # one row per match; pair j of this rank has (global pair % 5) matches
+    rows = []
+    for j, k in enumerate(mine):
+        for m in range(int(k) % 5):
+            rows.append([j, int(k) * 10 + m, 0, 0])
+    rows = torch.tensor(rows if rows else np.zeros((0, 4)), dtype=torch.int32).reshape(-1, 4)
+    g = rows.clone()
+    g[:, 0] = rank + world * g[:, 0]
+    allrows = gather_rows(g, world)
+    if rank == 0:
+        np.save(out_path, allrows.numpy())
+    dist.destroy_process_group()
+
+
+def test_gloo_merge_gather_maps_local_pairs_to_global():
+    world, n_pairs = 2, 23
+    out = os.path.join(os.environ.get("TMPDIR", "/tmp"), f"mg_{os.getpid()}.npy")
+    mp.spawn(_merge_gather_worker, args=(world, _free_port(), n_pairs, out), nprocs=world,
+             join=True)
+    got = np.load(out)
+    os.remove(out)
+    # every match's global pair index agrees with the payload written for that pair
+    np.testing.assert_array_equal(got[:, 1] // 10, got[:, 0])
+    want = sorted((k, k * 10 + m) for k in range(n_pairs) for m in range(k % 5))
+    assert sorted(map(tuple, got[:, :2].tolist())) == want
