@@ -28,3 +28,7 @@ def test_install_patches_every_route_and_uninstall_restores():
         assert msfm.guided.guided_match_pair is orig
     finally:
         sys.path.remove(REF)
+        # later tests resolve the reference's types through `msfm` when importable:
+        # leave no trace of it
+        for name in [n for n in sys.modules if n == "msfm" or n.startswith("msfm.")]:
+            del sys.modules[name]
