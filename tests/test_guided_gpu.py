@@ -345,3 +345,36 @@ def test_bench_workload_sample_matches_oracle():
 
     with ThreadPoolExecutor(8) as ex:
         assert all(ex.map(one, pick))
+
+
+def test_staged_rows_with_empty_lists_and_images():
+    """match_pairs_rows_staged with empty query lists, a zero-feature image and a
+    degenerate (NaN) F: identical to the resident path."""
+    import torch
+
+    from paper_1512_06235_b200 import scenes
+    from paper_1512_06235_b200.bank import HostBank
+    from paper_1512_06235_b200.guided import match_pairs_rows, match_pairs_rows_staged
+    from paper_1512_06235_b200.types import FeatureSet
+
+    scene, snap = scenes.build("C1", n_cameras=8)
+    wl = scenes.pair_workload(scene, snap)
+    ok = np.flatnonzero(wl.valid)
+    sets = dict(scene.feature_sets)
+    empty_id = max(sets) + 1
+    sets[empty_id] = FeatureSet(image_id=empty_id, width=640, height=480,
+                                xy=np.zeros((0, 2), np.float32), scale=np.zeros(0, np.float32),
+                                orientation=np.zeros(0, np.float32),
+                                descriptors=np.zeros((0, 128), np.uint8))
+    q = list(wl.q_img[ok]) + [int(wl.q_img[ok[0]]), empty_id]
+    t = list(wl.t_img[ok]) + [empty_id, int(wl.t_img[ok[0]])]
+    F = np.concatenate([wl.F[ok], np.full((1, 3, 3), np.nan), wl.F[ok[:1]]])
+    ql = [wl.untracked[int(wl.q_img[k])] for k in ok]
+    ql[1] = np.zeros(0, np.int32)                          # a pair with no queries
+    ql += [wl.untracked[int(wl.q_img[ok[0]])], np.zeros(0, np.int32)]
+    bank = _bank(sets)
+    want = match_pairs_rows(bank, q, t, F, ql, chunk_pairs=5)
+    got, _ = match_pairs_rows_staged(HostBank(sets), q, t, F, ql, chunk_pairs=5,
+                                     segment_images=2, first_chunk_pairs=3)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(got.view(np.int32), want.view(np.int32))
