@@ -187,3 +187,59 @@ def test_localize_all_holdouts_within_a_tenth_of_a_degree():
     assert len(newly) > 0
     for i in newly:
         assert _rot_err_deg(model.cameras[i].R, scene.cameras[i].R) < 0.1
+
+
+def _model_state(model):
+    pids = sorted(model.points)
+    return ([(p, sorted(model.points[p].track.items())) for p in pids],
+            np.stack([model.points[p].position for p in pids]) if pids else np.zeros((0, 3)))
+
+
+def test_densify_stage_is_deterministic():
+    """Two runs (and any `threads` value) leave byte-identical models, although the
+    merge and the dedupe run on atomics (reference: thread-count invariance)."""
+    from paper_1512_06235_b200 import scenes
+    from paper_1512_06235_b200.densify import densify_stage
+
+    scene, snap = scenes.build("C1", n_cameras=14)
+    states = []
+    for threads in (1, 8, 1):
+        model = scenes.snapshot_to_model(scene, snap)
+        densify_stage(model, scene.store(), threads=threads)
+        states.append(_model_state(model))
+    for tracks, X in states[1:]:
+        assert tracks == states[0][0]
+        assert np.array_equal(X, states[0][1])
+    assert len(states[0][0]) > len(snap.point_xyz)          # the stage added points
+
+
+def test_localize_all_is_order_invariant():
+    """localize_all gives the same newly-registered set and poses whatever order
+    the unregistered images are visited in (reference: order/thread invariance)."""
+    from golden_io import load_localize
+    from paper_1512_06235_b200 import scenes
+    from paper_1512_06235_b200.localize import localize_all
+
+    kw, scene, snap, z = load_localize("localize_holdout.npz")
+    store = scene.store()
+    K = {i: scene.cameras[i].K for i in store.sets}
+
+    class _NoGraph:
+        def neighbors(self, image_id):
+            return []
+
+        def match_count(self, a, b):
+            return 0
+
+    out = []
+    for order in (None, "reverse"):
+        model = scenes.snapshot_to_model(scene, snap)
+        unreg = [i for i in sorted(store.sets) if not model.is_registered(i)]
+        newly, _ = localize_all(model, store, _NoGraph(), K,
+                                order=None if order is None else unreg[::-1])
+        out.append((sorted(newly), {i: (model.cameras[i].R.copy(), model.cameras[i].t.copy())
+                                    for i in newly}))
+    assert out[0][0] == out[1][0] and out[0][0]
+    for i in out[0][0]:
+        assert np.array_equal(out[0][1][i][0], out[1][1][i][0])
+        assert np.array_equal(out[0][1][i][1], out[1][1][i][1])
