@@ -248,6 +248,8 @@ struct alignas(16) SGRec {
 #endif
 constexpr int SG_NT = MSFM_SG_NT;          // n8 member tiles per super-group
 constexpr int SG_MEMBERS = 8 * SG_NT;
+// per-candidate C' bits are one 16-bit mask over the super-group's groups (<= members)
+static_assert(SG_MEMBERS <= 16, "MSFM_SG_NT > 2 needs wider per-candidate group masks");
 #ifndef MSFM_MATCH_MINB
 #define MSFM_MATCH_MINB (SG_NT == 1 ? 6 : 4)
 #endif
