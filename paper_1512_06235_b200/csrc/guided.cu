@@ -165,6 +165,8 @@ struct GridBuildArgs {
     int32_t* sub; int32_t* rcount; int32_t* ccount; int32_t* rcur; int32_t* ccur;
     int32_t* rmem; int32_t* cmem; int4* rrec; int4* crec; const int32_t* norm2; double D;
     int img0;             // first image of the range this launch builds (blockIdx.x + img0)
+    const uint8_t* desc;  // when norm_out is set, grid_count also writes |desc|^2 there
+    int32_t* norm_out;
 };
 
 __device__ __forceinline__ int bucket_of(float v, double D, int nb) {
@@ -178,6 +180,18 @@ __global__ void grid_count_kernel(GridBuildArgs a) {
     const int n = a.img_n[img];
     const int nbx = a.dims[2 * img], nby = a.dims[2 * img + 1];
     for (int f = threadIdx.x; f < n; f += blockDim.x) {
+        if (a.norm_out) {
+            const uint4* row = reinterpret_cast<const uint4*>(a.desc + (off + f) * 128);
+            unsigned s = 0;
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                const uint4 v = __ldg(row + k);
+                const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int j = 0; j < 4; j++) s = __dp4a(w[j], w[j], s);   // u8 x u8, exact
+            }
+            a.norm_out[off + f] = (int32_t)s;
+        }
         float2 p = a.xy[off + f];
         int u = exact_subcell((double)p.x, a.D), v = exact_subcell((double)p.y, a.D);
         a.sub[off + f] = (u & 0xffff) | (v << 16);
@@ -1694,17 +1708,20 @@ extern "C" int msfm_grid_dims(int32_t width, int32_t height, double D, int32_t d
 
 extern "C" size_t msfm_grid_workspace_bytes(int64_t n_buckets_total) {
     int64_t nb = (n_buckets_total + 1 + SCAN_T * SCAN_PER - 1) / (SCAN_T * SCAN_PER) + 1;
-    return aligned_bytes<int32_t>(n_buckets_total + 1) * 2 + aligned_bytes<int32_t>(nb) + 1024;
+    return aligned_bytes<int32_t>(n_buckets_total + 1) * 2 + aligned_bytes<int32_t>(nb) * 2 +
+           1024;
 }
 
-extern "C" int msfm_grid_build_range(const msfm_bank* bank, const int32_t* d_dims,
-                                     const int64_t* d_roff, const int64_t* d_coff,
-                                     int64_t n_buckets_total, int32_t img0, int32_t img1,
-                                     int64_t bucket0, int64_t bucket1, int64_t feat0, double D,
-                                     int32_t* d_sub, int32_t* d_rstart, int32_t* d_cstart,
-                                     int32_t* d_rmem, int32_t* d_cmem, int32_t* d_rrec,
-                                     int32_t* d_crec, void* d_workspace, size_t workspace_bytes,
-                                     void* stream) {
+// the range build; with norms, the count pass also writes the range's |desc|^2 (the
+// staged matcher's per-range indexing: one pass over the rows instead of two)
+static int grid_build_range_impl(const msfm_bank* bank, const int32_t* d_dims,
+                                 const int64_t* d_roff, const int64_t* d_coff,
+                                 int64_t n_buckets_total, int32_t img0, int32_t img1,
+                                 int64_t bucket0, int64_t bucket1, int64_t feat0, double D,
+                                 int32_t* d_sub, int32_t* d_rstart, int32_t* d_cstart,
+                                 int32_t* d_rmem, int32_t* d_cmem, int32_t* d_rrec,
+                                 int32_t* d_crec, void* d_workspace, size_t workspace_bytes,
+                                 void* stream, int32_t* norm_out) {
     if (!bank || !(D > 0) || n_buckets_total < 0 || img0 < 0 || img1 < img0 ||
         img1 > bank->n_images || bucket0 < 0 || bucket1 < bucket0 || bucket1 > n_buckets_total ||
         feat0 < 0 || feat0 > INT32_MAX) {
@@ -1720,7 +1737,8 @@ extern "C" int msfm_grid_build_range(const msfm_bank* bank, const int32_t* d_dim
     int32_t* rcur = ar.take<int32_t>(n_buckets_total + 1);
     int32_t* ccur = ar.take<int32_t>(n_buckets_total + 1);
     int64_t nb = (n_buckets_total + 1 + SCAN_T * SCAN_PER - 1) / (SCAN_T * SCAN_PER) + 1;
-    int32_t* bsum = ar.take<int32_t>(nb);
+    int32_t* bsum0 = ar.take<int32_t>(nb);
+    int32_t* bsum1 = ar.take<int32_t>(nb);
     // counts go to the cursor arrays; the scan writes the CSR starts [bucket0, bucket1]
     // (the closing start included, = the next range's first start) without ever
     // touching a start another range already published
@@ -1730,15 +1748,19 @@ extern "C" int msfm_grid_build_range(const msfm_bank* bank, const int32_t* d_dim
     GridBuildArgs a{reinterpret_cast<const float2*>(bank->d_xy), bank->d_img_off, bank->d_img_n,
                     bank->d_img_wh, d_dims, d_roff, d_coff, d_sub, rcur, ccur, rcur, ccur,
                     d_rmem, d_cmem, reinterpret_cast<int4*>(d_rrec),
-                    reinterpret_cast<int4*>(d_crec), bank->d_norm2, D, img0};
+                    reinterpret_cast<int4*>(d_crec), bank->d_norm2, D, img0, bank->d_desc, norm_out};
     if (img1 > img0) {
         grid_count_kernel<<<img1 - img0, 256, 0, st>>>(a);
         MSFM_LAUNCH_CHECK();
         count_launches(1);
     }
-    int rc = exclusive_scan(rcur + bucket0, n, d_rstart + bucket0, bsum, st, (int32_t)feat0);
-    if (rc) return rc;
-    rc = exclusive_scan(ccur + bucket0, n, d_cstart + bucket0, bsum, st, (int32_t)feat0);
+    // row and column tables in one scan launch set
+    Scan2 sc;
+    sc.data[0] = rcur + bucket0; sc.data[1] = ccur + bucket0;
+    sc.copy[0] = d_rstart + bucket0; sc.copy[1] = d_cstart + bucket0;
+    sc.bsum[0] = bsum0; sc.bsum[1] = bsum1;
+    sc.n = n; sc.base0 = (int32_t)feat0;
+    int rc = exclusive_scan2(sc, st);
     if (rc) return rc;
     if (img1 > img0) {
         grid_scatter_kernel<<<img1 - img0, 256, 0, st>>>(a);
@@ -1746,6 +1768,20 @@ extern "C" int msfm_grid_build_range(const msfm_bank* bank, const int32_t* d_dim
         count_launches(1);
     }
     return MSFM_OK;
+}
+
+extern "C" int msfm_grid_build_range(const msfm_bank* bank, const int32_t* d_dims,
+                                     const int64_t* d_roff, const int64_t* d_coff,
+                                     int64_t n_buckets_total, int32_t img0, int32_t img1,
+                                     int64_t bucket0, int64_t bucket1, int64_t feat0, double D,
+                                     int32_t* d_sub, int32_t* d_rstart, int32_t* d_cstart,
+                                     int32_t* d_rmem, int32_t* d_cmem, int32_t* d_rrec,
+                                     int32_t* d_crec, void* d_workspace, size_t workspace_bytes,
+                                     void* stream) {
+    return grid_build_range_impl(bank, d_dims, d_roff, d_coff, n_buckets_total, img0, img1,
+                                 bucket0, bucket1, feat0, D, d_sub, d_rstart, d_cstart, d_rmem,
+                                 d_cmem, d_rrec, d_crec, d_workspace, workspace_bytes, stream,
+                                 nullptr);
 }
 
 extern "C" int msfm_grid_build(const msfm_bank* bank, const int32_t* d_dims, const int64_t* d_roff,
@@ -1936,16 +1972,15 @@ static int guided_match_impl(const msfm_bank* bank, const msfm_grids* grids, int
             // a plan hands the matcher the (otherwise read-only) |desc|^2 and index
             // arrays of its ranges to fill
             auto w32 = [](const int32_t* p) { return const_cast<int32_t*>(p); };
-            int rc = msfm_feature_norms(bank->d_desc + 128 * f0, f1 - f0,
-                                        w32(bank->d_norm2) + f0, st);
-            if (rc) return rc;
-            rc = msfm_grid_build_range(bank, grids->d_dims, grids->d_roff, grids->d_coff,
-                                       plan->n_buckets_total, plan->img0[r], i1,
-                                       plan->bucket0[r], plan->bucket1[r], f0, grids->D,
-                                       w32(grids->d_sub), w32(grids->d_rstart),
-                                       w32(grids->d_cstart), w32(grids->d_rmem),
-                                       w32(grids->d_cmem), w32(grids->d_rrec), w32(grids->d_crec),
-                                       plan->grid_workspace, plan->grid_workspace_bytes, st);
+            // |desc|^2 of the range computed by the build's count pass
+            int rc = grid_build_range_impl(bank, grids->d_dims, grids->d_roff, grids->d_coff,
+                                           plan->n_buckets_total, plan->img0[r], i1,
+                                           plan->bucket0[r], plan->bucket1[r], f0, grids->D,
+                                           w32(grids->d_sub), w32(grids->d_rstart),
+                                           w32(grids->d_cstart), w32(grids->d_rmem),
+                                           w32(grids->d_cmem), w32(grids->d_rrec),
+                                           w32(grids->d_crec), plan->grid_workspace,
+                                           plan->grid_workspace_bytes, st, w32(bank->d_norm2));
             if (rc) return rc;
         }
         plan_kernel<<<1, SCAN_T, 0, st>>>(a);
