@@ -7,3 +7,15 @@ a CUDA device the entry points raise DeviceUnavailableError.
 """
 
 __version__ = "0.1.0"
+
+
+def reserve_device_memory(gigabytes: float, device=None) -> None:
+    """Grow PyTorch's caching allocator by one block of ``gigabytes`` and release it
+    to the cache: later stage buffers are carved from it instead of each paying a
+    fresh ``cudaMalloc`` (tens of ms apiece on a fresh process), which is what makes
+    a pipeline's first call of every stage slow."""
+    import torch
+
+    dev = torch.device(device or "cuda")
+    block = torch.empty(int(gigabytes * (1 << 30)), dtype=torch.uint8, device=dev)
+    del block

@@ -33,7 +33,7 @@ from paper_1512_06235_b200.triangulation import triangulate_batch
 from paper_1512_06235_b200.types import Camera, DegenerateGeometryError
 
 config = sys.argv[1] if len(sys.argv) > 1 else "C4"
-n_cam = int(sys.argv[2]) if len(sys.argv) > 2 else None
+n_cam = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else None
 T = {}
 
 
@@ -57,6 +57,10 @@ def warm(name, fn):
     return out
 
 
+if "--reserve" in sys.argv:
+    # one cached device block for every stage's buffers (see reserve_device_memory)
+    from paper_1512_06235_b200 import reserve_device_memory
+    reserve_device_memory(float(sys.argv[sys.argv.index("--reserve") + 1]))
 t0 = time.perf_counter()
 scene, snap = scenes.build(config, n_cameras=n_cam)
 N = len(scene.cameras)
