@@ -161,7 +161,8 @@ typedef struct {
     float ratio;         /* Lowe ratio, compared in f32 (RATIO_GUIDED = 0.8)     */
     float single_cap;    /* single-candidate cap (SINGLE_CANDIDATE_CAP = 45)     */
     int32_t max_nt;      /* max target feature count over the batch (<= 65536)   */
-    int32_t chunk_pairs; /* pairs per internal chunk (workspace bound), 0 = auto  */
+    int32_t chunk_pairs; /* pairs per internal chunk (workspace bound); 0 = auto:
+                          * up to 8192 pairs and 48M query slots per chunk       */
     int32_t strategy;    /* candidate strategy of guided_match_pair (guided.py:425-431):
                           * 0 grid (cells of the samples, default), 1 linear
                           * (|rep line| <= d, guided.py:190-194), 2 radial (disks of

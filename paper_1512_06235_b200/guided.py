@@ -155,6 +155,7 @@ def match_pairs_rows(bank: FeatureBank, q_img, t_img, F, query_lists, *, d: floa
         raise ValueError(f"unknown strategy {strategy!r}")
     D = float(grid_d) if grid_d is not None else float(d) * float(inflation)
     P = len(q_img)
+    chunk_pairs = chunk_pairs or 1024       # several chunks: the readback overlaps compute
     dev = bank.device
     if device_inputs is None:
         device_inputs = prepare_pairs(bank, q_img, t_img, F, query_lists)
@@ -253,6 +254,8 @@ def match_pairs_rows_staged(host, q_img, t_img, F, query_lists, *, device=None,
         raise ValueError(f"cell half-size d must be positive, got {d}")
     D = float(grid_d) if grid_d is not None else float(d) * float(inflation)
     P = len(q_img)
+    # chunks of 1024 pairs: the upload and the row readback pipeline across them
+    chunk_pairs = chunk_pairs or 1024
     if bank is None or not getattr(bank, "staged", False) or bank.host is not host:
         bank = FeatureBank(host=host, device=device, staged=True)
     nimg = len(bank.image_ids)
