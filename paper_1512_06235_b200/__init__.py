@@ -8,6 +8,12 @@ a CUDA device the entry points raise DeviceUnavailableError.
 
 __version__ = "0.1.0"
 
+# use the caller's msfm classes (errors, Match, FeatureRef, ...) when the
+# reference package is importable (types.adopt_reference_types)
+from .types import adopt_reference_types as _adopt
+
+_adopt()
+
 
 def reserve_device_memory(gigabytes: float, device=None) -> None:
     """Grow PyTorch's caching allocator by one block of ``gigabytes`` and release it

@@ -15,6 +15,7 @@ import numpy as np
 
 from . import _lib
 from .bank import FeatureBank
+from .types import LocalizationResult, SetCover
 
 RATIO_UNGUIDED = 0.6     # matching.py:21
 SINGLE_CANDIDATE_CAP = 45.0
@@ -317,54 +318,82 @@ SET_COVER_ENGAGE_POINTS = 100_000
 RANKED_TOP_K = 10
 
 
-@dataclass
-class LocalizationResult:
-    image_id: int
-    method: str
-    correspondences: list = field(default_factory=list)
-    pose: object = None
-    inliers: int = 0
-    inlier_refs: list = field(default_factory=list)
-    reason: str = ""
-
-
-@dataclass
-class SetCover:
-    selected: list
-    k: int
-    coverage: dict
-
-
 def compute_set_cover(model, k: int = SET_COVER_K) -> SetCover:
-    """Lazy-greedy k-cover (localize.py:62-96): host side, off the per-image path."""
+    """k-cover of the cameras by points (localize.py:62-96): repeatedly take the
+    point that sees the most cameras still short of k views; ties go to the
+    longer track, then to the lower point id; stop when every camera has k views
+    or no point adds any.  Host side, off the per-image path.
+
+    Restated over arrays: the tracks become a CSR of camera slots with its
+    slot -> points inverse, and every point's score is a counter that drops by
+    one when a camera it sees reaches k (scores only fall).  A bucket queue
+    indexed by score, each bucket a heap of static (-length, id) ranks, yields
+    the argmax: entries whose score went stale are moved to their current
+    bucket when they surface."""
     import heapq
 
     if k < 1:
         raise ValueError(f"coverage target must be >= 1, got {k}")
-    remaining = {i: k for i in model.cameras}
-    coverage = {i: 0 for i in model.cameras}
+    cams = list(model.cameras)
+    pids = np.array(sorted(model.points), dtype=np.int64)
+    tracks = [list(model.points[int(p)].track) for p in pids]
+    lens = np.fromiter((len(t) for t in tracks), np.int64, len(tracks))
+    ptr = np.zeros(len(pids) + 1, np.int64)
+    np.cumsum(lens, out=ptr[1:])
+    img = np.fromiter((i for t in tracks for i in t), np.int64, int(ptr[-1]))
+    cam_ids = np.array(cams, dtype=np.int64)
+    slot = np.full(len(img), -1, np.int64)
+    if len(cams):
+        srt = np.argsort(cam_ids, kind="stable")
+        pos = np.minimum(np.searchsorted(cam_ids[srt], img), len(cams) - 1)
+        hit = cam_ids[srt][pos] == img
+        slot[hit] = srt[pos[hit]]
+    owner = np.repeat(np.arange(len(pids)), lens)
+    seen = slot >= 0
+    score = np.bincount(owner[seen], minlength=len(pids)).astype(np.int64)
+    by_slot = np.argsort(slot[seen], kind="stable")
+    obs_owner = owner[seen][by_slot]
+    obs_ptr = np.searchsorted(slot[seen][by_slot], np.arange(len(cams) + 1))
+    rank_order = np.lexsort((pids, -lens))          # rank r -> point index
+    top = int(score.max()) if len(pids) else 0
+    buckets = [[] for _ in range(top + 1)]
+    for r, p in enumerate(rank_order):              # ascending ranks: each list is a heap
+        if score[p] > 0:
+            buckets[score[p]].append(r)
+    remaining = np.full(len(cams), k, np.int64)
+    unsaturated = len(cams)
     selected = []
-
-    def score(pid):
-        return sum(1 for i in model.points[pid].track if remaining.get(i, 0) > 0)
-
-    heap = [(-score(p), -len(model.points[p].track), p) for p in sorted(model.points)]
-    heapq.heapify(heap)
-    while heap:
-        neg_s, neg_len, pid = heapq.heappop(heap)
-        s = score(pid)
-        if s == 0:
+    while top > 0 and unsaturated > 0:
+        if not buckets[top]:
+            top -= 1
             continue
-        if -neg_s != s:
-            heapq.heappush(heap, (-s, neg_len, pid))
+        r = heapq.heappop(buckets[top])
+        p = rank_order[r]
+        s = int(score[p])
+        if s != top:
+            if s > 0:
+                heapq.heappush(buckets[s], r)
             continue
-        selected.append(pid)
-        for i in model.points[pid].track:
-            if remaining.get(i, 0) > 0:
-                remaining[i] -= 1
-            coverage[i] = coverage.get(i, 0) + 1
-        if all(v == 0 for v in remaining.values()):
-            break
+        selected.append(int(pids[p]))
+        sl = slot[ptr[p]:ptr[p + 1]]
+        sl = sl[sl >= 0]
+        sl = sl[remaining[sl] > 0]
+        remaining[sl] -= 1
+        for c in sl[remaining[sl] == 0]:
+            score[obs_owner[obs_ptr[c]:obs_ptr[c + 1]]] -= 1
+            unsaturated -= 1
+    coverage = {i: 0 for i in cams}
+    sel_idx = np.searchsorted(pids, np.array(selected, dtype=np.int64))
+    if len(sel_idx):
+        per = np.concatenate([slot[ptr[p]:ptr[p + 1]] for p in sel_idx])
+        counts = np.bincount(per[per >= 0], minlength=len(cams))
+        for j, i in enumerate(cams):
+            coverage[i] = int(counts[j])
+        if (per < 0).any():                         # track images without a camera
+            for p in sel_idx:
+                for i, c in zip(tracks[p], slot[ptr[p]:ptr[p + 1]]):
+                    if c < 0:
+                        coverage[i] = coverage.get(i, 0) + 1
     return SetCover(selected=selected, k=k, coverage=coverage)
 
 

@@ -69,7 +69,7 @@ def coarse_snapshot(scene, registered, eta: float | None = 20.0) -> Snapshot:
     obs_pid = np.concatenate(obs_pid)
     # triangulable = seen in >= 2 images (GT model membership, synth.py:86-116)
     seen = np.bincount(obs_pid, minlength=n_pts)
-    tier_arr = np.array([tiers[i] if eta is not None else 1 << 40
+    tier_arr = np.array([tiers.get(i, 0) if eta is not None else 1 << 40
                          for i in range(len(scene.cameras))], dtype=np.int64)
     tier_of = tier_arr[obs_img]
     keep = reg_mask[obs_img] & (obs_fid < tier_of) & (seen[obs_pid] >= 2)

@@ -95,7 +95,10 @@ def _levels(rng, n):
     return rng.choice(_LEVELS, size=n, p=w / w.sum())
 
 
-def generate_scene(spec: SceneSpec) -> Scene:
+def generate_scene(spec: SceneSpec, first_cameras: int | None = None) -> Scene:
+    """``first_cameras``: stop after that many cameras' feature sets.  The draws
+    are sequential per camera, so those cameras (and every pose and point) are
+    exactly the full scene's; used to sample the 3000-camera C5 recipe."""
     rng = np.random.default_rng(spec.seed)
     centres = _rig(spec, rng)
     K = make_intrinsics(spec.focal, spec.image_width / 2.0, spec.image_height / 2.0)
@@ -123,7 +126,7 @@ def generate_scene(spec: SceneSpec) -> Scene:
 
     W, H = spec.image_width, spec.image_height
     sets, owners, warnings = {}, {}, []
-    for cam in cams:
+    for cam in cams[:first_cameras]:
         uv, depth = cam.project(X)
         if spec.pixel_noise > 0:
             uv = uv + rng.normal(0.0, spec.pixel_noise, size=uv.shape)

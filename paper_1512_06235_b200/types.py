@@ -355,3 +355,115 @@ class SearchStats:
     def add(self, queries: int, candidates: int) -> None:
         self.queries += queries
         self.candidates += candidates
+
+
+
+@dataclass
+class LocalizationResult:
+    """localize.py:41-48"""
+    image_id: int
+    method: str
+    correspondences: list = field(default_factory=list)
+    pose: object = None
+    inliers: int = 0
+    inlier_refs: list = field(default_factory=list)
+    reason: str = ""
+
+
+@dataclass
+class SetCover:
+    """localize.py:34-38"""
+    selected: list
+    k: int
+    coverage: dict
+
+
+# --------------------------------------------------------------------------
+# the caller's own classes (SURVEY.md §8b "Data crossing" / "Error conventions")
+# --------------------------------------------------------------------------
+# When the reference package ``msfm`` is importable, every value type and error
+# class above is replaced by the reference's own class, in this module and in
+# every module of the package that bound it, so a drop-in raises
+# ``msfm.errors.InsufficientDataError`` and returns ``msfm.matching.Match`` /
+# ``msfm.model.FeatureRef`` objects that compare, hash and sort with the
+# caller's.  On a box without ``msfm`` (the GPU pool) the classes above stand in.
+
+_REFERENCE_CLASSES = {
+    "MsfmError": ("msfm.errors", "MsfmError"),
+    "FormatError": ("msfm.errors", "FormatError"),
+    "DegenerateGeometryError": ("msfm.errors", "DegenerateGeometryError"),
+    "InsufficientDataError": ("msfm.errors", "InsufficientDataError"),
+    "NotRegisteredError": ("msfm.errors", "NotRegisteredError"),
+    "AlreadyRegisteredError": ("msfm.errors", "AlreadyRegisteredError"),
+    "FeatureSet": ("msfm.features", "FeatureSet"),
+    "FeatureStore": ("msfm.features", "FeatureStore"),
+    "FeatureRef": ("msfm.model", "FeatureRef"),
+    "Camera": ("msfm.model", "Camera"),
+    "Point3D": ("msfm.model", "Point3D"),
+    "Model": ("msfm.model", "Model"),
+    "Match": ("msfm.matching", "Match"),
+    "Edge": ("msfm.matching", "Edge"),
+    "MatchGraph": ("msfm.matching", "MatchGraph"),
+    "TwoViewGeometry": ("msfm.geometry", "TwoViewGeometry"),
+    "EpipolarLine": ("msfm.geometry", "EpipolarLine"),
+    "Triangulated": ("msfm.geometry", "Triangulated"),
+    "SearchStats": ("msfm.descriptors", "SearchStats"),
+    "LocalizationResult": ("msfm.localize", "LocalizationResult"),
+    "SetCover": ("msfm.localize", "SetCover"),
+}
+_LOCAL_CLASSES: dict = {}
+REFERENCE_TYPES = False
+
+
+def reference_available() -> bool:
+    import importlib.util
+
+    try:
+        return importlib.util.find_spec("msfm") is not None
+    except (ImportError, ValueError):
+        return False
+
+
+def adopt_reference_types() -> bool:
+    """Rebind the package's value types and errors to ``msfm``'s classes (idempotent).
+    Returns True when the reference classes are in use."""
+    global REFERENCE_TYPES, DeviceUnavailableError
+    import importlib
+    import sys
+
+    if REFERENCE_TYPES:
+        return True
+    if not reference_available():
+        return False
+    g = globals()
+    local = {}
+    ref = {}
+    for name, (mod, attr) in _REFERENCE_CLASSES.items():
+        try:
+            cls = getattr(importlib.import_module(mod), attr)
+        except (ImportError, AttributeError):
+            continue
+        ref[name] = cls
+    if "MsfmError" not in ref:
+        return False
+    for name in ref:
+        if name in g:
+            local[name] = g[name]
+    # the device error keeps its name but joins the reference hierarchy
+    old_dev = DeviceUnavailableError
+    DeviceUnavailableError = type("DeviceUnavailableError", (ref["MsfmError"], RuntimeError),
+                                  {"__doc__": old_dev.__doc__, "__module__": __name__})
+    local["DeviceUnavailableError"] = old_dev
+    ref["DeviceUnavailableError"] = DeviceUnavailableError
+    pkg = __name__.rsplit(".", 1)[0]
+    for mname, m in list(sys.modules.items()):
+        if m is None or not (mname == pkg or mname.startswith(pkg + ".")):
+            continue
+        d = vars(m)
+        for key, val in list(d.items()):
+            for name, old in local.items():
+                if val is old and name in ref:
+                    d[key] = ref[name]
+    _LOCAL_CLASSES.update(local)
+    REFERENCE_TYPES = True
+    return True

@@ -162,7 +162,58 @@ def ranked_cases():
     print("ranked", {q: len(out[f"r{q}_corr"]) for q in (9, 10, 11)}, "copy", len(corr))
 
 
+def setcover_cases():
+    """compute_set_cover (localize.py:62-96) on seeded models, several k, and the
+    forced set-cover path of localize_all (test_localize.py:289-295) on the
+    hold-out recipe."""
+    import copy
+
+    from msfm.localize import compute_set_cover, localize_all
+    from msfm.matching import MatchGraph
+
+    out = {}
+    cases = [dict(n_cameras=4, n_points=30, seed=13), dict(n_cameras=8, n_points=200, seed=7),
+             dict(n_cameras=12, n_points=700, visibility_fraction=0.7, seed=77),
+             dict(n_cameras=30, n_points=2500, visibility_fraction=0.6, seed=5)]
+    ks = [1, 3, 5, 40, 10_000]
+    for c, kw in enumerate(cases):
+        scene = generate_scene(SceneSpec(**kw))
+        model = partial_model(scene, range(kw["n_cameras"]))
+        out[f"c{c}_spec"] = np.array(repr(kw))
+        for k in ks:
+            cov = compute_set_cover(model, k)
+            out[f"c{c}_k{k}_selected"] = np.array(cov.selected, np.int64)
+            out[f"c{c}_k{k}_coverage"] = np.array(list(cov.coverage.items()), np.int64).reshape(-1, 2)
+    out["n_cases"] = np.array(len(cases))
+    out["ks"] = np.array(ks)
+    kw = dict(n_cameras=12, n_points=700, visibility_fraction=0.7, pixel_noise=0.3,
+              descriptor_noise=3.0, seed=77)
+    scene = generate_scene(SceneSpec(**kw))
+    store = scene.store()
+    model = copy.deepcopy(partial_model(scene, range(9)))
+    K = {i: scene.cameras[i].K for i in store.sets}
+    cover = compute_set_cover(model, 40).selected
+    newly, results = localize_all(model, store, MatchGraph(), K, force_set_cover=True,
+                                  set_cover_k=40)
+    out["forced_spec"] = np.array(repr(kw))
+    out["forced_cover"] = np.array(cover, np.int64)
+    out["forced_newly"] = np.array(newly, np.int64)
+    for r in results:
+        q = r.image_id
+        out[f"forced_q{q}_corr"] = np.array(r.correspondences, np.int32).reshape(-1, 2)
+        out[f"forced_q{q}_method"] = np.array(r.method)
+        if r.pose is not None:
+            out[f"forced_q{q}_R"], out[f"forced_q{q}_t"] = r.pose.R, r.pose.t
+            out[f"forced_q{q}_inliers"] = np.array(r.inliers)
+    np.savez_compressed(os.path.join(HERE, "setcover.npz"), **out)
+    print("setcover", {k: len(out[f"c3_k{k}_selected"]) for k in ks}, "forced newly", newly,
+          "cover", len(cover))
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["setcover"]:
+        setcover_cases()
+        sys.exit(0)
     if sys.argv[1:] == ["ranked"]:
         ranked_cases()
         sys.exit(0)

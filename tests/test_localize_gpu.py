@@ -202,3 +202,34 @@ def test_staged_knn_equals_resident_knn():
         torch.cuda.synchronize()
         for name in ("k1", "i1", "k2"):
             assert torch.equal(getattr(got, name)[:, :300], getattr(want, name)[:, :300]), (groups, name)
+
+
+def test_localize_all_forced_set_cover_equals_reference():
+    """localize_all(force_set_cover=True, set_cover_k=40) (test_localize.py:289-295):
+    the cover, correspondences, poses and newly registered images equal the
+    reference run recorded in setcover.npz."""
+    import os
+
+    from golden_io import GOLDEN
+    from paper_1512_06235_b200 import scenes
+    from paper_1512_06235_b200.localize import compute_set_cover, localize_all
+    from paper_1512_06235_b200.synth import SceneSpec, generate_scene
+
+    z = np.load(os.path.join(GOLDEN, "setcover.npz"))
+    scene = generate_scene(SceneSpec(**eval(str(z["forced_spec"]))))
+    snap = scenes.coarse_snapshot(scene, range(9), eta=None)
+    model = scenes.snapshot_to_model(scene, snap)
+    store = scene.store()
+    K = {i: scene.cameras[i].K for i in store.sets}
+    assert compute_set_cover(model, 40).selected == z["forced_cover"].tolist()
+    newly, results = localize_all(model, store, _NoGraph(), K, force_set_cover=True,
+                                  set_cover_k=40)
+    assert newly == z["forced_newly"].tolist()
+    for r in results:
+        q = r.image_id
+        assert [tuple(c) for c in z[f"forced_q{q}_corr"].tolist()] == r.correspondences
+        assert r.method == str(z[f"forced_q{q}_method"])
+        if f"forced_q{q}_R" in z:
+            np.testing.assert_allclose(r.pose.R, z[f"forced_q{q}_R"], atol=1e-6)
+            np.testing.assert_allclose(r.pose.t, z[f"forced_q{q}_t"], atol=1e-6, rtol=1e-6)
+            assert r.inliers == int(z[f"forced_q{q}_inliers"])

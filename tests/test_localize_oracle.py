@@ -1,5 +1,7 @@
 """The localization oracle is pinned to the reference's outputs."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -64,3 +66,60 @@ def test_pnp_oracle_on_localization_fixtures():
             R, t, mask = ol.pnp_ransac(X, uv, K, seed=q)
             np.testing.assert_array_equal(mask, z[f"q{q}_mask"])
             np.testing.assert_allclose(R, z[f"q{q}_R"], atol=1e-12)
+
+
+# ---------------------------------------------------------------- set cover --
+# compute_set_cover (localize.py:62-96) against the reference's own selections
+# (tests/golden/setcover.npz, make_golden_localize.py setcover) and the
+# properties the reference's tests assert (test_localize.py:97-125).
+
+def _setcover_model(spec_repr):
+    from paper_1512_06235_b200 import scenes
+    from paper_1512_06235_b200.synth import SceneSpec, generate_scene
+
+    kw = eval(str(spec_repr))
+    scene = generate_scene(SceneSpec(**kw))
+    snap = scenes.coarse_snapshot(scene, range(kw["n_cameras"]), eta=None)
+    return scenes.snapshot_to_model(scene, snap)
+
+
+def test_set_cover_equals_reference_golden():
+    from paper_1512_06235_b200.localize import compute_set_cover
+
+    z = np.load(os.path.join(GOLDEN, "setcover.npz"))
+    for c in range(int(z["n_cases"])):
+        model = _setcover_model(z[f"c{c}_spec"])
+        for k in z["ks"]:
+            cov = compute_set_cover(model, int(k))
+            assert cov.selected == z[f"c{c}_k{k}_selected"].tolist()
+            want = [tuple(r) for r in z[f"c{c}_k{k}_coverage"].tolist()]
+            assert list(cov.coverage.items()) == want
+
+
+def test_set_cover_properties():
+    """test_localize.py:97-125: feasible coverage, saturation, compression, minimality."""
+    from paper_1512_06235_b200.localize import compute_set_cover
+
+    z = np.load(os.path.join(GOLDEN, "setcover.npz"))
+    model = _setcover_model(z["c2_spec"])
+    vis = {i: sum(1 for p in model.points.values() if i in p.track) for i in model.cameras}
+    k = 5
+    cov = compute_set_cover(model, k)
+    assert all(cov.coverage[i] >= min(k, vis[i]) for i in model.cameras)
+    sat = compute_set_cover(_setcover_model(z["c0_spec"]), 10_000)
+    m0 = _setcover_model(z["c0_spec"])
+    assert sorted(sat.selected) == sorted(m0.points)
+    assert len(compute_set_cover(model, 2).selected) <= 0.5 * len(model.points)
+    k = 4
+    cov = compute_set_cover(model, k)
+    sel = set(cov.selected)
+    for pid in cov.selected[:20]:
+        rest = sel - {pid}
+        broken = False
+        for i in model.points[pid].track:
+            if vis.get(i, 0) >= k:
+                have = sum(1 for q in rest if i in model.points[q].track)
+                broken |= have < k
+        assert broken
+    with pytest.raises(ValueError):
+        compute_set_cover(model, 0)
