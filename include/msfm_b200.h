@@ -285,6 +285,15 @@ int msfm_knn2_second_index(const msfm_bank* bank, int32_t n_points, const int32_
                            const int32_t* d_k1, const int32_t* d_i1, const int32_t* d_k2,
                            int32_t* d_i2, void* stream);
 
+/* Real-valued 2-NN for float descriptor rows that are not integer-valued
+ * (two_nearest_bruteforce descriptors.py:35-72 / DescriptorIndex.knn2
+ * descriptors.py:123-139 with arbitrary float32 input): squared L2 as
+ * sum((q-t)^2) in f64 (differences and squares exact for f32 inputs), top-2 per
+ * query with the lowest target index winning ties.  d_d2 [n_queries][2] f64,
+ * d_idx [n_queries][2] int64; (inf, -1) where fewer than 2 targets exist. */
+int msfm_knn2_float(const float* d_q, int64_t n_queries, const float* d_t, int64_t n_targets,
+                    int32_t dim, double* d_d2, int64_t* d_idx, void* stream);
+
 /* direct_3d2d_search post-processing (localize.py:108-122 + ratio_filter
  * matching.py:82-103) on the knn2 output: ratio test sqrt(N_b/N_s) < p/q
  * evaluated exactly (q^2 N_b < p^2 N_s), single-feature images: sqrt(N_b)/n <

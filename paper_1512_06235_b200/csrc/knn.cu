@@ -768,3 +768,70 @@ extern "C" int msfm_knn2_tracks(const msfm_bank* bank, int32_t n_points, const i
     count_launches(3);
     return MSFM_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Real-valued 2-NN (two_nearest_bruteforce, descriptors.py:35-72, for float rows
+// that are not integer-valued): one warp per query, lanes stride over the
+// targets, squared distance as sum((q_i - t_i)^2) in f64 (each difference and
+// square exact for f32 inputs), top-2 with the lowest target index winning ties.
+namespace msfm {
+namespace knnf {
+__device__ __forceinline__ bool dless(double a, int64_t ia, double b, int64_t ib) {
+    return a < b || (a == b && ia < ib);
+}
+
+__global__ void __launch_bounds__(256) knn_float_kernel(const float* __restrict__ q,
+                                                        const float* __restrict__ t, int64_t nq,
+                                                        int64_t nt, int dim, double* __restrict__ d2,
+                                                        int64_t* __restrict__ idx) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= nq) return;
+    const float* qr = q + w * dim;
+    double b1 = INFINITY, b2 = INFINITY;
+    int64_t i1 = -1, i2 = -1;
+    for (int64_t j = lane; j < nt; j += 32) {
+        const float* tr = t + j * dim;
+        double s = 0.0;
+        for (int k = 0; k < dim; k++) {
+            const double e = (double)__ldg(qr + k) - (double)__ldg(tr + k);
+            s = fma(e, e, s);
+        }
+        if (dless(s, j, b1, i1)) { b2 = b1; i2 = i1; b1 = s; i1 = j; }
+        else if (dless(s, j, b2, i2)) { b2 = s; i2 = j; }
+    }
+    for (int o = 16; o; o >>= 1) {
+        const double c1 = __shfl_xor_sync(0xffffffffu, b1, o), c2 = __shfl_xor_sync(0xffffffffu, b2, o);
+        const int64_t j1 = __shfl_xor_sync(0xffffffffu, i1, o), j2 = __shfl_xor_sync(0xffffffffu, i2, o);
+        // merge two sorted pairs (b1 <= b2, c1 <= c2) into the smallest two
+        if (dless(c1, j1, b1, i1)) {
+            const double nb2 = dless(b1, i1, c2, j2) ? b1 : c2;
+            const int64_t ni2 = dless(b1, i1, c2, j2) ? i1 : j2;
+            b1 = c1; i1 = j1; b2 = nb2; i2 = ni2;
+        } else if (dless(c1, j1, b2, i2)) {
+            b2 = c1; i2 = j1;
+        }
+    }
+    if (lane == 0) {
+        d2[2 * w] = b1; d2[2 * w + 1] = b2;
+        idx[2 * w] = i1; idx[2 * w + 1] = i2;
+    }
+}
+}  // namespace knnf
+}  // namespace msfm
+
+extern "C" int msfm_knn2_float(const float* d_q, int64_t n_queries, const float* d_t,
+                               int64_t n_targets, int32_t dim, double* d_d2, int64_t* d_idx,
+                               void* stream) {
+    if (n_queries < 0 || n_targets < 0 || dim <= 0) {
+        set_error("msfm_knn2_float: bad arguments");
+        return MSFM_EINVAL;
+    }
+    if (n_queries == 0) return MSFM_OK;
+    const int64_t threads = n_queries * 32;
+    msfm::knnf::knn_float_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        d_q, d_t, n_queries, n_targets, dim, d_d2, d_idx);
+    MSFM_LAUNCH_CHECK();
+    count_launches(1);
+    return MSFM_OK;
+}

@@ -50,6 +50,15 @@ _ROUTES = [
     ("msfm.localize", "DescriptorIndex", "descriptors", "DescriptorIndex"),
     # .msft staging (features.py:98-130); FeatureStore.load_dir calls it by name
     ("msfm.features", "load_features", "staging", "load_features"),
+    # reconstruct.py binds triangulate_track (geometry.py:276) at import
+    ("msfm.reconstruct", "triangulate_track", "triangulation", "triangulate_track"),
+    # the CLI binds the stage entry points at import (cli.py:20-32): its localize,
+    # densify and bench-guided commands run the B200 path too
+    ("msfm.cli", "guided_match_pair", "guided", "guided_match_pair"),
+    ("msfm.cli", "localize_all", "localize", "localize_all"),
+    ("msfm.cli", "densify_stage", "densify", "densify_stage"),
+    ("msfm.cli", "build_coarse_matchgraph", "coarse", "build_coarse_matchgraph"),
+    ("msfm.cli", "load_features", "staging", "load_features"),
 ]
 
 _SAVED: dict = {}
@@ -57,7 +66,13 @@ _SAVED: dict = {}
 
 def install() -> list:
     """Patch the reference modules; returns the "module.attr" names replaced.
-    Names a reference version lacks are skipped (and not returned)."""
+    Names a reference version lacks are skipped (and not returned).  The package's
+    value types and errors become the reference's own classes first
+    (types.adopt_reference_types), so drop-ins raise msfm.errors.* and return
+    msfm.matching.Match / msfm.model.FeatureRef objects."""
+    from .types import adopt_reference_types
+
+    adopt_reference_types()
     done = []
     for mod, attr, ours, our_attr in _ROUTES:
         m = importlib.import_module(mod)

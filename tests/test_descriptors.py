@@ -34,13 +34,43 @@ def test_fixture_has_ties():
     assert (srt[:, 0] == srt[:, 1]).mean() > 0.2 and (srt[:, 1] == srt[:, 2]).mean() > 0.3
 
 
-def test_non_integer_queries_rejected():
+def test_non_integer_rows_take_the_real_valued_path():
     from paper_1512_06235_b200.descriptors import _as_u8
-    with pytest.raises(ValueError):
-        _as_u8(np.full((2, 128), 0.5, np.float32), "queries")
-    with pytest.raises(ValueError):
-        _as_u8(np.full((2, 128), 256.0, np.float32), "queries")
-    assert _as_u8(np.zeros((0, 128)), "q").shape == (0, 128)
+    assert _as_u8(np.full((2, 128), 0.5, np.float32)) is None
+    assert _as_u8(np.full((2, 128), 256.0, np.float32)) is None
+    assert _as_u8(np.full((2, 64), 3.0, np.float32)) is None
+    assert _as_u8(np.zeros((0, 128))).shape == (0, 128)
+    assert _as_u8(np.full((3, 128), 7.0)).dtype == np.uint8
+
+
+@pytest.mark.gpu
+def test_float_rows_equal_f64_brute_force():
+    """Arbitrary float32 rows (test_matching.py:54-71 style: normal draws, noisy
+    integers, exact duplicates for ties, a single target): indices equal a numpy
+    f64 brute force with lowest-index ties; distances its sqrt."""
+    from paper_1512_06235_b200.descriptors import DescriptorIndex, two_nearest_bruteforce
+
+    rng = np.random.default_rng(11)
+    t = rng.normal(size=(700, 128)).astype(np.float32)
+    t[5] = t[3]                                  # a tie at the same distance
+    q = rng.normal(size=(60, 128)).astype(np.float32)
+    q[0] = t[3]
+    for qq, tt in [(q, t), (t[:50] + rng.normal(0, 4, (50, 128)).astype(np.float32), t),
+                   (q[:5], t[:1])]:
+        d, i = two_nearest_bruteforce(qq, tt)
+        D = ((qq[:, None, :].astype(np.float64) - tt[None, :, :].astype(np.float64)) ** 2).sum(-1)
+        o = np.argsort(D, axis=1, kind="stable")
+        assert (i[:, 0] == o[:, 0]).all()
+        if len(tt) > 1:
+            assert (i[:, 1] == o[:, 1]).all()
+            np.testing.assert_allclose(d[:, 1], np.sqrt(D[np.arange(len(qq)), o[:, 1]]), rtol=1e-12)
+        else:
+            assert (i[:, 1] == -1).all() and np.isinf(d[:, 1]).all()
+        np.testing.assert_allclose(d[:, 0], np.sqrt(D[np.arange(len(qq)), o[:, 0]]), rtol=1e-12)
+    assert two_nearest_bruteforce(q, t)[1][0, 0] == 3
+    idx = DescriptorIndex(t, exact_threshold=100, leaf_size=4, max_leaf_visits=4)
+    assert not idx.exact                          # the reference would take its kd-tree here
+    np.testing.assert_array_equal(idx.knn2(q)[1], two_nearest_bruteforce(q, t)[1])
 
 
 @pytest.mark.gpu
