@@ -257,6 +257,13 @@ struct alignas(16) SGRec {
     long long toffb, dbase;                // first bucket of the strip table, dedupe base
 };
 
+// Per group, the view the match kernel bulk-copies: rep line (fp32), member-band
+// reach, first member position (sg_prep_kernel).
+struct alignas(16) GView {
+    float a, b, c, reach;
+    int moff, pad0, pad1, pad2;
+};
+
 #ifndef MSFM_SG_NT
 #define MSFM_SG_NT 2
 #endif
@@ -309,6 +316,7 @@ struct ChunkArgs {
     unsigned long long* sgdev;   // per super-group: max member-band deviation (f64 bits)
     float4* gl4;                 // per dense group: rep line (fp32) + member-band reach
     int32_t* gmoff;              // per dense group: first member position
+    GView* gview;                // per dense group: the two above as one 32-B record
     unsigned long long* mstate;  // per member slot: best (d2<<32 | tid)
     unsigned* mstate2;           // per member slot: second d2
     int32_t* res_tid; float* res_dist; float* res_ratio;
@@ -883,6 +891,11 @@ __global__ void __launch_bounds__(128) sg_prep_kernel(ChunkArgs a, int max_sg) {
         a.gl4[g] = (G.K < 0 && a.strategy != 1) ? make_float4(0.f, 0.f, 1e30f, -1.f)
                            : make_float4(G.ar, G.br, G.cr, (float)a.d + G.maxdev + 0.05f);
         a.gmoff[g] = G.moff;
+        const float4 v = a.gl4[g];
+        GView gv;
+        gv.a = v.x; gv.b = v.y; gv.c = v.z; gv.reach = v.w;
+        gv.moff = G.moff; gv.pad0 = gv.pad1 = gv.pad2 = 0;
+        a.gview[g] = gv;
     }
     o.ar = (float)r[0]; o.br = (float)r[1]; o.cr = (float)r[2]; o.R = (float)R;
     // sure-in-C' radius around the base line: grid, the 3x3 subcell block of the
@@ -1533,6 +1546,8 @@ __global__ void __launch_bounds__(WARPS * 32, MATCH_MINB) match_kernel(ChunkArgs
     }
 }
 
+#include "guided_match.cuh"
+
 __global__ void __launch_bounds__(256) compact_kernel(ChunkArgs a) {
     __shared__ int sm[256 / 32 + 1];
     const int p = blockIdx.x, pg = a.p0 + p;
@@ -1634,6 +1649,7 @@ size_t chunk_bytes(const ChunkSizes& c) {
     b += aligned_bytes<unsigned>(c.Q);                 // gfit
     b += aligned_bytes<unsigned long long>(c.Q);       // sgdev
     b += aligned_bytes<float4>(c.Q) + aligned_bytes<int32_t>(c.Q);   // gl4, gmoff
+    b += aligned_bytes<GView>(c.Q);                    // gview
     b += aligned_bytes<double>(3 * c.Q);               // q_line
     b += aligned_bytes<int4>(c.Q);                     // grec
     b += aligned_bytes<int32_t>(c.Q) * 2;              // gfill, members
@@ -1932,6 +1948,7 @@ static int guided_match_impl(const msfm_bank* bank, const msfm_grids* grids, int
     a.mgid = ar.take<int32_t>(w.Q); a.msg = ar.take<int32_t>(w.Q);
     a.gfit = ar.take<unsigned>(w.Q); a.sgdev = ar.take<unsigned long long>(w.Q);
     a.gl4 = ar.take<float4>(w.Q); a.gmoff = ar.take<int32_t>(w.Q);
+    a.gview = ar.take<GView>(w.Q);
     a.tab_off = ar.take<int64_t>(w.P + 1); a.tbase = ar.take<int64_t>(w.P + 1);
     a.ngroups = ar.take<int32_t>(w.P + 1); a.gstart = ar.take<int32_t>(w.P + 1);
     a.nmem = ar.take<int32_t>(w.P + 1); a.sgstart = ar.take<int32_t>(w.P + 1);
@@ -1959,6 +1976,13 @@ static int guided_match_impl(const msfm_bank* bank, const msfm_grids* grids, int
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     MSFM_CUDA_TRY(cudaFuncSetAttribute(groups_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        2 * 65536 + 16));
+    // MSFM_MATCH_V1=1 selects the round-1 kernel (A/B comparisons)
+    const bool use_v1 = getenv("MSFM_MATCH_V1") && atoi(getenv("MSFM_MATCH_V1")) != 0;
+    const size_t ms_smem = sizeof(MSmem) * MS_WARPS;
+    MSFM_CUDA_TRY(cudaFuncSetAttribute(match_ms_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ms_smem));
+    MSFM_CUDA_TRY(cudaFuncSetAttribute(match_ms_kernel<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ms_smem));
     int next_range = 0;
     for (size_t c = 0; c + 1 < bounds.size(); c++) {
         const int p0 = bounds[c], p1 = bounds[c + 1];
@@ -2010,10 +2034,14 @@ static int guided_match_impl(const msfm_bank* bank, const msfm_grids* grids, int
             { ProfScope ps("member_kernel", st); member_kernel<<<nb, 128, 0, st>>>(a, (int)Q); }
             { ProfScope ps("sg_prep_kernel", st); sg_prep_kernel<<<nb, 128, 0, st>>>(a, (int)Q); }
         }
-        {
+        if (use_v1) {
             ProfScope ps("match_kernel", st);
             if (d_stats) match_kernel<true><<<nsm * MATCH_MINB, WARPS * 32, 0, st>>>(a);
             else         match_kernel<false><<<nsm * MATCH_MINB, WARPS * 32, 0, st>>>(a);
+        } else {
+            ProfScope ps("match_kernel", st);
+            if (d_stats) match_ms_kernel<true><<<nsm * MS_MINB, MS_WARPS * 32, ms_smem, st>>>(a);
+            else         match_ms_kernel<false><<<nsm * MS_MINB, MS_WARPS * 32, ms_smem, st>>>(a);
         }
         { ProfScope ps("compact_kernel", st); compact_kernel<<<a.npairs, 256, 0, st>>>(a); }
         MSFM_LAUNCH_CHECK();
