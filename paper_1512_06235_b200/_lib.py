@@ -12,7 +12,8 @@ import os
 from .types import DeviceUnavailableError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmsfm_b200.so")
+# MSFM_B200_LIB: an alternative in-tree build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("MSFM_B200_LIB") or os.path.join(_HERE, "libmsfm_b200.so")
 
 c_int32_p = ctypes.POINTER(ctypes.c_int32)
 VP = ctypes.c_void_p

@@ -24,11 +24,14 @@
 
 constexpr int MS_WARPS = 4;            // warps per CTA
 #ifndef MSFM_MS_MINB
-#define MSFM_MS_MINB 5
+#define MSFM_MS_MINB 4
 #endif
 constexpr int MS_MINB = MSFM_MS_MINB;  // resident CTAs per SM
 constexpr int MS_CAP = 192;            // candidates per round (local index < 256)
 constexpr int KEY_NONE = 0x7fffffff;
+#ifndef MSFM_PF3
+#define MSFM_PF3 0
+#endif
 
 struct alignas(16) MSlot {
     SGRec sg;                  // 128 B
@@ -48,7 +51,7 @@ struct alignas(16) MSmem {
     unsigned short cid[MS_CAP];    // target-local feature id
     unsigned short ulist[MS_CAP];  // candidates whose C' bits are still to be decided
     unsigned anyb[MS_CAP / 32];    // stats: candidate inside some member band
-    uint64_t bar_q, bar_rec[2], bar_desc[2];
+    uint64_t bar_q, bar_rec[2];
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -96,13 +99,22 @@ __device__ __forceinline__ void ms_issue_rec(const ChunkArgs& a, MSlot& L, uint6
     if (ng) ms_bulk(L.gv, a.gview + SG.g0, ng * sizeof(GView), bar);
 }
 
-// descriptor rows of the slot's first 16 members (lanes < 16 issue one 128-B copy each)
-__device__ __forceinline__ void ms_issue_desc(const ChunkArgs& a, MSlot& L, uint64_t* bar) {
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+// descriptor rows of the slot's first 16 members: 128 16-B cp.async, 4 per lane
+// (completion: cp.async.wait_all before the SG starts)
+__device__ __forceinline__ void ms_issue_desc(const ChunkArgs& a, MSlot& L) {
     const int lane = threadIdx.x & 31;
     const int nm = min(L.sg.mcnt, 16);
-    if (lane == 0) ms_expect(bar, (uint32_t)(nm * 128));
-    __syncwarp();
-    if (lane < nm) ms_bulk(L.desc[lane], a.desc + (L.sg.qoff + L.mr[lane].fid) * 128, 128, bar);
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const int k = lane + 32 * q, j = k >> 3, part = k & 7;
+        if (j < nm) cp_async16(L.desc[j] + 16 * part, a.desc + (L.sg.qoff + L.mr[j].fid) * 128 + 16 * part);
+    }
 }
 
 __device__ __forceinline__ void ms_top2(int key, int& b1, int& b2) {
@@ -112,21 +124,21 @@ __device__ __forceinline__ void ms_top2(int key, int& b1, int& b2) {
 }
 
 // the reference's float64 band decision for one (member, candidate) element
-__device__ __forceinline__ bool ms_band_exact(const ChunkArgs& a, const SGRec& SG, const MemberRec& M,
-                                              float x, float y) {
-    const GroupRec& G = a.grp[SG.g0 + (int)((unsigned)M.slotgi >> SLOT_BITS)];
-    if (G.cnt == 1) return band_exact(G.sl0, G.sl1, G.sl2, true, x, y, a.d);
-    const double* L = a.q_line + 3 * (int64_t)(M.slotgi & SLOT_MASK);
-    return band_exact(L[0], L[1], L[2], false, x, y, a.d);
+__device__ __noinline__ bool ms_band_exact(const GroupRec* grp, const double* q_line, double d,
+                                           int g0, int slotgi, float x, float y) {
+    const GroupRec& G = grp[g0 + (int)((unsigned)slotgi >> SLOT_BITS)];
+    if (G.cnt == 1) return band_exact(G.sl0, G.sl1, G.sl2, true, x, y, d);
+    const double* L = q_line + 3 * (int64_t)(slotgi & SLOT_MASK);
+    return band_exact(L[0], L[1], L[2], false, x, y, d);
 }
 
-// fp32 prefilter, then the exact value near the edge (member_band of the v1 kernel)
+// fp32 prefilter, then the exact value near the edge
 __device__ __forceinline__ bool ms_member_band(const ChunkArgs& a, const SGRec& SG, const MemberRec& M,
                                                float x, float y) {
     const float v = fabsf(fmaf(M.a, x, fmaf(M.b, y, M.c)));
     if (v <= M.lo) return true;
     if (v > M.hi) return false;
-    return ms_band_exact(a, SG, M, x, y);
+    return ms_band_exact(a.grp, a.q_line, a.d, SG.g0, M.slotgi, x, y);
 }
 
 // C' membership of candidate (x, y, f) for group G (in_cprime of the v1 kernel)
@@ -135,16 +147,250 @@ __device__ __forceinline__ bool ms_in_cprime(const ChunkArgs& a, const GroupRec&
     return in_cprime(a, G, S, fx, fy, S.toff, f);
 }
 
+__device__ __forceinline__ MemberRec ms_member(const ChunkArgs& a, const MSlot& L, int j) {
+    return j < 16 ? L.mr[j] : a.mrec[L.sg.m0 + j];
+}
+
+// per-lane state of one member block: rows g, g+8 (band constants, descriptor
+// fragments in mma order, running top-2 keys)
+struct MsRows {
+    float ma0, mb0, mc0, lo0, hi0, ma1, mb1, mc1, lo1, hi1;
+    unsigned gb0, gb1;
+    unsigned af[4][4];
+    int k1a, k2a, k1b, k2b;
+};
+
+__device__ __forceinline__ void ms_ldB(const MSmem& S, const uint4* tdesc, int nt, int g, uint4& u0,
+                                       uint4& u1) {
+    const int f = S.cid[8 * nt + g];
+    u0 = __ldg(tdesc + 8 * f);
+    u1 = __ldg(tdesc + 8 * f + 1);
+}
+
+// one n8 tile: 4 mma k-steps, then the 4 elements of this lane
+__device__ __forceinline__ uint4 lds128v(const void* p) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(su32(p)));
+    return v;
+}
+
+template <bool CB, bool STATS, bool SLOTA>
+__device__ __forceinline__ void ms_tile(const ChunkArgs& a, MSmem& S, const MSlot& L, MsRows& R,
+                                        int mb0, int nt, const uint4& u0, const uint4& u1) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    int acc[4] = {0, 0, 0, 0};
+    if (SLOTA) {
+        const uint4* qd = reinterpret_cast<const uint4*>(&L.desc[0][0]) + lane;
+        uint4 q = lds128v(qd);
+        mma_u8(acc, q.x, q.y, q.z, q.w, u0.x, u0.y);
+        q = lds128v(qd + 32);
+        mma_u8(acc, q.x, q.y, q.z, q.w, u0.z, u0.w);
+        q = lds128v(qd + 64);
+        mma_u8(acc, q.x, q.y, q.z, q.w, u1.x, u1.y);
+        q = lds128v(qd + 96);
+        mma_u8(acc, q.x, q.y, q.z, q.w, u1.z, u1.w);
+    } else {
+        mma_u8(acc, R.af[0][0], R.af[0][1], R.af[0][2], R.af[0][3], u0.x, u0.y);
+        mma_u8(acc, R.af[1][0], R.af[1][1], R.af[1][2], R.af[1][3], u0.z, u0.w);
+        mma_u8(acc, R.af[2][0], R.af[2][1], R.af[2][2], R.af[2][3], u1.x, u1.y);
+        mma_u8(acc, R.af[3][0], R.af[3][1], R.af[3][2], R.af[3][3], u1.z, u1.w);
+    }
+    const int4 c0 = S.cand[8 * nt + 2 * t], c1 = S.cand[8 * nt + 2 * t + 1];
+    const float x0 = __int_as_float(c0.x), y0 = __int_as_float(c0.y);
+    const float x1 = __int_as_float(c1.x), y1 = __int_as_float(c1.y);
+    // elements: e0 (g, 2t), e1 (g, 2t+1), e2 (g+8, 2t), e3 (g+8, 2t+1)
+    const float v0 = fabsf(fmaf(R.ma0, x0, fmaf(R.mb0, y0, R.mc0)));
+    const float v1 = fabsf(fmaf(R.ma0, x1, fmaf(R.mb0, y1, R.mc0)));
+    const float v2 = fabsf(fmaf(R.ma1, x0, fmaf(R.mb1, y0, R.mc1)));
+    const float v3 = fabsf(fmaf(R.ma1, x1, fmaf(R.mb1, y1, R.mc1)));
+    bool i0 = v0 <= R.lo0, i1 = v1 <= R.lo0, i2 = v2 <= R.lo1, i3 = v3 <= R.lo1;
+    const bool edge = (v0 > R.lo0 && v0 <= R.hi0) || (v1 > R.lo0 && v1 <= R.hi0) ||
+                      (v2 > R.lo1 && v2 <= R.hi1) || (v3 > R.lo1 && v3 <= R.hi1);
+    if (CB) {
+        i0 = i0 && ((unsigned)c0.w & R.gb0); i1 = i1 && ((unsigned)c1.w & R.gb0);
+        i2 = i2 && ((unsigned)c0.w & R.gb1); i3 = i3 && ((unsigned)c1.w & R.gb1);
+    }
+    ms_top2(i0 ? c0.z - acc[0] * 512 : KEY_NONE, R.k1a, R.k2a);
+    ms_top2(i1 ? c1.z - acc[1] * 512 : KEY_NONE, R.k1a, R.k2a);
+    ms_top2(i2 ? c0.z - acc[2] * 512 : KEY_NONE, R.k1b, R.k2b);
+    ms_top2(i3 ? c1.z - acc[3] * 512 : KEY_NONE, R.k1b, R.k2b);
+    bool any0 = false, any1 = false;
+    if (STATS) { any0 = i0 || i2; any1 = i1 || i3; }
+    if (__any_sync(FULL, edge)) {
+        // within eps of the band edge: the reference's fp64 band value decides
+#pragma unroll 1
+        for (int e = 0; e < 4; e++) {
+            const float v = e == 0 ? v0 : e == 1 ? v1 : e == 2 ? v2 : v3;
+            const float lo = e < 2 ? R.lo0 : R.lo1, hi = e < 2 ? R.hi0 : R.hi1;
+            if (!(v > lo && v <= hi)) continue;
+            const int4 c = (e & 1) ? c1 : c0;
+            if (CB && !((unsigned)c.w & (e < 2 ? R.gb0 : R.gb1))) continue;
+            const MemberRec M = ms_member(a, L, mb0 + g + 8 * (e >> 1));
+            if (!ms_band_exact(a.grp, a.q_line, a.d, L.sg.g0, M.slotgi, __int_as_float(c.x),
+                               __int_as_float(c.y)))
+                continue;
+            const int av = e == 0 ? acc[0] : e == 1 ? acc[1] : e == 2 ? acc[2] : acc[3];
+            if (e < 2) ms_top2(c.z - av * 512, R.k1a, R.k2a);
+            else       ms_top2(c.z - av * 512, R.k1b, R.k2b);
+            if (STATS) { if (e & 1) any1 = true; else any0 = true; }
+        }
+    }
+    if (STATS) {
+        const unsigned b0 = __ballot_sync(FULL, any0), b1 = __ballot_sync(FULL, any1);
+        if (lane == 0) {
+            unsigned bits = 0;
+#pragma unroll
+            for (int tt = 0; tt < 4; tt++) {
+                if (b0 & (0x11111111u << tt)) bits |= 1u << (2 * tt);
+                if (b1 & (0x11111111u << tt)) bits |= 1u << (2 * tt + 1);
+            }
+            S.anyb[(8 * nt) >> 5] |= bits << ((8 * nt) & 31);
+        }
+    }
+}
+
+// One member block's tiles: lane (g, t) owns member rows g, g+8 (registers) and
+// candidate columns 2t, 2t+1 of every n8 tile.  CB: consult the candidates' C' bits.
+template <bool CB, bool STATS, bool SLOTA>
+__device__ __forceinline__ void ms_block(const ChunkArgs& a, MSmem& S, const MSlot& L, int mb0, int m,
+                                         int ntile, bool first_round) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const SGRec& SG = L.sg;
+    MsRows R;
+    R.ma0 = 0.f; R.mb0 = 0.f; R.mc0 = 1e30f; R.lo0 = -1.f; R.hi0 = -1.f;
+    R.ma1 = 0.f; R.mb1 = 0.f; R.mc1 = 1e30f; R.lo1 = -1.f; R.hi1 = -1.f;
+    R.gb0 = 0; R.gb1 = 0;
+    {
+        const int j0 = mb0 + g, j1 = mb0 + g + 8;
+        if (j0 < m) {
+            const MemberRec M = ms_member(a, L, j0);
+            R.ma0 = M.a; R.mb0 = M.b; R.mc0 = M.c; R.lo0 = M.lo; R.hi0 = M.hi;
+            R.gb0 = 1u << ((unsigned)M.slotgi >> SLOT_BITS);
+        }
+        if (j1 < m) {
+            const MemberRec M = ms_member(a, L, j1);
+            R.ma1 = M.a; R.mb1 = M.b; R.mc1 = M.c; R.lo1 = M.lo; R.hi1 = M.hi;
+            R.gb1 = 1u << ((unsigned)M.slotgi >> SLOT_BITS);
+        }
+        if (!SLOTA) {
+            // member blocks past the slot (one group of > 16 members, stats mode)
+            uint4 w00 = make_uint4(0, 0, 0, 0), w01 = w00, w10 = w00, w11 = w00;
+            if (j0 < m) {
+                const uint4* row = reinterpret_cast<const uint4*>(
+                    a.desc + (SG.qoff + ms_member(a, L, j0).fid) * 128) + 2 * t;
+                w00 = __ldg(row); w01 = __ldg(row + 1);
+            }
+            if (j1 < m) {
+                const uint4* row = reinterpret_cast<const uint4*>(
+                    a.desc + (SG.qoff + ms_member(a, L, j1).fid) * 128) + 2 * t;
+                w10 = __ldg(row); w11 = __ldg(row + 1);
+            }
+            R.af[0][0] = w00.x; R.af[0][1] = w10.x; R.af[0][2] = w00.y; R.af[0][3] = w10.y;
+            R.af[1][0] = w00.z; R.af[1][1] = w10.z; R.af[1][2] = w00.w; R.af[1][3] = w10.w;
+            R.af[2][0] = w01.x; R.af[2][1] = w11.x; R.af[2][2] = w01.y; R.af[2][3] = w11.y;
+            R.af[3][0] = w01.z; R.af[3][1] = w11.z; R.af[3][2] = w01.w; R.af[3][3] = w11.w;
+        }
+    }
+    R.k1a = KEY_NONE; R.k2a = KEY_NONE; R.k1b = KEY_NONE; R.k2b = KEY_NONE;
+    const uint4* tdesc = reinterpret_cast<const uint4*>(a.desc + SG.toff * 128) + 2 * t;
+#if MSFM_PF3
+    // candidate descriptor fragments two tiles ahead (three register buffers)
+    uint4 p0a, p0b, p1a, p1b, p2a, p2b;
+    ms_ldB(S, tdesc, 0, g, p0a, p0b);
+    if (1 < ntile) ms_ldB(S, tdesc, 1, g, p1a, p1b);
+    for (int nt = 0; nt < ntile; nt += 3) {
+        if (nt + 2 < ntile) ms_ldB(S, tdesc, nt + 2, g, p2a, p2b);
+        ms_tile<CB, STATS, SLOTA>(a, S, L, R, mb0, nt, p0a, p0b);
+        if (nt + 1 >= ntile) break;
+        if (nt + 3 < ntile) ms_ldB(S, tdesc, nt + 3, g, p0a, p0b);
+        ms_tile<CB, STATS, SLOTA>(a, S, L, R, mb0, nt + 1, p1a, p1b);
+        if (nt + 2 >= ntile) break;
+        if (nt + 4 < ntile) ms_ldB(S, tdesc, nt + 4, g, p1a, p1b);
+        ms_tile<CB, STATS, SLOTA>(a, S, L, R, mb0, nt + 2, p2a, p2b);
+    }
+#else
+    // candidate descriptor fragments one tile ahead (two register buffers)
+    uint4 p0a, p0b, p1a, p1b;
+    ms_ldB(S, tdesc, 0, g, p0a, p0b);
+    for (int nt = 0; nt < ntile; nt += 2) {
+        if (nt + 1 < ntile) ms_ldB(S, tdesc, nt + 1, g, p1a, p1b);
+        ms_tile<CB, STATS, SLOTA>(a, S, L, R, mb0, nt, p0a, p0b);
+        if (nt + 1 >= ntile) break;
+        if (nt + 2 < ntile) ms_ldB(S, tdesc, nt + 2, g, p0a, p0b);
+        ms_tile<CB, STATS, SLOTA>(a, S, L, R, mb0, nt + 1, p1a, p1b);
+    }
+#endif
+    // ---- reduce the per-lane top-2 over the 4 lanes (t) sharing a member row
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+        int o1 = __shfl_xor_sync(FULL, R.k1a, o), o2 = __shfl_xor_sync(FULL, R.k2a, o);
+        int lo = min(R.k1a, o1), hi = max(R.k1a, o1);
+        R.k1a = lo; R.k2a = min(hi, min(R.k2a, o2));
+        o1 = __shfl_xor_sync(FULL, R.k1b, o); o2 = __shfl_xor_sync(FULL, R.k2b, o);
+        lo = min(R.k1b, o1); hi = max(R.k1b, o1);
+        R.k1b = lo; R.k2b = min(hi, min(R.k2b, o2));
+    }
+    if (t == 0) {
+#pragma unroll
+        for (int r = 0; r < 2; r++) {
+            const int j = mb0 + g + 8 * r;
+            if (j >= m) continue;
+            const int k1 = r ? R.k1b : R.k1a, k2 = r ? R.k2b : R.k2a;
+            const MemberRec M = ms_member(a, L, j);
+            const int mslot = M.slotgi & SLOT_MASK;
+            const unsigned q2 = (unsigned)M.qn9 >> 9;
+            unsigned long long best = ~0ull;
+            unsigned sec = NONE;
+            if (k1 != KEY_NONE)
+                best = ((unsigned long long)(q2 + (unsigned)(k1 >> 8)) << 32) | (unsigned)S.cid[k1 & 255];
+            if (k2 != KEY_NONE) sec = q2 + (unsigned)(k2 >> 8);
+            if (!first_round) {
+                const unsigned long long ob = a.mstate[mslot];
+                const unsigned os = a.mstate2[mslot];
+                const unsigned bd = (unsigned)(best >> 32), od = (unsigned)(ob >> 32);
+                const unsigned nh = max(bd, od);
+                const unsigned long long nbest = (bd < od) ? best : ob;
+                sec = min(nh, min(sec, os));
+                best = nbest;
+            }
+            a.mstate[mslot] = best;
+            a.mstate2[mslot] = sec;
+        }
+    }
+}
+
+// Rearrange the slot's 16 member rows in place into per-lane mma A quads: lane
+// (g, t), k-step s gets {row g word 2s, row g+8 word 2s, row g word 2s+1, row g+8
+// word 2s+1} of its 32-byte column block [32t, 32t+32) — one LDS.128 per k-step.
+__device__ __forceinline__ void ms_quads(MSlot& L) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const uint4* r0 = reinterpret_cast<const uint4*>(L.desc[g]) + 2 * t;
+    const uint4* r1 = reinterpret_cast<const uint4*>(L.desc[g + 8]) + 2 * t;
+    const uint4 a0 = r0[0], a1 = r0[1], b0 = r1[0], b1 = r1[1];
+    __syncwarp();
+    uint4* q = reinterpret_cast<uint4*>(&L.desc[0][0]) + lane;     // [k-step][lane]
+    q[0] = make_uint4(a0.x, b0.x, a0.y, b0.y);
+    q[32] = make_uint4(a0.z, b0.z, a0.w, b0.w);
+    q[64] = make_uint4(a1.x, b1.x, a1.y, b1.y);
+    q[96] = make_uint4(a1.z, b1.z, a1.w, b1.w);
+    __syncwarp();
+}
+
 // One round: C' bits of the unsure candidates, then the distance tiles of every
 // member block against the round's n candidates; per-member top-2 merged into
 // mstate / mstate2 (first_round: written).
 template <bool STATS>
-__device__ void ms_round(const ChunkArgs& a, MSmem& S, const MSlot& L, int n, int nu,
-                         bool first_round, int& cols_total) {
-    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+__device__ __forceinline__ int ms_round(const ChunkArgs& a, MSmem& S, const MSlot& L, int n, int nu,
+                                     bool first_round) {
+    int cols_total = 0;
+    const int lane = threadIdx.x & 31;
     const SGRec& SG = L.sg;
     const int m = SG.mcnt;
-    // ---- C' bits of the candidates not surely inside every group's C'
+    const unsigned all_groups = (1u << SG.gcnt) - 1u;
+    // ---- C' bits: "0" only where some member band of the group holds the candidate
+    // and C'(group) does not; everywhere else the bit is never consulted (don't care)
+    bool partial = false;
     for (int u0 = 0; u0 < nu; u0 += 32) {
         const int uj = u0 + lane;
         if (uj < nu) {
@@ -154,167 +400,37 @@ __device__ void ms_round(const ChunkArgs& a, MSmem& S, const MSlot& L, int n, in
             const float px = __int_as_float(c.x), py = __int_as_float(c.y);
             const bool inner = px >= SG.border && px <= SG.W - SG.border && py >= SG.border &&
                                py <= SG.H - SG.border;
-            unsigned bits = 0;
+            unsigned bits = all_groups;
             for (int gi = 0; gi < SG.gcnt; gi++) {
                 const GView gv = L.gv[gi];
                 const float dg = fabsf(fmaf(gv.a, px, fmaf(gv.b, py, gv.c)));
-                if (dg <= SG.hsure && inner) { bits |= 1u << gi; continue; }
-                if (dg > gv.reach) continue;   // outside every member band of the group
+                if ((dg <= SG.hsure && inner) || dg > gv.reach) continue;
                 const int k0 = max(gv.moff - SG.m0, 0);
                 const int k1 = gi + 1 < SG.gcnt ? max(L.gv[gi + 1].moff - SG.m0, 0) : m;
                 bool any = false;
-                for (int k = k0; k < k1 && !any; k++) {
-                    const MemberRec M = k < 16 ? L.mr[k] : a.mrec[SG.m0 + k];
-                    any = ms_member_band(a, SG, M, px, py);
-                }
-                if (any && ms_in_cprime(a, a.grp[SG.g0 + gi], SG, px, py, f)) bits |= 1u << gi;
+                for (int k = k0; k < k1 && !any; k++) any = ms_member_band(a, SG, ms_member(a, L, k), px, py);
+                if (any && a.dbg) atomicAdd(&a.dbg[6], 1ull);
+                if (any && !in_cprime(a, a.grp[SG.g0 + gi], SG, px, py, SG.toff, f)) bits &= ~(1u << gi);
             }
             S.cand[j].w = (int)bits;
+            partial |= bits != all_groups;
         }
     }
-    // ---- pad the last n8 tile with candidates no member accepts
+    // ---- pad the last n8 tile with candidates no member accepts (NaN position: never
+    // inside a band, never near its edge)
     const int ntile = (n + 7) >> 3;
     if (lane < ntile * 8 - n) {
-        S.cand[n + lane] = make_int4(0, 0, 0, 0);
+        S.cand[n + lane] = make_int4(0x7fc00000, 0x7fc00000, 0, 0);
         S.cid[n + lane] = 0;
     }
     if (STATS)
         for (int w = lane; w < MS_CAP / 32; w += 32) S.anyb[w] = 0;
+    partial = __any_sync(FULL, partial);
     __syncwarp();
-    const uint4* tdesc = reinterpret_cast<const uint4*>(a.desc + SG.toff * 128) + 2 * t;
-    for (int mb0 = 0; mb0 < m; mb0 += 16) {
-        // ---- member rows g, g+8 of this block: band constants + descriptor fragments
-        float ma[2], mbv[2], mc[2], mlo[2], mhi[2];
-        unsigned gb[2];
-        unsigned aw[2][8];
-#pragma unroll
-        for (int r = 0; r < 2; r++) {
-            const int j = mb0 + g + 8 * r;
-            if (j < m) {
-                const MemberRec M = (j < 16) ? L.mr[j] : a.mrec[SG.m0 + j];
-                ma[r] = M.a; mbv[r] = M.b; mc[r] = M.c; mlo[r] = M.lo; mhi[r] = M.hi;
-                gb[r] = 1u << ((unsigned)M.slotgi >> SLOT_BITS);
-                uint4 w0, w1;
-                if (j < 16) {
-                    const uint4* row = reinterpret_cast<const uint4*>(L.desc[j]) + 2 * t;
-                    w0 = row[0]; w1 = row[1];
-                } else {
-                    const uint4* row = reinterpret_cast<const uint4*>(a.desc + (SG.qoff + M.fid) * 128) + 2 * t;
-                    w0 = __ldg(row); w1 = __ldg(row + 1);
-                }
-                aw[r][0] = w0.x; aw[r][1] = w0.y; aw[r][2] = w0.z; aw[r][3] = w0.w;
-                aw[r][4] = w1.x; aw[r][5] = w1.y; aw[r][6] = w1.z; aw[r][7] = w1.w;
-            } else {
-                ma[r] = 0.f; mbv[r] = 0.f; mc[r] = 1e30f; mlo[r] = -1.f; mhi[r] = -1.f; gb[r] = 0;
-#pragma unroll
-                for (int k = 0; k < 8; k++) aw[r][k] = 0;
-            }
-        }
-        int k1[2] = {KEY_NONE, KEY_NONE}, k2[2] = {KEY_NONE, KEY_NONE};
-        // candidate descriptor fragments, one n8 tile ahead
-        uint4 nx0, nx1;
-        {
-            const int f = S.cid[g];
-            nx0 = __ldg(tdesc + 8 * f);
-            nx1 = __ldg(tdesc + 8 * f + 1);
-        }
-        for (int nt = 0; nt < ntile; nt++) {
-            const uint4 x0 = nx0, x1 = nx1;
-            if (nt + 1 < ntile) {
-                const int f = S.cid[8 * (nt + 1) + g];
-                nx0 = __ldg(tdesc + 8 * f);
-                nx1 = __ldg(tdesc + 8 * f + 1);
-            }
-            int acc[4] = {0, 0, 0, 0};
-            mma_u8(acc, aw[0][0], aw[1][0], aw[0][1], aw[1][1], x0.x, x0.y);
-            mma_u8(acc, aw[0][2], aw[1][2], aw[0][3], aw[1][3], x0.z, x0.w);
-            mma_u8(acc, aw[0][4], aw[1][4], aw[0][5], aw[1][5], x1.x, x1.y);
-            mma_u8(acc, aw[0][6], aw[1][6], aw[0][7], aw[1][7], x1.z, x1.w);
-            const int4 c0 = S.cand[8 * nt + 2 * t], c1 = S.cand[8 * nt + 2 * t + 1];
-            unsigned ucm = 0;
-            bool any0 = false, any1 = false;
-#pragma unroll
-            for (int e = 0; e < 4; e++) {
-                const int r = e >> 1;               // member row (g, g+8)
-                const int4 c = (e & 1) ? c1 : c0;   // candidate column (2t, 2t+1)
-                const float px = __int_as_float(c.x), py = __int_as_float(c.y);
-                const float av = fabsf(fmaf(ma[r], px, fmaf(mbv[r], py, mc[r])));
-                const bool cb = ((unsigned)c.w & gb[r]) != 0u;
-                const bool in = av <= mlo[r] && cb;
-                if (!(av <= mlo[r]) && av <= mhi[r] && cb) ucm |= 1u << e;
-                if (STATS) { if (e & 1) any1 |= in; else any0 |= in; }
-                const int key = c.z - acc[e] * 512;
-                ms_top2(in ? key : KEY_NONE, k1[r], k2[r]);
-            }
-            if (__any_sync(FULL, ucm != 0)) {
-                // within eps of the band edge: the reference's fp64 band value decides
-#pragma unroll
-                for (int e = 0; e < 4; e++) {
-                    if (!((ucm >> e) & 1u)) continue;
-                    const int r = e >> 1;
-                    const int4 c = (e & 1) ? c1 : c0;
-                    const int j = mb0 + g + 8 * r;
-                    const MemberRec M = (j < 16) ? L.mr[j] : a.mrec[SG.m0 + j];
-                    if (ms_band_exact(a, SG, M, __int_as_float(c.x), __int_as_float(c.y))) {
-                        if (STATS) { if (e & 1) any1 = true; else any0 = true; }
-                        ms_top2(c.z - acc[e] * 512, k1[r], k2[r]);
-                    }
-                }
-            }
-            if (STATS) {
-                const unsigned b0 = __ballot_sync(FULL, any0), b1 = __ballot_sync(FULL, any1);
-                if (lane == 0) {
-                    unsigned bits = 0;
-#pragma unroll
-                    for (int tt = 0; tt < 4; tt++) {
-                        if (b0 & (0x11111111u << tt)) bits |= 1u << (2 * tt);
-                        if (b1 & (0x11111111u << tt)) bits |= 1u << (2 * tt + 1);
-                    }
-                    const int c8 = 8 * nt;
-                    S.anyb[c8 >> 5] |= bits << (c8 & 31);
-                }
-            }
-        }
-        // ---- reduce the per-lane top-2 over the 4 lanes (t) sharing a member row
-#pragma unroll
-        for (int r = 0; r < 2; r++) {
-#pragma unroll
-            for (int o = 1; o < 4; o <<= 1) {
-                const int o1 = __shfl_xor_sync(FULL, k1[r], o), o2 = __shfl_xor_sync(FULL, k2[r], o);
-                const int lo = min(k1[r], o1), hi = max(k1[r], o1);
-                k1[r] = lo;
-                k2[r] = min(hi, min(k2[r], o2));
-            }
-        }
-        if (t == 0) {
-#pragma unroll
-            for (int r = 0; r < 2; r++) {
-                const int j = mb0 + g + 8 * r;
-                if (j >= m) continue;
-                const MemberRec M = (j < 16) ? L.mr[j] : a.mrec[SG.m0 + j];
-                const int mslot = M.slotgi & SLOT_MASK;
-                const unsigned q2 = (unsigned)M.qn9 >> 9;
-                unsigned long long best = ~0ull;
-                unsigned sec = NONE;
-                if (k1[r] != KEY_NONE) {
-                    const unsigned d2 = q2 + (unsigned)(k1[r] >> 8);
-                    best = ((unsigned long long)d2 << 32) | (unsigned)S.cid[k1[r] & 255];
-                }
-                if (k2[r] != KEY_NONE) sec = q2 + (unsigned)(k2[r] >> 8);
-                if (!first_round) {
-                    const unsigned long long ob = a.mstate[mslot];
-                    const unsigned os = a.mstate2[mslot];
-                    const unsigned bd = (unsigned)(best >> 32), od = (unsigned)(ob >> 32);
-                    const unsigned nh = max(bd, od);
-                    const unsigned long long nbest = (bd < od) ? best : ob;
-                    sec = min(nh, min(sec, os));
-                    best = nbest;
-                }
-                a.mstate[mslot] = best;
-                a.mstate2[mslot] = sec;
-            }
-        }
-    }
+    if (partial) ms_block<true, STATS, true>(a, S, L, 0, m, ntile, first_round);
+    else         ms_block<false, STATS, true>(a, S, L, 0, m, ntile, first_round);
+    // member blocks past the slot (one group of > 16 members, stats mode only)
+    for (int mb0 = 16; mb0 < m; mb0 += 16) ms_block<true, STATS, false>(a, S, L, mb0, m, ntile, first_round);
     if (STATS) {
         __syncwarp();
         int cnt = lane < MS_CAP / 32 ? __popc(S.anyb[lane]) : 0;
@@ -323,10 +439,11 @@ __device__ void ms_round(const ChunkArgs& a, MSmem& S, const MSlot& L, int n, in
         cols_total += cnt;
     }
     __syncwarp();
+    return cols_total;
 }
 
 template <bool STATS>
-__global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(ChunkArgs a) {
+__global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(const __grid_constant__ ChunkArgs a) {
     extern __shared__ __align__(128) unsigned char ms_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     MSmem& S = reinterpret_cast<MSmem*>(ms_raw)[warp];
@@ -335,11 +452,10 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(ChunkA
     if (lane == 0) {
         ms_bar_init(&S.bar_q);
         ms_bar_init(&S.bar_rec[0]); ms_bar_init(&S.bar_rec[1]);
-        ms_bar_init(&S.bar_desc[0]); ms_bar_init(&S.bar_desc[1]);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
-    uint32_t ph_q = 0, ph_rec = 0, ph_desc = 0;   // phase bits (per slot: bit s)
+    uint32_t ph_q = 0, ph_rec = 0;     // phase bits (per slot: bit s)
     auto claim = [&]() {
         int s = 0;
         if (lane == 0) s = atomicAdd(a.sg_next, 1);
@@ -351,24 +467,23 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(ChunkA
         __syncwarp();
     };
     // prologue: slots 0 and 1 get the first two SGs (records + member data in flight)
-    int sid_s[2];
-    sid_s[0] = claim();
-    sid_s[1] = claim();
-#pragma unroll
-    for (int s = 0; s < 2; s++) {
-        if (sid_s[s] < total) {
-            load_sg(S.slot[s], sid_s[s]);
-            if (lane == 0) ms_issue_rec(a, S.slot[s], &S.bar_rec[s]);
-        }
+    int sid_cur = claim(), sid_nxt = claim();
+    if (sid_cur < total) {
+        load_sg(S.slot[0], sid_cur);
+        if (lane == 0) ms_issue_rec(a, S.slot[0], &S.bar_rec[0]);
     }
-    if (sid_s[0] < total) {
+    if (sid_nxt < total) {
+        load_sg(S.slot[1], sid_nxt);
+        if (lane == 0) ms_issue_rec(a, S.slot[1], &S.bar_rec[1]);
+    }
+    if (sid_cur < total) {
         ms_wait(&S.bar_rec[0], 0);
         ph_rec ^= 1u;
-        ms_issue_desc(a, S.slot[0], &S.bar_desc[0]);
+        ms_issue_desc(a, S.slot[0]);
     }
     int cur = 0;
     for (;;) {
-        const int sid = sid_s[cur];
+        const int sid = sid_cur;
         if (sid >= total) break;
         const int nxt = cur ^ 1;
         MSlot& L = S.slot[cur];
@@ -378,9 +493,10 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(ChunkA
             ms_expect(&S.bar_q, (uint32_t)sizeof(SGRec));
             ms_bulk(&S.sgq, a.sg + sid2, sizeof(SGRec), &S.bar_q);
         }
-        // this SG's member records / group views / member descriptors have landed
-        ms_wait(&S.bar_desc[cur], (ph_desc >> cur) & 1u);
-        ph_desc ^= 1u << cur;
+        // this SG's member descriptor rows (cp.async issued during the last SG)
+        cp_async_wait_all();
+        __syncwarp();
+        ms_quads(L);
         const SGRec& SG = L.sg;
         if (a.dbg && lane == 0) {
             atomicAdd(&a.dbg[0], 1ull);
@@ -397,11 +513,10 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(ChunkA
         int cols_total = 0;
         bool nxt_desc_issued = false;
         auto issue_next_desc = [&]() {
-            if (!nxt_desc_issued && sid_s[nxt] < total) {
+            if (!nxt_desc_issued && sid_nxt < total) {
                 ms_wait(&S.bar_rec[nxt], (ph_rec >> nxt) & 1u);
                 ph_rec ^= 1u << nxt;
-                ms_fence_async();
-                ms_issue_desc(a, S.slot[nxt], &S.bar_desc[nxt]);
+                ms_issue_desc(a, S.slot[nxt]);
             }
             nxt_desc_issued = true;
         };
@@ -429,42 +544,55 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(ChunkA
                 }
             }
         };
+        // Resumable gather state: the current 32-row batch (per-lane CSR span bs, len
+        // and its inclusive prefix), the next record index j0 in it, the prefetched
+        // record of j0 + lane, and the next batch's spans (prefetched).  A full
+        // candidate list suspends the gather for a round; the round runs outside the
+        // gather loop, so the two never compete for registers.
+        int r0 = SG.rlo, bs = 0, len = 0, incl = 0, tot = 0, j0 = 0;
         int nbs, ne1;
-        row_span(SG.rlo + lane, nbs, ne1);
-        for (int r0 = SG.rlo; r0 <= SG.rhi; r0 += 32) {
-            const int bs = nbs, len = ne1 - nbs;
+        int4 nrec = make_int4(0, 0, 0, 0);
+        auto rec_at = [&](int j) {
+            int o = 0;
+#pragma unroll
+            for (int sft = 16; sft > 0; sft >>= 1) {
+                const int v = __shfl_sync(FULL, incl, o + sft - 1);
+                if (v <= j) o += sft;
+            }
+            const int ob = __shfl_sync(FULL, bs, o & 31);
+            const int oex = __shfl_sync(FULL, incl - len, o & 31);
+            return ob + (j - oex);
+        };
+        auto open_batch = [&]() {
+            bs = nbs;
+            len = ne1 - nbs;
             row_span(r0 + 32 + lane, nbs, ne1);
-            int incl = len;
+            incl = len;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int y = __shfl_up_sync(FULL, incl, o);
                 if (lane >= o) incl += y;
             }
-            const int tot = __shfl_sync(FULL, incl, 31);
+            tot = __shfl_sync(FULL, incl, 31);
             if (a.dbg && lane == 0) atomicAdd(&a.dbg[2], (unsigned long long)tot);
-            auto rec_at = [&](int j) {
-                int o = 0;
-#pragma unroll
-                for (int s = 16; s > 0; s >>= 1) {
-                    const int v = __shfl_sync(FULL, incl, o + s - 1);
-                    if (v <= j) o += s;
+            j0 = 0;
+            const int ri = rec_at(lane);
+            nrec = lane < tot ? __ldg(mrec4 + ri) : make_int4(0, 0, 0, 0);
+        };
+        row_span(SG.rlo + lane, nbs, ne1);
+        if (r0 <= SG.rhi) open_batch();
+        for (;;) {
+            // ---- gather until the strip ends or the next record batch would overflow
+            bool full = false;
+            while (r0 <= SG.rhi) {
+                if (j0 >= tot) {
+                    r0 += 32;
+                    if (r0 > SG.rhi) break;
+                    open_batch();
+                    continue;
                 }
-                const int ob = __shfl_sync(FULL, bs, o & 31);
-                const int oex = __shfl_sync(FULL, incl - len, o & 31);
-                return ob + (j - oex);
-            };
-            int4 nrec = make_int4(0, 0, 0, 0);
-            {
-                const int ri = rec_at(lane);
-                if (lane < tot) nrec = __ldg(mrec4 + ri);
-            }
-            for (int j0 = 0; j0 < tot; j0 += 32) {
                 const int j = j0 + lane;
                 const int4 rec = nrec;
-                {
-                    const int ri = rec_at(j + 32);
-                    if (j + 32 < tot) nrec = __ldg(mrec4 + ri);
-                }
                 bool pass = false, sure = false;
                 const float px = __int_as_float(rec.x), py = __int_as_float(rec.y);
                 if (j < tot) {
@@ -475,18 +603,16 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(ChunkA
                 }
                 const unsigned bal = __ballot_sync(FULL, pass);
                 const int cnt = __popc(bal);
+                if (n + cnt > MS_CAP) { full = true; break; }
+                {
+                    const int ri = rec_at(j + 32);
+                    if (j + 32 < tot) nrec = __ldg(mrec4 + ri);
+                }
                 if (a.dbg && lane == 0) {
                     atomicAdd(&a.dbg[3], (unsigned long long)cnt);
                     atomicAdd(&a.dbg[4], (unsigned long long)__popc(__ballot_sync(FULL, pass && sure)));
                 } else if (a.dbg) {
                     __ballot_sync(FULL, pass && sure);
-                }
-                if (n + cnt > MS_CAP) {
-                    issue_next_desc();
-                    ms_round<STATS>(a, S, L, n, nu, first_round, cols_total);
-                    first_round = false;
-                    n = 0;
-                    nu = 0;
                 }
                 const int k = __popc(bal & ((1u << lane) - 1u));
                 const unsigned ubal = __ballot_sync(FULL, pass && !sure);
@@ -498,13 +624,18 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(ChunkA
                 }
                 n += cnt;
                 nu += __popc(ubal);
+                j0 += 32;
                 __syncwarp();
             }
-        }
-        issue_next_desc();
-        if (n > 0) {
-            ms_round<STATS>(a, S, L, n, nu, first_round, cols_total);
-            first_round = false;
+            __syncwarp();
+            issue_next_desc();
+            if (n > 0) {
+                cols_total += ms_round<STATS>(a, S, L, n, nu, first_round);
+                first_round = false;
+                n = 0;
+                nu = 0;
+            }
+            if (!full) break;
         }
         __syncwarp();
         // ---- ratio test + dedupe per member (ratio_filter / _dedupe_targets)
@@ -544,7 +675,8 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(ChunkA
         }
         __syncwarp();
         // ---- slot `cur` is free: it takes the SG after next
-        sid_s[cur] = sid2;
+        sid_cur = sid_nxt;
+        sid_nxt = sid2;
         if (sid2 < total) {
             ms_wait(&S.bar_q, ph_q);
             ph_q ^= 1u;

@@ -1,0 +1,17 @@
+# Build A/B variants of libmsfm_b200.so with extra -D flags for guided.cu:
+#   tools/build_variants.sh NAME "-DFLAG=1 ..." [NAME "-D..."]...
+# -> paper_1512_06235_b200/variants/libmsfm_NAME.so (select with MSFM_B200_LIB=...)
+set -e
+cd "$(dirname "$0")/../paper_1512_06235_b200/csrc"
+make -s >/dev/null
+mkdir -p ../variants
+while [ $# -ge 2 ]; do
+  name=$1; flags=$2; shift 2
+  /usr/local/cuda/bin/nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo \
+     -Xcompiler -fPIC -I../../include -fmad=false --expt-relaxed-constexpr -Xptxas -v $flags \
+     -c guided.cu -o /tmp/guided_$name.o 2> /tmp/guided_$name.log
+  grep -A2 "Function properties for.*match_ms_kernelILb0" /tmp/guided_$name.log | grep -i "spill\|regis" | tr '\n' ' '; echo " <- $name"
+  objs=$(ls *.o | grep -v '^guided.o$')
+  /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../variants/libmsfm_$name.so \
+     /tmp/guided_$name.o $objs -lcudart -Xcompiler -pthread
+done
