@@ -46,6 +46,9 @@ def parse():
     p.add_argument("--e2e-resident", action="store_true",
                    help="e2e: upload + index the whole bank before matching (no staging)")
     p.add_argument("--no-localize", action="store_true")
+    p.add_argument("--gather-chunks", type=int, default=4,
+                   help="N > 1: pair chunks per rank whose rows go to rank 0 while the next "
+                        "chunk computes")
     return p.parse_args()
 
 
@@ -248,14 +251,6 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def gather_to_rank0(res, world, dev):
-    """Variable-length gather of this rank's matches over NCCL: the device-packed
-    16-B rows (pair index local to the rank: global = rank + world * local)."""
-    from paper_1512_06235_b200.dist import gather_rows
-
-    rows, _ = res.packed()
-    return gather_rows(rows, world)
-
 
 def run_b200(args, rank, world):
     import torch
@@ -266,6 +261,8 @@ def run_b200(args, rank, world):
     from paper_1512_06235_b200.guided import (HostPairs, match_pairs, match_pairs_rows,
                                               match_pairs_rows_staged, prepare_pairs)
 
+    from paper_1512_06235_b200.dist import ChunkGather, chunk_bounds
+
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
     scene, wl, ok, snap = build_workload(args.cameras, with_snapshot=True)
@@ -273,16 +270,44 @@ def run_b200(args, rank, world):
     ql = [wl.untracked[int(wl.q_img[k])] for k in mine]
     host = HostBank(scene.feature_sets)
     bank = FeatureBank(host=host, device=dev)
-    inputs = prepare_pairs(bank, wl.q_img[mine], wl.t_img[mine], wl.F[mine], ql)
     D = 8.0 * 1.25
     bank.grid(D)
+    # N > 1: each rank's pairs in G chunks; chunk k's packed rows go to rank 0 (NCCL
+    # point-to-point, capacity-sized buffers known to every rank) while chunk k+1
+    # computes — the overlapped gather of SURVEY.md §8e
+    G = max(1, args.gather_chunks) if world > 1 else 1
+    qn = np.array([len(wl.untracked[int(wl.q_img[k])]) for k in ok], np.int64)
+    caps, bounds_of = [], []
+    for r in range(world):
+        mr = np.arange(r, len(ok), world)
+        b = chunk_bounds(len(mr), G)
+        bounds_of.append(b)
+        caps.append([int(qn[mr[b[k]:b[k + 1]]].sum()) for k in range(len(b) - 1)])
+    bounds = bounds_of[rank]
+    n_chunks = len(bounds) - 1
+    chunk_inputs = [prepare_pairs(bank, wl.q_img[mine[bounds[k]:bounds[k + 1]]],
+                                  wl.t_img[mine[bounds[k]:bounds[k + 1]]],
+                                  wl.F[mine[bounds[k]:bounds[k + 1]]], ql[bounds[k]:bounds[k + 1]])
+                    for k in range(n_chunks)]
+    gathered = {}
 
     def step():
-        res = match_pairs(bank, wl.q_img[mine], wl.t_img[mine], wl.F[mine], ql,
-                          device_inputs=inputs, chunk_pairs=args.chunk_pairs)
-        if world > 1:
-            gather_to_rank0(res, world, dev)
-        return res
+        gat = ChunkGather(world, rank, caps, dev) if world > 1 else None
+        out = []
+        for k in range(n_chunks):
+            sl = slice(bounds[k], bounds[k + 1])
+            res = match_pairs(bank, wl.q_img[mine[sl]], wl.t_img[mine[sl]], wl.F[mine[sl]], ql[sl],
+                              device_inputs=chunk_inputs[k], chunk_pairs=args.chunk_pairs)
+            out.append(res)
+            if gat is not None:
+                rows, cnt = res.packed_device()
+                gat.put(k, rows, cnt)
+        if gat is not None:
+            got = gat.finish()
+            if got is not None:
+                gathered.clear()
+                gathered.update(got)
+        return out
 
     def barrier():
         if world > 1:
@@ -291,7 +316,7 @@ def run_b200(args, rank, world):
     for _ in range(args.warmup):
         res = step()
     torch.cuda.synchronize()
-    n_matches_local = int(res.count.sum().item())
+    n_matches_local = int(sum(int(r.count.sum().item()) for r in res))
 
     # ---- timed region: device-resident inputs -> matches (gathered on rank 0)
     l0 = _lib.launch_count()
@@ -328,7 +353,23 @@ def run_b200(args, rank, world):
 
     # ---- the stage's next step on the same matches: device track merge (densify.py:68-158)
     try:
-        merge = track_merge_leg(bank, wl, mine, res, snap, dev, scene, world, rank, ok)
+        if world == 1:
+            rows_all, _ = res[0].packed()
+        else:
+            # rank 0 holds every rank's rows (the last timed step's gather)
+            from paper_1512_06235_b200.dist import merge_chunk_rows
+
+            rows_all = None
+            if rank == 0:
+                index = {}
+                for r in range(world):
+                    mr = np.arange(r, len(ok), world)
+                    b = bounds_of[r]
+                    for k in range(len(b) - 1):
+                        index[(r, k)] = mr[b[k]:b[k + 1]]
+                rows_all = torch.from_numpy(merge_chunk_rows(gathered, index)).to(dev)
+        merge = track_merge_leg(bank, wl, ok if world > 1 else mine, rows_all, snap, dev,
+                                scene) if rows_all is not None else None
     except Exception as exc:                        # never lose the step's line over it
         merge = {"error": f"{type(exc).__name__}: {exc}"}
 
@@ -374,6 +415,8 @@ def run_b200(args, rank, world):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = total_pairs / (float(te.item()) / 1e3)
 
+    # localization: query images sharded round-robin over the ranks (every rank runs)
+    loc = run_localization(args, dev, world, rank) if not args.no_localize else None
     if rank != 0:
         return
     cpu = None
@@ -394,7 +437,9 @@ def run_b200(args, rank, world):
                    "pairs": int(total_pairs), "cameras": args.cameras,
                    "mean_queries_per_pair": float(np.mean([len(wl.untracked[int(wl.q_img[k])]) for k in ok])),
                    "parallelism": f"pairs round-robin over {world} GPU(s), no collective on "
-                                  "the data path; match rows gathered over NCCL",
+                                  "the data path" + ("" if world == 1 else
+                                  f"; each rank's rows go to rank 0 in {G} chunks over NCCL "
+                                  "point-to-point, overlapping the next chunk's matching"),
                    "scaling_note": "C3's pair set sharded across ranks (BASELINE configs[2]); "
                                    "labelled weak per the sharded-independent-units rule",
                    "l2": "inputs larger than L2 (feature bank "
@@ -415,8 +460,8 @@ def run_b200(args, rank, world):
         "matches_per_step": n_matches_local if world == 1 else None,
         "track_merge": merge,
     }
-    if not args.no_localize:
-        line["localization"] = run_localization(args, dev, world)
+    if loc is not None:
+        line["localization"] = loc
         line["coarse_graph"] = coarse_graph_leg(dev)
     print(json.dumps(line), flush=True)
 
@@ -452,27 +497,17 @@ def coarse_graph_leg(dev, n_cameras=40):
             "wall_ms": dt * 1e3, "kernel_ms": kern}
 
 
-def track_merge_leg(bank, wl, mine, res, snap, dev, scene=None, world=1, rank=0, ok=None):
+def track_merge_leg(bank, wl, pairs, rows, snap, dev, scene=None):
     """msfm_merge_tracks over the step's matches + the coarse tracks (bank nodes).
-    With several ranks every rank's rows are gathered (NCCL) and rank 0 merges all
-    of them — the gather of tracks of an N-GPU run; other ranks return None."""
+    ``rows``: device int32 (n, 4) packed match rows whose pair column indexes
+    ``pairs``; with several ranks these are every rank's rows gathered on rank 0 —
+    the gather of tracks of an N-GPU run."""
     import torch
 
     from paper_1512_06235_b200 import _lib
     from paper_1512_06235_b200.densify import merge_tracks_nodes
 
-    rows, n = res.packed()
-    pairs = mine
-    if world > 1:
-        from paper_1512_06235_b200.dist import gather_rows
-
-        g = rows.clone()
-        g[:, 0] = rank + world * g[:, 0]            # rank-local pair -> index into `ok`
-        rows = gather_rows(g, world)
-        if rank != 0:
-            return None
-        pairs = ok
-        n = int(rows.shape[0])
+    n = int(rows.shape[0])
     qoff = torch.from_numpy(bank.offsets[bank.slots(wl.q_img[pairs])]).to(dev)
     toff = torch.from_numpy(bank.offsets[bank.slots(wl.t_img[pairs])]).to(dev)
     pk = rows[:, 0].long()
@@ -581,8 +616,12 @@ def cpu_localize_rate(scene, snap, queries, sample, seed=0):
     return len(jobs) / dt, min(cores, len(jobs)), len(jobs), dt
 
 
-def run_localization(args, dev, world=1):
+def run_localization(args, dev, world=1, rank=0):
+    """C2 localization leg.  With N ranks the 80 query images are sharded
+    round-robin (localize.py:256-267: images are independent given the snapshot);
+    the step time is the max over ranks; rank 0 returns the record."""
     import torch
+    import torch.distributed as tdist
 
     from paper_1512_06235_b200 import _lib, scenes
     from paper_1512_06235_b200.bank import FeatureBank, HostBank
@@ -590,7 +629,8 @@ def run_localization(args, dev, world=1):
                                                 knn2_tracks, knn2_tracks_staged, upload_points)
     from paper_1512_06235_b200.pnp import pnp_batch_flat
 
-    scene, snap, queries = build_localization()
+    scene, snap, all_queries = build_localization()
+    queries = all_queries[rank::world]
     S, n = scenes.track_sums(scene, snap)
     pts = PointSet(S=S, n=n, ids=np.arange(len(S)))
     host = HostBank({q: scene.feature_sets[q] for q in queries})
@@ -612,11 +652,18 @@ def run_localization(args, dev, world=1):
     for _ in range(args.warmup):
         corrs, res = step(bank, dp, d_xyz)
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
+    if world > 1:
+        tdist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
     for _ in range(args.steps):
         corrs, res = step(bank, dp, d_xyz)
+    e1.record()
     torch.cuda.synchronize()
-    dt = (time.perf_counter() - t0) / args.steps
+    tt = torch.tensor([e0.elapsed_time(e1) / 1e3 / args.steps], device=dev)
+    if world > 1:
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+    dt = float(tt.item())
     status = {}
     for r in res:
         status[r.status] = status.get(r.status, 0) + 1
@@ -651,12 +698,23 @@ def run_localization(args, dev, world=1):
         torch.cuda.synchronize()
         if i >= args.warmup:
             e2e.append(time.perf_counter() - t1)
+    te = torch.tensor([float(np.mean(e2e))], device=dev)
+    cnts = torch.tensor([status.get(k, 0) for k in ("ok", "none", "overflow", "insufficient")],
+                        device=dev, dtype=torch.int64)
+    if world > 1:
+        tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
+        tdist.all_reduce(cnts)
+    e2e_s = float(te.item())
+    status = {k: int(v) for k, v in zip(("ok", "none", "overflow", "insufficient"), cnts.tolist()) if v}
+    if rank != 0:
+        return None
     out = {"metric": "localized images/sec",
            "workload": f"C2: 100-camera scene, 8k feats/img, 20% coarse model (M={M} points), "
-                       f"{len(queries)} query images: exact kNN + ratio + seeded PnP-RANSAC",
-           "value": len(queries) / dt, "unit": "images/s",
+                       f"{len(all_queries)} query images: exact kNN + ratio + seeded PnP-RANSAC"
+                       + ("" if world == 1 else f", images round-robin over {world} GPUs"),
+           "value": len(all_queries) / dt, "unit": "images/s",
            "ms_per_step": dt * 1e3, "status_counts": status,
-           "e2e": {"value": len(queries) / float(np.mean(e2e)), "unit": "images/s",
+           "e2e": {"value": len(all_queries) / e2e_s, "unit": "images/s",
                    "h2d_bytes_per_step": int(host.nbytes + S.nbytes + n.nbytes + 8 * M + 24 * M),
                    "d2h_bytes_per_step": int(4 * len(queries) + 13 * 8 * len(res) +
                                              sum(r.mask.nbytes for r in res if r.mask is not None))},
@@ -667,7 +725,8 @@ def run_localization(args, dev, world=1):
                         "kernel_ms": k_ms, "alg_frac": (ops_alg / (k_ms / 1e3) / 1e12) / peak
                         if k_ms > 0 else 0.0,
                         "units": ncu_unit_utilization("ncu_knn_tc_kernel.json")}}
-    out["n_gpus"] = 1        # this leg runs on rank 0's GPU
+    out["n_gpus"] = world
+    out["roofline"]["note"] = "rank 0's image shard" if world > 1 else None
     if not args.no_cpu and world == 1:
         r, cores, ns, cdt = cpu_localize_rate(scene, snap, queries, max(cpu_cores(), 8))
         out["cpu_baseline"] = {"value": r, "unit": "images/s", "cores": cores, "kind": "port",
@@ -677,8 +736,31 @@ def run_localization(args, dev, world=1):
     return out
 
 
+def relaunch(args):
+    """--gpus N > 1 outside torchrun: start N ranks (one per GPU) with
+    torch.distributed.run on this node and return its exit code."""
+    import socket
+
+    if args.impl == "b200":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(json.dumps({"error": f"--gpus {args.gpus} but only {have} CUDA device(s) visible"}),
+                  flush=True)
+            return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if world > 1:

@@ -59,6 +59,26 @@ class PairMatches:
         total = int(off[P].item())
         return rows[:total], total
 
+    def packed_device(self, stream=None):
+        """Like ``packed`` without the host sync: (rows int32 (cap, 4), total int64 (1,)
+        on the device); rows past ``total`` are unspecified.  cap = the pair set's
+        query count (one row per query at most)."""
+        import torch
+
+        lib = _lib.load()
+        P = self.count.numel()
+        dev = self.q.device
+        off = torch.empty(P + 1, dtype=torch.int64, device=dev)
+        rows = torch.empty((max(self.q.numel(), 1), 4), dtype=torch.int32, device=dev)
+        if P:
+            _lib.check(lib.msfm_pack_matches(P, _lib.ptr(self._qoff_d), _lib.ptr(self.count),
+                                             _lib.ptr(self.q), _lib.ptr(self.t), _lib.ptr(self.dist),
+                                             _lib.ptr(self.ratio), _lib.ptr(off), _lib.ptr(rows),
+                                             _lib.stream_handle(stream)), "msfm_pack_matches")
+        else:
+            off.zero_()
+        return rows, off[P:P + 1]
+
     def rows_host(self, pinned=None):
         """Host structured array (MATCH_ROW: pair, q, t, dist, ratio) in pair order:
         one device-side pack and one D2H copy.  With ``pinned`` (int32 (>=total, 4),
