@@ -265,24 +265,25 @@ int msfm_ransac_samples_seeded(int32_t n_items, const uint64_t* seeds, const int
  *     key = n_p |f|^2 - 2 S_p.f     (N = |S - n f|^2 = n_p*key + |S_p|^2)
  * over the image's features, lowest feature index winning ties:
  *     k1[s][p], i1[s][p] (image-local feature id, -1 if none), k2[s][p]
- * (INT32_MAX when the image has < 2 features).  Row stride = n_points rounded
- * up to 128.  2 S.f runs on tcgen05 kind::i8 over two u8 digit planes
- * (2S = lo + 256 hi, lo = 2 (S mod 128), hi = S >> 7).
- * Requires max track length <= 100 (int32 keys); max_image_features bounds the
- * feature count of every query image.
+ * (INT64_MAX when the image has < 2 features).  Row stride = n_points rounded
+ * up to 128.  2 S.f runs on tcgen05 kind::i8 over u8 digit planes: points with
+ * track length <= 100 use two (2S = lo + 256 hi, lo = 2 (S mod 128), hi = S >> 7,
+ * int32 keys in the epilogue), longer tracks three base-256 digits of 2S and int64
+ * keys (any track length up to 32767; max_track > 100 enables that launch);
+ * max_image_features bounds the feature count of every query image.
  * ---------------------------------------------------------------------- */
 size_t msfm_knn_workspace_bytes(int32_t n_points, int32_t n_images, int32_t max_image_features);
 int msfm_knn2_tracks(const msfm_bank* bank, int32_t n_points, const int32_t* d_S,
                      const int32_t* d_n, int32_t n_images, const int32_t* d_images,
-                     int32_t max_track, int32_t max_image_features, int32_t* d_k1, int32_t* d_i1,
-                     int32_t* d_k2, void* d_workspace, size_t workspace_bytes, void* stream);
+                     int32_t max_track, int32_t max_image_features, int64_t* d_k1, int32_t* d_i1,
+                     int64_t* d_k2, void* d_workspace, size_t workspace_bytes, void* stream);
 
 /* Index of the second neighbour of msfm_knn2_tracks' output (the lowest feature
  * index other than i1 whose key equals k2, descriptors.py:61-63), -1 when there
  * is none: d_i2 [n_images][n_points rounded up to 128]. */
 int msfm_knn2_second_index(const msfm_bank* bank, int32_t n_points, const int32_t* d_S,
                            const int32_t* d_n, int32_t n_images, const int32_t* d_images,
-                           const int32_t* d_k1, const int32_t* d_i1, const int32_t* d_k2,
+                           const int64_t* d_k1, const int32_t* d_i1, const int64_t* d_k2,
                            int32_t* d_i2, void* stream);
 
 /* Real-valued 2-NN for float descriptor rows that are not integer-valued
@@ -303,7 +304,7 @@ int msfm_knn2_float(const float* d_q, int64_t n_queries, const float* d_t, int64
  * sum over query images of their feature counts (int32), offsets d_win_off[s]. */
 int msfm_direct_3d2d(const msfm_bank* bank, int32_t n_points, const int32_t* d_n,
                      const int64_t* d_SS, int32_t n_images, const int32_t* d_images,
-                     const int32_t* d_k1, const int32_t* d_i1, const int32_t* d_k2,
+                     const int64_t* d_k1, const int32_t* d_i1, const int64_t* d_k2,
                      int64_t ratio_p, int64_t ratio_q, double single_cap,
                      int32_t* d_win, const int64_t* d_win_off, int32_t* d_corr_row,
                      int32_t* d_corr_fid, int32_t* d_corr_n, void* stream);

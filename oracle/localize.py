@@ -28,14 +28,22 @@ class InsufficientDataError(Exception):
 
 def knn2_exact(S, n, F):
     """(idx_best, N_best, N_second) per point; N_second = -1 when F has 1 row."""
-    S = np.asarray(S, np.float64)
-    n = np.asarray(n, np.float64)
-    F = np.asarray(F, np.float64)
-    SS = (S * S).sum(1)
-    FF = (F * F).sum(1)
-    # exact: every partial sum is an integer < 2^53
-    N = SS[:, None] - 2.0 * n[:, None] * (S @ F.T) + (n[:, None] ** 2) * FF[None, :]
-    N = np.rint(N).astype(np.int64)
+    if len(n) and int(np.max(n)) > 1000:
+        # long tracks: N can pass 2^53, so every term in int64 (exact, slower)
+        S = np.asarray(S, np.int64)
+        n = np.asarray(n, np.int64)
+        F = np.asarray(F, np.int64)
+        N = ((S * S).sum(1)[:, None] - 2 * n[:, None] * (S @ F.T)
+             + (n[:, None] ** 2) * (F * F).sum(1)[None, :])
+    else:
+        S = np.asarray(S, np.float64)
+        n = np.asarray(n, np.float64)
+        F = np.asarray(F, np.float64)
+        SS = (S * S).sum(1)
+        FF = (F * F).sum(1)
+        # exact: every partial sum is an integer < 2^53
+        N = SS[:, None] - 2.0 * n[:, None] * (S @ F.T) + (n[:, None] ** 2) * FF[None, :]
+        N = np.rint(N).astype(np.int64)
     best = np.argmin(N, axis=1)
     rows = np.arange(len(N))
     nb = N[rows, best].copy()

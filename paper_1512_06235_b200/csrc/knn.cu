@@ -20,6 +20,8 @@
 #include <cuda.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace msfm {
@@ -37,19 +39,24 @@ constexpr uint32_t B_TILE_BYTES = TILE_N * KB;          // 16 KB
 constexpr uint32_t A_PLANE_BYTES = TILE_M * KB;         // 16 KB
 constexpr int INT_BIG = 0x7fffffff;
 
+constexpr long long KEY_BIG64 = 0x7fffffffffffffffLL;   // "no second neighbour"
+
 struct KnnSmem {
-    uint8_t a[2][A_PLANE_BYTES];            // lo, hi planes (1024-B aligned)
+    uint8_t a[3][A_PLANE_BYTES];            // digit planes of 2S (1024-B aligned)
     uint8_t b[KN_STAGES][B_TILE_BYTES];
     uint64_t full[KN_STAGES], empty[KN_STAGES];
     uint64_t a_full, a_empty;
     uint64_t t_full[2], t_empty[2];
     uint32_t tmem_base;
-    int merge_k1[EPI_WARPS / 4][TILE_M], merge_i1[EPI_WARPS / 4][TILE_M], merge_k2[EPI_WARPS / 4][TILE_M];
+    long long merge_k1[EPI_WARPS / 4][TILE_M], merge_k2[EPI_WARPS / 4][TILE_M];
+    int merge_i1[EPI_WARPS / 4][TILE_M];
     alignas(16) int fvs[];   // |f|^2 of the current unit's image (fn_stride ints)
 };
 
 struct KnnArgs {
-    const int32_t* n;          // [M_pad] track length (0 for padding rows)
+    const int32_t* count;      // rows of this launch's point subset (device)
+    const int32_t* rowmap;     // subset row -> output row
+    const int32_t* n;          // [M_pad] track length of each subset row
     const int32_t* fnorm;      // bank |f|^2
     const int32_t* fn_pad;     // [n_img][fn_stride] |f|^2 per query image, 16-B aligned tiles
     int fn_stride;
@@ -57,11 +64,10 @@ struct KnnArgs {
     const int32_t* img_n;      // bank image sizes
     const int32_t* images;     // [n_img] bank image index of each query image
     int n_img;
-    int m_tiles;
     int M;                     // real points
-    int32_t* out_k1;           // [n_img][M_pad]
+    long long* out_k1;         // [n_img][M_pad] (output rows)
     int32_t* out_i1;
-    int32_t* out_k2;
+    long long* out_k2;
     int M_pad;
 };
 
@@ -178,26 +184,38 @@ __device__ __forceinline__ void tc_fence_after() {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
-__device__ __forceinline__ int unit_tiles(const KnnArgs& a, int u, int& img, int& mt, int64_t& off,
-                                          int& n) {
+__device__ __forceinline__ int unit_tiles(const KnnArgs& a, int m_tiles, int u, int& img, int& mt,
+                                          int64_t& off, int& n) {
     // image-major: the CTAs running at one time share a few images' feature tiles
     // (L2 hits) instead of streaming every image once per point tile
-    const int s = u / a.m_tiles;
-    mt = u - s * a.m_tiles;
+    const int s = u / m_tiles;
+    mt = u - s * m_tiles;
     img = a.images[s];
     off = a.img_off[img];
     n = a.img_n[img];
     return (n + TILE_N - 1) / TILE_N;
 }
 
+// PLANES = 2: track length <= 100 (2S = lo + 256 hi, int32 keys, two accumulator
+// stages of 2 x 128 TMEM columns).  PLANES = 3: any track length up to 32767 (2S
+// in base-256 digits, int64 keys, one stage of 3 x 128 columns).
+template <int PLANES>
 __global__ void __launch_bounds__(KN_THREADS, 1)
-knn_tc_kernel(const __grid_constant__ CUtensorMap map_lo, const __grid_constant__ CUtensorMap map_hi,
-              const __grid_constant__ CUtensorMap map_b, KnnArgs a) {
+knn_tc_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_constant__ CUtensorMap map_p1,
+              const __grid_constant__ CUtensorMap map_p2, const __grid_constant__ CUtensorMap map_b,
+              KnnArgs a) {
+    using Key = typename std::conditional<PLANES == 2, int, long long>::type;
+    constexpr Key KBIG = PLANES == 2 ? (Key)INT_BIG : (Key)KEY_BIG64;
+    constexpr int ACC_STAGES = PLANES == 2 ? 2 : 1;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     KnnSmem& S = *reinterpret_cast<KnnSmem*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_units = a.m_tiles * a.n_img;
+    const int count = *a.count;
+    const int m_tiles = (count + TILE_M - 1) / TILE_M;
+    const int n_units = m_tiles * a.n_img;
+    if (n_units == 0) return;
+    const CUtensorMap* maps[3] = {&map_p0, &map_p1, &map_p2};
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < KN_STAGES; s++) {
@@ -232,16 +250,16 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_lo, const __grid_constant_
             for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
                 int img, mt, n;
                 int64_t off;
-                const int nt = unit_tiles(a, u, img, mt, off, n);
+                const int nt = unit_tiles(a, m_tiles, u, img, mt, off, n);
                 if (nt == 0) continue;
                 if (!first) {
                     mbar_wait(&S.a_empty, a_phase);
                     a_phase ^= 1;
                 }
                 first = 0;
-                mbar_expect_tx(&S.a_full, 2 * A_PLANE_BYTES);
-                tma_load_2d(S.a[0], &map_lo, &S.a_full, 0, mt * TILE_M);
-                tma_load_2d(S.a[1], &map_hi, &S.a_full, 0, mt * TILE_M);
+                mbar_expect_tx(&S.a_full, PLANES * A_PLANE_BYTES);
+#pragma unroll
+                for (int p = 0; p < PLANES; p++) tma_load_2d(S.a[p], maps[p], &S.a_full, 0, mt * TILE_M);
                 for (int j = 0; j < nt; j++) {
                     mbar_wait(&S.empty[stage], phase ^ 1);
                     mbar_expect_tx(&S.full[stage], B_TILE_BYTES);
@@ -255,11 +273,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_lo, const __grid_constant_
         if (lane == 0) {
             int stage = 0, acc = 0;
             uint32_t phase = 0, a_phase = 0, acc_phase = 0;
-            const uint32_t a_lo = smem_u32(S.a[0]), a_hi = smem_u32(S.a[1]);
             for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
                 int img, mt, n;
                 int64_t off;
-                const int nt = unit_tiles(a, u, img, mt, off, n);
+                const int nt = unit_tiles(a, m_tiles, u, img, mt, off, n);
                 if (nt == 0) continue;
                 mbar_wait(&S.a_full, a_phase);
                 a_phase ^= 1;
@@ -269,20 +286,18 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_lo, const __grid_constant_
                     mbar_wait(&S.full[stage], phase);
                     tc_fence_after();
                     const uint32_t b_addr = smem_u32(S.b[stage]);
-                    const uint32_t d_lo = tbase + (uint32_t)(acc * 256);
-                    const uint32_t d_hi = d_lo + 128;
 #pragma unroll
-                    for (int k = 0; k < KB / 32; k++) {
-                        umma_i8(d_lo, umma_desc_sw128(a_lo + 32 * k), umma_desc_sw128(b_addr + 32 * k), k > 0);
-                    }
+                    for (int p = 0; p < PLANES; p++) {
+                        const uint32_t d = tbase + (uint32_t)(acc * 256 + p * 128);
+                        const uint32_t ap = smem_u32(S.a[p]);
 #pragma unroll
-                    for (int k = 0; k < KB / 32; k++) {
-                        umma_i8(d_hi, umma_desc_sw128(a_hi + 32 * k), umma_desc_sw128(b_addr + 32 * k), k > 0);
+                        for (int k = 0; k < KB / 32; k++)
+                            umma_i8(d, umma_desc_sw128(ap + 32 * k), umma_desc_sw128(b_addr + 32 * k), k > 0);
                     }
                     umma_commit(&S.empty[stage]);     // B stage reusable once these MMAs retire
                     umma_commit(&S.t_full[acc]);      // accumulator ready for the epilogue
                     if (++stage == KN_STAGES) { stage = 0; phase ^= 1; }
-                    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                    if (++acc == ACC_STAGES) { acc = 0; acc_phase ^= 1; }
                 }
                 umma_commit(&S.a_empty);              // A planes reusable after this unit
             }
@@ -298,33 +313,33 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_lo, const __grid_constant_
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             int img, mt, n;
             int64_t off;
-            const int nt = unit_tiles(a, u, img, mt, off, n);
+            const int nt = unit_tiles(a, m_tiles, u, img, mt, off, n);
             const int grow = mt * TILE_M + row;
-            const int np = grow < a.M_pad ? a.n[grow] : 0;
+            const int np = grow < count ? a.n[grow] : 0;
             {
                 // stage the image's |f|^2 row in shared memory (broadcast reads per chunk)
-                const int slot = u / a.m_tiles;     // image slot of the unit (unit_tiles)
+                const int slot = u / m_tiles;       // image slot of the unit (unit_tiles)
                 const int4* src = reinterpret_cast<const int4*>(a.fn_pad + (int64_t)slot * a.fn_stride);
                 int4* dst = reinterpret_cast<int4*>(S.fvs);
                 for (int i = ew * 32 + lane; i < a.fn_stride / 4; i += EPI_WARPS * 32) dst[i] = __ldg(src + i);
                 asm volatile("bar.sync 1, %0;" ::"r"(EPI_WARPS * 32));
             }
             // running top-2 of this row over its column slice: k1 (best key), k2 (second
-            // smallest key value), best column = ibase + il.  Branch-free per score:
-            // two ops for the key, five for the update.
-            int k1 = INT_BIG, k2 = INT_BIG, il = 0, ibase = 0;
+            // smallest key value), best column = ibase + il.
+            Key k1 = KBIG, k2 = KBIG;
+            int il = 0, ibase = 0;
             for (int j = 0; j < nt; j++) {
                 mbar_wait_backoff(&S.t_full[acc], acc_phase);
                 tc_fence_after();
-                const uint32_t t_lo = tbase + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * 256 + half * EPI_COLS);
+                const uint32_t t0 = tbase + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * 256 + half * EPI_COLS);
                 const int cbase = j * TILE_N + half * EPI_COLS;
                 const int4* fp = reinterpret_cast<const int4*>(S.fvs + cbase);
                 const bool full = cbase + EPI_COLS <= n;
 #pragma unroll
                 for (int c0 = 0; c0 < EPI_COLS; c0 += 16) {
-                    uint32_t lo[16], hi[16];
-                    tmem_ld16(t_lo + c0, lo);
-                    tmem_ld16(t_lo + 128 + c0, hi);
+                    uint32_t pl[PLANES][16];
+#pragma unroll
+                    for (int p = 0; p < PLANES; p++) tmem_ld16(t0 + p * 128 + c0, pl[p]);
                     int fv[16];
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
@@ -332,55 +347,60 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_lo, const __grid_constant_
                         fv[4 * q] = f4.x; fv[4 * q + 1] = f4.y; fv[4 * q + 2] = f4.z; fv[4 * q + 3] = f4.w;
                     }
                     tmem_wait_ld();
-                    const int k1_in = k1;
-                    if (full) {
-                        // values only in the loop (three min/max per score); the
-                        // column of a new best is found afterwards, rarely
-                        int key[16];
+                    const Key k1_in = k1;
+                    const int lim = full ? 16 : n - (cbase + c0);
+                    Key key[16];
 #pragma unroll
-                        for (int c = 0; c < 16; c++) {
-                            key[c] = np * fv[c] - ((int)lo[c] + ((int)hi[c] << 8));
-                            k2 = min(k2, max(k1, key[c]));
-                            k1 = min(k1, key[c]);
+                    for (int c = 0; c < 16; c++) {
+                        if (PLANES == 2) {
+                            key[c] = (Key)(np * fv[c] - ((int)pl[0][c] + ((int)pl[1][c] << 8)));
+                        } else {
+                            key[c] = (Key)((long long)np * fv[c] -
+                                           ((long long)pl[0][c] + ((long long)pl[1][c] << 8) +
+                                            ((long long)pl[PLANES - 1][c] << 16)));
                         }
-                        if (k1 != k1_in) {
-#pragma unroll
-                            for (int c = 15; c >= 0; c--)
-                                if (key[c] == k1) il = c;     // lowest column at the best
-                        }
-                    } else {
-                        const int lim = n - (cbase + c0);
-#pragma unroll
-                        for (int c = 0; c < 16; c++) {
-                            const int key = c < lim ? np * fv[c] - ((int)lo[c] + ((int)hi[c] << 8)) : INT_BIG;
-                            k2 = min(k2, max(k1, key));
-                            if (key < k1) { k1 = key; il = c; }
-                        }
+                        if (!full && c >= lim) key[c] = KBIG;
                     }
-                    if (k1 != k1_in) ibase = cbase + c0;
+                    // values only in the loop (three min/max per score); the column of a
+                    // new best is found afterwards, rarely
+#pragma unroll
+                    for (int c = 0; c < 16; c++) {
+                        k2 = min(k2, max(k1, key[c]));
+                        k1 = min(k1, key[c]);
+                    }
+                    if (k1 != k1_in) {
+#pragma unroll
+                        for (int c = 15; c >= 0; c--)
+                            if (key[c] == k1) il = c;     // lowest column at the best
+                        ibase = cbase + c0;
+                    }
                 }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&S.t_empty[acc]);
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                if (++acc == ACC_STAGES) { acc = 0; acc_phase ^= 1; }
             }
-            int i1 = k1 == INT_BIG ? -1 : ibase + il;
+            int i1 = k1 == KBIG ? -1 : ibase + il;
             // merge the column slices of each row
-            S.merge_k1[half][row] = k1; S.merge_i1[half][row] = i1; S.merge_k2[half][row] = k2;
+            S.merge_k1[half][row] = k1 == KBIG ? KEY_BIG64 : (long long)k1;
+            S.merge_i1[half][row] = i1;
+            S.merge_k2[half][row] = k2 == KBIG ? KEY_BIG64 : (long long)k2;
             asm volatile("bar.sync 1, %0;" ::"r"(EPI_WARPS * 32));
             if (half == 0) {
+                long long b1 = S.merge_k1[0][row], b2 = S.merge_k2[0][row];
                 for (int h = 1; h < EPI_WARPS / 4; h++) {
-                    const int ok1 = S.merge_k1[h][row], oi1 = S.merge_i1[h][row], ok2 = S.merge_k2[h][row];
+                    const long long ok1 = S.merge_k1[h][row], ok2 = S.merge_k2[h][row];
+                    const int oi1 = S.merge_i1[h][row];
                     // best = min by (key, index); second = 2nd smallest key value
-                    const bool other_first = (ok1 < k1) || (ok1 == k1 && oi1 >= 0 && (i1 < 0 || oi1 < i1));
-                    const int hi_k = other_first ? k1 : ok1;
-                    if (other_first) { k1 = ok1; i1 = oi1; }
-                    k2 = min(hi_k, min(k2, ok2));
+                    const bool other_first = (ok1 < b1) || (ok1 == b1 && oi1 >= 0 && (i1 < 0 || oi1 < i1));
+                    const long long hi_k = other_first ? b1 : ok1;
+                    if (other_first) { b1 = ok1; i1 = oi1; }
+                    b2 = min(hi_k, min(b2, ok2));
                 }
-                const int slot = u / a.m_tiles;     // image slot of the unit (unit_tiles)
-                if (grow < a.M_pad) {
-                    const int64_t o = (int64_t)slot * a.M_pad + grow;
-                    a.out_k1[o] = k1; a.out_i1[o] = i1; a.out_k2[o] = k2;
+                const int slot = u / m_tiles;       // image slot of the unit (unit_tiles)
+                if (grow < count) {
+                    const int64_t o = (int64_t)slot * a.M_pad + a.rowmap[grow];
+                    a.out_k1[o] = b1; a.out_i1[o] = i1; a.out_k2[o] = b2;
                 }
             }
             asm volatile("bar.sync 1, %0;" ::"r"(EPI_WARPS * 32));
@@ -406,23 +426,52 @@ __global__ void fn_pad_kernel(const int32_t* __restrict__ fnorm, const int64_t* 
         out[(int64_t)s * stride + j] = j < n ? fnorm[off + j] : 0;
 }
 
+// Split the points into the short-track (n <= SHORT_N, two planes) and long-track
+// (three planes) subsets: a warp per point row claims a slot in its subset, writes
+// the row's digit planes there and the subset -> point row map.  Slot order inside
+// a subset is arbitrary (every row's top-2 is independent of its tile mates).
+constexpr int SHORT_N = 100;
 __global__ void digit_planes_kernel(const int32_t* __restrict__ S, const int32_t* __restrict__ n,
-                                    int64_t M, int64_t M_pad, uint8_t* __restrict__ lo,
-                                    uint8_t* __restrict__ hi, int32_t* __restrict__ npad) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= M_pad * 128) return;
-    const int64_t r = i >> 7;
-    const int v = r < M ? S[i] : 0;
-    // 2S = lo + 256 hi with lo = 2 (S mod 128), hi = S >> 7 (S <= 32767, n <= 128):
-    // the planes' GEMMs give 2 S.f directly
-    lo[i] = (uint8_t)((v & 127) << 1);
-    hi[i] = (uint8_t)(v >> 7);
-    if ((i & 127) == 0) npad[r] = r < M ? n[r] : 0;
+                                    int64_t M, int32_t* __restrict__ cnt,
+                                    uint8_t* __restrict__ s_lo, uint8_t* __restrict__ s_hi,
+                                    int32_t* __restrict__ s_n, int32_t* __restrict__ s_map,
+                                    uint8_t* __restrict__ l_p0, uint8_t* __restrict__ l_p1,
+                                    uint8_t* __restrict__ l_p2, int32_t* __restrict__ l_n,
+                                    int32_t* __restrict__ l_map) {
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= M) return;
+    const int nr = n[r];
+    const bool lng = nr > SHORT_N;
+    int pos = 0;
+    if (lane == 0) pos = atomicAdd(cnt + (lng ? 1 : 0), 1);
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    if (lane == 0) {
+        if (lng) { l_n[pos] = nr; l_map[pos] = (int32_t)r; }
+        else     { s_n[pos] = nr; s_map[pos] = (int32_t)r; }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const int k = lane + 32 * q;
+        const int v = S[r * 128 + k];
+        const int64_t o = (int64_t)pos * 128 + k;
+        if (!lng) {
+            // 2S = lo + 256 hi, lo = 2 (S mod 128), hi = S >> 7 (S <= 255 * 100)
+            s_lo[o] = (uint8_t)((v & 127) << 1);
+            s_hi[o] = (uint8_t)(v >> 7);
+        } else {
+            // 2S in base-256 digits (S <= 255 * 32767 < 2^23)
+            const int w = 2 * v;
+            l_p0[o] = (uint8_t)(w & 255);
+            l_p1[o] = (uint8_t)((w >> 8) & 255);
+            l_p2[o] = (uint8_t)(w >> 16);
+        }
+    }
 }
 
 // ratio test + one point per feature (localize.py:108-122, matching.py:82-103)
 struct DirectArgs {
-    const int32_t* n; const int64_t* SS; const int32_t* k1; const int32_t* i1; const int32_t* k2;
+    const int32_t* n; const int64_t* SS; const long long* k1; const int32_t* i1; const long long* k2;
     const int32_t* images; const int32_t* img_n;
     int32_t* win; const int64_t* win_off; int32_t* row_out; int32_t* fid_out; int32_t* cnt_out;
     int M, M_pad, n_img;
@@ -430,7 +479,7 @@ struct DirectArgs {
     double cap;
 };
 
-__device__ __forceinline__ long long exact_N(const DirectArgs& a, int s, int r, int32_t k) {
+__device__ __forceinline__ long long exact_N(const DirectArgs& a, int s, int r, long long k) {
     return (long long)a.n[r] * k + a.SS[r];
 }
 
@@ -439,8 +488,8 @@ __device__ __forceinline__ bool accepted(const DirectArgs& a, int s, int r, long
     const int i1 = a.i1[o];
     if (i1 < 0) return false;
     Nb = exact_N(a, s, r, a.k1[o]);
-    const int k2 = a.k2[o];
-    if (k2 == INT_BIG) return sqrt((double)Nb) / (double)a.n[r] < a.cap;
+    const long long k2 = a.k2[o];
+    if (k2 == KEY_BIG64) return sqrt((double)Nb) / (double)a.n[r] < a.cap;
     const long long Ns = exact_N(a, s, r, k2);
     return (__int128)a.q * a.q * Nb < (__int128)a.p * a.p * Ns;
 }
@@ -523,15 +572,16 @@ __global__ void knn_second_kernel(const uint8_t* __restrict__ desc, const int32_
                                   const int64_t* __restrict__ img_off, const int32_t* __restrict__ img_n,
                                   const int32_t* __restrict__ images, int n_img, int M, int M_pad,
                                   const int32_t* __restrict__ S, const int32_t* __restrict__ n,
-                                  const int32_t* __restrict__ k1, const int32_t* __restrict__ i1,
-                                  const int32_t* __restrict__ k2, int32_t* __restrict__ i2) {
+                                  const long long* __restrict__ k1, const int32_t* __restrict__ i1,
+                                  const long long* __restrict__ k2, int32_t* __restrict__ i2) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= n_img * M) return;
     const int s = warp / M, r = warp - s * M;
     const int64_t o = (int64_t)s * M_pad + r;
-    const int want = k2[o], best = i1[o];
+    const long long want = k2[o];
+    const int best = i1[o];
     if (lane == 0) i2[o] = -1;
-    if (best < 0 || want == INT_BIG) return;
+    if (best < 0 || want == KEY_BIG64) return;
     const int img = images[s];
     const int64_t off = img_off[img];
     const int nf = img_n[img];
@@ -545,7 +595,7 @@ __global__ void knn_second_kernel(const uint8_t* __restrict__ desc, const int32_
             long long dot = 0;
             for (int k = 0; k < 128; k++) dot += (long long)Sr[k] * d[k];
             const long long key = (long long)np * fnorm[off + f] - 2 * dot;
-            hit = (int32_t)key == want;
+            hit = key == want;
         }
         const unsigned b = __ballot_sync(0xffffffffu, hit);
         if (b) {
@@ -597,13 +647,16 @@ static int64_t fn_stride_of(int32_t max_n) {
 
 extern "C" size_t msfm_knn_workspace_bytes(int32_t n_points, int32_t n_images, int32_t max_n) {
     const int64_t M_pad = ((int64_t)n_points + TILE_M - 1) / TILE_M * TILE_M;
-    return aligned_bytes<uint8_t>(M_pad * 128) * 2 + aligned_bytes<int32_t>(M_pad) +
+    // short subset: 2 planes, long subset: 3 planes (each sized for every point),
+    // per-subset track lengths and row maps, 2 counters, the images' |f|^2 rows
+    return aligned_bytes<uint8_t>(M_pad * 128) * 5 + aligned_bytes<int32_t>(M_pad) * 4 +
+           aligned_bytes<int32_t>(2) +
            aligned_bytes<int32_t>((int64_t)(n_images > 0 ? n_images : 1) * fn_stride_of(max_n)) + 4096;
 }
 
 extern "C" int msfm_knn2_second_index(const msfm_bank* bank, int32_t n_points, const int32_t* d_S,
                                       const int32_t* d_n, int32_t n_images, const int32_t* d_images,
-                                      const int32_t* d_k1, const int32_t* d_i1, const int32_t* d_k2,
+                                      const int64_t* d_k1, const int32_t* d_i1, const int64_t* d_k2,
                                       int32_t* d_i2, void* stream) {
     if (!bank || n_points < 0 || n_images < 0) {
         set_error("msfm_knn2_second_index: bad arguments");
@@ -614,7 +667,8 @@ extern "C" int msfm_knn2_second_index(const msfm_bank* bank, int32_t n_points, c
     const int64_t warps = (int64_t)n_images * n_points;
     knn_second_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         bank->d_desc, bank->d_norm2, bank->d_img_off, bank->d_img_n, d_images, n_images, n_points,
-        M_pad, d_S, d_n, d_k1, d_i1, d_k2, d_i2);
+        M_pad, d_S, d_n, reinterpret_cast<const long long*>(d_k1), d_i1,
+        reinterpret_cast<const long long*>(d_k2), d_i2);
     MSFM_LAUNCH_CHECK();
     count_launches(1);
     return MSFM_OK;
@@ -658,7 +712,7 @@ extern "C" int msfm_gather_3d2d(const int32_t* d_corr_row, const int32_t* d_corr
 
 extern "C" int msfm_direct_3d2d(const msfm_bank* bank, int32_t n_points, const int32_t* d_n,
                                 const int64_t* d_SS, int32_t n_images, const int32_t* d_images,
-                                const int32_t* d_k1, const int32_t* d_i1, const int32_t* d_k2,
+                                const int64_t* d_k1, const int32_t* d_i1, const int64_t* d_k2,
                                 int64_t ratio_p, int64_t ratio_q, double single_cap,
                                 int32_t* d_win, const int64_t* d_win_off, int32_t* d_corr_row,
                                 int32_t* d_corr_fid, int32_t* d_corr_n, void* stream) {
@@ -670,7 +724,8 @@ extern "C" int msfm_direct_3d2d(const msfm_bank* bank, int32_t n_points, const i
     if (n_images == 0) return MSFM_OK;
     cudaStream_t st = (cudaStream_t)stream;
     DirectArgs a;
-    a.n = d_n; a.SS = d_SS; a.k1 = d_k1; a.i1 = d_i1; a.k2 = d_k2;
+    a.n = d_n; a.SS = d_SS; a.k1 = reinterpret_cast<const long long*>(d_k1); a.i1 = d_i1;
+    a.k2 = reinterpret_cast<const long long*>(d_k2);
     a.images = d_images; a.img_n = bank->d_img_n;
     a.win = d_win; a.win_off = d_win_off; a.row_out = d_corr_row; a.fid_out = d_corr_fid;
     a.cnt_out = d_corr_n;
@@ -692,15 +747,16 @@ extern "C" int msfm_direct_3d2d(const msfm_bank* bank, int32_t n_points, const i
 
 extern "C" int msfm_knn2_tracks(const msfm_bank* bank, int32_t n_points, const int32_t* d_S,
                                 const int32_t* d_n, int32_t n_images, const int32_t* d_images,
-                                int32_t max_track, int32_t max_n, int32_t* d_k1, int32_t* d_i1,
-                                int32_t* d_k2, void* d_workspace, size_t workspace_bytes,
+                                int32_t max_track, int32_t max_n, int64_t* d_k1, int32_t* d_i1,
+                                int64_t* d_k2, void* d_workspace, size_t workspace_bytes,
                                 void* stream) {
     if (!bank || n_points < 0 || n_images < 0 || (n_points > 0 && (!d_S || !d_n))) {
         set_error("msfm_knn2_tracks: bad arguments");
         return MSFM_EINVAL;
     }
-    if (max_track > 100) {
-        set_error("msfm_knn2_tracks: track length %d > 100 overflows the int32 rank key", max_track);
+    if (max_track > 32767) {
+        set_error("msfm_knn2_tracks: track length %d > 32767 (2S must fit three digit planes)",
+                  max_track);
         return MSFM_EINVAL;
     }
     if (n_points == 0 || n_images == 0) return MSFM_OK;
@@ -711,29 +767,39 @@ extern "C" int msfm_knn2_tracks(const msfm_bank* bank, int32_t n_points, const i
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t M_pad = ((int64_t)n_points + TILE_M - 1) / TILE_M * TILE_M;
     Arena ar(d_workspace, workspace_bytes);
-    uint8_t* lo = ar.take<uint8_t>(M_pad * 128);
-    uint8_t* hi = ar.take<uint8_t>(M_pad * 128);
-    int32_t* npad = ar.take<int32_t>(M_pad);
+    uint8_t* s_lo = ar.take<uint8_t>(M_pad * 128);
+    uint8_t* s_hi = ar.take<uint8_t>(M_pad * 128);
+    uint8_t* l_p0 = ar.take<uint8_t>(M_pad * 128);
+    uint8_t* l_p1 = ar.take<uint8_t>(M_pad * 128);
+    uint8_t* l_p2 = ar.take<uint8_t>(M_pad * 128);
+    int32_t* s_n = ar.take<int32_t>(M_pad);
+    int32_t* s_map = ar.take<int32_t>(M_pad);
+    int32_t* l_n = ar.take<int32_t>(M_pad);
+    int32_t* l_map = ar.take<int32_t>(M_pad);
+    int32_t* cnt = ar.take<int32_t>(2);
     const int64_t fstride = fn_stride_of(max_n);
     int32_t* fpad = ar.take<int32_t>((int64_t)n_images * fstride);
     fn_pad_kernel<<<dim3(8, n_images), 256, 0, st>>>(bank->d_norm2, bank->d_img_off, bank->d_img_n,
                                                     d_images, (int)fstride, fpad);
     MSFM_LAUNCH_CHECK();
-    digit_planes_kernel<<<(unsigned)((M_pad * 128 + 255) / 256), 256, 0, st>>>(d_S, d_n, n_points,
-                                                                             M_pad, lo, hi, npad);
+    MSFM_CUDA_TRY(cudaMemsetAsync(cnt, 0, 2 * sizeof(int32_t), st));
+    digit_planes_kernel<<<(unsigned)(((int64_t)n_points * 32 + 255) / 256), 256, 0, st>>>(
+        d_S, d_n, n_points, cnt, s_lo, s_hi, s_n, s_map, l_p0, l_p1, l_p2, l_n, l_map);
     MSFM_LAUNCH_CHECK();
     const int64_t n_total = bank->n_total;
     if (n_total <= 0) {
         set_error("msfm_knn2_tracks: empty feature bank");
         return MSFM_EINVAL;
     }
-    CUtensorMap mlo, mhi, mb;
+    CUtensorMap ms0, ms1, ml0, ml1, ml2, mb;
     int rc;
-    if ((rc = make_rows128_map(&mlo, lo, M_pad))) return rc;
-    if ((rc = make_rows128_map(&mhi, hi, M_pad))) return rc;
+    if ((rc = make_rows128_map(&ms0, s_lo, M_pad))) return rc;
+    if ((rc = make_rows128_map(&ms1, s_hi, M_pad))) return rc;
+    if ((rc = make_rows128_map(&ml0, l_p0, M_pad))) return rc;
+    if ((rc = make_rows128_map(&ml1, l_p1, M_pad))) return rc;
+    if ((rc = make_rows128_map(&ml2, l_p2, M_pad))) return rc;
     if ((rc = make_rows128_map(&mb, bank->d_desc, n_total))) return rc;
     KnnArgs a;
-    a.n = npad;
     a.fnorm = bank->d_norm2;
     a.fn_pad = fpad;
     a.fn_stride = (int)fstride;
@@ -741,31 +807,42 @@ extern "C" int msfm_knn2_tracks(const msfm_bank* bank, int32_t n_points, const i
     a.img_n = bank->d_img_n;
     a.images = d_images;
     a.n_img = n_images;
-    a.m_tiles = (int)(M_pad / TILE_M);
     a.M = n_points;
     a.M_pad = (int)M_pad;
-    a.out_k1 = d_k1;
+    a.out_k1 = reinterpret_cast<long long*>(d_k1);
     a.out_i1 = d_i1;
-    a.out_k2 = d_k2;
+    a.out_k2 = reinterpret_cast<long long*>(d_k2);
     const size_t smem = sizeof(KnnSmem) + (size_t)fstride * sizeof(int32_t) + 1024;
     if (smem > 227 * 1024) {
         set_error("msfm_knn2_tracks: %d features per image exceed the shared-memory |f|^2 row",
                   max_n);
         return MSFM_EINVAL;
     }
-    MSFM_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    MSFM_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+    MSFM_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int units = a.m_tiles * n_images;
-    const int grid = units < nsm ? units : nsm;
+    // the subsets' sizes stay on the device: each launch reads its count, grids are
+    // sized for the worst case (persistent CTAs, surplus CTAs exit at once)
+    const int64_t units = (M_pad / TILE_M) * n_images;
+    const int grid = (int)(units < nsm ? units : nsm);
     {
         ProfScope ps("knn_tc_kernel", st);
-        knn_tc_kernel<<<grid, KN_THREADS, smem, st>>>(mlo, mhi, mb, a);
+        a.count = cnt; a.rowmap = s_map; a.n = s_n;
+        knn_tc_kernel<2><<<grid, KN_THREADS, smem, st>>>(ms0, ms1, ms1, mb, a);
     }
     MSFM_LAUNCH_CHECK();
-    count_launches(3);
+    if (max_track > SHORT_N) {
+        ProfScope ps("knn_tc_kernel_long", st);
+        a.count = cnt + 1; a.rowmap = l_map; a.n = l_n;
+        knn_tc_kernel<3><<<grid, KN_THREADS, smem, st>>>(ml0, ml1, ml2, mb, a);
+        MSFM_LAUNCH_CHECK();
+        count_launches(1);
+    }
+    count_launches(4);
     return MSFM_OK;
 }
 

@@ -20,7 +20,7 @@ from .types import LocalizationResult, SetCover
 RATIO_UNGUIDED = 0.6     # matching.py:21
 SINGLE_CANDIDATE_CAP = 45.0
 MIN_CORRESPONDENCES = 16  # localize.py:30
-INT_BIG = 0x7FFFFFFF
+KEY_BIG = 0x7FFFFFFFFFFFFFFF      # no second neighbour (msfm_knn2_tracks)
 
 
 def ratio_fraction(ratio: float):
@@ -76,7 +76,7 @@ class DeviceKnn:
         n = pts.n.astype(np.int64)[None, :]
         SS = pts.SS[None, :]
         Nb = n * k1 + SS
-        Ns = np.where(k2 == INT_BIG, -1, n * k2 + SS)
+        Ns = np.where(k2 == KEY_BIG, -1, n * np.where(k2 == KEY_BIG, 0, k2) + SS)
         return i1, Nb, Ns
 
     def host(self, pts: PointSet, s: int):
@@ -88,7 +88,7 @@ class DeviceKnn:
         n = pts.n.astype(np.int64)
         SS = pts.SS
         Nb = n * k1 + SS
-        Ns = np.where(k2 == INT_BIG, -1, n * k2 + SS)
+        Ns = np.where(k2 == KEY_BIG, -1, n * np.where(k2 == KEY_BIG, 0, k2) + SS)
         return i1, Nb, Ns
 
 
@@ -112,8 +112,8 @@ def knn2_tracks(bank: FeatureBank, pts: PointSet, image_ids, stream=None,
         # (k1, i1, k2) rows of these images inside larger tables (row views)
         k1, i1, k2 = into
     else:
-        k1 = torch.empty((max(len(slots), 1), M_pad), dtype=torch.int32, device=dev)
-        i1 = torch.empty_like(k1)
+        k1 = torch.empty((max(len(slots), 1), M_pad), dtype=torch.int64, device=dev)
+        i1 = torch.empty((max(len(slots), 1), M_pad), dtype=torch.int32, device=dev)
         k2 = torch.empty_like(k1)
     cnt = bank.counts if counts is None else np.asarray(counts, np.int64)
     max_feat = int(cnt[slots].max()) if len(slots) else 0
@@ -131,7 +131,7 @@ def knn2_tracks(bank: FeatureBank, pts: PointSet, image_ids, stream=None,
                                     _lib.stream_handle(stream)), "msfm_knn2_tracks")
     out = DeviceKnn(k1, i1, k2, M_pad, keep=(ws, d_slots, d_cnt))
     if second:
-        out.i2 = torch.empty_like(k1)
+        out.i2 = torch.empty_like(i1)
         _lib.check(lib.msfm_knn2_second_index(ctypes.byref(b), M, _lib.ptr(dS), _lib.ptr(dn),
                                               len(slots), _lib.ptr(d_slots), _lib.ptr(k1),
                                               _lib.ptr(i1), _lib.ptr(k2), _lib.ptr(out.i2),
@@ -155,8 +155,8 @@ def knn2_tracks_staged(bank: FeatureBank, pts: PointSet, image_ids, device_point
     S = len(ids)
     assert list(bank.slots(ids)) == list(range(S)), "image_ids must be the bank's images in order"
     M_pad = (len(pts.n) + 127) // 128 * 128
-    k1 = torch.empty((max(S, 1), M_pad), dtype=torch.int32, device=dev)
-    i1 = torch.empty_like(k1)
+    k1 = torch.empty((max(S, 1), M_pad), dtype=torch.int64, device=dev)
+    i1 = torch.empty((max(S, 1), M_pad), dtype=torch.int32, device=dev)
     k2 = torch.empty_like(k1)
     cs = bank.__dict__.get("_h2d_stream")
     if cs is None:

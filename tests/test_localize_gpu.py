@@ -9,7 +9,7 @@ from oracle import localize as ol
 pytestmark = pytest.mark.gpu
 
 
-def _random_case(rng, M, sizes, max_n=10, dup=False):
+def _random_case(rng, M, sizes, max_n=10, dup=False, any_sum=False, min_n=1):
     from paper_1512_06235_b200.types import FeatureSet
     sets = {}
     for i, nf in enumerate(sizes):
@@ -20,22 +20,31 @@ def _random_case(rng, M, sizes, max_n=10, dup=False):
                              xy=rng.uniform(0, 400, size=(nf, 2)).astype(np.float32),
                              scale=np.ones(nf, np.float32), orientation=np.zeros(nf, np.float32),
                              descriptors=desc)
-    n = rng.integers(1, max_n + 1, size=M).astype(np.int32)
-    S = (rng.integers(0, 256, size=(M, 128)) * n[:, None]).astype(np.int32)
+    n = rng.integers(min_n, max_n + 1, size=M).astype(np.int32)
+    if any_sum:
+        # any track sum a track of n uint8 rows can have (every digit of 2S exercised)
+        S = (rng.random((M, 128)) * (255 * n[:, None] + 1)).astype(np.int64).astype(np.int32)
+    else:
+        S = (rng.integers(0, 256, size=(M, 128)) * n[:, None]).astype(np.int32)
     if dup and M > 3:
         S[2] = S[0] if n[2] == n[0] else S[2]
     return sets, S, n
 
 
-@pytest.mark.parametrize("M,sizes,max_n", [(1, [1], 1), (5, [3, 1, 0, 130], 4), (128, [128], 10),
-                                           (300, [257, 1000, 5], 10), (1000, [2000, 129], 100),
-                                           (200, [16000, 31], 12)])
-def test_knn_topk_matches_exact_oracle(M, sizes, max_n):
+@pytest.mark.parametrize("M,sizes,max_n,any_sum,min_n",
+                         [(1, [1], 1, False, 1), (5, [3, 1, 0, 130], 4, False, 1),
+                          (128, [128], 10, False, 1), (300, [257, 1000, 5], 10, False, 1),
+                          (1000, [2000, 129], 100, False, 1), (200, [16000, 31], 12, False, 1),
+                          # long tracks (C5's coarse model): three digit planes, int64 keys,
+                          # mixed with short ones in the same call
+                          (700, [3000, 64], 3000, True, 1), (300, [1500], 32767, True, 101),
+                          (257, [16000], 600, True, 90)])
+def test_knn_topk_matches_exact_oracle(M, sizes, max_n, any_sum, min_n):
     from paper_1512_06235_b200.bank import FeatureBank
     from paper_1512_06235_b200.localize import PointSet, knn2_tracks
 
     rng = np.random.default_rng(M + len(sizes))
-    sets, S, n = _random_case(rng, M, sizes, max_n, dup=True)
+    sets, S, n = _random_case(rng, M, sizes, max_n, dup=True, any_sum=any_sum, min_n=min_n)
     bank = FeatureBank(sets)
     pts = PointSet(S=S, n=n, ids=np.arange(M))
     imgs = [i for i in sets]
@@ -50,6 +59,13 @@ def test_knn_topk_matches_exact_oracle(M, sizes, max_n):
         np.testing.assert_array_equal(idx, oi)
         np.testing.assert_array_equal(nb, onb)
         np.testing.assert_array_equal(ns, ons)
+    if max_n > 100:
+        # the direct 3D-2D search on long tracks (int64 keys end to end)
+        from paper_1512_06235_b200.localize import direct_search
+        big = [i for i in imgs if len(sets[i].descriptors) > 1]
+        corr = direct_search(bank, pts, big)
+        for c, i in zip(corr, big):
+            np.testing.assert_array_equal(c, ol.direct_3d2d(np.arange(M), S, n, sets[i].descriptors))
 
 
 @pytest.mark.parametrize("name", ["localize_holdout.npz", "localize_c2mini.npz"])
