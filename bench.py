@@ -684,38 +684,50 @@ def run_localization(args, dev, world=1, rank=0):
     from paper_1512_06235_b200 import _lib, scenes
     from paper_1512_06235_b200.bank import FeatureBank, HostBank
     from paper_1512_06235_b200.localize import (PointSet, direct_search, gather_pnp_inputs,
-                                                knn2_tracks, knn2_tracks_staged, upload_points)
+                                                knn2_tracks, knn2_tracks_staged, track_sums_device)
     from paper_1512_06235_b200.pnp import pnp_batch_flat
 
     scene, snap, all_queries = build_localization()
     queries = all_queries[rank::world]
-    S, n = scenes.track_sums(scene, snap)
-    pts = PointSet(S=S, n=n, ids=np.arange(len(S)))
     host = HostBank({q: scene.feature_sets[q] for q in queries})
     Ks = [scene.cameras[q].K for q in queries]
+    # the coarse model's tracks as a CSR over a bank of the registered images: the
+    # query points' exact track sums (K7, mean_descriptor localize.py:51-59) are
+    # computed on the device inside every step
+    reg = [int(i) for i in snap.registered]
+    reg_host = HostBank({i: scene.feature_sets[i] for i in reg})
+    reg_bank = FeatureBank(host=reg_host, device=dev)
+    slot_of = {i: k for k, i in enumerate(reg_host.image_ids)}
+    track_row = (reg_host.offsets[[slot_of[int(i)] for i in snap.track_img]]
+                 + snap.track_fid).astype(np.int64)
+    n = np.diff(snap.track_ptr).astype(np.int32)
+    M = len(n)
 
-    def step(bank, dp, d_xyz, knn=None):
+    def points(rbank):
+        dS, dn, dSS = track_sums_device(rbank, snap.track_ptr, track_row)
+        return PointSet(S=None, n=n, ids=np.arange(M), dev=(dS, dn, dSS))
+
+    def step(bank, pts, d_xyz, knn=None):
         # device-resident flat correspondences: image k owns [off[k], off[k+1]); the
         # gate of localize.py:203 (> 16) selects the images that go to PnP, and their
         # 3D-2D pairs are gathered on the device
-        corr = direct_search(bank, pts, queries, device_points=dp, to_host=False, knn=knn)
+        corr = direct_search(bank, pts, queries, to_host=False, knn=knn)
         X, uv, toff, todo = gather_pnp_inputs(bank, corr, queries, d_xyz)
         res = pnp_batch_flat(X, uv, toff, [Ks[k] for k in todo], [queries[k] for k in todo],
                              device=dev)
         return toff, res
 
     bank = FeatureBank(host=host, device=dev)
-    dp = upload_points(pts, dev)
     d_xyz = torch.from_numpy(snap.point_xyz).to(dev)
     for _ in range(args.warmup):
-        corrs, res = step(bank, dp, d_xyz)
+        corrs, res = step(bank, points(reg_bank), d_xyz)
     torch.cuda.synchronize()
     if world > 1:
         tdist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
-        corrs, res = step(bank, dp, d_xyz)
+        corrs, res = step(bank, points(reg_bank), d_xyz)
     e1.record()
     torch.cuda.synchronize()
     tt = torch.tensor([e0.elapsed_time(e1) / 1e3 / args.steps], device=dev)
@@ -726,13 +738,13 @@ def run_localization(args, dev, world=1, rank=0):
     for r in res:
         status[r.status] = status.get(r.status, 0) + 1
     # roofline of the kNN kernel: 2 planes x 2*M*N*128 int8 ops vs 2x measured bf16 (int8 rate)
+    pts = points(reg_bank)
     _lib.profile_enable(True)
-    knn2_tracks(bank, pts, queries, device_points=dp)
+    knn2_tracks(bank, pts, queries)
     torch.cuda.synchronize()
     k_ms, k_n = _lib.profile_read("knn_tc_kernel")
     _lib.profile_enable(False)
     N_feat = int(sum(len(scene.feature_sets[q]) for q in queries))
-    M = len(S)
     ops_alg = 2.0 * M * N_feat * 128
     ops_hw = 2.0 * ops_alg
     peak, peak_kind = None, None
@@ -756,10 +768,12 @@ def run_localization(args, dev, world=1, rank=0):
     for i in range(args.warmup + args.steps):
         torch.cuda.synchronize()
         t1 = time.perf_counter()
+        # the registered images' rows go up and their tracks are summed on the device;
         # the query bank goes up in eight ranges, each range's kNN starting as it lands
-        dp2 = upload_points(pts, dev)
-        knn = knn2_tracks_staged(b2, pts, queries, dp2)
-        step(b2, dp2, pin_xyz.to(dev, non_blocking=True), knn=knn)
+        reg_bank.refill()
+        p2 = points(reg_bank)
+        knn = knn2_tracks_staged(b2, p2, queries, p2.dev)
+        step(b2, p2, pin_xyz.to(dev, non_blocking=True), knn=knn)
         torch.cuda.synchronize()
         if i >= args.warmup:
             e2e.append(time.perf_counter() - t1)
@@ -780,7 +794,8 @@ def run_localization(args, dev, world=1, rank=0):
            "value": len(all_queries) / dt, "unit": "images/s",
            "ms_per_step": dt * 1e3, "status_counts": status,
            "e2e": {"value": len(all_queries) / e2e_s, "unit": "images/s",
-                   "h2d_bytes_per_step": int(host.nbytes + S.nbytes + n.nbytes + 8 * M + 24 * M),
+                   "h2d_bytes_per_step": int(host.nbytes + reg_host.nbytes + 8 * (M + 1)
+                                             + 8 * len(track_row) + 24 * M),
                    "d2h_bytes_per_step": int(4 * len(queries) + 13 * 8 * len(res) +
                                              sum(r.mask.nbytes for r in res if r.mask is not None))},
            "roofline": {"bound": "tensor", "kernel": "knn_tc_kernel", "achieved": ach,

@@ -278,6 +278,14 @@ int msfm_knn2_tracks(const msfm_bank* bank, int32_t n_points, const int32_t* d_S
                      int32_t max_track, int32_t max_image_features, int64_t* d_k1, int32_t* d_i1,
                      int64_t* d_k2, void* d_workspace, size_t workspace_bytes, void* stream);
 
+/* K7 track sums (mean_descriptor localize.py:51-59 in exact integer form, the
+ * query points of msfm_knn2_tracks): point p's track is bank rows
+ * d_track_row[d_track_ptr[p] .. d_track_ptr[p+1]); outputs S [n_points][128] int32
+ * (sum of the u8 rows), n [n_points] track lengths, SS [n_points] = |S|^2 int64. */
+int msfm_track_sums(const msfm_bank* bank, int64_t n_points, const int64_t* d_track_ptr,
+                    const int64_t* d_track_row, int32_t* d_S, int32_t* d_n, int64_t* d_SS,
+                    void* stream);
+
 /* Index of the second neighbour of msfm_knn2_tracks' output (the lowest feature
  * index other than i1 whose key equals k2, descriptors.py:61-63), -1 when there
  * is none: d_i2 [n_images][n_points rounded up to 128]. */

@@ -90,6 +90,8 @@ _SIGS = {
                                         ctypes.c_size_t, VP]),
     "msfm_knn2_second_index": (ctypes.c_int, [ctypes.POINTER(Bank), ctypes.c_int32, VP, VP,
                                               ctypes.c_int32, VP, VP, VP, VP, VP, VP]),
+    "msfm_track_sums": (ctypes.c_int, [ctypes.POINTER(Bank), ctypes.c_int64, VP, VP, VP, VP, VP,
+                                       VP]),
     "msfm_knn2_float": (ctypes.c_int, [VP, ctypes.c_int64, VP, ctypes.c_int64, ctypes.c_int32,
                                        VP, VP, VP]),
     "msfm_gather_3d2d": (ctypes.c_int, [VP, VP, ctypes.c_int32, ctypes.c_int32, VP, VP, VP, VP,

@@ -912,3 +912,53 @@ extern "C" int msfm_knn2_float(const float* d_q, int64_t n_queries, const float*
     count_launches(1);
     return MSFM_OK;
 }
+
+// ---------------------------------------------------------------------------
+// K7 track sums (mean_descriptor, localize.py:51-59, in its exact integer form):
+// one warp per point, lane l owns descriptor bytes [4l, 4l+4); S[p] = sum over the
+// point's track (CSR rows of bank features) of the u8 rows, n[p] = track length,
+// SS[p] = |S[p]|^2 in int64.  Coalesced 128-B row reads, no atomics.
+namespace msfm {
+namespace k7 {
+__global__ void __launch_bounds__(256) track_sum_kernel(const uint8_t* __restrict__ desc,
+                                                        const int64_t* __restrict__ ptr,
+                                                        const int64_t* __restrict__ row, int64_t M,
+                                                        int32_t* __restrict__ S, int32_t* __restrict__ n,
+                                                        int64_t* __restrict__ SS) {
+    const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (p >= M) return;
+    const int64_t a = ptr[p], b = ptr[p + 1];
+    int s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    for (int64_t o = a; o < b; o++) {
+        const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(desc + row[o] * 128) + lane);
+        s0 += w & 255; s1 += (w >> 8) & 255; s2 += (w >> 16) & 255; s3 += w >> 24;
+    }
+    reinterpret_cast<int4*>(S + p * 128)[lane] = make_int4(s0, s1, s2, s3);
+    long long q = (long long)s0 * s0 + (long long)s1 * s1 + (long long)s2 * s2 + (long long)s3 * s3;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    if (lane == 0) {
+        n[p] = (int32_t)(b - a);
+        SS[p] = q;
+    }
+}
+}  // namespace k7
+}  // namespace msfm
+
+extern "C" int msfm_track_sums(const msfm_bank* bank, int64_t n_points, const int64_t* d_track_ptr,
+                               const int64_t* d_track_row, int32_t* d_S, int32_t* d_n,
+                               int64_t* d_SS, void* stream) {
+    if (!bank || n_points < 0 || (n_points > 0 && (!d_track_ptr || !d_track_row || !d_S || !d_n ||
+                                                   !d_SS))) {
+        set_error("msfm_track_sums: bad arguments");
+        return MSFM_EINVAL;
+    }
+    if (n_points == 0) return MSFM_OK;
+    const int64_t threads = n_points * 32;
+    msfm::k7::track_sum_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        bank->d_desc, d_track_ptr, d_track_row, n_points, d_S, d_n, d_SS);
+    MSFM_LAUNCH_CHECK();
+    count_launches(1);
+    return MSFM_OK;
+}

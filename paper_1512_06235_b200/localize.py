@@ -30,21 +30,50 @@ def ratio_fraction(ratio: float):
 
 @dataclass
 class PointSet:
-    """Exact query points: track sums S (M,128) int32, lengths n (M,), ids."""
+    """Exact query points: track sums S (M,128) int32, lengths n (M,), ids.
+    ``dev``: (S, n, |S|^2) already on the device (track_sums_device); S is then
+    None on the host until someone asks for it."""
 
     S: np.ndarray
     n: np.ndarray
     ids: np.ndarray
+    dev: tuple = None
 
     @property
     def SS(self) -> np.ndarray:
         """|S|^2 per point (int64), computed once."""
         ss = self.__dict__.get("_ss")
-        if ss is None or len(ss) != len(self.S):
-            S = self.S.astype(np.int64)
-            ss = (S * S).sum(1)
+        if ss is None or len(ss) != len(self.n):
+            if self.S is None:
+                ss = self.dev[2][:len(self.n)].cpu().numpy().astype(np.int64)
+            else:
+                S = self.S.astype(np.int64)
+                ss = (S * S).sum(1)
             self.__dict__["_ss"] = ss
         return ss
+
+
+def track_sums_device(bank: FeatureBank, track_ptr, track_row, stream=None):
+    """K7 (mean_descriptor localize.py:51-59, exact integer form) on the device:
+    point p's track is bank rows track_row[track_ptr[p]:track_ptr[p+1]].  Returns
+    (S int32 (M,128), n int32 (M,), |S|^2 int64 (M,)) device tensors."""
+    import torch
+
+    lib = _lib.load()
+    dev = bank.device
+    ptr = np.ascontiguousarray(track_ptr, np.int64)
+    M = len(ptr) - 1
+    d_ptr = _lib.h2d(ptr, dev)
+    d_row = _lib.h2d(np.ascontiguousarray(track_row, np.int64) if len(track_row) else
+                     np.zeros(1, np.int64), dev)
+    dS = torch.empty((max(M, 1), 128), dtype=torch.int32, device=dev)
+    dn = torch.empty(max(M, 1), dtype=torch.int32, device=dev)
+    dSS = torch.empty(max(M, 1), dtype=torch.int64, device=dev)
+    b = bank.cstruct()
+    _lib.check(lib.msfm_track_sums(ctypes.byref(b), M, _lib.ptr(d_ptr), _lib.ptr(d_row),
+                                   _lib.ptr(dS), _lib.ptr(dn), _lib.ptr(dSS),
+                                   _lib.stream_handle(stream)), "msfm_track_sums")
+    return dS, dn, dSS
 
 
 def points_from_snapshot(scene_sets, snap, ids=None) -> PointSet:
@@ -189,6 +218,8 @@ def upload_points(pts: PointSet, dev):
     PointSet, so repeated uploads are three async copies."""
     import torch
 
+    if pts.dev is not None:
+        return pts.dev
     pinned = pts.__dict__.get("_pinned")
     if pinned is None or pinned[0] is not pts.S:
         M = len(pts.n)
@@ -398,22 +429,30 @@ def compute_set_cover(model, k: int = SET_COVER_K) -> SetCover:
 
 
 def model_points(model, feature_store, point_ids) -> PointSet:
-    """Exact track sums of the listed points (mean_descriptor, localize.py:51-59)."""
+    """Exact track sums of the listed points (mean_descriptor, localize.py:51-59):
+    the tracks flattened to a CSR over a device bank of their images, summed by
+    the K7 kernel (msfm_track_sums) on the device."""
+    from itertools import chain
+
     pids = np.asarray(sorted(point_ids), dtype=np.int64)
-    S = np.zeros((len(pids), 128), dtype=np.int32)
-    n = np.zeros(len(pids), dtype=np.int32)
-    by_img: dict = {}
-    for r, p in enumerate(pids):
-        tr = model.points[int(p)].track
-        n[r] = len(tr)
-        for i, f in tr.items():
-            by_img.setdefault(i, ([], []))
-            by_img[i][0].append(r)
-            by_img[i][1].append(f)
-    for i, (rows, fids) in by_img.items():
-        d = np.asarray(feature_store.sets[i].descriptors)[np.asarray(fids)].astype(np.int32)
-        np.add.at(S, np.asarray(rows), d)
-    return PointSet(S=S, n=n, ids=pids)
+    tracks = [model.points[int(p)].track for p in pids]
+    n = np.fromiter((len(t) for t in tracks), np.int64, len(tracks))
+    ptr = np.zeros(len(pids) + 1, np.int64)
+    np.cumsum(n, out=ptr[1:])
+    total = int(ptr[-1])
+    imgs = np.fromiter(chain.from_iterable(t.keys() for t in tracks), np.int64, total)
+    fids = np.fromiter(chain.from_iterable(t.values() for t in tracks), np.int64, total)
+    used = sorted(set(imgs.tolist()))
+    bank = FeatureBank({int(i): feature_store.sets[int(i)] for i in used}) if used else None
+    if bank is None:
+        return PointSet(S=np.zeros((len(pids), 128), np.int32), n=n.astype(np.int32), ids=pids)
+    slot = np.array([bank.index_of[int(i)] for i in used], np.int64)
+    lut = dict(zip(used, bank.offsets[slot].tolist()))
+    base = np.fromiter((lut[i] for i in imgs.tolist()), np.int64, total)
+    dS, dn, dSS = track_sums_device(bank, ptr, base + fids)
+    pts = PointSet(S=None, n=n.astype(np.int32), ids=pids, dev=(dS, dn, dSS))
+    pts.__dict__["_track_bank"] = bank        # keeps the rows alive with the sums
+    return pts
 
 
 def direct_3d2d_search(model, point_ids, image_fs, feature_store, *, ratio=RATIO_UNGUIDED,

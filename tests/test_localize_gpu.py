@@ -249,3 +249,33 @@ def test_localize_all_forced_set_cover_equals_reference():
             np.testing.assert_allclose(r.pose.R, z[f"forced_q{q}_R"], atol=1e-6)
             np.testing.assert_allclose(r.pose.t, z[f"forced_q{q}_t"], atol=1e-6, rtol=1e-6)
             assert r.inliers == int(z[f"forced_q{q}_inliers"])
+
+
+def test_track_sums_device_equals_host():
+    """K7 (mean_descriptor localize.py:51-59 in exact integers): device sums over a
+    track CSR equal numpy's, incl. long tracks, a single-view and an empty track;
+    model_points (the drop-ins' path) equals the harness's host sums."""
+    from paper_1512_06235_b200 import scenes
+    from paper_1512_06235_b200.bank import FeatureBank
+    from paper_1512_06235_b200.localize import model_points, track_sums_device
+
+    rng = np.random.default_rng(5)
+    sets, _, _ = _random_case(rng, 1, [3000, 17, 900])
+    bank = FeatureBank(sets)
+    lens = np.array([0, 1, 7, 150, 2999, 3], np.int64)
+    ptr = np.zeros(len(lens) + 1, np.int64)
+    np.cumsum(lens, out=ptr[1:])
+    rows = rng.integers(0, bank.n_total, size=int(ptr[-1]))
+    dS, dn, dSS = track_sums_device(bank, ptr, rows)
+    D = np.concatenate([sets[i].descriptors for i in sorted(sets)]).astype(np.int64)
+    want = np.stack([D[rows[ptr[p]:ptr[p + 1]]].sum(0) for p in range(len(lens))])
+    np.testing.assert_array_equal(dS[:len(lens)].cpu().numpy(), want)
+    np.testing.assert_array_equal(dn[:len(lens)].cpu().numpy(), lens)
+    np.testing.assert_array_equal(dSS[:len(lens)].cpu().numpy(), (want * want).sum(1))
+    kw, scene, snap, z = load_localize("localize_c2mini.npz")
+    model = scenes.snapshot_to_model(scene, snap)
+    pts = model_points(model, scene.store(), sorted(model.points))
+    S, n = scenes.track_sums(scene, snap)
+    np.testing.assert_array_equal(pts.dev[0][:len(n)].cpu().numpy(), S)
+    np.testing.assert_array_equal(pts.n, n)
+    np.testing.assert_array_equal(pts.SS, (S.astype(np.int64) ** 2).sum(1))
