@@ -169,6 +169,10 @@ typedef struct {
                           * radius d*sqrt(2) around the samples, guided.py:273-285) */
     int32_t first_chunk_pairs; /* pairs of the first chunk when > 0 (a short first
                           * chunk starts matching sooner on a staged bank)       */
+    int64_t max_workspace_bytes; /* chunks are cut so one chunk's workspace stays
+                          * within this many bytes; 0 = a quarter of the device's
+                          * free memory at planning time (at most 48M query slots,
+                          * 2^26 per chunk hard limit, explicit chunk_pairs too) */
 } msfm_match_params;
 
 /* Pack the per-pair segments of msfm_guided_match's output into contiguous
@@ -428,8 +432,11 @@ int msfm_merge_tracks(const msfm_bank* bank, int64_t n_edges, const int32_t* d_u
  * first offending record), then the records in np.argsort(-scale, "stable")
  * order written to caller buffers (xy [n][2], scale, orientation [n] f32,
  * desc [n][128] u8; scale / orientation may be NULL; xy = NULL probes the
- * header only).  msfm_msft_load_many loads n_files into one set of buffers
- * at rows row_off[i] (e.g. the pinned host bank) on n_threads host threads.
+ * header only).  ``capacity`` is the record count the buffers were sized for (from
+ * a probe): a file whose header now says otherwise gets MSFM_MSFT_CHANGED and
+ * nothing is written.  msfm_msft_load_many loads n_files into one set of buffers
+ * at rows [row_off[i], row_off[i+1]) (n_files + 1 offsets; e.g. the pinned host
+ * bank) on n_threads host threads.
  * ---------------------------------------------------------------------- */
 #define MSFM_MSFT_OK 0
 #define MSFM_MSFT_TRUNCATED 1     /* shorter than the 24-byte header */
@@ -438,6 +445,7 @@ int msfm_merge_tracks(const msfm_bank* bank, int64_t n_edges, const int32_t* d_u
 #define MSFM_MSFT_BAD_SIZE 4      /* payload != count * 144 bytes */
 #define MSFM_MSFT_BOUNDS 5        /* x, y outside the image or scale <= 0 */
 #define MSFM_MSFT_IO 6
+#define MSFM_MSFT_CHANGED 7       /* record count differs from the caller's capacity */
 typedef struct {
     int32_t status;
     char magic[4];
@@ -448,7 +456,7 @@ typedef struct {
     float bad_x, bad_y, bad_scale;
 } msfm_msft_info;
 int msfm_msft_load(const char* path, msfm_msft_info* info, float* xy, float* scale,
-                   float* orientation, uint8_t* desc);
+                   float* orientation, uint8_t* desc, int64_t capacity);
 int msfm_msft_load_many(int32_t n_files, const char* const* paths, const int64_t* row_off,
                         msfm_msft_info* infos, float* xy, float* scale, float* orientation,
                         uint8_t* desc, int32_t n_threads);

@@ -22,6 +22,11 @@ def reserve_device_memory(gigabytes: float, device=None) -> None:
     a pipeline's first call of every stage slow."""
     import torch
 
-    dev = torch.device(device or "cuda")
-    block = torch.empty(int(gigabytes * (1 << 30)), dtype=torch.uint8, device=dev)
-    del block
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if isinstance(device, int):
+        dev = torch.device("cuda", device)
+    # PyTorch caches the freed block for the stream it was allocated on: only later
+    # allocations on the current stream of `dev` are carved from it
+    with torch.cuda.device(dev):
+        block = torch.empty(int(gigabytes * (1 << 30)), dtype=torch.uint8, device=dev)
+        del block

@@ -44,7 +44,8 @@ class MatchParams(ctypes.Structure):
     _fields_ = [("d", ctypes.c_double), ("ratio", ctypes.c_float),
                 ("single_cap", ctypes.c_float), ("max_nt", ctypes.c_int32),
                 ("chunk_pairs", ctypes.c_int32), ("strategy", ctypes.c_int32),
-                ("first_chunk_pairs", ctypes.c_int32)]
+                ("first_chunk_pairs", ctypes.c_int32),
+                ("max_workspace_bytes", ctypes.c_int64)]
 
 
 class StagePlan(ctypes.Structure):
@@ -76,7 +77,8 @@ _SIGS = {
                                                   VP, ctypes.c_int32]),
     "msfm_ransac_samples": (ctypes.c_int, [VP, ctypes.c_int32, ctypes.c_uint32, ctypes.c_int64,
                                            ctypes.c_int32, ctypes.c_int32, VP, VP]),
-    "msfm_msft_load": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(MsftInfo), VP, VP, VP, VP]),
+    "msfm_msft_load": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(MsftInfo), VP, VP, VP, VP,
+                                      ctypes.c_int64]),
     "msfm_msft_load_many": (ctypes.c_int, [ctypes.c_int32, VP, VP, VP, VP, VP, VP, VP,
                                            ctypes.c_int32]),
     "msfm_ransac_samples_seeded_device": (ctypes.c_int, [ctypes.c_int32, VP, VP, ctypes.c_int32,

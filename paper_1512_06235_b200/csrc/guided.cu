@@ -1822,15 +1822,23 @@ extern "C" int msfm_grid_build(const msfm_bank* bank, const int32_t* d_dims, con
 
 static void plan_chunks(int32_t n_pairs, const int64_t* h_qlist_off, const msfm_match_params* prm,
                         std::vector<int>& bounds, ChunkSizes& worst) {
-    // pairs per chunk, and at most 2^SLOT_BITS query slots per chunk (member records
-    // pack the chunk-local slot into SLOT_BITS bits)
-    // auto: large chunks (fewer kernel tails per stage: a C3 step in one chunk is
-    // 3.7% faster than in six) capped at AUTO_CHUNK_SLOTS query slots, which bounds
-    // the workspace to ~20 GB
+    // A chunk holds at most cp pairs, 2^SLOT_BITS query slots (member records pack
+    // the chunk-local slot into SLOT_BITS bits), AUTO_CHUNK_SLOTS slots, and as many
+    // slots as keep its workspace within the byte budget — explicit chunk_pairs
+    // included.  Auto mode: large chunks (fewer kernel tails per stage: a C3 step in
+    // one chunk is 3.7% faster than in six).
     const int cp = prm->chunk_pairs > 0 ? prm->chunk_pairs : 8192;
-    const int64_t qmax = std::min<int64_t>((int64_t)1 << SLOT_BITS,
-                                           prm->chunk_pairs > 0 ? ((int64_t)1 << SLOT_BITS)
-                                                                : AUTO_CHUNK_SLOTS);
+    int64_t budget = prm->max_workspace_bytes;
+    if (budget <= 0) {
+        size_t fr = 0, tot = 0;
+        budget = (cudaMemGetInfo(&fr, &tot) == cudaSuccess && fr > 0) ? (int64_t)(fr / 4)
+                                                                       : (int64_t)16 << 30;
+    }
+    const int64_t qmax = std::min<int64_t>((int64_t)1 << SLOT_BITS, AUTO_CHUNK_SLOTS);
+    auto bytes_of = [&](int64_t P, int64_t Q) {
+        ChunkSizes c{P, Q, 2 * (Q + P) + 2 * P, P * (int64_t)prm->max_nt};
+        return (int64_t)chunk_bytes(c);
+    };
     bounds.clear();
     worst = {0, 0, 0, 0};
     int p = 0;
@@ -1838,7 +1846,9 @@ static void plan_chunks(int32_t n_pairs, const int64_t* h_qlist_off, const msfm_
     while (p < n_pairs) {
         int e = p + 1;
         const int cap = (p == 0 && prm->first_chunk_pairs > 0) ? std::min(cp, prm->first_chunk_pairs) : cp;
-        while (e < n_pairs && e - p < cap && h_qlist_off[e + 1] - h_qlist_off[p] <= qmax) e++;
+        while (e < n_pairs && e - p < cap && h_qlist_off[e + 1] - h_qlist_off[p] <= qmax &&
+               bytes_of(e + 1 - p, h_qlist_off[e + 1] - h_qlist_off[p]) <= budget)
+            e++;
         ChunkSizes c;
         c.P = e - p;
         c.Q = h_qlist_off[e] - h_qlist_off[p];

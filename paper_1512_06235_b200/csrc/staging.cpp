@@ -59,8 +59,10 @@ int parse_header(const std::vector<uint8_t>& d, msfm_msft_info* info) {
     return info->status = MSFM_MSFT_OK;
 }
 
+// capacity: records the caller's buffers hold (sized from an earlier header read);
+// a file whose count no longer matches is rejected before anything is written
 int load_one(const char* path, msfm_msft_info* info, float* xy, float* scale, float* orient,
-             uint8_t* desc) {
+             uint8_t* desc, int64_t capacity) {
     memset(info, 0, sizeof(*info));
     info->bad_record = -1;
     std::vector<uint8_t> d;
@@ -68,6 +70,7 @@ int load_one(const char* path, msfm_msft_info* info, float* xy, float* scale, fl
     if (parse_header(d, info) != MSFM_MSFT_OK) return info->status;
     if (!xy) return info->status;          // header probe only
     const int64_t n = info->count;
+    if (n != capacity) return info->status = MSFM_MSFT_CHANGED;
     const uint8_t* rec = d.data() + HEADER_BYTES;
     // the reference's bounds test (x < 0 | x >= w | y < 0 | y >= h | scale <= 0), first hit
     const float W = (float)info->width, H = (float)info->height;
@@ -103,9 +106,9 @@ int load_one(const char* path, msfm_msft_info* info, float* xy, float* scale, fl
 }  // namespace
 
 extern "C" int msfm_msft_load(const char* path, msfm_msft_info* info, float* xy, float* scale,
-                              float* orientation, uint8_t* desc) {
+                              float* orientation, uint8_t* desc, int64_t capacity) {
     if (!path || !info) return MSFM_EINVAL;
-    load_one(path, info, xy, scale, orientation, desc);
+    load_one(path, info, xy, scale, orientation, desc, capacity);
     return MSFM_OK;
 }
 
@@ -120,7 +123,7 @@ extern "C" int msfm_msft_load_many(int32_t n_files, const char* const* paths, co
         for (int i = next++; i < n_files; i = next++) {
             const int64_t o = row_off[i];
             load_one(paths[i], infos + i, xy + 2 * o, scale ? scale + o : nullptr,
-                     orientation ? orientation + o : nullptr, desc + 128 * o);
+                     orientation ? orientation + o : nullptr, desc + 128 * o, row_off[i + 1] - o);
         }
     };
     std::vector<std::thread> pool;

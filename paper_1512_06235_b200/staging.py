@@ -45,6 +45,10 @@ def _raise_for(path, info):
     if st == 6:
         open(path, "rb").close()                      # raise the native OSError
         raise OSError(f"{path}: unreadable")
+    if st == 7:
+        # only a file rewritten between the size probe and the read gets here (the
+        # reference reads once); nothing was written to the caller's buffers
+        raise OSError(f"{path}: changed while loading ({info.count} records, sized for fewer/more)")
     if st == 1:
         raise FormatError(f"{path}: truncated header, file ends at byte {info.file_bytes}")
     if st == 2:
@@ -68,7 +72,7 @@ def load_features(path):
     lib = _lib.load(require_device=False)
     info = _lib.MsftInfo()
     bpath = os.fsencode(path)
-    lib.msfm_msft_load(bpath, ctypes.byref(info), None, None, None, None)
+    lib.msfm_msft_load(bpath, ctypes.byref(info), None, None, None, None, -1)
     if info.status != 0:
         _raise_for(path, info)
     n = int(info.count)
@@ -77,7 +81,7 @@ def load_features(path):
     orient = np.empty(n, np.float32)
     desc = np.empty((n, 128), np.uint8)
     lib.msfm_msft_load(bpath, ctypes.byref(info), xy.ctypes.data, scale.ctypes.data,
-                       orient.ctypes.data, desc.ctypes.data)
+                       orient.ctypes.data, desc.ctypes.data, n)
     if info.status != 0:
         _raise_for(path, info)
     return _feature_set_type()(image_id=int(info.image_id), width=int(info.width),
@@ -115,7 +119,7 @@ def host_bank_from_dir(directory, n_threads=None):
     paths = sorted(Path(directory).glob("*.msft"))
     infos = (_lib.MsftInfo * max(len(paths), 1))()
     for k, p in enumerate(paths):
-        lib.msfm_msft_load(os.fsencode(p), ctypes.byref(infos[k]), None, None, None, None)
+        lib.msfm_msft_load(os.fsencode(p), ctypes.byref(infos[k]), None, None, None, None, -1)
         if infos[k].status != 0:
             _raise_for(p, infos[k])
     ids = [int(infos[k].image_id) for k in range(len(paths))]
@@ -127,9 +131,8 @@ def host_bank_from_dir(directory, n_threads=None):
             seen.add(i)
     order = np.argsort(ids, kind="stable")
     counts = np.array([int(infos[k].count) for k in order], np.int64)
-    off = np.zeros(len(order), np.int64)
-    if len(order) > 1:
-        np.cumsum(counts[:-1], out=off[1:])
+    off = np.zeros(len(order) + 1, np.int64)
+    np.cumsum(counts, out=off[1:])
     n = int(counts.sum())
     xy = torch.empty((max(n, 1), 2), dtype=torch.float32).pin_memory()
     desc = torch.empty((max(n, 1), 128), dtype=torch.uint8).pin_memory()

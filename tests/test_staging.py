@@ -110,3 +110,26 @@ def test_directory_bank_equals_hostbank(tmp_path):
     _write(tmp_path / "zz_dup.msft", 3, 640, 480, *_random_set(rng, 4))
     with pytest.raises(FormatError):
         staging.load_dir(tmp_path)
+
+
+def test_load_rejects_a_file_that_changed_size(tmp_path):
+    """a file rewritten between the size probe and the read is rejected
+    before anything is written to the caller's buffers (capacity check)."""
+    import ctypes
+
+    from paper_1512_06235_b200 import _lib
+
+    rng = np.random.default_rng(4)
+    p = tmp_path / "img_001.msft"
+    _write(p, 1, 640, 480, *_random_set(rng, 40))
+    lib = _lib.load(require_device=False)
+    info = _lib.MsftInfo()
+    lib.msfm_msft_load(os.fsencode(p), ctypes.byref(info), None, None, None, None, -1)
+    assert info.status == 0 and info.count == 40
+    _write(p, 1, 640, 480, *_random_set(rng, 55))          # grew after the probe
+    xy = np.full((40, 2), -1.0, np.float32)
+    desc = np.full((40, 128), 7, np.uint8)
+    lib.msfm_msft_load(os.fsencode(p), ctypes.byref(info), xy.ctypes.data, None, None,
+                       desc.ctypes.data, 40)
+    assert info.status == 7 and info.count == 55
+    assert (xy == -1.0).all() and (desc == 7).all()
