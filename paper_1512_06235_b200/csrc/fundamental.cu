@@ -241,6 +241,74 @@ __device__ void fblock_sum(double (&v)[NV], double* sm) {
     __syncthreads();
 }
 
+// Fold one row (nonzero from column c0) into the upper-triangular 9x9 R (packed
+// by rows) with Givens rotations: the R of a stacked QR, so the design matrix's
+// singular values come out accurate down to ~1e-16 of the largest (the normal
+// matrix squares them and loses the small ones; geometry.py:132's planar gap
+// s[-2]/s[0] < 1e-9 needs them).
+__device__ __forceinline__ int rix(int i, int j) { return i * 9 - (i * (i - 1)) / 2 + (j - i); }
+
+__device__ void qr_fold(double R[45], double r[9], int c0) {
+    for (int j = c0; j < 9; j++) {
+        const double b = r[j];
+        if (b == 0.0) continue;
+        const double a = R[rix(j, j)];
+        const double rad = hypot(a, b);
+        const double c = a / rad, sn = b / rad;
+        R[rix(j, j)] = rad;
+        for (int k = j + 1; k < 9; k++) {
+            const double t1 = R[rix(j, k)], t2 = r[k];
+            R[rix(j, k)] = c * t1 + sn * t2;
+            r[k] = c * t2 - sn * t1;
+        }
+    }
+}
+
+__device__ void qr_merge(double Ra[45], const double Rb[45]) {
+    for (int i = 0; i < 9; i++) {
+        double r[9];
+        for (int k = 0; k < 9; k++) r[k] = k < i ? 0.0 : Rb[rix(i, k)];
+        qr_fold(Ra, r, i);
+    }
+}
+
+// singular values of the 9x9 upper-triangular R (one-sided Jacobi), descending
+__device__ void sv_of_r(const double R[45], double s[9]) {
+    double A[81];
+    for (int i = 0; i < 9; i++)
+        for (int j = 0; j < 9; j++) A[i * 9 + j] = j < i ? 0.0 : R[rix(i, j)];
+    for (int sweep = 0; sweep < 60; sweep++) {
+        double off = 0.0;
+        for (int p = 0; p < 8; p++)
+            for (int q = p + 1; q < 9; q++) {
+                double al = 0.0, be = 0.0, ga = 0.0;
+                for (int i = 0; i < 9; i++) {
+                    al += A[i * 9 + p] * A[i * 9 + p];
+                    be += A[i * 9 + q] * A[i * 9 + q];
+                    ga += A[i * 9 + p] * A[i * 9 + q];
+                }
+                if (ga == 0.0 || fabs(ga) <= 1e-17 * sqrt(al * be)) continue;
+                off = fmax(off, fabs(ga) / sqrt(al * be));
+                const double z = (be - al) / (2.0 * ga);
+                const double t = (z >= 0 ? 1.0 : -1.0) / (fabs(z) + sqrt(1.0 + z * z));
+                const double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
+                for (int i = 0; i < 9; i++) {
+                    const double x = A[i * 9 + p], y = A[i * 9 + q];
+                    A[i * 9 + p] = c * x - sn * y;
+                    A[i * 9 + q] = sn * x + c * y;
+                }
+            }
+        if (off < 1e-15) break;
+    }
+    for (int j = 0; j < 9; j++) {
+        double n2 = 0.0;
+        for (int i = 0; i < 9; i++) n2 += A[i * 9 + j] * A[i * 9 + j];
+        s[j] = sqrt(n2);
+    }
+    for (int i = 1; i < 9; i++)       // insertion sort, descending
+        for (int j = i; j > 0 && s[j] > s[j - 1]; j--) { const double t = s[j]; s[j] = s[j - 1]; s[j - 1] = t; }
+}
+
 __global__ void __launch_bounds__(FT) f_refit_kernel(FRefitArgs a) {
     const int p = blockIdx.x;
     if (!a.status[p]) return;
@@ -276,9 +344,10 @@ __global__ void __launch_bounds__(FT) f_refit_kernel(FRefitArgs a) {
     fblock_sum<2>(r2, sm);
     hq.s = sqrt(2.0) / fmax(sqrt(r2[0] / m), 1e-12);
     hc.s = sqrt(2.0) / fmax(sqrt(r2[1] / m), 1e-12);
-    // normal matrix of the inlier design matrix
-    double acc[45];
-    for (int k = 0; k < 45; k++) acc[k] = 0.0;
+    // normal matrix of the inlier design matrix (-> F), and the R factor of its QR
+    // (-> the singular values for the planar gap)
+    double acc[45], Rq[45];
+    for (int k = 0; k < 45; k++) { acc[k] = 0.0; Rq[k] = 0.0; }
     for (int i = threadIdx.x; i < n; i += FT) {
         const double xq = a.q[2 * (o + i)], yq = a.q[2 * (o + i) + 1];
         const double xc = a.c[2 * (o + i)], yc = a.c[2 * (o + i) + 1];
@@ -289,6 +358,29 @@ __global__ void __launch_bounds__(FT) f_refit_kernel(FRefitArgs a) {
         int k = 0;
         for (int u = 0; u < 9; u++)
             for (int v = u; v < 9; v++) acc[k++] += r[u] * r[v];
+        qr_fold(Rq, r, 0);
+    }
+    // tree-merge the per-thread R factors: warps by shuffles, then the warp results
+    {
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        for (int o = 1; o < 32; o <<= 1) {
+            double other[45];
+            for (int k = 0; k < 45; k++) other[k] = __shfl_xor_sync(0xffffffffu, Rq[k], o);
+            if ((lane & o) == 0) qr_merge(Rq, other);
+        }
+        __shared__ double rsm[FT / 32][45];
+        if (lane == 0)
+            for (int k = 0; k < 45; k++) rsm[w][k] = Rq[k];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int v = 1; v < FT / 32; v++) qr_merge(Rq, rsm[v]);
+            double sv[9];
+            sv_of_r(Rq, sv);
+            rsm[0][0] = sv[0] > 0.0 ? sv[7] / sv[0] : 0.0;
+        }
+        __syncthreads();
+        Rq[0] = rsm[0][0];
+        __syncthreads();
     }
     fblock_sum<45>(acc, sm);
     if (threadIdx.x == 0) {
@@ -299,8 +391,9 @@ __global__ void __launch_bounds__(FT) f_refit_kernel(FRefitArgs a) {
         double F[9], w[9];
         f_from_normal(M, hq, hc, F, w);
         for (int i = 0; i < 9; i++) Fs[i] = F[i];
-        // s[-2] / s[0] of the design matrix (0 for fewer than 9 rows, geometry.py:132)
-        a.gap_out[p] = m >= 9.0 ? sqrt(fmax(w[7], 0.0) / w[0]) : 0.0;
+        // s[-2] / s[0] of the design matrix (0 for fewer than 9 rows, geometry.py:132),
+        // from the singular values of its R factor
+        a.gap_out[p] = m >= 9.0 ? Rq[0] : 0.0;
         for (int i = 0; i < 9; i++) a.F_out[9 * (int64_t)p + i] = F[i];
     }
     __syncthreads();
