@@ -461,6 +461,39 @@ int msfm_msft_load_many(int32_t n_files, const char* const* paths, const int64_t
                         msfm_msft_info* infos, float* xy, float* scale, float* orientation,
                         uint8_t* desc, int32_t n_threads);
 
+/* ------------------------------------------------------------------------
+ * Host-only reader of the model snapshot text (.msfm, msfm.io.read_model
+ * io.py:51-84) into CSR arrays: cameras (id, f cx cy, R row-major, t, source
+ * line) and points (xyz, track CSR of (image, feature) in file order, source
+ * line; point ids = record order).  Validation in the reference's order —
+ * header, record syntax, Camera det(R) (model.py:38), Model.attach_camera /
+ * add_point rules (model.py:114-156) — stops at the first failure with
+ * status, line and the reference's message (MSFM_MODEL_DET: value/value_id carry
+ * det and the camera id; the caller formats numpy's repr).  Buffers NULL probes
+ * the counts; the fill call takes the probe's counts as capacities.
+ * ---------------------------------------------------------------------- */
+#define MSFM_MODEL_OK 0
+#define MSFM_MODEL_HEADER 1      /* "missing 'MSFM-MODEL 1' header" (no line prefix) */
+#define MSFM_MODEL_RECORD 2      /* "<line>: <message>" */
+#define MSFM_MODEL_UNKNOWN 3     /* "<line>: unknown record '<kind>'" */
+#define MSFM_MODEL_DET 4         /* "<line>: camera <id>: det(R) = <value>" */
+#define MSFM_MODEL_POSITION 5    /* PT with < 3 coordinates (accepted, unusable, by the reference) */
+#define MSFM_MODEL_IO 6
+#define MSFM_MODEL_CHANGED 7     /* counts differ from the fill call's capacities */
+typedef struct {
+    int32_t status, line;
+    char message[192];
+    double value;
+    int64_t value_id;
+    int64_t n_cams, n_points, n_obs;
+    char stage[128];
+    int32_t stage_truncated;
+} msfm_model_info;
+int msfm_model_read(const char* path, msfm_model_info* info, int32_t* cam_id, double* cam_fcc,
+                    double* cam_R, double* cam_t, int32_t* cam_line, double* pt_xyz,
+                    int64_t* track_ptr, int32_t* track_img, int32_t* track_fid, int32_t* pt_line,
+                    int64_t cap_cams, int64_t cap_points, int64_t cap_obs);
+
 #ifdef __cplusplus
 }
 #endif

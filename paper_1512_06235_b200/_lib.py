@@ -40,6 +40,14 @@ class MsftInfo(ctypes.Structure):
                 ("bad_y", ctypes.c_float), ("bad_scale", ctypes.c_float)]
 
 
+class ModelInfo(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("line", ctypes.c_int32),
+                ("message", ctypes.c_char * 192), ("value", ctypes.c_double),
+                ("value_id", ctypes.c_int64), ("n_cams", ctypes.c_int64),
+                ("n_points", ctypes.c_int64), ("n_obs", ctypes.c_int64),
+                ("stage", ctypes.c_char * 128), ("stage_truncated", ctypes.c_int32)]
+
+
 class MatchParams(ctypes.Structure):
     _fields_ = [("d", ctypes.c_double), ("ratio", ctypes.c_float),
                 ("single_cap", ctypes.c_float), ("max_nt", ctypes.c_int32),
@@ -77,6 +85,9 @@ _SIGS = {
                                                   VP, ctypes.c_int32]),
     "msfm_ransac_samples": (ctypes.c_int, [VP, ctypes.c_int32, ctypes.c_uint32, ctypes.c_int64,
                                            ctypes.c_int32, ctypes.c_int32, VP, VP]),
+    "msfm_model_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ModelInfo), VP, VP, VP, VP,
+                                       VP, VP, VP, VP, VP, VP, ctypes.c_int64, ctypes.c_int64,
+                                       ctypes.c_int64]),
     "msfm_msft_load": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(MsftInfo), VP, VP, VP, VP,
                                       ctypes.c_int64]),
     "msfm_msft_load_many": (ctypes.c_int, [ctypes.c_int32, VP, VP, VP, VP, VP, VP, VP,

@@ -50,6 +50,9 @@ _ROUTES = [
     ("msfm.localize", "DescriptorIndex", "descriptors", "DescriptorIndex"),
     # .msft staging (features.py:98-130); FeatureStore.load_dir calls it by name
     ("msfm.features", "load_features", "staging", "load_features"),
+    # model snapshots (io.py:51-84) read natively into the arrays the stages consume
+    ("msfm.io", "read_model", "model_io", "read_model"),
+    ("msfm.cli", "read_model", "model_io", "read_model"),
     # reconstruct.py binds triangulate_track (geometry.py:276) at import
     ("msfm.reconstruct", "triangulate_track", "triangulation", "triangulate_track"),
     # the CLI binds the stage entry points at import (cli.py:20-32): its localize,
