@@ -45,6 +45,18 @@ __device__ __forceinline__ void epiline(const double* F, double x, double y, boo
     }
 }
 
+// The segment-length tests of the clips (hypot(dx, dy) > tol, >= tol): glibc's hypot is
+// within an ulp of the exact value, which is >= max(|dx|, |dy|), so a segment with a
+// coordinate difference above 2 tol passes without evaluating the hypot.
+__device__ __forceinline__ bool seg_gt(double dx, double dy, double tol) {
+    if (fmax(fabs(dx), fabs(dy)) > 2.0 * tol) return true;
+    return np_hypot(dx, dy) > tol;
+}
+__device__ __forceinline__ bool seg_not_lt(double dx, double dy, double tol) {
+    if (fmax(fabs(dx), fabs(dy)) > 2.0 * tol) return true;
+    return !(np_hypot(dx, dy) < tol);
+}
+
 // clip_lines_batch (guided.py:297-338) with pad 0.
 __device__ bool clip_batch(const double l[3], double W, double H, double pa[2], double pb[2]) {
     const double a = l[0], b = l[1], c = l[2];
@@ -81,7 +93,7 @@ __device__ bool clip_batch(const double l[3], double W, double H, double pa[2], 
     if (imin < 0) return false;
     pa[0] = cx[imin]; pa[1] = cy[imin];
     pb[0] = cx[imax]; pb[1] = cy[imax];
-    return np_hypot(pb[0] - pa[0], pb[1] - pa[1]) > 1e-12;
+    return seg_gt(pb[0] - pa[0], pb[1] - pa[1], 1e-12);
 }
 
 // clip_line_to_bounds (guided.py:140-170), scalar path, used with pad = d.
@@ -120,7 +132,7 @@ __device__ bool clip_scalar(double a, double b, double c, double W, double H, do
     }
     pa[0] = px[imin]; pa[1] = py[imin];
     pb[0] = px[imax]; pb[1] = py[imax];
-    return !(np_hypot(pb[0] - pa[0], pb[1] - pa[1]) < 1e-12);
+    return seg_not_lt(pb[0] - pa[0], pb[1] - pa[1], 1e-12);
 }
 
 // group_queries composite key (guided.py:363-373), int64 wrap semantics.
@@ -301,22 +313,22 @@ struct ChunkArgs {
     const int32_t* pair_q; const int32_t* pair_t; const double* pair_F;
     const int64_t* qlist_off; const int32_t* qlist;
     const int64_t* qlist_src;    // optional: per-pair start of its list inside qlist
-    int32_t* q_fid;              // chunk-local query feature ids (filled by lines_kernel)
+    int32_t* q_fid;              // chunk-local query feature ids (filled by setup_kernel)
     int32_t p0, npairs; int64_t qbase;
     // chunk workspace
-    int64_t* tab_off; int64_t* tbase; int32_t* ngroups; int32_t* gstart; int32_t* nmem;
-    int32_t* sgstart; int32_t* sg_next; int32_t* nsg;
+    int64_t* tab_off; int64_t* tbase;
+    int32_t* sg_total;           // super-groups queued by the chunk's setup (atomic)
+    int32_t* sg_next;            // match kernel's queue head
     unsigned long long* tab_key; unsigned* tab_rep; unsigned* tab_cnt;
     int32_t* q_tab; double* q_line;
     int2* gtmp; float* gkey; int32_t* gpos; float4* gline; float4* gend; int2* sglist;
     int4* grec; int32_t* gfill; int32_t* members; GroupRec* grp; MemberRec* mrec; SGRec* sg;
-    int32_t* mgid;               // per member position: dense group id (-1: unused position)
-    int32_t* msg;                // per member position: super-group id
-    unsigned* gfit;              // per sorted group: bit i = group g+1+i fits g's line (tau)
+    int32_t* mgid;               // per member position: the pair's (sorted) group index
+    int32_t* msg;                // per member position: the pair's super-group index
+    unsigned* gfit;              // per group: first member position past its tau-fit run
     unsigned long long* sgdev;   // per super-group: max member-band deviation (f64 bits)
-    float4* gl4;                 // per dense group: rep line (fp32) + member-band reach
-    int32_t* gmoff;              // per dense group: first member position
-    GView* gview;                // per dense group: the two above as one 32-B record
+    GView* gview;                // per group: rep line (fp32), member-band reach, first member
+    int32_t* jmp_a; int32_t* jmp_b; int32_t* jmark;   // super-group walk (large pairs)
     unsigned long long* mstate;  // per member slot: best (d2<<32 | tid)
     unsigned* mstate2;           // per member slot: second d2
     int32_t* res_tid; float* res_dist; float* res_ratio;
@@ -333,322 +345,7 @@ __device__ __forceinline__ int nextpow2(int v) {
     return p;
 }
 
-__global__ void plan_kernel(ChunkArgs a) {
-    __shared__ int sm[SCAN_T / 32 + 1];
-    long long carry_t = 0, carry_d = 0;
-    for (int b0 = 0; b0 < a.npairs; b0 += SCAN_T) {
-        int p = b0 + threadIdx.x;
-        int ts = 0, nt = 0;
-        if (p < a.npairs) {
-            int pg = a.p0 + p;
-            int nq = (int)(a.qlist_off[pg + 1] - a.qlist_off[pg]);
-            ts = nextpow2(nq + 1);
-            nt = a.img_n[a.pair_t[pg]];
-        }
-        int tot_t, tot_d;
-        int ex_t = block_exclusive_scan<SCAN_T>(ts, &tot_t, sm);
-        int ex_d = block_exclusive_scan<SCAN_T>(nt, &tot_d, sm);
-        if (p < a.npairs) {
-            a.tab_off[p] = carry_t + ex_t;
-            a.tbase[p] = carry_d + ex_d;
-        }
-        carry_t += tot_t;
-        carry_d += tot_d;
-    }
-    if (threadIdx.x == 0) {
-        a.tab_off[a.npairs] = carry_t;
-        a.tbase[a.npairs] = carry_d;
-    }
-}
-
-#ifndef MSFM_LINES_T
-#define MSFM_LINES_T 1024
-#endif
-__global__ void __launch_bounds__(MSFM_LINES_T) lines_kernel(ChunkArgs a) {
-    const int p = blockIdx.x, pg = a.p0 + p;
-    const int64_t q0 = a.qlist_off[pg];
-    const int nq = (int)(a.qlist_off[pg + 1] - q0);
-    const int64_t s0 = q0 - a.qbase;
-    const int64_t t0 = a.tab_off[p];
-    const int tsize = (int)(a.tab_off[p + 1] - t0);
-    const int ti = a.pair_t[pg], qi = a.pair_q[pg];
-    const int nt = a.img_n[ti];
-    const int64_t db = a.tbase[p];
-    for (int e = threadIdx.x; e < tsize; e += blockDim.x) {
-        a.tab_key[t0 + e] = EMPTY;
-        a.tab_rep[t0 + e] = NONE;
-        a.tab_cnt[t0 + e] = 0;
-    }
-    for (int e = threadIdx.x; e < nt; e += blockDim.x) a.dedupe[db + e] = EMPTY;
-    for (int i = threadIdx.x; i < nq; i += blockDim.x) {
-        a.res_tid[s0 + i] = -1;
-        a.gfill[s0 + i] = 0;
-        a.mgid[s0 + i] = -1;
-    }
-    if (threadIdx.x == 0) { a.ngroups[p] = 0; a.nmem[p] = 0; }
-    __syncthreads();
-    double F[9];
-#pragma unroll
-    for (int j = 0; j < 9; j++) F[j] = a.pair_F[9 * (int64_t)pg + j];
-    if (isnan(F[0])) {
-        for (int i = threadIdx.x; i < nq; i += blockDim.x) a.q_tab[s0 + i] = -1;
-        return;
-    }
-    const double W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1];
-    const int64_t qoff = a.img_off[qi];
-    const unsigned mask = (unsigned)tsize - 1;
-    const int64_t qs = a.qlist_src ? a.qlist_src[pg] : q0;
-    for (int i = threadIdx.x; i < nq; i += blockDim.x) {
-        const int fid = a.qlist[qs + i];
-        a.q_fid[s0 + i] = fid;
-        const float2 p2 = a.xy[qoff + fid];
-        double l[3];
-        epiline(F, (double)p2.x, (double)p2.y, nq == 1, l);
-        const double nrm = np_hypot(l[0], l[1]);
-        int slot = -1;
-        if (nrm > 1e-12) {
-            l[0] /= nrm; l[1] /= nrm; l[2] /= nrm;
-            double pa[2], pb[2];
-            if (clip_batch(l, W, H, pa, pb)) {
-                const unsigned long long key = composite_key(pa, pb);
-                unsigned h = (unsigned)mix64(key) & mask;
-                while (true) {
-                    unsigned long long prev = atomicCAS(&a.tab_key[t0 + h], EMPTY, key);
-                    if (prev == EMPTY || prev == key) break;
-                    h = (h + 1) & mask;
-                }
-                atomicMin(&a.tab_rep[t0 + h], (unsigned)i);
-                atomicAdd(&a.tab_cnt[t0 + h], 1u);
-                slot = (int)h;
-                double* L = a.q_line + 3 * (s0 + i);
-                L[0] = l[0]; L[1] = l[1]; L[2] = l[2];
-            }
-        }
-        a.q_tab[s0 + i] = slot;
-    }
-}
-
-// Groups of a pair: compact the occupied hash slots, then order the groups by
-// the angle of their representative line (adaptive 4096-bucket counting sort)
-// so consecutive groups have nearly identical lines, and lay out their member
-// ranges in that order.  The order only affects how members are packed into
-// super-groups, never any result.
-constexpr int GB = 4096;
-constexpr int GT = 1024;   // groups_kernel threads per pair
-__global__ void __launch_bounds__(GT, 2) groups_kernel(ChunkArgs a) {
-    __shared__ int sm[GT / 32 + 1];
-    __shared__ int hist[GB];
-    __shared__ float fmin_s[GT / 32], fmax_s[GT / 32];
-    const int p = blockIdx.x, pg = a.p0 + p;
-    const int64_t s0 = a.qlist_off[pg] - a.qbase;
-    const int64_t t0 = a.tab_off[p];
-    const int tsize = (int)(a.tab_off[p + 1] - t0);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int gcarry = 0;
-    float lo = 1e30f, hi = -1e30f;
-    for (int e0 = 0; e0 < tsize; e0 += GT) {
-        const int e = e0 + threadIdx.x;
-        bool occ = false;
-        unsigned cnt = 0, rep = 0;
-        if (e < tsize) {
-            occ = a.tab_key[t0 + e] != EMPTY;
-            if (occ) { cnt = a.tab_cnt[t0 + e]; rep = a.tab_rep[t0 + e]; }
-        }
-        int gtot;
-        const int lg = block_exclusive_scan<GT>(occ ? 1 : 0, &gtot, sm);
-        if (occ) {
-            const int g = gcarry + lg;
-            a.gtmp[s0 + g] = make_int2((int)rep, (int)cnt);
-            const double* L = a.q_line + 3 * (s0 + rep);
-            float la = (float)L[0], lb = (float)L[1];
-            if (la < 0.f || (la == 0.f && lb < 0.f)) { la = -la; lb = -lb; }
-            const float ang = atan2f(lb, la);
-            a.gkey[s0 + g] = ang;
-            lo = fminf(lo, ang);
-            hi = fmaxf(hi, ang);
-            a.tab_rep[t0 + e] = (unsigned)g;
-        }
-        gcarry += gtot;
-    }
-    const int ng = gcarry;
-    for (int o = 16; o; o >>= 1) {
-        lo = fminf(lo, __shfl_xor_sync(FULL, lo, o));
-        hi = fmaxf(hi, __shfl_xor_sync(FULL, hi, o));
-    }
-    if (lane == 0) { fmin_s[wid] = lo; fmax_s[wid] = hi; }
-    for (int b = threadIdx.x; b < GB; b += GT) hist[b] = 0;
-    __syncthreads();
-    lo = fmin_s[0]; hi = fmax_s[0];
-    for (int w = 1; w < GT / 32; w++) { lo = fminf(lo, fmin_s[w]); hi = fmaxf(hi, fmax_s[w]); }
-    const float scale = (float)GB / fmaxf(hi - lo, 1e-20f);
-    for (int g = threadIdx.x; g < ng; g += GT) {
-        const int b = min(GB - 1, max(0, (int)((a.gkey[s0 + g] - lo) * scale)));
-        atomicAdd(&hist[b], 1);
-    }
-    __syncthreads();
-    // exclusive scan of the histogram (16 buckets per thread)
-    {
-        int v[GB / GT];
-        int s = 0;
-        for (int k = 0; k < GB / GT; k++) { v[k] = hist[threadIdx.x * (GB / GT) + k]; s += v[k]; }
-        int tot;
-        int ex = block_exclusive_scan<GT>(s, &tot, sm);
-        for (int k = 0; k < GB / GT; k++) { hist[threadIdx.x * (GB / GT) + k] = ex; ex += v[k]; }
-    }
-    __syncthreads();
-    for (int g = threadIdx.x; g < ng; g += GT) {
-        const int b = min(GB - 1, max(0, (int)((a.gkey[s0 + g] - lo) * scale)));
-        a.gpos[s0 + g] = atomicAdd(&hist[b], 1);
-    }
-    __syncthreads();
-    int mcarry = 0;
-    // write grec in sorted order (scatter by gpos), then scan counts in that order
-    for (int g = threadIdx.x; g < ng; g += GT) {
-        const int2 r = a.gtmp[s0 + g];
-        a.grec[s0 + a.gpos[s0 + g]] = make_int4(r.x, r.y, 0, 0);
-    }
-    __syncthreads();
-    for (int i0 = 0; i0 < ng; i0 += GT) {
-        const int i = i0 + threadIdx.x;
-        const int cnt = i < ng ? a.grec[s0 + i].y : 0;
-        int tot;
-        const int ex = block_exclusive_scan<GT>(cnt, &tot, sm);
-        if (i < ng) a.grec[s0 + i].z = (int)(s0 + mcarry + ex);
-        mcarry += tot;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < tsize; e += GT) {
-        if (a.tab_key[t0 + e] != EMPTY) a.tab_rep[t0 + e] = (unsigned)a.gpos[s0 + a.tab_rep[t0 + e]];
-    }
-    // boundary endpoints of every representative line (in sorted order)
-    const int ti = a.pair_t[pg];
-    const double W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1];
-    for (int g = threadIdx.x; g < ng; g += GT) {
-        const int4 gr = a.grec[s0 + g];
-        const double* L = a.q_line + 3 * (s0 + gr.x);
-        const double l[3] = {L[0], L[1], L[2]};
-        double pa[2] = {0, 0}, pb[2] = {0, 0};
-        clip_batch(l, W, H, pa, pb);
-        a.gline[s0 + g] = make_float4((float)l[0], (float)l[1], (float)l[2], 0.f);
-        a.gend[s0 + g] = make_float4((float)pa[0], (float)pa[1], (float)pb[0], (float)pb[1]);
-    }
-    __syncthreads();
-    // super-groups: greedy walk over the angle-ordered groups; a super-group holds
-    // at most SG_MEMBERS members and closes when the next group's line leaves the
-    // base line by more than SG_TAU px inside the image (stats mode: one per group).
-    // The tau tests run in parallel (gfit bit i: group g+1+i fits group g's line);
-    // one thread then walks the groups with integer work only.
-    if (a.stats_mode) {
-        for (int g = threadIdx.x; g < ng; g += GT) {
-            const int4 gr = a.grec[s0 + g];
-            a.sglist[s0 + g] = make_int2(gr.z, gr.y);
-        }
-        if (threadIdx.x == 0) a.nsg[p] = ng;
-    } else {
-        for (int g = threadIdx.x; g < ng; g += GT) {
-            const float4 ln = a.gline[s0 + g];
-            unsigned bits = 0;
-            const int lim = min(SG_MEMBERS, ng - 1 - g);
-            for (int i = 0; i < lim; i++) {
-                const float4 en = a.gend[s0 + g + 1 + i];
-                const float d1 = fabsf(fmaf(ln.x, en.x, fmaf(ln.y, en.y, ln.z)));
-                const float d2 = fabsf(fmaf(ln.x, en.z, fmaf(ln.y, en.w, ln.z)));
-                if (fmaxf(d1, d2) <= a.sg_tau) bits |= 1u << i;
-            }
-            a.gfit[s0 + g] = bits;
-        }
-        __syncthreads();
-        // The super-groups partition the member sequence into contiguous ranges, so the
-        // greedy walk is a chain over member positions: end[q] = where the super-group
-        // opened at position q closes (all q in parallel), then one thread follows the
-        // chain from 0 through shared memory.
-        extern __shared__ unsigned short send[];
-        const int nm = mcarry;
-        for (int g = threadIdx.x; g < ng; g += GT) {
-            const int4 gr = a.grec[s0 + g];
-            const int cnt = gr.y, rel0 = (int)(gr.z - s0);
-            const unsigned fit = a.gfit[s0 + g];
-            for (int k = 0; k < cnt; k++) {
-                const int q = rel0 + k, r = cnt - k;
-                int e;
-                if (r > SG_MEMBERS) {
-                    e = q + SG_MEMBERS;
-                } else {
-                    int cur = r, j = g + 1;
-                    e = -1;
-                    while (j < ng && cur < SG_MEMBERS && ((fit >> (j - g - 1)) & 1u)) {
-                        const int4 gj = a.grec[s0 + j];
-                        const int take = min(SG_MEMBERS - cur, gj.y);
-                        cur += take;
-                        if (take < gj.y) { e = (int)(gj.z - s0) + take; break; }
-                        j++;
-                    }
-                    if (e < 0) e = j < ng ? (int)(a.grec[s0 + j].z - s0) : nm;
-                }
-                send[q] = (unsigned short)e;
-            }
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int nsg = 0;
-            for (int q = 0; q < nm;) {
-                const int e = send[q];
-                a.sglist[s0 + nsg++] = make_int2((int)s0 + q, e - q);
-                q = e;
-            }
-            a.nsg[p] = nsg;
-        }
-    }
-    if (threadIdx.x == 0) { a.ngroups[p] = ng; a.nmem[p] = mcarry; }
-}
-
-__global__ void gscan_kernel(ChunkArgs a) {
-    __shared__ int sm[SCAN_T / 32 + 1];
-    int carry = 0, carry_sg = 0;
-    for (int b0 = 0; b0 < a.npairs; b0 += SCAN_T) {
-        int p = b0 + threadIdx.x;
-        int v = p < a.npairs ? a.ngroups[p] : 0;
-        int vs = 0;
-        if (p < a.npairs) vs = a.nsg[p];
-        int total, total_sg;
-        int ex = block_exclusive_scan<SCAN_T>(v, &total, sm);
-        int exs = block_exclusive_scan<SCAN_T>(vs, &total_sg, sm);
-        if (p < a.npairs) { a.gstart[p] = carry + ex; a.sgstart[p] = carry_sg + exs; }
-        carry += total;
-        carry_sg += total_sg;
-    }
-    if (threadIdx.x == 0) {
-        a.gstart[a.npairs] = carry;
-        a.sgstart[a.npairs] = carry_sg;
-        *a.sg_next = 0;
-    }
-}
-
-__global__ void __launch_bounds__(MSFM_LINES_T) scatter_kernel(ChunkArgs a) {
-    const int p = blockIdx.x, pg = a.p0 + p;
-    const int64_t q0 = a.qlist_off[pg];
-    const int nq = (int)(a.qlist_off[pg + 1] - q0);
-    const int64_t s0 = q0 - a.qbase;
-    const int64_t t0 = a.tab_off[p];
-    for (int i = threadIdx.x; i < nq; i += blockDim.x) {
-        const int h = a.q_tab[s0 + i];
-        if (h < 0) continue;
-        const int lg = (int)a.tab_rep[t0 + h];
-        const int4 g = a.grec[s0 + lg];
-        const int pos = g.z + atomicAdd(&a.gfill[s0 + lg], 1);
-        a.members[pos] = (int)(s0 + i);
-        a.mgid[pos] = a.gstart[p] + lg;
-    }
-}
-
-__device__ __forceinline__ int find_pair(const int32_t* gstart, int npairs, int gid) {
-    int lo = 0, hi = npairs - 1;
-    while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (gstart[mid] <= gid) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
+constexpr int GB = 4096;   // angle buckets of the per-pair group order
 
 // Upper bound of |dist_m(f) - dist_r(f)| over the image rectangle restricted to
 // the member's band (|dist_m| <= d + 0.5): the difference is affine, so its
@@ -728,208 +425,7 @@ __device__ double band_deviation(const double m[3], const double r[3], double W,
     return dev;
 }
 
-// |dist_g - dist_base| over the whole image rectangle (affine -> max at a corner)
-
-// Per group: the C' geometry of its representative line + member constants.
-__global__ void __launch_bounds__(128) prep_kernel(ChunkArgs a, int max_groups) {
-    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int total = a.gstart[a.npairs];
-    if (gid >= total || gid >= max_groups) return;
-    const int p = find_pair(a.gstart, a.npairs, gid);
-    const int pg = a.p0 + p;
-    const int64_t q0 = a.qlist_off[pg];
-    const int64_t s0 = q0 - a.qbase;
-    const int4 g = a.grec[s0 + (gid - a.gstart[p])];
-    const int ti = a.pair_t[pg];
-    const double W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1], D = a.D, d = a.d;
-    const double* rl = a.q_line + 3 * (s0 + g.x);
-    const double r[3] = {rl[0], rl[1], rl[2]};
-    GroupRec o;
-    o.p = p; o.rep = (int)(s0 + g.x); o.cnt = g.y; o.moff = g.z;
-    o.sl0 = r[0]; o.sl1 = r[1]; o.sl2 = r[2]; o.spare = 0.0;
-    o.pad1 = o.pad2 = o.pad3 = 0;
-    double maxdev = 0.0;
-    double pa[2] = {0, 0}, pb[2] = {0, 0}, len = 0.0;
-    o.K = -1;
-    if (clip_scalar(r[0], r[1], r[2], W, H, d, pa, pb)) {
-        len = np_hypot(pb[0] - pa[0], pb[1] - pa[1]);
-        long long K = (long long)ceil(len / d);
-        o.K = (int)(K < 1 ? 1 : K);
-    }
-    o.pax = pa[0]; o.pay = pa[1]; o.pbx64 = pb[0]; o.pby64 = pb[1];
-    o.ar = (float)r[0]; o.br = (float)r[1]; o.cr = (float)r[2];
-    o.maxdev = (float)(maxdev + 0.05);   // raised by member_kernel (atomic max of f32 bits)
-    const double hs2 = D * D - 0.25 * d * d;
-    o.hsure = hs2 > 0 ? (float)(sqrt(hs2) - 0.075) : -1.0f;
-    o.pbx = (float)pb[0]; o.pby = (float)pb[1];
-    o.dirx = len > 0 ? (float)((pa[0] - pb[0]) / len) : 0.f;
-    o.diry = len > 0 ? (float)((pa[1] - pb[1]) / len) : 0.f;
-    o.len = (float)len;
-    o.spacing = o.K > 0 ? fmaxf((float)(len / o.K), 1e-6f) : 1.0f;
-    o.invK = o.K > 0 ? (float)(1.0 / o.K) : 0.f;
-    o.dxf = (float)(pa[0] - pb[0]); o.dyf = (float)(pa[1] - pb[1]);
-    o.slack = (float)(4e-6 * (W + H + 4.0 * d) / D) + 1e-4f;
-    o.invD = (float)(1.0 / D);
-    a.grp[gid] = o;
-}
-
-// Per super-group: member window, its groups, the base line and strip.
-// Super-group shape (thread per super-group): group range and base line.
-__global__ void __launch_bounds__(128) sg_shape_kernel(ChunkArgs a, int max_sg) {
-    const int sid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int total = a.sgstart[a.npairs];
-    if (sid >= total || sid >= max_sg) return;
-    const int p = find_pair(a.sgstart, a.npairs, sid);
-    const int ls = sid - a.sgstart[p];
-    const int pg = a.p0 + p;
-    const int64_t s0 = a.qlist_off[pg] - a.qbase;
-    const int ng = a.ngroups[p];
-    SGRec o = {};
-    o.p = p;
-    int lg0, lg1;                       // group range [lg0, lg1] (sorted order)
-    const int2 sgm = a.sglist[s0 + ls];
-    o.m0 = sgm.x; o.mcnt = sgm.y;
-    if (a.stats_mode) {
-        lg0 = lg1 = ls;
-    } else {
-        // groups containing the first and last member (member offsets ascend with lg)
-        auto group_of = [&](int m) {
-            int lo = 0, hi = ng - 1;
-            while (lo < hi) {
-                int mid = (lo + hi + 1) >> 1;
-                if (a.grec[s0 + mid].z <= m) lo = mid; else hi = mid - 1;
-            }
-            return lo;
-        };
-        lg0 = group_of(o.m0);
-        lg1 = group_of(o.m0 + o.mcnt - 1);
-    }
-    o.g0 = a.gstart[p] + lg0;
-    o.gcnt = lg1 - lg0 + 1;
-    // base line: the middle group's representative (its chunk-local slot in rlo)
-    o.rlo = a.grp[a.gstart[p] + (lg0 + lg1) / 2].rep;
-    for (int j = 0; j < o.mcnt; j++) a.msg[o.m0 + j] = sid;
-    a.sgdev[sid] = 0ull;
-    a.sg[sid] = o;
-}
-
-// Per member (thread per member position): epilogue constants, the member band's
-// deviation from its group's representative line (-> GroupRec.maxdev) and from its
-// super-group's base line (-> sgdev), both as atomic maxima.
-__global__ void __launch_bounds__(128, 12) member_kernel(ChunkArgs a, int max_pos) {
-    const int pos = blockIdx.x * blockDim.x + threadIdx.x;
-    if (pos >= max_pos) return;
-    const int gid = a.mgid[pos];
-    if (gid < 0) return;
-    GroupRec& G = a.grp[gid];
-    const int p = G.p, pg = a.p0 + p;
-    const int ti = a.pair_t[pg], qi = a.pair_q[pg];
-    const double W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1], d = a.d;
-    const int64_t qoff = a.img_off[qi];
-    const int slot = a.members[pos];
-    const int fid = a.q_fid[slot];
-    double m[3];
-    if (G.cnt == 1) {
-        // a singleton's own band uses the dgemv-rounded line (guided.py:443-446, m == 1)
-        double F[9];
-        for (int j = 0; j < 9; j++) F[j] = a.pair_F[9 * (int64_t)pg + j];
-        const float2 p2 = a.xy[qoff + fid];
-        epiline(F, (double)p2.x, (double)p2.y, true, m);
-        double nrm = fmax(np_hypot(m[0], m[1]), 1e-15);
-        m[0] /= nrm; m[1] /= nrm; m[2] /= nrm;
-        G.sl0 = m[0]; G.sl1 = m[1]; G.sl2 = m[2];
-    } else {
-        const double* ml = a.q_line + 3 * (int64_t)slot;
-        m[0] = ml[0]; m[1] = ml[1]; m[2] = ml[2];
-    }
-    const double* rl = a.q_line + 3 * (int64_t)G.rep;
-    const double r[3] = {rl[0], rl[1], rl[2]};
-    const int sid = a.msg[pos];
-    const SGRec& SG = a.sg[sid];
-    const double* bl = a.q_line + 3 * (int64_t)SG.rlo;
-    const double b[3] = {bl[0], bl[1], bl[2]};
-    double rdev, sdev;
-    band_deviation2(m, r, b, W, H, d, rdev, sdev);
-    const float gdev = (float)(rdev + 0.05);
-    atomicMax(reinterpret_cast<unsigned*>(&G.maxdev), __float_as_uint(gdev));
-    atomicMax(&a.sgdev[sid], (unsigned long long)__double_as_longlong(sdev));
-    MemberRec mr;
-    mr.a = (float)m[0]; mr.b = (float)m[1]; mr.c = (float)m[2];
-    const float eps = (float)((fabs(m[0]) * W + fabs(m[1]) * H + fabs(m[2])) * 0x1p-20) + 1e-6f;
-    mr.lo = (float)d - eps;
-    mr.hi = (float)d + eps;
-    mr.qn9 = (unsigned)a.norm2[qoff + fid] << 9;
-    mr.fid = fid;
-    mr.slotgi = (int)((unsigned)slot | ((unsigned)(gid - SG.g0) << SLOT_BITS));
-    a.mrec[pos] = mr;
-}
-
-// Super-group strip geometry (thread per super-group), after member_kernel.
-__global__ void __launch_bounds__(128) sg_prep_kernel(ChunkArgs a, int max_sg) {
-    const int sid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int total = a.sgstart[a.npairs];
-    if (sid >= total || sid >= max_sg) return;
-    SGRec o = a.sg[sid];
-    const int pg = a.p0 + o.p;
-    const int ti = a.pair_t[pg];
-    const double W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1], D = a.D, d = a.d;
-    const double* bl = a.q_line + 3 * (int64_t)o.rlo;
-    const double r[3] = {bl[0], bl[1], bl[2]};
-    const double dev = __longlong_as_double((long long)a.sgdev[sid]);
-    bool all_k = true;
-    const double R = d + dev + 0.05;
-    double delta = 0.0;
-    for (int g = o.g0; g < o.g0 + o.gcnt; g++) {
-        const GroupRec& G = a.grp[g];
-        const double* gl = a.q_line + 3 * (int64_t)G.rep;
-        const double gr[3] = {gl[0], gl[1], gl[2]};
-        // |dist_g - dist_base| over the strip |dist_base| <= R inside the image
-        delta = fmax(delta, band_deviation(r, gr, W, H, R));
-        all_k = all_k && G.K >= 0;
-        // compact per-group view for the match kernel (groups shared by two
-        // super-groups get the same values twice)
-        a.gl4[g] = (G.K < 0 && a.strategy != 1) ? make_float4(0.f, 0.f, 1e30f, -1.f)
-                           : make_float4(G.ar, G.br, G.cr, (float)a.d + G.maxdev + 0.05f);
-        a.gmoff[g] = G.moff;
-        const float4 v = a.gl4[g];
-        GView gv;
-        gv.a = v.x; gv.b = v.y; gv.c = v.z; gv.reach = v.w;
-        gv.moff = G.moff; gv.pad0 = gv.pad1 = gv.pad2 = 0;
-        a.gview[g] = gv;
-    }
-    o.ar = (float)r[0]; o.br = (float)r[1]; o.cr = (float)r[2]; o.R = (float)R;
-    // sure-in-C' radius around the base line: grid, the 3x3 subcell block of the
-    // nearest sample (half-size D); radial, the disk of radius r around it; both with the
-    // sample spacing <= d.  Linear: the rep-line band itself (fp32 error << 0.05 px).
-    const double DC = a.strategy == 2 ? sqrt(a.r2) : D;
-    const double hs2 = DC * DC - 0.25 * d * d;
-    const double hs = a.strategy == 1 ? d - 0.05 : (hs2 > 0 ? sqrt(hs2) - 0.075 : -1.0);
-    o.hsure = (float)hs;
-    o.delta = (all_k || a.strategy == 1) ? (float)(delta + 0.01) : 1e30f;
-    o.border = a.strategy == 1 ? -1e30f : (float)(fmax(0.0, hs - d) + 0.05);
-    o.invD = (float)(1.0 / D);
-    o.W = (float)W; o.H = (float)H; o.pad0 = 0;
-    const bool horiz = fabs(r[1]) >= fabs(r[0]);
-    const int qi = a.pair_q[pg];
-    o.toff = a.img_off[ti]; o.qoff = a.img_off[qi];
-    o.nalong = horiz ? a.dims[2 * ti] : a.dims[2 * ti + 1];
-    o.toffb = horiz ? a.roff[ti] : a.coff[ti];
-    o.dbase = a.tbase[o.p];
-    const double al = horiz ? r[0] : r[1], be = horiz ? r[1] : r[0];
-    const double Pm = horiz ? W : H, Qm = horiz ? H : W;
-    const int nrows = horiz ? a.dims[2 * ti + 1] : a.dims[2 * ti];
-    double qv[4] = {(-R - r[2]) / be, (R - r[2]) / be, (-R - r[2] - al * Pm) / be, (R - r[2] - al * Pm) / be};
-    double qlo = fmin(fmin(qv[0], qv[1]), fmin(qv[2], qv[3]));
-    double qhi = fmax(fmax(qv[0], qv[1]), fmax(qv[2], qv[3]));
-    int rlo = (int)floor((fmax(qlo, 0.0) - 0.01) / D), rhi = (int)floor((fmin(qhi, Qm) + 0.01) / D);
-    o.horiz = horiz;
-    o.rlo = rlo < 0 ? 0 : rlo;
-    o.rhi = rhi > nrows - 1 ? nrows - 1 : rhi;
-    o.alpha = (float)al; o.beta = (float)be;
-    o.inv_alpha = fabs(al) > 1e-6 ? (float)(1.0 / al) : 0.f;
-    o.Pmax = (float)Pm;
-    a.sg[sid] = o;
-}
+#include "guided_setup.cuh"
 
 // mma.sync m16n8k32 u8 x u8 -> s32 (rows = candidates, cols = members)
 __device__ __forceinline__ void mma_u8(int (&c)[4], unsigned a0, unsigned a1, unsigned a2,
@@ -1040,512 +536,6 @@ __device__ __forceinline__ bool in_cprime(const ChunkArgs& a, const GroupRec& G,
     return in_cprime_exact(G, a.D, fx, fy, (short)(su & 0xffff), su >> 16);
 }
 
-struct alignas(16) WarpSmem {
-    float2 xy[CAP];              // candidate positions (from the bucket-ordered records)
-    unsigned nrm[CAP];           // candidate |desc|^2
-    unsigned short list[CAP];    // candidate feature ids (target-local)
-    unsigned short cmask[CAP];   // per candidate: groups (bit gi) whose C' contains it
-    unsigned short ulist[CAP];   // positions still to decide
-    unsigned sure[CAP / 32];     // candidate in C' of every group of the super-group
-    unsigned anyb[CAP / 8];      // stats: candidate inside some member band
-    SGRec sg;                    // this warp's super-group (broadcast reads)
-    float4 gl[SG_MAX_GROUPS];    // per group: rep line (fp32), member-band reach
-    MemberRec mr[SG_MEMBERS];    // the super-group's members (when mcnt <= SG_MEMBERS)
-    int gbeg[SG_MAX_GROUPS + 1]; // member range of each group within the super-group
-};
-static_assert(offsetof(WarpSmem, mr) % 16 == 0, "member records must be 16-B aligned");
-static_assert(sizeof(MemberRec) == 32, "MemberRec is read as two 16-B shared loads");
-
-
-__device__ __forceinline__ bool member_band(const ChunkArgs& a, int gid, const MemberRec& M,
-                                            float x, float y) {
-    const float v = fabsf(fmaf(M.a, x, fmaf(M.b, y, M.c)));
-    if (v <= M.lo) return true;
-    if (v > M.hi) return false;
-    const GroupRec& G = a.grp[gid];
-    if (G.cnt == 1) return band_exact(G.sl0, G.sl1, G.sl2, true, x, y, a.d);
-    const double* L = a.q_line + 3 * (int64_t)(M.slotgi & SLOT_MASK);
-    return band_exact(L[0], L[1], L[2], false, x, y, a.d);
-}
-
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-// volatile shared loads: re-read per tile instead of pinning registers across the loop
-__device__ __forceinline__ float4 lds_f4(const void* p) {
-    float4 v;
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(smem_addr(p)));
-    return v;
-}
-__device__ __forceinline__ uint4 lds_u4(const void* p) {
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(smem_addr(p)));
-    return v;
-}
-
-// member block [mt0, mt0 + SG_MEMBERS) of the super-group into S.mr; columns past the
-// last member get a line that never passes the band test
-__device__ __forceinline__ void stage_members(const ChunkArgs& a, WarpSmem& S, int m0, int m, int mt0) {
-    const int lane = threadIdx.x & 31;
-    if (lane < SG_MEMBERS) {
-        MemberRec M;
-        if (mt0 + lane < m) {
-            M = a.mrec[m0 + mt0 + lane];
-        } else {
-            M.a = 0.f; M.b = 0.f; M.c = 1e30f; M.lo = -1.f; M.hi = -1.f;
-            M.qn9 = 0; M.fid = 0; M.slotgi = 0;
-        }
-        S.mr[lane] = M;
-    }
-}
-
-template <bool STATS>
-__device__ void process_round(const ChunkArgs& a, WarpSmem& S, int n, int64_t toff, int64_t qoff,
-                              bool first_round, int& cols_total) {
-    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-    const SGRec& SG = S.sg;
-    const int m = SG.mcnt;
-    const MemberRec* MR = m <= SG_MEMBERS ? S.mr : a.mrec + SG.m0;
-    const unsigned all_groups = (1u << SG.gcnt) - 1u;
-    // ---- per-group C' bits of the candidates not surely inside every group's C'
-    int nu = 0;
-    for (int j0 = 0; j0 < n; j0 += 32) {
-        const int j = j0 + lane;
-        const bool sure = j < n && ((S.sure[j >> 5] >> (j & 31)) & 1u);
-        if (j < n) S.cmask[j] = sure ? (unsigned short)all_groups : 0;
-        const bool need = j < n && !sure;
-        const unsigned bal = __ballot_sync(FULL, need);
-        if (need) S.ulist[nu + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)j;
-        nu += __popc(bal);
-    }
-    __syncwarp();
-    if (a.dbg && lane == 0) {
-        atomicAdd(&a.dbg[5], (unsigned long long)nu);
-        atomicAdd(&a.dbg[7], (unsigned long long)((n + 15) >> 4) * ((m + 15) >> 4));
-        atomicAdd(&a.dbg[9], 1ull);
-    }
-    for (int u0 = 0; u0 < nu; u0 += 32) {
-        const int uj = u0 + lane;
-        if (uj < nu) {
-            const int j = S.ulist[uj];
-            const int f = S.list[j];
-            const float2 p2 = S.xy[j];
-            const bool inner = p2.x >= SG.border && p2.x <= SG.W - SG.border &&
-                               p2.y >= SG.border && p2.y <= SG.H - SG.border;
-            unsigned bits = 0;
-            for (int gi = 0; gi < SG.gcnt; gi++) {
-                // gl: rep line and member reach; a group whose line misses the image
-                // (K < 0) has gl = (0, 0, 1e30) and is never taken
-                const float4 gl = S.gl[gi];
-                const float dg = fabsf(fmaf(gl.x, p2.x, fmaf(gl.y, p2.y, gl.z)));
-                if (dg <= SG.hsure && inner) { bits |= 1u << gi; continue; }
-                // outside every member band of this group: the bit is never consulted
-                if (dg > gl.w) continue;
-                bool any = false;
-                for (int k = S.gbeg[gi]; k < S.gbeg[gi + 1] && !any; k++)
-                    any = member_band(a, SG.g0 + gi, MR[k], p2.x, p2.y);
-                if (any && a.dbg) atomicAdd(&a.dbg[6], 1ull);
-                if (any && in_cprime(a, a.grp[SG.g0 + gi], SG, p2.x, p2.y, toff, f))
-                    bits |= 1u << gi;
-            }
-            S.cmask[j] = (unsigned short)bits;
-        }
-    }
-    if (STATS) {
-        for (int w = lane; w < CAP / 8; w += 32) S.anyb[w] = 0;
-    }
-    __syncwarp();
-    const int ntiles = (n + 15) >> 4;
-    for (int mt0 = 0; mt0 < m; mt0 += SG_MEMBERS) {
-        if (m > SG_MEMBERS) {
-            __syncwarp();
-            stage_members(a, S, SG.m0, m, mt0);
-            __syncwarp();
-        }
-        // B fragments: member mt0 + 8 nt + g of n-tile nt, bytes [32t, 32t+32)
-        unsigned bw[SG_NT][8];
-#pragma unroll
-        for (int nt = 0; nt < SG_NT; nt++) {
-            const int j = mt0 + nt * 8 + g;
-            if (j < m) {
-                const int fid = S.mr[nt * 8 + g].fid;
-                const uint4* row = reinterpret_cast<const uint4*>(a.desc + (qoff + fid) * 128) + 2 * t;
-                const uint4 v0 = __ldg(row), v1 = __ldg(row + 1);
-                bw[nt][0] = v0.x; bw[nt][1] = v0.y; bw[nt][2] = v0.z; bw[nt][3] = v0.w;
-                bw[nt][4] = v1.x; bw[nt][5] = v1.y; bw[nt][6] = v1.z; bw[nt][7] = v1.w;
-            } else {
-#pragma unroll
-                for (int k = 0; k < 8; k++) bw[nt][k] = 0;
-            }
-        }
-        // epilogue columns: (nt, 2t + c) -> member mt0 + 8 nt + 2t + c; their constants
-        // are re-read from S.mr every tile (two 16-B shared loads per column)
-        constexpr int NC = 2 * SG_NT;    // epilogue columns per lane
-        unsigned b1[NC], b2[NC];
-#pragma unroll
-        for (int c = 0; c < NC; c++) { b1[c] = NONE; b2[c] = NONE; }
-        // candidate tile loads, double-buffered in registers so the next tile's
-        // L2 traffic overlaps this tile's mma + epilogue
-        struct Tile {
-            uint4 x00, x01, x10, x11;
-            unsigned tb0, tb1;
-        };
-        const uint4* tdesc = reinterpret_cast<const uint4*>(a.desc + toff * 128) + 2 * t;
-        auto load_tile = [&](int mt, Tile& T) {
-            const int r0 = mt * 16 + g, r1 = r0 + 8;
-            const bool v0 = r0 < n, v1 = r1 < n;
-            const int f0 = v0 ? S.list[r0] : 0, f1 = v1 ? S.list[r1] : 0;
-            const uint4* row0 = tdesc + 8 * f0;
-            const uint4* row1 = tdesc + 8 * f1;
-            T.x00 = __ldg(row0); T.x01 = __ldg(row0 + 1);
-            T.x10 = __ldg(row1); T.x11 = __ldg(row1 + 1);
-            T.tb0 = (S.nrm[v0 ? r0 : 0] << 9) | (unsigned)r0;
-            T.tb1 = (S.nrm[v1 ? r1 : 0] << 9) | (unsigned)r1;
-        };
-        auto do_tile = [&](int mt, const Tile& cur) {
-            const uint4 x00 = cur.x00, x01 = cur.x01, x10 = cur.x10, x11 = cur.x11;
-            const unsigned tb0 = cur.tb0, tb1 = cur.tb1;
-            const int r0 = mt * 16 + g, r1 = r0 + 8;
-            const unsigned cm0 = r0 < n ? S.cmask[r0] : 0u, cm1 = r1 < n ? S.cmask[r1] : 0u;
-            const float2 p0 = S.xy[r0 < n ? r0 : 0], p1 = S.xy[r1 < n ? r1 : 0];
-            int acc[SG_NT][4];
-#pragma unroll
-            for (int nt = 0; nt < SG_NT; nt++) {
-                acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0;
-                mma_u8(acc[nt], x00.x, x10.x, x00.y, x10.y, bw[nt][0], bw[nt][1]);
-                mma_u8(acc[nt], x00.z, x10.z, x00.w, x10.w, bw[nt][2], bw[nt][3]);
-                mma_u8(acc[nt], x01.x, x11.x, x01.y, x11.y, bw[nt][4], bw[nt][5]);
-                mma_u8(acc[nt], x01.z, x11.z, x01.w, x11.w, bw[nt][6], bw[nt][7]);
-            }
-            // Fast path: elements surely inside the member band (fp32 value <= d - eps) and
-            // inside the group's C' go straight into the top-2; elements within eps of the
-            // band edge are collected in ucm and decided with the reference's fp64 value
-            // afterwards (rare; top-2 is insensitive to the push order).
-            constexpr int NE = 4 * SG_NT;
-            unsigned ucm = 0;
-#ifdef MSFM_MATCH_TILE_STATS
-            unsigned inb = 0;
-#endif
-            bool any0 = false, any1 = false;
-            // column by column: one member's constants (two 16-B shared loads) live at a
-            // time, used by its two elements of this lane
-#pragma unroll
-            for (int c = 0; c < NC; c++) {
-              const MemberRec* Mc = &S.mr[(c >> 1) * 8 + 2 * t + (c & 1)];
-              const float4 MLc = lds_f4(&Mc->a);      // a, b, c, lo
-              const uint4 MHc = lds_u4(&Mc->hi);      // hi, qn9, fid, slotgi
-#pragma unroll
-              for (int rh = 0; rh < 2; rh++) {
-                const int nt = c >> 1, q = (c & 1) + 2 * rh, e = nt * 4 + q;
-                const bool rowhi = rh != 0;
-                const float2 P = rowhi ? p1 : p0;
-                const float av = fabsf(fmaf(MLc.x, P.x, fmaf(MLc.y, P.y, MLc.z)));
-#ifdef MSFM_MATCH_TILE_STATS
-                if (a.dbg && av <= __uint_as_float(MHc.x) && (rowhi ? r1 : r0) < n) inb |= 1u << e;
-#endif
-                const bool cbit = ((rowhi ? cm1 : cm0) >> (MHc.w >> SLOT_BITS)) & 1u;
-                const bool sure_in = av <= MLc.w && cbit;
-                if (!(av <= MLc.w) && av <= __uint_as_float(MHc.x) && cbit) ucm |= 1u << e;
-                if (STATS) { if (rowhi) any1 |= sure_in; else any0 |= sure_in; }
-                const unsigned key = (rowhi ? tb1 : tb0) + MHc.y - ((unsigned)acc[nt][q] << 10);
-                top2_push(sure_in ? key : NONE, b1[c], b2[c]);
-              }
-            }
-#ifdef MSFM_MATCH_TILE_STATS
-            if (a.dbg) {
-                // band-reach occupancy of the tile: elements near some member band, and
-                // (tile, 8-member block)s with none (MMA + epilogue work a skip could save)
-                int blk_empty = 0, blk = 0;
-#pragma unroll
-                for (int nt = 0; nt < SG_NT; nt++) {
-                    if (mt0 + nt * 8 >= m) continue;
-                    blk++;
-                    if (!__any_sync(FULL, ((inb >> (4 * nt)) & 0xFu) != 0)) blk_empty++;
-                }
-                unsigned ne = __popc(inb);
-#pragma unroll
-                for (int o = 16; o; o >>= 1) ne += __shfl_xor_sync(FULL, ne, o);
-                if (lane == 0) {
-                    const int rv = min(16, n - mt * 16), cv = min(16, m - mt0);
-                    atomicAdd(&a.dbg[10], (unsigned long long)(rv * cv));
-                    atomicAdd(&a.dbg[11], (unsigned long long)ne);
-                    atomicAdd(&a.dbg[12], (unsigned long long)blk_empty);
-                    atomicAdd(&a.dbg[13], (unsigned long long)blk);
-                }
-            }
-#endif
-            if (__any_sync(FULL, ucm != 0)) {
-#pragma unroll
-                for (int e = 0; e < NE; e++) {
-                    if (!((ucm >> e) & 1u)) continue;
-                    const int nt = e >> 2, q = e & 3, c = nt * 2 + (q & 1);
-                    const bool rowhi = q >= 2;
-                    const float2 P = rowhi ? p1 : p0;
-                    const uint4 MHc = lds_u4(&S.mr[(c >> 1) * 8 + 2 * t + (c & 1)].hi);
-                    const GroupRec& Gc = a.grp[SG.g0 + (int)(MHc.w >> SLOT_BITS)];
-                    const bool gemv = Gc.cnt == 1;
-                    const double* L = gemv ? &Gc.sl0 : a.q_line + 3 * (int64_t)(MHc.w & SLOT_MASK);
-                    if (band_exact(L[0], L[1], L[2], gemv, (double)P.x, (double)P.y, a.d)) {
-                        if (STATS) { if (rowhi) any1 = true; else any0 = true; }
-                        const unsigned key = (rowhi ? tb1 : tb0) + MHc.y - ((unsigned)acc[nt][q] << 10);
-                        top2_push(key, b1[c], b2[c]);
-                    }
-                }
-            }
-            if (STATS) {
-                unsigned m0 = __ballot_sync(FULL, any0);
-                unsigned m1 = __ballot_sync(FULL, any1);
-                if (lane == 0) {
-                    m0 |= m0 >> 1; m0 |= m0 >> 2;
-                    m1 |= m1 >> 1; m1 |= m1 >> 2;
-                    S.anyb[2 * mt] |= m0 & 0x11111111u;
-                    S.anyb[2 * mt + 1] |= m1 & 0x11111111u;
-                }
-            }
-        };
-        // two register tiles in flight: tile mt+1's loads overlap tile mt's mma + epilogue
-        Tile nxt;
-        if (ntiles > 0) load_tile(0, nxt);
-        for (int mt = 0; mt < ntiles; mt++) {
-            const Tile cur = nxt;
-            if (mt + 1 < ntiles) load_tile(mt + 1, nxt);
-            do_tile(mt, cur);
-        }
-        // reduce across the 8 lanes sharing t
-#pragma unroll
-        for (int c = 0; c < NC; c++) {
-#pragma unroll
-            for (int o = 4; o < 32; o <<= 1) {
-                unsigned o1 = __shfl_xor_sync(FULL, b1[c], o);
-                unsigned o2 = __shfl_xor_sync(FULL, b2[c], o);
-                top2_merge(b1[c], b2[c], o1, o2);
-            }
-        }
-        if (g == 0) {
-#pragma unroll
-            for (int c = 0; c < NC; c++) {
-                const int jj = (c >> 1) * 8 + 2 * t + (c & 1);
-                if (mt0 + jj >= m) continue;
-                const int mslot = S.mr[jj].slotgi & SLOT_MASK;
-                unsigned long long best = ~0ull;
-                unsigned sec = NONE;
-                if (b1[c] != NONE) {
-                    const unsigned d2 = b1[c] >> 9;
-                    const int tid = S.list[b1[c] & 511u];
-                    best = ((unsigned long long)d2 << 32) | (unsigned)tid;
-                }
-                if (b2[c] != NONE) sec = b2[c] >> 9;
-                if (!first_round) {
-                    const unsigned long long ob = a.mstate[mslot];
-                    const unsigned os = a.mstate2[mslot];
-                    const unsigned bd = (unsigned)(best >> 32), od = (unsigned)(ob >> 32);
-                    const unsigned nh = max(bd, od);
-                    const unsigned long long nbest = (bd < od) ? best : ob;
-                    sec = min(nh, min(sec, os));
-                    best = nbest;
-                }
-                a.mstate[mslot] = best;
-                a.mstate2[mslot] = sec;
-            }
-        }
-    }
-    if (STATS) {
-        __syncwarp();
-        int cnt = 0;
-        for (int w = lane; w < ntiles * 2; w += 32) cnt += __popc(S.anyb[w]);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
-        cols_total += cnt;
-    }
-    __syncwarp();
-}
-
-template <bool STATS>
-__global__ void __launch_bounds__(WARPS * 32, MATCH_MINB) match_kernel(ChunkArgs a) {
-    __shared__ WarpSmem smem[WARPS];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    WarpSmem& S = smem[warp];
-    const int total = a.sgstart[a.npairs];
-    const float Df = (float)a.D;
-    static_assert(sizeof(SGRec) % 16 == 0, "SGRec must be 16-byte granular");
-    constexpr int SG_CHUNKS = (int)(sizeof(SGRec) / 16);
-    // the next super-group's id and record are fetched while the current one runs
-    int nsid = 0;
-    if (lane == 0) nsid = atomicAdd(a.sg_next, 1);
-    nsid = __shfl_sync(FULL, nsid, 0);
-    uint4 nrec = make_uint4(0, 0, 0, 0);
-    if (nsid < total && lane < SG_CHUNKS) nrec = __ldg(reinterpret_cast<const uint4*>(a.sg + nsid) + lane);
-    for (;;) {
-        const int sid = nsid;
-        if (sid >= total) break;
-        if (lane < SG_CHUNKS) reinterpret_cast<uint4*>(&S.sg)[lane] = nrec;
-        __syncwarp();
-        if (lane == 0) nsid = atomicAdd(a.sg_next, 1);
-        nsid = __shfl_sync(FULL, nsid, 0);
-        if (nsid < total && lane < SG_CHUNKS)
-            nrec = __ldg(reinterpret_cast<const uint4*>(a.sg + nsid) + lane);
-        const SGRec& SG = S.sg;
-        if (a.dbg && lane == 0) {
-            atomicAdd(&a.dbg[0], 1ull);
-            atomicAdd(&a.dbg[1], (unsigned long long)SG.mcnt);
-            atomicAdd(&a.dbg[8], (unsigned long long)SG.gcnt);
-        }
-        if (lane <= SG.gcnt) {
-            S.gbeg[lane] = lane < SG.gcnt ? max(a.gmoff[SG.g0 + lane] - SG.m0, 0) : SG.mcnt;
-            if (lane < SG.gcnt) S.gl[lane] = a.gl4[SG.g0 + lane];
-        }
-        stage_members(a, S, SG.m0, SG.mcnt, 0);
-        __syncwarp();
-        const int pg = a.p0 + SG.p;
-        const int64_t toff = SG.toff, qoff = SG.qoff;
-        const int nalong = SG.nalong;
-        const int64_t toffb = SG.toffb;
-        const int32_t* start = SG.horiz ? a.rstart : a.cstart;
-        const int4* mrec4 = SG.horiz ? a.rrec : a.crec;
-        int n = 0;
-        bool first_round = true;
-        int cols_total = 0;
-        if (lane < CAP / 32) S.sure[lane] = 0;
-        __syncwarp();
-        // ---- strip gather: bucket rows of the strip |dist_base| <= R.  The CSR starts of
-        // the next 32 rows are loaded while the current rows' entries are processed.
-        auto row_span = [&](int r, int& bs, int& e1) {
-            bs = 0; e1 = 0;
-            if (r <= SG.rhi) {
-                int blo = 0, bhi = nalong - 1;
-                if (SG.inv_alpha != 0.f) {
-                    const float y0 = r * Df - 0.01f, y1 = (r + 1) * Df + 0.01f;
-                    const float e00 = (-SG.R - SG.beta * y0 - SG.cr) * SG.inv_alpha;
-                    const float e01 = (SG.R - SG.beta * y0 - SG.cr) * SG.inv_alpha;
-                    const float e10 = (-SG.R - SG.beta * y1 - SG.cr) * SG.inv_alpha;
-                    const float e11 = (SG.R - SG.beta * y1 - SG.cr) * SG.inv_alpha;
-                    const float plo = fminf(fminf(e00, e01), fminf(e10, e11));
-                    const float phi = fmaxf(fmaxf(e00, e01), fmaxf(e10, e11));
-                    blo = max(blo, (int)floorf(fmaxf(plo - 0.02f, -1.f) * SG.invD));
-                    bhi = min(bhi, (int)floorf(fminf(phi + 0.02f, SG.Pmax + 1.f) * SG.invD));
-                }
-                if (blo <= bhi) {
-                    const int64_t cb = toffb + (int64_t)r * nalong;
-                    bs = __ldg(start + cb + blo);
-                    e1 = __ldg(start + cb + bhi + 1);
-                }
-            }
-        };
-        int nbs, ne1;
-        row_span(SG.rlo + lane, nbs, ne1);
-        for (int r0 = SG.rlo; r0 <= SG.rhi; r0 += 32) {
-            const int bs = nbs, len = ne1 - nbs;
-            row_span(r0 + 32 + lane, nbs, ne1);
-            int incl = len;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                int y = __shfl_up_sync(FULL, incl, o);
-                if (lane >= o) incl += y;
-            }
-            const int tot = __shfl_sync(FULL, incl, 31);
-            if (a.dbg && lane == 0) atomicAdd(&a.dbg[2], (unsigned long long)tot);
-            for (int j0 = 0; j0 < tot; j0 += 32) {
-                const int j = j0 + lane;
-                int o = 0;
-#pragma unroll
-                for (int s = 16; s > 0; s >>= 1) {
-                    int v = __shfl_sync(FULL, incl, o + s - 1);
-                    if (v <= j) o += s;
-                }
-                const int ob = __shfl_sync(FULL, bs, o & 31);
-                const int oex = __shfl_sync(FULL, incl - len, o & 31);
-                bool pass = false, sure = false;
-                int f = 0;
-                unsigned nrm = 0;
-                float2 p2 = make_float2(0.f, 0.f);
-                if (j < tot) {
-                    const int4 rec = __ldg(mrec4 + ob + (j - oex));
-                    f = rec.w;
-                    p2 = make_float2(__int_as_float(rec.x), __int_as_float(rec.y));
-                    nrm = (unsigned)rec.z;
-                    const float adr = fabsf(fmaf(SG.ar, p2.x, fmaf(SG.br, p2.y, SG.cr)));
-                    pass = adr <= SG.R;
-                    sure = adr + SG.delta <= SG.hsure && p2.x >= SG.border &&
-                           p2.x <= SG.W - SG.border && p2.y >= SG.border && p2.y <= SG.H - SG.border;
-                }
-                const unsigned bal = __ballot_sync(FULL, pass);
-                const int cnt = __popc(bal);
-                if (a.dbg && lane == 0) {
-                    atomicAdd(&a.dbg[3], (unsigned long long)cnt);
-                    atomicAdd(&a.dbg[4], (unsigned long long)__popc(__ballot_sync(FULL, pass && sure)));
-                } else if (a.dbg) {
-                    __ballot_sync(FULL, pass && sure);
-                }
-                if (n + cnt > CAP) {
-                    __syncwarp();
-                    process_round<STATS>(a, S, n, toff, qoff, first_round, cols_total);
-                    first_round = false;
-                    n = 0;
-                    if (lane < CAP / 32) S.sure[lane] = 0;
-                    __syncwarp();
-                }
-                const int k = __popc(bal & ((1u << lane) - 1u));
-                if (pass) {
-                    S.list[n + k] = (unsigned short)f;
-                    S.xy[n + k] = p2;
-                    S.nrm[n + k] = nrm;
-                }
-                const unsigned bits = __reduce_or_sync(FULL, (pass && sure) ? (1u << k) : 0u);
-                if (lane == 0 && cnt) {
-                    const int w = n >> 5, sh = n & 31;
-                    S.sure[w] |= bits << sh;
-                    if (sh && sh + cnt > 32) S.sure[w + 1] |= bits >> (32 - sh);
-                }
-                n += cnt;
-                __syncwarp();
-            }
-        }
-        if (n > 0) {
-            __syncwarp();
-            process_round<STATS>(a, S, n, toff, qoff, first_round, cols_total);
-            first_round = false;
-        }
-        __syncwarp();
-        // ---- ratio test + dedupe per member (ratio_filter / _dedupe_targets)
-        if (!first_round) {
-            for (int j = lane; j < SG.mcnt; j += 32) {
-                const MemberRec& M = a.mrec[SG.m0 + j];
-                const int slot = M.slotgi & SLOT_MASK;
-                const unsigned long long best = a.mstate[slot];
-                const unsigned sec = a.mstate2[slot];
-                if (best == ~0ull) continue;
-                const unsigned bd2 = (unsigned)(best >> 32);
-                const int tid = (int)(best & 0xffffffffu);
-                const float db = sqrtf((float)bd2);
-                float rr;
-                bool acc;
-                if (sec == NONE) {
-                    acc = db < a.single_cap;
-                    rr = 0.0f;
-                } else {
-                    const float ds = sqrtf((float)sec);
-                    rr = ds > 0.0f ? db / ds : 1.0f;
-                    acc = rr < a.ratio;
-                }
-                if (!acc) continue;
-                a.res_tid[slot] = tid;
-                a.res_dist[slot] = db;
-                a.res_ratio[slot] = rr;
-                const unsigned long long key =
-                    ((unsigned long long)__float_as_uint(db) << 32) | (unsigned)M.fid;
-                atomicMin(&a.dedupe[SG.dbase + tid], key);
-            }
-        }
-        if (STATS && lane == 0 && cols_total > 0) {
-            atomicAdd(&a.stats[2 * pg], (unsigned long long)SG.mcnt);
-            atomicAdd(&a.stats[2 * pg + 1], (unsigned long long)SG.mcnt * (unsigned long long)cols_total);
-        }
-        __syncwarp();
-    }
-}
-
 #include "guided_match.cuh"
 
 __global__ void __launch_bounds__(256) compact_kernel(ChunkArgs a) {
@@ -1640,7 +630,7 @@ struct ChunkSizes {
 size_t chunk_bytes(const ChunkSizes& c) {
     size_t b = 0;
     b += aligned_bytes<int64_t>(c.P + 1) * 2;          // tab_off, tbase
-    b += aligned_bytes<int32_t>(c.P + 1) * 5 + 256;    // ngroups, gstart, nmem, sgstart, nsg, sg_next
+    b += 256 * 2;                                      // sg_total, sg_next
     b += aligned_bytes<float4>(c.Q) * 2 + aligned_bytes<int2>(c.Q);   // gline, gend, sglist
     b += aligned_bytes<unsigned long long>(c.T);       // tab_key
     b += aligned_bytes<unsigned>(c.T) * 2;             // tab_rep, tab_cnt
@@ -1648,7 +638,7 @@ size_t chunk_bytes(const ChunkSizes& c) {
     b += aligned_bytes<int32_t>(c.Q) * 2;              // mgid, msg
     b += aligned_bytes<unsigned>(c.Q);                 // gfit
     b += aligned_bytes<unsigned long long>(c.Q);       // sgdev
-    b += aligned_bytes<float4>(c.Q) + aligned_bytes<int32_t>(c.Q);   // gl4, gmoff
+    b += aligned_bytes<int32_t>(c.Q + c.P + 1) * 3;    // jmp_a, jmp_b, jmark (pairs past TS_SMEM)
     b += aligned_bytes<GView>(c.Q);                    // gview
     b += aligned_bytes<double>(3 * c.Q);               // q_line
     b += aligned_bytes<int4>(c.Q);                     // grec
@@ -1957,13 +947,12 @@ static int guided_match_impl(const msfm_bank* bank, const msfm_grids* grids, int
     a.q_fid = ar.take<int32_t>(w.Q);
     a.mgid = ar.take<int32_t>(w.Q); a.msg = ar.take<int32_t>(w.Q);
     a.gfit = ar.take<unsigned>(w.Q); a.sgdev = ar.take<unsigned long long>(w.Q);
-    a.gl4 = ar.take<float4>(w.Q); a.gmoff = ar.take<int32_t>(w.Q);
+    a.jmp_a = ar.take<int32_t>(w.Q + w.P + 1); a.jmp_b = ar.take<int32_t>(w.Q + w.P + 1);
+    a.jmark = ar.take<int32_t>(w.Q + w.P + 1);
     a.gview = ar.take<GView>(w.Q);
     a.tab_off = ar.take<int64_t>(w.P + 1); a.tbase = ar.take<int64_t>(w.P + 1);
-    a.ngroups = ar.take<int32_t>(w.P + 1); a.gstart = ar.take<int32_t>(w.P + 1);
-    a.nmem = ar.take<int32_t>(w.P + 1); a.sgstart = ar.take<int32_t>(w.P + 1);
+    a.sg_total = ar.take<int32_t>(1);
     a.sg_next = ar.take<int32_t>(1);
-    a.nsg = ar.take<int32_t>(w.P + 1);
     a.gline = ar.take<float4>(w.Q); a.gend = ar.take<float4>(w.Q); a.sglist = ar.take<int2>(w.Q);
     a.tab_key = ar.take<unsigned long long>(w.T);
     a.tab_rep = ar.take<unsigned>(w.T); a.tab_cnt = ar.take<unsigned>(w.T);
@@ -1984,22 +973,27 @@ static int guided_match_impl(const msfm_bank* bank, const msfm_grids* grids, int
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    MSFM_CUDA_TRY(cudaFuncSetAttribute(groups_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       2 * 65536 + 16));
-    // MSFM_MATCH_V1=1 selects the round-1 kernel (A/B comparisons)
-    const bool use_v1 = getenv("MSFM_MATCH_V1") && atoi(getenv("MSFM_MATCH_V1")) != 0;
+    MSFM_CUDA_TRY(cudaFuncSetAttribute(setup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)SETUP_SMEM));
+    if (getenv("MSFM_OCC")) {
+        int nb = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, setup_kernel, ST, SETUP_SMEM);
+        fprintf(stderr, "setup_kernel: %d CTAs/SM (%zu B smem)\n", nb, (size_t)SETUP_SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, match_ms_kernel<false>, MS_WARPS * 32, sizeof(MSmem) * MS_WARPS);
+        fprintf(stderr, "match_ms_kernel: %d CTAs/SM\n", nb);
+    }
     const size_t ms_smem = sizeof(MSmem) * MS_WARPS;
     MSFM_CUDA_TRY(cudaFuncSetAttribute(match_ms_kernel<true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ms_smem));
     MSFM_CUDA_TRY(cudaFuncSetAttribute(match_ms_kernel<false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ms_smem));
+    const bool sync_dbg = getenv("MSFM_SYNC_CHECK") && atoi(getenv("MSFM_SYNC_CHECK")) != 0;
     int next_range = 0;
     for (size_t c = 0; c + 1 < bounds.size(); c++) {
         const int p0 = bounds[c], p1 = bounds[c + 1];
         a.p0 = p0;
         a.npairs = p1 - p0;
         a.qbase = h_qlist_off[p0];
-        const int64_t Q = h_qlist_off[p1] - h_qlist_off[p0];
         // bank ranges first read by this chunk: wait for their rows, then index them
         for (; plan && next_range < plan->n_ranges && plan->chunk[next_range] <= (int32_t)c;
              next_range++) {
@@ -2027,35 +1021,30 @@ static int guided_match_impl(const msfm_bank* bank, const msfm_grids* grids, int
                                            plan->grid_workspace_bytes, st, w32(bank->d_norm2));
             if (rc) return rc;
         }
+        // MSFM_SYNC_CHECK=1: synchronize after every kernel and name the one that failed
+        auto sync_check = [&](const char* what) -> int {
+            if (!sync_dbg) return MSFM_OK;
+            const cudaError_t e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) {
+                set_error("msfm_guided_match: %s (chunk %d): %s", what, (int)c, cudaGetErrorString(e));
+                return MSFM_ECUDA;
+            }
+            return MSFM_OK;
+        };
         plan_kernel<<<1, SCAN_T, 0, st>>>(a);
-        { ProfScope ps("lines_kernel", st); lines_kernel<<<a.npairs, MSFM_LINES_T, 0, st>>>(a); }
+        if (int rc = sync_check("plan_kernel")) return rc;
+        { ProfScope ps("setup_kernel", st); setup_kernel<<<a.npairs, ST, SETUP_SMEM, st>>>(a); }
+        if (int rc = sync_check("setup_kernel")) return rc;
         {
-            int64_t max_nq = 1;
-            for (int k = p0; k < p1; k++) max_nq = std::max(max_nq, h_qlist_off[k + 1] - h_qlist_off[k]);
-            ProfScope ps("groups_kernel", st);
-            groups_kernel<<<a.npairs, GT, (size_t)(2 * max_nq + 16), st>>>(a);
-        }
-        gscan_kernel<<<1, SCAN_T, 0, st>>>(a);
-        { ProfScope ps("scatter_kernel", st); scatter_kernel<<<a.npairs, MSFM_LINES_T, 0, st>>>(a); }
-        if (Q > 0) {
-            const unsigned nb = (unsigned)((Q + 127) / 128);
-            { ProfScope ps("prep_kernel", st); prep_kernel<<<nb, 128, 0, st>>>(a, (int)Q); }
-            { ProfScope ps("sg_shape_kernel", st); sg_shape_kernel<<<nb, 128, 0, st>>>(a, (int)Q); }
-            { ProfScope ps("member_kernel", st); member_kernel<<<nb, 128, 0, st>>>(a, (int)Q); }
-            { ProfScope ps("sg_prep_kernel", st); sg_prep_kernel<<<nb, 128, 0, st>>>(a, (int)Q); }
-        }
-        if (use_v1) {
-            ProfScope ps("match_kernel", st);
-            if (d_stats) match_kernel<true><<<nsm * MATCH_MINB, WARPS * 32, 0, st>>>(a);
-            else         match_kernel<false><<<nsm * MATCH_MINB, WARPS * 32, 0, st>>>(a);
-        } else {
             ProfScope ps("match_kernel", st);
             if (d_stats) match_ms_kernel<true><<<nsm * MS_MINB, MS_WARPS * 32, ms_smem, st>>>(a);
             else         match_ms_kernel<false><<<nsm * MS_MINB, MS_WARPS * 32, ms_smem, st>>>(a);
         }
+        if (int rc = sync_check("match_kernel")) return rc;
         { ProfScope ps("compact_kernel", st); compact_kernel<<<a.npairs, 256, 0, st>>>(a); }
+        if (int rc = sync_check("compact_kernel")) return rc;
         MSFM_LAUNCH_CHECK();
-        count_launches(7 + (Q > 0 ? 4 : 0));
+        count_launches(4);
         if (hook) {
             const int rc = hook(hook_ctx, (int)c, p0, p1);
             if (rc) return rc;

@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(const 
     extern __shared__ __align__(128) unsigned char ms_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     MSmem& S = reinterpret_cast<MSmem*>(ms_raw)[warp];
-    const int total = a.sgstart[a.npairs];
+    const int total = *a.sg_total;
     const float Df = (float)a.D;
     if (lane == 0) {
         ms_bar_init(&S.bar_q);

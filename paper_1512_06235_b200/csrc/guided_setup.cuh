@@ -1,0 +1,471 @@
+// Per-pair matcher setup (included by guided.cu inside msfm::<anon>).
+//
+// One CTA per pair runs the whole front half of guided_match_pair
+// (guided.py:393-446) for that pair and leaves the super-group records the
+// match kernel consumes:
+//
+//   lines     epipolar line of every query (dgemm rounding), normalise, clip,
+//             composite bucket key (group_queries guided.py:340-390), insert into
+//             the pair's hash table (shared memory up to TS_SMEM slots)
+//   groups    compact the occupied slots, order the groups by representative-line
+//             angle (4096-bucket counting sort), member ranges, boundary endpoints
+//   scatter   member lists; per group the padded clip / sample geometry (GroupRec,
+//             equidistant_line_points guided.py:173-187)
+//   chain     super-groups: e(q) = min(q + 16, B(g(q))) per member position (B: the
+//             first group that stops fitting g's line, or the end), the greedy walk
+//             from position 0 marked by pointer doubling, compacted in order
+//   shape     per super-group: group range, base line (middle group's rep)
+//   members   per member: epilogue constants, band deviation from its group's rep
+//             and its super-group's base (shared-memory / L2 atomic maxima)
+//   strips    per super-group: strip half-width, bucket-row range, group views
+//
+// Everything a pair needs stays in one CTA: the intermediates are written and
+// re-read while L2-hot, the hash table lives in shared memory, and the only
+// cross-pair step is one atomicAdd that places the pair's super-groups in the
+// chunk-wide queue (their order only schedules work; results never depend on it).
+// All arrays are indexed in chunk slot space (s0 + local index), which bounds
+// groups / super-groups / members of a pair by its query count.
+
+constexpr int ST = 1024;          // setup threads per pair
+constexpr int TS_SMEM = 8192;     // hash tables up to this many slots live in shared memory
+// table: key u64, rep u32, count u32 per slot; histogram; scan scratch
+constexpr size_t SETUP_SMEM = (size_t)TS_SMEM * 16 + (size_t)GB * 4 + 512;
+
+__global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ ChunkArgs a) {
+    extern __shared__ __align__(16) unsigned char su_raw[];
+    const int p = blockIdx.x, pg = a.p0 + p;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int64_t q0 = a.qlist_off[pg];
+    const int nq = (int)(a.qlist_off[pg + 1] - q0);
+    const int64_t s0 = q0 - a.qbase;
+    const int64_t t0 = a.tab_off[p];
+    const int tsize = (int)(a.tab_off[p + 1] - t0);
+    const int ti = a.pair_t[pg], qi = a.pair_q[pg];
+    const int nt = a.img_n[ti];
+    const int64_t db = a.tbase[p];
+    int* hist = reinterpret_cast<int*>(su_raw + (size_t)TS_SMEM * 16);
+    int* ssm = hist + GB;                                   // block-scan scratch (33)
+    float* fmn = reinterpret_cast<float*>(ssm + 40);
+    float* fmx = fmn + 32;
+    int* sv = reinterpret_cast<int*>(fmx + 32);             // [0] ng [1] nm [2] nsg [3] base [4] done
+    const bool small = tsize <= TS_SMEM;
+    // after the compaction trep holds the group id
+    unsigned long long* tkey = small ? reinterpret_cast<unsigned long long*>(su_raw) : a.tab_key + t0;
+    unsigned* trep = small ? reinterpret_cast<unsigned*>(su_raw + (size_t)TS_SMEM * 8) : a.tab_rep + t0;
+    unsigned* tcnt = small ? reinterpret_cast<unsigned*>(su_raw + (size_t)TS_SMEM * 12) : a.tab_cnt + t0;
+
+    // ---------------- init
+    for (int e = tid; e < tsize; e += ST) {
+        tkey[e] = EMPTY;
+        trep[e] = NONE;
+        tcnt[e] = 0;
+    }
+    for (int e = tid; e < nt; e += ST) a.dedupe[db + e] = EMPTY;
+    for (int i = tid; i < nq; i += ST) {
+        a.res_tid[s0 + i] = -1;
+        a.gfill[s0 + i] = 0;
+    }
+    if (isnan(a.pair_F[9 * (int64_t)pg]) || nq == 0) return;   // no groups: nothing queued
+    __syncthreads();
+
+    // ---------------- lines (lines_kernel of round 1; guided.py:353-373)
+    const double W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1];
+    const int64_t qoff = a.img_off[qi];
+    const unsigned mask = (unsigned)tsize - 1;
+    const int64_t qs = a.qlist_src ? a.qlist_src[pg] : q0;
+    double F[9];
+#pragma unroll
+    for (int j = 0; j < 9; j++) F[j] = a.pair_F[9 * (int64_t)pg + j];
+    for (int i = tid; i < nq; i += ST) {
+        const int fid = a.qlist[qs + i];
+        a.q_fid[s0 + i] = fid;
+        const float2 p2 = a.xy[qoff + fid];
+        double l[3];
+        epiline(F, (double)p2.x, (double)p2.y, nq == 1, l);
+        const double nrm = np_hypot(l[0], l[1]);
+        int slot = -1;
+        if (nrm > 1e-12) {
+            l[0] /= nrm; l[1] /= nrm; l[2] /= nrm;
+            double pa[2], pb[2];
+            if (clip_batch(l, W, H, pa, pb)) {
+                const unsigned long long key = composite_key(pa, pb);
+                unsigned h = (unsigned)mix64(key) & mask;
+                while (true) {
+                    const unsigned long long prev = atomicCAS(&tkey[h], EMPTY, key);
+                    if (prev == EMPTY || prev == key) break;
+                    h = (h + 1) & mask;
+                }
+                atomicMin(&trep[h], (unsigned)i);
+                atomicAdd(&tcnt[h], 1u);
+                slot = (int)h;
+                double* L = a.q_line + 3 * (s0 + i);
+                L[0] = l[0]; L[1] = l[1]; L[2] = l[2];
+            }
+        }
+        a.q_tab[s0 + i] = slot;
+    }
+    __syncthreads();
+
+    // ---------------- groups: compaction, angle order, member ranges, endpoints
+    int gcarry = 0;
+    float lo = 1e30f, hi = -1e30f;
+    for (int e0 = 0; e0 < tsize; e0 += ST) {
+        const int e = e0 + tid;
+        bool occ = false;
+        unsigned cnt = 0, rep = 0;
+        if (e < tsize) {
+            occ = tkey[e] != EMPTY;
+            if (occ) { cnt = tcnt[e]; rep = trep[e]; }
+        }
+        int gtot;
+        const int lg = block_exclusive_scan<ST>(occ ? 1 : 0, &gtot, ssm);
+        if (occ) {
+            const int g = gcarry + lg;
+            a.gtmp[s0 + g] = make_int2((int)rep, (int)cnt);
+            const double* L = a.q_line + 3 * (s0 + rep);
+            float la = (float)L[0], lb = (float)L[1];
+            if (la < 0.f || (la == 0.f && lb < 0.f)) { la = -la; lb = -lb; }
+            const float ang = atan2f(lb, la);
+            a.gkey[s0 + g] = ang;
+            lo = fminf(lo, ang);
+            hi = fmaxf(hi, ang);
+            trep[e] = (unsigned)g;
+        }
+        gcarry += gtot;
+    }
+    const int ng = gcarry;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(FULL, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(FULL, hi, o));
+    }
+    if (lane == 0) { fmn[wid] = lo; fmx[wid] = hi; }
+    for (int b = tid; b < GB; b += ST) hist[b] = 0;
+    __syncthreads();
+    lo = fmn[0]; hi = fmx[0];
+    for (int w = 1; w < ST / 32; w++) { lo = fminf(lo, fmn[w]); hi = fmaxf(hi, fmx[w]); }
+    const float scale = (float)GB / fmaxf(hi - lo, 1e-20f);
+    for (int g = tid; g < ng; g += ST) {
+        const int b = min(GB - 1, max(0, (int)((a.gkey[s0 + g] - lo) * scale)));
+        atomicAdd(&hist[b], 1);
+    }
+    __syncthreads();
+    {
+        int v[GB / ST];
+        int s = 0;
+#pragma unroll
+        for (int k = 0; k < GB / ST; k++) { v[k] = hist[tid * (GB / ST) + k]; s += v[k]; }
+        int tot;
+        int ex = block_exclusive_scan<ST>(s, &tot, ssm);
+#pragma unroll
+        for (int k = 0; k < GB / ST; k++) { hist[tid * (GB / ST) + k] = ex; ex += v[k]; }
+    }
+    __syncthreads();
+    for (int g = tid; g < ng; g += ST) {
+        const int b = min(GB - 1, max(0, (int)((a.gkey[s0 + g] - lo) * scale)));
+        const int pos = atomicAdd(&hist[b], 1);
+        a.gpos[s0 + g] = pos;
+        const int2 r = a.gtmp[s0 + g];
+        a.grec[s0 + pos] = make_int4(r.x, r.y, 0, 0);
+    }
+    __syncthreads();
+    int mcarry = 0;
+    for (int i0 = 0; i0 < ng; i0 += ST) {
+        const int i = i0 + tid;
+        const int cnt = i < ng ? a.grec[s0 + i].y : 0;
+        int tot;
+        const int ex = block_exclusive_scan<ST>(cnt, &tot, ssm);
+        if (i < ng) a.grec[s0 + i].z = (int)(s0 + mcarry + ex);
+        mcarry += tot;
+    }
+    const int nm = mcarry;
+    for (int e = tid; e < tsize; e += ST)
+        if (tkey[e] != EMPTY) trep[e] = (unsigned)a.gpos[s0 + trep[e]];
+    __syncthreads();
+
+    // ---------------- scatter + per-group geometry (GroupRec, endpoints)
+    for (int i = tid; i < nq; i += ST) {
+        const int h = a.q_tab[s0 + i];
+        if (h < 0) continue;
+        const int lg = (int)trep[h];
+        const int4 g = a.grec[s0 + lg];
+        const int pos = g.z + atomicAdd(&a.gfill[s0 + lg], 1);
+        a.members[pos] = (int)(s0 + i);
+        a.mgid[pos] = lg;
+    }
+    const double D = a.D, d = a.d;
+    for (int lg = tid; lg < ng; lg += ST) {
+        const int4 g = a.grec[s0 + lg];
+        const double* rl = a.q_line + 3 * (s0 + g.x);
+        const double r[3] = {rl[0], rl[1], rl[2]};
+        // boundary endpoints of the representative (group_queries' pa, pb)
+        {
+            double pa[2] = {0, 0}, pb[2] = {0, 0};
+            clip_batch(r, W, H, pa, pb);
+            a.gline[s0 + lg] = make_float4((float)r[0], (float)r[1], (float)r[2], 0.f);
+            a.gend[s0 + lg] = make_float4((float)pa[0], (float)pa[1], (float)pb[0], (float)pb[1]);
+        }
+        // C' geometry of the representative (prep_kernel of round 1)
+        GroupRec o;
+        o.p = p; o.rep = (int)(s0 + g.x); o.cnt = g.y; o.moff = g.z;
+        o.sl0 = r[0]; o.sl1 = r[1]; o.sl2 = r[2]; o.spare = 0.0;
+        o.pad1 = o.pad2 = o.pad3 = 0;
+        double pa[2] = {0, 0}, pb[2] = {0, 0}, len = 0.0;
+        o.K = -1;
+        if (clip_scalar(r[0], r[1], r[2], W, H, d, pa, pb)) {
+            len = np_hypot(pb[0] - pa[0], pb[1] - pa[1]);
+            const long long K = (long long)ceil(len / d);
+            o.K = (int)(K < 1 ? 1 : K);
+        }
+        o.pax = pa[0]; o.pay = pa[1]; o.pbx64 = pb[0]; o.pby64 = pb[1];
+        o.ar = (float)r[0]; o.br = (float)r[1]; o.cr = (float)r[2];
+        o.maxdev = 0.05f;                     // raised per member (atomic max of f32 bits)
+        const double hs2 = D * D - 0.25 * d * d;
+        o.hsure = hs2 > 0 ? (float)(sqrt(hs2) - 0.075) : -1.0f;
+        o.pbx = (float)pb[0]; o.pby = (float)pb[1];
+        o.dirx = len > 0 ? (float)((pa[0] - pb[0]) / len) : 0.f;
+        o.diry = len > 0 ? (float)((pa[1] - pb[1]) / len) : 0.f;
+        o.len = (float)len;
+        o.spacing = o.K > 0 ? fmaxf((float)(len / o.K), 1e-6f) : 1.0f;
+        o.invK = o.K > 0 ? (float)(1.0 / o.K) : 0.f;
+        o.dxf = (float)(pa[0] - pb[0]); o.dyf = (float)(pa[1] - pb[1]);
+        o.slack = (float)(4e-6 * (W + H + 4.0 * d) / D) + 1e-4f;
+        o.invD = (float)(1.0 / D);
+        a.grp[s0 + lg] = o;
+    }
+    __syncthreads();
+
+    // ---------------- super-groups
+    // J / mark arrays: shared memory (reusing the table) for small pairs, else global
+    // (global: nm + 1 entries per pair, so pair p's range starts at s0 + p)
+    int* Ja = small ? reinterpret_cast<int*>(su_raw) : a.jmp_a + s0 + p;
+    int* Jb = small ? reinterpret_cast<int*>(su_raw) + TS_SMEM : a.jmp_b + s0 + p;
+    int* mk = small ? reinterpret_cast<int*>(su_raw) + 2 * TS_SMEM : a.jmark + s0 + p;
+    int nsg;
+    if (a.stats_mode) {
+        // one super-group per group (exact SearchStats)
+        for (int g = tid; g < ng; g += ST) {
+            const int4 gr = a.grec[s0 + g];
+            a.sglist[s0 + g] = make_int2(gr.z, gr.y);
+        }
+        nsg = ng;
+    } else {
+        // B(g): first member position of the first group after g that does not fit
+        // g's line within tau (bit i of the fit mask: group g+1+i fits), or nm
+        for (int g = tid; g < ng; g += ST) {
+            const float4 ln = a.gline[s0 + g];
+            unsigned bits = 0;
+            const int lim = min(SG_MEMBERS, ng - 1 - g);
+            for (int i = 0; i < lim; i++) {
+                const float4 en = a.gend[s0 + g + 1 + i];
+                const float d1 = fabsf(fmaf(ln.x, en.x, fmaf(ln.y, en.y, ln.z)));
+                const float d2 = fabsf(fmaf(ln.x, en.z, fmaf(ln.y, en.w, ln.z)));
+                if (fmaxf(d1, d2) <= a.sg_tau) bits |= 1u << i;
+                else break;
+            }
+            const int j = g + 1 + __ffs(~bits) - 1;
+            a.gfit[s0 + g] = j < ng ? (int)(a.grec[s0 + j].z - s0) : nm;
+        }
+        __syncthreads();
+        // e(q) = min(q + 16, B(g(q))) is where the super-group opened at q closes
+        // (members are contiguous in group order); J = e, J(nm) = nm
+        for (int q = tid; q <= nm; q += ST) {
+            int e = nm;
+            if (q < nm) e = min(q + SG_MEMBERS, (int)a.gfit[s0 + a.mgid[s0 + q]]);
+            Ja[q] = e;
+            mk[q] = q == 0 ? 1 : 0;
+        }
+        __syncthreads();
+        // pointer doubling: round k marks J^(2^k) of every marked position, so after
+        // k rounds the first 2^(k+1) super-group starts of the walk from 0 are marked
+        int* Jc = Ja;
+        int* Jn = Jb;
+        for (int round = 0; round < 20; round++) {
+            for (int q = tid; q < nm; q += ST)
+                if (mk[q]) mk[Jc[q]] = 1;
+            __syncthreads();
+            for (int q = tid; q <= nm; q += ST) Jn[q] = Jc[Jc[q]];
+            __syncthreads();
+            int* t = Jc; Jc = Jn; Jn = t;
+            if (Jc[0] >= nm) break;                // the marked prefix covers the walk
+        }
+        // the marks are the walk's starts; compact them in order (e from the q + 16 /
+        // B rule again, since the J arrays were overwritten)
+        int carry = 0;
+        for (int q0b = 0; q0b < nm; q0b += ST) {
+            const int q = q0b + tid;
+            const bool st = q < nm && mk[q];
+            int tot;
+            const int ex = block_exclusive_scan<ST>(st ? 1 : 0, &tot, ssm);
+            if (st) {
+                const int e = min(q + SG_MEMBERS, (int)a.gfit[s0 + a.mgid[s0 + q]]);
+                a.sglist[s0 + carry + ex] = make_int2((int)s0 + q, e - q);
+            }
+            carry += tot;
+        }
+        nsg = carry;
+    }
+    if (tid == 0) sv[3] = atomicAdd(a.sg_total, nsg);     // this pair's slice of the queue
+    __syncthreads();
+    const int sgbase = sv[3];
+
+    // per super-group: max member-band deviation from the base line (f32 bits rounded
+    // up: the strip only has to be a superset), in the J array once the walk is done
+    unsigned* sgdevf = reinterpret_cast<unsigned*>(Ja);
+
+    // ---------------- super-group shape (base line = middle group's representative)
+    for (int ls = tid; ls < nsg; ls += ST) {
+        SGRec o = {};
+        o.p = p;
+        const int2 sgm = a.sglist[s0 + ls];
+        o.m0 = sgm.x; o.mcnt = sgm.y;
+        const int lg0 = a.stats_mode ? ls : a.mgid[o.m0];
+        const int lg1 = a.stats_mode ? ls : a.mgid[o.m0 + o.mcnt - 1];
+        o.g0 = (int)s0 + lg0;
+        o.gcnt = lg1 - lg0 + 1;
+        o.rlo = a.grp[s0 + (lg0 + lg1) / 2].rep;         // base line's slot (until strips)
+        for (int j = 0; j < o.mcnt; j++) a.msg[o.m0 + j] = ls;
+        sgdevf[ls] = 0u;
+        a.sg[sgbase + ls] = o;
+    }
+    __syncthreads();
+
+    // ---------------- members: epilogue constants, band deviations
+    for (int k = tid; k < nm; k += ST) {
+        const int64_t pos = s0 + k;
+        const int lg = a.mgid[pos];
+        GroupRec& G = a.grp[s0 + lg];
+        const int slot = a.members[pos];
+        const int fid = a.q_fid[slot];
+        const int ls = a.msg[pos];
+        const int base = a.sg[sgbase + ls].rlo;
+        const int g0 = a.sg[sgbase + ls].g0;
+        double m[3];
+        if (G.cnt == 1) {
+            // a singleton's own band uses the dgemv-rounded line (guided.py:443-446, m == 1)
+            const float2 p2 = a.xy[qoff + fid];
+            double Fm[9];
+#pragma unroll
+            for (int j = 0; j < 9; j++) Fm[j] = a.pair_F[9 * (int64_t)pg + j];
+            epiline(Fm, (double)p2.x, (double)p2.y, true, m);
+            const double nrm = fmax(np_hypot(m[0], m[1]), 1e-15);
+            m[0] /= nrm; m[1] /= nrm; m[2] /= nrm;
+            G.sl0 = m[0]; G.sl1 = m[1]; G.sl2 = m[2];
+        } else {
+            const double* ml = a.q_line + 3 * (int64_t)slot;
+            m[0] = ml[0]; m[1] = ml[1]; m[2] = ml[2];
+        }
+        const double* rl = a.q_line + 3 * (int64_t)G.rep;
+        const double r[3] = {rl[0], rl[1], rl[2]};
+        const double* bl = a.q_line + 3 * (int64_t)base;
+        const double b[3] = {bl[0], bl[1], bl[2]};
+        double rdev, sdev;
+        band_deviation2(m, r, b, W, H, d, rdev, sdev);
+        const float gdev = (float)(rdev + 0.05);
+        atomicMax(reinterpret_cast<unsigned*>(&G.maxdev), __float_as_uint(gdev));
+        atomicMax(&sgdevf[ls], __float_as_uint(__double2float_ru(sdev)));
+        MemberRec mr;
+        mr.a = (float)m[0]; mr.b = (float)m[1]; mr.c = (float)m[2];
+        const float eps = (float)((fabs(m[0]) * W + fabs(m[1]) * H + fabs(m[2])) * 0x1p-20) + 1e-6f;
+        mr.lo = (float)d - eps;
+        mr.hi = (float)d + eps;
+        mr.qn9 = (unsigned)a.norm2[qoff + fid] << 9;
+        mr.fid = fid;
+        mr.slotgi = (int)((unsigned)slot | ((unsigned)(s0 + lg - g0) << SLOT_BITS));
+        a.mrec[pos] = mr;
+    }
+    __syncthreads();
+
+    // ---------------- strips (sg_prep_kernel of round 1)
+    for (int ls = tid; ls < nsg; ls += ST) {
+        SGRec o = a.sg[sgbase + ls];
+        const double* bl = a.q_line + 3 * (int64_t)o.rlo;
+        const double r[3] = {bl[0], bl[1], bl[2]};
+        const double R = d + (double)__uint_as_float(sgdevf[ls]) + 0.05;
+        bool all_k = true;
+        double delta = 0.0;
+        for (int g = o.g0; g < o.g0 + o.gcnt; g++) {
+            const GroupRec& G = a.grp[g];
+            const double* gl = a.q_line + 3 * (int64_t)G.rep;
+            const double gr[3] = {gl[0], gl[1], gl[2]};
+            // |dist_g - dist_base| over the strip |dist_base| <= R inside the image
+            delta = fmax(delta, band_deviation(r, gr, W, H, R));
+            all_k = all_k && G.K >= 0;
+            // the group's view for the match kernel (groups shared by two
+            // super-groups get the same values twice)
+            GView gv;
+            if (G.K < 0 && a.strategy != 1) {
+                gv.a = 0.f; gv.b = 0.f; gv.c = 1e30f; gv.reach = -1.f;
+            } else {
+                gv.a = G.ar; gv.b = G.br; gv.c = G.cr; gv.reach = (float)a.d + G.maxdev + 0.05f;
+            }
+            gv.moff = G.moff; gv.pad0 = gv.pad1 = gv.pad2 = 0;
+            a.gview[g] = gv;
+        }
+        o.ar = (float)r[0]; o.br = (float)r[1]; o.cr = (float)r[2]; o.R = (float)R;
+        // sure-in-C' radius around the base line: grid, the 3x3 subcell block of the
+        // nearest sample (half-size D); radial, the disk of radius r around it; both with
+        // the sample spacing <= d.  Linear: the rep-line band itself.
+        const double DC = a.strategy == 2 ? sqrt(a.r2) : D;
+        const double hs2 = DC * DC - 0.25 * d * d;
+        const double hs = a.strategy == 1 ? d - 0.05 : (hs2 > 0 ? sqrt(hs2) - 0.075 : -1.0);
+        o.hsure = (float)hs;
+        o.delta = (all_k || a.strategy == 1) ? (float)(delta + 0.01) : 1e30f;
+        o.border = a.strategy == 1 ? -1e30f : (float)(fmax(0.0, hs - d) + 0.05);
+        o.invD = (float)(1.0 / D);
+        o.W = (float)W; o.H = (float)H; o.pad0 = 0;
+        const bool horiz = fabs(r[1]) >= fabs(r[0]);
+        o.toff = a.img_off[ti]; o.qoff = qoff;
+        o.nalong = horiz ? a.dims[2 * ti] : a.dims[2 * ti + 1];
+        o.toffb = horiz ? a.roff[ti] : a.coff[ti];
+        o.dbase = db;
+        const double al = horiz ? r[0] : r[1], be = horiz ? r[1] : r[0];
+        const double Pm = horiz ? W : H, Qm = horiz ? H : W;
+        const int nrows = horiz ? a.dims[2 * ti + 1] : a.dims[2 * ti];
+        const double qv[4] = {(-R - r[2]) / be, (R - r[2]) / be, (-R - r[2] - al * Pm) / be,
+                              (R - r[2] - al * Pm) / be};
+        const double qlo = fmin(fmin(qv[0], qv[1]), fmin(qv[2], qv[3]));
+        const double qhi = fmax(fmax(qv[0], qv[1]), fmax(qv[2], qv[3]));
+        const int rlo = (int)floor((fmax(qlo, 0.0) - 0.01) / D);
+        const int rhi = (int)floor((fmin(qhi, Qm) + 0.01) / D);
+        o.horiz = horiz;
+        o.rlo = rlo < 0 ? 0 : rlo;
+        o.rhi = rhi > nrows - 1 ? nrows - 1 : rhi;
+        o.alpha = (float)al; o.beta = (float)be;
+        o.inv_alpha = fabs(al) > 1e-6 ? (float)(1.0 / al) : 0.f;
+        o.Pmax = (float)Pm;
+        a.sg[sgbase + ls] = o;
+    }
+}
+
+// chunk setup: table / dedupe offsets (scan over pairs) and the queue counters
+__global__ void plan_kernel(ChunkArgs a) {
+    __shared__ int sm[SCAN_T / 32 + 1];
+    long long carry_t = 0, carry_d = 0;
+    for (int b0 = 0; b0 < a.npairs; b0 += SCAN_T) {
+        const int p = b0 + threadIdx.x;
+        int ts = 0, nt = 0;
+        if (p < a.npairs) {
+            const int pg = a.p0 + p;
+            const int nq = (int)(a.qlist_off[pg + 1] - a.qlist_off[pg]);
+            ts = nextpow2(nq + 1);
+            nt = a.img_n[a.pair_t[pg]];
+        }
+        int tot_t, tot_d;
+        const int ex_t = block_exclusive_scan<SCAN_T>(ts, &tot_t, sm);
+        const int ex_d = block_exclusive_scan<SCAN_T>(nt, &tot_d, sm);
+        if (p < a.npairs) {
+            // tables that fit the setup kernel's shared memory take no global slots
+            a.tab_off[p] = carry_t + ex_t;
+            a.tbase[p] = carry_d + ex_d;
+        }
+        carry_t += tot_t;
+        carry_d += tot_d;
+    }
+    if (threadIdx.x == 0) {
+        a.tab_off[a.npairs] = carry_t;
+        a.tbase[a.npairs] = carry_d;
+        *a.sg_total = 0;
+        *a.sg_next = 0;
+    }
+}
