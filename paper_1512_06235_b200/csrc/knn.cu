@@ -20,6 +20,7 @@
 #include <cuda.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <type_traits>
 
 #include "common.cuh"
@@ -50,6 +51,9 @@ struct KnnSmem {
     uint32_t tmem_base;
     long long merge_k1[EPI_WARPS / 4][TILE_M], merge_k2[EPI_WARPS / 4][TILE_M];
     int merge_i1[EPI_WARPS / 4][TILE_M];
+    // fvs[fn_stride]: |f|^2 of the current unit's image; with SAVEK it is followed by
+    // savek[EPI_WARPS * 32][16]: per epilogue thread, the 16 keys of the chunk that
+    // holds its running best (the column is looked up once per unit)
     alignas(16) int fvs[];   // |f|^2 of the current unit's image (fn_stride ints)
 };
 
@@ -174,6 +178,19 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
         : "r"(taddr));
 }
 
+__device__ __forceinline__ uint4 lds_u4(const void* p) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(smem_u32(p)));
+    return v;
+}
+
+__device__ __forceinline__ void sts_u4(void* p, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(p)), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
 __device__ __forceinline__ void tmem_wait_ld() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -199,7 +216,9 @@ __device__ __forceinline__ int unit_tiles(const KnnArgs& a, int m_tiles, int u, 
 // PLANES = 2: track length <= 100 (2S = lo + 256 hi, int32 keys, two accumulator
 // stages of 2 x 128 TMEM columns).  PLANES = 3: any track length up to 32767 (2S
 // in base-256 digits, int64 keys, one stage of 3 x 128 columns).
-template <int PLANES>
+constexpr size_t SAVEK_BYTES = (size_t)EPI_WARPS * 32 * 16 * sizeof(int);
+
+template <int PLANES, bool SAVEK>
 __global__ void __launch_bounds__(KN_THREADS, 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_constant__ CUtensorMap map_p1,
               const __grid_constant__ CUtensorMap map_p2, const __grid_constant__ CUtensorMap map_b,
@@ -333,22 +352,21 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_constant_
                 tc_fence_after();
                 const uint32_t t0 = tbase + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * 256 + half * EPI_COLS);
                 const int cbase = j * TILE_N + half * EPI_COLS;
-                const int4* fp = reinterpret_cast<const int4*>(S.fvs + cbase);
+                const uint4* fp = reinterpret_cast<const uint4*>(S.fvs + cbase);
                 const bool full = cbase + EPI_COLS <= n;
-#pragma unroll
-                for (int c0 = 0; c0 < EPI_COLS; c0 += 16) {
-                    uint32_t pl[PLANES][16];
-#pragma unroll
-                    for (int p = 0; p < PLANES; p++) tmem_ld16(t0 + p * 128 + c0, pl[p]);
+                // scores of one 16-column chunk -> running top-2 (FULLC: every column is
+                // a feature of the image, no per-column bound tests)
+                auto scores = [&](int c0, const uint32_t (&pl)[PLANES][16], auto full_tag) {
+                    constexpr bool FULLC = decltype(full_tag)::value;
                     int fv[16];
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
-                        const int4 f4 = fp[(c0 >> 2) + q];
-                        fv[4 * q] = f4.x; fv[4 * q + 1] = f4.y; fv[4 * q + 2] = f4.z; fv[4 * q + 3] = f4.w;
+                        const uint4 f4 = lds_u4(fp + (c0 >> 2) + q);
+                        fv[4 * q] = (int)f4.x; fv[4 * q + 1] = (int)f4.y;
+                        fv[4 * q + 2] = (int)f4.z; fv[4 * q + 3] = (int)f4.w;
                     }
-                    tmem_wait_ld();
                     const Key k1_in = k1;
-                    const int lim = full ? 16 : n - (cbase + c0);
+                    const int lim = FULLC ? 16 : n - (cbase + c0);
                     Key key[16];
 #pragma unroll
                     for (int c = 0; c < 16; c++) {
@@ -359,7 +377,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_constant_
                                            ((long long)pl[0][c] + ((long long)pl[1][c] << 8) +
                                             ((long long)pl[PLANES - 1][c] << 16)));
                         }
-                        if (!full && c >= lim) key[c] = KBIG;
+                        if (!FULLC && c >= lim) key[c] = KBIG;
                     }
                     // values only in the loop (three min/max per score); the column of a
                     // new best is found afterwards, rarely
@@ -368,17 +386,46 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_constant_
                         k2 = min(k2, max(k1, key[c]));
                         k1 = min(k1, key[c]);
                     }
-                    if (k1 != k1_in) {
+                    if (SAVEK) {
+                        // a new best: keep the chunk's keys (predicated stores, no
+                        // divergent search); its column is found once per unit
+                        if (k1 != k1_in) {
+                            uint4* sk = reinterpret_cast<uint4*>(S.fvs + a.fn_stride) + (ew * 32 + lane) * 4;
+#pragma unroll
+                            for (int q = 0; q < 4; q++)
+                                sts_u4(sk + q, make_uint4((unsigned)key[4 * q], (unsigned)key[4 * q + 1],
+                                                          (unsigned)key[4 * q + 2], (unsigned)key[4 * q + 3]));
+                            ibase = cbase + c0;
+                        }
+                    } else if (k1 != k1_in) {
 #pragma unroll
                         for (int c = 15; c >= 0; c--)
                             if (key[c] == k1) il = c;     // lowest column at the best
                         ibase = cbase + c0;
                     }
+                };
+                auto release = [&]() {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&S.t_empty[acc]);
+                };
+#pragma unroll
+                for (int c0 = 0; c0 < EPI_COLS; c0 += 16) {
+                    uint32_t pl[PLANES][16];
+#pragma unroll
+                    for (int p = 0; p < PLANES; p++) tmem_ld16(t0 + p * 128 + c0, pl[p]);
+                    tmem_wait_ld();
+                    if (full) scores(c0, pl, std::true_type{});
+                    else      scores(c0, pl, std::false_type{});
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&S.t_empty[acc]);
+                release();
                 if (++acc == ACC_STAGES) { acc = 0; acc_phase ^= 1; }
+            }
+            if (SAVEK && k1 != KBIG) {
+                const int* sk = S.fvs + a.fn_stride + (ew * 32 + lane) * 16;
+                il = 15;
+                for (int c = 15; c >= 0; c--)
+                    if ((Key)sk[c] == k1) il = c;         // lowest column at the best
             }
             int i1 = k1 == KBIG ? -1 : ibase + il;
             // merge the column slices of each row
@@ -818,9 +865,14 @@ extern "C" int msfm_knn2_tracks(const msfm_bank* bank, int32_t n_points, const i
                   max_n);
         return MSFM_EINVAL;
     }
-    MSFM_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    // the saved-chunk epilogue when its 32 KB fit next to the |f|^2 row
+    const bool savek = smem + SAVEK_BYTES <= 227 * 1024;
+    const size_t smem2 = savek ? smem + SAVEK_BYTES : smem;
+    MSFM_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)std::min<size_t>(smem + SAVEK_BYTES, 227 * 1024)));
+    MSFM_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
-    MSFM_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    MSFM_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
@@ -832,13 +884,14 @@ extern "C" int msfm_knn2_tracks(const msfm_bank* bank, int32_t n_points, const i
     {
         ProfScope ps("knn_tc_kernel", st);
         a.count = cnt; a.rowmap = s_map; a.n = s_n;
-        knn_tc_kernel<2><<<grid, KN_THREADS, smem, st>>>(ms0, ms1, ms1, mb, a);
+        if (savek) knn_tc_kernel<2, true><<<grid, KN_THREADS, smem2, st>>>(ms0, ms1, ms1, mb, a);
+        else       knn_tc_kernel<2, false><<<grid, KN_THREADS, smem, st>>>(ms0, ms1, ms1, mb, a);
     }
     MSFM_LAUNCH_CHECK();
     if (max_track > SHORT_N) {
         ProfScope ps("knn_tc_kernel_long", st);
         a.count = cnt + 1; a.rowmap = l_map; a.n = l_n;
-        knn_tc_kernel<3><<<grid, KN_THREADS, smem, st>>>(ml0, ml1, ml2, mb, a);
+        knn_tc_kernel<3, false><<<grid, KN_THREADS, smem, st>>>(ml0, ml1, ml2, mb, a);
         MSFM_LAUNCH_CHECK();
         count_launches(1);
     }
