@@ -28,6 +28,7 @@ constexpr int MS_WARPS = 4;            // warps per CTA
 #endif
 constexpr int MS_MINB = MSFM_MS_MINB;  // resident CTAs per SM
 constexpr int MS_CAP = 192;            // candidates per round (local index < 256)
+constexpr int MS_RING = 3;             // n8 tiles of candidate rows in flight (cp.async ring)
 constexpr int KEY_NONE = 0x7fffffff;
 #ifndef MSFM_PF3
 #define MSFM_PF3 0
@@ -51,6 +52,7 @@ struct alignas(16) MSmem {
     unsigned short cid[MS_CAP];    // target-local feature id
     unsigned short ulist[MS_CAP];  // candidates whose C' bits are still to be decided
     unsigned anyb[MS_CAP / 32];    // stats: candidate inside some member band
+    uint4 bring[MS_RING][64];      // candidate descriptor rows of the next tiles (swizzled 16-B chunks)
     uint64_t bar_q, bar_rec[2];
 };
 
@@ -104,6 +106,13 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_all;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 // descriptor rows of the slot's first 16 members: 128 16-B cp.async, 4 per lane
 // (completion: cp.async.wait_all before the SG starts)
@@ -293,34 +302,34 @@ __device__ __forceinline__ void ms_block(const ChunkArgs& a, MSmem& S, const MSl
         }
     }
     R.k1a = KEY_NONE; R.k2a = KEY_NONE; R.k1b = KEY_NONE; R.k2b = KEY_NONE;
-    const uint4* tdesc = reinterpret_cast<const uint4*>(a.desc + SG.toff * 128) + 2 * t;
-#if MSFM_PF3
-    // candidate descriptor fragments two tiles ahead (three register buffers)
-    uint4 p0a, p0b, p1a, p1b, p2a, p2b;
-    ms_ldB(S, tdesc, 0, g, p0a, p0b);
-    if (1 < ntile) ms_ldB(S, tdesc, 1, g, p1a, p1b);
-    for (int nt = 0; nt < ntile; nt += 3) {
-        if (nt + 2 < ntile) ms_ldB(S, tdesc, nt + 2, g, p2a, p2b);
-        ms_tile<CB, STATS, SLOTA>(a, S, L, R, mb0, nt, p0a, p0b);
-        if (nt + 1 >= ntile) break;
-        if (nt + 3 < ntile) ms_ldB(S, tdesc, nt + 3, g, p0a, p0b);
-        ms_tile<CB, STATS, SLOTA>(a, S, L, R, mb0, nt + 1, p1a, p1b);
-        if (nt + 2 >= ntile) break;
-        if (nt + 4 < ntile) ms_ldB(S, tdesc, nt + 4, g, p1a, p1b);
-        ms_tile<CB, STATS, SLOTA>(a, S, L, R, mb0, nt + 2, p2a, p2b);
+    // Candidate descriptor rows go through a ring of MS_RING tiles in shared memory:
+    // tile nt + 2's rows are copied (cp.async, 16-B chunks, chunk p of row r at slot
+    // p ^ r so a lane quad's reads spread over the banks) while tile nt is matched,
+    // so the tile loop never waits on an L2 round trip.
+    const uint8_t* tbase = a.desc + SG.toff * 128;
+    auto issue = [&](int nt) {
+        uint4* buf = S.bring[nt % MS_RING];
+#pragma unroll
+        for (int c = lane; c < 64; c += 32) {
+            const int row = c >> 3, part = c & 7;
+            const int f = S.cid[8 * nt + row];
+            cp_async16(buf + row * 8 + (part ^ row), tbase + (size_t)f * 128 + part * 16);
+        }
+    };
+    issue(0);
+    cp_async_commit();
+    if (1 < ntile) issue(1);
+    cp_async_commit();
+    for (int nt = 0; nt < ntile; nt++) {
+        if (nt + 2 < ntile) issue(nt + 2);
+        cp_async_commit();
+        cp_async_wait_group<2>();
+        __syncwarp();
+        const uint4* buf = S.bring[nt % MS_RING];
+        const uint4 u0 = buf[g * 8 + ((2 * t) ^ g)], u1 = buf[g * 8 + ((2 * t + 1) ^ g)];
+        ms_tile<CB, STATS, SLOTA>(a, S, L, R, mb0, nt, u0, u1);
+        __syncwarp();
     }
-#else
-    // candidate descriptor fragments one tile ahead (two register buffers)
-    uint4 p0a, p0b, p1a, p1b;
-    ms_ldB(S, tdesc, 0, g, p0a, p0b);
-    for (int nt = 0; nt < ntile; nt += 2) {
-        if (nt + 1 < ntile) ms_ldB(S, tdesc, nt + 1, g, p1a, p1b);
-        ms_tile<CB, STATS, SLOTA>(a, S, L, R, mb0, nt, p0a, p0b);
-        if (nt + 1 >= ntile) break;
-        if (nt + 2 < ntile) ms_ldB(S, tdesc, nt + 2, g, p0a, p0b);
-        ms_tile<CB, STATS, SLOTA>(a, S, L, R, mb0, nt + 1, p1a, p1b);
-    }
-#endif
     // ---- reduce the per-lane top-2 over the 4 lanes (t) sharing a member row
 #pragma unroll
     for (int o = 1; o < 4; o <<= 1) {

@@ -29,8 +29,7 @@ for chunk in chunks:
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     km, kn = _lib.profile_read("match_kernel")
-    others = {k: _lib.profile_read(k)[0] for k in ("setup_kernel", "lines_kernel", "groups_kernel", "scatter_kernel",
-              "prep_kernel", "sg_shape_kernel", "member_kernel", "sg_prep_kernel", "compact_kernel")}
+    others = {k: _lib.profile_read(k)[0] for k in ("setup_kernel", "gather_kernel", "compact_kernel")}
     _lib.profile_enable(False)
     n = int(res.count.sum())
     print(f"chunk={chunk}: step {ms:.2f} ms ({ms*1e3/len(ok):.2f} us/pair, {len(ok)/ms*1e3:.0f} pairs/s) "
