@@ -235,16 +235,22 @@ __global__ void grid_scatter_kernel(GridBuildArgs a) {
 // ------------------------------------------------------------------ matching
 // Per-group context, computed once by prep_kernel (one thread per group) so the
 // warp-per-group match kernel starts from fp32 values and never divides in fp64.
-struct GroupRec {
-    int p, rep, cnt, moff;                 // chunk-local pair, rep slot, members, member offset
-    float ar, br, cr, hsure;               // rep line (fp32), sure-in-C' radius
+// The first 32 bytes are what the setup kernel re-reads after writing the record;
+// the rest is only read by the match kernel (stored evict-first).
+struct alignas(16) GroupRec {
+    int rep, cnt, moff, K;                 // rep slot, members, member offset; K<0: the rep
+                                           // line misses the padded image (C' empty)
+    float maxdev, ar, br, cr;              // max member-band deviation; rep line (fp32)
+    int p, pad1;                           // chunk-local pair
+    float hsure, len;                      // sure-in-C' radius
     float pbx, pby, dirx, diry;            // padded segment origin (pb) and direction
-    float len, spacing, invK, invD;
-    float dxf, dyf, slack, maxdev;         // maxdev: max member-band deviation from the rep line
-    int K, pad1, pad2, pad3;               // K<0: the rep line misses the padded image (C' empty)
+    float spacing, invK, invD, dxf;
+    float dyf, slack;
+    int pad2, pad3;
     double pax, pay, pbx64, pby64;         // exact sample interpolation (guided.py:187)
     double sl0, sl1, sl2, spare;           // singleton member's own (dgemv) line
 };
+static_assert(sizeof(GroupRec) == 160, "GroupRec: 32 hot bytes + 128 match-only bytes");
 
 // Per-member epilogue constants (prep_kernel), indexed like members[].
 struct MemberRec {

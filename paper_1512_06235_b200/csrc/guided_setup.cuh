@@ -60,9 +60,11 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
         trep[e] = NONE;
         tcnt[e] = 0;
     }
-    for (int e = tid; e < nt; e += ST) a.dedupe[db + e] = EMPTY;
+    // outputs the setup never re-reads are stored evict-first (st.global.cs) so they
+    // do not push the phases' re-read data (lines, group records) out of L2
+    for (int e = tid; e < nt; e += ST) __stcs(reinterpret_cast<unsigned long long*>(a.dedupe + db + e), EMPTY);
     for (int i = tid; i < nq; i += ST) {
-        a.res_tid[s0 + i] = -1;
+        __stcs(a.res_tid + s0 + i, -1);
         a.gfill[s0 + i] = 0;
     }
     if (isnan(a.pair_F[9 * (int64_t)pg]) || nq == 0) return;   // no groups: nothing queued
@@ -231,7 +233,15 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
         o.dxf = (float)(pa[0] - pb[0]); o.dyf = (float)(pa[1] - pb[1]);
         o.slack = (float)(4e-6 * (W + H + 4.0 * d) / D) + 1e-4f;
         o.invD = (float)(1.0 / D);
-        a.grp[s0 + lg] = o;
+        {
+            // hot 32 B (re-read by the later phases): normal stores; the rest evict-first
+            int4* dst = reinterpret_cast<int4*>(a.grp + s0 + lg);
+            const int4* w = reinterpret_cast<const int4*>(&o);
+            dst[0] = w[0];
+            dst[1] = w[1];
+#pragma unroll
+            for (int k = 2; k < 10; k++) __stcs(dst + k, w[k]);
+        }
     }
     __syncthreads();
 
@@ -372,7 +382,11 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
         mr.qn9 = (unsigned)a.norm2[qoff + fid] << 9;
         mr.fid = fid;
         mr.slotgi = (int)((unsigned)slot | ((unsigned)(s0 + lg - g0) << SLOT_BITS));
-        a.mrec[pos] = mr;
+        {
+            const int4* w = reinterpret_cast<const int4*>(&mr);
+            __stcs(reinterpret_cast<int4*>(a.mrec + pos), w[0]);
+            __stcs(reinterpret_cast<int4*>(a.mrec + pos) + 1, w[1]);
+        }
     }
     __syncthreads();
 
@@ -400,7 +414,11 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
                 gv.a = G.ar; gv.b = G.br; gv.c = G.cr; gv.reach = (float)a.d + G.maxdev + 0.05f;
             }
             gv.moff = G.moff; gv.pad0 = gv.pad1 = gv.pad2 = 0;
-            a.gview[g] = gv;
+            {
+                const int4* w = reinterpret_cast<const int4*>(&gv);
+                __stcs(reinterpret_cast<int4*>(a.gview + g), w[0]);
+                __stcs(reinterpret_cast<int4*>(a.gview + g) + 1, w[1]);
+            }
         }
         o.ar = (float)r[0]; o.br = (float)r[1]; o.cr = (float)r[2]; o.R = (float)R;
         // sure-in-C' radius around the base line: grid, the 3x3 subcell block of the
@@ -434,7 +452,12 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
         o.alpha = (float)al; o.beta = (float)be;
         o.inv_alpha = fabs(al) > 1e-6 ? (float)(1.0 / al) : 0.f;
         o.Pmax = (float)Pm;
-        a.sg[sgbase + ls] = o;
+        {
+            int4* dst = reinterpret_cast<int4*>(a.sg + sgbase + ls);
+            const int4* w = reinterpret_cast<const int4*>(&o);
+#pragma unroll
+            for (int k = 0; k < 8; k++) __stcs(dst + k, w[k]);
+        }
     }
 }
 
