@@ -73,6 +73,15 @@ __device__ __forceinline__ void ms_bulk(void* dst, const void* src, uint32_t byt
         "l"(src), "r"(bytes), "r"(su32(b))
         : "memory");
 }
+// the same with an L2 evict-first policy: per-super-group records are read once
+__device__ __forceinline__ void ms_bulk_ef(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile(
+        "{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+        " cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], pol;\n}\n" ::"r"(su32(dst)),
+        "l"(src), "r"(bytes), "r"(su32(b))
+        : "memory");
+}
 // bounded parity wait: a protocol bug traps instead of hanging the GPU
 __device__ __forceinline__ void ms_wait(uint64_t* b, uint32_t parity) {
     const uint32_t addr = su32(b);
@@ -97,8 +106,8 @@ __device__ __forceinline__ void ms_issue_rec(const ChunkArgs& a, MSlot& L, uint6
     const SGRec& SG = L.sg;
     const int nm = min(SG.mcnt, 16), ng = SG.gcnt;
     ms_expect(bar, (uint32_t)(nm * sizeof(MemberRec) + ng * sizeof(GView)));
-    if (nm) ms_bulk(L.mr, a.mrec + SG.m0, nm * sizeof(MemberRec), bar);
-    if (ng) ms_bulk(L.gv, a.gview + SG.g0, ng * sizeof(GView), bar);
+    if (nm) ms_bulk_ef(L.mr, a.mrec + SG.m0, nm * sizeof(MemberRec), bar);
+    if (ng) ms_bulk_ef(L.gv, a.gview + SG.g0, ng * sizeof(GView), bar);
 }
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -500,7 +509,7 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(const 
         const int sid2 = claim();
         if (sid2 < total && lane == 0) {
             ms_expect(&S.bar_q, (uint32_t)sizeof(SGRec));
-            ms_bulk(&S.sgq, a.sg + sid2, sizeof(SGRec), &S.bar_q);
+            ms_bulk_ef(&S.sgq, a.sg + sid2, sizeof(SGRec), &S.bar_q);
         }
         // this SG's member descriptor rows (cp.async issued during the last SG)
         cp_async_wait_all();
