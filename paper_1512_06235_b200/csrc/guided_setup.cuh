@@ -31,6 +31,95 @@ constexpr int TS_SMEM = 8192;     // hash tables up to this many slots live in s
 // table: key u64, rep u32, count u32 per slot; histogram; scan scratch
 constexpr size_t SETUP_SMEM = (size_t)TS_SMEM * 16 + (size_t)GB * 4 + 512;
 
+// Upper bounds of |dist_m - dist_r| (and - dist_b) over the member band (|dist_m| <=
+// B = d + 0.5) inside the image, in fp32: the polygon's vertices (image corners inside
+// the band, band-edge crossings of the borders) with every inclusion test widened by
+// half a pixel and the result raised by 0.01 px.  Extra evaluation points only raise
+// the maximum, and the fp32 errors (~1e-3 px on 3k-px images) are far below the
+// margins, so these stay upper bounds; the deviations only size strips and C'-test
+// reaches, never decide a match.
+__device__ void band_deviation2_f(const double md[3], const double rd[3], const double bd[3], float W,
+                                  float H, float d, float& dev_r, float& dev_b) {
+    const float m0 = (float)md[0], m1 = (float)md[1], m2 = (float)md[2];
+    const float ra = (float)(md[0] - rd[0]), rb = (float)(md[1] - rd[1]), rc = (float)(md[2] - rd[2]);
+    const float ba = (float)(md[0] - bd[0]), bb = (float)(md[1] - bd[1]), bc = (float)(md[2] - bd[2]);
+    const float B = d + 0.5f, Bc = B + 0.01f, tol = 0.5f;
+    float vr = 0.f, vb = 0.f;
+    const float cx[4] = {0.f, W, 0.f, W}, cy[4] = {0.f, 0.f, H, H};
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        if (fabsf(fmaf(m0, cx[k], fmaf(m1, cy[k], m2))) <= Bc) {
+            vr = fmaxf(vr, fabsf(fmaf(ra, cx[k], fmaf(rb, cy[k], rc))));
+            vb = fmaxf(vb, fabsf(fmaf(ba, cx[k], fmaf(bb, cy[k], bc))));
+        }
+    }
+    const float i1 = fabsf(m1) > 1e-12f ? 1.0f / m1 : 0.f;
+    const float i0 = fabsf(m0) > 1e-12f ? 1.0f / m0 : 0.f;
+#pragma unroll
+    for (int s = -1; s <= 1; s += 2) {
+        if (i1 != 0.f) {
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+                const float x = e ? W : 0.f;
+                const float y = (s * B - m2 - m0 * x) * i1;
+                if (y >= -tol && y <= H + tol) {
+                    vr = fmaxf(vr, fabsf(fmaf(ra, x, fmaf(rb, y, rc))));
+                    vb = fmaxf(vb, fabsf(fmaf(ba, x, fmaf(bb, y, bc))));
+                }
+            }
+        }
+        if (i0 != 0.f) {
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+                const float y = e ? H : 0.f;
+                const float x = (s * B - m2 - m1 * y) * i0;
+                if (x >= -tol && x <= W + tol) {
+                    vr = fmaxf(vr, fabsf(fmaf(ra, x, fmaf(rb, y, rc))));
+                    vb = fmaxf(vb, fabsf(fmaf(ba, x, fmaf(bb, y, bc))));
+                }
+            }
+        }
+    }
+    dev_r = vr + 0.01f;
+    dev_b = vb + 0.01f;
+}
+
+// max |dist_g - dist_base| over the strip |dist_base| <= R inside the image (fp32
+// upper bound, as above)
+__device__ float band_deviation_f(const double bd[3], const double gd[3], float W, float H, float R) {
+    const float m0 = (float)bd[0], m1 = (float)bd[1], m2 = (float)bd[2];
+    const float da = (float)(bd[0] - gd[0]), db = (float)(bd[1] - gd[1]), dc = (float)(bd[2] - gd[2]);
+    const float Rc = R + 0.01f, tol = 0.5f;
+    float v = 0.f;
+    const float cx[4] = {0.f, W, 0.f, W}, cy[4] = {0.f, 0.f, H, H};
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+        if (fabsf(fmaf(m0, cx[k], fmaf(m1, cy[k], m2))) <= Rc)
+            v = fmaxf(v, fabsf(fmaf(da, cx[k], fmaf(db, cy[k], dc))));
+    const float i1 = fabsf(m1) > 1e-12f ? 1.0f / m1 : 0.f;
+    const float i0 = fabsf(m0) > 1e-12f ? 1.0f / m0 : 0.f;
+#pragma unroll
+    for (int s = -1; s <= 1; s += 2) {
+        if (i1 != 0.f) {
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+                const float x = e ? W : 0.f;
+                const float y = (s * R - m2 - m0 * x) * i1;
+                if (y >= -tol && y <= H + tol) v = fmaxf(v, fabsf(fmaf(da, x, fmaf(db, y, dc))));
+            }
+        }
+        if (i0 != 0.f) {
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+                const float y = e ? H : 0.f;
+                const float x = (s * R - m2 - m1 * y) * i0;
+                if (x >= -tol && x <= W + tol) v = fmaxf(v, fabsf(fmaf(da, x, fmaf(db, y, dc))));
+            }
+        }
+    }
+    return v + 0.01f;
+}
+
 __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ ChunkArgs a) {
     extern __shared__ __align__(16) unsigned char su_raw[];
     const int p = blockIdx.x, pg = a.p0 + p;
@@ -369,11 +458,11 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
         const double r[3] = {rl[0], rl[1], rl[2]};
         const double* bl = a.q_line + 3 * (int64_t)base;
         const double b[3] = {bl[0], bl[1], bl[2]};
-        double rdev, sdev;
-        band_deviation2(m, r, b, W, H, d, rdev, sdev);
-        const float gdev = (float)(rdev + 0.05);
+        float rdev, sdev;
+        band_deviation2_f(m, r, b, (float)W, (float)H, (float)d, rdev, sdev);
+        const float gdev = rdev + 0.05f;
         atomicMax(reinterpret_cast<unsigned*>(&G.maxdev), __float_as_uint(gdev));
-        atomicMax(&sgdevf[ls], __float_as_uint(__double2float_ru(sdev)));
+        atomicMax(&sgdevf[ls], __float_as_uint(sdev));
         MemberRec mr;
         mr.a = (float)m[0]; mr.b = (float)m[1]; mr.c = (float)m[2];
         const float eps = (float)((fabs(m[0]) * W + fabs(m[1]) * H + fabs(m[2])) * 0x1p-20) + 1e-6f;
@@ -403,7 +492,7 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
             const double* gl = a.q_line + 3 * (int64_t)G.rep;
             const double gr[3] = {gl[0], gl[1], gl[2]};
             // |dist_g - dist_base| over the strip |dist_base| <= R inside the image
-            delta = fmax(delta, band_deviation(r, gr, W, H, R));
+            delta = fmax(delta, (double)band_deviation_f(r, gr, (float)W, (float)H, (float)R));
             all_k = all_k && G.K >= 0;
             // the group's view for the match kernel (groups shared by two
             // super-groups get the same values twice)
