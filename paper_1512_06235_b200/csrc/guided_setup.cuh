@@ -142,6 +142,19 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
     unsigned long long* tkey = small ? reinterpret_cast<unsigned long long*>(su_raw) : a.tab_key + t0;
     unsigned* trep = small ? reinterpret_cast<unsigned*>(su_raw + (size_t)TS_SMEM * 8) : a.tab_rep + t0;
     unsigned* tcnt = small ? reinterpret_cast<unsigned*>(su_raw + (size_t)TS_SMEM * 12) : a.tab_cnt + t0;
+    // small pairs keep the per-position / per-group indices the later phases re-read
+    // as u16 in shared memory the table and histogram free up: the member's group
+    // (from the scatter on, over the count array), its query (over the histogram),
+    // each group's fit boundary (chain phase) and then each member's super-group
+    // (both over the count array's second half)
+    unsigned short* mg16 = reinterpret_cast<unsigned short*>(su_raw + (size_t)TS_SMEM * 12);
+    unsigned short* fit16 = mg16 + TS_SMEM;
+    unsigned short* sg16 = mg16 + TS_SMEM;
+    unsigned short* mq16 = reinterpret_cast<unsigned short*>(su_raw + (size_t)TS_SMEM * 16);
+    auto MGID = [&](int k) { return small ? (int)mg16[k] : a.mgid[s0 + k]; };
+    auto MSG = [&](int k) { return small ? (int)sg16[k] : a.msg[s0 + k]; };
+    auto MSLOT = [&](int k) { return small ? (int)(s0 + mq16[k]) : a.members[s0 + k]; };
+    auto GFIT = [&](int g) { return small ? (int)fit16[g] : (int)a.gfit[s0 + g]; };
 
     // ---------------- init
     for (int e = tid; e < tsize; e += ST) {
@@ -281,8 +294,13 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
         const int lg = (int)trep[h];
         const int4 g = a.grec[s0 + lg];
         const int pos = g.z + atomicAdd(&a.gfill[s0 + lg], 1);
-        a.members[pos] = (int)(s0 + i);
-        a.mgid[pos] = lg;
+        if (small) {
+            mg16[pos - s0] = (unsigned short)lg;
+            mq16[pos - s0] = (unsigned short)i;
+        } else {
+            a.members[pos] = (int)(s0 + i);
+            a.mgid[pos] = lg;
+        }
     }
     const double D = a.D, d = a.d;
     for (int lg = tid; lg < ng; lg += ST) {
@@ -363,14 +381,16 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
                 else break;
             }
             const int j = g + 1 + __ffs(~bits) - 1;
-            a.gfit[s0 + g] = j < ng ? (int)(a.grec[s0 + j].z - s0) : nm;
+            const int bnd = j < ng ? (int)(a.grec[s0 + j].z - s0) : nm;
+            if (small) fit16[g] = (unsigned short)bnd;
+            else a.gfit[s0 + g] = bnd;
         }
         __syncthreads();
         // e(q) = min(q + 16, B(g(q))) is where the super-group opened at q closes
         // (members are contiguous in group order); J = e, J(nm) = nm
         for (int q = tid; q <= nm; q += ST) {
             int e = nm;
-            if (q < nm) e = min(q + SG_MEMBERS, (int)a.gfit[s0 + a.mgid[s0 + q]]);
+            if (q < nm) e = min(q + SG_MEMBERS, GFIT(MGID(q)));
             Ja[q] = e;
             mk[q] = q == 0 ? 1 : 0;
         }
@@ -397,7 +417,7 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
             int tot;
             const int ex = block_exclusive_scan<ST>(st ? 1 : 0, &tot, ssm);
             if (st) {
-                const int e = min(q + SG_MEMBERS, (int)a.gfit[s0 + a.mgid[s0 + q]]);
+                const int e = min(q + SG_MEMBERS, GFIT(MGID(q)));
                 a.sglist[s0 + carry + ex] = make_int2((int)s0 + q, e - q);
             }
             carry += tot;
@@ -411,6 +431,7 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
     // per super-group: max member-band deviation from the base line (f32 bits rounded
     // up: the strip only has to be a superset), in the J array once the walk is done
     unsigned* sgdevf = reinterpret_cast<unsigned*>(Ja);
+    int2* sgbl = small ? reinterpret_cast<int2*>(Jb) : reinterpret_cast<int2*>(a.sglist + s0) + 0;
 
     // ---------------- super-group shape (base line = middle group's representative)
     for (int ls = tid; ls < nsg; ls += ST) {
@@ -418,13 +439,17 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
         o.p = p;
         const int2 sgm = a.sglist[s0 + ls];
         o.m0 = sgm.x; o.mcnt = sgm.y;
-        const int lg0 = a.stats_mode ? ls : a.mgid[o.m0];
-        const int lg1 = a.stats_mode ? ls : a.mgid[o.m0 + o.mcnt - 1];
+        const int lg0 = a.stats_mode ? ls : MGID(o.m0 - (int)s0);
+        const int lg1 = a.stats_mode ? ls : MGID(o.m0 + o.mcnt - 1 - (int)s0);
         o.g0 = (int)s0 + lg0;
         o.gcnt = lg1 - lg0 + 1;
         o.rlo = a.grp[s0 + (lg0 + lg1) / 2].rep;         // base line's slot (until strips)
-        for (int j = 0; j < o.mcnt; j++) a.msg[o.m0 + j] = ls;
+        for (int j = 0; j < o.mcnt; j++) {
+            if (small) sg16[o.m0 - s0 + j] = (unsigned short)ls;
+            else a.msg[o.m0 + j] = ls;
+        }
         sgdevf[ls] = 0u;
+        sgbl[ls] = make_int2(o.rlo, lg0);
         a.sg[sgbase + ls] = o;
     }
     __syncthreads();
@@ -432,13 +457,14 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
     // ---------------- members: epilogue constants, band deviations
     for (int k = tid; k < nm; k += ST) {
         const int64_t pos = s0 + k;
-        const int lg = a.mgid[pos];
+        const int lg = MGID(k);
         GroupRec& G = a.grp[s0 + lg];
-        const int slot = a.members[pos];
+        const int slot = MSLOT(k);
         const int fid = a.q_fid[slot];
-        const int ls = a.msg[pos];
-        const int base = a.sg[sgbase + ls].rlo;
-        const int g0 = a.sg[sgbase + ls].g0;
+        const int ls = MSG(k);
+        const int2 bl2 = sgbl[ls];
+        const int base = bl2.x;
+        const int g0 = (int)s0 + bl2.y;
         double m[3];
         if (G.cnt == 1) {
             // a singleton's own band uses the dgemv-rounded line (guided.py:443-446, m == 1)
