@@ -32,17 +32,18 @@ constexpr int TS_SMEM = 8192;     // hash tables up to this many slots live in s
 constexpr size_t SETUP_SMEM = (size_t)TS_SMEM * 16 + (size_t)GB * 4 + 512;
 
 // Upper bounds of |dist_m - dist_r| (and - dist_b) over the member band (|dist_m| <=
-// B = d + 0.5) inside the image, in fp32: the polygon's vertices (image corners inside
+// B = d + 0.5) inside the image, in fp32 (lines rounded to f32: < 1e-3 px on 3k-px
+// images): the polygon's vertices (image corners inside
 // the band, band-edge crossings of the borders) with every inclusion test widened by
 // half a pixel and the result raised by 0.01 px.  Extra evaluation points only raise
 // the maximum, and the fp32 errors (~1e-3 px on 3k-px images) are far below the
 // margins, so these stay upper bounds; the deviations only size strips and C'-test
 // reaches, never decide a match.
-__device__ void band_deviation2_f(const double md[3], const double rd[3], const double bd[3], float W,
+__device__ void band_deviation2_f(const float m[3], const float r[3], const float b[3], float W,
                                   float H, float d, float& dev_r, float& dev_b) {
-    const float m0 = (float)md[0], m1 = (float)md[1], m2 = (float)md[2];
-    const float ra = (float)(md[0] - rd[0]), rb = (float)(md[1] - rd[1]), rc = (float)(md[2] - rd[2]);
-    const float ba = (float)(md[0] - bd[0]), bb = (float)(md[1] - bd[1]), bc = (float)(md[2] - bd[2]);
+    const float m0 = m[0], m1 = m[1], m2 = m[2];
+    const float ra = m0 - r[0], rb = m1 - r[1], rc = m2 - r[2];
+    const float ba = m0 - b[0], bb = m1 - b[1], bc = m2 - b[2];
     const float B = d + 0.5f, Bc = B + 0.01f, tol = 0.5f;
     float vr = 0.f, vb = 0.f;
     const float cx[4] = {0.f, W, 0.f, W}, cy[4] = {0.f, 0.f, H, H};
@@ -86,9 +87,9 @@ __device__ void band_deviation2_f(const double md[3], const double rd[3], const 
 
 // max |dist_g - dist_base| over the strip |dist_base| <= R inside the image (fp32
 // upper bound, as above)
-__device__ float band_deviation_f(const double bd[3], const double gd[3], float W, float H, float R) {
-    const float m0 = (float)bd[0], m1 = (float)bd[1], m2 = (float)bd[2];
-    const float da = (float)(bd[0] - gd[0]), db = (float)(bd[1] - gd[1]), dc = (float)(bd[2] - gd[2]);
+__device__ float band_deviation_f(const float b[3], const float g[3], float W, float H, float R) {
+    const float m0 = b[0], m1 = b[1], m2 = b[2];
+    const float da = m0 - g[0], db = m1 - g[1], dc = m2 - g[2];
     const float Rc = R + 0.01f, tol = 0.5f;
     float v = 0.f;
     const float cx[4] = {0.f, W, 0.f, W}, cy[4] = {0.f, 0.f, H, H};
@@ -449,7 +450,7 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
             else a.msg[o.m0 + j] = ls;
         }
         sgdevf[ls] = 0u;
-        sgbl[ls] = make_int2(o.rlo, lg0);
+        sgbl[ls] = make_int2((lg0 + lg1) / 2, lg0);
         a.sg[sgbase + ls] = o;
     }
     __syncthreads();
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
         const int fid = a.q_fid[slot];
         const int ls = MSG(k);
         const int2 bl2 = sgbl[ls];
-        const int base = bl2.x;
+        const GroupRec& GB = a.grp[s0 + bl2.x];     // the super-group's base group
         const int g0 = (int)s0 + bl2.y;
         double m[3];
         if (G.cnt == 1) {
@@ -480,12 +481,12 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
             const double* ml = a.q_line + 3 * (int64_t)slot;
             m[0] = ml[0]; m[1] = ml[1]; m[2] = ml[2];
         }
-        const double* rl = a.q_line + 3 * (int64_t)G.rep;
-        const double r[3] = {rl[0], rl[1], rl[2]};
-        const double* bl = a.q_line + 3 * (int64_t)base;
-        const double b[3] = {bl[0], bl[1], bl[2]};
+        // (the group's and the base's rep lines as the f32 copies of their records)
+        const float mf[3] = {(float)m[0], (float)m[1], (float)m[2]};
+        const float r[3] = {G.ar, G.br, G.cr};
+        const float b[3] = {GB.ar, GB.br, GB.cr};
         float rdev, sdev;
-        band_deviation2_f(m, r, b, (float)W, (float)H, (float)d, rdev, sdev);
+        band_deviation2_f(mf, r, b, (float)W, (float)H, (float)d, rdev, sdev);
         const float gdev = rdev + 0.05f;
         atomicMax(reinterpret_cast<unsigned*>(&G.maxdev), __float_as_uint(gdev));
         atomicMax(&sgdevf[ls], __float_as_uint(sdev));
@@ -513,12 +514,12 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
         const double R = d + (double)__uint_as_float(sgdevf[ls]) + 0.05;
         bool all_k = true;
         double delta = 0.0;
+        const float rf[3] = {(float)r[0], (float)r[1], (float)r[2]};
         for (int g = o.g0; g < o.g0 + o.gcnt; g++) {
             const GroupRec& G = a.grp[g];
-            const double* gl = a.q_line + 3 * (int64_t)G.rep;
-            const double gr[3] = {gl[0], gl[1], gl[2]};
+            const float gr[3] = {G.ar, G.br, G.cr};
             // |dist_g - dist_base| over the strip |dist_base| <= R inside the image
-            delta = fmax(delta, (double)band_deviation_f(r, gr, (float)W, (float)H, (float)R));
+            delta = fmax(delta, (double)band_deviation_f(rf, gr, (float)W, (float)H, (float)R));
             all_k = all_k && G.K >= 0;
             // the group's view for the match kernel (groups shared by two
             // super-groups get the same values twice)
