@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
     for (int e = tid; e < nt; e += ST) __stcs(reinterpret_cast<unsigned long long*>(a.dedupe + db + e), EMPTY);
     for (int i = tid; i < nq; i += ST) {
         __stcs(a.res_tid + s0 + i, -1);
-        a.gfill[s0 + i] = 0;
+        if (!small) a.gfill[s0 + i] = 0;
     }
     if (isnan(a.pair_F[9 * (int64_t)pg]) || nq == 0) return;   // no groups: nothing queued
     __syncthreads();
@@ -289,12 +289,18 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
     __syncthreads();
 
     // ---------------- scatter + per-group geometry (GroupRec, endpoints)
+    // member fill counters: shared memory over the dead key array (small pairs)
+    unsigned* gfill = small ? reinterpret_cast<unsigned*>(su_raw) : reinterpret_cast<unsigned*>(a.gfill + s0);
+    if (small) {
+        for (int g = tid; g < ng; g += ST) gfill[g] = 0u;
+        __syncthreads();
+    }
     for (int i = tid; i < nq; i += ST) {
         const int h = a.q_tab[s0 + i];
         if (h < 0) continue;
         const int lg = (int)trep[h];
         const int4 g = a.grec[s0 + lg];
-        const int pos = g.z + atomicAdd(&a.gfill[s0 + lg], 1);
+        const int pos = g.z + (int)atomicAdd(&gfill[lg], 1u);
         if (small) {
             mg16[pos - s0] = (unsigned short)lg;
             mq16[pos - s0] = (unsigned short)i;
