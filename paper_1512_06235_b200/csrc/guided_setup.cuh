@@ -438,7 +438,8 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
     // per super-group: max member-band deviation from the base line (f32 bits rounded
     // up: the strip only has to be a superset), in the J array once the walk is done
     unsigned* sgdevf = reinterpret_cast<unsigned*>(Ja);
-    int2* sgbl = small ? reinterpret_cast<int2*>(Jb) : reinterpret_cast<int2*>(a.sglist + s0) + 0;
+    unsigned* sgbl = reinterpret_cast<unsigned*>(Jb);     // base group | first group << 16
+    unsigned* sgdelf = reinterpret_cast<unsigned*>(mk);   // max rep deviation (f32 bits; inf: a rep misses)
 
     // ---------------- super-group shape (base line = middle group's representative)
     for (int ls = tid; ls < nsg; ls += ST) {
@@ -456,7 +457,8 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
             else a.msg[o.m0 + j] = ls;
         }
         sgdevf[ls] = 0u;
-        sgbl[ls] = make_int2((lg0 + lg1) / 2, lg0);
+        sgbl[ls] = (unsigned)((lg0 + lg1) / 2) | ((unsigned)lg0 << 16);
+        sgdelf[ls] = 0u;
         a.sg[sgbase + ls] = o;
     }
     __syncthreads();
@@ -469,9 +471,9 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
         const int slot = MSLOT(k);
         const int fid = a.q_fid[slot];
         const int ls = MSG(k);
-        const int2 bl2 = sgbl[ls];
-        const GroupRec& GB = a.grp[s0 + bl2.x];     // the super-group's base group
-        const int g0 = (int)s0 + bl2.y;
+        const unsigned bl2 = sgbl[ls];
+        const GroupRec& GB = a.grp[s0 + (bl2 & 0xffffu)];     // the super-group's base group
+        const int g0 = (int)s0 + (int)(bl2 >> 16);
         double m[3];
         if (G.cnt == 1) {
             // a singleton's own band uses the dgemv-rounded line (guided.py:443-446, m == 1)
@@ -512,36 +514,44 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
     }
     __syncthreads();
 
-    // ---------------- strips (sg_prep_kernel of round 1)
+    // ---------------- strips.  (a) per (super-group, group) — the first member of each
+    // group within its super-group: |dist_g - dist_base| over the strip (atomic max in
+    // shared memory) and the group's view (groups shared by two super-groups get the
+    // same view twice)
+    for (int k = tid; k < nm; k += ST) {
+        const int lg = MGID(k);
+        const int ls = MSG(k);
+        if (k > 0 && MGID(k - 1) == lg && MSG(k - 1) == ls) continue;
+        const GroupRec& G = a.grp[s0 + lg];
+        const GroupRec& GB = a.grp[s0 + (sgbl[ls] & 0xffffu)];
+        const float R = (float)d + __uint_as_float(sgdevf[ls]) + 0.05f;
+        const float bf[3] = {GB.ar, GB.br, GB.cr};
+        const float gr[3] = {G.ar, G.br, G.cr};
+        const float dlt = (G.K < 0 && a.strategy != 1) ? __int_as_float(0x7f800000)
+                                                        : band_deviation_f(bf, gr, (float)W, (float)H, R);
+        atomicMax(&sgdelf[ls], __float_as_uint(dlt));
+        GView gv;
+        if (G.K < 0 && a.strategy != 1) {
+            gv.a = 0.f; gv.b = 0.f; gv.c = 1e30f; gv.reach = -1.f;
+        } else {
+            gv.a = G.ar; gv.b = G.br; gv.c = G.cr; gv.reach = (float)a.d + G.maxdev + 0.05f;
+        }
+        gv.moff = G.moff; gv.pad0 = gv.pad1 = gv.pad2 = 0;
+        const int4* w = reinterpret_cast<const int4*>(&gv);
+        __stcs(reinterpret_cast<int4*>(a.gview + s0 + lg), w[0]);
+        __stcs(reinterpret_cast<int4*>(a.gview + s0 + lg) + 1, w[1]);
+    }
+    __syncthreads();
+    // (b) per super-group: strip half-width, sure radius, bucket-row range (sg_prep_kernel
+    // of round 1)
     for (int ls = tid; ls < nsg; ls += ST) {
         SGRec o = a.sg[sgbase + ls];
         const double* bl = a.q_line + 3 * (int64_t)o.rlo;
         const double r[3] = {bl[0], bl[1], bl[2]};
         const double R = d + (double)__uint_as_float(sgdevf[ls]) + 0.05;
-        bool all_k = true;
-        double delta = 0.0;
-        const float rf[3] = {(float)r[0], (float)r[1], (float)r[2]};
-        for (int g = o.g0; g < o.g0 + o.gcnt; g++) {
-            const GroupRec& G = a.grp[g];
-            const float gr[3] = {G.ar, G.br, G.cr};
-            // |dist_g - dist_base| over the strip |dist_base| <= R inside the image
-            delta = fmax(delta, (double)band_deviation_f(rf, gr, (float)W, (float)H, (float)R));
-            all_k = all_k && G.K >= 0;
-            // the group's view for the match kernel (groups shared by two
-            // super-groups get the same values twice)
-            GView gv;
-            if (G.K < 0 && a.strategy != 1) {
-                gv.a = 0.f; gv.b = 0.f; gv.c = 1e30f; gv.reach = -1.f;
-            } else {
-                gv.a = G.ar; gv.b = G.br; gv.c = G.cr; gv.reach = (float)a.d + G.maxdev + 0.05f;
-            }
-            gv.moff = G.moff; gv.pad0 = gv.pad1 = gv.pad2 = 0;
-            {
-                const int4* w = reinterpret_cast<const int4*>(&gv);
-                __stcs(reinterpret_cast<int4*>(a.gview + g), w[0]);
-                __stcs(reinterpret_cast<int4*>(a.gview + g) + 1, w[1]);
-            }
-        }
+        const float dlt = __uint_as_float(sgdelf[ls]);
+        const bool all_k = !isinf(dlt);
+        const double delta = all_k ? (double)dlt : 0.0;
         o.ar = (float)r[0]; o.br = (float)r[1]; o.cr = (float)r[2]; o.R = (float)R;
         // sure-in-C' radius around the base line: grid, the 3x3 subcell block of the
         // nearest sample (half-size D); radial, the disk of radius r around it; both with
