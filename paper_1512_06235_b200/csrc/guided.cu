@@ -327,6 +327,7 @@ struct ChunkArgs {
     int32_t* sg_next;            // match kernel's queue head
     unsigned long long* tab_key; unsigned* tab_rep; unsigned* tab_cnt;
     int32_t* q_tab; double* q_line;
+    float4* q_lf;                // per clipped query: its line in f32 + |q|^2 bits (setup re-reads)
     int2* gtmp; float* gkey; int32_t* gpos; float4* gline; float4* gend; int2* sglist;
     int4* grec; int32_t* gfill; int32_t* members; GroupRec* grp; MemberRec* mrec; SGRec* sg;
     int32_t* mgid;               // per member position: the pair's (sorted) group index
@@ -647,6 +648,7 @@ size_t chunk_bytes(const ChunkSizes& c) {
     b += aligned_bytes<int32_t>(c.Q + c.P + 1) * 3;    // jmp_a, jmp_b, jmark (pairs past TS_SMEM)
     b += aligned_bytes<GView>(c.Q);                    // gview
     b += aligned_bytes<double>(3 * c.Q);               // q_line
+    b += aligned_bytes<float4>(c.Q);                   // q_lf
     b += aligned_bytes<int4>(c.Q);                     // grec
     b += aligned_bytes<int32_t>(c.Q) * 2;              // gfill, members
     b += aligned_bytes<GroupRec>(c.Q);                 // grp
@@ -963,6 +965,7 @@ static int guided_match_impl(const msfm_bank* bank, const msfm_grids* grids, int
     a.tab_key = ar.take<unsigned long long>(w.T);
     a.tab_rep = ar.take<unsigned>(w.T); a.tab_cnt = ar.take<unsigned>(w.T);
     a.q_tab = ar.take<int32_t>(w.Q); a.q_line = ar.take<double>(3 * w.Q);
+    a.q_lf = ar.take<float4>(w.Q);
     a.grec = ar.take<int4>(w.Q);
     a.gfill = ar.take<int32_t>(w.Q); a.members = ar.take<int32_t>(w.Q);
     a.grp = ar.take<GroupRec>(w.Q);

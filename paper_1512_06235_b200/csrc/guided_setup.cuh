@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
     float* fmx = fmn + 32;
     int* sv = reinterpret_cast<int*>(fmx + 32);             // [0] ng [1] nm [2] nsg [3] base [4] done
     const bool small = tsize <= TS_SMEM;
+    long long tmark[5] = {0, 0, 0, 0, 0};    // phase clocks (msfm_debug_counters)
     // after the compaction trep holds the group id
     unsigned long long* tkey = small ? reinterpret_cast<unsigned long long*>(su_raw) : a.tab_key + t0;
     unsigned* trep = small ? reinterpret_cast<unsigned*>(su_raw + (size_t)TS_SMEM * 8) : a.tab_rep + t0;
@@ -172,6 +173,7 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
     }
     if (isnan(a.pair_F[9 * (int64_t)pg]) || nq == 0) return;   // no groups: nothing queued
     __syncthreads();
+    if (a.dbg && tid == 0) tmark[0] = clock64();
 
     // ---------------- lines (lines_kernel of round 1; guided.py:353-373)
     const double W = a.img_wh[2 * ti], H = a.img_wh[2 * ti + 1];
@@ -205,11 +207,14 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
                 slot = (int)h;
                 double* L = a.q_line + 3 * (s0 + i);
                 L[0] = l[0]; L[1] = l[1]; L[2] = l[2];
+                a.q_lf[s0 + i] = make_float4((float)l[0], (float)l[1], (float)l[2],
+                                             __int_as_float(a.norm2[qoff + fid]));
             }
         }
         a.q_tab[s0 + i] = slot;
     }
     __syncthreads();
+    if (a.dbg && tid == 0) tmark[1] = clock64();
 
     // ---------------- groups: compaction, angle order, member ranges, endpoints
     int gcarry = 0;
@@ -287,6 +292,7 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
     for (int e = tid; e < tsize; e += ST)
         if (tkey[e] != EMPTY) trep[e] = (unsigned)a.gpos[s0 + trep[e]];
     __syncthreads();
+    if (a.dbg && tid == 0) tmark[2] = clock64();
 
     // ---------------- scatter + per-group geometry (GroupRec, endpoints)
     // member fill counters: shared memory over the dead key array (small pairs)
@@ -358,6 +364,7 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
         }
     }
     __syncthreads();
+    if (a.dbg && tid == 0) tmark[3] = clock64();
 
     // ---------------- super-groups
     // J / mark arrays: shared memory (reusing the table) for small pairs, else global
@@ -462,6 +469,7 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
         a.sg[sgbase + ls] = o;
     }
     __syncthreads();
+    if (a.dbg && tid == 0) tmark[4] = clock64();
 
     // ---------------- members: epilogue constants, band deviations
     for (int k = tid; k < nm; k += ST) {
@@ -474,23 +482,21 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
         const unsigned bl2 = sgbl[ls];
         const GroupRec& GB = a.grp[s0 + (bl2 & 0xffffu)];     // the super-group's base group
         const int g0 = (int)s0 + (int)(bl2 >> 16);
-        double m[3];
+        const float4 lf = a.q_lf[slot];       // the member's line (f32) and |q|^2
+        float mf[3] = {lf.x, lf.y, lf.z};
         if (G.cnt == 1) {
             // a singleton's own band uses the dgemv-rounded line (guided.py:443-446, m == 1)
             const float2 p2 = a.xy[qoff + fid];
-            double Fm[9];
+            double Fm[9], m[3];
 #pragma unroll
             for (int j = 0; j < 9; j++) Fm[j] = a.pair_F[9 * (int64_t)pg + j];
             epiline(Fm, (double)p2.x, (double)p2.y, true, m);
             const double nrm = fmax(np_hypot(m[0], m[1]), 1e-15);
             m[0] /= nrm; m[1] /= nrm; m[2] /= nrm;
             G.sl0 = m[0]; G.sl1 = m[1]; G.sl2 = m[2];
-        } else {
-            const double* ml = a.q_line + 3 * (int64_t)slot;
-            m[0] = ml[0]; m[1] = ml[1]; m[2] = ml[2];
+            mf[0] = (float)m[0]; mf[1] = (float)m[1]; mf[2] = (float)m[2];
         }
         // (the group's and the base's rep lines as the f32 copies of their records)
-        const float mf[3] = {(float)m[0], (float)m[1], (float)m[2]};
         const float r[3] = {G.ar, G.br, G.cr};
         const float b[3] = {GB.ar, GB.br, GB.cr};
         float rdev, sdev;
@@ -499,11 +505,13 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
         atomicMax(reinterpret_cast<unsigned*>(&G.maxdev), __float_as_uint(gdev));
         atomicMax(&sgdevf[ls], __float_as_uint(sdev));
         MemberRec mr;
-        mr.a = (float)m[0]; mr.b = (float)m[1]; mr.c = (float)m[2];
-        const float eps = (float)((fabs(m[0]) * W + fabs(m[1]) * H + fabs(m[2])) * 0x1p-20) + 1e-6f;
+        mr.a = mf[0]; mr.b = mf[1]; mr.c = mf[2];
+        // fp32 band-value error bound (from the f32 line: the bound's own
+        // relative change is ~1e-7, far inside its slack)
+        const float eps = (fabsf(mf[0]) * (float)W + fabsf(mf[1]) * (float)H + fabsf(mf[2])) * 0x1p-20f * 1.0001f + 1e-6f;
         mr.lo = (float)d - eps;
         mr.hi = (float)d + eps;
-        mr.qn9 = (unsigned)a.norm2[qoff + fid] << 9;
+        mr.qn9 = (unsigned)__float_as_int(lf.w) << 9;
         mr.fid = fid;
         mr.slotgi = (int)((unsigned)slot | ((unsigned)(s0 + lg - g0) << SLOT_BITS));
         {
@@ -589,6 +597,17 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
             const int4* w = reinterpret_cast<const int4*>(&o);
 #pragma unroll
             for (int k = 0; k < 8; k++) __stcs(dst + k, w[k]);
+        }
+    }
+    if (a.dbg) {
+        __syncthreads();
+        if (tid == 0) {
+            const long long t5 = clock64();
+            atomicAdd(&a.dbg[11], (unsigned long long)(tmark[1] - tmark[0]));   // lines
+            atomicAdd(&a.dbg[12], (unsigned long long)(tmark[2] - tmark[1]));   // groups
+            atomicAdd(&a.dbg[13], (unsigned long long)(tmark[3] - tmark[2]));   // scatter + geometry
+            atomicAdd(&a.dbg[14], (unsigned long long)(tmark[4] - tmark[3]));   // chain + shape
+            atomicAdd(&a.dbg[15], (unsigned long long)(t5 - tmark[4]));         // members + strips
         }
     }
 }

@@ -45,7 +45,8 @@ torch.cuda.synchronize()
 lib.msfm_debug_counters(1, cnt.ctypes.data)
 lib.msfm_debug_counters(0, None)
 names = ["supergroups", "members", "gathered", "passing", "sure", "unsure", "exactC'", "mtiles*ntiles", "groups", "rounds",
-         "tile elements", "near-band elems", "empty 16x8 blks", "16x8 blocks"]
+         "tile elements", "setup: lines clk", "setup: groups clk", "setup: scatter+geo clk",
+         "setup: chain+shape clk", "setup: members+strips clk"]
 P = len(ok)
 for k, nme in enumerate(names):
     print(f"  {nme:14s} {cnt[k]:>12d}  per pair {cnt[k]/P:10.1f}  per SG {cnt[k]/max(cnt[0],1):8.2f}")
