@@ -53,6 +53,8 @@ struct alignas(16) MSmem {
     unsigned short ulist[MS_CAP];  // candidates whose C' bits are still to be decided
     unsigned anyb[MS_CAP / 32];    // stats: candidate inside some member band
     uint4 bring[MS_RING][64];      // candidate descriptor rows of the next tiles (swizzled 16-B chunks)
+    unsigned long long mbest[16];  // running best (d2 << 32 | target) of the slot's first 16 members
+    unsigned msec[16];             // and second d2 (members past 16: a.mstate / a.mstate2)
     uint64_t bar_q, bar_rec[2];
 };
 
@@ -363,17 +365,19 @@ __device__ __forceinline__ void ms_block(const ChunkArgs& a, MSmem& S, const MSl
             if (k1 != KEY_NONE)
                 best = ((unsigned long long)(q2 + (unsigned)(k1 >> 8)) << 32) | (unsigned)S.cid[k1 & 255];
             if (k2 != KEY_NONE) sec = q2 + (unsigned)(k2 >> 8);
+            unsigned long long* pb = j < 16 ? &S.mbest[j] : &a.mstate[mslot];
+            unsigned* ps = j < 16 ? &S.msec[j] : &a.mstate2[mslot];
             if (!first_round) {
-                const unsigned long long ob = a.mstate[mslot];
-                const unsigned os = a.mstate2[mslot];
+                const unsigned long long ob = *pb;
+                const unsigned os = *ps;
                 const unsigned bd = (unsigned)(best >> 32), od = (unsigned)(ob >> 32);
                 const unsigned nh = max(bd, od);
                 const unsigned long long nbest = (bd < od) ? best : ob;
                 sec = min(nh, min(sec, os));
                 best = nbest;
             }
-            a.mstate[mslot] = best;
-            a.mstate2[mslot] = sec;
+            *pb = best;
+            *ps = sec;
         }
     }
 }
@@ -427,7 +431,9 @@ __device__ __forceinline__ int ms_round(const ChunkArgs& a, MSmem& S, const MSlo
                 const int k1 = gi + 1 < SG.gcnt ? max(L.gv[gi + 1].moff - SG.m0, 0) : m;
                 bool any = false;
                 for (int k = k0; k < k1 && !any; k++) any = ms_member_band(a, SG, ms_member(a, L, k), px, py);
+#ifndef MSFM_MATCH_CLOCKS
                 if (any && a.dbg) atomicAdd(&a.dbg[6], 1ull);
+#endif
                 if (any && !in_cprime(a, a.grp[SG.g0 + gi], SG, px, py, SG.toff, f)) bits &= ~(1u << gi);
             }
             S.cand[j].w = (int)bits;
@@ -503,6 +509,10 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(const 
     for (;;) {
         const int sid = sid_cur;
         if (sid >= total) break;
+#ifdef MSFM_MATCH_CLOCKS
+        const long long c0 = clock64();
+        long long c_round = 0;
+#endif
         const int nxt = cur ^ 1;
         MSlot& L = S.slot[cur];
         // the SG after next: its record goes to sgq
@@ -515,6 +525,9 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(const 
         cp_async_wait_all();
         __syncwarp();
         ms_quads(L);
+#ifdef MSFM_MATCH_CLOCKS
+        const long long c1 = clock64();
+#endif
         const SGRec& SG = L.sg;
         if (a.dbg && lane == 0) {
             atomicAdd(&a.dbg[0], 1ull);
@@ -592,7 +605,9 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(const 
                 if (lane >= o) incl += y;
             }
             tot = __shfl_sync(FULL, incl, 31);
+#ifndef MSFM_MATCH_CLOCKS
             if (a.dbg && lane == 0) atomicAdd(&a.dbg[2], (unsigned long long)tot);
+#endif
             j0 = 0;
             const int ri = rec_at(lane);
             nrec = lane < tot ? __ldg(mrec4 + ri) : make_int4(0, 0, 0, 0);
@@ -626,12 +641,14 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(const 
                     const int ri = rec_at(j + 32);
                     if (j + 32 < tot) nrec = __ldg(mrec4 + ri);
                 }
+#ifndef MSFM_MATCH_CLOCKS
                 if (a.dbg && lane == 0) {
                     atomicAdd(&a.dbg[3], (unsigned long long)cnt);
                     atomicAdd(&a.dbg[4], (unsigned long long)__popc(__ballot_sync(FULL, pass && sure)));
                 } else if (a.dbg) {
                     __ballot_sync(FULL, pass && sure);
                 }
+#endif
                 const int k = __popc(bal & ((1u << lane) - 1u));
                 const unsigned ubal = __ballot_sync(FULL, pass && !sure);
                 if (pass) {
@@ -648,7 +665,13 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(const 
             __syncwarp();
             issue_next_desc();
             if (n > 0) {
+#ifdef MSFM_MATCH_CLOCKS
+                const long long cr = clock64();
+#endif
                 cols_total += ms_round<STATS>(a, S, L, n, nu, first_round);
+#ifdef MSFM_MATCH_CLOCKS
+                c_round += clock64() - cr;
+#endif
                 first_round = false;
                 n = 0;
                 nu = 0;
@@ -656,13 +679,16 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(const 
             if (!full) break;
         }
         __syncwarp();
+#ifdef MSFM_MATCH_CLOCKS
+        const long long c2 = clock64();
+#endif
         // ---- ratio test + dedupe per member (ratio_filter / _dedupe_targets)
         if (!first_round) {
             for (int j = lane; j < SG.mcnt; j += 32) {
                 const MemberRec M = j < 16 ? L.mr[j] : a.mrec[SG.m0 + j];
                 const int slot = M.slotgi & SLOT_MASK;
-                const unsigned long long best = a.mstate[slot];
-                const unsigned sec = a.mstate2[slot];
+                const unsigned long long best = j < 16 ? S.mbest[j] : a.mstate[slot];
+                const unsigned sec = j < 16 ? S.msec[j] : a.mstate2[slot];
                 if (best == ~0ull) continue;
                 const unsigned bd2 = (unsigned)(best >> 32);
                 const int tid = (int)(best & 0xffffffffu);
@@ -704,6 +730,15 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(const 
             if (lane == 0) ms_issue_rec(a, L, &S.bar_rec[cur]);
         }
         __syncwarp();
+#ifdef MSFM_MATCH_CLOCKS
+        if (a.dbg && lane == 0) {
+            const long long c3 = clock64();
+            atomicAdd(&a.dbg[5], (unsigned long long)(c1 - c0));                // SG setup
+            atomicAdd(&a.dbg[7], (unsigned long long)(c2 - c1 - c_round));      // gather
+            atomicAdd(&a.dbg[9], (unsigned long long)c_round);                  // rounds
+            atomicAdd(&a.dbg[10], (unsigned long long)(c3 - c2));               // ratio + rotation
+        }
+#endif
         cur = nxt;
     }
 }
