@@ -413,6 +413,9 @@ __device__ __forceinline__ int ms_round(const ChunkArgs& a, MSmem& S, const MSlo
     // ---- C' bits: "0" only where some member band of the group holds the candidate
     // and C'(group) does not; everywhere else the bit is never consulted (don't care)
     bool partial = false;
+#ifdef MSFM_MATCH_CLOCKS
+    const long long c_cb0 = clock64();
+#endif
     for (int u0 = 0; u0 < nu; u0 += 32) {
         const int uj = u0 + lane;
         if (uj < nu) {
@@ -440,6 +443,10 @@ __device__ __forceinline__ int ms_round(const ChunkArgs& a, MSmem& S, const MSlo
             partial |= bits != all_groups;
         }
     }
+#ifdef MSFM_MATCH_CLOCKS
+    if (a.dbg && lane == 0) atomicAdd(&a.dbg[9], (unsigned long long)(clock64() - c_cb0));
+    const long long c_t0 = clock64();
+#endif
     // ---- pad the last n8 tile with candidates no member accepts (NaN position: never
     // inside a band, never near its edge)
     const int ntile = (n + 7) >> 3;
@@ -455,6 +462,9 @@ __device__ __forceinline__ int ms_round(const ChunkArgs& a, MSmem& S, const MSlo
     else         ms_block<false, STATS, true>(a, S, L, 0, m, ntile, first_round);
     // member blocks past the slot (one group of > 16 members, stats mode only)
     for (int mb0 = 16; mb0 < m; mb0 += 16) ms_block<true, STATS, false>(a, S, L, mb0, m, ntile, first_round);
+#ifdef MSFM_MATCH_CLOCKS
+    if (a.dbg && lane == 0) atomicAdd(&a.dbg[6], (unsigned long long)(clock64() - c_t0));
+#endif
     if (STATS) {
         __syncwarp();
         int cnt = lane < MS_CAP / 32 ? __popc(S.anyb[lane]) : 0;
@@ -735,7 +745,6 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(const 
             const long long c3 = clock64();
             atomicAdd(&a.dbg[5], (unsigned long long)(c1 - c0));                // SG setup
             atomicAdd(&a.dbg[7], (unsigned long long)(c2 - c1 - c_round));      // gather
-            atomicAdd(&a.dbg[9], (unsigned long long)c_round);                  // rounds
             atomicAdd(&a.dbg[10], (unsigned long long)(c3 - c2));               // ratio + rotation
         }
 #endif
