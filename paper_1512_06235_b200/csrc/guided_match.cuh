@@ -543,6 +543,9 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(const 
             atomicAdd(&a.dbg[0], 1ull);
             atomicAdd(&a.dbg[1], (unsigned long long)SG.mcnt);
             atomicAdd(&a.dbg[8], (unsigned long long)SG.gcnt);
+#ifndef MSFM_MATCH_CLOCKS
+            atomicAdd(&a.dbg[5], (unsigned long long)(SG.rhi - SG.rlo + 1));   // strip rows
+#endif
         }
         const unsigned all_groups = (1u << SG.gcnt) - 1u;
         const int nalong = SG.nalong;

@@ -44,7 +44,7 @@ res = match_pairs(bank, wl.q_img[ok], wl.t_img[ok], wl.F[ok], ql, device_inputs=
 torch.cuda.synchronize()
 lib.msfm_debug_counters(1, cnt.ctypes.data)
 lib.msfm_debug_counters(0, None)
-names = ["supergroups", "members", "gathered", "passing", "sure", "match: SG setup clk", "match: tiles clk",
+names = ["supergroups", "members", "gathered", "passing", "sure", "strip rows (clk: SG setup)", "match: tiles clk",
          "match: gather clk", "groups", "match: C' bits clk", "match: ratio clk", "setup: lines clk", "setup: groups clk", "setup: scatter+geo clk",
          "setup: chain+shape clk", "setup: members+strips clk"]
 P = len(ok)
