@@ -828,9 +828,21 @@ static void plan_chunks(int32_t n_pairs, const int64_t* h_qlist_off, const msfm_
     const int cp = prm->chunk_pairs > 0 ? prm->chunk_pairs : 8192;
     int64_t budget = prm->max_workspace_bytes;
     if (budget <= 0) {
-        size_t fr = 0, tot = 0;
-        budget = (cudaMemGetInfo(&fr, &tot) == cudaSuccess && fr > 0) ? (int64_t)(fr / 4)
-                                                                       : (int64_t)16 << 30;
+        // a quarter of the device memory free at the first planning on this device:
+        // cudaMemGetInfo itself can stall a step for tens of ms (measured 2-74 ms in
+        // the staged e2e loop), so it is asked once per device and process
+        static int64_t cached[64];
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= 64 || cached[dev] <= 0) {
+            size_t fr = 0, tot = 0;
+            const int64_t b = (cudaMemGetInfo(&fr, &tot) == cudaSuccess && fr > 0) ? (int64_t)(fr / 4)
+                                                                                 : (int64_t)16 << 30;
+            if (dev >= 0 && dev < 64) cached[dev] = b;
+            budget = b;
+        } else {
+            budget = cached[dev];
+        }
     }
     const int64_t qmax = std::min<int64_t>((int64_t)1 << SLOT_BITS, AUTO_CHUNK_SLOTS);
     auto bytes_of = [&](int64_t P, int64_t Q) {
