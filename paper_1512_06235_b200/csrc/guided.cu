@@ -311,6 +311,7 @@ struct ChunkArgs {
     const int4* rrec; const int4* crec;   // bucket-ordered (x, y, |desc|^2, id)
     double D, d;
     float ratio, single_cap;
+    int tie_fid;                 // ratio > 1: ties at the minimum resolve to the lowest target id
     int stats_mode;              // 1: one super-group per group (exact SearchStats)
     int strategy;                // 0 grid, 1 linear, 2 radial (msfm_match_params)
     double r2;                   // radial: (d * sqrt(2))^2 as the reference rounds it
@@ -924,8 +925,8 @@ static int guided_match_impl(const msfm_bank* bank, const msfm_grids* grids, int
         set_error("msfm_guided_match: images with more than 65536 features are not supported");
         return MSFM_EINVAL;
     }
-    if (!(prm->ratio <= 1.0f)) {
-        set_error("msfm_guided_match: ratio > 1 is not supported (got %g)", (double)prm->ratio);
+    if (prm->ratio != prm->ratio) {
+        set_error("msfm_guided_match: ratio is NaN");
         return MSFM_EINVAL;
     }
     if (n_pairs == 0) return MSFM_OK;
@@ -948,6 +949,7 @@ static int guided_match_impl(const msfm_bank* bank, const msfm_grids* grids, int
     a.rrec = reinterpret_cast<const int4*>(grids->d_rrec);
     a.crec = reinterpret_cast<const int4*>(grids->d_crec);
     a.D = grids->D; a.d = prm->d; a.ratio = prm->ratio; a.single_cap = prm->single_cap;
+    a.tie_fid = prm->ratio > 1.0f ? 1 : 0;
     if (prm->strategy < 0 || prm->strategy > 2) {
         set_error("msfm_guided_match: unknown strategy %d", prm->strategy);
         return MSFM_EINVAL;
@@ -1000,13 +1002,17 @@ static int guided_match_impl(const msfm_bank* bank, const msfm_grids* grids, int
         int nb = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, setup_kernel, ST, SETUP_SMEM);
         fprintf(stderr, "setup_kernel: %d CTAs/SM (%zu B smem)\n", nb, (size_t)SETUP_SMEM);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, match_ms_kernel<false>, MS_WARPS * 32, sizeof(MSmem) * MS_WARPS);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, match_ms_kernel<false, false>, MS_WARPS * 32, sizeof(MSmem) * MS_WARPS);
         fprintf(stderr, "match_ms_kernel: %d CTAs/SM\n", nb);
     }
     const size_t ms_smem = sizeof(MSmem) * MS_WARPS;
-    MSFM_CUDA_TRY(cudaFuncSetAttribute(match_ms_kernel<true>,
+    MSFM_CUDA_TRY(cudaFuncSetAttribute(match_ms_kernel<true, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ms_smem));
-    MSFM_CUDA_TRY(cudaFuncSetAttribute(match_ms_kernel<false>,
+    MSFM_CUDA_TRY(cudaFuncSetAttribute(match_ms_kernel<false, false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ms_smem));
+    MSFM_CUDA_TRY(cudaFuncSetAttribute(match_ms_kernel<true, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ms_smem));
+    MSFM_CUDA_TRY(cudaFuncSetAttribute(match_ms_kernel<false, true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ms_smem));
     const bool sync_dbg = getenv("MSFM_SYNC_CHECK") && atoi(getenv("MSFM_SYNC_CHECK")) != 0;
     int next_range = 0;
@@ -1058,8 +1064,14 @@ static int guided_match_impl(const msfm_bank* bank, const msfm_grids* grids, int
         if (int rc = sync_check("setup_kernel")) return rc;
         {
             ProfScope ps("match_kernel", st);
-            if (d_stats) match_ms_kernel<true><<<nsm * MS_MINB, MS_WARPS * 32, ms_smem, st>>>(a);
-            else         match_ms_kernel<false><<<nsm * MS_MINB, MS_WARPS * 32, ms_smem, st>>>(a);
+            const dim3 grid(nsm * MS_MINB), block(MS_WARPS * 32);
+            if (a.tie_fid) {
+                if (d_stats) match_ms_kernel<true, true><<<grid, block, ms_smem, st>>>(a);
+                else         match_ms_kernel<false, true><<<grid, block, ms_smem, st>>>(a);
+            } else {
+                if (d_stats) match_ms_kernel<true, false><<<grid, block, ms_smem, st>>>(a);
+                else         match_ms_kernel<false, false><<<grid, block, ms_smem, st>>>(a);
+            }
         }
         if (int rc = sync_check("match_kernel")) return rc;
         { ProfScope ps("compact_kernel", st); compact_kernel<<<a.npairs, 256, 0, st>>>(a); }

@@ -372,7 +372,8 @@ __device__ __forceinline__ void ms_block(const ChunkArgs& a, MSmem& S, const MSl
                 const unsigned os = *ps;
                 const unsigned bd = (unsigned)(best >> 32), od = (unsigned)(ob >> 32);
                 const unsigned nh = max(bd, od);
-                const unsigned long long nbest = (bd < od) ? best : ob;
+                // (d2, target) order: a tie across rounds keeps the lower target id
+                const unsigned long long nbest = best < ob ? best : ob;
                 sec = min(nh, min(sec, os));
                 best = nbest;
             }
@@ -399,10 +400,43 @@ __device__ __forceinline__ void ms_quads(MSlot& L) {
     __syncwarp();
 }
 
+// ratio > 1 only: the round's candidates reordered by target id (their rank among the
+// round's unique ids), the key's local index rewritten to the new position
+__device__ __forceinline__ void ms_order_by_target(MSmem& S, int n) {
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+    int4 rc[MS_CAP / 32];
+    unsigned short rid[MS_CAP / 32];
+    int rank[MS_CAP / 32];
+#pragma unroll
+    for (int q = 0; q < MS_CAP / 32; q++) {
+        const int j = lane + 32 * q;
+        rank[q] = -1;
+        if (j < n) {
+            rc[q] = S.cand[j];
+            rid[q] = S.cid[j];
+            int r = 0;
+            for (int i = 0; i < n; i++) r += S.cid[i] < rid[q];
+            rank[q] = r;
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < MS_CAP / 32; q++) {
+        if (rank[q] >= 0) {
+            int4 c = rc[q];
+            c.z = (c.z & ~0xff) | rank[q];
+            S.cand[rank[q]] = c;
+            S.cid[rank[q]] = rid[q];
+        }
+    }
+    __syncwarp();
+}
+
 // One round: C' bits of the unsure candidates, then the distance tiles of every
 // member block against the round's n candidates; per-member top-2 merged into
 // mstate / mstate2 (first_round: written).
-template <bool STATS>
+template <bool STATS, bool TIE>
 __device__ __forceinline__ int ms_round(const ChunkArgs& a, MSmem& S, const MSlot& L, int n, int nu,
                                      bool first_round) {
     int cols_total = 0;
@@ -447,6 +481,11 @@ __device__ __forceinline__ int ms_round(const ChunkArgs& a, MSmem& S, const MSlo
     if (a.dbg && lane == 0) atomicAdd(&a.dbg[9], (unsigned long long)(clock64() - c_cb0));
     const long long c_t0 = clock64();
 #endif
+    // ---- ratio > 1 accepts a tie at the minimum (ratio 1), and the reference's argmin
+    // then names the lowest target id among the tied candidates: order the round's
+    // candidates by target id so the key's local index (the tie-break) follows it
+    // (target ids are unique within a super-group's strip)
+    if (TIE) ms_order_by_target(S, n);
     // ---- pad the last n8 tile with candidates no member accepts (NaN position: never
     // inside a band, never near its edge)
     const int ntile = (n + 7) >> 3;
@@ -476,7 +515,8 @@ __device__ __forceinline__ int ms_round(const ChunkArgs& a, MSmem& S, const MSlo
     return cols_total;
 }
 
-template <bool STATS>
+// TIE (ratio > 1): candidates of a round ordered by target id before the tiles
+template <bool STATS, bool TIE>
 __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(const __grid_constant__ ChunkArgs a) {
     extern __shared__ __align__(128) unsigned char ms_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -681,7 +721,7 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(const 
 #ifdef MSFM_MATCH_CLOCKS
                 const long long cr = clock64();
 #endif
-                cols_total += ms_round<STATS>(a, S, L, n, nu, first_round);
+                cols_total += ms_round<STATS, TIE>(a, S, L, n, nu, first_round);
 #ifdef MSFM_MATCH_CLOCKS
                 c_round += clock64() - cr;
 #endif

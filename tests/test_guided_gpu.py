@@ -378,3 +378,50 @@ def test_staged_rows_with_empty_lists_and_images():
                                      segment_images=2, first_chunk_pairs=3)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(got.view(np.int32), want.view(np.int32))
+
+
+@pytest.mark.parametrize("ratio", [1.5, 4.0])
+def test_ratio_above_one_ties_resolve_to_lowest_target(ratio):
+    """ratio > 1 (the reference accepts any ratio, matching.py:82-103): a tie at the
+    minimum distance is then accepted with ratio 1 and names the lowest target id
+    among the tied candidates (np.argmin over the sorted candidate list,
+    guided.py:460).  Ties are forced by copying each target feature's descriptor onto
+    its nearest neighbour in the image; every pair of a small C3 scene against the C
+    oracle, bit-exact."""
+    import dataclasses
+
+    from oracle import guided as og
+    from paper_1512_06235_b200 import scenes
+    from paper_1512_06235_b200.guided import match_pairs
+
+    scene, snap = scenes.build("C3", n_cameras=6)
+    rng = np.random.default_rng(7)
+    sets = {}
+    for i, fs in scene.feature_sets.items():
+        desc = np.array(fs.descriptors, copy=True)
+        xy = np.asarray(fs.xy, np.float64)
+        pick = rng.choice(len(desc), size=len(desc) // 3, replace=False)
+        for j in pick:       # nearest other feature takes j's descriptor
+            d2 = ((xy - xy[j]) ** 2).sum(axis=1)
+            d2[j] = np.inf
+            desc[int(np.argmin(d2))] = desc[j]
+        sets[i] = dataclasses.replace(fs, descriptors=desc)
+    wl = scenes.pair_workload(scene, snap)
+    ok = np.flatnonzero(wl.valid)
+    bank = _bank(sets)
+    ql = [wl.untracked[int(wl.q_img[k])] for k in ok]
+    pk, q, t, d, r = match_pairs(bank, wl.q_img[ok], wl.t_img[ok], wl.F[ok], ql,
+                                 ratio=ratio).to_host()
+    ties = total = 0
+    for j, k in enumerate(ok):
+        fq, ft = sets[int(wl.q_img[k])], sets[int(wl.t_img[k])]
+        oq, ot, od, orr, _ = og.guided_match(fq.xy, fq.descriptors, ft.xy, ft.descriptors,
+                                             ft.width, ft.height, wl.F[k], ql[j], ratio=ratio)
+        sel = pk == j
+        np.testing.assert_array_equal(q[sel], oq)
+        np.testing.assert_array_equal(t[sel], ot)
+        np.testing.assert_array_equal(d[sel], od)
+        np.testing.assert_array_equal(r[sel], orr)
+        ties += int((orr == 1.0).sum())
+        total += len(oq)
+    assert total > 1000 and ties > 50, (total, ties)
