@@ -183,10 +183,25 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
     double F[9];
 #pragma unroll
     for (int j = 0; j < 9; j++) F[j] = a.pair_F[9 * (int64_t)pg + j];
+    // the next query's id, position and |q|^2 are loaded while this one's fp64
+    // geometry runs (the loads are a two-deep dependent chain through qlist)
+    int fid_n = 0, n2_n = 0;
+    float2 p2_n = make_float2(0.f, 0.f);
+    if (tid < nq) {
+        fid_n = __ldg(a.qlist + qs + tid);
+        p2_n = __ldg(a.xy + qoff + fid_n);
+        n2_n = __ldg(a.norm2 + qoff + fid_n);
+    }
     for (int i = tid; i < nq; i += ST) {
-        const int fid = a.qlist[qs + i];
+        const int fid = fid_n;
+        const float2 p2 = p2_n;
+        const int qn2 = n2_n;
+        if (i + ST < nq) {
+            fid_n = __ldg(a.qlist + qs + i + ST);
+            p2_n = __ldg(a.xy + qoff + fid_n);
+            n2_n = __ldg(a.norm2 + qoff + fid_n);
+        }
         a.q_fid[s0 + i] = fid;
-        const float2 p2 = a.xy[qoff + fid];
         double l[3];
         epiline(F, (double)p2.x, (double)p2.y, nq == 1, l);
         const double nrm = np_hypot(l[0], l[1]);
@@ -207,8 +222,7 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
                 slot = (int)h;
                 double* L = a.q_line + 3 * (s0 + i);
                 L[0] = l[0]; L[1] = l[1]; L[2] = l[2];
-                a.q_lf[s0 + i] = make_float4((float)l[0], (float)l[1], (float)l[2],
-                                             __int_as_float(a.norm2[qoff + fid]));
+                a.q_lf[s0 + i] = make_float4((float)l[0], (float)l[1], (float)l[2], __int_as_float(qn2));
             }
         }
         a.q_tab[s0 + i] = slot;
@@ -217,20 +231,18 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
     if (a.dbg && tid == 0) tmark[1] = clock64();
 
     // ---------------- groups: compaction, angle order, member ranges, endpoints
-    int gcarry = 0;
+    // one block scan: thread tid owns slots tid, tid + ST, ...; group ids are handed
+    // out thread-major (any order: groups are re-ordered by angle below)
     float lo = 1e30f, hi = -1e30f;
-    for (int e0 = 0; e0 < tsize; e0 += ST) {
-        const int e = e0 + tid;
-        bool occ = false;
-        unsigned cnt = 0, rep = 0;
-        if (e < tsize) {
-            occ = tkey[e] != EMPTY;
-            if (occ) { cnt = tcnt[e]; rep = trep[e]; }
-        }
-        int gtot;
-        const int lg = block_exclusive_scan<ST>(occ ? 1 : 0, &gtot, ssm);
-        if (occ) {
-            const int g = gcarry + lg;
+    int gcarry;
+    {
+        int mine = 0;
+        for (int e = tid; e < tsize; e += ST) mine += tkey[e] != EMPTY;
+        const int gbase = block_exclusive_scan<ST>(mine, &gcarry, ssm);
+        int g = gbase;
+        for (int e = tid; e < tsize; e += ST) {
+            if (tkey[e] == EMPTY) continue;
+            const unsigned cnt = tcnt[e], rep = trep[e];
             a.gtmp[s0 + g] = make_int2((int)rep, (int)cnt);
             const double* L = a.q_line + 3 * (s0 + rep);
             float la = (float)L[0], lb = (float)L[1];
@@ -240,8 +252,8 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
             lo = fminf(lo, ang);
             hi = fmaxf(hi, ang);
             trep[e] = (unsigned)g;
+            g++;
         }
-        gcarry += gtot;
     }
     const int ng = gcarry;
 #pragma unroll
@@ -424,17 +436,19 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
         }
         // the marks are the walk's starts; compact them in order (e from the q + 16 /
         // B rule again, since the J arrays were overwritten)
-        int carry = 0;
-        for (int q0b = 0; q0b < nm; q0b += ST) {
-            const int q = q0b + tid;
-            const bool st = q < nm && mk[q];
-            int tot;
-            const int ex = block_exclusive_scan<ST>(st ? 1 : 0, &tot, ssm);
-            if (st) {
+        // (one block scan: thread tid owns positions tid, tid + ST, ...; super-group
+        // ids thread-major — their order only schedules work)
+        int carry;
+        {
+            int mine = 0;
+            for (int q = tid; q < nm; q += ST) mine += mk[q] != 0;
+            int k = block_exclusive_scan<ST>(mine, &carry, ssm);
+            for (int q = tid; q < nm; q += ST) {
+                if (!mk[q]) continue;
                 const int e = min(q + SG_MEMBERS, GFIT(MGID(q)));
-                a.sglist[s0 + carry + ex] = make_int2((int)s0 + q, e - q);
+                a.sglist[s0 + k] = make_int2((int)s0 + q, e - q);
+                k++;
             }
-            carry += tot;
         }
         nsg = carry;
     }
