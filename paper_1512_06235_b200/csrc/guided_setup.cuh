@@ -343,6 +343,18 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
         GroupRec o;
         o.p = p; o.rep = (int)(s0 + g.x); o.cnt = g.y; o.moff = g.z;
         o.sl0 = r[0]; o.sl1 = r[1]; o.sl2 = r[2]; o.spare = 0.0;
+        if (g.y == 1) {
+            // a singleton's own band uses the dgemv-rounded line (guided.py:443-446,
+            // m == 1): computed here, once per group, for the exact fallbacks
+            const int fid = a.q_fid[s0 + g.x];
+            const float2 p2 = a.xy[qoff + fid];
+            double Fm[9], m[3];
+#pragma unroll
+            for (int j = 0; j < 9; j++) Fm[j] = a.pair_F[9 * (int64_t)pg + j];
+            epiline(Fm, (double)p2.x, (double)p2.y, true, m);
+            const double nrm = fmax(np_hypot(m[0], m[1]), 1e-15);
+            o.sl0 = m[0] / nrm; o.sl1 = m[1] / nrm; o.sl2 = m[2] / nrm;
+        }
         o.pad1 = o.pad2 = o.pad3 = 0;
         double pa[2] = {0, 0}, pb[2] = {0, 0}, len = 0.0;
         o.K = -1;
@@ -497,19 +509,10 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
         const GroupRec& GB = a.grp[s0 + (bl2 & 0xffffu)];     // the super-group's base group
         const int g0 = (int)s0 + (int)(bl2 >> 16);
         const float4 lf = a.q_lf[slot];       // the member's line (f32) and |q|^2
-        float mf[3] = {lf.x, lf.y, lf.z};
-        if (G.cnt == 1) {
-            // a singleton's own band uses the dgemv-rounded line (guided.py:443-446, m == 1)
-            const float2 p2 = a.xy[qoff + fid];
-            double Fm[9], m[3];
-#pragma unroll
-            for (int j = 0; j < 9; j++) Fm[j] = a.pair_F[9 * (int64_t)pg + j];
-            epiline(Fm, (double)p2.x, (double)p2.y, true, m);
-            const double nrm = fmax(np_hypot(m[0], m[1]), 1e-15);
-            m[0] /= nrm; m[1] /= nrm; m[2] /= nrm;
-            G.sl0 = m[0]; G.sl1 = m[1]; G.sl2 = m[2];
-            mf[0] = (float)m[0]; mf[1] = (float)m[1]; mf[2] = (float)m[2];
-        }
+        // the member's line in f32 (a singleton's dgemv-rounded line differs from it by
+        // an ulp of the f64 value, far inside the fp32 band's error bound eps; the
+        // exact fallbacks read the dgemv line from the group record)
+        const float mf[3] = {lf.x, lf.y, lf.z};
         // (the group's and the base's rep lines as the f32 copies of their records)
         const float r[3] = {G.ar, G.br, G.cr};
         const float b[3] = {GB.ar, GB.br, GB.cr};
