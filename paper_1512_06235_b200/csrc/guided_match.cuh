@@ -109,7 +109,14 @@ __device__ __forceinline__ void ms_issue_rec(const ChunkArgs& a, MSlot& L, uint6
     const int nm = min(SG.mcnt, 16), ng = SG.gcnt;
     ms_expect(bar, (uint32_t)(nm * sizeof(MemberRec) + ng * sizeof(GView)));
     if (nm) ms_bulk_ef(L.mr, a.mrec + SG.m0, nm * sizeof(MemberRec), bar);
-    if (ng) ms_bulk_ef(L.gv, a.gview + SG.g0, ng * sizeof(GView), bar);
+    if (ng) {
+        ms_bulk_ef(L.gv, a.gview + SG.g0, ng * sizeof(GView), bar);
+        // the groups' full records (exact C' samples, singleton lines) into L2: the rare
+        // exact paths then wait on an L2 hit instead of DRAM
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.grp + SG.g0),
+                     "r"((uint32_t)(ng * sizeof(GroupRec)))
+                     : "memory");
+    }
 }
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {

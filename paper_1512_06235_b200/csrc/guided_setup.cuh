@@ -411,12 +411,15 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
             const float4 ln = a.gline[s0 + g];
             unsigned bits = 0;
             const int lim = min(SG_MEMBERS, ng - 1 - g);
-            for (int i = 0; i < lim; i++) {
-                const float4 en = a.gend[s0 + g + 1 + i];
-                const float d1 = fabsf(fmaf(ln.x, en.x, fmaf(ln.y, en.y, ln.z)));
-                const float d2 = fabsf(fmaf(ln.x, en.z, fmaf(ln.y, en.w, ln.z)));
-                if (fmaxf(d1, d2) <= a.sg_tau) bits |= 1u << i;
-                else break;
+            // all the following groups' endpoints in flight at once (no early exit)
+#pragma unroll
+            for (int i = 0; i < SG_MEMBERS; i++) {
+                if (i < lim) {
+                    const float4 en = a.gend[s0 + g + 1 + i];
+                    const float d1 = fabsf(fmaf(ln.x, en.x, fmaf(ln.y, en.y, ln.z)));
+                    const float d2 = fabsf(fmaf(ln.x, en.z, fmaf(ln.y, en.w, ln.z)));
+                    if (fmaxf(d1, d2) <= a.sg_tau) bits |= 1u << i;
+                }
             }
             const int j = g + 1 + __ffs(~bits) - 1;
             const int bnd = j < ng ? (int)(a.grec[s0 + j].z - s0) : nm;

@@ -45,7 +45,7 @@ torch.cuda.synchronize()
 lib.msfm_debug_counters(1, cnt.ctypes.data)
 lib.msfm_debug_counters(0, None)
 names = ["supergroups", "members", "gathered", "passing", "sure", "strip rows (clk: SG setup)", "match: tiles clk",
-         "match: gather clk", "groups", "match: C' bits clk", "match: ratio clk", "setup: lines clk", "setup: groups clk", "setup: scatter+geo clk",
+         "(cbstats) annulus member loops | gather clk", "groups", "(cbstats) C' band-edge exact | C' clk", "(cbstats) (cand, group) tests | ratio clk", "setup: lines clk", "setup: groups clk", "setup: scatter+geo clk",
          "setup: chain+shape clk", "setup: members+strips clk"]
 P = len(ok)
 for k, nme in enumerate(names):
