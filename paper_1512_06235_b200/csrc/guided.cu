@@ -171,6 +171,8 @@ __global__ void norms_kernel(const uint8_t* __restrict__ desc, int64_t n, int32_
 }
 
 // ------------------------------------------------------------------ grid build
+constexpr int GRID_SPLIT = 8;   // CTAs per image in the grid build
+
 struct GridBuildArgs {
     const float2* xy; const int64_t* img_off; const int32_t* img_n; const int32_t* img_wh;
     const int32_t* dims; const int64_t* roff; const int64_t* coff;
@@ -187,11 +189,13 @@ __device__ __forceinline__ int bucket_of(float v, double D, int nb) {
 }
 
 __global__ void grid_count_kernel(GridBuildArgs a) {
-    const int img = a.img0 + blockIdx.x;
+    // GRID_SPLIT CTAs per image (a range of 8 images would otherwise run on 8 SMs)
+    const int img = a.img0 + blockIdx.x / GRID_SPLIT;
+    const int part = blockIdx.x % GRID_SPLIT;
     const int64_t off = a.img_off[img];
     const int n = a.img_n[img];
     const int nbx = a.dims[2 * img], nby = a.dims[2 * img + 1];
-    for (int f = threadIdx.x; f < n; f += blockDim.x) {
+    for (int f = part * blockDim.x + threadIdx.x; f < n; f += GRID_SPLIT * blockDim.x) {
         if (a.norm_out) {
             const uint4* row = reinterpret_cast<const uint4*>(a.desc + (off + f) * 128);
             unsigned s = 0;
@@ -214,11 +218,13 @@ __global__ void grid_count_kernel(GridBuildArgs a) {
 }
 
 __global__ void grid_scatter_kernel(GridBuildArgs a) {
-    const int img = a.img0 + blockIdx.x;
+    // GRID_SPLIT CTAs per image (a range of 8 images would otherwise run on 8 SMs)
+    const int img = a.img0 + blockIdx.x / GRID_SPLIT;
+    const int part = blockIdx.x % GRID_SPLIT;
     const int64_t off = a.img_off[img];
     const int n = a.img_n[img];
     const int nbx = a.dims[2 * img], nby = a.dims[2 * img + 1];
-    for (int f = threadIdx.x; f < n; f += blockDim.x) {
+    for (int f = part * blockDim.x + threadIdx.x; f < n; f += GRID_SPLIT * blockDim.x) {
         float2 p = a.xy[off + f];
         int bx = bucket_of(p.x, a.D, nbx), by = bucket_of(p.y, a.D, nby);
         int r = atomicAdd(&a.rcur[a.roff[img] + (int64_t)by * nbx + bx], 1);
@@ -770,7 +776,7 @@ static int grid_build_range_impl(const msfm_bank* bank, const int32_t* d_dims,
                     d_rmem, d_cmem, reinterpret_cast<int4*>(d_rrec),
                     reinterpret_cast<int4*>(d_crec), bank->d_norm2, D, img0, bank->d_desc, norm_out};
     if (img1 > img0) {
-        grid_count_kernel<<<img1 - img0, 256, 0, st>>>(a);
+        grid_count_kernel<<<(img1 - img0) * GRID_SPLIT, 256, 0, st>>>(a);
         MSFM_LAUNCH_CHECK();
         count_launches(1);
     }
@@ -783,7 +789,7 @@ static int grid_build_range_impl(const msfm_bank* bank, const int32_t* d_dims,
     int rc = exclusive_scan2(sc, st);
     if (rc) return rc;
     if (img1 > img0) {
-        grid_scatter_kernel<<<img1 - img0, 256, 0, st>>>(a);
+        grid_scatter_kernel<<<(img1 - img0) * GRID_SPLIT, 256, 0, st>>>(a);
         MSFM_LAUNCH_CHECK();
         count_launches(1);
     }
