@@ -168,7 +168,9 @@ typedef struct {
                           * (|rep line| <= d, guided.py:190-194), 2 radial (disks of
                           * radius d*sqrt(2) around the samples, guided.py:273-285) */
     int32_t first_chunk_pairs; /* pairs of the first chunk when > 0 (a short first
-                          * chunk starts matching sooner on a staged bank)       */
+                          * chunk starts matching sooner on a staged bank); the
+                          * last chunk is then cut to 2x as many pairs too (its
+                          * readback is the one no later chunk hides)            */
     int64_t max_workspace_bytes; /* chunks are cut so one chunk's workspace stays
                           * within this many bytes; 0 = a quarter of the device's
                           * free memory at planning time (at most 48M query slots,

@@ -878,6 +878,13 @@ static void plan_chunks(int32_t n_pairs, const int64_t* h_qlist_off, const msfm_
         bounds.push_back(e);
         p = e;
     }
+    // pipelined (first_chunk_pairs > 0): a short last chunk too, so the readback that
+    // no later chunk hides is small (a split chunk only shrinks: the worst sizes hold)
+    const int tail = 2 * prm->first_chunk_pairs;
+    if (prm->first_chunk_pairs > 0 && bounds.size() >= 2) {
+        const int b0 = bounds[bounds.size() - 2], b1 = bounds.back();
+        if (b1 - b0 > 2 * tail) bounds.insert(bounds.end() - 1, b1 - tail);
+    }
 }
 
 extern "C" int32_t msfm_guided_chunk_bounds(int32_t n_pairs, const int64_t* h_qlist_off,
