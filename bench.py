@@ -321,7 +321,8 @@ def run_b200(args, rank, world):
 
     from paper_1512_06235_b200.dist import ChunkGather, chunk_bounds
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", 0 if os.environ.get("MSFM_BENCH_BACKEND") == "gloo"
+                       else int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
     scene, wl, ok, snap = build_workload(args.cameras, with_snapshot=True)
     mine = ok[rank::world]                     # round-robin over pair order (weak scaling)
@@ -824,7 +825,7 @@ def relaunch(args):
     if args.impl == "b200":
         import torch
         have = torch.cuda.device_count()
-        if have < args.gpus:
+        if have < args.gpus and os.environ.get("MSFM_BENCH_BACKEND") != "gloo":
             print(json.dumps({"error": f"--gpus {args.gpus} but only {have} CUDA device(s) visible"}),
                   flush=True)
             return 2
@@ -846,6 +847,9 @@ def main():
     if world > 1:
         import torch.distributed as dist
         backend = "nccl" if args.impl == "b200" else "gloo"
+        # rehearsal of the N-rank code path on one GPU (NCCL refuses two ranks on
+        # one device): every rank on cuda:0, host collectives over gloo
+        backend = os.environ.get("MSFM_BENCH_BACKEND", backend)
         dist.init_process_group(backend=backend)
     try:
         if args.impl == "reference":
