@@ -1028,20 +1028,37 @@ static int guided_match_impl(const msfm_bank* bank, const msfm_grids* grids, int
     MSFM_CUDA_TRY(cudaFuncSetAttribute(match_ms_kernel<false, true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ms_smem));
     const bool sync_dbg = getenv("MSFM_SYNC_CHECK") && atoi(getenv("MSFM_SYNC_CHECK")) != 0;
-    int next_range = 0;
-    for (size_t c = 0; c + 1 < bounds.size(); c++) {
-        const int p0 = bounds[c], p1 = bounds[c + 1];
-        a.p0 = p0;
-        a.npairs = p1 - p0;
-        a.qbase = h_qlist_off[p0];
-        // bank ranges first read by this chunk: wait for their rows, then index them
-        for (; plan && next_range < plan->n_ranges && plan->chunk[next_range] <= (int32_t)c;
-             next_range++) {
-            const int r = next_range;
+    // Staged plans: every range is indexed on a high-priority side stream as soon as
+    // its rows land, so range r + 1's grid build runs beside chunk c's kernels (in the
+    // tail of its persistent match kernel) instead of between chunks on `st`; chunk c
+    // waits only for the builds of the ranges it reads.  Ranges write disjoint bucket
+    // and |desc|^2 rows, and the builds share the plan's workspace in stream order.
+    std::vector<cudaEvent_t> built;
+    struct EvGuard {
+        std::vector<cudaEvent_t>& v;
+        ~EvGuard() { for (cudaEvent_t e : v) cudaEventDestroy(e); }
+    } ev_guard{built};
+    if (plan && plan->n_ranges > 0) {
+        static cudaStream_t side[64];
+        if (dev < 0 || dev >= 64) {
+            set_error("msfm_guided_match_rows: device index %d out of range", dev);
+            return MSFM_EINVAL;
+        }
+        if (!side[dev]) {
+            int lo = 0, hi = 0;
+            MSFM_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            MSFM_CUDA_TRY(cudaStreamCreateWithPriority(&side[dev], cudaStreamNonBlocking, hi));
+        }
+        cudaStream_t ix = side[dev];
+        cudaEvent_t e0;
+        MSFM_CUDA_TRY(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+        built.push_back(e0);
+        MSFM_CUDA_TRY(cudaEventRecord(e0, st));        // everything `st` did before
+        MSFM_CUDA_TRY(cudaStreamWaitEvent(ix, e0, 0));
+        for (int r = 0; r < plan->n_ranges; r++) {
             if (plan->landed && plan->landed[r])
-                MSFM_CUDA_TRY(cudaStreamWaitEvent(st, (cudaEvent_t)plan->landed[r], 0));
+                MSFM_CUDA_TRY(cudaStreamWaitEvent(ix, (cudaEvent_t)plan->landed[r], 0));
             const int64_t f0 = plan->feat0[r], f1 = plan->feat1[r];
-            const int i1 = plan->img1[r];
             if (f1 < f0 || f1 > bank->n_total) {
                 set_error("msfm_guided_match_rows: stage range %d rows [%lld, %lld)", r,
                           (long long)f0, (long long)f1);
@@ -1052,15 +1069,30 @@ static int guided_match_impl(const msfm_bank* bank, const msfm_grids* grids, int
             auto w32 = [](const int32_t* p) { return const_cast<int32_t*>(p); };
             // |desc|^2 of the range computed by the build's count pass
             int rc = grid_build_range_impl(bank, grids->d_dims, grids->d_roff, grids->d_coff,
-                                           plan->n_buckets_total, plan->img0[r], i1,
+                                           plan->n_buckets_total, plan->img0[r], plan->img1[r],
                                            plan->bucket0[r], plan->bucket1[r], f0, grids->D,
                                            w32(grids->d_sub), w32(grids->d_rstart),
                                            w32(grids->d_cstart), w32(grids->d_rmem),
                                            w32(grids->d_cmem), w32(grids->d_rrec),
                                            w32(grids->d_crec), plan->grid_workspace,
-                                           plan->grid_workspace_bytes, st, w32(bank->d_norm2));
+                                           plan->grid_workspace_bytes, ix, w32(bank->d_norm2));
             if (rc) return rc;
+            cudaEvent_t e;
+            MSFM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            built.push_back(e);
+            MSFM_CUDA_TRY(cudaEventRecord(e, ix));
         }
+    }
+    int next_range = 0;
+    for (size_t c = 0; c + 1 < bounds.size(); c++) {
+        const int p0 = bounds[c], p1 = bounds[c + 1];
+        a.p0 = p0;
+        a.npairs = p1 - p0;
+        a.qbase = h_qlist_off[p0];
+        // bank ranges first read by this chunk: wait for their grid builds
+        for (; plan && next_range < plan->n_ranges && plan->chunk[next_range] <= (int32_t)c;
+             next_range++)
+            MSFM_CUDA_TRY(cudaStreamWaitEvent(st, built[next_range + 1], 0));
         // MSFM_SYNC_CHECK=1: synchronize after every kernel and name the one that failed
         auto sync_check = [&](const char* what) -> int {
             if (!sync_dbg) return MSFM_OK;
@@ -1096,6 +1128,8 @@ static int guided_match_impl(const msfm_bank* bank, const msfm_grids* grids, int
             if (rc) return rc;
         }
     }
+    // later work on `st` (the next step's uploads into the bank) follows every build
+    if (!built.empty()) MSFM_CUDA_TRY(cudaStreamWaitEvent(st, built.back(), 0));
     return MSFM_OK;
 }
 
