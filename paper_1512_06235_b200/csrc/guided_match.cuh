@@ -122,6 +122,15 @@ __device__ __forceinline__ void ms_issue_rec(const ChunkArgs& a, MSlot& L, uint6
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async16_u32(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ uint4 lds128_u32(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_all;" ::: "memory");
 }
@@ -232,8 +241,9 @@ __device__ __forceinline__ void ms_tile(const ChunkArgs& a, MSmem& S, const MSlo
     const float v2 = fabsf(fmaf(R.ma1, x0, fmaf(R.mb1, y0, R.mc1)));
     const float v3 = fabsf(fmaf(R.ma1, x1, fmaf(R.mb1, y1, R.mc1)));
     bool i0 = v0 <= R.lo0, i1 = v1 <= R.lo0, i2 = v2 <= R.lo1, i3 = v3 <= R.lo1;
-    const bool edge = (v0 > R.lo0 && v0 <= R.hi0) || (v1 > R.lo0 && v1 <= R.hi0) ||
-                      (v2 > R.lo1 && v2 <= R.hi1) || (v3 > R.lo1 && v3 <= R.hi1);
+    // branch-free: some element in (lo, hi]
+    const bool edge = ((v0 <= R.hi0) & !i0) | ((v1 <= R.hi0) & !i1) | ((v2 <= R.hi1) & !i2) |
+                      ((v3 <= R.hi1) & !i3);
     if (CB) {
         i0 = i0 && ((unsigned)c0.w & R.gb0); i1 = i1 && ((unsigned)c1.w & R.gb0);
         i2 = i2 && ((unsigned)c0.w & R.gb1); i3 = i3 && ((unsigned)c1.w & R.gb1);
@@ -324,27 +334,34 @@ __device__ __forceinline__ void ms_block(const ChunkArgs& a, MSmem& S, const MSl
     // tile nt + 2's rows are copied (cp.async, 16-B chunks, chunk p of row r at slot
     // p ^ r so a lane quad's reads spread over the banks) while tile nt is matched,
     // so the tile loop never waits on an L2 round trip.
-    const uint8_t* tbase = a.desc + SG.toff * 128;
-    auto issue = [&](int nt) {
-        uint4* buf = S.bring[nt % MS_RING];
-#pragma unroll
-        for (int c = lane; c < 64; c += 32) {
-            const int row = c >> 3, part = c & 7;
-            const int f = S.cid[8 * nt + row];
-            cp_async16(buf + row * 8 + (part ^ row), tbase + (size_t)f * 128 + part * 16);
-        }
+    // Per-lane constants of the ring addressing: lane copies chunk `part` of rows prow
+    // and prow + 4 of every tile; ring slots are 1 KB apart (offsets rotate, no modulo).
+    const int prow = lane >> 3, part = lane & 7;
+    const uint8_t* src = a.desc + SG.toff * 128 + part * 16;
+    const uint32_t ring0 = su32(&S.bring[0][0]);
+    const uint32_t dst0 = ring0 + (uint32_t)(prow * 8 + (part ^ prow)) * 16u;
+    const uint32_t dst1 = ring0 + (uint32_t)((prow + 4) * 8 + (part ^ (prow + 4))) * 16u;
+    const uint32_t rd0 = ring0 + (uint32_t)(g * 8 + ((2 * t) ^ g)) * 16u;
+    const uint32_t rd1 = ring0 + (uint32_t)(g * 8 + ((2 * t + 1) ^ g)) * 16u;
+    constexpr uint32_t SLOT = 64 * 16, RING_END = MS_RING * SLOT;
+    auto issue = [&](int nt, uint32_t k) {
+        const unsigned f0 = S.cid[8 * nt + prow], f1 = S.cid[8 * nt + prow + 4];
+        cp_async16_u32(dst0 + k, src + f0 * 128u);
+        cp_async16_u32(dst1 + k, src + f1 * 128u);
     };
-    issue(0);
+    issue(0, 0);
     cp_async_commit();
-    if (1 < ntile) issue(1);
+    if (1 < ntile) issue(1, SLOT);
     cp_async_commit();
+    uint32_t kin = 2 * SLOT, kout = 0;
     for (int nt = 0; nt < ntile; nt++) {
-        if (nt + 2 < ntile) issue(nt + 2);
+        if (nt + 2 < ntile) issue(nt + 2, kin);
+        kin = kin + SLOT == RING_END ? 0 : kin + SLOT;
         cp_async_commit();
         cp_async_wait_group<2>();
         __syncwarp();
-        const uint4* buf = S.bring[nt % MS_RING];
-        const uint4 u0 = buf[g * 8 + ((2 * t) ^ g)], u1 = buf[g * 8 + ((2 * t + 1) ^ g)];
+        const uint4 u0 = lds128_u32(rd0 + kout), u1 = lds128_u32(rd1 + kout);
+        kout = kout + SLOT == RING_END ? 0 : kout + SLOT;
         ms_tile<CB, STATS, SLOTA>(a, S, L, R, mb0, nt, u0, u1);
         __syncwarp();
     }
