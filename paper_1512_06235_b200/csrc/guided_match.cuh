@@ -474,6 +474,9 @@ __device__ __forceinline__ int ms_round(const ChunkArgs& a, MSmem& S, const MSlo
 #ifdef MSFM_MATCH_CLOCKS
     const long long c_cb0 = clock64();
 #endif
+    const float c_x0 = SG.border, c_x1 = SG.W - SG.border, c_y1 = SG.H - SG.border;
+    const float c_hs = SG.hsure;
+    const int c_gcnt = SG.gcnt, c_m0 = SG.m0;
     for (int u0 = 0; u0 < nu; u0 += 32) {
         const int uj = u0 + lane;
         if (uj < nu) {
@@ -481,15 +484,14 @@ __device__ __forceinline__ int ms_round(const ChunkArgs& a, MSmem& S, const MSlo
             const int f = S.cid[j];
             const int4 c = S.cand[j];
             const float px = __int_as_float(c.x), py = __int_as_float(c.y);
-            const bool inner = px >= SG.border && px <= SG.W - SG.border && py >= SG.border &&
-                               py <= SG.H - SG.border;
+            const bool inner = (px >= c_x0) & (px <= c_x1) & (py >= c_x0) & (py <= c_y1);
             unsigned bits = all_groups;
-            for (int gi = 0; gi < SG.gcnt; gi++) {
+            for (int gi = 0; gi < c_gcnt; gi++) {
                 const GView gv = L.gv[gi];
                 const float dg = fabsf(fmaf(gv.a, px, fmaf(gv.b, py, gv.c)));
-                if ((dg <= SG.hsure && inner) || dg > gv.reach) continue;
-                const int k0 = max(gv.moff - SG.m0, 0);
-                const int k1 = gi + 1 < SG.gcnt ? max(L.gv[gi + 1].moff - SG.m0, 0) : m;
+                if ((dg <= c_hs && inner) || dg > gv.reach) continue;
+                const int k0 = max(gv.moff - c_m0, 0);
+                const int k1 = gi + 1 < c_gcnt ? max(L.gv[gi + 1].moff - c_m0, 0) : m;
                 bool any = false;
                 for (int k = k0; k < k1 && !any; k++) any = ms_member_band(a, SG, ms_member(a, L, k), px, py);
 #ifndef MSFM_MATCH_CLOCKS
@@ -692,12 +694,19 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(const 
         row_span(SG.rlo + lane, nbs, ne1);
         if (r0 <= SG.rhi) open_batch();
         for (;;) {
+            // the strip and "sure" constants in registers for this gather pass (SG lives
+            // in shared memory, which the candidate stores below could alias: the
+            // compiler would reload it per batch); not live across the round
+            const float g_ar = SG.ar, g_br = SG.br, g_cr = SG.cr, g_R = SG.R;
+            const float g_delta = SG.delta, g_hs = SG.hsure;
+            const float g_x0 = SG.border, g_x1 = SG.W - SG.border, g_y1 = SG.H - SG.border;
+            const int g_rhi = SG.rhi;
             // ---- gather until the strip ends or the next record batch would overflow
             bool full = false;
-            while (r0 <= SG.rhi) {
+            while (r0 <= g_rhi) {
                 if (j0 >= tot) {
                     r0 += 32;
-                    if (r0 > SG.rhi) break;
+                    if (r0 > g_rhi) break;
                     open_batch();
                     continue;
                 }
@@ -706,10 +715,9 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(const 
                 bool pass = false, sure = false;
                 const float px = __int_as_float(rec.x), py = __int_as_float(rec.y);
                 if (j < tot) {
-                    const float adr = fabsf(fmaf(SG.ar, px, fmaf(SG.br, py, SG.cr)));
-                    pass = adr <= SG.R;
-                    sure = adr + SG.delta <= SG.hsure && px >= SG.border &&
-                           px <= SG.W - SG.border && py >= SG.border && py <= SG.H - SG.border;
+                    const float adr = fabsf(fmaf(g_ar, px, fmaf(g_br, py, g_cr)));
+                    pass = adr <= g_R;
+                    sure = (adr + g_delta <= g_hs) & (px >= g_x0) & (px <= g_x1) & (py >= g_x0) & (py <= g_y1);
                 }
                 const unsigned bal = __ballot_sync(FULL, pass);
                 const int cnt = __popc(bal);
