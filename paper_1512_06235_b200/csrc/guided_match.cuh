@@ -162,10 +162,14 @@ __device__ __forceinline__ void ms_top2(int key, int& b1, int& b2) {
 // the reference's float64 band decision for one (member, candidate) element
 __device__ __noinline__ bool ms_band_exact(const GroupRec* grp, const double* q_line, double d,
                                            int g0, int slotgi, float x, float y) {
+    // the group record's singleton line and the slot's own line are loaded together
+    // (one round trip; q_line holds every slot's line, singletons included)
     const GroupRec& G = grp[g0 + (int)((unsigned)slotgi >> SLOT_BITS)];
-    if (G.cnt == 1) return band_exact(G.sl0, G.sl1, G.sl2, true, x, y, d);
     const double* L = q_line + 3 * (int64_t)(slotgi & SLOT_MASK);
-    return band_exact(L[0], L[1], L[2], false, x, y, d);
+    const int cnt = G.cnt;
+    const double s0 = G.sl0, s1 = G.sl1, s2 = G.sl2;
+    const double l0 = L[0], l1 = L[1], l2 = L[2];
+    return cnt == 1 ? band_exact(s0, s1, s2, true, x, y, d) : band_exact(l0, l1, l2, false, x, y, d);
 }
 
 // fp32 prefilter, then the exact value near the edge
