@@ -341,7 +341,11 @@ __device__ __forceinline__ void ms_block(const ChunkArgs& a, MSmem& S, const MSl
     // Per-lane constants of the ring addressing: lane copies chunk `part` of rows prow
     // and prow + 4 of every tile; ring slots are 1 KB apart (offsets rotate, no modulo).
     const int prow = lane >> 3, part = lane & 7;
-    const uint8_t* src = a.desc + SG.toff * 128 + part * 16;
+    // opaque copy: keeps the per-lane row base in one register pair, so each copy's
+    // address is a single 64-bit multiply-add (f * 128 + base) instead of being
+    // re-derived from SG.toff
+    uint64_t src;
+    asm("mov.b64 %0, %1;" : "=l"(src) : "l"(reinterpret_cast<uint64_t>(a.desc + SG.toff * 128 + part * 16)));
     const uint32_t ring0 = su32(&S.bring[0][0]);
     const uint32_t dst0 = ring0 + (uint32_t)(prow * 8 + (part ^ prow)) * 16u;
     const uint32_t dst1 = ring0 + (uint32_t)((prow + 4) * 8 + (part ^ (prow + 4))) * 16u;
@@ -350,8 +354,8 @@ __device__ __forceinline__ void ms_block(const ChunkArgs& a, MSmem& S, const MSl
     constexpr uint32_t SLOT = 64 * 16, RING_END = MS_RING * SLOT;
     auto issue = [&](int nt, uint32_t k) {
         const unsigned f0 = S.cid[8 * nt + prow], f1 = S.cid[8 * nt + prow + 4];
-        cp_async16_u32(dst0 + k, src + f0 * 128u);
-        cp_async16_u32(dst1 + k, src + f1 * 128u);
+        cp_async16_u32(dst0 + k, reinterpret_cast<const void*>(src + f0 * 128ull));
+        cp_async16_u32(dst1 + k, reinterpret_cast<const void*>(src + f1 * 128ull));
     };
     issue(0, 0);
     cp_async_commit();
