@@ -484,7 +484,8 @@ __device__ __forceinline__ int ms_round(const ChunkArgs& a, MSmem& S, const MSlo
 #endif
     const float c_x0 = SG.border, c_x1 = SG.W - SG.border, c_y1 = SG.H - SG.border;
     const float c_hs = SG.hsure;
-    const int c_gcnt = SG.gcnt, c_m0 = SG.m0;
+    const int c_gcnt = SG.gcnt, c_m0 = SG.m0, c_g0 = SG.g0;
+    int nany = 0;                      // (candidate, group) pairs decided exactly (counter)
     for (int u0 = 0; u0 < nu; u0 += 32) {
         const int uj = u0 + lane;
         if (uj < nu) {
@@ -502,10 +503,8 @@ __device__ __forceinline__ int ms_round(const ChunkArgs& a, MSmem& S, const MSlo
                 const int k1 = gi + 1 < c_gcnt ? max(L.gv[gi + 1].moff - c_m0, 0) : m;
                 bool any = false;
                 for (int k = k0; k < k1 && !any; k++) any = ms_member_band(a, SG, ms_member(a, L, k), px, py);
-#ifndef MSFM_MATCH_CLOCKS
-                if (any && a.dbg) atomicAdd(&a.dbg[6], 1ull);
-#endif
-                if (any && !in_cprime(a, a.grp[SG.g0 + gi], SG, px, py, SG.toff, f)) bits &= ~(1u << gi);
+                nany += any;
+                if (any && !in_cprime(a, a.grp[c_g0 + gi], SG, px, py, SG.toff, f)) bits &= ~(1u << gi);
             }
             S.cand[j].w = (int)bits;
             partial |= bits != all_groups;
@@ -514,6 +513,8 @@ __device__ __forceinline__ int ms_round(const ChunkArgs& a, MSmem& S, const MSlo
 #ifdef MSFM_MATCH_CLOCKS
     if (a.dbg && lane == 0) atomicAdd(&a.dbg[9], (unsigned long long)(clock64() - c_cb0));
     const long long c_t0 = clock64();
+#else
+    if (a.dbg && nany) atomicAdd(&a.dbg[6], (unsigned long long)nany);
 #endif
     // ---- ratio > 1 accepts a tie at the minimum (ratio 1), and the reference's argmin
     // then names the lowest target id among the tied candidates: order the round's
@@ -734,14 +735,6 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(const 
                     const int ri = rec_at(j + 32);
                     if (j + 32 < tot) nrec = __ldg(mrec4 + ri);
                 }
-#ifndef MSFM_MATCH_CLOCKS
-                if (a.dbg && lane == 0) {
-                    atomicAdd(&a.dbg[3], (unsigned long long)cnt);
-                    atomicAdd(&a.dbg[4], (unsigned long long)__popc(__ballot_sync(FULL, pass && sure)));
-                } else if (a.dbg) {
-                    __ballot_sync(FULL, pass && sure);
-                }
-#endif
                 const int k = __popc(bal & ((1u << lane) - 1u));
                 const unsigned ubal = __ballot_sync(FULL, pass && !sure);
                 if (pass) {
@@ -757,6 +750,13 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(const 
             }
             __syncwarp();
             issue_next_desc();
+#ifndef MSFM_MATCH_CLOCKS
+            // counters once per round: passing = n, surely in every C' = n - nu
+            if (a.dbg && lane == 0) {
+                atomicAdd(&a.dbg[3], (unsigned long long)n);
+                atomicAdd(&a.dbg[4], (unsigned long long)(n - nu));
+            }
+#endif
             if (n > 0) {
 #ifdef MSFM_MATCH_CLOCKS
                 const long long cr = clock64();
