@@ -860,9 +860,14 @@ static void plan_chunks(int32_t n_pairs, const int64_t* h_qlist_off, const msfm_
     worst = {0, 0, 0, 0};
     int p = 0;
     bounds.push_back(0);
+    // pipelined (first_chunk_pairs > 0): chunk sizes ramp first, 4 first, 16 first, ...
+    // up to chunk_pairs, so each chunk's compute covers the upload of the next one's
+    // images and the matcher starts after a few images instead of a chunk's worth
+    int ramp = prm->first_chunk_pairs > 0 ? prm->first_chunk_pairs : cp;
     while (p < n_pairs) {
         int e = p + 1;
-        const int cap = (p == 0 && prm->first_chunk_pairs > 0) ? std::min(cp, prm->first_chunk_pairs) : cp;
+        const int cap = std::min(cp, ramp);
+        if (ramp < cp) ramp = ramp > cp / 4 ? cp : ramp * 4;
         while (e < n_pairs && e - p < cap && h_qlist_off[e + 1] - h_qlist_off[p] <= qmax &&
                bytes_of(e + 1 - p, h_qlist_off[e + 1] - h_qlist_off[p]) <= budget)
             e++;
@@ -878,12 +883,22 @@ static void plan_chunks(int32_t n_pairs, const int64_t* h_qlist_off, const msfm_
         bounds.push_back(e);
         p = e;
     }
-    // pipelined (first_chunk_pairs > 0): a short last chunk too, so the readback that
-    // no later chunk hides is small (a split chunk only shrinks: the worst sizes hold)
-    const int tail = 2 * prm->first_chunk_pairs;
-    if (prm->first_chunk_pairs > 0 && bounds.size() >= 2) {
-        const int b0 = bounds[bounds.size() - 2], b1 = bounds.back();
-        if (b1 - b0 > 2 * tail) bounds.insert(bounds.end() - 1, b1 - tail);
+    // pipelined (first_chunk_pairs > 0): the last chunk ramps down too (pieces of 16,
+    // 4 and 1 first_chunk_pairs cut from its end), so each chunk's readback hides
+    // behind the next chunk's compute and the one no chunk hides is small (a split
+    // chunk only shrinks: the worst sizes hold)
+    const int first = prm->first_chunk_pairs;
+    if (first > 0 && bounds.size() >= 2) {
+        const int b0 = bounds[bounds.size() - 2];
+        int end = bounds.back();
+        std::vector<int> cuts;
+        for (int64_t sz = first; sz <= 16 * (int64_t)first; sz *= 4)   // last piece first
+            if (end - b0 > 2 * sz) {
+                end -= (int)sz;
+                cuts.push_back(end);
+            }
+        std::reverse(cuts.begin(), cuts.end());
+        bounds.insert(bounds.end() - 1, cuts.begin(), cuts.end());
     }
 }
 
