@@ -552,37 +552,40 @@ __device__ __forceinline__ bool in_cprime(const ChunkArgs& a, const GroupRec& G,
 
 #include "guided_match.cuh"
 
-__global__ void __launch_bounds__(256) compact_kernel(ChunkArgs a) {
-    __shared__ int sm[256 / 32 + 1];
+constexpr int CT = 1024;   // compact_kernel threads (one pair per CTA)
+__global__ void __launch_bounds__(CT) compact_kernel(ChunkArgs a) {
+    __shared__ int sm[CT / 32 + 1];
     const int p = blockIdx.x, pg = a.p0 + p;
     const int64_t q0 = a.qlist_off[pg];
     const int nq = (int)(a.qlist_off[pg + 1] - q0);
     const int64_t s0 = q0 - a.qbase;
     const int64_t db = a.tbase[p];
     int carry = 0;
-    for (int i0 = 0; i0 < nq; i0 += 256) {
+    for (int i0 = 0; i0 < nq; i0 += CT) {
         const int i = i0 + threadIdx.x;
         bool keep = false;
         int tid = -1, qid = 0;
-        float dist = 0.f;
+        float dist = 0.f, ratio = 0.f;
         if (i < nq) {
+            // the slot's four fields load together (no dependence on tid)
             tid = a.res_tid[s0 + i];
+            qid = a.q_fid[s0 + i];
+            dist = a.res_dist[s0 + i];
+            ratio = a.res_ratio[s0 + i];
             if (tid >= 0) {
-                qid = a.q_fid[s0 + i];
-                dist = a.res_dist[s0 + i];
                 const unsigned long long key =
                     ((unsigned long long)__float_as_uint(dist) << 32) | (unsigned)qid;
                 keep = a.dedupe[db + tid] == key;
             }
         }
         int tot;
-        const int ex = block_exclusive_scan<256>(keep ? 1 : 0, &tot, sm);
+        const int ex = block_exclusive_scan<CT>(keep ? 1 : 0, &tot, sm);
         if (keep) {
             const int64_t o = q0 + carry + ex;
             a.out_q[o] = qid;
             a.out_t[o] = tid;
             a.out_dist[o] = dist;
-            a.out_ratio[o] = a.res_ratio[s0 + i];
+            a.out_ratio[o] = ratio;
         }
         carry += tot;
     }
@@ -1134,7 +1137,7 @@ static int guided_match_impl(const msfm_bank* bank, const msfm_grids* grids, int
             }
         }
         if (int rc = sync_check("match_kernel")) return rc;
-        { ProfScope ps("compact_kernel", st); compact_kernel<<<a.npairs, 256, 0, st>>>(a); }
+        { ProfScope ps("compact_kernel", st); compact_kernel<<<a.npairs, CT, 0, st>>>(a); }
         if (int rc = sync_check("compact_kernel")) return rc;
         MSFM_LAUNCH_CHECK();
         count_launches(4);
