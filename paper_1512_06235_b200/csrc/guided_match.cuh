@@ -53,6 +53,7 @@ struct alignas(16) MSmem {
     unsigned short ulist[MS_CAP];  // candidates whose C' bits are still to be decided
     unsigned anyb[MS_CAP / 32];    // stats: candidate inside some member band
     uint4 bring[MS_RING][64];      // candidate descriptor rows of the next tiles (swizzled 16-B chunks)
+    int rbs[32], rex[32];          // gather batch: CSR start / batch start of the k-th non-empty row
     unsigned long long mbest[16];  // running best (d2 << 32 | target) of the slot's first 16 members
     unsigned msec[16];             // and second d2 (members past 16: a.mstate / a.mstate2)
     uint64_t bar_q, bar_rec[2];
@@ -671,16 +672,18 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(const 
         int r0 = SG.rlo, bs = 0, len = 0, incl = 0, tot = 0, j0 = 0;
         int nbs, ne1;
         int4 nrec = make_int4(0, 0, 0, 0);
-        auto rec_at = [&](int j) {
-            int o = 0;
-#pragma unroll
-            for (int sft = 16; sft > 0; sft >>= 1) {
-                const int v = __shfl_sync(FULL, incl, o + sft - 1);
-                if (v <= j) o += sft;
-            }
-            const int ob = __shfl_sync(FULL, bs, o & 31);
-            const int oex = __shfl_sync(FULL, incl - len, o & 31);
-            return ob + (j - oex);
+        // record index of batch position j = w0 + lane: the row holding j is the last
+        // non-empty row starting at or before j.  Non-empty rows' starts are distinct, so
+        // the window's starts form one bit mask (OR-reduction); rows are ranked among the
+        // non-empty ones, whose (CSR start, batch start) open_batch keeps in shared memory.
+        auto rec_at = [&](int w0) {
+            const int excl = incl - len;
+            const bool ne = len > 0;
+            const unsigned bit = (ne && excl >= w0 && excl < w0 + 32) ? 1u << (excl - w0) : 0u;
+            const unsigned mask = __reduce_or_sync(FULL, bit);
+            const int before = __popc(__ballot_sync(FULL, ne && excl < w0));
+            const int k = max(before + __popc(mask & (0xffffffffu >> (31 - lane))) - 1, 0);
+            return S.rbs[k] + (w0 + lane - S.rex[k]);
         };
         auto open_batch = [&]() {
             bs = nbs;
@@ -693,11 +696,20 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(const 
                 if (lane >= o) incl += y;
             }
             tot = __shfl_sync(FULL, incl, 31);
+            {
+                const unsigned nem = __ballot_sync(FULL, len > 0);
+                if (len > 0) {
+                    const int rk = __popc(nem & ((1u << lane) - 1u));
+                    S.rbs[rk] = bs;
+                    S.rex[rk] = incl - len;
+                }
+                __syncwarp();
+            }
 #ifndef MSFM_MATCH_CLOCKS
             if (a.dbg && lane == 0) atomicAdd(&a.dbg[2], (unsigned long long)tot);
 #endif
             j0 = 0;
-            const int ri = rec_at(lane);
+            const int ri = rec_at(0);
             nrec = lane < tot ? __ldg(mrec4 + ri) : make_int4(0, 0, 0, 0);
         };
         row_span(SG.rlo + lane, nbs, ne1);
@@ -732,7 +744,7 @@ __global__ void __launch_bounds__(MS_WARPS * 32, MS_MINB) match_ms_kernel(const 
                 const int cnt = __popc(bal);
                 if (n + cnt > MS_CAP) { full = true; break; }
                 {
-                    const int ri = rec_at(j + 32);
+                    const int ri = rec_at(j0 + 32);
                     if (j + 32 < tot) nrec = __ldg(mrec4 + ri);
                 }
                 const int k = __popc(bal & ((1u << lane) - 1u));
