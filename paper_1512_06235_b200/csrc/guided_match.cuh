@@ -147,10 +147,15 @@ __device__ __forceinline__ void cp_async_wait_group() {
 __device__ __forceinline__ void ms_issue_desc(const ChunkArgs& a, MSlot& L) {
     const int lane = threadIdx.x & 31;
     const int nm = min(L.sg.mcnt, 16);
+    const int part = lane & 7, j0 = lane >> 3;      // lane copies chunk `part` of rows j0 + 4q
+    uint64_t src;                                   // opaque: one IMAD.WIDE per copy
+    asm("mov.b64 %0, %1;" : "=l"(src) : "l"(reinterpret_cast<uint64_t>(a.desc + L.sg.qoff * 128 + part * 16)));
+    const uint32_t dst = su32(L.desc[j0] + 16 * part);
 #pragma unroll
     for (int q = 0; q < 4; q++) {
-        const int k = lane + 32 * q, j = k >> 3, part = k & 7;
-        if (j < nm) cp_async16(L.desc[j] + 16 * part, a.desc + (L.sg.qoff + L.mr[j].fid) * 128 + 16 * part);
+        const int j = j0 + 4 * q;
+        if (j < nm)
+            cp_async16_u32(dst + q * 4 * 128, reinterpret_cast<const void*>(src + (unsigned)L.mr[j].fid * 128ull));
     }
 }
 
