@@ -157,6 +157,10 @@ __device__ __forceinline__ void ms_issue_desc(const ChunkArgs& a, MSlot& L) {
         if (j < nm)
             cp_async16_u32(dst + q * 4 * 128, reinterpret_cast<const void*>(src + (unsigned)L.mr[j].fid * 128ull));
     }
+    // the members' f64 lines into L2 (the exact band fallback near a band edge reads
+    // them; written by the setup kernel long before, they are back in DRAM by now)
+    if (lane < nm)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.q_line + 3 * (int64_t)(L.mr[lane].slotgi & SLOT_MASK)));
 }
 
 __device__ __forceinline__ void ms_top2(int key, int& b1, int& b2) {
