@@ -247,7 +247,9 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
             const double* L = a.q_line + 3 * (s0 + rep);
             float la = (float)L[0], lb = (float)L[1];
             if (la < 0.f || (la == 0.f && lb < 0.f)) { la = -la; lb = -lb; }
-            const float ang = atan2f(lb, la);
+            // a monotone pseudo-angle of the direction (la >= 0 half-plane): the key
+            // only buckets groups for the angle order, any monotone map of atan2 will do
+            const float ang = lb / fmaxf(fabsf(la) + fabsf(lb), 1e-30f);
             a.gkey[s0 + g] = ang;
             lo = fminf(lo, ang);
             hi = fmaxf(hi, ang);
