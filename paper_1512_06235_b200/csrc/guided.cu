@@ -359,7 +359,7 @@ __device__ __forceinline__ int nextpow2(int v) {
     return p;
 }
 
-constexpr int GB = 4096;   // angle buckets of the per-pair group order
+constexpr int GB = 8192;   // angle buckets of the per-pair group order
 
 // Upper bound of |dist_m(f) - dist_r(f)| over the image rectangle restricted to
 // the member's band (|dist_m| <= d + 0.5): the difference is affine, so its
