@@ -290,7 +290,27 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
         const int pos = atomicAdd(&hist[b], 1);
         a.gpos[s0 + g] = pos;
         const int2 r = a.gtmp[s0 + g];
-        a.grec[s0 + pos] = make_int4(r.x, r.y, 0, 0);
+        a.grec[s0 + pos] = make_int4(r.x, r.y, 0, g);     // .w: the group (for the sort below)
+    }
+    __syncthreads();
+    // the atomics leave a bucket's few groups in arbitrary order: sort each bucket by
+    // (key, group) so the super-group walk sees the exact angle order (fewer breaks)
+    for (int b = tid; b < GB; b += ST) {
+        const int e = hist[b], st = b == 0 ? 0 : hist[b - 1];
+        if (e - st < 2) continue;
+        for (int i = st + 1; i < e; i++) {
+            const int4 v = a.grec[s0 + i];
+            const float kv = a.gkey[s0 + v.w];
+            int j = i - 1;
+            for (; j >= st; j--) {
+                const int4 u = a.grec[s0 + j];
+                const float ku = a.gkey[s0 + u.w];
+                if (ku < kv || (ku == kv && u.w < v.w)) break;
+                a.grec[s0 + j + 1] = u;
+            }
+            a.grec[s0 + j + 1] = v;
+        }
+        for (int i = st; i < e; i++) a.gpos[s0 + a.grec[s0 + i].w] = i;
     }
     __syncthreads();
     int mcarry = 0;
