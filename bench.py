@@ -215,6 +215,19 @@ def ncu_traffic_per_pair():
     return j.get("dram_bytes_per_pair")
 
 
+def ncu_traffic_source():
+    """Where roofline.traffic comes from: the committed ncu capture's report name."""
+    path = os.path.join(REPO, "profiles", "ncu_match_kernel.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        j = json.load(f)
+    return (f"profiles/ncu_match_kernel.json: dram__bytes_read.sum + dram__bytes_write.sum "
+            f"per pair from one ncu --set full capture ({j.get('report')}, "
+            f"{j.get('pairs_per_launch', 0):.0f} pairs) of this build's match kernel on the C3 "
+            f"step (tools/r2_measure_final.sh), scaled to this launch's pairs")
+
+
 # --------------------------------------------------------------- main legs --
 
 def kdtree_footnote(n_images=2, seed=0):
@@ -507,6 +520,7 @@ def run_b200(args, rank, world):
                      "frac": achieved / peak, "peak_kind": peak_kind,
                      "kernel": "match_kernel",
                      "traffic": (tpp * len(mine) / max(k_n, 1)) if tpp else None,
+                     "traffic_source": ncu_traffic_source(),
                      "algorithmic_bytes_per_launch": alg / max(k_n, 1),
                      "launches": k_n, "kernel_ms_per_step": k_ms,
                      "step_frac": (alg / (step_ms / 1e3) / 1e9) / peak,
