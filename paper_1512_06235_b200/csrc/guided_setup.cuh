@@ -286,11 +286,13 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
     }
     __syncthreads();
     for (int g = tid; g < ng; g += ST) {
-        const int b = min(GB - 1, max(0, (int)((a.gkey[s0 + g] - lo) * scale)));
+        const float key = a.gkey[s0 + g];
+        const int b = min(GB - 1, max(0, (int)((key - lo) * scale)));
         const int pos = atomicAdd(&hist[b], 1);
         a.gpos[s0 + g] = pos;
         const int2 r = a.gtmp[s0 + g];
-        a.grec[s0 + pos] = make_int4(r.x, r.y, 0, g);     // .w: the group (for the sort below)
+        // .z: the key, .w: the group (for the sort below; .z becomes the member offset)
+        a.grec[s0 + pos] = make_int4(r.x, r.y, __float_as_int(key), g);
     }
     __syncthreads();
     // the atomics leave a bucket's few groups in arbitrary order: sort each bucket by
@@ -300,11 +302,11 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
         if (e - st < 2) continue;
         for (int i = st + 1; i < e; i++) {
             const int4 v = a.grec[s0 + i];
-            const float kv = a.gkey[s0 + v.w];
+            const float kv = __int_as_float(v.z);
             int j = i - 1;
             for (; j >= st; j--) {
                 const int4 u = a.grec[s0 + j];
-                const float ku = a.gkey[s0 + u.w];
+                const float ku = __int_as_float(u.z);
                 if (ku < kv || (ku == kv && u.w < v.w)) break;
                 a.grec[s0 + j + 1] = u;
             }
