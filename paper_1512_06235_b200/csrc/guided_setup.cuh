@@ -546,8 +546,19 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
         float rdev, sdev;
         band_deviation2_f(mf, r, b, (float)W, (float)H, (float)d, rdev, sdev);
         const float gdev = rdev + 0.05f;
-        atomicMax(reinterpret_cast<unsigned*>(&G.maxdev), __float_as_uint(gdev));
-        atomicMax(&sgdevf[ls], __float_as_uint(sdev));
+        // members of a group / super-group sit in consecutive lanes: reduce each run in
+        // the warp first, one atomic per run (the shared-memory maxima serialised up to
+        // 16 ways per super-group otherwise)
+        {
+            const unsigned act = __activemask();
+            const unsigned below = (1u << lane) - 1u;
+            const unsigned mg = __match_any_sync(act, lg);
+            const unsigned gmax = __reduce_max_sync(mg, __float_as_uint(gdev));
+            if (!(mg & below)) atomicMax(reinterpret_cast<unsigned*>(&G.maxdev), gmax);
+            const unsigned ms = __match_any_sync(act, ls);
+            const unsigned smax = __reduce_max_sync(ms, __float_as_uint(sdev));
+            if (!(ms & below)) atomicMax(&sgdevf[ls], smax);
+        }
         MemberRec mr;
         mr.a = mf[0]; mr.b = mf[1]; mr.c = mf[2];
         // fp32 band-value error bound (from the f32 line: the bound's own
