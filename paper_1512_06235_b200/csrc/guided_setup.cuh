@@ -460,18 +460,38 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
             mk[q] = q == 0 ? 1 : 0;
         }
         __syncthreads();
-        // pointer doubling: round k marks J^(2^k) of every marked position, so after
-        // k rounds the first 2^(k+1) super-group starts of the walk from 0 are marked
-        int* Jc = Ja;
-        int* Jn = Jb;
-        for (int round = 0; round < 20; round++) {
-            for (int q = tid; q < nm; q += ST)
-                if (mk[q]) mk[Jc[q]] = 1;
+        // The walk 0 -> e(0) -> e(e(0)) ... in three passes.  Positions are cut into
+        // segments of S >= 16; a step moves at most 16, so the walk enters segment w at
+        // one of its first 16 positions.  (A) each warp walks its segment from all 16
+        // possible entries (a lane each) and records where each leaves it; (B) one
+        // thread chains the segments' entries; (C) each warp re-walks its segment from
+        // the resolved entry and marks the super-group starts.
+        {
+            __shared__ int cx_exit[ST / 32][16];
+            __shared__ int cx_entry[ST / 32];
+            constexpr int NSEG = ST / 32;
+            const int S = max(SG_MEMBERS, (nm + NSEG - 1) / NSEG);
+            const int nseg = (nm + S - 1) / S;
+            if (wid < nseg && lane < 16) {
+                const int lo = wid * S, hi = min(lo + S, nm);
+                int q = lo + lane;
+                while (q < hi) q = Ja[q];
+                cx_exit[wid][lane] = q;
+            }
             __syncthreads();
-            for (int q = tid; q <= nm; q += ST) Jn[q] = Jc[Jc[q]];
+            if (tid == 0) {
+                int q = 0;
+                for (int w = 0; w < nseg; w++) {
+                    cx_entry[w] = q;
+                    q = cx_exit[w][q - w * S];
+                }
+            }
             __syncthreads();
-            int* t = Jc; Jc = Jn; Jn = t;
-            if (Jc[0] >= nm) break;                // the marked prefix covers the walk
+            if (wid < nseg && lane == 0) {
+                const int hi = min((wid + 1) * S, nm);
+                for (int q = cx_entry[wid]; q < hi; q = Ja[q]) mk[q] = 1;
+            }
+            __syncthreads();
         }
         // the marks are the walk's starts; compact them in order (e from the q + 16 /
         // B rule again, since the J arrays were overwritten)
