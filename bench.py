@@ -114,6 +114,8 @@ class ClockSampler:
 
     def __init__(self, device_index=0):
         self.samples, self.stop, self.dev = [], threading.Event(), device_index
+        self.ready = threading.Event()   # set at the first sample (NVML init is slow)
+        self.nvml = False
 
     def _run_nvml(self):
         """NVML sampling every ~5 ms (the timed region is a few hundred ms)."""
@@ -125,11 +127,13 @@ class ClockSampler:
             mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
             bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
                     nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+            self.nvml = True
             while not self.stop.is_set():
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
                 self.samples.append([str(sm), str(mx)] +
                                     ["Active" if r & b else "Not Active" for b in bits])
+                self.ready.set()
                 self.stop.wait(0.005)
         finally:
             nv.nvmlShutdown()
@@ -147,13 +151,20 @@ class ClockSampler:
                                      capture_output=True, text=True, timeout=5).stdout.strip()
                 if out:
                     self.samples.append([x.strip() for x in out.split(",")])
+                    self.ready.set()
             except Exception:
                 pass
             self.stop.wait(0.2)
 
     def __enter__(self):
+        # the sampler is running before the timed region starts: wait for its first
+        # sample, then keep only what it records from here on (a timed region of a
+        # few tens of ms otherwise ends before NVML has initialised)
         self.th = threading.Thread(target=self._run, daemon=True)
         self.th.start()
+        self.ready.wait(timeout=5.0)
+        if self.nvml:                    # 5-ms NVML samples: keep the timed region's only
+            self.samples.clear()
         return self
 
     def __exit__(self, *a):
