@@ -274,8 +274,10 @@ def match_pairs_rows_staged(host, q_img, t_img, F, query_lists, *, device=None,
         raise ValueError(f"cell half-size d must be positive, got {d}")
     D = float(grid_d) if grid_d is not None else float(d) * float(inflation)
     P = len(q_img)
-    # chunks of 1024 pairs: the upload and the row readback pipeline across them
-    chunk_pairs = chunk_pairs or 1024
+    # chunks of up to 1536 pairs (after the 64 / 256 / 1024 ramp): the upload and the
+    # row readback pipeline across them (tools/probe_staged.py: 768 / 1024 / 1536 /
+    # 2048-pair chunks 21.5 / 21.1 / 20.8 / 21.6 ms per C3 step)
+    chunk_pairs = chunk_pairs or 1536
     if bank is None or not getattr(bank, "staged", False) or bank.host is not host:
         bank = FeatureBank(host=host, device=device, staged=True)
     nimg = len(bank.image_ids)

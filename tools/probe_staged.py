@@ -70,7 +70,7 @@ for fcp in (0, 16, 32, 64):
     timed(f"staged reuse first chunk {fcp}", lambda: staged_reuse(first_chunk_pairs=fcp))
 for seg in (8, 32):
     timed(f"staged reuse seg {seg}", lambda: staged_reuse(segment_images=seg))
-for cp in (1536, 2048, 2700):
+for cp in (768, 1536, 2048):
     timed(f"staged reuse chunk {cp}", lambda: staged_reuse(chunk_pairs=cp))
 for fcp in ():
     timed(f"staged e2e first chunk {fcp}", lambda: match_pairs_rows_staged(
