@@ -167,9 +167,10 @@ typedef struct {
                           * 0 grid (cells of the samples, default), 1 linear
                           * (|rep line| <= d, guided.py:190-194), 2 radial (disks of
                           * radius d*sqrt(2) around the samples, guided.py:273-285) */
-    int32_t first_chunk_pairs; /* pairs of the first chunk when > 0 (a short first
-                          * chunk starts matching sooner on a staged bank); the
-                          * last chunk is then cut to 2x as many pairs too (its
+    int32_t first_chunk_pairs; /* when > 0 (pipelined / staged use): chunk sizes ramp
+                          * first, 4x, 16x ... up to chunk_pairs, so matching starts
+                          * after few images have landed, and pieces of 16x, 4x, 1x
+                          * first are cut from the end of the last chunk (its
                           * readback is the one no later chunk hides)            */
     int64_t max_workspace_bytes; /* chunks are cut so one chunk's workspace stays
                           * within this many bytes; 0 = a quarter of the device's
