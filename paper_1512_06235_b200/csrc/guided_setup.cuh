@@ -297,9 +297,21 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
     __syncthreads();
     // the atomics leave a bucket's few groups in arbitrary order: sort each bucket by
     // (key, group) so the super-group walk sees the exact angle order (fewer breaks)
+    auto before = [](const int4& u, const int4& v) {   // (key, group) order
+        const float ku = __int_as_float(u.z), kv = __int_as_float(v.z);
+        return ku < kv || (ku == kv && u.w < v.w);
+    };
     for (int b = tid; b < GB; b += ST) {
         const int e = hist[b], st = b == 0 ? 0 : hist[b - 1];
         if (e - st < 2) continue;
+        if (e - st == 2) {                                  // the common case: one swap
+            int4 u = a.grec[s0 + st], v = a.grec[s0 + st + 1];
+            if (before(v, u)) {
+                a.grec[s0 + st] = v; a.grec[s0 + st + 1] = u;
+                a.gpos[s0 + v.w] = st; a.gpos[s0 + u.w] = st + 1;
+            }
+            continue;
+        }
         for (int i = st + 1; i < e; i++) {
             const int4 v = a.grec[s0 + i];
             const float kv = __int_as_float(v.z);
