@@ -613,10 +613,10 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
     // group within its super-group: |dist_g - dist_base| over the strip (atomic max in
     // shared memory) and the group's view (groups shared by two super-groups get the
     // same view twice)
-    for (int k = tid; k < nm; k += ST) {
-        const int lg = MGID(k);
-        const int ls = MSG(k);
-        if (k > 0 && MGID(k - 1) == lg && MSG(k - 1) == ls) continue;
+    // Per group: its member run [gm0, gm1) meets at most two super-groups when it has
+    // <= 16 members (a super-group opened inside a group runs at least to the group's
+    // end), the ones holding its first and last member; longer groups walk their run.
+    auto strip_head = [&](int lg, int ls) {
         const GroupRec& G = a.grp[s0 + lg];
         const GroupRec& GB = a.grp[s0 + (sgbl[ls] & 0xffffu)];
         const float R = (float)d + __uint_as_float(sgdevf[ls]) + 0.05f;
@@ -635,6 +635,19 @@ __global__ void __launch_bounds__(ST, 1) setup_kernel(const __grid_constant__ Ch
         const int4* w = reinterpret_cast<const int4*>(&gv);
         __stcs(reinterpret_cast<int4*>(a.gview + s0 + lg), w[0]);
         __stcs(reinterpret_cast<int4*>(a.gview + s0 + lg) + 1, w[1]);
+    };
+    for (int lg = tid; lg < ng; lg += ST) {
+        const int gm0 = a.grec[s0 + lg].z - (int)s0;
+        const int gm1 = lg + 1 < ng ? a.grec[s0 + lg + 1].z - (int)s0 : nm;
+        if (gm1 <= gm0) continue;
+        const int ls0 = MSG(gm0), ls1 = MSG(gm1 - 1);
+        if (gm1 - gm0 <= SG_MEMBERS) {
+            strip_head(lg, ls0);
+            if (ls1 != ls0) strip_head(lg, ls1);
+        } else {
+            for (int k = gm0; k < gm1; k++)
+                if (k == gm0 || MSG(k) != MSG(k - 1)) strip_head(lg, MSG(k));
+        }
     }
     __syncthreads();
     // (b) per super-group: strip half-width, sure radius, bucket-row range (sg_prep_kernel
