@@ -8,16 +8,18 @@
 //             composite bucket key (group_queries guided.py:340-390), insert into
 //             the pair's hash table (shared memory up to TS_SMEM slots)
 //   groups    compact the occupied slots, order the groups by representative-line
-//             angle (4096-bucket counting sort), member ranges, boundary endpoints
+//             angle (pseudo-angle key, GB-bucket counting sort, each bucket sorted
+//             by (key, group)), member ranges, boundary endpoints
 //   scatter   member lists; per group the padded clip / sample geometry (GroupRec,
 //             equidistant_line_points guided.py:173-187)
 //   chain     super-groups: e(q) = min(q + 16, B(g(q))) per member position (B: the
 //             first group that stops fitting g's line, or the end), the greedy walk
-//             from position 0 marked by pointer doubling, compacted in order
+//             from position 0 found in three segmented passes, compacted in order
 //   shape     per super-group: group range, base line (middle group's rep)
 //   members   per member: epilogue constants, band deviation from its group's rep
 //             and its super-group's base (shared-memory / L2 atomic maxima)
-//   strips    per super-group: strip half-width, bucket-row range, group views
+//   strips    per (super-group, group): rep deviation from the base, group views;
+//             per super-group: strip half-width, sure radius, bucket-row range
 //
 // Everything a pair needs stays in one CTA: the intermediates are written and
 // re-read while L2-hot, the hash table lives in shared memory, and the only
