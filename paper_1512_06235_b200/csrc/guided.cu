@@ -304,7 +304,7 @@ static_assert(SG_MEMBERS <= 16, "MSFM_SG_NT > 2 needs wider per-candidate group 
 #define MSFM_MATCH_MINB (SG_NT == 1 ? 6 : 4)
 #endif
 constexpr int MATCH_MINB = MSFM_MATCH_MINB;   // resident CTAs (4 warps) per SM
-constexpr float SG_TAU = 16.0f;
+constexpr float SG_TAU = 24.0f;
 constexpr int SG_MAX_GROUPS = SG_MEMBERS;
 
 struct ChunkArgs {
